@@ -1,0 +1,65 @@
+"""Scalar-loop brute force for ONE example -- TEST INFRASTRUCTURE ONLY (see oracle/__init__).
+
+No numpy matmul, no vectorisation: plain Python floats (IEEE fp64), one loop per index,
+so it checks ``oracle.score_forward`` (P8 of SURVEY.md §8(c)) through an independent
+evaluation order.  Same paper passages as the batched oracle: PAPER.md:96 (pooling),
+95 (standardisation), 116-119 / 225 (DCN-v2 cross), 229-233 (MLP), north star (sigmoid).
+"""
+from __future__ import annotations
+
+import math
+from typing import Dict, List, Sequence
+
+
+def _mat_vec(M: List[List[float]], v: List[float]) -> List[float]:
+    out = []
+    for row in M:
+        s = 0.0
+        for a, b in zip(row, v):
+            s += a * b
+        out.append(s)
+    return out
+
+
+def brute_score_one(cfg, tables: Sequence, P: Dict, indices, offsets, dense_row, b: int, batch: int) -> float:
+    """Score of example ``b`` (fp64 Python floats).  ``tables[t]`` supports ``gather_f64`` or
+    indexing; ``P`` holds fp64 numpy parameters (``oracle.to_f64`` of the stored values)."""
+    T, d = cfg.n_tables, cfg.dim
+    x0: List[float] = []
+    for t in range(T):
+        lo, hi = int(offsets[t * batch + b]), int(offsets[t * batch + b + 1])
+        acc = [0.0] * d
+        for j in range(lo, hi):
+            r = int(indices[j])
+            tab = tables[t]
+            row = tab.gather_f64([r])[0] if hasattr(tab, "gather_f64") else tab[r]
+            for c in range(d):
+                acc[c] += float(row[c])
+        x0.extend(acc)
+    for f in range(cfg.n_dense):
+        sd = max(float(P["norm/std"][f]), 1e-8)
+        x0.append((float(dense_row[f]) - float(P["norm/mean"][f])) / sd)
+
+    tolist = lambda a: [[float(v) for v in r] for r in a] if getattr(a, "ndim", 1) == 2 else [float(v) for v in a]
+    xl = list(x0)
+    if cfg.backbone == "dcn_full":
+        for l in range(cfg.n_cross):
+            y = _mat_vec(tolist(P[f"dcn/{l}/W"]), xl)
+            bb = tolist(P[f"dcn/{l}/b"])
+            xl = [x0[i] * (y[i] + bb[i]) + xl[i] for i in range(len(xl))]
+    elif cfg.backbone == "dcn_lowrank":
+        for l in range(cfg.n_cross):
+            t_ = _mat_vec(tolist(P[f"dcn/{l}/V"]), xl)
+            y = _mat_vec(tolist(P[f"dcn/{l}/U"]), t_)
+            bb = tolist(P[f"dcn/{l}/b"])
+            xl = [x0[i] * (y[i] + bb[i]) + xl[i] for i in range(len(xl))]
+    else:
+        raise NotImplementedError("brute force covers the DCN-v2 configs")
+    h = xl
+    for i in range(len(cfg.mlp_dims)):
+        y = _mat_vec(tolist(P[f"mlp/{i}/W"]), h)
+        c = tolist(P[f"mlp/{i}/b"])
+        h = [max(0.0, y[j] + c[j]) for j in range(len(y))]
+    m = tolist(P["head/w"])[0]
+    z = sum(m[j] * h[j] for j in range(len(h))) + float(P["head/b"][0])
+    return 1.0 / (1.0 + math.exp(-z)) if z >= 0 else math.exp(z) / (1.0 + math.exp(z))
