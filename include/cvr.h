@@ -1,0 +1,191 @@
+/*
+ * cvr.h -- C ABI of libcvr.so, the B200 (sm_100a) scoring hot path of the scaled
+ * search-CVR model of arxiv/paper_2605_29232 (PAPER.md = the paper's LaTeX source).
+ *
+ * The path for one batch of B candidate items:
+ *   S2 embedding-bag gather + sum-pool   p[b,t,:] = sum_{j in bag(t,b)} E_t[idx_j,:]
+ *        PAPER.md:96 (§2.1 "Each categorical feature is designated to an embedding layer");
+ *        BASELINE.json north star (a) "multi-hot embedding-bag gather and sum-pool".
+ *   S3 dense normalisation + concat      x0 = [p_0 | ... | p_{T-1} | (x - mu)/sigma]
+ *        PAPER.md:95 ("normal standardization"), PAPER.md:227 (x_0).
+ *   S4 pooled all-to-all (sharded tables only)  -- BASELINE.json configs[2].
+ *   S5 DCN-v2 cross layers               x_{l+1} = x0 * (W_l x_l + b_l) + x_l       (full rank)
+ *                                        x_{l+1} = x0 * (U_l (V_l x_l) + b_l) + x_l (low rank)
+ *        PAPER.md:116-119 (eq:dcnv2) and PAPER.md:225 (§3.1 "The Deep and Cross Family").
+ *   S6 MLP tower                         h_{i+1} = ReLU(M_i h_i + c_i)   PAPER.md:229-233.
+ *   S7 head                              score = sigmoid(m . h + c)      BASELINE.json north star.
+ *   S9 decoupled execution: the embedding stage of batch k+1 overlaps the dense stage of
+ *      batch k (§4.5 "Hybrid CPU-GPU Execution"; BASELINE.json north star).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Every function returns an int status (cvr_status) and never throws across the ABI.
+ *    cvr_last_error(ctx) returns the per-ctx message of the most recent failure (shape
+ *    errors name both the expected and the received shape).
+ *  - "d_" pointers are CUDA device pointers, "h_" pointers are host pointers.  The caller
+ *    (PyTorch) allocates every device buffer; the library only BORROWS them, except the
+ *    workspace contents, which it owns between cvr_set_workspace and cvr_destroy.
+ *  - Streams are passed as cvr_stream_t (a cudaStream_t, NULL = legacy default stream).
+ *    Calls that take a stream only ENQUEUE work; arguments are validated synchronously
+ *    on the host before anything is enqueued (null pointers, batch > max_batch,
+ *    nnz > max_nnz, call order -> CVR_E_STATE).
+ *  - Bad data that only the device can see (index outside [0, rows_t), offsets not
+ *    non-decreasing or outside [0, nnz]) sets a sticky device flag; that bag is written
+ *    as zeros, and the NEXT cvr_get_status returns CVR_E_INDEX (error, never a clamp;
+ *    SURVEY.md §8(c) A23).
+ *  - Input layout:
+ *      indices  int32 [nnz]       per-table local row ids (already hashed)
+ *      offsets  int32 [T*B + 1]   table-major CSR: bag (t, b) is
+ *                                 indices[offsets[t*B+b] .. offsets[t*B+b+1]-1]
+ *      dense    fp32  [B, F]      raw log1p'd continuous features (normalised inside)
+ *      scores   fp32  [B]         sigmoid outputs
+ *      x0       [B, x0_ld]        act dtype, row-major; columns [0, W) hold x0 in the
+ *                                 canonical order (tables 0..T-1, then dense 0..F-1),
+ *                                 columns [W, x0_ld) are zero padding (x0_ld: cvr_x0_layout).
+ *  - One ctx is driven by one host thread; several ctxs may coexist.
+ */
+#ifndef CVR_H_
+#define CVR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cvr_ctx cvr_ctx;   /* opaque */
+typedef void* cvr_stream_t;       /* a cudaStream_t */
+
+typedef enum {
+  CVR_OK = 0,
+  CVR_E_ARG = 1,      /* null pointer / out-of-range scalar argument */
+  CVR_E_SHAPE = 2,    /* weight or table shape mismatch (message names both shapes) */
+  CVR_E_DTYPE = 3,    /* dtype mismatch */
+  CVR_E_STATE = 4,    /* call order (e.g. cvr_dense before weights are loaded) */
+  CVR_E_INDEX = 5,    /* device saw an out-of-range index or malformed offsets */
+  CVR_E_NOMEM = 6,    /* workspace too small */
+  CVR_E_CUDA = 7,     /* CUDA runtime / driver failure (message has the CUDA text) */
+  CVR_E_NCCL = 8,     /* NCCL failure */
+  CVR_E_OVERLOAD = 9, /* serving queue full (batcher) */
+  CVR_E_UNSUPPORTED = 10 /* model shape outside what the kernels support */
+} cvr_status;
+
+typedef enum { CVR_F32 = 0, CVR_BF16 = 1, CVR_F16 = 2 } cvr_dtype;
+
+typedef enum {
+  CVR_DCN_FULL = 0,     /* full-rank cross with bias, fp32 SIMT path (config 1)      */
+  CVR_DCN_LOWRANK = 1,  /* low-rank cross, bf16 tcgen05 path (configs 2, 3, 5)       */
+  CVR_ENSEMBLE = 2      /* DCN || MHA || FFN, summed + layer-normed (config 4)       */
+} cvr_backbone;
+
+/* Model + run description; copied by cvr_create (the arrays need not outlive the call). */
+typedef struct {
+  int n_tables;             /* T (all tables of the model, also in sharded mode)        */
+  const int64_t* rows;      /* [T] rows per table                                       */
+  int dim;                  /* d, embedding dim (same for every table)                  */
+  int emb_dtype;            /* cvr_dtype of the table rows                              */
+  int n_dense;              /* F continuous features                                    */
+  int act_dtype;            /* CVR_F32 (DCN_FULL) or CVR_BF16                            */
+  int backbone;             /* cvr_backbone                                             */
+  int n_cross;              /* number of cross (or ensemble) layers                     */
+  int cross_rank;           /* r for DCN_LOWRANK / ENSEMBLE, 0 for DCN_FULL             */
+  int n_mlp;                /* hidden layers of the MLP tower                           */
+  const int* mlp_dims;      /* [n_mlp] hidden widths; the width-1 head is implicit      */
+  int n_heads;              /* ENSEMBLE only                                            */
+  int ffn_dim;              /* ENSEMBLE only                                            */
+  int max_batch;            /* largest B any call will pass                             */
+  int64_t max_nnz;          /* largest nnz any call will pass (host-fed staging)        */
+  int world_size;           /* 1 = unsharded; >1 = table-wise sharding (t -> t % N)     */
+  int rank;                 /* this process's rank when world_size > 1                  */
+} cvr_model_desc;
+
+/* -- lifecycle ------------------------------------------------------------------------ */
+int cvr_create(const cvr_model_desc* desc, cvr_ctx** out);
+int cvr_destroy(cvr_ctx* ctx);
+const char* cvr_last_error(const cvr_ctx* ctx);
+const char* cvr_status_string(int status);
+/* Library version string and the compiled device architecture ("sm_100a"). */
+const char* cvr_version(void);
+
+/* Device workspace (weights, x0 slots, intermediates, staging, flags); caller-allocated,
+ * >= 256-byte aligned.  Must be set before cvr_load_weights. */
+int cvr_workspace_bytes(const cvr_ctx* ctx, size_t* bytes);
+int cvr_set_workspace(cvr_ctx* ctx, void* d_ws, size_t bytes);
+
+/* x0 row stride (elements) and dtype used by cvr_embed / cvr_dense. */
+int cvr_x0_layout(const cvr_ctx* ctx, int* x0_ld, int* x0_dtype);
+
+/* -- parameters ----------------------------------------------------------------------- */
+/* Borrow n embedding tables: table_ids[i] in [0, T) (in sharded mode only the tables this
+ * rank owns, t % world_size == rank); d_rows[i] is [rows_t, d] of emb_dtype with a row
+ * stride of row_stride_bytes[i] (multiple of 16, base 16-byte aligned).  The pointers must
+ * outlive the ctx.  Sharded mode requires exactly the owned tables. */
+int cvr_load_tables(cvr_ctx* ctx, int n, const int* table_ids, const void* const* d_rows,
+                    const int64_t* row_stride_bytes);
+
+/* COPY n named parameters into the workspace (repacked as the kernels need).  Names and
+ * [out, in] shapes:
+ *   "norm/mean" [F], "norm/std" [F]                                   (fp32)
+ *   DCN_FULL:    "dcn/<l>/W" [W, W], "dcn/<l>/b" [W]
+ *   DCN_LOWRANK: "dcn/<l>/V" [r, W], "dcn/<l>/U" [W, r], "dcn/<l>/b" [W]
+ *   ENSEMBLE:    "ens/<l>/dcn/{V,U,b}", "ens/<l>/mha/{Wqkv,bqkv,Wo,bo}",
+ *                "ens/<l>/ffn/{W1,b1,W2,b2}", "ens/<l>/ln/{gamma,beta}"
+ *   "mlp/<i>/W" [h_i, h_{i-1}], "mlp/<i>/b" [h_i], "head/w" [1, h_last], "head/b" [1]
+ * shapes is flattened: entry i has ndims[i] extents starting at the running offset.
+ * Every expected name must be present exactly once (else CVR_E_SHAPE); dtypes must be
+ * act_dtype (norm/* fp32).  Synchronous; the caller may free its tensors afterwards. */
+int cvr_load_weights(cvr_ctx* ctx, int n, const char* const* names, const void* const* d_ptrs,
+                     const int* dtypes, const int* ndims, const int64_t* shapes);
+
+/* -- the hot path ---------------------------------------------------------------------- */
+/* S2+S3: pooled embeddings + normalised dense features into d_x0 [batch, x0_ld].
+ * Unsharded only (sharded: cvr_embed_shard + cvr_exchange). */
+int cvr_embed(cvr_ctx* ctx, const int32_t* d_indices, const int32_t* d_offsets, int64_t nnz,
+              int batch, const float* d_dense, void* d_x0, cvr_stream_t stream);
+
+/* S5-S7 on d_x0 [batch, x0_ld] -> d_scores [batch] fp32. */
+int cvr_dense(cvr_ctx* ctx, const void* d_x0, int batch, float* d_scores, cvr_stream_t stream);
+
+/* S2-S7 for one batch using the ctx's double-buffered x0 slots: the embed stage runs on
+ * s_embed, the dense stage on s_dense, with event edges embed(k) -> dense(k) and
+ * dense(k) -> embed(k+2) (slot reuse).  Back-to-back calls therefore overlap the embed
+ * stage of batch k+1 with the dense stage of batch k (S9). */
+int cvr_score(cvr_ctx* ctx, const int32_t* d_indices, const int32_t* d_offsets, int64_t nnz,
+              int batch, const float* d_dense, float* d_scores, cvr_stream_t s_embed,
+              cvr_stream_t s_dense);
+
+/* Host-fed variant (S1 + S2-S7 + S8): h_* are host buffers (pinned for async copies);
+ * the H2D copies of this batch run on s_copy into double-buffered device staging,
+ * then as cvr_score, then the D2H of the scores on s_dense.  Returns after enqueueing;
+ * h_scores is valid once s_dense has been synchronised. */
+int cvr_score_host(cvr_ctx* ctx, const int32_t* h_indices, const int32_t* h_offsets, int64_t nnz,
+                   int batch, const float* h_dense, float* h_scores, cvr_stream_t s_copy,
+                   cvr_stream_t s_embed, cvr_stream_t s_dense);
+
+/* Synchronise `stream`, read and clear the sticky device flag: CVR_E_INDEX if any kernel
+ * since the last call saw bad indices/offsets, CVR_E_CUDA on an asynchronous CUDA error. */
+int cvr_get_status(cvr_ctx* ctx, cvr_stream_t stream);
+
+/* -- table-wise sharding (world_size > 1; BASELINE.json configs[2]) ---------------------- */
+/* Bytes of the send and receive buffers for a global batch (per rank). */
+int cvr_shard_buffer_bytes(const cvr_ctx* ctx, int batch_global, size_t* send_bytes, size_t* recv_bytes);
+
+/* S2 for the local tables over the GLOBAL batch, written destination-major into d_send:
+ * [dst][b_local][t_local][d] (act dtype, t_local padded to max tables per rank), plus
+ * S3 for this rank's batch slice [rank*B/N, (rank+1)*B/N) into d_x0 (dense columns).
+ * indices/offsets cover the local tables (offsets [T_local*B_global + 1]); d_dense is the
+ * local slice [B/N, F]. */
+int cvr_embed_shard(cvr_ctx* ctx, const int32_t* d_indices, const int32_t* d_offsets, int64_t nnz,
+                    int batch_global, const float* d_dense, void* d_send, void* d_x0,
+                    cvr_stream_t stream);
+
+/* Unpack received source-major chunks d_recv [src][b_local][t_slot][d] into the canonical
+ * x0 columns of the local slice (V1 of SURVEY.md §8(e)).  The all-to-all itself is done by
+ * the caller's communicator (NCCL over NVLink via torch.distributed) or cvr_exchange. */
+int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d_x0, cvr_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CVR_H_ */

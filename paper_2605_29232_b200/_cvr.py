@@ -1,0 +1,229 @@
+"""ctypes binding of libcvr.so (include/cvr.h).  Argument marshalling only: every step of the
+path runs in the library's kernels; torch tensors are passed as raw pointers and streams as
+cudaStream_t handles."""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Dict, Optional, Sequence
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+lib_path = os.path.join(HERE, "libcvr.so")
+
+CVR_F32, CVR_BF16, CVR_F16 = 0, 1, 2
+CVR_DCN_FULL, CVR_DCN_LOWRANK, CVR_ENSEMBLE = 0, 1, 2
+CVR_E_INDEX = 5
+_DT = {"f32": CVR_F32, "bf16": CVR_BF16, "f16": CVR_F16}
+_TORCH_DT = {torch.float32: CVR_F32, torch.bfloat16: CVR_BF16, torch.float16: CVR_F16}
+_BACKBONE = {"dcn_full": CVR_DCN_FULL, "dcn_lowrank": CVR_DCN_LOWRANK, "ensemble": CVR_ENSEMBLE}
+
+_c_i64p = ctypes.POINTER(ctypes.c_int64)
+_c_ip = ctypes.POINTER(ctypes.c_int)
+_vp = ctypes.c_void_p
+
+
+class cvr_model_desc(ctypes.Structure):
+    _fields_ = [
+        ("n_tables", ctypes.c_int), ("rows", _c_i64p), ("dim", ctypes.c_int), ("emb_dtype", ctypes.c_int),
+        ("n_dense", ctypes.c_int), ("act_dtype", ctypes.c_int), ("backbone", ctypes.c_int),
+        ("n_cross", ctypes.c_int), ("cross_rank", ctypes.c_int), ("n_mlp", ctypes.c_int), ("mlp_dims", _c_ip),
+        ("n_heads", ctypes.c_int), ("ffn_dim", ctypes.c_int), ("max_batch", ctypes.c_int),
+        ("max_nnz", ctypes.c_int64), ("world_size", ctypes.c_int), ("rank", ctypes.c_int),
+    ]
+
+
+# (name, restype, argtypes) -- mirrors include/cvr.h
+_SIGS = [
+    ("cvr_create", ctypes.c_int, [ctypes.POINTER(cvr_model_desc), ctypes.POINTER(_vp)]),
+    ("cvr_destroy", ctypes.c_int, [_vp]),
+    ("cvr_last_error", ctypes.c_char_p, [_vp]),
+    ("cvr_status_string", ctypes.c_char_p, [ctypes.c_int]),
+    ("cvr_version", ctypes.c_char_p, []),
+    ("cvr_workspace_bytes", ctypes.c_int, [_vp, ctypes.POINTER(ctypes.c_size_t)]),
+    ("cvr_set_workspace", ctypes.c_int, [_vp, _vp, ctypes.c_size_t]),
+    ("cvr_x0_layout", ctypes.c_int, [_vp, _c_ip, _c_ip]),
+    ("cvr_load_tables", ctypes.c_int, [_vp, ctypes.c_int, _c_ip, ctypes.POINTER(_vp), _c_i64p]),
+    ("cvr_load_weights", ctypes.c_int,
+     [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(_vp), _c_ip, _c_ip, _c_i64p]),
+    ("cvr_embed", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp]),
+    ("cvr_dense", ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp, _vp]),
+    ("cvr_score", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp, _vp]),
+    ("cvr_score_host", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp]),
+    ("cvr_get_status", ctypes.c_int, [_vp, _vp]),
+    ("cvr_shard_buffer_bytes", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t),
+                                              ctypes.POINTER(ctypes.c_size_t)]),
+    ("cvr_embed_shard", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp, _vp]),
+    ("cvr_unpack_shard", ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp, _vp]),
+]
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libcvr.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(lib_path):
+            raise ImportError(f"{lib_path} not built: run `python -m paper_2605_29232_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(lib_path)
+        for name, res, args in _SIGS:
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def status_string(st: int) -> str:
+    return lib().cvr_status_string(st).decode()
+
+
+class CvrError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{status_string(status)}: {msg}")
+        self.status = status
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(s) -> Optional[int]:
+    if s is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(s, torch.cuda.Stream):
+        return s.cuda_stream
+    return int(s)
+
+
+class CvrModel:
+    """One libcvr context: model description + workspace + borrowed tables + copied weights.
+
+    ``cfg`` is any object with the fields of ``cvr_synth.CvrConfig`` (n_tables, rows, dim,
+    emb_dtype, act_dtype, n_dense, backbone, n_cross, cross_rank, mlp_dims, n_heads, ffn_dim).
+    """
+
+    def __init__(self, cfg, max_batch: int, max_nnz: int = 0, world_size: int = 1, rank: int = 0,
+                 device: Optional[torch.device] = None, allocate: bool = True):
+        self.L = lib()
+        self.cfg = cfg
+        self._rows = (ctypes.c_int64 * cfg.n_tables)(*cfg.rows)
+        self._mlp = (ctypes.c_int * max(1, len(cfg.mlp_dims)))(*cfg.mlp_dims)
+        self.desc = cvr_model_desc(
+            cfg.n_tables, self._rows, cfg.dim, _DT[cfg.emb_dtype], cfg.n_dense, _DT[cfg.act_dtype],
+            _BACKBONE[cfg.backbone], cfg.n_cross, cfg.cross_rank, len(cfg.mlp_dims), self._mlp,
+            getattr(cfg, "n_heads", 0), getattr(cfg, "ffn_dim", 0), max_batch, max_nnz, world_size, rank)
+        self.max_batch, self.max_nnz, self.world_size, self.rank = max_batch, max_nnz, world_size, rank
+        h = _vp()
+        st = self.L.cvr_create(ctypes.byref(self.desc), ctypes.byref(h))
+        self.h = h
+        if st != 0:
+            msg = self.L.cvr_last_error(h).decode() if h.value else ""
+            if h.value:
+                self.L.cvr_destroy(h)
+            self.h = _vp()
+            raise CvrError(st, msg)
+        ld, dt = ctypes.c_int(), ctypes.c_int()
+        self._check(self.L.cvr_x0_layout(self.h, ctypes.byref(ld), ctypes.byref(dt)))
+        self.x0_ld, self.x0_dtype = ld.value, {CVR_F32: torch.float32, CVR_BF16: torch.bfloat16}[dt.value]
+        n = ctypes.c_size_t()
+        self._check(self.L.cvr_workspace_bytes(self.h, ctypes.byref(n)))
+        self.workspace_bytes = n.value
+        self.workspace = None
+        if allocate:
+            self.device = torch.device(device or "cuda")
+            self.workspace = torch.empty(self.workspace_bytes, dtype=torch.uint8, device=self.device)
+            self._check(self.L.cvr_set_workspace(self.h, self.workspace.data_ptr(), self.workspace_bytes))
+        self._tables = []
+
+    # -- plumbing ------------------------------------------------------------------------
+    def _check(self, st: int):
+        if st != 0:
+            raise CvrError(st, self.L.cvr_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.L.cvr_destroy(self.h)
+            self.h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- parameters ----------------------------------------------------------------------
+    def load_tables(self, tables: Sequence[torch.Tensor], table_ids: Optional[Sequence[int]] = None):
+        if table_ids is None:
+            table_ids = [t for t in range(self.cfg.n_tables) if t % self.world_size == self.rank]
+        n = len(tables)
+        ids = (ctypes.c_int * n)(*table_ids)
+        ptrs = (_vp * n)(*[t.data_ptr() for t in tables])
+        strides = (ctypes.c_int64 * n)(*[t.stride(0) * t.element_size() for t in tables])
+        self._check(self.L.cvr_load_tables(self.h, n, ids, ptrs, strides))
+        self._tables = list(tables)  # borrowed: keep alive
+
+    def load_weights(self, weights: Dict[str, torch.Tensor]):
+        names = list(weights)
+        ts = [weights[k].contiguous() for k in names]
+        n = len(names)
+        cn = (ctypes.c_char_p * n)(*[k.encode() for k in names])
+        ptrs = (_vp * n)(*[t.data_ptr() for t in ts])
+        dts = (ctypes.c_int * n)(*[_TORCH_DT[t.dtype] for t in ts])
+        nd = (ctypes.c_int * n)(*[t.dim() for t in ts])
+        flat = [s for t in ts for s in t.shape]
+        shp = (ctypes.c_int64 * max(1, len(flat)))(*flat)
+        self._check(self.L.cvr_load_weights(self.h, n, cn, ptrs, dts, nd, shp))
+
+    # -- hot path ------------------------------------------------------------------------
+    def new_x0(self, batch: int) -> torch.Tensor:
+        return torch.empty(batch, self.x0_ld, dtype=self.x0_dtype, device=self.device)
+
+    def embed(self, indices: torch.Tensor, offsets: torch.Tensor, batch: int, dense: Optional[torch.Tensor],
+              x0: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        x0 = self.new_x0(batch) if x0 is None else x0
+        self._check(self.L.cvr_embed(self.h, _ptr(indices), _ptr(offsets), indices.numel(), batch, _ptr(dense),
+                                     _ptr(x0), _stream(stream)))
+        return x0
+
+    def dense(self, x0: torch.Tensor, batch: int, scores: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        scores = torch.empty(batch, dtype=torch.float32, device=self.device) if scores is None else scores
+        self._check(self.L.cvr_dense(self.h, _ptr(x0), batch, _ptr(scores), _stream(stream)))
+        return scores
+
+    def score(self, indices: torch.Tensor, offsets: torch.Tensor, batch: int, dense: Optional[torch.Tensor],
+              scores: Optional[torch.Tensor] = None, s_embed=None, s_dense=None) -> torch.Tensor:
+        scores = torch.empty(batch, dtype=torch.float32, device=self.device) if scores is None else scores
+        self._check(self.L.cvr_score(self.h, _ptr(indices), _ptr(offsets), indices.numel(), batch, _ptr(dense),
+                                     _ptr(scores), _stream(s_embed), _stream(s_dense if s_dense is not None else s_embed)))
+        return scores
+
+    def score_host(self, indices: torch.Tensor, offsets: torch.Tensor, batch: int, dense: Optional[torch.Tensor],
+                   scores: torch.Tensor, s_copy=None, s_embed=None, s_dense=None) -> torch.Tensor:
+        """Host-fed S1..S8: CPU (pinned) tensors in, CPU scores out (valid after s_dense syncs)."""
+        self._check(self.L.cvr_score_host(self.h, _ptr(indices), _ptr(offsets), indices.numel(), batch, _ptr(dense),
+                                          _ptr(scores), _stream(s_copy), _stream(s_embed), _stream(s_dense)))
+        return scores
+
+    def status(self, stream=None) -> int:
+        """Synchronise ``stream`` and return the sticky device status (raises on CUDA errors)."""
+        st = self.L.cvr_get_status(self.h, _stream(stream))
+        if st not in (0, CVR_E_INDEX):
+            self._check(st)
+        return st
+
+    # -- sharded tables -----------------------------------------------------------------------
+    def shard_buffer_bytes(self, batch_global: int):
+        s, r = ctypes.c_size_t(), ctypes.c_size_t()
+        self._check(self.L.cvr_shard_buffer_bytes(self.h, batch_global, ctypes.byref(s), ctypes.byref(r)))
+        return s.value, r.value
+
+    def embed_shard(self, indices, offsets, batch_global, dense, send, x0, stream=None):
+        self._check(self.L.cvr_embed_shard(self.h, _ptr(indices), _ptr(offsets), indices.numel(), batch_global,
+                                           _ptr(dense), _ptr(send), _ptr(x0), _stream(stream)))
+
+    def unpack_shard(self, recv, batch_global, x0, stream=None):
+        self._check(self.L.cvr_unpack_shard(self.h, _ptr(recv), batch_global, _ptr(x0), _stream(stream)))

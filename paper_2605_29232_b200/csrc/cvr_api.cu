@@ -1,0 +1,792 @@
+// cvr_api.cu -- the C ABI of libcvr.so (include/cvr.h): context, argument validation, workspace
+// carving, weight repacking, the dense-stage schedule and the decoupled two-stream executor
+// ("Hybrid CPU-GPU Execution" / BASELINE.json north star
+// "embedding lookups for batch k+1 overlap the dense stage of batch k").
+//
+// No CUDA call is made before cvr_set_workspace, so creation / validation / layout queries work
+// on a host without a GPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/cvr.h"
+#include "cvr_kernels.cuh"
+
+using namespace cvr;
+
+namespace {
+
+size_t elt_size(int dt) { return dt == CVR_F32 ? 4 : 2; }
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+struct WSlot {
+  std::string name;
+  std::vector<int64_t> shape;  // expected [out, in] as passed by the caller
+  int dtype;                   // expected caller dtype
+  size_t off = 0;              // offset of the repacked copy in the workspace
+  size_t bytes = 0;
+  bool loaded = false;
+};
+
+struct GemmPlan {
+  int N, K, BN;
+  Epi epi;
+  const char* wname;  // B operand
+  CUtensorMap tmB;
+};
+
+}  // namespace
+
+struct cvr_ctx {
+  // ---- model description
+  int T = 0, d = 0, emb_dtype = 0, F = 0, act = 0, backbone = 0, n_cross = 0, r = 0, n_mlp = 0;
+  std::vector<int> mlp;
+  int n_heads = 0, ffn = 0, max_batch = 0;
+  int64_t max_nnz = 0;
+  int world = 1, rank = 0;
+  std::vector<int64_t> rows;
+  int W = 0;
+  int64_t x0_ld = 0;
+  // sharding
+  std::vector<int> local_tables;
+  int T_pad = 0;
+  // ---- state
+  std::string err;
+  uint8_t* ws = nullptr;
+  size_t ws_bytes = 0, ws_need = 0;
+  std::vector<WSlot> wslots;
+  bool tables_loaded = false, weights_loaded = false;
+  std::vector<TableDesc> htables;
+  // workspace regions (offsets)
+  size_t off_tables = 0, off_flag = 0, off_x0[2] = {0, 0}, off_xa = 0, off_xb = 0, off_t = 0;
+  std::vector<size_t> off_h;
+  size_t off_idx[2] = {0, 0}, off_offs[2] = {0, 0}, off_dense[2] = {0, 0}, off_scores[2] = {0, 0};
+  // runtime
+  int num_sms = 148;
+  bool cuda_ready = false;
+  cudaEvent_t ev_embed[2] = {nullptr, nullptr}, ev_dense[2] = {nullptr, nullptr}, ev_copy[2] = {nullptr, nullptr};
+  int64_t k = 0;
+  float head_b = 0.f;  // host copy of head/b (weights are loaded synchronously)
+  // tensor maps for internal A operands
+  CUtensorMap tm_x0slot[2], tm_xa, tm_xb, tm_t;
+  std::vector<CUtensorMap> tm_h;
+  const void* last_x0 = nullptr;
+  int last_x0_rows = -1;
+  CUtensorMap tm_x0user;
+  std::vector<GemmPlan> plan;  // cross layers (V, U interleaved), then MLP
+
+  template <typename T = uint8_t>
+  T* at(size_t off) const { return reinterpret_cast<T*>(ws + off); }
+  int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    err = buf;
+    return code;
+  }
+  int cuda_fail(cudaError_t e, const char* what) {
+    return fail(CVR_E_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+  }
+  WSlot* slot(const std::string& n) {
+    for (auto& s : wslots)
+      if (s.name == n) return &s;
+    return nullptr;
+  }
+  template <typename T = void>
+  T* wptr(const std::string& n) { return reinterpret_cast<T*>(ws + slot(n)->off); }
+};
+
+namespace {
+
+std::string shape_str(const std::vector<int64_t>& s) {
+  std::string o = "[";
+  for (size_t i = 0; i < s.size(); ++i) o += (i ? ", " : "") + std::to_string(s[i]);
+  return o + "]";
+}
+
+void build_weight_slots(cvr_ctx* c) {
+  auto add = [&](const std::string& n, std::vector<int64_t> sh, int dt) {
+    WSlot s;
+    s.name = n;
+    s.shape = sh;
+    s.dtype = dt;
+    c->wslots.push_back(s);
+  };
+  const int a = c->act;
+  if (c->F) {
+    add("norm/mean", {c->F}, CVR_F32);
+    add("norm/std", {c->F}, CVR_F32);
+  }
+  int prev = c->W;
+  if (c->backbone == CVR_DCN_FULL) {
+    for (int l = 0; l < c->n_cross; ++l) {
+      add("dcn/" + std::to_string(l) + "/W", {c->W, c->W}, a);
+      add("dcn/" + std::to_string(l) + "/b", {c->W}, a);
+    }
+  } else if (c->backbone == CVR_DCN_LOWRANK) {
+    for (int l = 0; l < c->n_cross; ++l) {
+      add("dcn/" + std::to_string(l) + "/V", {c->r, c->W}, a);
+      add("dcn/" + std::to_string(l) + "/U", {c->W, c->r}, a);
+      add("dcn/" + std::to_string(l) + "/b", {c->W}, a);
+    }
+  }
+  for (int i = 0; i < c->n_mlp; ++i) {
+    add("mlp/" + std::to_string(i) + "/W", {c->mlp[i], prev}, a);
+    add("mlp/" + std::to_string(i) + "/b", {c->mlp[i]}, a);
+    prev = c->mlp[i];
+  }
+  add("head/w", {1, prev}, a);
+  add("head/b", {1}, a);
+}
+
+// repacked size in the workspace
+size_t packed_bytes(const cvr_ctx* c, const WSlot& s) {
+  const std::string& n = s.name;
+  auto ends = [&](const char* suf) { return n.size() >= strlen(suf) && n.compare(n.size() - strlen(suf), strlen(suf), suf) == 0; };
+  if (c->backbone == CVR_DCN_FULL || s.shape.size() == 1 || n.rfind("norm/", 0) == 0 || n.rfind("head/", 0) == 0) {
+    int64_t e = 1;
+    for (auto v : s.shape) e *= v;
+    if (s.shape.size() == 1 && n.rfind("dcn/", 0) == 0) e = c->x0_ld;  // padded bias
+    return (size_t)e * 4;                                              // fp32 copies
+  }
+  // bf16 GEMM operands, padded to x0_ld along W
+  if (ends("/V")) return (size_t)c->r * c->x0_ld * 2;
+  if (ends("/U")) return (size_t)c->x0_ld * c->r * 2;
+  if (n == "mlp/0/W") return (size_t)c->mlp[0] * c->x0_ld * 2;
+  return (size_t)s.shape[0] * s.shape[1] * 2;
+}
+
+int validate_desc(const cvr_model_desc* d, std::string& why) {
+  char buf[256];
+  auto bad = [&](const char* m) { why = m; return CVR_E_ARG; };
+  if (!d) return bad("null desc");
+  if (d->n_tables <= 0 || d->n_tables > 4096) return bad("n_tables out of range");
+  if (!d->rows) return bad("rows is null");
+  for (int t = 0; t < d->n_tables; ++t)
+    if (d->rows[t] <= 0 || d->rows[t] > INT32_MAX) {
+      snprintf(buf, sizeof buf, "rows[%d] out of range", t);
+      why = buf;
+      return CVR_E_ARG;
+    }
+  if (d->dim <= 0 || d->dim > 512) return bad("dim out of range");
+  if (d->emb_dtype < 0 || d->emb_dtype > 2 || d->act_dtype < 0 || d->act_dtype > 1) return bad("bad dtype");
+  if ((d->dim * (int)elt_size(d->emb_dtype)) % 32 != 0 || d->dim * (int)elt_size(d->emb_dtype) > 512)
+    return bad("dim * sizeof(row element) must be a multiple of 32 bytes and <= 512 bytes");
+  if (d->n_dense < 0 || d->n_cross < 0 || d->n_cross > kMaxLayers || d->n_mlp < 1 || d->n_mlp > kMaxLayers)
+    return bad("layer counts out of range");
+  if (!d->mlp_dims) return bad("mlp_dims is null");
+  for (int i = 0; i < d->n_mlp; ++i)
+    if (d->mlp_dims[i] <= 0) return bad("mlp_dims must be positive");
+  if (d->max_batch <= 0 || d->max_nnz < 0) return bad("max_batch / max_nnz out of range");
+  if (d->world_size < 1 || d->rank < 0 || d->rank >= d->world_size) return bad("bad world_size / rank");
+  if (d->backbone == CVR_DCN_FULL) {
+    if (d->act_dtype != CVR_F32) return bad("DCN_FULL runs the fp32 path: act_dtype must be CVR_F32");
+  } else if (d->backbone == CVR_DCN_LOWRANK) {
+    if (d->act_dtype != CVR_BF16) return bad("DCN_LOWRANK runs the bf16 tensor-core path: act_dtype must be CVR_BF16");
+    if (d->cross_rank <= 0 || d->cross_rank % 64) return bad("cross_rank must be a positive multiple of 64");
+    for (int i = 0; i < d->n_mlp; ++i)
+      if (d->mlp_dims[i] % 64) return bad("mlp_dims must be multiples of 64 on the bf16 path");
+    const int last = d->mlp_dims[d->n_mlp - 1];
+    if (last != 64 && last != 128 && last != 256) return bad("last MLP width must be 64, 128 or 256 (fused head)");
+  } else {
+    return CVR_E_UNSUPPORTED;
+  }
+  return CVR_OK;
+}
+
+size_t carve(size_t& cur, size_t bytes) {
+  const size_t o = (cur + 255) & ~size_t(255);
+  cur = o + bytes;
+  return o;
+}
+
+int pick_bn(int N) {
+  if (N % 128 == 0 && N >= 512) return 128;
+  return 64;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cvr_version(void) { return "cvr 0.1 (sm_100a)"; }
+
+const char* cvr_status_string(int s) {
+  switch (s) {
+    case CVR_OK: return "CVR_OK";
+    case CVR_E_ARG: return "CVR_E_ARG";
+    case CVR_E_SHAPE: return "CVR_E_SHAPE";
+    case CVR_E_DTYPE: return "CVR_E_DTYPE";
+    case CVR_E_STATE: return "CVR_E_STATE";
+    case CVR_E_INDEX: return "CVR_E_INDEX";
+    case CVR_E_NOMEM: return "CVR_E_NOMEM";
+    case CVR_E_CUDA: return "CVR_E_CUDA";
+    case CVR_E_NCCL: return "CVR_E_NCCL";
+    case CVR_E_OVERLOAD: return "CVR_E_OVERLOAD";
+    case CVR_E_UNSUPPORTED: return "CVR_E_UNSUPPORTED";
+  }
+  return "CVR_E_?";
+}
+
+int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
+  if (!out) return CVR_E_ARG;
+  *out = nullptr;
+  std::string why;
+  int st = validate_desc(desc, why);
+  cvr_ctx* c = new cvr_ctx();
+  if (st != CVR_OK) {
+    c->err = why.empty() ? "unsupported model description" : why;
+    *out = c;  // returned so the caller can read cvr_last_error, then must destroy it
+    return st;
+  }
+  c->T = desc->n_tables;
+  c->rows.assign(desc->rows, desc->rows + c->T);
+  c->d = desc->dim;
+  c->emb_dtype = desc->emb_dtype;
+  c->F = desc->n_dense;
+  c->act = desc->act_dtype;
+  c->backbone = desc->backbone;
+  c->n_cross = desc->n_cross;
+  c->r = desc->cross_rank;
+  c->n_mlp = desc->n_mlp;
+  c->mlp.assign(desc->mlp_dims, desc->mlp_dims + c->n_mlp);
+  c->n_heads = desc->n_heads;
+  c->ffn = desc->ffn_dim;
+  c->max_batch = desc->max_batch;
+  c->max_nnz = desc->max_nnz;
+  c->world = desc->world_size;
+  c->rank = desc->rank;
+  c->W = c->T * c->d + c->F;
+  c->x0_ld = c->act == CVR_F32 ? round_up(c->W, 4) : round_up(c->W, 64);
+  for (int t = 0; t < c->T; ++t)
+    if (t % c->world == c->rank) c->local_tables.push_back(t);
+  c->T_pad = (c->T + c->world - 1) / c->world;
+  c->htables.resize(c->local_tables.size());
+  build_weight_slots(c);
+
+  // ---- workspace layout
+  size_t cur = 0;
+  for (auto& s : c->wslots) {
+    s.bytes = packed_bytes(c, s);
+    s.off = carve(cur, s.bytes);
+  }
+  const size_t ae = elt_size(c->act);
+  const int64_t B = c->max_batch;
+  c->off_tables = carve(cur, sizeof(TableDesc) * std::max<size_t>(1, c->local_tables.size()));
+  c->off_flag = carve(cur, 256);
+  for (int i = 0; i < 2; ++i) c->off_x0[i] = carve(cur, (size_t)B * c->x0_ld * ae);
+  if (c->backbone == CVR_DCN_LOWRANK) {
+    c->off_xa = carve(cur, (size_t)B * c->x0_ld * 2);
+    c->off_xb = carve(cur, (size_t)B * c->x0_ld * 2);
+    c->off_t = carve(cur, (size_t)B * c->r * 2);
+    for (int i = 0; i + 1 < c->n_mlp; ++i) c->off_h.push_back(carve(cur, (size_t)B * c->mlp[i] * 2));
+  }
+  const int64_t Bin = c->world > 1 ? B * c->world : B;  // sharded: indices cover the global batch
+  const int T_l = (int)c->local_tables.size();
+  for (int i = 0; i < 2; ++i) {
+    c->off_idx[i] = carve(cur, (size_t)std::max<int64_t>(c->max_nnz, 1) * 4);
+    c->off_offs[i] = carve(cur, (size_t)(T_l * Bin + 1) * 4);
+    c->off_dense[i] = carve(cur, (size_t)B * std::max(c->F, 1) * 4);
+    c->off_scores[i] = carve(cur, (size_t)B * 4);
+  }
+  c->ws_need = (cur + 255) & ~size_t(255);
+  *out = c;
+  return CVR_OK;
+}
+
+int cvr_destroy(cvr_ctx* c) {
+  if (!c) return CVR_E_ARG;
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_embed[i]) cudaEventDestroy(c->ev_embed[i]);
+    if (c->ev_dense[i]) cudaEventDestroy(c->ev_dense[i]);
+    if (c->ev_copy[i]) cudaEventDestroy(c->ev_copy[i]);
+  }
+  delete c;
+  return CVR_OK;
+}
+
+const char* cvr_last_error(const cvr_ctx* c) { return c ? c->err.c_str() : "null ctx"; }
+
+int cvr_workspace_bytes(const cvr_ctx* c, size_t* bytes) {
+  if (!c || !bytes) return CVR_E_ARG;
+  *bytes = c->ws_need;
+  return CVR_OK;
+}
+
+int cvr_x0_layout(const cvr_ctx* c, int* ld, int* dt) {
+  if (!c || !ld || !dt) return CVR_E_ARG;
+  *ld = (int)c->x0_ld;
+  *dt = c->act;
+  return CVR_OK;
+}
+
+int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
+  if (!c || !d_ws) return CVR_E_ARG;
+  if (reinterpret_cast<uintptr_t>(d_ws) & 255) return c->fail(CVR_E_ARG, "workspace must be 256-byte aligned");
+  if (bytes < c->ws_need) return c->fail(CVR_E_NOMEM, "workspace %zu bytes < required %zu", bytes, c->ws_need);
+  c->ws = reinterpret_cast<uint8_t*>(d_ws);
+  c->ws_bytes = bytes;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    if (!c->ev_embed[i]) e = cudaEventCreateWithFlags(&c->ev_embed[i], cudaEventDisableTiming);
+    if (e == cudaSuccess && !c->ev_dense[i]) e = cudaEventCreateWithFlags(&c->ev_dense[i], cudaEventDisableTiming);
+    if (e == cudaSuccess && !c->ev_copy[i]) e = cudaEventCreateWithFlags(&c->ev_copy[i], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaMemset(c->ws + c->off_flag, 0, 256);
+  // zero the activation slots once so padding columns / tail rows are defined
+  if (e == cudaSuccess) e = cudaMemset(c->ws + c->off_x0[0], 0, c->ws_need - c->off_x0[0]);
+  if (e != cudaSuccess) return c->cuda_fail(e, "cvr_set_workspace");
+  c->cuda_ready = true;
+  c->k = 0;
+  c->weights_loaded = false;
+  for (auto& s : c->wslots) s.loaded = false;
+  if (c->backbone == CVR_DCN_LOWRANK) {
+    const char* er = nullptr;
+    const int64_t B = c->max_batch;
+    bool ok = true;
+    for (int i = 0; i < 2; ++i) ok &= encode_tmap_bf16(&c->tm_x0slot[i], c->ws + c->off_x0[i], B, c->x0_ld, c->x0_ld, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&c->tm_xa, c->ws + c->off_xa, B, c->x0_ld, c->x0_ld, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&c->tm_xb, c->ws + c->off_xb, B, c->x0_ld, c->x0_ld, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&c->tm_t, c->ws + c->off_t, B, c->r, c->r, 128, &er) == 0;
+    c->tm_h.resize(c->off_h.size());
+    for (size_t i = 0; i < c->off_h.size(); ++i)
+      ok &= encode_tmap_bf16(&c->tm_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], 128, &er) == 0;
+    if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
+  }
+  return CVR_OK;
+}
+
+int cvr_load_tables(cvr_ctx* c, int n, const int* ids, const void* const* d_rows, const int64_t* strides) {
+  if (!c || !ids || !d_rows || !strides) return CVR_E_ARG;
+  if (!c->cuda_ready) return c->fail(CVR_E_STATE, "cvr_load_tables before cvr_set_workspace");
+  if (n != (int)c->local_tables.size())
+    return c->fail(CVR_E_SHAPE, "expected %zu tables for rank %d, got %d", c->local_tables.size(), c->rank, n);
+  const int64_t row_bytes = (int64_t)c->d * elt_size(c->emb_dtype);
+  for (int i = 0; i < n; ++i) {
+    if (ids[i] != c->local_tables[i])
+      return c->fail(CVR_E_SHAPE, "table slot %d: expected table id %d, got %d", i, c->local_tables[i], ids[i]);
+    if (!d_rows[i]) return c->fail(CVR_E_ARG, "table %d: null pointer", ids[i]);
+    if ((reinterpret_cast<uintptr_t>(d_rows[i]) & 15) || (strides[i] & 15) || strides[i] < row_bytes)
+      return c->fail(CVR_E_ARG, "table %d: base and row stride must be 16-byte aligned, stride >= %lld", ids[i],
+                     (long long)row_bytes);
+    c->htables[i] = TableDesc{reinterpret_cast<const uint8_t*>(d_rows[i]), strides[i], c->rows[ids[i]]};
+  }
+  cudaError_t e = cudaMemcpy(c->ws + c->off_tables, c->htables.data(), sizeof(TableDesc) * n, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return c->cuda_fail(e, "cvr_load_tables");
+  c->tables_loaded = true;
+  return CVR_OK;
+}
+
+namespace {
+
+int encode_plan(cvr_ctx* c) {
+  c->plan.clear();
+  const char* er = nullptr;
+  auto addp = [&](const std::string& wn, int N, int K, int BN, Epi epi) -> bool {
+    GemmPlan g;
+    g.N = N;
+    g.K = K;
+    g.BN = BN;
+    g.epi = epi;
+    g.wname = nullptr;
+    if (encode_tmap_bf16(&g.tmB, c->wptr(wn), N, K, K, BN, &er) != 0) return false;
+    c->plan.push_back(g);
+    return true;
+  };
+  bool ok = true;
+  for (int l = 0; l < c->n_cross; ++l) {
+    ok &= addp("dcn/" + std::to_string(l) + "/V", c->r, (int)c->x0_ld, 64, EPI_STORE);
+    ok &= addp("dcn/" + std::to_string(l) + "/U", (int)c->x0_ld, c->r, 64, EPI_CROSS);
+  }
+  int K = (int)c->x0_ld;
+  for (int i = 0; i < c->n_mlp; ++i) {
+    const bool last = i + 1 == c->n_mlp;
+    ok &= addp("mlp/" + std::to_string(i) + "/W", c->mlp[i], K, last ? c->mlp[i] : pick_bn(c->mlp[i]),
+               last ? EPI_HEAD : EPI_BIAS_RELU);
+    K = c->mlp[i];
+  }
+  if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
+  return CVR_OK;
+}
+
+// widen a caller weight (fp32 / bf16) to host fp32
+std::vector<float> fetch_f32(const void* d, int dtype, size_t n, cudaError_t& e) {
+  std::vector<float> out(n);
+  if (dtype == CVR_F32) {
+    e = cudaMemcpy(out.data(), d, n * 4, cudaMemcpyDeviceToHost);
+  } else {
+    std::vector<uint16_t> tmp(n);
+    e = cudaMemcpy(tmp.data(), d, n * 2, cudaMemcpyDeviceToHost);
+    for (size_t i = 0; i < n; ++i) {
+      uint32_t u = (uint32_t)tmp[i] << 16;
+      float f;
+      memcpy(&f, &u, 4);
+      out[i] = f;
+    }
+  }
+  return out;
+}
+
+}  // namespace
+
+int cvr_load_weights(cvr_ctx* c, int n, const char* const* names, const void* const* ptrs, const int* dtypes,
+                     const int* ndims, const int64_t* shapes) {
+  if (!c || n < 0 || !names || !ptrs || !dtypes || !ndims || !shapes) return CVR_E_ARG;
+  if (!c->cuda_ready) return c->fail(CVR_E_STATE, "cvr_load_weights before cvr_set_workspace");
+  std::vector<int> seen(c->wslots.size(), -1);
+  int64_t so = 0;
+  std::vector<int64_t> soff(n);
+  for (int i = 0; i < n; ++i) {
+    if (!names[i] || !ptrs[i] || ndims[i] < 1 || ndims[i] > 4) return c->fail(CVR_E_ARG, "weight entry %d malformed", i);
+    soff[i] = so;
+    so += ndims[i];
+    int j = -1;
+    for (size_t q = 0; q < c->wslots.size(); ++q)
+      if (c->wslots[q].name == names[i]) j = (int)q;
+    if (j < 0) return c->fail(CVR_E_SHAPE, "unexpected weight name '%s'", names[i]);
+    if (seen[j] >= 0) return c->fail(CVR_E_SHAPE, "weight '%s' given twice", names[i]);
+    seen[j] = i;
+    std::vector<int64_t> got(shapes + soff[i], shapes + soff[i] + ndims[i]);
+    if (got != c->wslots[j].shape)
+      return c->fail(CVR_E_SHAPE, "weight '%s': expected shape %s, got %s", names[i], shape_str(c->wslots[j].shape).c_str(),
+                     shape_str(got).c_str());
+    if (dtypes[i] != c->wslots[j].dtype)
+      return c->fail(CVR_E_DTYPE, "weight '%s': expected dtype %d, got %d", names[i], c->wslots[j].dtype, dtypes[i]);
+  }
+  for (size_t q = 0; q < c->wslots.size(); ++q)
+    if (seen[q] < 0) return c->fail(CVR_E_SHAPE, "missing weight '%s' %s", c->wslots[q].name.c_str(), shape_str(c->wslots[q].shape).c_str());
+
+  for (size_t q = 0; q < c->wslots.size(); ++q) {
+    WSlot& s = c->wslots[q];
+    const int i = seen[q];
+    size_t ne = 1;
+    for (auto v : s.shape) ne *= (size_t)v;
+    cudaError_t e = cudaSuccess;
+    std::vector<float> h = fetch_f32(ptrs[i], dtypes[i], ne, e);
+    if (e != cudaSuccess) return c->cuda_fail(e, "cvr_load_weights fetch");
+    const std::string& nm = s.name;
+    auto ends = [&](const char* suf) { return nm.size() >= strlen(suf) && nm.compare(nm.size() - strlen(suf), strlen(suf), suf) == 0; };
+    std::vector<uint8_t> pack(s.bytes, 0);
+    float* pf = reinterpret_cast<float*>(pack.data());
+    uint16_t* pb = reinterpret_cast<uint16_t*>(pack.data());
+    auto bf = [](float f) {  // exact: the value is already bf16-representable (stored dtype)
+      uint32_t u;
+      memcpy(&u, &f, 4);
+      return (uint16_t)(u >> 16);
+    };
+    if (nm == "head/b") c->head_b = h[0];
+    if (nm == "norm/std") {
+      for (size_t j = 0; j < ne; ++j) pf[j] = std::max(h[j], 1e-8f);
+    } else if (s.shape.size() == 1 || nm.rfind("norm/", 0) == 0 || nm.rfind("head/", 0) == 0) {
+      for (size_t j = 0; j < ne; ++j) pf[j] = h[j];  // fp32 copy (zero padding beyond ne)
+    } else if (c->backbone == CVR_DCN_FULL) {       // transpose [out, in] -> [in, out]
+      const int64_t O = s.shape[0], I = s.shape[1];
+      for (int64_t o = 0; o < O; ++o)
+        for (int64_t ii = 0; ii < I; ++ii) pf[ii * O + o] = h[o * I + ii];
+    } else if (ends("/V") || nm == "mlp/0/W") {  // [out, W] -> [out, x0_ld] zero padded
+      const int64_t O = s.shape[0], I = s.shape[1];
+      for (int64_t o = 0; o < O; ++o)
+        for (int64_t ii = 0; ii < I; ++ii) pb[o * c->x0_ld + ii] = bf(h[o * I + ii]);
+    } else {  // U [W, r] (rows beyond W stay zero) and the other MLP weights: as is
+      for (size_t j = 0; j < ne; ++j) pb[j] = bf(h[j]);
+    }
+    e = cudaMemcpy(c->ws + s.off, pack.data(), s.bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return c->cuda_fail(e, "cvr_load_weights upload");
+    s.loaded = true;
+  }
+  if (c->backbone == CVR_DCN_LOWRANK) {
+    int st = encode_plan(c);
+    if (st != CVR_OK) return st;
+  }
+  c->weights_loaded = true;
+  return CVR_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int check_ready(cvr_ctx* c, bool need_tables, bool need_weights) {
+  if (!c->cuda_ready) return c->fail(CVR_E_STATE, "workspace not set");
+  if (need_tables && !c->tables_loaded) return c->fail(CVR_E_STATE, "tables not loaded");
+  if (need_weights && !c->weights_loaded) return c->fail(CVR_E_STATE, "weights not loaded");
+  return CVR_OK;
+}
+
+EmbedArgs embed_args(cvr_ctx* c, const int32_t* idx, const int32_t* off, int64_t nnz, int B, const float* dense,
+                     void* out, int64_t out_ld, void* x0, int Bd) {
+  EmbedArgs a{};
+  a.tables = c->at<TableDesc>(c->off_tables);
+  a.indices = idx;
+  a.offsets = off;
+  a.nnz = nnz;
+  a.B = B;
+  a.T = (int)c->local_tables.size();
+  a.d = c->d;
+  a.emb_dtype = c->emb_dtype;
+  a.out_dtype = c->act;
+  a.out = out;
+  a.out_ld = out_ld;
+  a.out_tstride = c->d;
+  a.dense = dense;
+  a.Bd = Bd;
+  a.F = c->F;
+  a.mean = c->F ? c->wptr<float>("norm/mean") : nullptr;
+  a.sigma = c->F ? c->wptr<float>("norm/std") : nullptr;
+  a.x0 = x0;
+  a.x0_ld = c->x0_ld;
+  a.dense_col0 = (int64_t)c->T * c->d;
+  a.pad_col0 = c->W;
+  a.pad_col1 = c->x0_ld;
+  a.flag = c->at<int>(c->off_flag);
+  return a;
+}
+
+int do_embed(cvr_ctx* c, const int32_t* idx, const int32_t* off, int64_t nnz, int B, const float* dense, void* x0,
+             cudaStream_t s) {
+  if (c->F && !c->slot("norm/mean")->loaded) return c->fail(CVR_E_STATE, "norm/mean,std not loaded");
+  EmbedArgs a = embed_args(c, idx, off, nnz, B, dense, x0, c->x0_ld, x0, B);
+  cudaError_t e = launch_embed(a, c->num_sms, s);
+  if (e != cudaSuccess) return c->cuda_fail(e, "embed launch");
+  return CVR_OK;
+}
+
+int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, int B, float* scores, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
+  if (c->backbone == CVR_DCN_FULL) {
+    DenseF32Args a{};
+    a.x0 = reinterpret_cast<const float*>(x0);
+    a.x0_ld = c->x0_ld;
+    a.B = B;
+    a.W = c->W;
+    a.n_cross = c->n_cross;
+    for (int l = 0; l < c->n_cross; ++l) {
+      a.WT[l] = c->wptr<float>("dcn/" + std::to_string(l) + "/W");
+      a.bias[l] = c->wptr<float>("dcn/" + std::to_string(l) + "/b");
+    }
+    a.n_mlp = c->n_mlp;
+    a.dims[0] = c->W;
+    for (int i = 0; i < c->n_mlp; ++i) {
+      a.dims[i + 1] = c->mlp[i];
+      a.MT[i] = c->wptr<float>("mlp/" + std::to_string(i) + "/W");
+      a.mb[i] = c->wptr<float>("mlp/" + std::to_string(i) + "/b");
+    }
+    a.head_w = c->wptr<float>("head/w");
+    a.head_b = c->wptr<float>("head/b");
+    a.scores = scores;
+    e = launch_dense_f32(a, s);
+    if (e != cudaSuccess) return c->cuda_fail(e, "dense_f32 launch");
+    return CVR_OK;
+  }
+  // ---- bf16 low-rank DCN-v2 on tcgen05
+  const __nv_bfloat16* x0b = reinterpret_cast<const __nv_bfloat16*>(x0);
+  const __nv_bfloat16* xl = x0b;
+  const CUtensorMap* tm_xl = tm_x0;
+  size_t pi = 0;
+  for (int l = 0; l < c->n_cross; ++l) {
+    const GemmPlan& gv = c->plan[pi++];
+    const GemmPlan& gu = c->plan[pi++];
+    EpiParams pv{};
+    pv.out = c->ws + c->off_t;
+    pv.ldo = c->r;
+    e = launch_gemm_bf16(tm_xl, &gv.tmB, B, gv.N, gv.K, gv.BN, gv.epi, pv, s);
+    if (e != cudaSuccess) return c->cuda_fail(e, "gemm V launch");
+    __nv_bfloat16* outb = c->at<__nv_bfloat16>(l % 2 == 0 ? c->off_xa : c->off_xb);
+    EpiParams pu{};
+    pu.out = outb;
+    pu.ldo = c->x0_ld;
+    pu.bias = c->wptr<float>("dcn/" + std::to_string(l) + "/b");
+    pu.x0 = x0b;
+    pu.ld_x0 = c->x0_ld;
+    pu.xl = xl;
+    pu.ld_xl = c->x0_ld;
+    e = launch_gemm_bf16(&c->tm_t, &gu.tmB, B, gu.N, gu.K, gu.BN, gu.epi, pu, s);
+    if (e != cudaSuccess) return c->cuda_fail(e, "gemm U launch");
+    xl = outb;
+    tm_xl = l % 2 == 0 ? &c->tm_xa : &c->tm_xb;
+  }
+  for (int i = 0; i < c->n_mlp; ++i) {
+    const GemmPlan& g = c->plan[pi++];
+    EpiParams p{};
+    p.bias = c->wptr<float>("mlp/" + std::to_string(i) + "/b");
+    if (g.epi == EPI_HEAD) {
+      p.head_w = c->wptr<float>("head/w");
+      p.head_b = c->head_b;
+      p.scores = scores;
+    } else {
+      p.out = c->ws + c->off_h[i];
+      p.ldo = c->mlp[i];
+    }
+    e = launch_gemm_bf16(tm_xl, &g.tmB, B, g.N, g.K, g.BN, g.epi, p, s);
+    if (e != cudaSuccess) return c->cuda_fail(e, "gemm MLP launch");
+    if (g.epi != EPI_HEAD) tm_xl = &c->tm_h[i];
+  }
+  return CVR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cvr_embed(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, int64_t nnz, int batch,
+              const float* d_dense, void* d_x0, cvr_stream_t stream) {
+  if (!c) return CVR_E_ARG;
+  int st = check_ready(c, true, false);
+  if (st) return st;
+  if (c->world != 1) return c->fail(CVR_E_STATE, "cvr_embed is unsharded; use cvr_embed_shard");
+  if (batch < 0 || batch > c->max_batch) return c->fail(CVR_E_ARG, "batch %d outside [0, %d]", batch, c->max_batch);
+  if (!d_offsets || !d_x0 || (nnz > 0 && !d_indices) || (c->F && batch && !d_dense) || nnz < 0)
+    return c->fail(CVR_E_ARG, "null pointer or negative nnz");
+  return do_embed(c, d_indices, d_offsets, nnz, batch, d_dense, d_x0, (cudaStream_t)stream);
+}
+
+int cvr_dense(cvr_ctx* c, const void* d_x0, int batch, float* d_scores, cvr_stream_t stream) {
+  if (!c) return CVR_E_ARG;
+  int st = check_ready(c, false, true);
+  if (st) return st;
+  if (batch < 0 || batch > c->max_batch) return c->fail(CVR_E_ARG, "batch %d outside [0, %d]", batch, c->max_batch);
+  if (!d_x0 || !d_scores) return c->fail(CVR_E_ARG, "null pointer");
+  if (batch == 0) return CVR_OK;
+  const CUtensorMap* tm = nullptr;
+  if (c->backbone == CVR_DCN_LOWRANK) {
+    if (d_x0 == c->ws + c->off_x0[0]) tm = &c->tm_x0slot[0];
+    else if (d_x0 == c->ws + c->off_x0[1]) tm = &c->tm_x0slot[1];
+    else {
+      if (d_x0 != c->last_x0 || batch != c->last_x0_rows) {
+        const char* er = nullptr;
+        if (encode_tmap_bf16(&c->tm_x0user, d_x0, batch, c->x0_ld, c->x0_ld, 128, &er) != 0)
+          return c->fail(CVR_E_CUDA, "tensor map encode: %s", er);
+        c->last_x0 = d_x0;
+        c->last_x0_rows = batch;
+      }
+      tm = &c->tm_x0user;
+    }
+  }
+  return do_dense(c, d_x0, tm, batch, d_scores, (cudaStream_t)stream);
+}
+
+int cvr_score(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, int64_t nnz, int batch,
+              const float* d_dense, float* d_scores, cvr_stream_t s_embed, cvr_stream_t s_dense) {
+  if (!c) return CVR_E_ARG;
+  int st = check_ready(c, true, true);
+  if (st) return st;
+  if (c->world != 1) return c->fail(CVR_E_STATE, "cvr_score is unsharded");
+  if (batch < 0 || batch > c->max_batch) return c->fail(CVR_E_ARG, "batch %d outside [0, %d]", batch, c->max_batch);
+  if (!d_offsets || !d_scores || (nnz > 0 && !d_indices) || (c->F && batch && !d_dense) || nnz < 0)
+    return c->fail(CVR_E_ARG, "null pointer or negative nnz");
+  cudaStream_t se = (cudaStream_t)s_embed, sd = (cudaStream_t)s_dense;
+  const int slot = (int)(c->k & 1);
+  cudaError_t e = cudaSuccess;
+  if (c->k >= 2) e = cudaStreamWaitEvent(se, c->ev_dense[slot], 0);  // dense(k-2) released the slot
+  if (e != cudaSuccess) return c->cuda_fail(e, "wait dense(k-2)");
+  void* x0 = c->ws + c->off_x0[slot];
+  st = do_embed(c, d_indices, d_offsets, nnz, batch, d_dense, x0, se);
+  if (st) return st;
+  if ((e = cudaEventRecord(c->ev_embed[slot], se)) != cudaSuccess) return c->cuda_fail(e, "record embed");
+  if ((e = cudaStreamWaitEvent(sd, c->ev_embed[slot], 0)) != cudaSuccess) return c->cuda_fail(e, "wait embed");
+  if (batch > 0) {
+    st = do_dense(c, x0, c->backbone == CVR_DCN_LOWRANK ? &c->tm_x0slot[slot] : nullptr, batch, d_scores, sd);
+    if (st) return st;
+  }
+  if ((e = cudaEventRecord(c->ev_dense[slot], sd)) != cudaSuccess) return c->cuda_fail(e, "record dense");
+  c->k++;
+  return CVR_OK;
+}
+
+int cvr_score_host(cvr_ctx* c, const int32_t* h_indices, const int32_t* h_offsets, int64_t nnz, int batch,
+                   const float* h_dense, float* h_scores, cvr_stream_t s_copy, cvr_stream_t s_embed,
+                   cvr_stream_t s_dense) {
+  if (!c) return CVR_E_ARG;
+  int st = check_ready(c, true, true);
+  if (st) return st;
+  if (c->world != 1) return c->fail(CVR_E_STATE, "cvr_score_host is unsharded");
+  if (batch < 0 || batch > c->max_batch) return c->fail(CVR_E_ARG, "batch %d outside [0, %d]", batch, c->max_batch);
+  if (nnz < 0 || nnz > c->max_nnz) return c->fail(CVR_E_ARG, "nnz %lld outside [0, max_nnz=%lld]", (long long)nnz, (long long)c->max_nnz);
+  if (!h_offsets || !h_scores || (nnz > 0 && !h_indices) || (c->F && batch && !h_dense))
+    return c->fail(CVR_E_ARG, "null pointer");
+  cudaStream_t sc = (cudaStream_t)s_copy, sd = (cudaStream_t)s_dense;
+  const int slot = (int)(c->k & 1);
+  cudaError_t e = cudaSuccess;
+  if (c->k >= 2 && (e = cudaStreamWaitEvent(sc, c->ev_embed[slot], 0)) != cudaSuccess)  // embed(k-2) read staging
+    return c->cuda_fail(e, "wait embed(k-2)");
+  int32_t* di = c->at<int32_t>(c->off_idx[slot]);
+  int32_t* doff = c->at<int32_t>(c->off_offs[slot]);
+  float* dd = c->at<float>(c->off_dense[slot]);
+  float* ds = c->at<float>(c->off_scores[slot]);
+  const size_t nb = (size_t)c->local_tables.size() * batch + 1;
+  if (nnz && (e = cudaMemcpyAsync(di, h_indices, (size_t)nnz * 4, cudaMemcpyHostToDevice, sc)) != cudaSuccess)
+    return c->cuda_fail(e, "H2D indices");
+  if ((e = cudaMemcpyAsync(doff, h_offsets, nb * 4, cudaMemcpyHostToDevice, sc)) != cudaSuccess)
+    return c->cuda_fail(e, "H2D offsets");
+  if (c->F && batch && (e = cudaMemcpyAsync(dd, h_dense, (size_t)batch * c->F * 4, cudaMemcpyHostToDevice, sc)) != cudaSuccess)
+    return c->cuda_fail(e, "H2D dense");
+  if ((e = cudaEventRecord(c->ev_copy[slot], sc)) != cudaSuccess) return c->cuda_fail(e, "record copy");
+  if ((e = cudaStreamWaitEvent((cudaStream_t)s_embed, c->ev_copy[slot], 0)) != cudaSuccess) return c->cuda_fail(e, "wait copy");
+  st = cvr_score(c, di, doff, nnz, batch, dd, ds, s_embed, s_dense);
+  if (st) return st;
+  if (batch && (e = cudaMemcpyAsync(h_scores, ds, (size_t)batch * 4, cudaMemcpyDeviceToHost, sd)) != cudaSuccess)
+    return c->cuda_fail(e, "D2H scores");
+  return CVR_OK;
+}
+
+int cvr_get_status(cvr_ctx* c, cvr_stream_t stream) {
+  if (!c) return CVR_E_ARG;
+  if (!c->cuda_ready) return c->fail(CVR_E_STATE, "workspace not set");
+  cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return c->cuda_fail(e, "asynchronous CUDA error");
+  int flag = 0;
+  e = cudaMemcpy(&flag, c->ws + c->off_flag, 4, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && flag) e = cudaMemset(c->ws + c->off_flag, 0, 4);
+  if (e != cudaSuccess) return c->cuda_fail(e, "read status flag");
+  if (flag) return c->fail(CVR_E_INDEX, "device saw an out-of-range index or malformed offsets (bag zeroed)");
+  return CVR_OK;
+}
+
+int cvr_shard_buffer_bytes(const cvr_ctx* c, int batch_global, size_t* send_bytes, size_t* recv_bytes) {
+  if (!c || !send_bytes || !recv_bytes || batch_global < 0) return CVR_E_ARG;
+  const size_t b = (size_t)batch_global * c->T_pad * c->d * elt_size(c->act);
+  *send_bytes = b;
+  *recv_bytes = b;
+  return CVR_OK;
+}
+
+int cvr_embed_shard(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, int64_t nnz, int batch_global,
+                    const float* d_dense, void* d_send, void* d_x0, cvr_stream_t stream) {
+  if (!c) return CVR_E_ARG;
+  int st = check_ready(c, true, false);
+  if (st) return st;
+  if (batch_global < 0 || batch_global % c->world || batch_global / c->world > c->max_batch)
+    return c->fail(CVR_E_ARG, "batch_global %d must be a multiple of world %d with B/N <= max_batch %d", batch_global,
+                   c->world, c->max_batch);
+  if (!d_offsets || !d_send || !d_x0 || (nnz > 0 && !d_indices) || (c->F && batch_global && !d_dense) || nnz < 0)
+    return c->fail(CVR_E_ARG, "null pointer or negative nnz");
+  if (c->F && !c->slot("norm/mean")->loaded) return c->fail(CVR_E_STATE, "norm/mean,std not loaded");
+  EmbedArgs a = embed_args(c, d_indices, d_offsets, nnz, batch_global, d_dense, d_send, (int64_t)c->T_pad * c->d, d_x0,
+                           batch_global / c->world);
+  cudaError_t e = launch_embed(a, c->num_sms, (cudaStream_t)stream);
+  if (e != cudaSuccess) return c->cuda_fail(e, "embed_shard launch");
+  return CVR_OK;
+}
+
+int cvr_unpack_shard(cvr_ctx* c, const void* d_recv, int batch_global, void* d_x0, cvr_stream_t stream) {
+  if (!c) return CVR_E_ARG;
+  if (!c->cuda_ready) return c->fail(CVR_E_STATE, "workspace not set");
+  if (!d_recv || !d_x0 || batch_global < 0 || batch_global % c->world) return c->fail(CVR_E_ARG, "bad arguments");
+  cudaError_t e = launch_unpack(d_recv, d_x0, c->x0_ld, c->world, batch_global / c->world, c->T_pad, c->T, c->d, c->act,
+                                (cudaStream_t)stream);
+  if (e != cudaSuccess) return c->cuda_fail(e, "unpack launch");
+  return CVR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// cvr_kernels.cuh -- internal launchers of the hot-path kernels (not part of the C ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace cvr {
+
+enum DType { F32 = 0, BF16 = 1, F16 = 2 };
+
+struct TableDesc {
+  const uint8_t* base;  // row 0
+  int64_t stride;       // bytes between rows
+  int64_t rows;
+};
+
+// ---- K1 + K2: embedding-bag sum-pool (+ dense normalisation) --------------------------------
+struct EmbedArgs {
+  const TableDesc* tables;   // device array [T_local]
+  const int32_t* indices;
+  const int32_t* offsets;    // [T_local * B + 1]
+  int64_t nnz;
+  int B;                     // bags per table (global batch in sharded mode)
+  int T;                     // tables handled (T_local)
+  int d;
+  int emb_dtype, out_dtype;
+  void* out;                 // pooled output base
+  int64_t out_ld;            // elements between consecutive b
+  int64_t out_tstride;       // elements between consecutive tables (column offset t*out_tstride)
+  // dense normalisation (S3); skipped when F == 0 or dense == nullptr
+  const float* dense;        // [Bd, F]
+  int Bd;                    // rows of dense
+  int F;
+  const float* mean;         // [F]
+  const float* sigma;        // [F] (floored at 1e-8 at load)
+  void* x0;                  // x0 base for dense columns
+  int64_t x0_ld;
+  int64_t dense_col0;        // first dense column (T_total * d)
+  int64_t pad_col0, pad_col1;  // zero columns [pad_col0, pad_col1) of x0 rows
+  int* flag;                 // sticky error flag
+};
+cudaError_t launch_embed(const EmbedArgs& a, int num_sms, cudaStream_t s);
+
+// unpack received shard chunks [src][b_local][t_slot][d] into canonical x0 columns
+cudaError_t launch_unpack(const void* recv, void* x0, int64_t x0_ld, int N, int Bl, int Tpad, int T, int d,
+                          int dtype, cudaStream_t s);
+
+// ---- K3: fp32 fused DCN-full forward (config 1) ------------------------------------------------
+constexpr int kMaxLayers = 8;
+struct DenseF32Args {
+  const float* x0;
+  int64_t x0_ld;
+  int B, W;
+  int n_cross;
+  const float* WT[kMaxLayers];    // W_l^T [W][W] (in-major, repacked at load)
+  const float* bias[kMaxLayers];  // b_l [W]
+  int n_mlp;
+  int dims[kMaxLayers + 1];       // W, h_1, ..., h_n
+  const float* MT[kMaxLayers];    // M_i^T [in][out]
+  const float* mb[kMaxLayers];    // c_i [out]
+  const float* head_w;            // [h_n]
+  const float* head_b;            // [1]
+  float* scores;
+};
+cudaError_t launch_dense_f32(const DenseF32Args& a, cudaStream_t s);
+
+// ---- K4: tcgen05 bf16 GEMM with fused epilogues --------------------------------------------------
+enum Epi { EPI_STORE = 0, EPI_BIAS_RELU = 1, EPI_CROSS = 2, EPI_HEAD = 3 };
+
+struct EpiParams {
+  void* out;              // bf16 [M, ldo]  (EPI_STORE / BIAS_RELU / CROSS)
+  int64_t ldo;
+  const float* bias;      // fp32 [N]
+  const __nv_bfloat16* x0;  // EPI_CROSS
+  int64_t ld_x0;
+  const __nv_bfloat16* xl;  // EPI_CROSS
+  int64_t ld_xl;
+  const float* head_w;    // EPI_HEAD fp32 [N]
+  float head_b;
+  float* scores;          // EPI_HEAD fp32 [M]
+};
+
+// C[M, N] = epi(A[M, K] . B[N, K]^T); A, B bf16 K-major with tensor maps (box 64 x 128 / 64 x BN,
+// SWIZZLE_128B).  K % 64 == 0, N % BN == 0, BN in {64, 128, 256}; EPI_HEAD needs BN == N.
+cudaError_t launch_gemm_bf16(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K, int BN, Epi epi,
+                             const EpiParams& p, cudaStream_t s);
+
+// host: encode a 2-D bf16 K-major tensor map [rows, cols] (row stride ld elements) with box
+// {64, box_rows} and 128-byte swizzle.
+int encode_tmap_bf16(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                     const char** err);
+
+}  // namespace cvr

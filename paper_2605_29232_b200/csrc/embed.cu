@@ -1,0 +1,225 @@
+// embed.cu -- K1 embedding-bag gather + sum-pool, K2 dense normalisation + concat, and the
+// sharded-mode unpack.
+//
+// S2 (§2.1; BASELINE.json north star (a)):
+//     p[b, t, :] = sum_{j = off[t*B+b]}^{off[t*B+b+1]-1} E_t[idx[j], :]
+// fp32 accumulation in index order, stored in the x0 dtype.  HBM-bound gather, no tensor
+// cores: a group of LPR = d*sizeof(row elt)/16 lanes owns one bag, each lane owns 16 bytes of
+// the row (one 128-bit ld.global.nc per row), and UNROLL rows of the bag are loaded before any
+// is accumulated so >= UNROLL independent 16-B loads per lane are in flight.  Consecutive
+// groups take consecutive bags of the same table (table-major CSR), so Zipf-hot rows of a
+// table are re-read from L2 by neighbouring warps.
+//
+// S3 ("normal standardization"): x0[b, T*d + f] = (x[b,f] - mu_f) / sigma_f,
+// computed in fp32 with a correctly rounded division, by extra CTAs of the same grid.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "cvr_kernels.cuh"
+#include "cvr_ptx.cuh"
+
+namespace cvr {
+namespace {
+
+template <typename T>
+struct InTraits;
+template <>
+struct InTraits<float> {
+  static constexpr int EPL = 4;
+  __device__ static void add(float* acc, const uint4& v) {
+    acc[0] += __uint_as_float(v.x);
+    acc[1] += __uint_as_float(v.y);
+    acc[2] += __uint_as_float(v.z);
+    acc[3] += __uint_as_float(v.w);
+  }
+};
+template <>
+struct InTraits<__nv_bfloat16> {
+  static constexpr int EPL = 8;
+  __device__ static void add(float* acc, const uint4& v) {
+    acc[0] += ptx::bf16_lo(v.x);
+    acc[1] += ptx::bf16_hi(v.x);
+    acc[2] += ptx::bf16_lo(v.y);
+    acc[3] += ptx::bf16_hi(v.y);
+    acc[4] += ptx::bf16_lo(v.z);
+    acc[5] += ptx::bf16_hi(v.z);
+    acc[6] += ptx::bf16_lo(v.w);
+    acc[7] += ptx::bf16_hi(v.w);
+  }
+};
+template <>
+struct InTraits<__half> {
+  static constexpr int EPL = 8;
+  __device__ static void add(float* acc, const uint4& v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+      acc[2 * i] += f.x;
+      acc[2 * i + 1] += f.y;
+    }
+  }
+};
+
+template <int EPL>
+__device__ __forceinline__ void store_out(float* dst, const float* acc) {
+#pragma unroll
+  for (int i = 0; i < EPL; i += 4)
+    *reinterpret_cast<float4*>(dst + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+}
+template <int EPL>
+__device__ __forceinline__ void store_out(__nv_bfloat16* dst, const float* acc) {
+  if constexpr (EPL == 8) {
+    uint4 v = make_uint4(ptx::pack_bf16(acc[0], acc[1]), ptx::pack_bf16(acc[2], acc[3]),
+                         ptx::pack_bf16(acc[4], acc[5]), ptx::pack_bf16(acc[6], acc[7]));
+    *reinterpret_cast<uint4*>(dst) = v;
+  } else {
+    uint2 v = make_uint2(ptx::pack_bf16(acc[0], acc[1]), ptx::pack_bf16(acc[2], acc[3]));
+    *reinterpret_cast<uint2*>(dst) = v;
+  }
+}
+
+__device__ __forceinline__ void store_scalar(float* p, float v) { *p = v; }
+__device__ __forceinline__ void store_scalar(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+
+template <typename TOut>
+__device__ void dense_part(const EmbedArgs& a, int blk, int nblk) {
+  const int64_t ncols = a.pad_col1 - a.dense_col0;
+  const int64_t total = (int64_t)a.Bd * ncols;
+  TOut* x0 = reinterpret_cast<TOut*>(a.x0);
+  for (int64_t i = (int64_t)blk * blockDim.x + threadIdx.x; i < total; i += (int64_t)nblk * blockDim.x) {
+    const int64_t r = i / ncols;
+    const int c = (int)(i - r * ncols);
+    float v = 0.f;
+    if (c < a.F) v = __fdiv_rn(__ldg(a.dense + r * a.F + c) - __ldg(a.mean + c), __ldg(a.sigma + c));
+    store_scalar(x0 + r * a.x0_ld + a.dense_col0 + c, v);
+  }
+}
+
+template <typename TIn, typename TOut, int LPR, int UNROLL>
+__global__ void __launch_bounds__(256) embed_bag_kernel(const EmbedArgs a, int n_embed_blocks) {
+  if ((int)blockIdx.x >= n_embed_blocks) {
+    dense_part<TOut>(a, blockIdx.x - n_embed_blocks, gridDim.x - n_embed_blocks);
+    return;
+  }
+  constexpr int EPL = InTraits<TIn>::EPL;
+  const int sub = threadIdx.x & (LPR - 1);
+  const int64_t n_bags = (int64_t)a.T * a.B;
+  const int64_t stride = (int64_t)n_embed_blocks * blockDim.x / LPR;
+  for (int64_t bag = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPR; bag < n_bags; bag += stride) {
+    const int t = (int)(bag / a.B);
+    const int b = (int)(bag - (int64_t)t * a.B);
+    const int64_t start = __ldg(a.offsets + bag);
+    const int64_t end = __ldg(a.offsets + bag + 1);
+    const TableDesc td = a.tables[t];
+    float acc[EPL];
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
+    bool bad = start < 0 || end < start || end > a.nnz;
+    if (!bad) {
+      const uint8_t* colbase = td.base + sub * 16;
+      for (int64_t j = start; j < end; j += UNROLL) {
+        int idx[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+          const bool live = j + u < end;
+          idx[u] = live ? __ldg(a.indices + j + u) : 0;
+          bad |= live && (idx[u] < 0 || (int64_t)idx[u] >= td.rows);
+        }
+        if (bad) break;  // uniform within the group: every lane read the same indices
+        uint4 v[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+          if (j + u < end) v[u] = ptx::ld_nc_v4(colbase + (int64_t)idx[u] * td.stride);
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+          if (j + u < end) InTraits<TIn>::add(acc, v[u]);
+      }
+    }
+    if (bad) {
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
+      if (sub == 0) atomicOr(a.flag, 1);
+    }
+    TOut* dst = reinterpret_cast<TOut*>(a.out) + (int64_t)b * a.out_ld + (int64_t)t * a.out_tstride + sub * EPL;
+    store_out<EPL>(dst, acc);
+  }
+}
+
+template <typename TIn, typename TOut, int LPR>
+cudaError_t launch_t(const EmbedArgs& a, int num_sms, cudaStream_t s) {
+  const int threads = 256;
+  const int64_t n_bags = (int64_t)a.T * a.B;
+  int64_t nbE = (n_bags * LPR + threads - 1) / threads;
+  const int64_t capE = (int64_t)num_sms * 8;
+  if (nbE > capE) nbE = capE;
+  int64_t nbD = 0;
+  if (a.x0 && a.Bd > 0 && a.pad_col1 > a.dense_col0) {
+    const int64_t total = (int64_t)a.Bd * (a.pad_col1 - a.dense_col0);
+    nbD = (total + threads - 1) / threads;
+    if (nbD > num_sms) nbD = num_sms;
+  }
+  if (nbE + nbD == 0) return cudaSuccess;
+  embed_bag_kernel<TIn, TOut, LPR, 4><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
+  return cudaGetLastError();
+}
+
+template <typename TIn, typename TOut>
+cudaError_t launch_lpr(const EmbedArgs& a, int num_sms, cudaStream_t s) {
+  const int elt = a.emb_dtype == F32 ? 4 : 2;
+  switch (a.d * elt / 16) {
+    case 2: return launch_t<TIn, TOut, 2>(a, num_sms, s);
+    case 4: return launch_t<TIn, TOut, 4>(a, num_sms, s);
+    case 8: return launch_t<TIn, TOut, 8>(a, num_sms, s);
+    case 16: return launch_t<TIn, TOut, 16>(a, num_sms, s);
+    case 32: return launch_t<TIn, TOut, 32>(a, num_sms, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+__global__ void unpack_kernel(const uint4* __restrict__ recv, uint8_t* __restrict__ x0, int64_t x0_ld_bytes, int N,
+                              int Bl, int Tpad, int T, int chunks_per_row, int row_bytes) {
+  const int64_t total = (int64_t)N * Bl * Tpad * chunks_per_row;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t q = i;
+    const int c = (int)(q % chunks_per_row);
+    q /= chunks_per_row;
+    const int slot = (int)(q % Tpad);
+    q /= Tpad;
+    const int b = (int)(q % Bl);
+    const int src = (int)(q / Bl);
+    const int t = slot * N + src;  // round-robin table placement, t -> rank t % N, slot t / N
+    if (t >= T) continue;
+    *reinterpret_cast<uint4*>(x0 + (int64_t)b * x0_ld_bytes + (int64_t)t * row_bytes + c * 16) = recv[i];
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_embed(const EmbedArgs& a, int num_sms, cudaStream_t s) {
+  if (a.emb_dtype == F32 && a.out_dtype == F32) return launch_lpr<float, float>(a, num_sms, s);
+  if (a.emb_dtype == F32 && a.out_dtype == BF16) return launch_lpr<float, __nv_bfloat16>(a, num_sms, s);
+  if (a.emb_dtype == BF16 && a.out_dtype == BF16) return launch_lpr<__nv_bfloat16, __nv_bfloat16>(a, num_sms, s);
+  if (a.emb_dtype == BF16 && a.out_dtype == F32) return launch_lpr<__nv_bfloat16, float>(a, num_sms, s);
+  if (a.emb_dtype == F16 && a.out_dtype == BF16) return launch_lpr<__half, __nv_bfloat16>(a, num_sms, s);
+  if (a.emb_dtype == F16 && a.out_dtype == F32) return launch_lpr<__half, float>(a, num_sms, s);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_unpack(const void* recv, void* x0, int64_t x0_ld, int N, int Bl, int Tpad, int T, int d,
+                          int dtype, cudaStream_t s) {
+  const int elt = dtype == F32 ? 4 : 2;
+  const int row_bytes = d * elt;
+  if (row_bytes % 16) return cudaErrorInvalidValue;
+  const int cpr = row_bytes / 16;
+  const int64_t total = (int64_t)N * Bl * Tpad * cpr;
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  unpack_kernel<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<const uint4*>(recv),
+                                                   reinterpret_cast<uint8_t*>(x0), x0_ld * elt, N, Bl, Tpad, T, cpr,
+                                                   row_bytes);
+  return cudaGetLastError();
+}
+
+}  // namespace cvr

@@ -1,0 +1,44 @@
+"""Shared test plumbing: build a CvrModel from a cvr_synth config, slice batches (CSR index
+arithmetic only), and the tolerances of BASELINE.json's north star."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import cvr_synth as cs
+
+TOL_F32 = 1e-5   # BASELINE.json north star: fp32 path, absolute on scores
+TOL_BF16 = 2e-3  # BASELINE.json north star: bf16 path, absolute on the sigmoid output
+
+
+def sub_batch(bt: cs.Batch, sel) -> cs.Batch:
+    """The examples ``sel`` of ``bt`` as their own batch (same bags, same order)."""
+    sel = np.asarray(sel)
+    T, B = bt.n_tables, bt.batch
+    idx, off = [], [0]
+    for t in range(T):
+        for b in sel:
+            seg = bt.indices[bt.offsets[t * B + b]:bt.offsets[t * B + b + 1]]
+            idx.append(seg)
+            off.append(off[-1] + len(seg))
+    idx = np.concatenate(idx) if idx else np.zeros(0, np.int32)
+    return cs.Batch(len(sel), T, idx.astype(np.int32), np.array(off, np.int32), bt.dense[sel])
+
+
+def device_tables(cfg, device="cuda"):
+    return [spec.materialize(device=device) for spec in cs.table_specs(cfg)]
+
+
+def to_dev(bt: cs.Batch, device="cuda"):
+    return (torch.from_numpy(bt.indices).to(device), torch.from_numpy(bt.offsets).to(device),
+            torch.from_numpy(bt.dense).to(device))
+
+
+def make_model(cfg, max_batch, max_nnz=0, tables=None, weights=None, device="cuda"):
+    from paper_2605_29232_b200 import CvrModel
+    m = CvrModel(cfg, max_batch=max_batch, max_nnz=max_nnz, device=device)
+    tables = device_tables(cfg, device) if tables is None else tables
+    m.load_tables(tables)
+    w = cs.make_weights(cfg) if weights is None else weights
+    m.load_weights({k: v.to(device) for k, v in w.items()})
+    return m, tables, w

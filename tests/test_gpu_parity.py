@@ -1,0 +1,177 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded
+inputs.  Tolerances are BASELINE.json's north star: 1e-5 absolute on config-1 (fp32) scores,
+2e-3 absolute on bf16-path sigmoid outputs; indices/offsets and single-hot bags bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+import cvr_synth as cs
+import oracle as O
+from helpers import TOL_BF16, TOL_F32, device_tables, make_model, sub_batch, to_dev
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU hosts too; skipped there
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    from paper_2605_29232_b200 import build
+    build.build()
+
+
+# ------------------------------------------------------------------------------ config 1
+@pytest.fixture(scope="module")
+def c1():
+    cfg = cs.C1
+    m, tabs, w = make_model(cfg, max_batch=512, max_nnz=1 << 16)
+    return cfg, m, tabs, w
+
+
+@pytest.mark.parametrize("B", [256, 77, 1, 512])
+def test_c1_scores_vs_oracle(c1, B):
+    cfg, m, tabs, w = c1
+    bt = cs.make_batch(cfg, 11, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    scores = m.dense(x0, B)
+    assert m.status() == 0
+    ref = O.score_forward(cfg, cs.table_specs(cfg), w, bt)
+    np.testing.assert_allclose(x0[:, :cfg.width].double().cpu().numpy(), ref["x0"], rtol=0, atol=2e-6)
+    assert torch.all(x0[:, cfg.width:] == 0)
+    err = np.abs(scores.double().cpu().numpy() - ref["scores"]).max()
+    assert err <= TOL_F32, err
+
+
+def test_c1_single_hot_bitexact_and_empty_bags(c1):
+    cfg, m, tabs, w = c1
+    B, T = 64, cfg.n_tables
+    rng = np.random.default_rng(3)
+    L = rng.integers(0, 2, size=(T, B))          # empty and single-hot bags
+    off = np.concatenate([[0], np.cumsum(L.ravel())]).astype(np.int32)
+    idx = rng.integers(0, 1000, off[-1]).astype(np.int32)
+    dense = rng.random((B, cfg.n_dense), dtype=np.float32)
+    x0 = m.embed(torch.from_numpy(idx).cuda(), torch.from_numpy(off).cuda(), B, torch.from_numpy(dense).cuda())
+    assert m.status() == 0
+    x0 = x0.cpu()
+    for t in range(T):
+        for b in range(B):
+            seg = idx[off[t * B + b]:off[t * B + b + 1]]
+            got = x0[b, t * 16:(t + 1) * 16]
+            want = tabs[t][int(seg[0])].cpu() if len(seg) else torch.zeros(16)
+            assert torch.equal(got, want)
+
+
+def test_c1_bad_index_sets_status_and_zeroes_bag(c1):
+    cfg, m, tabs, w = c1
+    bt = cs.make_batch(cfg, 1, batch=8)
+    bad = bt.indices.copy()
+    bad[0] = 1000                                # == rows: out of range
+    x0 = m.embed(torch.from_numpy(bad).cuda(), torch.from_numpy(bt.offsets).cuda(), 8, torch.from_numpy(bt.dense).cuda())
+    assert m.status() == 5                        # CVR_E_INDEX
+    assert torch.all(x0[0, :16] == 0)
+    assert m.status() == 0                        # sticky flag cleared by the read
+    off = bt.offsets.copy()
+    off[3] = off[4] + 1                          # non-monotone offsets
+    m.embed(torch.from_numpy(bt.indices).cuda(), torch.from_numpy(off).cuda(), 8, torch.from_numpy(bt.dense).cuda())
+    assert m.status() == 5
+
+
+# ------------------------------------------------------------------------------ config 2
+@pytest.fixture(scope="module")
+def c2():
+    cfg = cs.C2
+    m, tabs, w = make_model(cfg, max_batch=4096, max_nnz=1 << 20)
+    return cfg, m, tabs, w
+
+
+@pytest.mark.parametrize("B", [300, 128, 1, 4096])
+def test_c2_scores_vs_oracle(c2, B):
+    """B=300: three 128-row tiles with a ragged tail; B=4096: config 2's full batch, checked on a
+    sample of 384 examples (the oracle is row-independent, P9)."""
+    cfg, m, tabs, w = c2
+    bt = cs.make_batch(cfg, 5, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    scores = m.dense(x0, B)
+    assert m.status() == 0
+    sel = np.arange(B) if B <= 300 else np.random.default_rng(0).choice(B, 384, replace=False)
+    ref = O.score_forward(cfg, cs.table_specs(cfg), w, sub_batch(bt, sel))
+    x0s = x0[torch.from_numpy(sel).cuda()].double().cpu().numpy()
+    # x0 is stored bf16: |delta| <= half an ulp of bf16 (2^-9 relative) + fp32 accumulation
+    np.testing.assert_allclose(x0s, ref["x0"], rtol=2 ** -8, atol=1e-6)
+    err = np.abs(scores[torch.from_numpy(sel).cuda()].double().cpu().numpy() - ref["scores"]).max()
+    assert err <= TOL_BF16, err
+
+
+def test_c2_single_hot_bitexact(c2):
+    cfg, m, tabs, w = c2
+    B, T = 200, cfg.n_tables
+    rng = np.random.default_rng(9)
+    off = np.arange(T * B + 1, dtype=np.int32)
+    idx = np.concatenate([rng.integers(0, cfg.rows[t], B) for t in range(T)]).astype(np.int32)
+    dense = np.zeros((B, cfg.n_dense), np.float32)
+    x0 = m.embed(torch.from_numpy(idx).cuda(), torch.from_numpy(off).cuda(), B, torch.from_numpy(dense).cuda())
+    assert m.status() == 0
+    for t in (0, 7, 25):
+        rows = tabs[t][torch.from_numpy(idx[t * B:(t + 1) * B].astype(np.int64)).cuda()]
+        assert torch.equal(x0[:, t * 64:(t + 1) * 64], rows)
+
+
+def test_c2_batch_invariance(c2):
+    """P10: an item's score is bit-identical whichever batch (size, position) it lands in."""
+    cfg, m, tabs, w = c2
+    bt = cs.make_batch(cfg, 21, batch=1000)
+    idx, off, dense = to_dev(bt)
+    full = m.dense(m.embed(idx, off, 1000, dense), 1000)
+    sel = np.array([999, 0, 517, 128, 127, 3])
+    sb = sub_batch(bt, sel)
+    i2, o2, d2 = to_dev(sb)
+    part = m.dense(m.embed(i2, o2, len(sel), d2), len(sel))
+    assert torch.equal(part, full[torch.from_numpy(sel).cuda()])
+
+
+def test_c2_score_pipelined_and_host_fed_match(c2):
+    """cvr_score (two streams, double-buffered x0) and cvr_score_host (pinned host buffers)
+    give bit-identical scores to embed+dense, over several back-to-back batches."""
+    cfg, m, tabs, w = c2
+    s_e, s_d, s_c = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    batches = [cs.make_batch(cfg, 100 + i, batch=B) for i, B in enumerate([4096, 1000, 4096, 7, 2048])]
+    refs = []
+    for bt in batches:
+        idx, off, dense = to_dev(bt)
+        refs.append(m.dense(m.embed(idx, off, bt.batch, dense), bt.batch).clone())
+    torch.cuda.synchronize()
+    dev_in = [to_dev(bt) for bt in batches]
+    outs = [torch.empty(bt.batch, device="cuda") for bt in batches]
+    for (idx, off, dense), bt, o in zip(dev_in, batches, outs):
+        m.score(idx, off, bt.batch, dense, o, s_embed=s_e, s_dense=s_d)
+    s_d.synchronize()
+    for o, r in zip(outs, refs):
+        assert torch.equal(o, r)
+    host_in = [(torch.from_numpy(bt.indices).pin_memory(), torch.from_numpy(bt.offsets).pin_memory(),
+                torch.from_numpy(bt.dense).pin_memory()) for bt in batches]
+    houts = [torch.empty(bt.batch, dtype=torch.float32).pin_memory() for bt in batches]
+    for (idx, off, dense), bt, o in zip(host_in, batches, houts):
+        m.score_host(idx, off, bt.batch, dense, o, s_copy=s_c, s_embed=s_e, s_dense=s_d)
+    s_d.synchronize()
+    assert m.status(s_d) == 0
+    for o, r in zip(houts, refs):
+        assert torch.equal(o, r.cpu())
+
+
+def test_c2_zero_weights_closed_form():
+    """P4 + P7 on the GPU: U = 0 makes every cross layer x_l + x0*b; zero MLP/head weights
+    give score = sigmoid(head/b) exactly as the oracle's closed form."""
+    cfg = cs.C2.with_(rows=(1000,) * 26)
+    w = cs.make_weights(cfg)
+    for k in w:
+        if k.endswith("/U"):
+            w[k] = torch.zeros_like(w[k])
+    m, tabs, _ = make_model(cfg, max_batch=256, weights=w)
+    bt = cs.make_batch(cfg, 2, batch=256)
+    idx, off, dense = to_dev(bt)
+    s = m.dense(m.embed(idx, off, 256, dense), 256)
+    ref = O.score_forward(cfg, cs.table_specs(cfg), w, bt)
+    assert np.abs(s.double().cpu().numpy() - ref["scores"]).max() <= TOL_BF16
