@@ -309,6 +309,20 @@ class Batch:
         return int(self.offsets[-1])
 
 
+def sub_batch(bt: Batch, sel) -> Batch:
+    """Examples ``sel`` of ``bt`` as their own batch (same bags, same order): CSR slicing only."""
+    sel = np.asarray(sel)
+    T, B = bt.n_tables, bt.batch
+    idx, off = [], [0]
+    for t in range(T):
+        for b in sel:
+            seg = bt.indices[bt.offsets[t * B + b]:bt.offsets[t * B + b + 1]]
+            idx.append(seg)
+            off.append(off[-1] + len(seg))
+    idx = np.concatenate(idx) if idx else np.zeros(0, np.int32)
+    return Batch(len(sel), T, idx.astype(np.int32), np.array(off, np.int32), bt.dense[sel])
+
+
 def bag_lengths(cfg: CvrConfig, k: int, batch: Optional[int] = None) -> np.ndarray:
     B = cfg.batch if batch is None else batch
     rng = _rng(cfg, STREAM_LENGTHS, k)

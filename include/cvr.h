@@ -185,6 +185,36 @@ int cvr_embed_shard(cvr_ctx* ctx, const int32_t* d_indices, const int32_t* d_off
  * the caller's communicator (NCCL over NVLink via torch.distributed) or cvr_exchange. */
 int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d_x0, cvr_stream_t stream);
 
+/* Options (defaults in brackets): "graphs" [1] replay the executor stages of cvr_score /
+ * cvr_score_host as cached CUDA graphs (keyed by their pointer / size arguments; captured on first
+ * use; 32 entries, LRU); "pdl" [1] launch dependent GEMMs with programmatic stream serialization. */
+int cvr_set_option(cvr_ctx* ctx, const char* key, int64_t value);
+
+/* -- utility ----------------------------------------------------------------------------------
+ * C[M, N] = A[M, K] . B[N, K]^T on the same tcgen05/TMA kernel the dense stage uses (tests and
+ * tile tuning): bf16 row-major operands with leading dimensions lda/ldb/ldc (elements, multiples
+ * of 8), fp32 accumulation, bf16 output; epi 0 = plain store, 1 = ReLU(C + bias[N]) (fp32 bias).
+ * K % 64 == 0, N % bn == 0, bn in {64, 128}.  Enqueued on `stream`. */
+int cvr_gemm_bf16(const void* d_A, int64_t lda, const void* d_B, int64_t ldb, void* d_C, int64_t ldc, int M, int N,
+                  int K, int epi, const float* d_bias, int bn, cvr_stream_t stream);
+
+/* -- accounting / measurement -------------------------------------------------------------- */
+/* Number of kernels this ctx has launched since creation (every entry point counts its launches). */
+int cvr_launch_count(const cvr_ctx* ctx, int64_t* n);
+
+typedef struct {
+  char name[32];     /* kernel role: embed_bag_pool, gemm_xV, gemm_tU_cross, gemm_mlp_relu, ... */
+  int64_t launches;
+  double total_ms;   /* sum of CUDA-event durations measured on the launching stream */
+  double min_ms, max_ms;
+} cvr_kernel_stat;
+
+/* Record a CUDA event pair around each of the next max_launches kernel launches (on the stream
+ * the kernel is launched on).  cvr_profile_end synchronises on those events, aggregates them per
+ * kernel role into out[0 .. min(*n_out, max_out)) and stops recording. */
+int cvr_profile_begin(cvr_ctx* ctx, int max_launches);
+int cvr_profile_end(cvr_ctx* ctx, cvr_kernel_stat* out, int max_out, int* n_out);
+
 #ifdef __cplusplus
 }
 #endif

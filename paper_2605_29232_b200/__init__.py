@@ -8,7 +8,7 @@ There is no CPU fallback: if the extension is missing or no CUDA device is prese
 raise.
 """
 from ._cvr import (  # noqa: F401
-    CVR_BF16, CVR_DCN_FULL, CVR_DCN_LOWRANK, CVR_ENSEMBLE, CVR_F16, CVR_F32, CvrError, CvrModel, lib, lib_path,
+    CVR_BF16, CVR_DCN_FULL, CVR_DCN_LOWRANK, CVR_ENSEMBLE, CVR_F16, CVR_F32, CvrError, CvrModel, gemm_bf16, lib, lib_path,
     status_string,
 )
 

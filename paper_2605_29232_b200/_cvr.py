@@ -34,6 +34,11 @@ class cvr_model_desc(ctypes.Structure):
     ]
 
 
+class cvr_kernel_stat(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_int64), ("total_ms", ctypes.c_double),
+                ("min_ms", ctypes.c_double), ("max_ms", ctypes.c_double)]
+
+
 # (name, restype, argtypes) -- mirrors include/cvr.h
 _SIGS = [
     ("cvr_create", ctypes.c_int, [ctypes.POINTER(cvr_model_desc), ctypes.POINTER(_vp)]),
@@ -56,6 +61,12 @@ _SIGS = [
                                               ctypes.POINTER(ctypes.c_size_t)]),
     ("cvr_embed_shard", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp, _vp]),
     ("cvr_unpack_shard", ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp, _vp]),
+    ("cvr_gemm_bf16", ctypes.c_int, [_vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int,
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp]),
+    ("cvr_set_option", ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int64]),
+    ("cvr_launch_count", ctypes.c_int, [_vp, _c_i64p]),
+    ("cvr_profile_begin", ctypes.c_int, [_vp, ctypes.c_int]),
+    ("cvr_profile_end", ctypes.c_int, [_vp, ctypes.POINTER(cvr_kernel_stat), ctypes.c_int, _c_ip]),
 ]
 
 _lib = None
@@ -97,6 +108,19 @@ def _stream(s) -> Optional[int]:
     if isinstance(s, torch.cuda.Stream):
         return s.cuda_stream
     return int(s)
+
+
+def gemm_bf16(A: torch.Tensor, B: torch.Tensor, C: Optional[torch.Tensor] = None, bias: Optional[torch.Tensor] = None,
+              bn: int = 64, stream=None) -> torch.Tensor:
+    """C = A @ B^T (bf16, fp32 accumulate) [+ bias, ReLU] on libcvr's tcgen05 GEMM (cvr_gemm_bf16)."""
+    M, K = A.shape
+    N = B.shape[0]
+    C = torch.empty(M, N, dtype=torch.bfloat16, device=A.device) if C is None else C
+    st = lib().cvr_gemm_bf16(A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), C.data_ptr(), C.stride(0), M, N, K,
+                             0 if bias is None else 1, _ptr(bias), bn, _stream(stream))
+    if st != 0:
+        raise CvrError(st, "cvr_gemm_bf16")
+    return C
 
 
 class CvrModel:
@@ -227,3 +251,38 @@ class CvrModel:
 
     def unpack_shard(self, recv, batch_global, x0, stream=None):
         self._check(self.L.cvr_unpack_shard(self.h, _ptr(recv), batch_global, _ptr(x0), _stream(stream)))
+
+    def set_option(self, key: str, value: int):
+        self._check(self.L.cvr_set_option(self.h, key.encode(), int(value)))
+
+    def score_raw(self, idx_ptr: int, off_ptr: int, nnz: int, batch: int, dense_ptr: int, scores_ptr: int,
+                  s_embed: int, s_dense: int):
+        """cvr_score with pre-extracted pointers / stream handles (lowest host overhead)."""
+        st = self.L.cvr_score(self.h, idx_ptr, off_ptr, nnz, batch, dense_ptr, scores_ptr, s_embed, s_dense)
+        if st:
+            self._check(st)
+
+    def score_host_raw(self, idx_ptr: int, off_ptr: int, nnz: int, batch: int, dense_ptr: int, scores_ptr: int,
+                       s_copy: int, s_embed: int, s_dense: int):
+        st = self.L.cvr_score_host(self.h, idx_ptr, off_ptr, nnz, batch, dense_ptr, scores_ptr, s_copy, s_embed,
+                                   s_dense)
+        if st:
+            self._check(st)
+
+    # -- accounting ----------------------------------------------------------------------------
+    def launch_count(self) -> int:
+        n = ctypes.c_int64()
+        self._check(self.L.cvr_launch_count(self.h, ctypes.byref(n)))
+        return n.value
+
+    def profile_begin(self, max_launches: int):
+        self._check(self.L.cvr_profile_begin(self.h, max_launches))
+
+    def profile_end(self) -> Dict[str, dict]:
+        buf = (cvr_kernel_stat * 16)()
+        n = ctypes.c_int()
+        self._check(self.L.cvr_profile_end(self.h, buf, 16, ctypes.byref(n)))
+        return {buf[i].name.decode(): {"launches": buf[i].launches, "total_ms": buf[i].total_ms,
+                                        "avg_ms": buf[i].total_ms / max(1, buf[i].launches),
+                                        "min_ms": buf[i].min_ms, "max_ms": buf[i].max_ms}
+                for i in range(min(n.value, 16))}

@@ -20,6 +20,10 @@
 
 using namespace cvr;
 
+enum KernelId { K_EMBED = 0, K_GEMM_V, K_GEMM_U, K_GEMM_MLP, K_GEMM_HEAD, K_DENSE_F32, K_UNPACK, K_COUNT };
+static const char* kKernelNames[K_COUNT] = {"embed_bag_pool", "gemm_xV",      "gemm_tU_cross", "gemm_mlp_relu",
+                                            "gemm_mlp_head",  "dense_f32_dcn", "shard_unpack"};
+
 namespace {
 
 size_t elt_size(int dt) { return dt == CVR_F32 ? 4 : 2; }
@@ -74,12 +78,41 @@ struct cvr_ctx {
   int64_t k = 0;
   float head_b = 0.f;  // host copy of head/b (weights are loaded synchronously)
   // tensor maps for internal A operands
-  CUtensorMap tm_x0slot[2], tm_xa, tm_xb, tm_t;
+  CUtensorMap tm_x0slot[2], tm_xa, tm_xb, tm_t;   // A-operand / epilogue-input maps, box {64, 128}
   std::vector<CUtensorMap> tm_h;
+  CUtensorMap st_xa, st_xb, st_t;                 // output (TMA store) maps, box {64, 32}
+  std::vector<CUtensorMap> st_h;
+  bool pdl = true;
+  // CUDA-graph cache for the executor stages (cvr_score / cvr_score_host)
+  struct GraphEntry {
+    uint64_t key[7];
+    cudaGraphExec_t exec;
+    int64_t n_kernels;
+    uint64_t last_use;
+  };
+  std::vector<GraphEntry> graphs;
+  bool use_graphs = true;
+  uint64_t use_clock = 0;
   const void* last_x0 = nullptr;
   int last_x0_rows = -1;
   CUtensorMap tm_x0user;
   std::vector<GemmPlan> plan;  // cross layers (V, U interleaved), then MLP
+  // launch accounting + optional per-launch CUDA-event timing (cvr_profile_begin/end)
+  int64_t launches = 0;
+  bool prof_on = false;
+  size_t prof_cap = 0, prof_n = 0;
+  std::vector<cudaEvent_t> prof_ev;
+  std::vector<int> prof_kid;
+  void pbeg(cudaStream_t s) {
+    if (prof_on && prof_n < prof_cap) cudaEventRecord(prof_ev[2 * prof_n], s);
+  }
+  void pend(int kid, cudaStream_t s) {
+    ++launches;
+    if (prof_on && prof_n < prof_cap) {
+      cudaEventRecord(prof_ev[2 * prof_n + 1], s);
+      prof_kid[prof_n++] = kid;
+    }
+  }
 
   template <typename T = uint8_t>
   T* at(size_t off) const { return reinterpret_cast<T*>(ws + off); }
@@ -209,7 +242,7 @@ size_t carve(size_t& cur, size_t bytes) {
 }
 
 int pick_bn(int N) {
-  if (N % 128 == 0 && N >= 512) return 128;
+  if (N > 256 && N % 128 == 0) return 128;
   return 64;
 }
 
@@ -304,6 +337,8 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
 
 int cvr_destroy(cvr_ctx* c) {
   if (!c) return CVR_E_ARG;
+  for (auto ev : c->prof_ev) cudaEventDestroy(ev);
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   for (int i = 0; i < 2; ++i) {
     if (c->ev_embed[i]) cudaEventDestroy(c->ev_embed[i]);
     if (c->ev_dense[i]) cudaEventDestroy(c->ev_dense[i]);
@@ -358,9 +393,15 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     ok &= encode_tmap_bf16(&c->tm_xa, c->ws + c->off_xa, B, c->x0_ld, c->x0_ld, 128, &er) == 0;
     ok &= encode_tmap_bf16(&c->tm_xb, c->ws + c->off_xb, B, c->x0_ld, c->x0_ld, 128, &er) == 0;
     ok &= encode_tmap_bf16(&c->tm_t, c->ws + c->off_t, B, c->r, c->r, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&c->st_xa, c->ws + c->off_xa, B, c->x0_ld, c->x0_ld, 32, &er) == 0;
+    ok &= encode_tmap_bf16(&c->st_xb, c->ws + c->off_xb, B, c->x0_ld, c->x0_ld, 32, &er) == 0;
+    ok &= encode_tmap_bf16(&c->st_t, c->ws + c->off_t, B, c->r, c->r, 32, &er) == 0;
     c->tm_h.resize(c->off_h.size());
-    for (size_t i = 0; i < c->off_h.size(); ++i)
+    c->st_h.resize(c->off_h.size());
+    for (size_t i = 0; i < c->off_h.size(); ++i) {
       ok &= encode_tmap_bf16(&c->tm_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], 128, &er) == 0;
+      ok &= encode_tmap_bf16(&c->st_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], 32, &er) == 0;
+    }
     if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
   }
   return CVR_OK;
@@ -405,8 +446,8 @@ int encode_plan(cvr_ctx* c) {
   };
   bool ok = true;
   for (int l = 0; l < c->n_cross; ++l) {
-    ok &= addp("dcn/" + std::to_string(l) + "/V", c->r, (int)c->x0_ld, 64, EPI_STORE);
-    ok &= addp("dcn/" + std::to_string(l) + "/U", (int)c->x0_ld, c->r, 64, EPI_CROSS);
+    ok &= addp("dcn/" + std::to_string(l) + "/V", c->r, (int)c->x0_ld, pick_bn(c->r), EPI_STORE);
+    ok &= addp("dcn/" + std::to_string(l) + "/U", (int)c->x0_ld, c->r, pick_bn((int)c->x0_ld), EPI_CROSS);
   }
   int K = (int)c->x0_ld;
   for (int i = 0; i < c->n_mlp; ++i) {
@@ -556,7 +597,9 @@ int do_embed(cvr_ctx* c, const int32_t* idx, const int32_t* off, int64_t nnz, in
              cudaStream_t s) {
   if (c->F && !c->slot("norm/mean")->loaded) return c->fail(CVR_E_STATE, "norm/mean,std not loaded");
   EmbedArgs a = embed_args(c, idx, off, nnz, B, dense, x0, c->x0_ld, x0, B);
+  c->pbeg(s);
   cudaError_t e = launch_embed(a, c->num_sms, s);
+  c->pend(K_EMBED, s);
   if (e != cudaSuccess) return c->cuda_fail(e, "embed launch");
   return CVR_OK;
 }
@@ -584,55 +627,120 @@ int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, int B, float*
     a.head_w = c->wptr<float>("head/w");
     a.head_b = c->wptr<float>("head/b");
     a.scores = scores;
+    c->pbeg(s);
     e = launch_dense_f32(a, s);
+    c->pend(K_DENSE_F32, s);
     if (e != cudaSuccess) return c->cuda_fail(e, "dense_f32 launch");
     return CVR_OK;
   }
   // ---- bf16 low-rank DCN-v2 on tcgen05
-  const __nv_bfloat16* x0b = reinterpret_cast<const __nv_bfloat16*>(x0);
-  const __nv_bfloat16* xl = x0b;
   const CUtensorMap* tm_xl = tm_x0;
   size_t pi = 0;
+  auto gemm = [&](const GemmPlan& g, const CUtensorMap* A, const CUtensorMap* out, const CUtensorMap* x0m,
+                  const CUtensorMap* xlm, const float* bias, int kid) -> cudaError_t {
+    GemmArgs a{};
+    a.tmA = A;
+    a.tmB = &g.tmB;
+    a.tmOut = out;
+    a.tmX0 = x0m;
+    a.tmXl = xlm;
+    a.bias = bias;
+    a.M = B;
+    a.N = g.N;
+    a.K = g.K;
+    a.BN = g.BN;
+    a.epi = g.epi;
+    a.num_sms = c->num_sms;
+    a.pdl = c->pdl;
+    if (g.epi == EPI_HEAD) {
+      a.head_w = c->wptr<float>("head/w");
+      a.head_b = c->head_b;
+      a.scores = scores;
+    }
+    c->pbeg(s);
+    cudaError_t r = launch_gemm_bf16(a, s);
+    c->pend(kid, s);
+    return r;
+  };
   for (int l = 0; l < c->n_cross; ++l) {
     const GemmPlan& gv = c->plan[pi++];
     const GemmPlan& gu = c->plan[pi++];
-    EpiParams pv{};
-    pv.out = c->ws + c->off_t;
-    pv.ldo = c->r;
-    e = launch_gemm_bf16(tm_xl, &gv.tmB, B, gv.N, gv.K, gv.BN, gv.epi, pv, s);
+    e = gemm(gv, tm_xl, &c->st_t, nullptr, nullptr, nullptr, K_GEMM_V);
     if (e != cudaSuccess) return c->cuda_fail(e, "gemm V launch");
-    __nv_bfloat16* outb = c->at<__nv_bfloat16>(l % 2 == 0 ? c->off_xa : c->off_xb);
-    EpiParams pu{};
-    pu.out = outb;
-    pu.ldo = c->x0_ld;
-    pu.bias = c->wptr<float>("dcn/" + std::to_string(l) + "/b");
-    pu.x0 = x0b;
-    pu.ld_x0 = c->x0_ld;
-    pu.xl = xl;
-    pu.ld_xl = c->x0_ld;
-    e = launch_gemm_bf16(&c->tm_t, &gu.tmB, B, gu.N, gu.K, gu.BN, gu.epi, pu, s);
+    const bool even = l % 2 == 0;
+    e = gemm(gu, &c->tm_t, even ? &c->st_xa : &c->st_xb, tm_x0, tm_xl,
+             c->wptr<float>("dcn/" + std::to_string(l) + "/b"), K_GEMM_U);
     if (e != cudaSuccess) return c->cuda_fail(e, "gemm U launch");
-    xl = outb;
-    tm_xl = l % 2 == 0 ? &c->tm_xa : &c->tm_xb;
+    tm_xl = even ? &c->tm_xa : &c->tm_xb;
   }
   for (int i = 0; i < c->n_mlp; ++i) {
     const GemmPlan& g = c->plan[pi++];
-    EpiParams p{};
-    p.bias = c->wptr<float>("mlp/" + std::to_string(i) + "/b");
-    if (g.epi == EPI_HEAD) {
-      p.head_w = c->wptr<float>("head/w");
-      p.head_b = c->head_b;
-      p.scores = scores;
-    } else {
-      p.out = c->ws + c->off_h[i];
-      p.ldo = c->mlp[i];
-    }
-    e = launch_gemm_bf16(tm_xl, &g.tmB, B, g.N, g.K, g.BN, g.epi, p, s);
+    const bool head = g.epi == EPI_HEAD;
+    e = gemm(g, tm_xl, head ? nullptr : &c->st_h[i], nullptr, nullptr, c->wptr<float>("mlp/" + std::to_string(i) + "/b"),
+             head ? K_GEMM_HEAD : K_GEMM_MLP);
     if (e != cudaSuccess) return c->cuda_fail(e, "gemm MLP launch");
-    if (g.epi != EPI_HEAD) tm_xl = &c->tm_h[i];
+    if (!head) tm_xl = &c->tm_h[i];
   }
   return CVR_OK;
 }
+
+}  // namespace
+
+namespace {
+
+// Run one executor stage: replay a cached CUDA graph keyed by the stage's arguments, or capture one
+// (the stage's launches become graph nodes; PDL launches become programmatic edges).  Falls back to
+// direct launches on the legacy stream, while profiling, or inside a caller's own capture.
+template <typename F>
+int run_stage(cvr_ctx* c, const uint64_t (&key)[7], cudaStream_t s, F&& enqueue) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (!c->use_graphs || s == nullptr || c->prof_on || cudaStreamIsCapturing(s, &cs) != cudaSuccess ||
+      cs != cudaStreamCaptureStatusNone)
+    return enqueue(s);
+  for (auto& g : c->graphs) {
+    if (memcmp(g.key, key, sizeof g.key) == 0) {
+      g.last_use = ++c->use_clock;
+      cudaError_t e = cudaGraphLaunch(g.exec, s);
+      if (e != cudaSuccess) return c->cuda_fail(e, "cudaGraphLaunch");
+      c->launches += g.n_kernels;
+      return CVR_OK;
+    }
+  }
+  const int64_t l0 = c->launches;
+  cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return c->cuda_fail(e, "cudaStreamBeginCapture");
+  int st = enqueue(s);
+  cudaGraph_t graph = nullptr;
+  e = cudaStreamEndCapture(s, &graph);
+  const int64_t nk = c->launches - l0;
+  c->launches = l0;
+  if (st != CVR_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (e != cudaSuccess) return c->cuda_fail(e, "cudaStreamEndCapture");
+  cvr_ctx::GraphEntry ge;
+  memcpy(ge.key, key, sizeof ge.key);
+  e = cudaGraphInstantiate(&ge.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return c->cuda_fail(e, "cudaGraphInstantiate");
+  ge.n_kernels = nk;
+  ge.last_use = ++c->use_clock;
+  if (c->graphs.size() >= 32) {  // evict the least recently used
+    size_t lru = 0;
+    for (size_t i = 1; i < c->graphs.size(); ++i)
+      if (c->graphs[i].last_use < c->graphs[lru].last_use) lru = i;
+    cudaGraphExecDestroy(c->graphs[lru].exec);
+    c->graphs.erase(c->graphs.begin() + lru);
+  }
+  c->graphs.push_back(ge);
+  e = cudaGraphLaunch(ge.exec, s);
+  if (e != cudaSuccess) return c->cuda_fail(e, "cudaGraphLaunch");
+  c->launches += nk;
+  return CVR_OK;
+}
+
+uint64_t u64(const void* p) { return (uint64_t)(uintptr_t)p; }
 
 }  // namespace
 
@@ -647,7 +755,9 @@ int cvr_embed(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, in
   if (batch < 0 || batch > c->max_batch) return c->fail(CVR_E_ARG, "batch %d outside [0, %d]", batch, c->max_batch);
   if (!d_offsets || !d_x0 || (nnz > 0 && !d_indices) || (c->F && batch && !d_dense) || nnz < 0)
     return c->fail(CVR_E_ARG, "null pointer or negative nnz");
-  return do_embed(c, d_indices, d_offsets, nnz, batch, d_dense, d_x0, (cudaStream_t)stream);
+  const uint64_t ke[7] = {3, u64(d_indices), u64(d_offsets), (uint64_t)nnz, (uint64_t)batch, u64(d_dense), u64(d_x0)};
+  return run_stage(c, ke, (cudaStream_t)stream,
+                   [&](cudaStream_t s) { return do_embed(c, d_indices, d_offsets, nnz, batch, d_dense, d_x0, s); });
 }
 
 int cvr_dense(cvr_ctx* c, const void* d_x0, int batch, float* d_scores, cvr_stream_t stream) {
@@ -672,7 +782,8 @@ int cvr_dense(cvr_ctx* c, const void* d_x0, int batch, float* d_scores, cvr_stre
       tm = &c->tm_x0user;
     }
   }
-  return do_dense(c, d_x0, tm, batch, d_scores, (cudaStream_t)stream);
+  const uint64_t kd[7] = {4, u64(d_x0), (uint64_t)batch, u64(d_scores), 0, 0, 0};
+  return run_stage(c, kd, (cudaStream_t)stream, [&](cudaStream_t s) { return do_dense(c, d_x0, tm, batch, d_scores, s); });
 }
 
 int cvr_score(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, int64_t nnz, int batch,
@@ -690,12 +801,15 @@ int cvr_score(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, in
   if (c->k >= 2) e = cudaStreamWaitEvent(se, c->ev_dense[slot], 0);  // dense(k-2) released the slot
   if (e != cudaSuccess) return c->cuda_fail(e, "wait dense(k-2)");
   void* x0 = c->ws + c->off_x0[slot];
-  st = do_embed(c, d_indices, d_offsets, nnz, batch, d_dense, x0, se);
+  const uint64_t ke[7] = {1, u64(d_indices), u64(d_offsets), (uint64_t)nnz, (uint64_t)batch, u64(d_dense), u64(x0)};
+  st = run_stage(c, ke, se, [&](cudaStream_t s) { return do_embed(c, d_indices, d_offsets, nnz, batch, d_dense, x0, s); });
   if (st) return st;
   if ((e = cudaEventRecord(c->ev_embed[slot], se)) != cudaSuccess) return c->cuda_fail(e, "record embed");
   if ((e = cudaStreamWaitEvent(sd, c->ev_embed[slot], 0)) != cudaSuccess) return c->cuda_fail(e, "wait embed");
   if (batch > 0) {
-    st = do_dense(c, x0, c->backbone == CVR_DCN_LOWRANK ? &c->tm_x0slot[slot] : nullptr, batch, d_scores, sd);
+    const CUtensorMap* tm = c->backbone == CVR_DCN_LOWRANK ? &c->tm_x0slot[slot] : nullptr;
+    const uint64_t kd[7] = {2, u64(x0), (uint64_t)batch, u64(d_scores), 0, 0, 0};
+    st = run_stage(c, kd, sd, [&](cudaStream_t s) { return do_dense(c, x0, tm, batch, d_scores, s); });
     if (st) return st;
   }
   if ((e = cudaEventRecord(c->ev_dense[slot], sd)) != cudaSuccess) return c->cuda_fail(e, "record dense");
@@ -774,7 +888,9 @@ int cvr_embed_shard(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offse
   if (c->F && !c->slot("norm/mean")->loaded) return c->fail(CVR_E_STATE, "norm/mean,std not loaded");
   EmbedArgs a = embed_args(c, d_indices, d_offsets, nnz, batch_global, d_dense, d_send, (int64_t)c->T_pad * c->d, d_x0,
                            batch_global / c->world);
+  c->pbeg((cudaStream_t)stream);
   cudaError_t e = launch_embed(a, c->num_sms, (cudaStream_t)stream);
+  c->pend(K_EMBED, (cudaStream_t)stream);
   if (e != cudaSuccess) return c->cuda_fail(e, "embed_shard launch");
   return CVR_OK;
 }
@@ -783,10 +899,111 @@ int cvr_unpack_shard(cvr_ctx* c, const void* d_recv, int batch_global, void* d_x
   if (!c) return CVR_E_ARG;
   if (!c->cuda_ready) return c->fail(CVR_E_STATE, "workspace not set");
   if (!d_recv || !d_x0 || batch_global < 0 || batch_global % c->world) return c->fail(CVR_E_ARG, "bad arguments");
+  c->pbeg((cudaStream_t)stream);
   cudaError_t e = launch_unpack(d_recv, d_x0, c->x0_ld, c->world, batch_global / c->world, c->T_pad, c->T, c->d, c->act,
                                 (cudaStream_t)stream);
+  c->pend(K_UNPACK, (cudaStream_t)stream);
   if (e != cudaSuccess) return c->cuda_fail(e, "unpack launch");
   return CVR_OK;
+}
+
+int cvr_launch_count(const cvr_ctx* c, int64_t* n) {
+  if (!c || !n) return CVR_E_ARG;
+  *n = c->launches;
+  return CVR_OK;
+}
+
+int cvr_profile_begin(cvr_ctx* c, int max_launches) {
+  if (!c || max_launches < 0) return CVR_E_ARG;
+  if (!c->cuda_ready) return c->fail(CVR_E_STATE, "workspace not set");
+  while (c->prof_ev.size() < (size_t)max_launches * 2) {
+    cudaEvent_t ev;
+    cudaError_t e = cudaEventCreate(&ev);
+    if (e != cudaSuccess) return c->cuda_fail(e, "profile event create");
+    c->prof_ev.push_back(ev);
+  }
+  c->prof_kid.assign((size_t)max_launches, 0);
+  c->prof_cap = (size_t)max_launches;
+  c->prof_n = 0;
+  c->prof_on = true;
+  return CVR_OK;
+}
+
+int cvr_profile_end(cvr_ctx* c, cvr_kernel_stat* out, int max_out, int* n_out) {
+  if (!c || !n_out || (max_out > 0 && !out)) return CVR_E_ARG;
+  c->prof_on = false;
+  cvr_kernel_stat agg[K_COUNT];
+  memset(agg, 0, sizeof agg);
+  for (size_t i = 0; i < c->prof_n; ++i) {
+    cudaError_t e = cudaEventSynchronize(c->prof_ev[2 * i + 1]);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, c->prof_ev[2 * i], c->prof_ev[2 * i + 1]);
+    if (e != cudaSuccess) return c->cuda_fail(e, "profile read");
+    cvr_kernel_stat& a = agg[c->prof_kid[i]];
+    if (a.launches == 0 || ms < a.min_ms) a.min_ms = ms;
+    if (a.launches == 0 || ms > a.max_ms) a.max_ms = ms;
+    a.total_ms += ms;
+    a.launches++;
+  }
+  int n = 0;
+  for (int k = 0; k < K_COUNT; ++k) {
+    if (!agg[k].launches) continue;
+    if (n < max_out) {
+      out[n] = agg[k];
+      snprintf(out[n].name, sizeof out[n].name, "%s", kKernelNames[k]);
+    }
+    ++n;
+  }
+  *n_out = n;
+  c->prof_n = 0;
+  return CVR_OK;
+}
+
+int cvr_gemm_bf16(const void* d_A, int64_t lda, const void* d_B, int64_t ldb, void* d_C, int64_t ldc, int M, int N,
+                  int K, int epi, const float* d_bias, int bn, cvr_stream_t stream) {
+  if (!d_A || !d_B || !d_C || M < 0 || N <= 0 || K <= 0 || (epi == 1 && !d_bias)) return CVR_E_ARG;
+  if (epi != 0 && epi != 1) return CVR_E_ARG;
+  if (K % 64 || N % bn || (bn != 64 && bn != 128) || lda < K || ldb < K || ldc < N || (lda | ldb | ldc) & 7)
+    return CVR_E_UNSUPPORTED;
+  if (M == 0) return CVR_OK;
+  const char* er = nullptr;
+  CUtensorMap ta, tb, tc;
+  if (encode_tmap_bf16(&ta, d_A, M, K, lda, 128, &er) || encode_tmap_bf16(&tb, d_B, N, K, ldb, bn, &er) ||
+      encode_tmap_bf16(&tc, d_C, M, N, ldc, 32, &er))
+    return CVR_E_CUDA;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  GemmArgs a{};
+  a.tmA = &ta;
+  a.tmB = &tb;
+  a.tmOut = &tc;
+  a.bias = d_bias;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.BN = bn;
+  a.epi = epi == 0 ? EPI_STORE : EPI_BIAS_RELU;
+  a.num_sms = sms;
+  a.pdl = false;
+  return launch_gemm_bf16(a, (cudaStream_t)stream) == cudaSuccess ? CVR_OK : CVR_E_CUDA;
+}
+
+int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
+  if (!c || !key) return CVR_E_ARG;
+  if (!strcmp(key, "graphs")) {
+    c->use_graphs = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    return CVR_OK;
+  }
+  if (!strcmp(key, "pdl")) {
+    c->pdl = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    return CVR_OK;
+  }
+  return c->fail(CVR_E_ARG, "unknown option '%s'", key);
 }
 
 }  // extern "C"

@@ -68,23 +68,25 @@ cudaError_t launch_dense_f32(const DenseF32Args& a, cudaStream_t s);
 // ---- K4: tcgen05 bf16 GEMM with fused epilogues --------------------------------------------------
 enum Epi { EPI_STORE = 0, EPI_BIAS_RELU = 1, EPI_CROSS = 2, EPI_HEAD = 3 };
 
-struct EpiParams {
-  void* out;              // bf16 [M, ldo]  (EPI_STORE / BIAS_RELU / CROSS)
-  int64_t ldo;
-  const float* bias;      // fp32 [N]
-  const __nv_bfloat16* x0;  // EPI_CROSS
-  int64_t ld_x0;
-  const __nv_bfloat16* xl;  // EPI_CROSS
-  int64_t ld_xl;
-  const float* head_w;    // EPI_HEAD fp32 [N]
+struct GemmArgs {
+  const CUtensorMap* tmA;    // A [M, K] bf16, box {64, 128}
+  const CUtensorMap* tmB;    // B [N, K] bf16, box {64, BN}
+  const CUtensorMap* tmOut;  // C [M, N] bf16, box {64, 32} (not EPI_HEAD)
+  const CUtensorMap* tmX0;   // EPI_CROSS: x0 [M, N], box {64, 128}
+  const CUtensorMap* tmXl;   // EPI_CROSS: x_l [M, N], box {64, 128}
+  const float* bias;         // fp32 [N] (not EPI_STORE)
+  const float* head_w;       // EPI_HEAD fp32 [N]
   float head_b;
-  float* scores;          // EPI_HEAD fp32 [M]
+  float* scores;             // EPI_HEAD fp32 [M]
+  int M, N, K, BN;
+  Epi epi;
+  int num_sms;
+  bool pdl;                  // launch with programmatic stream serialization
 };
 
-// C[M, N] = epi(A[M, K] . B[N, K]^T); A, B bf16 K-major with tensor maps (box 64 x 128 / 64 x BN,
-// SWIZZLE_128B).  K % 64 == 0, N % BN == 0, BN in {64, 128, 256}; EPI_HEAD needs BN == N.
-cudaError_t launch_gemm_bf16(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K, int BN, Epi epi,
-                             const EpiParams& p, cudaStream_t s);
+// C[M, N] = epi(A[M, K] . B[N, K]^T).  K % 64 == 0, N % BN == 0, BN in {64, 128, 256};
+// EPI_HEAD needs BN == N.  Persistent: grid = min(tiles, num_sms).
+cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s);
 
 // host: encode a 2-D bf16 K-major tensor map [rows, cols] (row stride ld elements) with box
 // {64, box_rows} and 128-byte swizzle.

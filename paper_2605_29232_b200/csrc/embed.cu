@@ -150,8 +150,10 @@ template <typename TIn, typename TOut, int LPR>
 cudaError_t launch_t(const EmbedArgs& a, int num_sms, cudaStream_t s) {
   const int threads = 256;
   const int64_t n_bags = (int64_t)a.T * a.B;
+  // one bag per lane group, no grid-stride loop: short-lived CTAs let the block scheduler interleave
+  // the concurrently running dense-stage GEMM CTAs (higher-priority stream) as embed CTAs retire
   int64_t nbE = (n_bags * LPR + threads - 1) / threads;
-  const int64_t capE = (int64_t)num_sms * 8;
+  const int64_t capE = (int64_t)num_sms * 64;
   if (nbE > capE) nbE = capE;
   int64_t nbD = 0;
   if (a.x0 && a.Bd > 0 && a.pad_col1 > a.dense_col0) {

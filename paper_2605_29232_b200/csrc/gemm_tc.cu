@@ -8,13 +8,19 @@
 //   EPI_HEAD       s = sigmoid(ReLU(A B^T + b) . m + c)   last MLP layer + head, h never stored
 //                                                    (BASELINE.json north star)
 //
-// A [M, K] and B [N, K] are bf16, K-major, moved by TMA into 128-byte-swizzled shared memory
-// (BK = 64 elements = one swizzle atom).  One CTA computes a BM=128 x BN tile: warp 0 is the
-// TMA producer, warp 1 allocates TMEM and one elected lane issues tcgen05.mma (M=128, N=BN,
-// K=16) into a 128-lane x BN-column fp32 TMEM accumulator, warps 2-5 are the epilogue (each
-// reads its 32-lane TMEM quadrant with tcgen05.ld, one row per thread).  A STAGES-deep
-// full/empty mbarrier ring overlaps TMA with MMA.  No split-K: every row's result depends only
-// on that row, in a fixed K order, so scores are batch-invariant.
+// Design (persistent, warp-specialised, one CTA per SM):
+//   * A [M, K] and B [N, K] bf16, K-major, moved by TMA into 128-byte-swizzled shared memory
+//     (BK = 64 elements = one swizzle atom) through a STAGES-deep full/empty mbarrier ring.
+//   * warp 0 = TMA producer (also loads the x0 / x_l epilogue tiles of EPI_CROSS by TMA);
+//     warp 1 = TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16);
+//     warps 2-5 = epilogue, each owning a 32-lane TMEM quadrant (= 32 rows of the tile).
+//   * Two TMEM accumulators (2 x BN columns): the epilogue of tile i overlaps the MMAs of
+//     tile i+1.  Output tiles are staged in swizzled shared memory and written by TMA stores.
+//   * Tiles are visited n-fastest so CTAs working at the same time share the A row block in L2.
+//   * Programmatic dependent launch: the prologue (barrier init, TMEM alloc, descriptor
+//     prefetch) runs before griddepcontrol.wait, overlapping the previous kernel's tail.
+//   * No split-K: every row's result depends only on that row, in a fixed K order, so scores are
+//     batch-invariant.
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
@@ -27,15 +33,24 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 192;
+constexpr int kSmemBudget = 225 * 1024;
 
-template <int BN>
+template <int BN, int EPI>
 struct Cfg {
-  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int A_BYTES = BM * BK * 2;       // 16 KB
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
-  static constexpr int TMEM_COLS = BN;  // 64 / 128 / 256: powers of two >= 32
-  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  static constexpr int SUB = BM * 64 * 2;           // one 128 x 64 bf16 sub-tile (16 KB)
+  static constexpr int NSUB = BN / 64;
+  static constexpr int OUT_BYTES = EPI == EPI_HEAD ? 0 : NSUB * SUB;              // per accumulator
+  static constexpr int EIN_BYTES = EPI == EPI_CROSS ? 2 * NSUB * SUB : 0;          // x0 + x_l tiles
+  static constexpr int EPI_BYTES = 2 * (OUT_BYTES + EIN_BYTES);                    // double-buffered
+  static constexpr int BAR_BYTES = 256;
+  static constexpr int STAGES_FIT = (kSmemBudget - 1024 - BAR_BYTES - EPI_BYTES) / STAGE;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr int TMEM_COLS = 2 * BN;          // two accumulators; BN in {64,128,256}
+  static constexpr int SMEM = 1024 + STAGES * STAGE + EPI_BYTES + BAR_BYTES;
+  static_assert(STAGES >= 2, "shared memory budget");
 };
 
 __device__ __forceinline__ float sigmoid_f32(float z) {
@@ -44,144 +59,222 @@ __device__ __forceinline__ float sigmoid_f32(float z) {
   return e / (1.f + e);
 }
 
-__device__ __forceinline__ void load16_bf16(const __nv_bfloat16* p, float (&v)[16]) {
-  const uint4 a = *reinterpret_cast<const uint4*>(p);
-  const uint4 b = *reinterpret_cast<const uint4*>(p + 8);
-  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    v[2 * i] = ptx::bf16_lo(w[i]);
-    v[2 * i + 1] = ptx::bf16_hi(w[i]);
-  }
+// 16-byte chunk `ch` (0..7) of row `r` in a 128-B-swizzled [rows x 64] bf16 sub-tile
+__device__ __forceinline__ uint32_t swz(uint32_t sub_base, int r, int ch) {
+  return sub_base + r * 128 + ((ch ^ (r & 7)) << 4);
 }
-__device__ __forceinline__ void store16_bf16(__nv_bfloat16* p, const float (&v)[16]) {
-  uint4 a, b;
-  a.x = ptx::pack_bf16(v[0], v[1]);
-  a.y = ptx::pack_bf16(v[2], v[3]);
-  a.z = ptx::pack_bf16(v[4], v[5]);
-  a.w = ptx::pack_bf16(v[6], v[7]);
-  b.x = ptx::pack_bf16(v[8], v[9]);
-  b.y = ptx::pack_bf16(v[10], v[11]);
-  b.z = ptx::pack_bf16(v[12], v[13]);
-  b.w = ptx::pack_bf16(v[14], v[15]);
-  *reinterpret_cast<uint4*>(p) = a;
-  *reinterpret_cast<uint4*>(p + 8) = b;
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const EpiParams p, int M, int K) {
-  using C = Cfg<BN>;
+                     const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmX0,
+                     const __grid_constant__ CUtensorMap tmXl, const float* __restrict__ bias,
+                     const float* __restrict__ head_w, float head_b, float* __restrict__ scores, int M, int N,
+                     int K) {
+  using C = Cfg<BN, EPI>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint8_t* sB = sA + C::STAGES * C::A_BYTES;
+  uint8_t* sOut = sB + C::STAGES * C::B_BYTES;     // [2][NSUB][SUB]
+  uint8_t* sEin = sOut + 2 * C::OUT_BYTES;         // [2][x0 NSUB subs | x_l NSUB subs]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEin + 2 * C::EIN_BYTES);
+  uint64_t* full = bars;
   uint64_t* empty = full + C::STAGES;
-  uint64_t* done = empty + C::STAGES;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* tfull = empty + C::STAGES;   // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;          // [2] accumulator drained (4 epilogue warps)
+  uint64_t* efull = tempty + 2;          // [2] epilogue input tiles landed
+  uint64_t* eempty = efull + 2;          // [2] epilogue input tiles consumed (4 warps)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(eempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+  const int n_tiles_n = N / BN;
+  const int n_tiles = ((M + BM - 1) / BM) * n_tiles_n;
   const int nk = K / BK;
 
   if (threadIdx.x == 0) {
-#pragma unroll
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
-    ptx::mbar_init(done, 1);
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&tfull[a], 1);
+      ptx::mbar_init(&tempty[a], 4);
+      ptx::mbar_init(&efull[a], 1);
+      ptx::mbar_init(&eempty[a], 4);
+    }
     ptx::fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
+    if (EPI != EPI_HEAD) ptx::prefetch_tmap(&tmOut);
+    if (EPI == EPI_CROSS) {
+      ptx::prefetch_tmap(&tmX0);
+      ptx::prefetch_tmap(&tmXl);
+    }
   }
   if (warp == 1) ptx::tmem_alloc(tmem_holder, C::TMEM_COLS);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  ptx::griddep_wait();  // inputs written by the previous kernel are visible from here on
 
   if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % C::STAGES;
-        if (kb >= C::STAGES) ptx::mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
-        ptx::mbar_arrive_expect_tx(&full[s], C::STAGE);
-        ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
-        ptx::tma_load_2d(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);
+    if (lane == 0) {  // ================= TMA producer
+      int g = 0;      // global k-block counter (ring position)
+      int it = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+        const int m0 = (tile / n_tiles_n) * BM, n0 = (tile % n_tiles_n) * BN;
+        if constexpr (EPI == EPI_CROSS) {
+          const int a = it & 1;
+          if (it >= 2) ptx::mbar_wait(&eempty[a], ((it >> 1) - 1) & 1);
+          ptx::mbar_arrive_expect_tx(&efull[a], C::EIN_BYTES);
+          uint8_t* base = sEin + a * C::EIN_BYTES;
+#pragma unroll
+          for (int j = 0; j < C::NSUB; ++j) {
+            ptx::tma_load_2d(base + j * C::SUB, &tmX0, &efull[a], n0 + j * 64, m0);
+            ptx::tma_load_2d(base + (C::NSUB + j) * C::SUB, &tmXl, &efull[a], n0 + j * 64, m0);
+          }
+        }
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % C::STAGES;
+          if (g >= C::STAGES) ptx::mbar_wait(&empty[s], ((g / C::STAGES) - 1) & 1);
+          ptx::mbar_arrive_expect_tx(&full[s], C::STAGE);
+          ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
+          ptx::tma_load_2d(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);
+        }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer (single thread)
+    if (lane == 0) {  // ================= MMA issuer
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % C::STAGES;
-        ptx::mbar_wait(&full[s], (kb / C::STAGES) & 1);
+      int g = 0, it = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+        const int a = it & 1;
+        if (it >= 2) ptx::mbar_wait(&tempty[a], ((it >> 1) - 1) & 1);
         ptx::tc_fence_after();
-        const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
-        const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
+        const uint32_t acc = tmem + a * BN;
+        for (int kb = 0; kb < nk; ++kb, ++g) {
+          const int s = g % C::STAGES;
+          ptx::mbar_wait(&full[s], (g / C::STAGES) & 1);
+          ptx::tc_fence_after();
+          const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
+          const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)  // K step 16 = 32 bytes = +2 in the 16-byte address field
-          ptx::umma_bf16_ss(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-        ptx::umma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
-      }
-      ptx::umma_commit(done);  // accumulator complete
-    }
-    __syncwarp();
-  } else {  // ---- epilogue warps 2..5: TMEM quadrant q = warp % 4 holds rows 32q .. 32q+31
-    ptx::mbar_wait(done, 0);
-    ptx::tc_fence_after();
-    const int q = warp & 3;
-    const int m = m0 + q * 32 + lane;
-    const bool live = m < M;
-    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
-    float z = 0.f;
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      uint32_t r[16];
-      ptx::tmem_ld_32x32b_x16(trow + c, r);
-      ptx::tmem_wait_ld();
-      float v[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-      const int n = n0 + c;
-      if constexpr (EPI == EPI_STORE) {
-        if (live) store16_bf16(reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)m * p.ldo + n, v);
-      } else if constexpr (EPI == EPI_BIAS_RELU) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j] + __ldg(p.bias + n + j), 0.f);
-        if (live) store16_bf16(reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)m * p.ldo + n, v);
-      } else if constexpr (EPI == EPI_CROSS) {
-        if (live) {
-          float x0v[16], xlv[16];
-          load16_bf16(p.x0 + (int64_t)m * p.ld_x0 + n, x0v);
-          load16_bf16(p.xl + (int64_t)m * p.ld_xl + n, xlv);
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = x0v[j] * (v[j] + __ldg(p.bias + n + j)) + xlv[j];
-          store16_bf16(reinterpret_cast<__nv_bfloat16*>(p.out) + (int64_t)m * p.ldo + n, v);
+          for (int k = 0; k < BK / 16; ++k)  // K step 16 = 32 bytes = +2 in the 16-byte address field
+            ptx::umma_bf16_ss(acc, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          ptx::umma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
         }
-      } else {  // EPI_HEAD: h = ReLU(acc + b) kept in fp32, dotted with the head weights
-#pragma unroll
-        for (int j = 0; j < 16; ++j) z = fmaf(fmaxf(v[j] + __ldg(p.bias + n + j), 0.f), __ldg(p.head_w + n + j), z);
+        ptx::umma_commit(&tfull[a]);    // accumulator a complete
       }
     }
-    if constexpr (EPI == EPI_HEAD) {
-      if (live) p.scores[m] = sigmoid_f32(z + p.head_b);
+  } else {  // ================= epilogue warps 2..5: TMEM quadrant q = warp % 4 -> rows 32q .. 32q+31
+    const int q = warp & 3;
+    const int r = q * 32 + lane;  // row within the tile
+    int it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+      const int m0 = (tile / n_tiles_n) * BM, n0 = (tile % n_tiles_n) * BN;
+      const int a = it & 1;
+      ptx::mbar_wait(&tfull[a], (it >> 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t trow = tmem + a * BN + ((uint32_t)(q * 32) << 16);
+      const uint32_t out_base = ptx::smem_u32(sOut + a * C::OUT_BYTES);
+      const uint32_t ein_base = ptx::smem_u32(sEin + a * C::EIN_BYTES);
+      if constexpr (EPI == EPI_CROSS) ptx::mbar_wait(&efull[a], (it >> 1) & 1);
+      if constexpr (EPI != EPI_HEAD) {
+        // the TMA store issued from this buffer two tiles ago must have finished reading it
+        if (lane == 0) ptx::bulk_wait_read<1>();
+        __syncwarp();
+      }
+      float z = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v0[16], v1[16];
+        ptx::tmem_ld_32x32b_x16(trow + c, v0);
+        ptx::tmem_ld_32x32b_x16(trow + c + 16, v1);
+        ptx::tmem_wait_ld();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          v[j] = __uint_as_float(v0[j]);
+          v[16 + j] = __uint_as_float(v1[j]);
+        }
+        const int n = n0 + c;
+        if constexpr (EPI == EPI_HEAD) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) z = fmaf(fmaxf(v[j] + __ldg(bias + n + j), 0.f), __ldg(head_w + n + j), z);
+        } else {
+          const int sub = c >> 6, ch0 = (c & 63) >> 3;  // 4 chunks of 8 columns
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float* w = v + 8 * u;
+            if constexpr (EPI == EPI_BIAS_RELU) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) w[j] = fmaxf(w[j] + __ldg(bias + n + 8 * u + j), 0.f);
+            } else if constexpr (EPI == EPI_CROSS) {
+              const uint4 xa = lds128(swz(ein_base + sub * C::SUB, r, ch0 + u));
+              const uint4 xb = lds128(swz(ein_base + (C::NSUB + sub) * C::SUB, r, ch0 + u));
+              const uint32_t x0w[4] = {xa.x, xa.y, xa.z, xa.w}, xlw[4] = {xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                w[2 * j] = ptx::bf16_lo(x0w[j]) * (w[2 * j] + __ldg(bias + n + 8 * u + 2 * j)) + ptx::bf16_lo(xlw[j]);
+                w[2 * j + 1] =
+                    ptx::bf16_hi(x0w[j]) * (w[2 * j + 1] + __ldg(bias + n + 8 * u + 2 * j + 1)) + ptx::bf16_hi(xlw[j]);
+              }
+            }
+            uint4 o;
+            o.x = ptx::pack_bf16(w[0], w[1]);
+            o.y = ptx::pack_bf16(w[2], w[3]);
+            o.z = ptx::pack_bf16(w[4], w[5]);
+            o.w = ptx::pack_bf16(w[6], w[7]);
+            sts128(swz(out_base + sub * C::SUB, r, ch0 + u), o);
+          }
+        }
+      }
+      // accumulator (and epilogue inputs) consumed: hand them back
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        ptx::mbar_arrive(&tempty[a]);
+        if constexpr (EPI == EPI_CROSS) ptx::mbar_arrive(&eempty[a]);
+      }
+      if constexpr (EPI == EPI_HEAD) {
+        const int m = m0 + r;
+        if (m < M) scores[m] = sigmoid_f32(z + head_b);
+      } else {
+        ptx::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int j = 0; j < C::NSUB; ++j)
+            ptx::tma_store_2d(&tmOut, sOut + a * C::OUT_BYTES + j * C::SUB + q * 32 * 128, n0 + j * 64, m0 + q * 32);
+          ptx::bulk_commit();
+        }
+      }
+    }
+    if constexpr (EPI != EPI_HEAD) {
+      if (lane == 0) ptx::bulk_wait<0>();
     }
   }
   ptx::tc_fence_before();
   __syncthreads();
+  ptx::griddep_launch();
   if (warp == 1) ptx::tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
 template <int BN, int EPI>
-cudaError_t launch_t(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K, const EpiParams& p,
-                     cudaStream_t s) {
-  using C = Cfg<BN>;
+cudaError_t launch_t(const GemmArgs& g, cudaStream_t s) {
+  using C = Cfg<BN, EPI>;
   auto kern = gemm_bf16_kernel<BN, EPI>;
   static bool attr_done = false;
   if (!attr_done) {
@@ -189,36 +282,56 @@ cudaError_t launch_t(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int 
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  dim3 grid(N / BN, (M + BM - 1) / BM);
-  kern<<<grid, kThreads, C::SMEM, s>>>(*tmA, *tmB, p, M, K);
-  return cudaGetLastError();
-}
-
-template <int BN>
-cudaError_t launch_bn(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K, Epi epi,
-                      const EpiParams& p, cudaStream_t s) {
-  switch (epi) {
-    case EPI_STORE: return launch_t<BN, EPI_STORE>(tmA, tmB, M, N, K, p, s);
-    case EPI_BIAS_RELU: return launch_t<BN, EPI_BIAS_RELU>(tmA, tmB, M, N, K, p, s);
-    case EPI_CROSS: return launch_t<BN, EPI_CROSS>(tmA, tmB, M, N, K, p, s);
-    case EPI_HEAD: return launch_t<BN, EPI_HEAD>(tmA, tmB, M, N, K, p, s);
-  }
-  return cudaErrorInvalidValue;
+  const int n_tiles = ((g.M + BM - 1) / BM) * (g.N / BN);
+  const int grid = n_tiles < g.num_sms ? n_tiles : g.num_sms;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g.pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const CUtensorMap* dummy = g.tmA;
+  return cudaLaunchKernelEx(&cfg, kern, *g.tmA, *g.tmB, *(g.tmOut ? g.tmOut : dummy), *(g.tmX0 ? g.tmX0 : dummy),
+                            *(g.tmXl ? g.tmXl : dummy), g.bias, g.head_w, g.head_b, g.scores, g.M, g.N, g.K);
 }
 
 }  // namespace
 
-cudaError_t launch_gemm_bf16(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K, int BN, Epi epi,
-                             const EpiParams& p, cudaStream_t s) {
-  if (M <= 0) return cudaSuccess;
-  if (K % BK || N % BN || (epi == EPI_HEAD && BN != N)) return cudaErrorInvalidValue;
-  switch (BN) {
-    case 64: return launch_bn<64>(tmA, tmB, M, N, K, epi, p, s);
-    case 128: return launch_bn<128>(tmA, tmB, M, N, K, epi, p, s);
-    case 256: return launch_bn<256>(tmA, tmB, M, N, K, epi, p, s);
+// instantiated (BN, epilogue) pairs: the shared-memory budget allows the double-buffered
+// x0/x_l/out tiles of EPI_CROSS only at BN = 64, and staged bf16 outputs up to BN = 128.
+cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
+  if (g.M <= 0) return cudaSuccess;
+  if (g.K % BK || g.N % g.BN || (g.epi == EPI_HEAD && g.BN != g.N)) return cudaErrorInvalidValue;
+  if (g.epi != EPI_HEAD && !g.tmOut) return cudaErrorInvalidValue;
+  if (g.epi == EPI_CROSS && (!g.tmX0 || !g.tmXl)) return cudaErrorInvalidValue;
+  switch (g.epi) {
+    case EPI_STORE:
+      if (g.BN == 64) return launch_t<64, EPI_STORE>(g, s);
+      if (g.BN == 128) return launch_t<128, EPI_STORE>(g, s);
+      break;
+    case EPI_BIAS_RELU:
+      if (g.BN == 64) return launch_t<64, EPI_BIAS_RELU>(g, s);
+      if (g.BN == 128) return launch_t<128, EPI_BIAS_RELU>(g, s);
+      break;
+    case EPI_CROSS:
+      if (g.BN == 64) return launch_t<64, EPI_CROSS>(g, s);
+      break;
+    case EPI_HEAD:
+      if (g.BN == 64) return launch_t<64, EPI_HEAD>(g, s);
+      if (g.BN == 128) return launch_t<128, EPI_HEAD>(g, s);
+      if (g.BN == 256) return launch_t<256, EPI_HEAD>(g, s);
+      break;
   }
   return cudaErrorInvalidValue;
 }
+
+namespace {
+
+}  // namespace
 
 int encode_tmap_bf16(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                      const char** err) {

@@ -6,23 +6,10 @@ import numpy as np
 import torch
 
 import cvr_synth as cs
+from cvr_synth import sub_batch  # noqa: F401
 
 TOL_F32 = 1e-5   # BASELINE.json north star: fp32 path, absolute on scores
 TOL_BF16 = 2e-3  # BASELINE.json north star: bf16 path, absolute on the sigmoid output
-
-
-def sub_batch(bt: cs.Batch, sel) -> cs.Batch:
-    """The examples ``sel`` of ``bt`` as their own batch (same bags, same order)."""
-    sel = np.asarray(sel)
-    T, B = bt.n_tables, bt.batch
-    idx, off = [], [0]
-    for t in range(T):
-        for b in sel:
-            seg = bt.indices[bt.offsets[t * B + b]:bt.offsets[t * B + b + 1]]
-            idx.append(seg)
-            off.append(off[-1] + len(seg))
-    idx = np.concatenate(idx) if idx else np.zeros(0, np.int32)
-    return cs.Batch(len(sel), T, idx.astype(np.int32), np.array(off, np.int32), bt.dense[sel])
 
 
 def device_tables(cfg, device="cuda"):
