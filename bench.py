@@ -142,7 +142,7 @@ def gemm_flops(cfg, B) -> dict:
     W, r = cfg.width, cfg.cross_rank
     dims = [W] + list(cfg.mlp_dims)
     mlp = sum(2 * B * dims[i] * dims[i + 1] for i in range(len(cfg.mlp_dims) - 1))
-    return {"gemm_xV": 2 * B * W * r, "gemm_tU_cross": 2 * B * r * W,
+    return {"gemm_xV": 2 * B * W * r, "gemm_tU_cross": 2 * B * r * W, "cross_fused": 4 * B * W * r,
             "gemm_mlp_relu_total": mlp, "gemm_mlp_head": 2 * B * dims[-2] * dims[-1] + 2 * B * dims[-1]}
 
 
@@ -265,7 +265,7 @@ def run_cvr(args, cfg):
 
     clocks = ClockSampler(local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches_per_step = 1 + 2 * cfg.n_cross + len(cfg.mlp_dims)
+    launches_per_step = 1 + 2 * cfg.n_cross + len(cfg.mlp_dims)  # upper bound (fused cross: 1 per layer)
     with clocks:
         barrier(world)
         torch.cuda.synchronize(dev)

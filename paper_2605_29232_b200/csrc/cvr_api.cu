@@ -12,6 +12,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -20,9 +21,9 @@
 
 using namespace cvr;
 
-enum KernelId { K_EMBED = 0, K_GEMM_V, K_GEMM_U, K_GEMM_MLP, K_GEMM_HEAD, K_DENSE_F32, K_UNPACK, K_COUNT };
+enum KernelId { K_EMBED = 0, K_GEMM_V, K_GEMM_U, K_GEMM_MLP, K_GEMM_HEAD, K_DENSE_F32, K_UNPACK, K_CROSS_FUSED, K_COUNT };
 static const char* kKernelNames[K_COUNT] = {"embed_bag_pool", "gemm_xV",      "gemm_tU_cross", "gemm_mlp_relu",
-                                            "gemm_mlp_head",  "dense_f32_dcn", "shard_unpack"};
+                                            "gemm_mlp_head",  "dense_f32_dcn", "shard_unpack", "cross_fused"};
 
 namespace {
 
@@ -81,6 +82,11 @@ struct cvr_ctx {
   CUtensorMap tm_x0slot[2], tm_xa, tm_xb, tm_t;   // A-operand / epilogue-input maps, box {64, 128}
   std::vector<CUtensorMap> tm_h;
   CUtensorMap st_xa, st_xb, st_t;                 // output (TMA store) maps, box {64, 32}
+  std::vector<CUtensorMap> tm_v256;               // V_l with box {64, 256} (fused cross layer)
+  bool fused_cross = false;                       // K5 (r == 256)
+  unsigned long long* dbg = nullptr;              // CVR_DEBUG_TIMING: phase stamps of the last fused launch
+  int dbg_ctas = 0;
+  size_t off_part = 0;
   std::vector<CUtensorMap> st_h;
   bool pdl = true;
   // CUDA-graph cache for the executor stages (cvr_score / cvr_score_host)
@@ -320,6 +326,9 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
     c->off_xa = carve(cur, (size_t)B * c->x0_ld * 2);
     c->off_xb = carve(cur, (size_t)B * c->x0_ld * 2);
     c->off_t = carve(cur, (size_t)B * c->r * 2);
+    if (c->r == 256) {  // K5 scratch; K5 itself is opt-in ("fused_cross"): measured slower than 2 GEMMs at B=4096
+      c->off_part = carve(cur, cross_fused_partial_bytes(c->max_batch));
+    }
     for (int i = 0; i + 1 < c->n_mlp; ++i) c->off_h.push_back(carve(cur, (size_t)B * c->mlp[i] * 2));
   }
   const int64_t Bin = c->world > 1 ? B * c->world : B;  // sharded: indices cover the global batch
@@ -337,6 +346,19 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
 
 int cvr_destroy(cvr_ctx* c) {
   if (!c) return CVR_E_ARG;
+  if (c->dbg) {  // debug: per-phase averages of the last fused cross launch
+    std::vector<unsigned long long> h((size_t)c->dbg_ctas * 8);
+    cudaDeviceSynchronize();
+    cudaMemcpy(h.data(), c->dbg, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull;
+    for (int b = 0; b < c->dbg_ctas; ++b) t0 = std::min(t0, h[b * 8]);
+    double avg[7] = {0};
+    for (int b = 0; b < c->dbg_ctas; ++b)
+      for (int i = 0; i < 7; ++i) avg[i] += (double)(h[b * 8 + i] - t0) / c->dbg_ctas;
+    fprintf(stderr, "cross_fused phases (us from first CTA start): start %.2f wait %.2f A %.2f sync1 %.2f B %.2f sync2 %.2f end %.2f\n",
+            avg[0] / 1e3, avg[1] / 1e3, avg[2] / 1e3, avg[3] / 1e3, avg[4] / 1e3, avg[5] / 1e3, avg[6] / 1e3);
+    cudaFree(c->dbg);
+  }
   for (auto ev : c->prof_ev) cudaEventDestroy(ev);
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   for (int i = 0; i < 2; ++i) {
@@ -381,6 +403,7 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
   // zero the activation slots once so padding columns / tail rows are defined
   if (e == cudaSuccess) e = cudaMemset(c->ws + c->off_x0[0], 0, c->ws_need - c->off_x0[0]);
   if (e != cudaSuccess) return c->cuda_fail(e, "cvr_set_workspace");
+  if (getenv("CVR_DEBUG_TIMING") && !c->dbg) cudaMalloc(&c->dbg, (size_t)(c->max_batch / 128 + 1) * 4 * 8 * 8);
   c->cuda_ready = true;
   c->k = 0;
   c->weights_loaded = false;
@@ -449,6 +472,11 @@ int encode_plan(cvr_ctx* c) {
     ok &= addp("dcn/" + std::to_string(l) + "/V", c->r, (int)c->x0_ld, pick_bn(c->r), EPI_STORE);
     ok &= addp("dcn/" + std::to_string(l) + "/U", (int)c->x0_ld, c->r, pick_bn((int)c->x0_ld), EPI_CROSS);
   }
+  c->tm_v256.assign(c->n_cross, CUtensorMap{});
+  if (c->r == 256)
+    for (int l = 0; l < c->n_cross; ++l)
+      ok &= encode_tmap_bf16(&c->tm_v256[l], c->wptr("dcn/" + std::to_string(l) + "/V"), c->r, c->x0_ld, c->x0_ld, 256,
+                             &er) == 0;
   int K = (int)c->x0_ld;
   for (int i = 0; i < c->n_mlp; ++i) {
     const bool last = i + 1 == c->n_mlp;
@@ -665,9 +693,33 @@ int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, int B, float*
   for (int l = 0; l < c->n_cross; ++l) {
     const GemmPlan& gv = c->plan[pi++];
     const GemmPlan& gu = c->plan[pi++];
+    const bool even = l % 2 == 0;
+    if (c->fused_cross) {
+      CrossFusedArgs a{};
+      a.tmXl = tm_xl;
+      a.tmV = &c->tm_v256[l];
+      a.tmT = &c->tm_t;
+      a.tmU = &gu.tmB;
+      a.tmX0 = tm_x0;
+      a.tmOut = even ? &c->st_xa : &c->st_xb;
+      a.bias = c->wptr<float>("dcn/" + std::to_string(l) + "/b");
+      a.part = c->at<float>(c->off_part);
+      a.t_out = c->at<__nv_bfloat16>(c->off_t);
+      a.M = B;
+      a.W = (int)c->x0_ld;
+      a.R = c->r;
+      a.pdl = c->pdl;
+      a.dbg = c->dbg;
+      c->dbg_ctas = (B + 127) / 128 * 4;
+      c->pbeg(s);
+      e = launch_cross_fused(a, s);
+      c->pend(K_CROSS_FUSED, s);
+      if (e != cudaSuccess) return c->cuda_fail(e, "cross_fused launch");
+      tm_xl = even ? &c->tm_xa : &c->tm_xb;
+      continue;
+    }
     e = gemm(gv, tm_xl, &c->st_t, nullptr, nullptr, nullptr, K_GEMM_V);
     if (e != cudaSuccess) return c->cuda_fail(e, "gemm V launch");
-    const bool even = l % 2 == 0;
     e = gemm(gu, &c->tm_t, even ? &c->st_xa : &c->st_xb, tm_x0, tm_xl,
              c->wptr<float>("dcn/" + std::to_string(l) + "/b"), K_GEMM_U);
     if (e != cudaSuccess) return c->cuda_fail(e, "gemm U launch");
@@ -993,6 +1045,13 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return CVR_E_ARG;
   if (!strcmp(key, "graphs")) {
     c->use_graphs = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    return CVR_OK;
+  }
+  if (!strcmp(key, "fused_cross")) {
+    if (value && !(c->backbone == CVR_DCN_LOWRANK && c->r == 256)) return c->fail(CVR_E_UNSUPPORTED, "fused cross needs r == 256");
+    c->fused_cross = value != 0;
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     return CVR_OK;

@@ -88,6 +88,24 @@ struct GemmArgs {
 // EPI_HEAD needs BN == N.  Persistent: grid = min(tiles, num_sms).
 cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s);
 
+// ---- K5: fused low-rank cross layer (cluster of 4 CTAs per 128-row block, r = 256) ----------------
+struct CrossFusedArgs {
+  const CUtensorMap* tmXl;   // x_l [M, W] box {64, 128}
+  const CUtensorMap* tmV;    // V   [r, W] box {64, 256}
+  const CUtensorMap* tmT;    // t   [M, r] box {64, 128}
+  const CUtensorMap* tmU;    // U   [W, r] box {64, 64}
+  const CUtensorMap* tmX0;   // x0  [M, W] box {64, 128}
+  const CUtensorMap* tmOut;  // x_{l+1} [M, W] box {64, 32}
+  const float* bias;         // b_l fp32 [W]
+  float* part;               // fp32 scratch, cross_fused_partial_bytes(max_batch)
+  __nv_bfloat16* t_out;      // t [max_batch, r] bf16
+  int M, W, R;
+  bool pdl;
+  unsigned long long* dbg;   // optional per-CTA phase timestamps (CVR_DEBUG_TIMING)
+};
+size_t cross_fused_partial_bytes(int max_batch);
+cudaError_t launch_cross_fused(const CrossFusedArgs& g, cudaStream_t s);
+
 // host: encode a 2-D bf16 K-major tensor map [rows, cols] (row stride ld elements) with box
 // {64, box_rows} and 128-byte swizzle.
 int encode_tmap_bf16(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,

@@ -175,3 +175,23 @@ def test_c2_zero_weights_closed_form():
     s = m.dense(m.embed(idx, off, 256, dense), 256)
     ref = O.score_forward(cfg, cs.table_specs(cfg), w, bt)
     assert np.abs(s.double().cpu().numpy() - ref["scores"]).max() <= TOL_BF16
+
+
+def test_c2_fused_and_unfused_cross_agree(c2):
+    """K5 (one clustered kernel per cross layer) and the two-GEMM path both meet the oracle; they differ
+    only by fp32 summation order inside t = x_l V^T (K-split partials vs one accumulator)."""
+    cfg, m, tabs, w = c2
+    B = 520
+    bt = cs.make_batch(cfg, 77, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    s_u = m.dense(x0, B).clone()
+    m.set_option("fused_cross", 1)
+    try:
+        s_f = m.dense(x0, B).clone()
+    finally:
+        m.set_option("fused_cross", 0)
+    ref = O.score_forward(cfg, cs.table_specs(cfg), w, bt)["scores"]
+    for s in (s_f, s_u):
+        assert np.abs(s.double().cpu().numpy() - ref).max() <= TOL_BF16
+    assert (s_f - s_u).abs().max().item() <= 5e-4
