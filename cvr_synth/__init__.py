@@ -374,3 +374,17 @@ def request_trace(qps: float, duration_s: float, seed: int = 1005, mu: float = m
     t = t[t < duration_s]
     n = np.clip(np.rint(np.exp(mu + sigma * rng.normal(size=t.shape[0]))), 1, cap).astype(np.int64)
     return t, n
+
+
+def make_item_pool(cfg: CvrConfig, pool_size: int = 1 << 16, k: int = 5000) -> Batch:
+    """A seeded pool of config-style items (A21: items draw from a seeded pool): the features of
+    ``pool_size`` candidate items as one batch (table-major CSR + dense rows)."""
+    return make_batch(cfg, k, batch=pool_size)
+
+
+def make_requests(qps: float, duration_s: float, pool_size: int, seed: int = 1005):
+    """Config 5 request trace: [(t_arrival, item_ids)], Poisson arrivals at ``qps`` queries/s, items per
+    query clip(rint(lognormal(ln 50, 0.8)), 1, 500) drawn uniformly from the pool (A21)."""
+    t, n = request_trace(qps, duration_s, seed=seed)
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence(seed, spawn_key=(STREAM_TRACE, 7, int(qps)))))
+    return [(float(ti), rng.integers(0, pool_size, int(ni)).astype(np.int32)) for ti, ni in zip(t, n)]

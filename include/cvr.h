@@ -199,6 +199,27 @@ int cvr_set_option(cvr_ctx* ctx, const char* key, int64_t value);
 int cvr_gemm_bf16(const void* d_A, int64_t lda, const void* d_B, int64_t ldb, void* d_C, int64_t ldc, int M, int N,
                   int K, int epi, const float* d_bias, int bn, cvr_stream_t stream);
 
+/* -- serving: stage 0 batch assembly (host) -------------------------------
+ * Concatenate n_req requests (request r = n_items[r] candidate items of one query, PAPER.md:1560
+ * "Client-Side Batching") into one batch in the library's input layout.  Request r carries its own
+ * table-major CSR (h_offsets[r] [T*n_r + 1], h_indices[r]) and dense rows h_dense[r] [n_r, F]
+ * (host memory).  Output: out_offsets [T*B + 1], out_indices (capacity out_indices_cap), out_dense
+ * [B, F] with B = sum n_items, items in request order (the scatter map is implicit: request r owns
+ * rows [sum_{q<r} n_q, sum_{q<=r} n_q)).  Pure host memcpy work (typically into pinned staging);
+ * CVR_E_NOMEM if the indices do not fit, CVR_E_INDEX if a request's offsets decrease. */
+int cvr_concat_requests(int n_req, int n_tables, int n_dense, const int* n_items, const int32_t* const* h_offsets,
+                        const int32_t* const* h_indices, const float* const* h_dense, int32_t* out_offsets,
+                        int32_t* out_indices, int64_t out_indices_cap, float* out_dense, int64_t* out_nnz);
+
+/* Gather n items of a host-resident item pool (table-major CSR pool_offsets [T*P + 1],
+ * pool_indices, pool_dense [P, F]; a feature store) into one batch in the library's input layout:
+ * out_offsets [T*n + 1], out_indices, out_dense [n, F], item i of the batch = pool item item_ids[i].
+ * Host-only; CVR_E_INDEX on an item id outside [0, P), CVR_E_NOMEM if the indices do not fit. */
+int cvr_gather_items(int n_tables, int n_dense, int64_t pool_size, const int32_t* pool_offsets,
+                     const int32_t* pool_indices, const float* pool_dense, int n, const int32_t* item_ids,
+                     int32_t* out_offsets, int32_t* out_indices, int64_t out_indices_cap, float* out_dense,
+                     int64_t* out_nnz);
+
 /* -- accounting / measurement -------------------------------------------------------------- */
 /* Number of kernels this ctx has launched since creation (every entry point counts its launches). */
 int cvr_launch_count(const cvr_ctx* ctx, int64_t* n);

@@ -64,6 +64,11 @@ _SIGS = [
     ("cvr_gemm_bf16", ctypes.c_int, [_vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp]),
     ("cvr_set_option", ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int64]),
+    ("cvr_concat_requests", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_ip, ctypes.POINTER(_vp),
+                                           ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp, ctypes.c_int64, _vp,
+                                           _c_i64p]),
+    ("cvr_gather_items", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, _vp, _vp, _vp, ctypes.c_int, _vp,
+                                        _vp, _vp, ctypes.c_int64, _vp, _c_i64p]),
     ("cvr_launch_count", ctypes.c_int, [_vp, _c_i64p]),
     ("cvr_profile_begin", ctypes.c_int, [_vp, ctypes.c_int]),
     ("cvr_profile_end", ctypes.c_int, [_vp, ctypes.POINTER(cvr_kernel_stat), ctypes.c_int, _c_ip]),

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -99,6 +100,7 @@ struct cvr_ctx {
   std::vector<GraphEntry> graphs;
   bool use_graphs = true;
   uint64_t use_clock = 0;
+  std::vector<std::array<uint64_t, 7>> seen_keys;
   const void* last_x0 = nullptr;
   int last_x0_rows = -1;
   CUtensorMap tm_x0user;
@@ -758,6 +760,17 @@ int run_stage(cvr_ctx* c, const uint64_t (&key)[7], cudaStream_t s, F&& enqueue)
       return CVR_OK;
     }
   }
+  // capture only keys seen before: one-off shapes (dynamic batching) launch directly
+  bool seen = false;
+  for (auto& k : c->seen_keys)
+    if (memcmp(k.data(), key, sizeof(uint64_t) * 7) == 0) seen = true;
+  if (!seen) {
+    std::array<uint64_t, 7> k;
+    memcpy(k.data(), key, sizeof(uint64_t) * 7);
+    if (c->seen_keys.size() >= 256) c->seen_keys.erase(c->seen_keys.begin());
+    c->seen_keys.push_back(k);
+    return enqueue(s);
+  }
   const int64_t l0 = c->launches;
   cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return c->cuda_fail(e, "cudaStreamBeginCapture");
@@ -1063,6 +1076,91 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     return CVR_OK;
   }
   return c->fail(CVR_E_ARG, "unknown option '%s'", key);
+}
+
+int cvr_concat_requests(int n_req, int n_tables, int n_dense, const int* n_items, const int32_t* const* h_offsets,
+                        const int32_t* const* h_indices, const float* const* h_dense, int32_t* out_offsets,
+                        int32_t* out_indices, int64_t out_indices_cap, float* out_dense, int64_t* out_nnz) {
+  if (n_req < 0 || n_tables <= 0 || n_dense < 0 || !n_items || !h_offsets || !h_indices || !out_offsets ||
+      !out_indices || !out_nnz || (n_dense && (!h_dense || !out_dense)))
+    return CVR_E_ARG;
+  int64_t B = 0;
+  for (int r = 0; r < n_req; ++r) {
+    if (n_items[r] < 0 || !h_offsets[r]) return CVR_E_ARG;
+    B += n_items[r];
+  }
+  // table-major: for t, for request r, for item i: bag (t, r, i)
+  int64_t pos = 0, bag = 0;
+  out_offsets[0] = 0;
+  for (int t = 0; t < n_tables; ++t) {
+    for (int r = 0; r < n_req; ++r) {
+      const int n = n_items[r];
+      const int32_t* off = h_offsets[r] + (int64_t)t * n;
+      const int32_t lo = off[0], hi = off[n];
+      if (hi < lo) return CVR_E_INDEX;
+      const int64_t len = hi - lo;
+      if (pos + len > out_indices_cap) return CVR_E_NOMEM;
+      if (len) memcpy(out_indices + pos, h_indices[r] + lo, (size_t)len * 4);
+      for (int i = 0; i < n; ++i) out_offsets[++bag] = (int32_t)(pos + (off[i + 1] - lo));
+      pos += len;
+    }
+  }
+  if (n_dense) {
+    int64_t row = 0;
+    for (int r = 0; r < n_req; ++r) {
+      memcpy(out_dense + row * n_dense, h_dense[r], (size_t)n_items[r] * n_dense * 4);
+      row += n_items[r];
+    }
+  }
+  (void)B;
+  *out_nnz = pos;
+  return CVR_OK;
+}
+
+int cvr_gather_items(int n_tables, int n_dense, int64_t pool_size, const int32_t* pool_offsets,
+                     const int32_t* pool_indices, const float* pool_dense, int n, const int32_t* item_ids,
+                     int32_t* out_offsets, int32_t* out_indices, int64_t out_indices_cap, float* out_dense,
+                     int64_t* out_nnz) {
+  if (n_tables <= 0 || n_dense < 0 || pool_size <= 0 || n < 0 || !pool_offsets || !pool_indices || !item_ids ||
+      !out_offsets || !out_indices || !out_nnz || (n_dense && (!pool_dense || !out_dense)))
+    return CVR_E_ARG;
+  for (int i = 0; i < n; ++i)
+    if (item_ids[i] < 0 || item_ids[i] >= pool_size) return CVR_E_INDEX;
+  // pass 1 (parallel over tables): bag lengths -> per-table totals; pass 2: copy at prefix offsets
+  std::vector<int64_t> tot(n_tables + 1, 0);
+  int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+  for (int t = 0; t < n_tables; ++t) {
+    const int32_t* off = pool_offsets + (int64_t)t * pool_size;
+    int64_t s = 0;
+    for (int i = 0; i < n; ++i) {
+      const int64_t it = item_ids[i];
+      const int32_t len = off[it + 1] - off[it];
+      bad |= len < 0;
+      s += len;
+    }
+    tot[t + 1] = s;
+  }
+  if (bad) return CVR_E_INDEX;
+  for (int t = 0; t < n_tables; ++t) tot[t + 1] += tot[t];
+  if (tot[n_tables] > out_indices_cap) return CVR_E_NOMEM;
+  out_offsets[0] = 0;
+#pragma omp parallel for schedule(static)
+  for (int t = 0; t < n_tables; ++t) {
+    const int32_t* off = pool_offsets + (int64_t)t * pool_size;
+    int64_t pos = tot[t];
+    for (int i = 0; i < n; ++i) {
+      const int64_t it = item_ids[i];
+      const int32_t lo = off[it], hi = off[it + 1];
+      for (int32_t q = lo; q < hi; ++q) out_indices[pos++] = pool_indices[q];
+      out_offsets[(int64_t)t * n + i + 1] = (int32_t)pos;
+    }
+  }
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < (n_dense ? n : 0); ++i)
+    memcpy(out_dense + (int64_t)i * n_dense, pool_dense + (int64_t)item_ids[i] * n_dense, (size_t)n_dense * 4);
+  *out_nnz = tot[n_tables];
+  return CVR_OK;
 }
 
 }  // extern "C"

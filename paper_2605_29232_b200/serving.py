@@ -1,0 +1,190 @@
+"""Serving machinery of the scoring path (config 5):
+
+* ``DynamicBatcher`` -- server-side dynamic batching with a coalescing window (PAPER.md:1560
+  "Server-Side Batching dynamically aggregates independent requests", Table 6).
+  Requests (one query's candidate items each: "Client-Side Batching") are queued FIFO and dispatched
+  as the longest FIFO prefix of WHOLE requests with at most ``max_items`` items, either when the queue
+  holds >= max_items items or when the oldest queued request has waited ``window_s`` (window anchored
+  at the oldest request; requests never split or reordered).  A full queue rejects the
+  newest request (CVR_E_OVERLOAD semantics).
+* ``nearest_rank`` -- percentile by nearest rank.
+* ``two_stage_schedule`` -- the simulated-clock model of the decoupled two-stage executor (S9):
+  stage A of batch k+1 overlaps stage B of batch k, with ``slots`` x0 buffers.
+* ``Server`` -- the real loop: admits requests at their scheduled (open-loop) arrival times, batches
+  them, assembles each batch on the host (libcvr ``cvr_gather_items`` into pinned staging, stage 0),
+  scores it through ``cvr_score_host`` (H2D -> embed stream -> dense stream -> D2H, S1-S8) and stamps
+  completion when the scores are on the host.  Latency = completion - scheduled arrival.
+
+Host logic only: every score is computed by libcvr's kernels.
+"""
+from __future__ import annotations
+
+import collections
+import ctypes
+import math
+import time
+from dataclasses import dataclass
+from typing import Deque, List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from ._cvr import CvrError, lib
+
+CVR_E_OVERLOAD = 9
+
+
+@dataclass
+class Request:
+    rid: int
+    t_arrival: float          # scheduled arrival time (s, open loop)
+    n_items: int
+    item_ids: Optional[np.ndarray] = None   # pool item ids (serving benchmark)
+
+
+class DynamicBatcher:
+    def __init__(self, max_items: int = 8192, window_s: float = 0.002, queue_capacity: int = 1 << 16):
+        if max_items < 1 or window_s < 0 or queue_capacity < 1:
+            raise ValueError("max_items >= 1, window_s >= 0, queue_capacity >= 1")
+        self.max_items, self.window_s, self.capacity = max_items, window_s, queue_capacity
+        self.q: Deque[Request] = collections.deque()
+        self.items = 0
+        self.rejected = 0
+
+    def __len__(self):
+        return len(self.q)
+
+    def submit(self, req: Request) -> bool:
+        """Queue a request; False (overload) if the queue is full."""
+        if len(self.q) >= self.capacity:
+            self.rejected += 1
+            return False
+        self.q.append(req)
+        self.items += req.n_items
+        return True
+
+    def next_deadline(self) -> Optional[float]:
+        return self.q[0].t_arrival + self.window_s if self.q else None
+
+    def poll(self, now: float) -> Optional[List[Request]]:
+        """The batch to dispatch at time ``now``, or None."""
+        if not self.q:
+            return None
+        if self.items < self.max_items and now < self.q[0].t_arrival + self.window_s:
+            return None
+        out, n = [], 0
+        while self.q and (not out or n + self.q[0].n_items <= self.max_items):
+            r = self.q.popleft()
+            n += r.n_items
+            out.append(r)
+        self.items -= n
+        return out
+
+
+def nearest_rank(samples: Sequence[float], p: float) -> float:
+    """Nearest-rank percentile: the ceil(p/100 * N)-th smallest sample (1-based)."""
+    s = sorted(samples)
+    if not s:
+        return float("nan")
+    k = max(1, math.ceil(p / 100.0 * len(s)))
+    return s[k - 1]
+
+
+def two_stage_schedule(a_costs: Sequence[float], b_costs: Sequence[float], slots: int = 2, t0: float = 0.0):
+    """Completion times of batches through a two-stage pipeline (stage A on one resource, stage B on
+    another): A(k) starts when A(k-1) is done and its x0 slot is free (B(k-slots) done); B(k) starts
+    when A(k) and B(k-1) are done."""
+    a_done, b_done = [], []
+    for k, (a, b) in enumerate(zip(a_costs, b_costs)):
+        start_a = max(t0, a_done[-1] if a_done else t0, b_done[k - slots] if k >= slots else t0)
+        a_done.append(start_a + a)
+        start_b = max(a_done[-1], b_done[-1] if b_done else t0)
+        b_done.append(start_b + b)
+    return b_done
+
+
+class ItemPoolView:
+    """A host-resident item pool in the library's CSR layout (table-major offsets [T*P+1])."""
+
+    def __init__(self, offsets: np.ndarray, indices: np.ndarray, dense: np.ndarray, n_tables: int):
+        self.P = dense.shape[0]
+        self.T, self.F = n_tables, dense.shape[1]
+        self.offsets = np.ascontiguousarray(offsets, dtype=np.int32)
+        self.indices = np.ascontiguousarray(indices, dtype=np.int32)
+        self.dense = np.ascontiguousarray(dense, dtype=np.float32)
+        assert self.offsets.shape == (self.T * self.P + 1,)
+
+    def gather(self, item_ids: np.ndarray, out_off: torch.Tensor, out_idx: torch.Tensor, out_dense: torch.Tensor) -> int:
+        """Assemble the batch (cvr_gather_items) into the given (pinned) host tensors; returns nnz."""
+        ids = np.ascontiguousarray(item_ids, dtype=np.int32)
+        nnz = ctypes.c_int64()
+        st = lib().cvr_gather_items(self.T, self.F, self.P, self.offsets.ctypes.data, self.indices.ctypes.data,
+                                    self.dense.ctypes.data, len(ids), ids.ctypes.data, out_off.data_ptr(),
+                                    out_idx.data_ptr(), out_idx.numel(), out_dense.data_ptr(), ctypes.byref(nnz))
+        if st:
+            raise CvrError(st, "cvr_gather_items")
+        return nnz.value
+
+
+class Server:
+    """Open-loop serving of a request trace through DynamicBatcher + cvr_score_host."""
+
+    def __init__(self, model, pool: ItemPoolView, max_items: int = 8192, window_s: float = 0.002,
+                 host_slots: int = 3, max_nnz: Optional[int] = None):
+        self.m, self.pool = model, pool
+        self.batcher = DynamicBatcher(max_items, window_s)
+        dev = model.device
+        self.s_copy, self.s_embed = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        self.s_dense = torch.cuda.Stream(dev, priority=-1)
+        T, F = pool.T, pool.F
+        cap = max_nnz or model.max_nnz
+        self.slots = [dict(off=torch.empty(T * max_items + 1, dtype=torch.int32).pin_memory(),
+                           idx=torch.empty(cap, dtype=torch.int32).pin_memory(),
+                           dense=torch.empty(max_items, F, dtype=torch.float32).pin_memory(),
+                           scores=torch.empty(max_items, dtype=torch.float32).pin_memory(),
+                           ev=torch.cuda.Event(), busy=False)
+                      for _ in range(host_slots)]
+
+    def run(self, reqs: List[Request], keep_scores: bool = False):
+        lat = np.full(len(reqs), np.nan)
+        sizes: List[int] = []
+        scores = {} if keep_scores else None
+        inflight: Deque = collections.deque()
+        free = collections.deque(range(len(self.slots)))
+        i, done = 0, 0
+        h_c, h_e, h_d = self.s_copy.cuda_stream, self.s_embed.cuda_stream, self.s_dense.cuda_stream
+        t_start = time.perf_counter() + 0.01
+        clock = lambda: time.perf_counter() - t_start
+        while done < len(reqs):
+            now = clock()
+            while i < len(reqs) and reqs[i].t_arrival <= now:
+                if not self.batcher.submit(reqs[i]):
+                    lat[reqs[i].rid] = np.inf
+                    done += 1
+                i += 1
+            while inflight and inflight[0][1]["ev"].query():
+                batch, slot, si = inflight.popleft()
+                t_done = clock()
+                row = 0
+                for r in batch:
+                    lat[r.rid] = t_done - r.t_arrival
+                    if keep_scores:
+                        scores[r.rid] = slot["scores"][row:row + r.n_items].numpy().copy()
+                    row += r.n_items
+                done += len(batch)
+                free.append(si)
+            if free:
+                batch = self.batcher.poll(clock())
+                if batch:
+                    si = free.popleft()
+                    slot = self.slots[si]
+                    ids = np.concatenate([r.item_ids for r in batch])
+                    B = len(ids)
+                    nnz = self.pool.gather(ids, slot["off"], slot["idx"], slot["dense"])
+                    self.m.score_host_raw(slot["idx"].data_ptr(), slot["off"].data_ptr(), nnz, B,
+                                          slot["dense"].data_ptr(), slot["scores"].data_ptr(), h_c, h_e, h_d)
+                    slot["ev"].record(self.s_dense)
+                    inflight.append((batch, slot, si))
+                    sizes.append(B)
+        torch.cuda.synchronize()
+        return lat, np.array(sizes), scores

@@ -1,0 +1,76 @@
+"""Table-wise sharded scoring (BASELINE.json configs[2]).
+
+Tables are placed round-robin (table t on rank t mod N, A18).  Per batch of B_global examples:
+
+  1. every rank pools ITS tables for the GLOBAL batch straight into a destination-major send buffer
+     [dst][b_local][t_slot][d] (libcvr ``cvr_embed_shard``; slot = t div N, padded to ceil(T/N)) and
+     normalises the dense features of its own batch slice into its local x0;
+  2. one all-to-all exchanges the pooled rows (the only collective on the path; NCCL over NVLink
+     through ``torch.distributed`` on GPUs, gloo in the CPU tests of this host logic);
+  3. ``cvr_unpack_shard`` writes the received source-major chunks [src][b_local][t_slot][d] into the
+     canonical x0 columns of the local slice (V1 of SURVEY.md §8(e));
+  4. the dense stage runs data-parallel on the local slice of B_global / N examples.
+
+Pooled values are bit-identical to the unsharded path for every N (the exchange is a copy, P11).
+"""
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+import torch
+import torch.distributed as dist
+
+
+def local_tables(n_tables: int, world: int, rank: int):
+    return [t for t in range(n_tables) if t % world == rank]
+
+
+def slots_per_rank(n_tables: int, world: int) -> int:
+    return (n_tables + world - 1) // world
+
+
+def exchange(send: torch.Tensor, recv: torch.Tensor, group=None) -> None:
+    """All-to-all of equal chunks: chunk dst of ``send`` goes to rank dst, chunk src of ``recv`` comes
+    from rank src (both 1-D byte/element views of [N][chunk])."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_to_all_single(recv, send, group=group)
+    else:
+        recv.copy_(send)
+
+
+class ShardedScorer:
+    """One rank of the sharded scoring path."""
+
+    def __init__(self, cfg, world_size: int, rank: int, batch_global: int, max_nnz: int,
+                 device: Optional[torch.device] = None, group=None):
+        from ._cvr import CvrModel
+        if batch_global % world_size:
+            raise ValueError("batch_global must be a multiple of world_size (A18)")
+        self.cfg, self.N, self.rank, self.group = cfg, world_size, rank, group
+        self.B, self.Bl = batch_global, batch_global // world_size
+        self.model = CvrModel(cfg, max_batch=self.Bl, max_nnz=max_nnz, world_size=world_size, rank=rank,
+                              device=device)
+        self.device = self.model.device
+        sb, rb = self.model.shard_buffer_bytes(batch_global)
+        self.send = torch.empty(sb, dtype=torch.uint8, device=self.device)
+        self.recv = torch.empty(rb, dtype=torch.uint8, device=self.device)
+        self.x0 = self.model.new_x0(self.Bl)
+        self.tables = local_tables(cfg.n_tables, world_size, rank)
+
+    def load_tables(self, tables: Sequence[torch.Tensor]):
+        self.model.load_tables(tables, self.tables)
+
+    def load_weights(self, weights):
+        self.model.load_weights(weights)
+
+    def score(self, indices: torch.Tensor, offsets: torch.Tensor, dense_local: torch.Tensor,
+              scores: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """indices/offsets: this rank's tables over the global batch; dense_local: [B/N, F]."""
+        scores = torch.empty(self.Bl, dtype=torch.float32, device=self.device) if scores is None else scores
+        s = stream or torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(s):
+            self.model.embed_shard(indices, offsets, self.B, dense_local, self.send, self.x0, stream=s)
+            exchange(self.send, self.recv, self.group)
+            self.model.unpack_shard(self.recv, self.B, self.x0, stream=s)
+            self.model.dense(self.x0, self.Bl, scores, stream=s)
+        return scores

@@ -1,0 +1,63 @@
+"""Sharded-table path on one GPU: N ranks emulated in sequence (their kernels do not wait on each
+other), the all-to-all emulated by chunk copies.  Pooled x0 and scores must be bit-identical to the
+unsharded path (P11), and scores within 2e-3 of the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import cvr_synth as cs
+import oracle as O
+from helpers import TOL_BF16, make_model, to_dev
+
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+@pytest.fixture(scope="module")
+def c3small():
+    from paper_2605_29232_b200 import build
+    build.build()
+    cfg = cs.C3.with_(rows=(20000,) * 100)     # config-3 structure (100 fp16 tables x 128, W = 12864)
+    tabs = [s.materialize(device="cuda") for s in cs.table_specs(cfg)]
+    w = cs.make_weights(cfg)
+    ref_model, _, _ = make_model(cfg, max_batch=512, max_nnz=1 << 20, tables=tabs, weights=w)
+    return cfg, tabs, w, ref_model
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_matches_unsharded(c3small, world):
+    from paper_2605_29232_b200 import CvrModel
+    from paper_2605_29232_b200.sharded import local_tables
+    cfg, tabs, w, ref = c3small
+    B = 256
+    Bl = B // world
+    bt = cs.make_batch(cfg, 9, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0_ref = ref.embed(idx, off, B, dense)
+    s_ref = ref.dense(x0_ref, B)
+    ranks = []
+    for r in range(world):
+        m = CvrModel(cfg, max_batch=Bl, max_nnz=1 << 20, world_size=world, rank=r)
+        lt = local_tables(cfg.n_tables, world, r)
+        m.load_tables([tabs[t] for t in lt], lt)
+        m.load_weights({k: v.cuda() for k, v in w.items()})
+        lb = cs.make_batch(cfg, 9, batch=B, tables=lt)
+        sb, rb = m.shard_buffer_bytes(B)
+        send = torch.empty(sb, dtype=torch.uint8, device="cuda")
+        x0 = m.new_x0(Bl)
+        li, lo, _ = to_dev(lb)
+        m.embed_shard(li, lo, B, dense[r * Bl:(r + 1) * Bl].contiguous(), send, x0)
+        ranks.append((m, send, x0))
+    torch.cuda.synchronize()
+    for r, (m, send, x0) in enumerate(ranks):
+        assert m.status() == 0
+        chunk = send.numel() // world
+        recv = torch.cat([ranks[s][1][r * chunk:(r + 1) * chunk] for s in range(world)])   # all-to-all
+        m.unpack_shard(recv, B, x0)
+        s = m.dense(x0, Bl)
+        torch.cuda.synchronize()
+        assert torch.equal(x0, x0_ref[r * Bl:(r + 1) * Bl]), f"rank {r}: x0 differs"
+        assert torch.equal(s, s_ref[r * Bl:(r + 1) * Bl]), f"rank {r}: scores differ"
+    ref_scores = O.score_forward(cfg, cs.table_specs(cfg), w, cs.sub_batch(bt, np.arange(0, B, 8)))["scores"]
+    assert np.abs(s_ref[::8].double().cpu().numpy() - ref_scores).max() <= TOL_BF16
