@@ -22,9 +22,14 @@
 
 using namespace cvr;
 
-enum KernelId { K_EMBED = 0, K_GEMM_V, K_GEMM_U, K_GEMM_MLP, K_GEMM_HEAD, K_DENSE_F32, K_UNPACK, K_CROSS_FUSED, K_COUNT };
-static const char* kKernelNames[K_COUNT] = {"embed_bag_pool", "gemm_xV",      "gemm_tU_cross", "gemm_mlp_relu",
-                                            "gemm_mlp_head",  "dense_f32_dcn", "shard_unpack", "cross_fused"};
+enum KernelId {
+  K_EMBED = 0, K_GEMM_V, K_GEMM_U, K_GEMM_MLP, K_GEMM_HEAD, K_DENSE_F32, K_UNPACK, K_CROSS_FUSED,
+  K_ENS_QKV, K_MHA, K_ENS_OPROJ, K_ENS_FFN1, K_ENS_FFN2_LN, K_HEAD_FIN, K_COUNT
+};
+static const char* kKernelNames[K_COUNT] = {
+    "embed_bag_pool", "gemm_xV",  "gemm_tU_cross",  "gemm_mlp_relu", "gemm_mlp_head", "dense_f32_dcn",
+    "shard_unpack",   "cross_fused", "gemm_ens_qkv", "mha64",       "gemm_ens_oproj", "gemm_ens_ffn1",
+    "gemm_ens_ffn2_ln", "head_finalize"};
 
 namespace {
 
@@ -85,6 +90,16 @@ struct cvr_ctx {
   CUtensorMap st_xa, st_xb, st_t;                 // output (TMA store) maps, box {64, 32}
   std::vector<CUtensorMap> tm_v256;               // V_l with box {64, 256} (fused cross layer)
   bool fused_cross = false;                       // K5 (r == 256)
+  // ensemble (config 4) buffers and maps
+  struct Ens {
+    size_t off_S = 0, off_qkv = 0, off_O = 0, off_hf = 0;
+    CUtensorMap flat_x0[2], tok_x0[2], flat_xa, flat_xb, tok_xa, tok_xb, sttok_xa, sttok_xb;
+    CUtensorMap st_qkv, tm_O, st_hf, tm_hf;
+    std::vector<CUtensorMap> V, U, Wqkv, Wo, W1, W2;
+    CUtensorMap flat_user, tok_user;
+  } ens;
+  size_t off_hpart = 0;   // split-head partial dot products [max_batch, last/256]
+  int head_parts = 0;     // 0: head fused into the last MLP GEMM (last <= 256); else #256-wide parts
   unsigned long long* dbg = nullptr;              // CVR_DEBUG_TIMING: phase stamps of the last fused launch
   int dbg_ctas = 0;
   size_t off_part = 0;
@@ -178,6 +193,24 @@ void build_weight_slots(cvr_ctx* c) {
       add("dcn/" + std::to_string(l) + "/U", {c->W, c->r}, a);
       add("dcn/" + std::to_string(l) + "/b", {c->W}, a);
     }
+  } else if (c->backbone == CVR_ENSEMBLE) {
+    const int D = c->d;
+    for (int l = 0; l < c->n_cross; ++l) {
+      const std::string p = "ens/" + std::to_string(l) + "/";
+      add(p + "dcn/V", {c->r, c->W}, a);
+      add(p + "dcn/U", {c->W, c->r}, a);
+      add(p + "dcn/b", {c->W}, a);
+      add(p + "mha/Wqkv", {3 * D, D}, a);
+      add(p + "mha/bqkv", {3 * D}, a);
+      add(p + "mha/Wo", {D, D}, a);
+      add(p + "mha/bo", {D}, a);
+      add(p + "ffn/W1", {c->ffn, D}, a);
+      add(p + "ffn/b1", {c->ffn}, a);
+      add(p + "ffn/W2", {D, c->ffn}, a);
+      add(p + "ffn/b2", {D}, a);
+      add(p + "ln/gamma", {D}, a);
+      add(p + "ln/beta", {D}, a);
+    }
   }
   for (int i = 0; i < c->n_mlp; ++i) {
     add("mlp/" + std::to_string(i) + "/W", {c->mlp[i], prev}, a);
@@ -198,6 +231,7 @@ size_t packed_bytes(const cvr_ctx* c, const WSlot& s) {
     if (s.shape.size() == 1 && n.rfind("dcn/", 0) == 0) e = c->x0_ld;  // padded bias
     return (size_t)e * 4;                                              // fp32 copies
   }
+  if (c->backbone == CVR_ENSEMBLE) return (size_t)s.shape[0] * s.shape[1] * 2;  // W == x0_ld: no padding
   // bf16 GEMM operands, padded to x0_ld along W
   if (ends("/V")) return (size_t)c->r * c->x0_ld * 2;
   if (ends("/U")) return (size_t)c->x0_ld * c->r * 2;
@@ -236,7 +270,19 @@ int validate_desc(const cvr_model_desc* d, std::string& why) {
     for (int i = 0; i < d->n_mlp; ++i)
       if (d->mlp_dims[i] % 64) return bad("mlp_dims must be multiples of 64 on the bf16 path");
     const int last = d->mlp_dims[d->n_mlp - 1];
-    if (last != 64 && last != 128 && last != 256) return bad("last MLP width must be 64, 128 or 256 (fused head)");
+    if (!(last == 64 || last == 128 || last == 256 || last % 256 == 0))
+      return bad("last MLP width must be 64, 128, 256 (fused head) or a multiple of 256 (split head)");
+  } else if (d->backbone == CVR_ENSEMBLE) {
+    if (d->act_dtype != CVR_BF16) return bad("ENSEMBLE runs the bf16 tensor-core path: act_dtype must be CVR_BF16");
+    if (d->n_heads != 4 || d->dim != 256)
+      return bad("ensemble layer: 4 heads x 64 over tokens of dim 256 (BASELINE.json configs[3], A20)");
+    if (d->n_dense != 0) return bad("ensemble: the tokens are the pooled tables, no dense features (A20)");
+    if (d->cross_rank <= 0 || d->cross_rank % 128) return bad("ensemble cross_rank must be a multiple of 128");
+    if (d->ffn_dim <= 0 || d->ffn_dim % 128) return bad("ffn_dim must be a multiple of 128");
+    for (int i = 0; i + 1 < d->n_mlp; ++i)
+      if (d->mlp_dims[i] % 128) return bad("hidden MLP widths must be multiples of 128 on the ensemble path");
+    const int last = d->mlp_dims[d->n_mlp - 1];
+    if (!(last == 64 || last == 128 || last == 256 || last % 256 == 0)) return bad("last MLP width: 64/128/256 or k*256");
   } else {
     return CVR_E_UNSUPPORTED;
   }
@@ -332,6 +378,21 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
       c->off_part = carve(cur, cross_fused_partial_bytes(c->max_batch));
     }
     for (int i = 0; i + 1 < c->n_mlp; ++i) c->off_h.push_back(carve(cur, (size_t)B * c->mlp[i] * 2));
+  } else if (c->backbone == CVR_ENSEMBLE) {
+    const int64_t BT = B * c->T;  // tokens
+    c->off_xa = carve(cur, (size_t)B * c->x0_ld * 2);
+    c->off_xb = carve(cur, (size_t)B * c->x0_ld * 2);
+    c->off_t = carve(cur, (size_t)B * c->r * 2);
+    c->ens.off_S = carve(cur, (size_t)B * c->x0_ld * 4);
+    c->ens.off_qkv = carve(cur, (size_t)BT * 3 * c->d * 2);
+    c->ens.off_O = carve(cur, (size_t)BT * c->d * 2);
+    c->ens.off_hf = carve(cur, (size_t)BT * c->ffn * 2);
+    for (int i = 0; i + 1 < c->n_mlp; ++i) c->off_h.push_back(carve(cur, (size_t)B * c->mlp[i] * 2));
+  }
+  if (c->backbone != CVR_DCN_FULL) {
+    const int last = c->mlp[c->n_mlp - 1];
+    c->head_parts = (last == 64 || last == 128 || last == 256) ? 0 : last / 256;
+    if (c->head_parts) c->off_hpart = carve(cur, (size_t)B * c->head_parts * 4);
   }
   const int64_t Bin = c->world > 1 ? B * c->world : B;  // sharded: indices cover the global batch
   const int T_l = (int)c->local_tables.size();
@@ -429,6 +490,35 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     }
     if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
   }
+  if (c->backbone == CVR_ENSEMBLE) {
+    const char* er = nullptr;
+    const int64_t B = c->max_batch, BT = B * c->T, D = c->d, W = c->x0_ld;
+    auto& E = c->ens;
+    bool ok = true;
+    for (int i = 0; i < 2; ++i) {
+      ok &= encode_tmap_bf16(&E.flat_x0[i], c->ws + c->off_x0[i], B, W, W, 128, &er) == 0;
+      ok &= encode_tmap_bf16(&E.tok_x0[i], c->ws + c->off_x0[i], BT, D, D, 128, &er) == 0;
+    }
+    ok &= encode_tmap_bf16(&E.flat_xa, c->ws + c->off_xa, B, W, W, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&E.flat_xb, c->ws + c->off_xb, B, W, W, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&E.tok_xa, c->ws + c->off_xa, BT, D, D, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&E.tok_xb, c->ws + c->off_xb, BT, D, D, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&E.sttok_xa, c->ws + c->off_xa, BT, D, D, 32, &er) == 0;
+    ok &= encode_tmap_bf16(&E.sttok_xb, c->ws + c->off_xb, BT, D, D, 32, &er) == 0;
+    ok &= encode_tmap_bf16(&c->tm_t, c->ws + c->off_t, B, c->r, c->r, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&c->st_t, c->ws + c->off_t, B, c->r, c->r, 32, &er) == 0;
+    ok &= encode_tmap_bf16(&E.st_qkv, c->ws + E.off_qkv, BT, 3 * D, 3 * D, 32, &er) == 0;
+    ok &= encode_tmap_bf16(&E.tm_O, c->ws + E.off_O, BT, D, D, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&E.st_hf, c->ws + E.off_hf, BT, c->ffn, c->ffn, 32, &er) == 0;
+    ok &= encode_tmap_bf16(&E.tm_hf, c->ws + E.off_hf, BT, c->ffn, c->ffn, 128, &er) == 0;
+    c->tm_h.resize(c->off_h.size());
+    c->st_h.resize(c->off_h.size());
+    for (size_t i = 0; i < c->off_h.size(); ++i) {
+      ok &= encode_tmap_bf16(&c->tm_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], 128, &er) == 0;
+      ok &= encode_tmap_bf16(&c->st_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], 32, &er) == 0;
+    }
+    if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
+  }
   return CVR_OK;
 }
 
@@ -482,11 +572,52 @@ int encode_plan(cvr_ctx* c) {
   int K = (int)c->x0_ld;
   for (int i = 0; i < c->n_mlp; ++i) {
     const bool last = i + 1 == c->n_mlp;
-    ok &= addp("mlp/" + std::to_string(i) + "/W", c->mlp[i], K, last ? c->mlp[i] : pick_bn(c->mlp[i]),
-               last ? EPI_HEAD : EPI_BIAS_RELU);
+    const int bn = last ? (c->head_parts ? 256 : c->mlp[i]) : pick_bn(c->mlp[i]);
+    const Epi ep = last ? (c->head_parts ? EPI_HEAD_PARTIAL : EPI_HEAD) : EPI_BIAS_RELU;
+    ok &= addp("mlp/" + std::to_string(i) + "/W", c->mlp[i], K, bn, ep);
     K = c->mlp[i];
   }
   if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
+  return CVR_OK;
+}
+
+int encode_plan_ensemble(cvr_ctx* c) {
+  const char* er = nullptr;
+  auto& E = c->ens;
+  const int D = c->d, W = (int)c->x0_ld, r = c->r, F = c->ffn;
+  E.V.assign(c->n_cross, {});
+  E.U.assign(c->n_cross, {});
+  E.Wqkv.assign(c->n_cross, {});
+  E.Wo.assign(c->n_cross, {});
+  E.W1.assign(c->n_cross, {});
+  E.W2.assign(c->n_cross, {});
+  bool ok = true;
+  for (int l = 0; l < c->n_cross; ++l) {
+    const std::string p = "ens/" + std::to_string(l) + "/";
+    ok &= encode_tmap_bf16(&E.V[l], c->wptr(p + "dcn/V"), r, W, W, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&E.U[l], c->wptr(p + "dcn/U"), W, r, r, 64, &er) == 0;
+    ok &= encode_tmap_bf16(&E.Wqkv[l], c->wptr(p + "mha/Wqkv"), 3 * D, D, D, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&E.Wo[l], c->wptr(p + "mha/Wo"), D, D, D, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&E.W1[l], c->wptr(p + "ffn/W1"), F, D, D, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&E.W2[l], c->wptr(p + "ffn/W2"), D, F, F, 256, &er) == 0;
+  }
+  if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
+  // head MLP: same plan as the low-rank path (GemmPlan per mlp layer)
+  c->plan.clear();
+  int K = W;
+  for (int i = 0; i < c->n_mlp; ++i) {
+    const bool last = i + 1 == c->n_mlp;
+    GemmPlan g;
+    g.N = c->mlp[i];
+    g.K = K;
+    g.BN = last ? (c->head_parts ? 256 : c->mlp[i]) : 128;
+    g.epi = last ? (c->head_parts ? EPI_HEAD_PARTIAL : EPI_HEAD) : EPI_BIAS_RELU;
+    g.wname = nullptr;
+    if (encode_tmap_bf16(&g.tmB, c->wptr("mlp/" + std::to_string(i) + "/W"), g.N, K, K, g.BN, &er) != 0)
+      return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
+    c->plan.push_back(g);
+    K = c->mlp[i];
+  }
   return CVR_OK;
 }
 
@@ -578,6 +709,9 @@ int cvr_load_weights(cvr_ctx* c, int n, const char* const* names, const void* co
   if (c->backbone == CVR_DCN_LOWRANK) {
     int st = encode_plan(c);
     if (st != CVR_OK) return st;
+  } else if (c->backbone == CVR_ENSEMBLE) {
+    int st = encode_plan_ensemble(c);
+    if (st != CVR_OK) return st;
   }
   c->weights_loaded = true;
   return CVR_OK;
@@ -634,7 +768,137 @@ int do_embed(cvr_ctx* c, const int32_t* idx, const int32_t* off, int64_t nnz, in
   return CVR_OK;
 }
 
-int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, int B, float* scores, cudaStream_t s) {
+GemmArgs gemm_args(cvr_ctx* c, const GemmPlan& g, const CUtensorMap* A, int M) {
+  GemmArgs a{};
+  a.tmA = A;
+  a.tmB = &g.tmB;
+  a.M = M;
+  a.N = g.N;
+  a.K = g.K;
+  a.BN = g.BN;
+  a.epi = g.epi;
+  a.num_sms = c->num_sms;
+  a.pdl = c->pdl;
+  return a;
+}
+
+cudaError_t run_gemm(cvr_ctx* c, const GemmArgs& a, int kid, cudaStream_t s) {
+  c->pbeg(s);
+  cudaError_t r = launch_gemm_bf16(a, s);
+  c->pend(kid, s);
+  return r;
+}
+
+// S6 + S7: hidden MLP layers (bias + ReLU) then the head: fused into the last GEMM's epilogue when
+// the last width fits one N tile (<= 256), else 256-wide partial dot products + a fixed-order finaliser.
+int run_mlp_head(cvr_ctx* c, const CUtensorMap* tm_in, size_t pi, int B, float* scores, cudaStream_t s) {
+  cudaError_t e;
+  for (int i = 0; i < c->n_mlp; ++i) {
+    const GemmPlan& g = c->plan[pi++];
+    GemmArgs a = gemm_args(c, g, tm_in, B);
+    a.bias = c->wptr<float>("mlp/" + std::to_string(i) + "/b");
+    int kid = K_GEMM_MLP;
+    if (g.epi == EPI_HEAD) {
+      a.head_w = c->wptr<float>("head/w");
+      a.head_b = c->head_b;
+      a.scores = scores;
+      kid = K_GEMM_HEAD;
+    } else if (g.epi == EPI_HEAD_PARTIAL) {
+      a.head_w = c->wptr<float>("head/w");
+      a.partial = c->at<float>(c->off_hpart);
+      kid = K_GEMM_HEAD;
+    } else {
+      a.tmOut = &c->st_h[i];
+    }
+    if ((e = run_gemm(c, a, kid, s)) != cudaSuccess) return c->cuda_fail(e, "gemm MLP launch");
+    if (g.epi == EPI_HEAD_PARTIAL) {
+      c->pbeg(s);
+      e = launch_head_finalize(c->at<float>(c->off_hpart), c->head_parts, c->head_b, scores, B, s);
+      c->pend(K_HEAD_FIN, s);
+      if (e != cudaSuccess) return c->cuda_fail(e, "head finalize launch");
+    }
+    if (g.epi == EPI_BIAS_RELU) tm_in = &c->tm_h[i];
+  }
+  return CVR_OK;
+}
+
+// S5' (config 4, A20/A26): per layer Y = LN_token(DCN(X) + MHA(X) + FFN(X)); the branch sum is kept in
+// fp32 (S) and the LN runs in the FFN2 epilogue.
+int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, const CUtensorMap* tok_x0, int B,
+                      float* scores, cudaStream_t s) {
+  auto& E = c->ens;
+  cudaError_t e;
+  const int D = c->d, W = (int)c->x0_ld, r = c->r, T = c->T, BT = B * T;
+  float* S = c->at<float>(E.off_S);
+  const CUtensorMap* flat_xl = flat_x0;
+  const CUtensorMap* tok_xl = tok_x0;
+  GemmPlan gp;  // scratch plan for per-call GemmArgs
+  auto ga = [&](const CUtensorMap* A, const CUtensorMap* Bm, int M, int N, int K, int BN, Epi epi) {
+    GemmArgs a{};
+    a.tmA = A;
+    a.tmB = Bm;
+    a.M = M;
+    a.N = N;
+    a.K = K;
+    a.BN = BN;
+    a.epi = epi;
+    a.num_sms = c->num_sms;
+    a.pdl = c->pdl;
+    return a;
+  };
+  (void)gp;
+  for (int l = 0; l < c->n_cross; ++l) {
+    const std::string p = "ens/" + std::to_string(l) + "/";
+    const bool even = l % 2 == 0;
+    // DCN branch: t = X V^T ; S = x0 * (t U^T + b) + X   (fp32, A26)
+    GemmArgs a1 = ga(flat_xl, &E.V[l], B, r, W, 128, EPI_STORE);
+    a1.tmOut = &c->st_t;
+    if ((e = run_gemm(c, a1, K_GEMM_V, s)) != cudaSuccess) return c->cuda_fail(e, "ens V");
+    GemmArgs a2 = ga(&c->tm_t, &E.U[l], B, W, r, 64, EPI_CROSS_F32);
+    a2.tmX0 = flat_x0;
+    a2.tmXl = flat_xl;
+    a2.bias = c->wptr<float>(p + "dcn/b");
+    a2.out_f32 = S;
+    a2.ld_f32 = W;
+    if ((e = run_gemm(c, a2, K_GEMM_U, s)) != cudaSuccess) return c->cuda_fail(e, "ens U");
+    // MHA branch: qkv = X Wqkv^T + b ; O = attention ; S += O Wo^T + bo
+    GemmArgs a3 = ga(tok_xl, &E.Wqkv[l], BT, 3 * D, D, 128, EPI_BIAS);
+    a3.tmOut = &E.st_qkv;
+    a3.bias = c->wptr<float>(p + "mha/bqkv");
+    if ((e = run_gemm(c, a3, K_ENS_QKV, s)) != cudaSuccess) return c->cuda_fail(e, "ens qkv");
+    c->pbeg(s);
+    e = launch_mha64(c->at<__nv_bfloat16>(E.off_qkv), c->at<__nv_bfloat16>(E.off_O), B, c->n_heads, s);
+    c->pend(K_MHA, s);
+    if (e != cudaSuccess) return c->cuda_fail(e, "mha64");
+    GemmArgs a4 = ga(&E.tm_O, &E.Wo[l], BT, D, D, 128, EPI_BIAS_ADD_F32);
+    a4.bias = c->wptr<float>(p + "mha/bo");
+    a4.in_f32 = S;
+    a4.ld_in = D;
+    a4.out_f32 = S;
+    a4.ld_f32 = D;
+    if ((e = run_gemm(c, a4, K_ENS_OPROJ, s)) != cudaSuccess) return c->cuda_fail(e, "ens oproj");
+    // FFN branch + branch sum + LN: X' = LN(W2 ReLU(W1 X + b1) + b2 + S) * gamma + beta
+    GemmArgs a5 = ga(tok_xl, &E.W1[l], BT, c->ffn, D, 128, EPI_BIAS_RELU);
+    a5.tmOut = &E.st_hf;
+    a5.bias = c->wptr<float>(p + "ffn/b1");
+    if ((e = run_gemm(c, a5, K_ENS_FFN1, s)) != cudaSuccess) return c->cuda_fail(e, "ens ffn1");
+    GemmArgs a6 = ga(&E.tm_hf, &E.W2[l], BT, D, c->ffn, 256, EPI_SUM_LN);
+    a6.tmOut = even ? &E.sttok_xa : &E.sttok_xb;
+    a6.bias = c->wptr<float>(p + "ffn/b2");
+    a6.in_f32 = S;
+    a6.ld_in = D;
+    a6.gamma = c->wptr<float>(p + "ln/gamma");
+    a6.beta = c->wptr<float>(p + "ln/beta");
+    if ((e = run_gemm(c, a6, K_ENS_FFN2_LN, s)) != cudaSuccess) return c->cuda_fail(e, "ens ffn2+ln");
+    flat_xl = even ? &E.flat_xa : &E.flat_xb;
+    tok_xl = even ? &E.tok_xa : &E.tok_xb;
+  }
+  (void)x0;
+  return run_mlp_head(c, flat_xl, 0, B, scores, s);
+}
+
+int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, const CUtensorMap* tm_x0_tok, int B, float* scores,
+             cudaStream_t s) {
   cudaError_t e = cudaSuccess;
   if (c->backbone == CVR_DCN_FULL) {
     DenseF32Args a{};
@@ -663,35 +927,12 @@ int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, int B, float*
     if (e != cudaSuccess) return c->cuda_fail(e, "dense_f32 launch");
     return CVR_OK;
   }
+  const float* hb = nullptr;  // (unused; keeps the two backbones' code paths parallel)
+  (void)hb;
+  if (c->backbone == CVR_ENSEMBLE) return do_dense_ensemble(c, x0, tm_x0, tm_x0_tok, B, scores, s);
   // ---- bf16 low-rank DCN-v2 on tcgen05
   const CUtensorMap* tm_xl = tm_x0;
   size_t pi = 0;
-  auto gemm = [&](const GemmPlan& g, const CUtensorMap* A, const CUtensorMap* out, const CUtensorMap* x0m,
-                  const CUtensorMap* xlm, const float* bias, int kid) -> cudaError_t {
-    GemmArgs a{};
-    a.tmA = A;
-    a.tmB = &g.tmB;
-    a.tmOut = out;
-    a.tmX0 = x0m;
-    a.tmXl = xlm;
-    a.bias = bias;
-    a.M = B;
-    a.N = g.N;
-    a.K = g.K;
-    a.BN = g.BN;
-    a.epi = g.epi;
-    a.num_sms = c->num_sms;
-    a.pdl = c->pdl;
-    if (g.epi == EPI_HEAD) {
-      a.head_w = c->wptr<float>("head/w");
-      a.head_b = c->head_b;
-      a.scores = scores;
-    }
-    c->pbeg(s);
-    cudaError_t r = launch_gemm_bf16(a, s);
-    c->pend(kid, s);
-    return r;
-  };
   for (int l = 0; l < c->n_cross; ++l) {
     const GemmPlan& gv = c->plan[pi++];
     const GemmPlan& gu = c->plan[pi++];
@@ -720,22 +961,18 @@ int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, int B, float*
       tm_xl = even ? &c->tm_xa : &c->tm_xb;
       continue;
     }
-    e = gemm(gv, tm_xl, &c->st_t, nullptr, nullptr, nullptr, K_GEMM_V);
-    if (e != cudaSuccess) return c->cuda_fail(e, "gemm V launch");
-    e = gemm(gu, &c->tm_t, even ? &c->st_xa : &c->st_xb, tm_x0, tm_xl,
-             c->wptr<float>("dcn/" + std::to_string(l) + "/b"), K_GEMM_U);
-    if (e != cudaSuccess) return c->cuda_fail(e, "gemm U launch");
+    GemmArgs av = gemm_args(c, gv, tm_xl, B);
+    av.tmOut = &c->st_t;
+    if ((e = run_gemm(c, av, K_GEMM_V, s)) != cudaSuccess) return c->cuda_fail(e, "gemm V launch");
+    GemmArgs au = gemm_args(c, gu, &c->tm_t, B);
+    au.tmOut = even ? &c->st_xa : &c->st_xb;
+    au.tmX0 = tm_x0;
+    au.tmXl = tm_xl;
+    au.bias = c->wptr<float>("dcn/" + std::to_string(l) + "/b");
+    if ((e = run_gemm(c, au, K_GEMM_U, s)) != cudaSuccess) return c->cuda_fail(e, "gemm U launch");
     tm_xl = even ? &c->tm_xa : &c->tm_xb;
   }
-  for (int i = 0; i < c->n_mlp; ++i) {
-    const GemmPlan& g = c->plan[pi++];
-    const bool head = g.epi == EPI_HEAD;
-    e = gemm(g, tm_xl, head ? nullptr : &c->st_h[i], nullptr, nullptr, c->wptr<float>("mlp/" + std::to_string(i) + "/b"),
-             head ? K_GEMM_HEAD : K_GEMM_MLP);
-    if (e != cudaSuccess) return c->cuda_fail(e, "gemm MLP launch");
-    if (!head) tm_xl = &c->tm_h[i];
-  }
-  return CVR_OK;
+  return run_mlp_head(c, tm_xl, pi, B, scores, s);
 }
 
 }  // namespace
@@ -833,22 +1070,31 @@ int cvr_dense(cvr_ctx* c, const void* d_x0, int batch, float* d_scores, cvr_stre
   if (!d_x0 || !d_scores) return c->fail(CVR_E_ARG, "null pointer");
   if (batch == 0) return CVR_OK;
   const CUtensorMap* tm = nullptr;
-  if (c->backbone == CVR_DCN_LOWRANK) {
-    if (d_x0 == c->ws + c->off_x0[0]) tm = &c->tm_x0slot[0];
-    else if (d_x0 == c->ws + c->off_x0[1]) tm = &c->tm_x0slot[1];
-    else {
+  const CUtensorMap* tmt = nullptr;
+  if (c->backbone != CVR_DCN_FULL) {
+    const bool ens = c->backbone == CVR_ENSEMBLE;
+    if (d_x0 == c->ws + c->off_x0[0]) {
+      tm = ens ? &c->ens.flat_x0[0] : &c->tm_x0slot[0];
+      tmt = &c->ens.tok_x0[0];
+    } else if (d_x0 == c->ws + c->off_x0[1]) {
+      tm = ens ? &c->ens.flat_x0[1] : &c->tm_x0slot[1];
+      tmt = &c->ens.tok_x0[1];
+    } else {
       if (d_x0 != c->last_x0 || batch != c->last_x0_rows) {
         const char* er = nullptr;
-        if (encode_tmap_bf16(&c->tm_x0user, d_x0, batch, c->x0_ld, c->x0_ld, 128, &er) != 0)
+        if (encode_tmap_bf16(&c->tm_x0user, d_x0, batch, c->x0_ld, c->x0_ld, 128, &er) != 0 ||
+            (ens && encode_tmap_bf16(&c->ens.tok_user, d_x0, (int64_t)batch * c->T, c->d, c->d, 128, &er) != 0))
           return c->fail(CVR_E_CUDA, "tensor map encode: %s", er);
         c->last_x0 = d_x0;
         c->last_x0_rows = batch;
       }
       tm = &c->tm_x0user;
+      tmt = &c->ens.tok_user;
     }
   }
   const uint64_t kd[7] = {4, u64(d_x0), (uint64_t)batch, u64(d_scores), 0, 0, 0};
-  return run_stage(c, kd, (cudaStream_t)stream, [&](cudaStream_t s) { return do_dense(c, d_x0, tm, batch, d_scores, s); });
+  return run_stage(c, kd, (cudaStream_t)stream,
+                   [&](cudaStream_t s) { return do_dense(c, d_x0, tm, tmt, batch, d_scores, s); });
 }
 
 int cvr_score(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, int64_t nnz, int batch,
@@ -872,9 +1118,11 @@ int cvr_score(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, in
   if ((e = cudaEventRecord(c->ev_embed[slot], se)) != cudaSuccess) return c->cuda_fail(e, "record embed");
   if ((e = cudaStreamWaitEvent(sd, c->ev_embed[slot], 0)) != cudaSuccess) return c->cuda_fail(e, "wait embed");
   if (batch > 0) {
-    const CUtensorMap* tm = c->backbone == CVR_DCN_LOWRANK ? &c->tm_x0slot[slot] : nullptr;
+    const bool ens = c->backbone == CVR_ENSEMBLE;
+    const CUtensorMap* tm = c->backbone == CVR_DCN_LOWRANK ? &c->tm_x0slot[slot] : ens ? &c->ens.flat_x0[slot] : nullptr;
+    const CUtensorMap* tmt = ens ? &c->ens.tok_x0[slot] : nullptr;
     const uint64_t kd[7] = {2, u64(x0), (uint64_t)batch, u64(d_scores), 0, 0, 0};
-    st = run_stage(c, kd, sd, [&](cudaStream_t s) { return do_dense(c, x0, tm, batch, d_scores, s); });
+    st = run_stage(c, kd, sd, [&](cudaStream_t s) { return do_dense(c, x0, tm, tmt, batch, d_scores, s); });
     if (st) return st;
   }
   if ((e = cudaEventRecord(c->ev_dense[slot], sd)) != cudaSuccess) return c->cuda_fail(e, "record dense");

@@ -66,7 +66,17 @@ struct DenseF32Args {
 cudaError_t launch_dense_f32(const DenseF32Args& a, cudaStream_t s);
 
 // ---- K4: tcgen05 bf16 GEMM with fused epilogues --------------------------------------------------
-enum Epi { EPI_STORE = 0, EPI_BIAS_RELU = 1, EPI_CROSS = 2, EPI_HEAD = 3 };
+enum Epi {
+  EPI_STORE = 0,         // bf16 C
+  EPI_BIAS_RELU = 1,     // bf16 ReLU(C + b)
+  EPI_CROSS = 2,         // bf16 x0 * (C + b) + x_l
+  EPI_HEAD = 3,          // fp32 sigmoid(ReLU(C + b) . m + c)            (BN == N)
+  EPI_BIAS = 4,          // bf16 C + b
+  EPI_CROSS_F32 = 5,     // fp32 x0 * (C + b) + x_l                      (ensemble DCN branch)
+  EPI_BIAS_ADD_F32 = 6,  // fp32 C + b + in_f32                          (ensemble MHA out-proj)
+  EPI_SUM_LN = 7,        // bf16 LN_row(C + b + in_f32) * gamma + beta   (ensemble FFN2 + LN, BN == N)
+  EPI_HEAD_PARTIAL = 8   // fp32 partial[m][tile] = ReLU(C + b) . m over the tile's columns
+};
 
 struct GemmArgs {
   const CUtensorMap* tmA;    // A [M, K] bf16, box {64, 128}
@@ -78,6 +88,13 @@ struct GemmArgs {
   const float* head_w;       // EPI_HEAD fp32 [N]
   float head_b;
   float* scores;             // EPI_HEAD fp32 [M]
+  float* out_f32;            // EPI_CROSS_F32 / EPI_BIAS_ADD_F32: fp32 [M, ld_f32]
+  int64_t ld_f32;
+  const float* in_f32;       // EPI_BIAS_ADD_F32 / EPI_SUM_LN: fp32 [M, ld_in] (may alias out_f32)
+  int64_t ld_in;
+  const float* gamma;        // EPI_SUM_LN [N]
+  const float* beta;         // EPI_SUM_LN [N]
+  float* partial;            // EPI_HEAD_PARTIAL [M, N / BN]
   int M, N, K, BN;
   Epi epi;
   int num_sms;
@@ -87,6 +104,12 @@ struct GemmArgs {
 // C[M, N] = epi(A[M, K] . B[N, K]^T).  K % 64 == 0, N % BN == 0, BN in {64, 128, 256};
 // EPI_HEAD needs BN == N.  Persistent: grid = min(tiles, num_sms).
 cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s);
+
+// ---- K7: multi-head self-attention over the 64 tokens of each example (config 4) ------------------
+// qkv [B*S, 3*D] bf16 (Q | K | V, head h at columns h*64 of each), out [B*S, D] bf16; S = 64, dh = 64.
+cudaError_t launch_mha64(const __nv_bfloat16* qkv, __nv_bfloat16* out, int B, int n_heads, cudaStream_t s);
+// scores[m] = sigmoid(sum_j partial[m][j] + c), j in fixed order (EPI_HEAD_PARTIAL finaliser)
+cudaError_t launch_head_finalize(const float* partial, int n_parts, float c, float* scores, int M, cudaStream_t s);
 
 // ---- K5: fused low-rank cross layer (cluster of 4 CTAs per 128-row block, r = 256) ----------------
 struct CrossFusedArgs {

@@ -35,6 +35,14 @@ constexpr int BK = 64;
 constexpr int kThreads = 192;
 constexpr int kSmemBudget = 225 * 1024;
 
+template <int EPI>
+struct EpiTraits {
+  static constexpr bool kSmemOut = EPI == EPI_STORE || EPI == EPI_BIAS_RELU || EPI == EPI_CROSS || EPI == EPI_BIAS ||
+                                   EPI == EPI_SUM_LN;
+  static constexpr bool kEin = EPI == EPI_CROSS || EPI == EPI_CROSS_F32;   // x0 / x_l tiles by TMA
+  static constexpr bool kBias = EPI != EPI_STORE;
+};
+
 template <int BN, int EPI>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;       // 16 KB
@@ -42,9 +50,10 @@ struct Cfg {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int SUB = BM * 64 * 2;           // one 128 x 64 bf16 sub-tile (16 KB)
   static constexpr int NSUB = BN / 64;
-  static constexpr int OUT_BYTES = EPI == EPI_HEAD ? 0 : NSUB * SUB;              // per accumulator
-  static constexpr int EIN_BYTES = EPI == EPI_CROSS ? 2 * NSUB * SUB : 0;          // x0 + x_l tiles
-  static constexpr int EPI_BYTES = 2 * (OUT_BYTES + EIN_BYTES);                    // double-buffered
+  static constexpr int OUT_BUFS = BN == 256 ? 1 : 2;
+  static constexpr int OUT_BYTES = EpiTraits<EPI>::kSmemOut ? NSUB * SUB : 0;     // per buffer
+  static constexpr int EIN_BYTES = EpiTraits<EPI>::kEin ? 2 * NSUB * SUB : 0;     // x0 + x_l tiles, per acc
+  static constexpr int EPI_BYTES = OUT_BUFS * OUT_BYTES + 2 * EIN_BYTES;
   static constexpr int BAR_BYTES = 256;
   static constexpr int STAGES_FIT = (kSmemBudget - 1024 - BAR_BYTES - EPI_BYTES) / STAGE;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
@@ -71,21 +80,80 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
 __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
   asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
+__device__ __forceinline__ void ld32_tmem(uint32_t taddr, float (&v)[32]) {
+  uint32_t v0[16], v1[16];
+  ptx::tmem_ld_32x32b_x16(taddr, v0);
+  ptx::tmem_ld_32x32b_x16(taddr + 16, v1);
+  ptx::tmem_wait_ld();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    v[j] = __uint_as_float(v0[j]);
+    v[16 + j] = __uint_as_float(v1[j]);
+  }
+}
+__device__ __forceinline__ void st32_tmem(uint32_t taddr, const float (&v)[32]) {
+  uint32_t v0[16], v1[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    v0[j] = __float_as_uint(v[j]);
+    v1[j] = __float_as_uint(v[16 + j]);
+  }
+  ptx::tmem_st_32x32b_x16(taddr, v0);
+  ptx::tmem_st_32x32b_x16(taddr + 16, v1);
+}
+__device__ __forceinline__ void ld32_f32(const float* p, float (&v)[32]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 f = *reinterpret_cast<const float4*>(p + 4 * j);
+    v[4 * j] = f.x;
+    v[4 * j + 1] = f.y;
+    v[4 * j + 2] = f.z;
+    v[4 * j + 3] = f.w;
+  }
+}
+__device__ __forceinline__ void st32_f32(float* p, const float (&v)[32]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    *reinterpret_cast<float4*>(p + 4 * j) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+}
+// 32 columns (4 swizzled 16-byte chunks) of row r into / out of a bf16 staging sub-tile
+__device__ __forceinline__ void sts32_bf16(uint32_t sub_base, int r, int ch0, const float (&v)[32]) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    uint4 o;
+    o.x = ptx::pack_bf16(v[8 * u], v[8 * u + 1]);
+    o.y = ptx::pack_bf16(v[8 * u + 2], v[8 * u + 3]);
+    o.z = ptx::pack_bf16(v[8 * u + 4], v[8 * u + 5]);
+    o.w = ptx::pack_bf16(v[8 * u + 6], v[8 * u + 7]);
+    sts128(swz(sub_base, r, ch0 + u), o);
+  }
+}
+__device__ __forceinline__ void lds32_bf16(uint32_t sub_base, int r, int ch0, float (&v)[32]) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint4 x = lds128(swz(sub_base, r, ch0 + u));
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      v[8 * u + 2 * j] = ptx::bf16_lo(w[j]);
+      v[8 * u + 2 * j + 1] = ptx::bf16_hi(w[j]);
+    }
+  }
+}
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmX0,
-                     const __grid_constant__ CUtensorMap tmXl, const float* __restrict__ bias,
-                     const float* __restrict__ head_w, float head_b, float* __restrict__ scores, int M, int N,
-                     int K) {
+                     const __grid_constant__ CUtensorMap tmXl, const GemmArgs g) {
   using C = Cfg<BN, EPI>;
+  using T = EpiTraits<EPI>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = sA + C::STAGES * C::A_BYTES;
-  uint8_t* sOut = sB + C::STAGES * C::B_BYTES;     // [2][NSUB][SUB]
-  uint8_t* sEin = sOut + 2 * C::OUT_BYTES;         // [2][x0 NSUB subs | x_l NSUB subs]
+  uint8_t* sOut = sB + C::STAGES * C::B_BYTES;         // [OUT_BUFS][NSUB][SUB]
+  uint8_t* sEin = sOut + C::OUT_BUFS * C::OUT_BYTES;   // [2][x0 NSUB subs | x_l NSUB subs]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sEin + 2 * C::EIN_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = full + C::STAGES;
@@ -96,6 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(eempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int M = g.M, N = g.N, K = g.K;
   const int n_tiles_n = N / BN;
   const int n_tiles = ((M + BM - 1) / BM) * n_tiles_n;
   const int nk = K / BK;
@@ -116,8 +185,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
-    if (EPI != EPI_HEAD) ptx::prefetch_tmap(&tmOut);
-    if (EPI == EPI_CROSS) {
+    if (T::kSmemOut) ptx::prefetch_tmap(&tmOut);
+    if (T::kEin) {
       ptx::prefetch_tmap(&tmX0);
       ptx::prefetch_tmap(&tmXl);
     }
@@ -131,11 +200,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ================= TMA producer
-      int g = 0;      // global k-block counter (ring position)
+      int gk = 0;     // global k-block counter (ring position)
       int it = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
         const int m0 = (tile / n_tiles_n) * BM, n0 = (tile % n_tiles_n) * BN;
-        if constexpr (EPI == EPI_CROSS) {
+        if constexpr (T::kEin) {
           const int a = it & 1;
           if (it >= 2) ptx::mbar_wait(&eempty[a], ((it >> 1) - 1) & 1);
           ptx::mbar_arrive_expect_tx(&efull[a], C::EIN_BYTES);
@@ -146,9 +215,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tma_load_2d(base + (C::NSUB + j) * C::SUB, &tmXl, &efull[a], n0 + j * 64, m0);
           }
         }
-        for (int kb = 0; kb < nk; ++kb, ++g) {
-          const int s = g % C::STAGES;
-          if (g >= C::STAGES) ptx::mbar_wait(&empty[s], ((g / C::STAGES) - 1) & 1);
+        for (int kb = 0; kb < nk; ++kb, ++gk) {
+          const int s = gk % C::STAGES;
+          if (gk >= C::STAGES) ptx::mbar_wait(&empty[s], ((gk / C::STAGES) - 1) & 1);
           ptx::mbar_arrive_expect_tx(&full[s], C::STAGE);
           ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
           ptx::tma_load_2d(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);
@@ -158,15 +227,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ================= MMA issuer
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN);
-      int g = 0, it = 0;
+      int gk = 0, it = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
         const int a = it & 1;
         if (it >= 2) ptx::mbar_wait(&tempty[a], ((it >> 1) - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t acc = tmem + a * BN;
-        for (int kb = 0; kb < nk; ++kb, ++g) {
-          const int s = g % C::STAGES;
-          ptx::mbar_wait(&full[s], (g / C::STAGES) & 1);
+        for (int kb = 0; kb < nk; ++kb, ++gk) {
+          const int s = gk % C::STAGES;
+          ptx::mbar_wait(&full[s], (gk / C::STAGES) & 1);
           ptx::tc_fence_after();
           const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
           const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
@@ -183,61 +252,98 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = q * 32 + lane;  // row within the tile
     int it = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
-      const int m0 = (tile / n_tiles_n) * BM, n0 = (tile % n_tiles_n) * BN;
+      const int m0 = (tile / n_tiles_n) * BM, tn = tile % n_tiles_n, n0 = tn * BN;
+      const int m = m0 + r;
+      const bool live = m < M;
       const int a = it & 1;
       ptx::mbar_wait(&tfull[a], (it >> 1) & 1);
       ptx::tc_fence_after();
       const uint32_t trow = tmem + a * BN + ((uint32_t)(q * 32) << 16);
-      const uint32_t out_base = ptx::smem_u32(sOut + a * C::OUT_BYTES);
+      const uint32_t out_base = ptx::smem_u32(sOut + (C::OUT_BUFS == 2 ? a : 0) * C::OUT_BYTES);
       const uint32_t ein_base = ptx::smem_u32(sEin + a * C::EIN_BYTES);
-      if constexpr (EPI == EPI_CROSS) ptx::mbar_wait(&efull[a], (it >> 1) & 1);
-      if constexpr (EPI != EPI_HEAD) {
-        // the TMA store issued from this buffer two tiles ago must have finished reading it
-        if (lane == 0) ptx::bulk_wait_read<1>();
+      if constexpr (T::kEin) ptx::mbar_wait(&efull[a], (it >> 1) & 1);
+      if constexpr (T::kSmemOut) {
+        // the TMA store that last read this staging buffer must have finished reading it
+        if (lane == 0) {
+          if constexpr (C::OUT_BUFS == 2) ptx::bulk_wait_read<1>();
+          else ptx::bulk_wait_read<0>();
+        }
         __syncwarp();
       }
       float z = 0.f;
+      if constexpr (EPI == EPI_SUM_LN) {
+        // pass 1: y = acc + b + in, written back into TMEM; row sum
+        float sum = 0.f;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t v0[16], v1[16];
-        ptx::tmem_ld_32x32b_x16(trow + c, v0);
-        ptx::tmem_ld_32x32b_x16(trow + c + 16, v1);
-        ptx::tmem_wait_ld();
-        float v[32];
+        for (int c = 0; c < BN; c += 32) {
+          float v[32], x[32];
+          ld32_tmem(trow + c, v);
+          if (live) ld32_f32(g.in_f32 + (int64_t)m * g.ld_in + n0 + c, x);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          v[j] = __uint_as_float(v0[j]);
-          v[16 + j] = __uint_as_float(v1[j]);
+          for (int j = 0; j < 32; ++j) {
+            v[j] = v[j] + __ldg(g.bias + n0 + c + j) + (live ? x[j] : 0.f);
+            sum += v[j];
+          }
+          st32_tmem(trow + c, v);
         }
-        const int n = n0 + c;
-        if constexpr (EPI == EPI_HEAD) {
+        ptx::tmem_wait_st();
+        const float mean = sum / (float)BN;
+        float var = 0.f;  // pass 2: centred second moment (biased variance, A20)
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          ld32_tmem(trow + c, v);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) z = fmaf(fmaxf(v[j] + __ldg(bias + n + j), 0.f), __ldg(head_w + n + j), z);
-        } else {
-          const int sub = c >> 6, ch0 = (c & 63) >> 3;  // 4 chunks of 8 columns
+          for (int j = 0; j < 32; ++j) var = fmaf(v[j] - mean, v[j] - mean, var);
+        }
+        const float rstd = 1.f / sqrtf(var / (float)BN + 1e-5f);
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {  // pass 3: normalise, affine, bf16
+          float v[32];
+          ld32_tmem(trow + c, v);
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            float* w = v + 8 * u;
+          for (int j = 0; j < 32; ++j)
+            v[j] = (v[j] - mean) * rstd * __ldg(g.gamma + n0 + c + j) + __ldg(g.beta + n0 + c + j);
+          sts32_bf16(out_base + (c >> 6) * C::SUB, r, (c & 63) >> 3, v);
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          ld32_tmem(trow + c, v);
+          const int n = n0 + c;
+          if constexpr (T::kBias) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += __ldg(g.bias + n + j);
+          }
+          if constexpr (EPI == EPI_HEAD || EPI == EPI_HEAD_PARTIAL) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) z = fmaf(fmaxf(v[j], 0.f), __ldg(g.head_w + n + j), z);
+          } else if constexpr (EPI == EPI_BIAS_ADD_F32) {
+            if (live) {
+              float x[32];
+              ld32_f32(g.in_f32 + (int64_t)m * g.ld_in + n, x);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] += x[j];
+              st32_f32(g.out_f32 + (int64_t)m * g.ld_f32 + n, v);
+            }
+          } else {
             if constexpr (EPI == EPI_BIAS_RELU) {
 #pragma unroll
-              for (int j = 0; j < 8; ++j) w[j] = fmaxf(w[j] + __ldg(bias + n + 8 * u + j), 0.f);
-            } else if constexpr (EPI == EPI_CROSS) {
-              const uint4 xa = lds128(swz(ein_base + sub * C::SUB, r, ch0 + u));
-              const uint4 xb = lds128(swz(ein_base + (C::NSUB + sub) * C::SUB, r, ch0 + u));
-              const uint32_t x0w[4] = {xa.x, xa.y, xa.z, xa.w}, xlw[4] = {xb.x, xb.y, xb.z, xb.w};
-#pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                w[2 * j] = ptx::bf16_lo(x0w[j]) * (w[2 * j] + __ldg(bias + n + 8 * u + 2 * j)) + ptx::bf16_lo(xlw[j]);
-                w[2 * j + 1] =
-                    ptx::bf16_hi(x0w[j]) * (w[2 * j + 1] + __ldg(bias + n + 8 * u + 2 * j + 1)) + ptx::bf16_hi(xlw[j]);
-              }
+              for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
             }
-            uint4 o;
-            o.x = ptx::pack_bf16(w[0], w[1]);
-            o.y = ptx::pack_bf16(w[2], w[3]);
-            o.z = ptx::pack_bf16(w[4], w[5]);
-            o.w = ptx::pack_bf16(w[6], w[7]);
-            sts128(swz(out_base + sub * C::SUB, r, ch0 + u), o);
+            if constexpr (T::kEin) {
+              float x0v[32], xlv[32];
+              lds32_bf16(ein_base + (c >> 6) * C::SUB, r, (c & 63) >> 3, x0v);
+              lds32_bf16(ein_base + (C::NSUB + (c >> 6)) * C::SUB, r, (c & 63) >> 3, xlv);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = x0v[j] * v[j] + xlv[j];
+            }
+            if constexpr (EPI == EPI_CROSS_F32) {
+              if (live) st32_f32(g.out_f32 + (int64_t)m * g.ld_f32 + n, v);
+            } else {
+              sts32_bf16(out_base + (c >> 6) * C::SUB, r, (c & 63) >> 3, v);
+            }
           }
         }
       }
@@ -246,23 +352,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) {
         ptx::mbar_arrive(&tempty[a]);
-        if constexpr (EPI == EPI_CROSS) ptx::mbar_arrive(&eempty[a]);
+        if constexpr (T::kEin) ptx::mbar_arrive(&eempty[a]);
       }
       if constexpr (EPI == EPI_HEAD) {
-        const int m = m0 + r;
-        if (m < M) scores[m] = sigmoid_f32(z + head_b);
-      } else {
+        if (live) g.scores[m] = sigmoid_f32(z + g.head_b);
+      } else if constexpr (EPI == EPI_HEAD_PARTIAL) {
+        if (live) g.partial[(int64_t)m * n_tiles_n + tn] = z;
+      } else if constexpr (T::kSmemOut) {
         ptx::fence_async_smem();
         __syncwarp();
         if (lane == 0) {
+          const uint8_t* ob = sOut + (C::OUT_BUFS == 2 ? a : 0) * C::OUT_BYTES;
 #pragma unroll
           for (int j = 0; j < C::NSUB; ++j)
-            ptx::tma_store_2d(&tmOut, sOut + a * C::OUT_BYTES + j * C::SUB + q * 32 * 128, n0 + j * 64, m0 + q * 32);
+            ptx::tma_store_2d(&tmOut, ob + j * C::SUB + q * 32 * 128, n0 + j * 64, m0 + q * 32);
           ptx::bulk_commit();
         }
       }
     }
-    if constexpr (EPI != EPI_HEAD) {
+    if constexpr (T::kSmemOut) {
       if (lane == 0) ptx::bulk_wait<0>();
     }
   }
@@ -296,7 +404,7 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s) {
   cfg.numAttrs = 1;
   const CUtensorMap* dummy = g.tmA;
   return cudaLaunchKernelEx(&cfg, kern, *g.tmA, *g.tmB, *(g.tmOut ? g.tmOut : dummy), *(g.tmX0 ? g.tmX0 : dummy),
-                            *(g.tmXl ? g.tmXl : dummy), g.bias, g.head_w, g.head_b, g.scores, g.M, g.N, g.K);
+                            *(g.tmXl ? g.tmXl : dummy), g);
 }
 
 }  // namespace
@@ -305,33 +413,31 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s) {
 // x0/x_l/out tiles of EPI_CROSS only at BN = 64, and staged bf16 outputs up to BN = 128.
 cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
   if (g.M <= 0) return cudaSuccess;
-  if (g.K % BK || g.N % g.BN || (g.epi == EPI_HEAD && g.BN != g.N)) return cudaErrorInvalidValue;
-  if (g.epi != EPI_HEAD && !g.tmOut) return cudaErrorInvalidValue;
-  if (g.epi == EPI_CROSS && (!g.tmX0 || !g.tmXl)) return cudaErrorInvalidValue;
-  switch (g.epi) {
-    case EPI_STORE:
-      if (g.BN == 64) return launch_t<64, EPI_STORE>(g, s);
-      if (g.BN == 128) return launch_t<128, EPI_STORE>(g, s);
-      break;
-    case EPI_BIAS_RELU:
-      if (g.BN == 64) return launch_t<64, EPI_BIAS_RELU>(g, s);
-      if (g.BN == 128) return launch_t<128, EPI_BIAS_RELU>(g, s);
-      break;
-    case EPI_CROSS:
-      if (g.BN == 64) return launch_t<64, EPI_CROSS>(g, s);
-      break;
-    case EPI_HEAD:
-      if (g.BN == 64) return launch_t<64, EPI_HEAD>(g, s);
-      if (g.BN == 128) return launch_t<128, EPI_HEAD>(g, s);
-      if (g.BN == 256) return launch_t<256, EPI_HEAD>(g, s);
-      break;
-  }
+  const bool full_row = g.epi == EPI_HEAD || g.epi == EPI_SUM_LN;
+  if (g.K % BK || g.N % g.BN || (full_row && g.BN != g.N)) return cudaErrorInvalidValue;
+  if ((g.epi == EPI_STORE || g.epi == EPI_BIAS_RELU || g.epi == EPI_CROSS || g.epi == EPI_BIAS ||
+       g.epi == EPI_SUM_LN) && !g.tmOut)
+    return cudaErrorInvalidValue;
+  if ((g.epi == EPI_CROSS || g.epi == EPI_CROSS_F32) && (!g.tmX0 || !g.tmXl)) return cudaErrorInvalidValue;
+#define CVR_CASE(BN_, EPI_) \
+  if (g.BN == BN_ && g.epi == EPI_) return launch_t<BN_, EPI_>(g, s);
+  CVR_CASE(64, EPI_STORE)
+  CVR_CASE(128, EPI_STORE)
+  CVR_CASE(64, EPI_BIAS_RELU)
+  CVR_CASE(128, EPI_BIAS_RELU)
+  CVR_CASE(64, EPI_CROSS)
+  CVR_CASE(64, EPI_HEAD)
+  CVR_CASE(128, EPI_HEAD)
+  CVR_CASE(256, EPI_HEAD)
+  CVR_CASE(128, EPI_BIAS)
+  CVR_CASE(64, EPI_CROSS_F32)
+  CVR_CASE(64, EPI_BIAS_ADD_F32)
+  CVR_CASE(128, EPI_BIAS_ADD_F32)
+  CVR_CASE(256, EPI_SUM_LN)
+  CVR_CASE(256, EPI_HEAD_PARTIAL)
+#undef CVR_CASE
   return cudaErrorInvalidValue;
 }
-
-namespace {
-
-}  // namespace
 
 int encode_tmap_bf16(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                      const char** err) {

@@ -1,0 +1,66 @@
+"""Config 4 (backbone-scaled ensemble, BASELINE.json configs[3]) on the GPU against the fp64 oracle:
+4 ensemble layers Y = LN_token(DCN(X) + MHA(X) + FFN(X)) (reading A20) + head 16384-2048-512-1.
+Tolerance 2e-3 absolute on the sigmoid output (bf16 path)."""
+import numpy as np
+import pytest
+import torch
+
+import cvr_synth as cs
+import oracle as O
+from helpers import TOL_BF16, make_model, to_dev
+
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+
+@pytest.fixture(scope="module")
+def c4small():
+    from paper_2605_29232_b200 import build
+    build.build()
+    cfg = cs.C4.with_(rows=(20000,) * 64)
+    m, tabs, w = make_model(cfg, max_batch=512, max_nnz=1 << 20)
+    return cfg, m, tabs, w
+
+
+@pytest.mark.parametrize("B", [64, 130])
+def test_c4_scores_vs_oracle(c4small, B):
+    cfg, m, tabs, w = c4small
+    bt = cs.make_batch(cfg, 4, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    s = m.dense(x0, B)
+    assert m.status() == 0
+    ref = O.score_forward(cfg, cs.table_specs(cfg), w, bt)
+    err = np.abs(s.double().cpu().numpy() - ref["scores"])
+    assert err.max() <= TOL_BF16, (err.max(), np.percentile(err, 99))
+
+
+def test_c4_batch_invariance(c4small):
+    cfg, m, tabs, w = c4small
+    bt = cs.make_batch(cfg, 6, batch=300)
+    idx, off, dense = to_dev(bt)
+    full = m.dense(m.embed(idx, off, 300, dense), 300)
+    sel = np.array([299, 5, 128])
+    i2, o2, d2 = to_dev(cs.sub_batch(bt, sel))
+    part = m.dense(m.embed(i2, o2, 3, d2), 3)
+    assert torch.equal(part, full[torch.from_numpy(sel).cuda()])
+
+
+def test_c4_full_size_sampled():
+    """BASELINE.json configs[3] at full size (64 x 1e6 x 256 bf16 tables, B = 8192), the oracle on a
+    sample of 24 examples."""
+    from paper_2605_29232_b200 import build
+    build.build()
+    cfg = cs.C4
+    m, tabs, w = make_model(cfg, max_batch=8192, max_nnz=1 << 22)
+    bt = cs.make_batch(cfg, 0)
+    idx, off, dense = to_dev(bt)
+    s = m.dense(m.embed(idx, off, 8192, dense), 8192)
+    assert m.status() == 0
+    sel = np.random.default_rng(2).choice(8192, 24, replace=False)
+    ref = O.score_forward(cfg, cs.table_specs(cfg), w, cs.sub_batch(bt, sel))["scores"]
+    err = np.abs(s[torch.from_numpy(sel).cuda()].double().cpu().numpy() - ref)
+    assert err.max() <= TOL_BF16, err.max()
+    del m, tabs
+    torch.cuda.empty_cache()
