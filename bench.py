@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="cvr", choices=["cvr", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4", "c3s"],
+                    help="workload (default: config 2, the metric's single-GPU config)")
     ap.add_argument("--ring", type=int, default=8, help="distinct pre-uploaded batches cycled through")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -137,18 +138,54 @@ def embed_bytes(cfg, bt) -> int:
             + bt.batch * cfg.n_dense * (4 + act))
 
 
-def gemm_flops(cfg, B) -> dict:
-    """2 FLOPs per MAC (SPEC.md:328 convention) per launch role, for batch B."""
+FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965  # FP32 lanes x FMA x max SM clock (GHz) = 74.4 TFLOP/s
+
+
+def launch_work(cfg, B) -> dict:
+    """Algorithmic work of ONE launch of each kernel role for batch B: (bound, amount), amount in FLOPs
+    (2 per MAC) for tensor / alu roles."""
     W, r = cfg.width, cfg.cross_rank
     dims = [W] + list(cfg.mlp_dims)
-    mlp = sum(2 * B * dims[i] * dims[i + 1] for i in range(len(cfg.mlp_dims) - 1))
-    return {"gemm_xV": 2 * B * W * r, "gemm_tU_cross": 2 * B * r * W, "cross_fused": 4 * B * W * r,
-            "gemm_mlp_relu_total": mlp, "gemm_mlp_head": 2 * B * dims[-2] * dims[-1] + 2 * B * dims[-1]}
+    hidden = [2 * B * dims[i] * dims[i + 1] for i in range(len(cfg.mlp_dims) - 1)]
+    w = {"gemm_mlp_relu": ("tensor", sum(hidden) / max(1, len(hidden))),
+         "gemm_mlp_head": ("tensor", 2 * B * dims[-2] * dims[-1] + 2 * B * dims[-1]),
+         "head_finalize": ("alu", 2 * B * max(1, dims[-1] // 256))}
+    if cfg.backbone == "dcn_full":
+        w["dense_f32_dcn"] = ("alu", 2 * B * (cfg.n_cross * W * W + sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1))
+                                              + dims[-1]))
+    else:
+        w["gemm_xV"] = ("tensor", 2 * B * W * r)
+        w["gemm_tU_cross"] = ("tensor", 2 * B * r * W)
+        w["cross_fused"] = ("tensor", 4 * B * W * r)
+        w["cross_stack"] = ("tensor", cfg.n_cross * 4 * B * W * r)
+    if cfg.backbone == "ensemble":
+        S, D, F, H = cfg.n_tables, cfg.dim, cfg.ffn_dim, cfg.n_heads
+        BT = B * S
+        w.update({"gemm_ens_qkv": ("tensor", 2 * BT * D * 3 * D), "gemm_ens_oproj": ("tensor", 2 * BT * D * D),
+                  "gemm_ens_ffn1": ("tensor", 2 * BT * D * F), "gemm_ens_ffn2_ln": ("tensor", 2 * BT * F * D),
+                  "mha64": ("tensor", 4 * B * H * S * S * (D // H))})
+    return w
 
 
 def dense_flops_per_example(cfg) -> int:
-    f = gemm_flops(cfg, 1)
-    return cfg.n_cross * (f["gemm_xV"] + f["gemm_tU_cross"]) + f["gemm_mlp_relu_total"] + f["gemm_mlp_head"]
+    w = launch_work(cfg, 1)
+    layer_roles = ["gemm_xV", "gemm_tU_cross"]  # (cross_stack = n_cross x these two, one launch) + (["gemm_ens_qkv", "gemm_ens_oproj", "gemm_ens_ffn1",
+                                                    "gemm_ens_ffn2_ln", "mha64"] if cfg.backbone == "ensemble" else [])
+    if cfg.backbone == "dcn_full":
+        return int(w["dense_f32_dcn"][1])
+    n_hidden = len(cfg.mlp_dims) - 1
+    return int(cfg.n_cross * sum(w[k][1] for k in layer_roles) + n_hidden * w["gemm_mlp_relu"][1] + w["gemm_mlp_head"][1])
+
+
+WORKLOADS = {
+    "c1": "c1: BASELINE.json configs[0] tiny fp32 (8 x 1000 x 16 fp32 tables, 2 full-rank crosses, MLP 141-64-32-1)",
+    "c2": "c2: BASELINE.json configs[1] single-GPU bf16 DCN-v2 scoring (embed -> 3 low-rank cross -> MLP "
+          "1728-1024-512-256-1 -> sigmoid)",
+    "c3s": "c3-S: BASELINE.json configs[2] strong-scaling variant (100 x 5e6 x 128 fp16 tables, B=65536, W=12864)",
+    "c4": "c4: BASELINE.json configs[3] backbone-scaled (64 x 1e6 x 256 bf16, 4 ensemble layers DCN||MHA||FFN + LN, "
+          "head 16384-2048-512-1)",
+}
+TOL = {"c1": 1e-5, "c2": 2e-3, "c3s": 2e-3, "c4": 2e-3}
 
 
 # ----------------------------------------------------------------------------- distributed
@@ -197,13 +234,14 @@ def run_reference(args, cfg):
         return
     tabs = cs.table_specs(cfg)
     w = cs.make_weights(cfg)
-    bt0 = cs.make_batch(cfg, 0)
+    probe = min(cfg.batch, 64)
+    bt0 = cs.make_batch(cfg, 0, batch=probe)
     t = time.perf_counter()
     O.score_forward(cfg, tabs, w, bt0)
-    t_full = time.perf_counter() - t
+    t_full = (time.perf_counter() - t) * cfg.batch / probe
     steps = args.steps + args.warmup
     S = int(cfg.batch * min(1.0, 120.0 / max(1, steps) / max(t_full, 1e-3)))
-    S = max(32, S // 32 * 32)
+    S = max(8, S // 8 * 8)
     batches = [cs.make_batch(cfg, 10 + (i % args.ring), batch=S) for i in range(min(steps, args.ring))]
     for i in range(args.warmup):
         O.score_forward(cfg, tabs, w, batches[i % len(batches)])
@@ -212,13 +250,12 @@ def run_reference(args, cfg):
         O.score_forward(cfg, tabs, w, batches[i % len(batches)])
     el = time.perf_counter() - t0
     v = args.steps * S / el
-    sample = f"{S} examples of config 2 per step (batch shape of BASELINE.json configs[1], sampled to bound CPU time)"
+    sample = f"{S} examples of {cfg.name} per step (sampled from the {cfg.name} batch to bound CPU time)"
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (cvr_synth, seeded)",
-        "config": {"workload": "c2: BASELINE.json configs[1] single-GPU bf16 DCN-v2 scoring",
-                   "global_batch": S, "oracle": "numpy fp64 (oracle/)"},
+        "config": {"workload": WORKLOADS[cfg.name], "global_batch": S, "oracle": "numpy fp64 (oracle/)"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": host_cores(), "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -236,7 +273,7 @@ def run_cvr(args, cfg):
     # inputs: tables (HBM, > L2), weights, a ring of distinct batches (per-rank seeds)
     tables = [s.materialize(device=dev) for s in cs.table_specs(cfg)]
     weights = cs.make_weights(cfg)
-    ring = [cs.make_batch(cfg, 1000 * rank + i) for i in range(args.ring)]
+    ring = [cs.make_batch(cfg, 1000 * rank + i) for i in range(args.ring if cfg.name != "c3s" else 2)]
     max_nnz = max(b.nnz for b in ring)
     m = CvrModel(cfg, max_batch=B, max_nnz=max_nnz, device=dev)
     m.load_tables(tables)
@@ -265,7 +302,7 @@ def run_cvr(args, cfg):
 
     clocks = ClockSampler(local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches_per_step = 1 + 2 * cfg.n_cross + len(cfg.mlp_dims)  # upper bound (fused cross: 1 per layer)
+    launches_per_step = 2 + 7 * cfg.n_cross + len(cfg.mlp_dims)  # upper bound over the backbones
     with clocks:
         barrier(world)
         torch.cuda.synchronize(dev)
@@ -359,7 +396,8 @@ def run_cvr(args, cfg):
     # ---- per-kernel roofline (CUDA events on the launching stream, inside the timed region)
     pk = peaks()
     ebytes = float(np.mean([embed_bytes(cfg, b) for b in ring]))
-    gf = gemm_flops(cfg, B)
+    work = launch_work(cfg, B)
+    bf16_peak = pk["bf16_sustained"] or pk["bf16"]
     kernels = {}
     for name, st in kstats.items():
         avg_s = st["avg_ms"] / 1e3
@@ -368,14 +406,12 @@ def run_cvr(args, cfg):
             kernels[name] = {"bound": "hbm", "avg_us": st["avg_ms"] * 1e3, "launches": st["launches"],
                              "achieved": ach, "unit": "GB/s", "frac": ach / pk["hbm"], "algorithmic_bytes": ebytes}
         else:
-            if name == "gemm_mlp_relu":
-                per = gf["gemm_mlp_relu_total"] / (len(cfg.mlp_dims) - 1)
-            else:
-                per = gf[name]
+            bound, per = work[name]
             ach = per / avg_s / 1e12
-            peak = pk["bf16_sustained"] or pk["bf16"]
-            kernels[name] = {"bound": "tensor", "avg_us": st["avg_ms"] * 1e3, "launches": st["launches"],
-                             "achieved": ach, "unit": "TFLOP/s", "frac": ach / peak, "flops_per_launch": per}
+            peak = bf16_peak if bound == "tensor" else FP32_SIMT_TFLOPS
+            kernels[name] = {"bound": bound, "avg_us": st["avg_ms"] * 1e3, "launches": st["launches"],
+                             "achieved": ach, "unit": "TFLOP/s", "frac": ach / peak, "flops_per_launch": per,
+                             "peak": peak}
     share = {k: v["total_ms"] / max(1e-9, sum(s["total_ms"] for s in kstats.values())) for k, v in kstats.items()}
     dom = max(kstats, key=lambda k: kstats[k]["total_ms"])
     dk = kernels[dom]
@@ -385,22 +421,22 @@ def run_cvr(args, cfg):
         with open(tp) as f:
             traffic = json.load(f).get(dom)
     roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"],
-                "peak": pk["hbm"] if dk["bound"] == "hbm" else (pk["bf16_sustained"] or pk["bf16"]),
+                "peak": pk["hbm"] if dk["bound"] == "hbm" else dk["peak"],
                 "unit": dk["unit"], "frac": dk["frac"], "traffic": traffic,
                 "peak_source": f"MEASURED_PEAKS.json ({pk['source']}; bf16 sustained for kernels inside the step)",
                 "share_of_kernel_time": share[dom]}
-    dense_ach = dense_flops_per_example(cfg) * B / (
-        sum(v["total_ms"] for k, v in kstats.items() if k.startswith("gemm")) / args.steps / 1e3) / 1e12
+    dense_ms = sum(v["total_ms"] for k, v in kstats.items() if k != "embed_bag_pool") / args.steps
+    dense_ach = dense_flops_per_example(cfg) * B / (dense_ms / 1e3) / 1e12
 
     # ---- parity spot check (outside the timed region): 64 examples of the last ring batch vs the oracle
     parity = None
     try:
         import oracle as O
-        sel = np.arange(0, B, B // 64)
+        sel = np.arange(0, B, max(1, B // (16 if cfg.name == "c4" else 64)))
         bt = ring[(args.steps - 1) % R]
         ref = O.score_forward(cfg, cs.table_specs(cfg), weights, cs.sub_batch(bt, sel))["scores"]
         got = outs[(args.steps - 1) % R][torch.from_numpy(sel).to(dev)].double().cpu().numpy()
-        parity = {"max_abs_err": float(np.abs(got - ref).max()), "n": int(len(sel)), "tol": 2e-3}
+        parity = {"max_abs_err": float(np.abs(got - ref).max()), "n": int(len(sel)), "tol": TOL[cfg.name]}
     except Exception as e:  # noqa: BLE001
         parity = {"error": str(e)}
 
@@ -409,27 +445,28 @@ def run_cvr(args, cfg):
     if world == 1 and not args.no_cpu_baseline:
         import oracle as O
         tabs = cs.table_specs(cfg)
+        sub = B if cfg.name in ("c1", "c2") else 64
         n_ex, t0, k = 0, time.perf_counter(), 0
         while True:
-            O.score_forward(cfg, tabs, weights, ring[k % R])
-            n_ex += B
+            bt = ring[k % R] if sub == B else cs.sub_batch(ring[k % R], np.arange(sub))
+            O.score_forward(cfg, tabs, weights, bt)
+            n_ex += sub
             k += 1
             if time.perf_counter() - t0 >= args.cpu_seconds:
                 break
         el = time.perf_counter() - t0
         cpu = {"value": n_ex / el, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
-               "sample": f"{k} full config-2 batches ({n_ex} examples, {el:.1f} s) through oracle.score_forward "
-                         f"(numpy fp64, table rows regenerated on demand)"}
+               "sample": f"{k} x {sub} examples of {cfg.name} ({n_ex} examples, {el:.1f} s) through "
+                         f"oracle.score_forward (numpy fp64, table rows regenerated on demand)"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": el_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16", "data": "synthetic (cvr_synth: seeded, BASELINE.json configs[1] shapes/distributions)",
-        "config": {"workload": "c2: BASELINE.json configs[1] single-GPU bf16 DCN-v2 scoring (embed -> 3 low-rank "
-                               "cross -> MLP 1728-1024-512-256-1 -> sigmoid)",
-                   "global_batch": B * world, "batch_per_gpu": B, "tables": "26 x rows log-uniform[1e5,1e6] x 64 bf16",
+        "dtype": "f32" if cfg.act_dtype == "f32" else "bf16", "data": "synthetic (cvr_synth: seeded, BASELINE.json configs[1] shapes/distributions)",
+        "config": {"workload": WORKLOADS[cfg.name], "global_batch": B * world, "batch_per_gpu": B,
                    "parallelism": f"replicas x{world} (two-stream decoupled executor per GPU)",
-                   "l2": "inputs larger than L2 (1.30 GB tables, ring of %d distinct batches)" % R},
+                   "l2": "inputs larger than L2 (%.2f GB of tables, ring of %d distinct batches)" % (
+                       sum(t.numel() * t.element_size() for t in tables) / 1e9, R)},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -187,7 +187,9 @@ int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d
 
 /* Options (defaults in brackets): "graphs" [1] replay the executor stages of cvr_score /
  * cvr_score_host as cached CUDA graphs (keyed by their pointer / size arguments; captured on first
- * use; 32 entries, LRU); "pdl" [1] launch dependent GEMMs with programmatic stream serialization; "fused_cross" [0; allowed when r == 256]
+ * use; 32 entries, LRU); "pdl" [1] launch dependent GEMMs with programmatic stream serialization; "fused_cross" [0; allowed when r == 256]; "stack" [0] run the whole low-rank cross stack as one persistent kernel with per-(layer, row-block)
+ * completion counters instead of 2 x n_cross GEMM launches; "a_resident" [0] the U GEMM of a low-rank cross layer keeps
+ * the 128 x r block of t resident in shared memory across its N tiles
  * run each low-rank cross layer as one clustered kernel (K5) instead of two GEMMs. */
 int cvr_set_option(cvr_ctx* ctx, const char* key, int64_t value);
 

@@ -24,12 +24,12 @@ using namespace cvr;
 
 enum KernelId {
   K_EMBED = 0, K_GEMM_V, K_GEMM_U, K_GEMM_MLP, K_GEMM_HEAD, K_DENSE_F32, K_UNPACK, K_CROSS_FUSED,
-  K_ENS_QKV, K_MHA, K_ENS_OPROJ, K_ENS_FFN1, K_ENS_FFN2_LN, K_HEAD_FIN, K_COUNT
+  K_ENS_QKV, K_MHA, K_ENS_OPROJ, K_ENS_FFN1, K_ENS_FFN2_LN, K_HEAD_FIN, K_CROSS_STACK, K_COUNT
 };
 static const char* kKernelNames[K_COUNT] = {
     "embed_bag_pool", "gemm_xV",  "gemm_tU_cross",  "gemm_mlp_relu", "gemm_mlp_head", "dense_f32_dcn",
     "shard_unpack",   "cross_fused", "gemm_ens_qkv", "mha64",       "gemm_ens_oproj", "gemm_ens_ffn1",
-    "gemm_ens_ffn2_ln", "head_finalize"};
+    "gemm_ens_ffn2_ln", "head_finalize", "cross_stack"};
 
 namespace {
 
@@ -105,6 +105,11 @@ struct cvr_ctx {
   size_t off_part = 0;
   std::vector<CUtensorMap> st_h;
   bool pdl = true;
+  // measured on B200 at B = 4096 (scripts/dense_ab.py): separate streaming GEMMs 105.5 us/dense stage,
+  // resident-A U GEMM 108.4, persistent cross stack 118 -- both kept as options, off by default
+  bool a_resident = false;  // U GEMM keeps t resident (K = r <= 256)
+  bool stack = false;       // the cross stack as one persistent dependency-driven kernel
+  size_t off_stack_tbl = 0, off_stack_done = 0;
   // CUDA-graph cache for the executor stages (cvr_score / cvr_score_host)
   struct GraphEntry {
     uint64_t key[7];
@@ -295,7 +300,11 @@ size_t carve(size_t& cur, size_t bytes) {
   return o;
 }
 
-int pick_bn(int N) {
+// N-tile width: wide tiles halve the bytes ingested per FLOP (measured: 4096x1024x1728 13.5 us at BN=256
+// vs 16.2 at 128), as long as enough tiles remain to cover the SMs.
+int pick_bn(int N, int64_t M = 0) {
+  const int64_t mt = (M + 127) / 128;
+  if (N % 256 == 0 && N > 256 && mt * (N / 256) >= 100) return 256;
   if (N > 256 && N % 128 == 0) return 128;
   return 64;
 }
@@ -374,6 +383,8 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
     c->off_xa = carve(cur, (size_t)B * c->x0_ld * 2);
     c->off_xb = carve(cur, (size_t)B * c->x0_ld * 2);
     c->off_t = carve(cur, (size_t)B * c->r * 2);
+    c->off_stack_tbl = carve(cur, sizeof(CrossStackTables));
+    c->off_stack_done = carve(cur, sizeof(int) * 2 * kMaxLayers * ((B + 127) / 128));
     if (c->r == 256) {  // K5 scratch; K5 itself is opt-in ("fused_cross"): measured slower than 2 GEMMs at B=4096
       c->off_part = carve(cur, cross_fused_partial_bytes(c->max_batch));
     }
@@ -409,6 +420,36 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
 
 int cvr_destroy(cvr_ctx* c) {
   if (!c) return CVR_E_ARG;
+  if (c->dbg && c->stack && !c->fused_cross) {  // debug: cross-stack timeline of the last launch
+    std::vector<unsigned long long> h(148 * 32);
+    cudaDeviceSynchronize();
+    cudaMemcpy(h.data(), c->dbg, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull;
+    for (int b = 0; b < 148; ++b)
+      if (h[b * 32 + 31]) t0 = std::min(t0, h[b * 32 + 31]);
+    for (int g = 0; g < 2 * c->n_cross; ++g) {
+      double mx = 0, mn = 1e30, sm = 0, w0 = 1e30, w1 = 0;
+      int n = 0;
+      for (int b = 0; b < 148; ++b) {
+        if (h[b * 32 + g]) {
+          const double v = (double)(h[b * 32 + g] - t0) / 1e3;
+          mx = std::max(mx, v);
+          mn = std::min(mn, v);
+          sm += v;
+          ++n;
+        }
+        if (h[b * 32 + 16 + g]) {
+          const double v = (double)(h[b * 32 + 16 + g] - t0) / 1e3;
+          w0 = std::min(w0, v);
+          w1 = std::max(w1, v);
+        }
+      }
+      fprintf(stderr, "stack gemm %d: first-dep-ready %.2f..%.2f us, chunk done min %.2f avg %.2f max %.2f us (%d ctas)\n",
+              g, w0, w1, mn, n ? sm / n : 0.0, mx, n);
+    }
+    cudaFree(c->dbg);
+    c->dbg = nullptr;
+  }
   if (c->dbg) {  // debug: per-phase averages of the last fused cross launch
     std::vector<unsigned long long> h((size_t)c->dbg_ctas * 8);
     cudaDeviceSynchronize();
@@ -466,7 +507,10 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
   // zero the activation slots once so padding columns / tail rows are defined
   if (e == cudaSuccess) e = cudaMemset(c->ws + c->off_x0[0], 0, c->ws_need - c->off_x0[0]);
   if (e != cudaSuccess) return c->cuda_fail(e, "cvr_set_workspace");
-  if (getenv("CVR_DEBUG_TIMING") && !c->dbg) cudaMalloc(&c->dbg, (size_t)(c->max_batch / 128 + 1) * 4 * 8 * 8);
+  if (getenv("CVR_DEBUG_TIMING") && !c->dbg) {
+    cudaMalloc(&c->dbg, 160 * 32 * 8 + (size_t)(c->max_batch / 128 + 1) * 4 * 8 * 8);
+    cudaMemset(c->dbg, 0, 160 * 32 * 8);
+  }
   c->cuda_ready = true;
   c->k = 0;
   c->weights_loaded = false;
@@ -572,7 +616,7 @@ int encode_plan(cvr_ctx* c) {
   int K = (int)c->x0_ld;
   for (int i = 0; i < c->n_mlp; ++i) {
     const bool last = i + 1 == c->n_mlp;
-    const int bn = last ? (c->head_parts ? 256 : c->mlp[i]) : pick_bn(c->mlp[i]);
+    const int bn = last ? (c->head_parts ? 256 : c->mlp[i]) : pick_bn(c->mlp[i], c->max_batch);
     const Epi ep = last ? (c->head_parts ? EPI_HEAD_PARTIAL : EPI_HEAD) : EPI_BIAS_RELU;
     ok &= addp("mlp/" + std::to_string(i) + "/W", c->mlp[i], K, bn, ep);
     K = c->mlp[i];
@@ -596,9 +640,9 @@ int encode_plan_ensemble(cvr_ctx* c) {
     const std::string p = "ens/" + std::to_string(l) + "/";
     ok &= encode_tmap_bf16(&E.V[l], c->wptr(p + "dcn/V"), r, W, W, 128, &er) == 0;
     ok &= encode_tmap_bf16(&E.U[l], c->wptr(p + "dcn/U"), W, r, r, 64, &er) == 0;
-    ok &= encode_tmap_bf16(&E.Wqkv[l], c->wptr(p + "mha/Wqkv"), 3 * D, D, D, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&E.Wqkv[l], c->wptr(p + "mha/Wqkv"), 3 * D, D, D, 256, &er) == 0;
     ok &= encode_tmap_bf16(&E.Wo[l], c->wptr(p + "mha/Wo"), D, D, D, 128, &er) == 0;
-    ok &= encode_tmap_bf16(&E.W1[l], c->wptr(p + "ffn/W1"), F, D, D, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&E.W1[l], c->wptr(p + "ffn/W1"), F, D, D, 256, &er) == 0;
     ok &= encode_tmap_bf16(&E.W2[l], c->wptr(p + "ffn/W2"), D, F, F, 256, &er) == 0;
   }
   if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
@@ -610,7 +654,7 @@ int encode_plan_ensemble(cvr_ctx* c) {
     GemmPlan g;
     g.N = c->mlp[i];
     g.K = K;
-    g.BN = last ? (c->head_parts ? 256 : c->mlp[i]) : 128;
+    g.BN = last ? (c->head_parts ? 256 : c->mlp[i]) : pick_bn(c->mlp[i], c->max_batch);
     g.epi = last ? (c->head_parts ? EPI_HEAD_PARTIAL : EPI_HEAD) : EPI_BIAS_RELU;
     g.wname = nullptr;
     if (encode_tmap_bf16(&g.tmB, c->wptr("mlp/" + std::to_string(i) + "/W"), g.N, K, K, g.BN, &er) != 0)
@@ -709,6 +753,17 @@ int cvr_load_weights(cvr_ctx* c, int n, const char* const* names, const void* co
   if (c->backbone == CVR_DCN_LOWRANK) {
     int st = encode_plan(c);
     if (st != CVR_OK) return st;
+    CrossStackTables tb;
+    memset(&tb, 0, sizeof tb);
+    for (int l = 0; l < c->n_cross; ++l) {
+      tb.V[l] = c->plan[2 * l].tmB;
+      tb.U[l] = c->plan[2 * l + 1].tmB;
+    }
+    tb.xa = c->tm_xa;
+    tb.xb = c->tm_xb;
+    tb.t = c->tm_t;
+    cudaError_t e = cudaMemcpy(c->ws + c->off_stack_tbl, &tb, sizeof tb, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return c->cuda_fail(e, "upload cross-stack tables");
   } else if (c->backbone == CVR_ENSEMBLE) {
     int st = encode_plan_ensemble(c);
     if (st != CVR_OK) return st;
@@ -862,7 +917,7 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     a2.ld_f32 = W;
     if ((e = run_gemm(c, a2, K_GEMM_U, s)) != cudaSuccess) return c->cuda_fail(e, "ens U");
     // MHA branch: qkv = X Wqkv^T + b ; O = attention ; S += O Wo^T + bo
-    GemmArgs a3 = ga(tok_xl, &E.Wqkv[l], BT, 3 * D, D, 128, EPI_BIAS);
+    GemmArgs a3 = ga(tok_xl, &E.Wqkv[l], BT, 3 * D, D, 256, EPI_BIAS);
     a3.tmOut = &E.st_qkv;
     a3.bias = c->wptr<float>(p + "mha/bqkv");
     if ((e = run_gemm(c, a3, K_ENS_QKV, s)) != cudaSuccess) return c->cuda_fail(e, "ens qkv");
@@ -878,7 +933,7 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     a4.ld_f32 = D;
     if ((e = run_gemm(c, a4, K_ENS_OPROJ, s)) != cudaSuccess) return c->cuda_fail(e, "ens oproj");
     // FFN branch + branch sum + LN: X' = LN(W2 ReLU(W1 X + b1) + b2 + S) * gamma + beta
-    GemmArgs a5 = ga(tok_xl, &E.W1[l], BT, c->ffn, D, 128, EPI_BIAS_RELU);
+    GemmArgs a5 = ga(tok_xl, &E.W1[l], BT, c->ffn, D, 256, EPI_BIAS_RELU);
     a5.tmOut = &E.st_hf;
     a5.bias = c->wptr<float>(p + "ffn/b1");
     if ((e = run_gemm(c, a5, K_ENS_FFN1, s)) != cudaSuccess) return c->cuda_fail(e, "ens ffn1");
@@ -933,6 +988,27 @@ int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, const CUtenso
   // ---- bf16 low-rank DCN-v2 on tcgen05
   const CUtensorMap* tm_xl = tm_x0;
   size_t pi = 0;
+  if (c->stack && !c->fused_cross && c->n_cross > 0) {
+    CrossStackArgs a{};
+    a.xa = c->at<__nv_bfloat16>(c->off_xa);
+    a.xb = c->at<__nv_bfloat16>(c->off_xb);
+    a.t = c->at<__nv_bfloat16>(c->off_t);
+    for (int l = 0; l < c->n_cross; ++l) a.bias[l] = c->wptr<float>("dcn/" + std::to_string(l) + "/b");
+    a.done = c->at<int>(c->off_stack_done);
+    a.M = B;
+    a.W = (int)c->x0_ld;
+    a.R = c->r;
+    a.L = c->n_cross;
+    a.num_sms = c->num_sms;
+    a.dbg = c->dbg;
+    c->pbeg(s);
+    e = launch_cross_stack(tm_x0, c->at<CrossStackTables>(c->off_stack_tbl), a, s);
+    c->pend(K_CROSS_STACK, s);
+    if (e != cudaSuccess) return c->cuda_fail(e, "cross_stack launch");
+    pi = 2 * c->n_cross;
+    tm_xl = (c->n_cross - 1) % 2 == 0 ? &c->tm_xa : &c->tm_xb;
+    return run_mlp_head(c, tm_xl, pi, B, scores, s);
+  }
   for (int l = 0; l < c->n_cross; ++l) {
     const GemmPlan& gv = c->plan[pi++];
     const GemmPlan& gu = c->plan[pi++];
@@ -969,6 +1045,7 @@ int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, const CUtenso
     au.tmX0 = tm_x0;
     au.tmXl = tm_xl;
     au.bias = c->wptr<float>("dcn/" + std::to_string(l) + "/b");
+    au.a_resident = c->a_resident;
     if ((e = run_gemm(c, au, K_GEMM_U, s)) != cudaSuccess) return c->cuda_fail(e, "gemm U launch");
     tm_xl = even ? &c->tm_xa : &c->tm_xb;
   }
@@ -1276,7 +1353,7 @@ int cvr_gemm_bf16(const void* d_A, int64_t lda, const void* d_B, int64_t ldb, vo
                   int K, int epi, const float* d_bias, int bn, cvr_stream_t stream) {
   if (!d_A || !d_B || !d_C || M < 0 || N <= 0 || K <= 0 || (epi == 1 && !d_bias)) return CVR_E_ARG;
   if (epi != 0 && epi != 1) return CVR_E_ARG;
-  if (K % 64 || N % bn || (bn != 64 && bn != 128) || lda < K || ldb < K || ldc < N || (lda | ldb | ldc) & 7)
+  if (K % 64 || N % bn || (bn != 64 && bn != 128 && bn != 256) || lda < K || ldb < K || ldc < N || (lda | ldb | ldc) & 7)
     return CVR_E_UNSUPPORTED;
   if (M == 0) return CVR_OK;
   const char* er = nullptr;
@@ -1313,6 +1390,18 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
   if (!strcmp(key, "fused_cross")) {
     if (value && !(c->backbone == CVR_DCN_LOWRANK && c->r == 256)) return c->fail(CVR_E_UNSUPPORTED, "fused cross needs r == 256");
     c->fused_cross = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    return CVR_OK;
+  }
+  if (!strcmp(key, "stack")) {
+    c->stack = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    return CVR_OK;
+  }
+  if (!strcmp(key, "a_resident")) {
+    c->a_resident = value != 0;
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     return CVR_OK;

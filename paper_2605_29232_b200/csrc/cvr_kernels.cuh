@@ -99,6 +99,7 @@ struct GemmArgs {
   Epi epi;
   int num_sms;
   bool pdl;                  // launch with programmatic stream serialization
+  bool a_resident;           // K <= 256: keep the A block resident, contiguous tile runs per CTA
 };
 
 // C[M, N] = epi(A[M, K] . B[N, K]^T).  K % 64 == 0, N % BN == 0, BN in {64, 128, 256};
@@ -128,6 +129,25 @@ struct CrossFusedArgs {
 };
 size_t cross_fused_partial_bytes(int max_batch);
 cudaError_t launch_cross_fused(const CrossFusedArgs& g, cudaStream_t s);
+
+// ---- the whole low-rank cross stack as one persistent dependency-driven kernel ------------------------
+struct CrossStackTables {        // device-resident (64-byte aligned), built at cvr_load_weights
+  CUtensorMap V[kMaxLayers];     // V_l [r, W], box {64, 64}
+  CUtensorMap U[kMaxLayers];     // U_l [W, r], box {64, 64}
+  CUtensorMap xa, xb;            // layer outputs (A operand / x_l epilogue input), box {64, 128}
+  CUtensorMap t;                 // t [max_batch, r], box {64, 128}
+};
+struct CrossStackArgs {
+  __nv_bfloat16* xa;
+  __nv_bfloat16* xb;
+  __nv_bfloat16* t;
+  const float* bias[kMaxLayers];
+  int* done;                     // [2L][ceil(M/128)] completion counters (zeroed per launch)
+  int M, W, R, L, num_sms;
+  unsigned long long* dbg;       // optional [grid][32] timestamps (CVR_DEBUG_TIMING)
+};
+cudaError_t launch_cross_stack(const CUtensorMap* tmX0, const CrossStackTables* d_tables, const CrossStackArgs& a,
+                               cudaStream_t s);
 
 // host: encode a 2-D bf16 K-major tensor map [rows, cols] (row stride ld elements) with box
 // {64, box_rows} and 128-byte swizzle.

@@ -26,6 +26,7 @@
 
 #include "cvr_kernels.cuh"
 #include "cvr_ptx.cuh"
+#include "cvr_tile.cuh"
 
 namespace cvr {
 namespace {
@@ -43,11 +44,12 @@ struct EpiTraits {
   static constexpr bool kBias = EPI != EPI_STORE;
 };
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool AR = false>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;       // 16 KB
   static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int AR_BYTES = AR ? 4 * A_BYTES : 0;   // resident A block (K <= 256)
+  static constexpr int STAGE = (AR ? 0 : A_BYTES) + B_BYTES;
   static constexpr int SUB = BM * 64 * 2;           // one 128 x 64 bf16 sub-tile (16 KB)
   static constexpr int NSUB = BN / 64;
   static constexpr int OUT_BUFS = BN == 256 ? 1 : 2;
@@ -55,103 +57,30 @@ struct Cfg {
   static constexpr int EIN_BYTES = EpiTraits<EPI>::kEin ? 2 * NSUB * SUB : 0;     // x0 + x_l tiles, per acc
   static constexpr int EPI_BYTES = OUT_BUFS * OUT_BYTES + 2 * EIN_BYTES;
   static constexpr int BAR_BYTES = 256;
-  static constexpr int STAGES_FIT = (kSmemBudget - 1024 - BAR_BYTES - EPI_BYTES) / STAGE;
+  static constexpr int STAGES_FIT = (kSmemBudget - 1024 - BAR_BYTES - EPI_BYTES - AR_BYTES) / STAGE;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int TMEM_COLS = 2 * BN;          // two accumulators; BN in {64,128,256}
-  static constexpr int SMEM = 1024 + STAGES * STAGE + EPI_BYTES + BAR_BYTES;
+  static constexpr int SMEM = 1024 + AR_BYTES + STAGES * STAGE + EPI_BYTES + BAR_BYTES;
   static_assert(STAGES >= 2, "shared memory budget");
 };
 
-__device__ __forceinline__ float sigmoid_f32(float z) {
-  if (z >= 0.f) return 1.f / (1.f + expf(-z));
-  const float e = expf(z);
-  return e / (1.f + e);
-}
+using namespace tile;
 
-// 16-byte chunk `ch` (0..7) of row `r` in a 128-B-swizzled [rows x 64] bf16 sub-tile
-__device__ __forceinline__ uint32_t swz(uint32_t sub_base, int r, int ch) {
-  return sub_base + r * 128 + ((ch ^ (r & 7)) << 4);
-}
-__device__ __forceinline__ uint4 lds128(uint32_t a) {
-  uint4 v;
-  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
-  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
-}
-__device__ __forceinline__ void ld32_tmem(uint32_t taddr, float (&v)[32]) {
-  uint32_t v0[16], v1[16];
-  ptx::tmem_ld_32x32b_x16(taddr, v0);
-  ptx::tmem_ld_32x32b_x16(taddr + 16, v1);
-  ptx::tmem_wait_ld();
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    v[j] = __uint_as_float(v0[j]);
-    v[16 + j] = __uint_as_float(v1[j]);
-  }
-}
-__device__ __forceinline__ void st32_tmem(uint32_t taddr, const float (&v)[32]) {
-  uint32_t v0[16], v1[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    v0[j] = __float_as_uint(v[j]);
-    v1[j] = __float_as_uint(v[16 + j]);
-  }
-  ptx::tmem_st_32x32b_x16(taddr, v0);
-  ptx::tmem_st_32x32b_x16(taddr + 16, v1);
-}
-__device__ __forceinline__ void ld32_f32(const float* p, float (&v)[32]) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const float4 f = *reinterpret_cast<const float4*>(p + 4 * j);
-    v[4 * j] = f.x;
-    v[4 * j + 1] = f.y;
-    v[4 * j + 2] = f.z;
-    v[4 * j + 3] = f.w;
-  }
-}
-__device__ __forceinline__ void st32_f32(float* p, const float (&v)[32]) {
-#pragma unroll
-  for (int j = 0; j < 8; ++j)
-    *reinterpret_cast<float4*>(p + 4 * j) = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-}
-// 32 columns (4 swizzled 16-byte chunks) of row r into / out of a bf16 staging sub-tile
-__device__ __forceinline__ void sts32_bf16(uint32_t sub_base, int r, int ch0, const float (&v)[32]) {
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    uint4 o;
-    o.x = ptx::pack_bf16(v[8 * u], v[8 * u + 1]);
-    o.y = ptx::pack_bf16(v[8 * u + 2], v[8 * u + 3]);
-    o.z = ptx::pack_bf16(v[8 * u + 4], v[8 * u + 5]);
-    o.w = ptx::pack_bf16(v[8 * u + 6], v[8 * u + 7]);
-    sts128(swz(sub_base, r, ch0 + u), o);
-  }
-}
-__device__ __forceinline__ void lds32_bf16(uint32_t sub_base, int r, int ch0, float (&v)[32]) {
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const uint4 x = lds128(swz(sub_base, r, ch0 + u));
-    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      v[8 * u + 2 * j] = ptx::bf16_lo(w[j]);
-      v[8 * u + 2 * j + 1] = ptx::bf16_hi(w[j]);
-    }
-  }
-}
-
-template <int BN, int EPI>
+// AR (A resident, K <= 256): each CTA walks a contiguous run of tiles in m-major order and loads the
+// 128 x K A block once per m-block into a resident buffer; the ring only streams B tiles.  This cuts the
+// N/BN-fold re-read of A of a small-K, wide-N GEMM (the U GEMM of a cross layer).
+template <int BN, int EPI, bool AR>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmX0,
                      const __grid_constant__ CUtensorMap tmXl, const GemmArgs g) {
-  using C = Cfg<BN, EPI>;
+  using C = Cfg<BN, EPI, AR>;
   using T = EpiTraits<EPI>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = sA + C::STAGES * C::A_BYTES;
+  uint8_t* sAR = smem;                                  // resident A (AR only)
+  uint8_t* sA = smem + C::AR_BYTES;
+  uint8_t* sB = sA + (AR ? 0 : C::STAGES * C::A_BYTES);
   uint8_t* sOut = sB + C::STAGES * C::B_BYTES;         // [OUT_BUFS][NSUB][SUB]
   uint8_t* sEin = sOut + C::OUT_BUFS * C::OUT_BYTES;   // [2][x0 NSUB subs | x_l NSUB subs]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sEin + 2 * C::EIN_BYTES);
@@ -161,13 +90,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tempty = tfull + 2;          // [2] accumulator drained (4 epilogue warps)
   uint64_t* efull = tempty + 2;          // [2] epilogue input tiles landed
   uint64_t* eempty = efull + 2;          // [2] epilogue input tiles consumed (4 warps)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(eempty + 2);
+  uint64_t* afull = eempty + 2;          // resident A landed (AR)
+  uint64_t* aempty = afull + 1;          // resident A no longer read by MMAs (AR)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(aempty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = g.M, N = g.N, K = g.K;
   const int n_tiles_n = N / BN;
   const int n_tiles = ((M + BM - 1) / BM) * n_tiles_n;
   const int nk = K / BK;
+  // tile walk: strided over the grid, or (AR) a contiguous balanced run per CTA
+  const int t_begin = AR ? (int)((int64_t)n_tiles * blockIdx.x / gridDim.x) : (int)blockIdx.x;
+  const int t_end = AR ? (int)((int64_t)n_tiles * (blockIdx.x + 1) / gridDim.x) : n_tiles;
+  const int t_step = AR ? 1 : (int)gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -180,6 +115,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&efull[a], 1);
       ptx::mbar_init(&eempty[a], 4);
     }
+    ptx::mbar_init(afull, 1);
+    ptx::mbar_init(aempty, 1);
     ptx::fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -202,8 +139,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {  // ================= TMA producer
       int gk = 0;     // global k-block counter (ring position)
       int it = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+      int cur_m = -1, a_loads = 0;
+      for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
         const int m0 = (tile / n_tiles_n) * BM, n0 = (tile % n_tiles_n) * BN;
+        if constexpr (AR) {
+          if (m0 != cur_m) {
+            if (a_loads > 0) ptx::mbar_wait(aempty, (a_loads - 1) & 1);
+            ptx::mbar_arrive_expect_tx(afull, nk * C::A_BYTES);
+            for (int kb = 0; kb < nk; ++kb) ptx::tma_load_2d(sAR + kb * C::A_BYTES, &tmA, afull, kb * BK, m0);
+            cur_m = m0;
+            ++a_loads;
+          }
+        }
         if constexpr (T::kEin) {
           const int a = it & 1;
           if (it >= 2) ptx::mbar_wait(&eempty[a], ((it >> 1) - 1) & 1);
@@ -219,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = gk % C::STAGES;
           if (gk >= C::STAGES) ptx::mbar_wait(&empty[s], ((gk / C::STAGES) - 1) & 1);
           ptx::mbar_arrive_expect_tx(&full[s], C::STAGE);
-          ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
+          if constexpr (!AR) ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
           ptx::tma_load_2d(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);
         }
       }
@@ -228,8 +175,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {  // ================= MMA issuer
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN);
       int gk = 0, it = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+      int cur_m = -1, a_loads = 0;
+      for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
         const int a = it & 1;
+        const int m0 = (tile / n_tiles_n) * BM;
+        if constexpr (AR) {
+          if (m0 != cur_m) {
+            ptx::mbar_wait(afull, a_loads & 1);
+            cur_m = m0;
+            ++a_loads;
+          }
+        }
         if (it >= 2) ptx::mbar_wait(&tempty[a], ((it >> 1) - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t acc = tmem + a * BN;
@@ -237,7 +193,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = gk % C::STAGES;
           ptx::mbar_wait(&full[s], (gk / C::STAGES) & 1);
           ptx::tc_fence_after();
-          const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
+          const uint64_t ad = ptx::sdesc_kmajor_sw128(
+              ptx::smem_u32(AR ? sAR + kb * C::A_BYTES : sA + s * C::A_BYTES));
           const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)  // K step 16 = 32 bytes = +2 in the 16-byte address field
@@ -245,13 +202,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           ptx::umma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
         }
         ptx::umma_commit(&tfull[a]);    // accumulator a complete
+        if constexpr (AR) {             // last tile of this m-block: the resident A may be replaced
+          const int nt = tile + t_step;
+          if (nt >= t_end || (nt / n_tiles_n) * BM != m0) ptx::umma_commit(aempty);
+        }
       }
     }
   } else {  // ================= epilogue warps 2..5: TMEM quadrant q = warp % 4 -> rows 32q .. 32q+31
     const int q = warp & 3;
     const int r = q * 32 + lane;  // row within the tile
     int it = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+    for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
       const int m0 = (tile / n_tiles_n) * BM, tn = tile % n_tiles_n, n0 = tn * BN;
       const int m = m0 + r;
       const bool live = m < M;
@@ -380,10 +341,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) ptx::tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, bool AR = false>
 cudaError_t launch_t(const GemmArgs& g, cudaStream_t s) {
-  using C = Cfg<BN, EPI>;
-  auto kern = gemm_bf16_kernel<BN, EPI>;
+  using C = Cfg<BN, EPI, AR>;
+  auto kern = gemm_bf16_kernel<BN, EPI, AR>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -423,13 +384,17 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
   if (g.BN == BN_ && g.epi == EPI_) return launch_t<BN_, EPI_>(g, s);
   CVR_CASE(64, EPI_STORE)
   CVR_CASE(128, EPI_STORE)
+  CVR_CASE(256, EPI_STORE)
+  CVR_CASE(256, EPI_BIAS_RELU)
   CVR_CASE(64, EPI_BIAS_RELU)
   CVR_CASE(128, EPI_BIAS_RELU)
+  if (g.BN == 64 && g.epi == EPI_CROSS && g.K <= 256 && g.a_resident) return launch_t<64, EPI_CROSS, true>(g, s);
   CVR_CASE(64, EPI_CROSS)
   CVR_CASE(64, EPI_HEAD)
   CVR_CASE(128, EPI_HEAD)
   CVR_CASE(256, EPI_HEAD)
   CVR_CASE(128, EPI_BIAS)
+  CVR_CASE(256, EPI_BIAS)
   CVR_CASE(64, EPI_CROSS_F32)
   CVR_CASE(64, EPI_BIAS_ADD_F32)
   CVR_CASE(128, EPI_BIAS_ADD_F32)

@@ -1,0 +1,36 @@
+"""A/B the dense stage (graph-replayed) under library options, interleaved to cancel drift."""
+import os, sys, json, itertools
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch, cvr_synth as cs
+from paper_2605_29232_b200 import CvrModel
+
+cfg = cs.CONFIGS[os.environ.get("CFG", "c2")]
+B = cfg.batch
+m = CvrModel(cfg, max_batch=B, max_nnz=1 << 22)
+tabs = [s.materialize(device="cuda") for s in cs.table_specs(cfg)]
+m.load_tables(tabs); m.load_weights({k: v.cuda() for k, v in cs.make_weights(cfg).items()})
+bt = cs.make_batch(cfg, 0)
+idx, off, dense = (torch.from_numpy(bt.indices).cuda(), torch.from_numpy(bt.offsets).cuda(), torch.from_numpy(bt.dense).cuda())
+s = torch.cuda.Stream()
+x0 = m.embed(idx, off, B, dense, stream=s)
+sc = torch.empty(B, device="cuda")
+settings = json.loads(sys.argv[1]) if len(sys.argv) > 1 else [{}, {"a_resident": 0}]
+K = int(os.environ.get("K", "200"))
+res = {i: [] for i in range(len(settings))}
+for rep in range(3):
+    for i, st in enumerate(settings):
+        for k, v in st.items():
+            m.set_option(k, v)
+        for _ in range(5):
+            m.dense(x0, B, sc, stream=s)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        for _ in range(K):
+            m.dense(x0, B, sc, stream=s)
+        b.record(s); torch.cuda.synchronize()
+        res[i].append(a.elapsed_time(b) / K * 1e3)
+        for k in st:  # restore defaults
+            m.set_option(k, {"a_resident": 0, "pdl": 1, "fused_cross": 0, "graphs": 1, "stack": 0}.get(k, 1))
+for i, st in enumerate(settings):
+    print(json.dumps({"setting": st, "us_per_dense": [round(x, 2) for x in res[i]], "min": round(min(res[i]), 2)}))

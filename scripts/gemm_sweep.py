@@ -28,11 +28,11 @@ for name, M, N, K in shapes:
     C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     fl = 2 * M * N * K
     row = {"gemm": name, "M": M, "N": N, "K": K, "cublas_us": timeit(lambda: torch.matmul(A, B.T, out=C))}
-    for bn in (64, 128):
+    for bn in (64, 128, 256):
         if N % bn == 0:
             row[f"cvr_bn{bn}_us"] = timeit(lambda: gemm_bf16(A, B, C=C, bn=bn))
     row["cublas_tflops"] = fl / row["cublas_us"] / 1e6
-    for bn in (64, 128):
+    for bn in (64, 128, 256):
         if f"cvr_bn{bn}_us" in row:
             row[f"cvr_bn{bn}_tflops"] = fl / row[f"cvr_bn{bn}_us"] / 1e6
     res.append(row)

@@ -195,3 +195,37 @@ def test_c2_fused_and_unfused_cross_agree(c2):
     for s in (s_f, s_u):
         assert np.abs(s.double().cpu().numpy() - ref).max() <= TOL_BF16
     assert (s_f - s_u).abs().max().item() <= 5e-4
+
+
+def test_c2_a_resident_bitexact(c2):
+    """The resident-A U GEMM (contiguous tile runs, t loaded once per m-block) computes exactly the same
+    MMAs in the same K order as the streaming variant: bit-identical scores."""
+    cfg, m, tabs, w = c2
+    B = 777
+    bt = cs.make_batch(cfg, 31, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    s_st = m.dense(x0, B).clone()
+    m.set_option("a_resident", 1)
+    try:
+        s_ar = m.dense(x0, B).clone()
+    finally:
+        m.set_option("a_resident", 0)
+    assert torch.equal(s_ar, s_st)
+
+
+@pytest.mark.parametrize("B", [4096, 333])
+def test_c2_cross_stack_bitexact(c2, B):
+    """The persistent dependency-driven cross stack runs the same tiles, K order and epilogue as the
+    per-GEMM launches: bit-identical scores, for a full and a ragged batch."""
+    cfg, m, tabs, w = c2
+    bt = cs.make_batch(cfg, 41, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    s_plain = m.dense(x0, B).clone()
+    m.set_option("stack", 1)
+    try:
+        s_stack = m.dense(x0, B).clone()
+    finally:
+        m.set_option("stack", 0)
+    assert torch.equal(s_stack, s_plain)
