@@ -169,7 +169,8 @@ def launch_work(cfg, B) -> dict:
 
 def dense_flops_per_example(cfg) -> int:
     w = launch_work(cfg, 1)
-    layer_roles = ["gemm_xV", "gemm_tU_cross"]  # (cross_stack = n_cross x these two, one launch) + (["gemm_ens_qkv", "gemm_ens_oproj", "gemm_ens_ffn1",
+    # (cross_stack = n_cross x the two cross GEMMs in one launch)
+    layer_roles = ["gemm_xV", "gemm_tU_cross"] + (["gemm_ens_qkv", "gemm_ens_oproj", "gemm_ens_ffn1",
                                                     "gemm_ens_ffn2_ln", "mha64"] if cfg.backbone == "ensemble" else [])
     if cfg.backbone == "dcn_full":
         return int(w["dense_f32_dcn"][1])

@@ -109,6 +109,7 @@ struct cvr_ctx {
   // resident-A U GEMM 108.4, persistent cross stack 118 -- both kept as options, off by default
   bool a_resident = false;  // U GEMM keeps t resident (K = r <= 256)
   bool stack = false;       // the cross stack as one persistent dependency-driven kernel
+  bool embed_v2 = true;     // warp-batched embedding-bag kernel
   size_t off_stack_tbl = 0, off_stack_done = 0;
   // CUDA-graph cache for the executor stages (cvr_score / cvr_score_host)
   struct GraphEntry {
@@ -809,6 +810,7 @@ EmbedArgs embed_args(cvr_ctx* c, const int32_t* idx, const int32_t* off, int64_t
   a.pad_col0 = c->W;
   a.pad_col1 = c->x0_ld;
   a.flag = c->at<int>(c->off_flag);
+  a.v2 = c->embed_v2;
   return a;
 }
 
@@ -1390,6 +1392,12 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
   if (!strcmp(key, "fused_cross")) {
     if (value && !(c->backbone == CVR_DCN_LOWRANK && c->r == 256)) return c->fail(CVR_E_UNSUPPORTED, "fused cross needs r == 256");
     c->fused_cross = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    return CVR_OK;
+  }
+  if (!strcmp(key, "embed_v2")) {
+    c->embed_v2 = value != 0;
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     return CVR_OK;

@@ -39,6 +39,7 @@ struct EmbedArgs {
   int64_t dense_col0;        // first dense column (T_total * d)
   int64_t pad_col0, pad_col1;  // zero columns [pad_col0, pad_col1) of x0 rows
   int* flag;                 // sticky error flag
+  bool v2;                   // warp-batched variant (batched offsets / staged index runs)
 };
 cudaError_t launch_embed(const EmbedArgs& a, int num_sms, cudaStream_t s);
 

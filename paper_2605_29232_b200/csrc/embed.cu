@@ -146,6 +146,95 @@ __global__ void __launch_bounds__(256) embed_bag_kernel(const EmbedArgs a, int n
   }
 }
 
+// v2: warp-batched bags.  A warp owns BPW = NS * (32/LPR) consecutive bags (table-major, so they are
+// contiguous in offsets[] and their indices are one contiguous run of indices[]).  The warp loads the
+// BPW+1 offsets with ONE coalesced load, stages the whole index run in shared memory with coalesced
+// loads, then each lane group walks its bags' rows (UNROLL 16-byte loads in flight per lane).  The
+// dependent offset -> index -> row chain is paid once per BPW bags instead of once per bag.
+template <int LPR>
+struct V2Shape {
+  static constexpr int G = 32 / LPR;                                   // lane groups (bags) per pass
+  static constexpr int NS = (G >= 16) ? 1 : (G >= 8 ? 3 : (G >= 4 ? 4 : (G >= 2 ? 8 : 16)));
+  static constexpr int BPW = NS * G;                                   // bags per warp, <= 31
+  static constexpr int IDX_CAP = 512;                                  // staged indices per warp
+};
+
+template <typename TIn, typename TOut, int LPR, int UNROLL>
+__global__ void __launch_bounds__(256) embed_bag_v2_kernel(const EmbedArgs a, int n_embed_blocks) {
+  using Sh = V2Shape<LPR>;
+  constexpr int EPL = InTraits<TIn>::EPL;
+  __shared__ int sidx[8][Sh::IDX_CAP];
+  if ((int)blockIdx.x >= n_embed_blocks) {
+    dense_part<TOut>(a, blockIdx.x - n_embed_blocks, gridDim.x - n_embed_blocks);
+    return;
+  }
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int grp = lane / LPR, sub = lane & (LPR - 1);
+  const int64_t n_bags = (int64_t)a.T * a.B;
+  const int64_t total_warps = (int64_t)n_embed_blocks * (blockDim.x >> 5);
+  int* my_idx = sidx[wib];
+  for (int64_t bag0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wib) * Sh::BPW; bag0 < n_bags;
+       bag0 += total_warps * Sh::BPW) {
+    const int nb = (int)(n_bags - bag0 < Sh::BPW ? n_bags - bag0 : Sh::BPW);
+    const int64_t off_l = lane <= nb ? (int64_t)__ldg(a.offsets + bag0 + lane) : 0;
+    const int64_t base = __shfl_sync(0xffffffffu, off_l, 0);
+    const int64_t endall = __shfl_sync(0xffffffffu, off_l, nb);
+    // a bag is bad if its offsets decrease or leave [0, nnz]
+    const int64_t off_n = __shfl_down_sync(0xffffffffu, off_l, 1);
+    const bool bag_bad = lane < nb && (off_l < 0 || off_n < off_l || off_n > a.nnz);
+    const unsigned bad_mask = __ballot_sync(0xffffffffu, bag_bad);
+    const int64_t run = endall - base;
+    const bool staged = bad_mask == 0 && run >= 0 && run <= Sh::IDX_CAP;
+    if (staged) {
+      for (int k = lane; k < run; k += 32) my_idx[k] = __ldg(a.indices + base + k);
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int sl = 0; sl < Sh::NS; ++sl) {
+      const int bl = sl * Sh::G + grp;                              // bag within the warp's run
+      const int64_t st = __shfl_sync(0xffffffffu, off_l, min(bl, 31));
+      const int64_t en = __shfl_sync(0xffffffffu, off_l, min(bl + 1, 31));
+      if (bl >= nb) continue;
+      const int64_t bag = bag0 + bl;
+      const int t = (int)(bag / a.B);
+      const int b = (int)(bag - (int64_t)t * a.B);
+      const TableDesc td = a.tables[t];
+      float acc[EPL];
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
+      bool bad = (bad_mask >> bl) & 1u;
+      if (!bad) {
+        const uint8_t* colbase = td.base + sub * 16;
+        for (int64_t j = st; j < en; j += UNROLL) {
+          int idx[UNROLL];
+#pragma unroll
+          for (int u = 0; u < UNROLL; ++u) {
+            const bool live = j + u < en;
+            idx[u] = live ? (staged ? my_idx[j + u - base] : __ldg(a.indices + j + u)) : 0;
+            bad |= live && (idx[u] < 0 || (int64_t)idx[u] >= td.rows);
+          }
+          if (bad) break;
+          uint4 v[UNROLL];
+#pragma unroll
+          for (int u = 0; u < UNROLL; ++u)
+            if (j + u < en) v[u] = ptx::ld_nc_v4(colbase + (int64_t)idx[u] * td.stride);
+#pragma unroll
+          for (int u = 0; u < UNROLL; ++u)
+            if (j + u < en) InTraits<TIn>::add(acc, v[u]);
+        }
+      }
+      if (bad) {
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
+        if (sub == 0) atomicOr(a.flag, 1);
+      }
+      TOut* dst = reinterpret_cast<TOut*>(a.out) + (int64_t)b * a.out_ld + (int64_t)t * a.out_tstride + sub * EPL;
+      store_out<EPL>(dst, acc);
+    }
+    __syncwarp();
+  }
+}
+
 template <typename TIn, typename TOut, int LPR>
 cudaError_t launch_t(const EmbedArgs& a, int num_sms, cudaStream_t s) {
   const int threads = 256;
@@ -161,8 +250,16 @@ cudaError_t launch_t(const EmbedArgs& a, int num_sms, cudaStream_t s) {
     nbD = (total + threads - 1) / threads;
     if (nbD > num_sms) nbD = num_sms;
   }
+  if (a.v2) {
+    const int64_t warps = (n_bags + V2Shape<LPR>::BPW - 1) / V2Shape<LPR>::BPW;
+    nbE = (warps + 7) / 8;
+    if (nbE > capE) nbE = capE;
+  }
   if (nbE + nbD == 0) return cudaSuccess;
-  embed_bag_kernel<TIn, TOut, LPR, 4><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
+  if (a.v2)
+    embed_bag_v2_kernel<TIn, TOut, LPR, 4><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
+  else
+    embed_bag_kernel<TIn, TOut, LPR, 4><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
   return cudaGetLastError();
 }
 

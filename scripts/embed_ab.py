@@ -1,0 +1,31 @@
+"""A/B the embedding stage (graph-replayed) for embed_v2 on/off; reports us and algorithmic GB/s."""
+import os, sys, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch, cvr_synth as cs
+from paper_2605_29232_b200 import CvrModel
+cfg = cs.CONFIGS[os.environ.get("CFG", "c2")]
+B = cfg.batch
+m = CvrModel(cfg, max_batch=B, max_nnz=1 << 23)
+tabs = [s.materialize(device="cuda") for s in cs.table_specs(cfg)]
+m.load_tables(tabs); m.load_weights({k: v.cuda() for k, v in cs.make_weights(cfg).items()})
+ring = [cs.make_batch(cfg, 700 + i, index_mode=os.environ.get("IDX")) for i in range(4)]
+dev = [(torch.from_numpy(b.indices).cuda(), torch.from_numpy(b.offsets).cuda(), torch.from_numpy(b.dense).cuda()) for b in ring]
+row = cfg.dim * (4 if cfg.emb_dtype == "f32" else 2); act = 4 if cfg.act_dtype == "f32" else 2
+byts = sum(b.nnz * (row + 4) + (cfg.n_tables * B + 1) * 4 + B * cfg.n_tables * cfg.dim * act + B * cfg.n_dense * (4 + act) for b in ring) / len(ring)
+s = torch.cuda.Stream()
+x0 = m.new_x0(B)
+K = 200
+for rep in range(3):
+    for v2 in (1, 0):
+        m.set_option("embed_v2", v2)
+        for i in range(8):
+            m.embed(*dev[i % 4][:2], B, dev[i % 4][2], x0=x0, stream=s)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        for i in range(K):
+            m.embed(*dev[i % 4][:2], B, dev[i % 4][2], x0=x0, stream=s)
+        b.record(s); torch.cuda.synchronize()
+        us = a.elapsed_time(b) / K * 1e3
+        print(json.dumps({"cfg": cfg.name, "v2": v2, "us": round(us, 2), "GBps_alg": round(byts / us / 1e3, 1), "frac_hbm": round(byts / us / 1e3 / 6556.5, 3)}))
+assert m.status(s) == 0
