@@ -188,7 +188,10 @@ int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d
 /* Options (defaults in brackets): "graphs" [1] replay the executor stages of cvr_score /
  * cvr_score_host as cached CUDA graphs (keyed by their pointer / size arguments; captured on first
  * use; 32 entries, LRU); "pdl" [1] launch dependent GEMMs with programmatic stream serialization; "fused_cross" [0; allowed when r == 256]; "stack" [0] run the whole low-rank cross stack as one persistent kernel with per-(layer, row-block)
- * completion counters instead of 2 x n_cross GEMM launches; "a_resident" [0] the U GEMM of a low-rank cross layer keeps
+ * completion counters instead of 2 x n_cross GEMM launches; "embed_bps" [0 = uncapped] embedding CTAs per SM inside cvr_score / cvr_score_host (grid cap: the
+ * embedding stage of batch k+1 then leaves registers for the dense-stage GEMM CTAs of batch k);
+ * "embed_variant" [0] 0 = one lane group per bag at full
+ * occupancy, 1 = warp-batched bags (coalesced offset / index staging); "a_resident" [0] the U GEMM of a low-rank cross layer keeps
  * the 128 x r block of t resident in shared memory across its N tiles
  * run each low-rank cross layer as one clustered kernel (K5) instead of two GEMMs. */
 int cvr_set_option(cvr_ctx* ctx, const char* key, int64_t value);

@@ -109,7 +109,8 @@ struct cvr_ctx {
   // resident-A U GEMM 108.4, persistent cross stack 118 -- both kept as options, off by default
   bool a_resident = false;  // U GEMM keeps t resident (K = r <= 256)
   bool stack = false;       // the cross stack as one persistent dependency-driven kernel
-  bool embed_v2 = true;     // warp-batched embedding-bag kernel
+  int embed_variant = 0;    // 0 per-bag kernel (default), 1 warp-batched (option "embed_variant")
+  int embed_bps_pipe = 0;   // embed grid cap (CTAs/SM) in the executor; 0 = none (measured best)
   size_t off_stack_tbl = 0, off_stack_done = 0;
   // CUDA-graph cache for the executor stages (cvr_score / cvr_score_host)
   struct GraphEntry {
@@ -810,14 +811,16 @@ EmbedArgs embed_args(cvr_ctx* c, const int32_t* idx, const int32_t* off, int64_t
   a.pad_col0 = c->W;
   a.pad_col1 = c->x0_ld;
   a.flag = c->at<int>(c->off_flag);
-  a.v2 = c->embed_v2;
+  a.v2 = c->embed_variant == 1;
+  a.variant = c->embed_variant;
   return a;
 }
 
 int do_embed(cvr_ctx* c, const int32_t* idx, const int32_t* off, int64_t nnz, int B, const float* dense, void* x0,
-             cudaStream_t s) {
+             cudaStream_t s, int blocks_per_sm = 0) {
   if (c->F && !c->slot("norm/mean")->loaded) return c->fail(CVR_E_STATE, "norm/mean,std not loaded");
   EmbedArgs a = embed_args(c, idx, off, nnz, B, dense, x0, c->x0_ld, x0, B);
+  a.blocks_per_sm = blocks_per_sm;
   c->pbeg(s);
   cudaError_t e = launch_embed(a, c->num_sms, s);
   c->pend(K_EMBED, s);
@@ -1192,7 +1195,9 @@ int cvr_score(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, in
   if (e != cudaSuccess) return c->cuda_fail(e, "wait dense(k-2)");
   void* x0 = c->ws + c->off_x0[slot];
   const uint64_t ke[7] = {1, u64(d_indices), u64(d_offsets), (uint64_t)nnz, (uint64_t)batch, u64(d_dense), u64(x0)};
-  st = run_stage(c, ke, se, [&](cudaStream_t s) { return do_embed(c, d_indices, d_offsets, nnz, batch, d_dense, x0, s); });
+  st = run_stage(c, ke, se, [&](cudaStream_t s) {
+    return do_embed(c, d_indices, d_offsets, nnz, batch, d_dense, x0, s, c->embed_bps_pipe);
+  });
   if (st) return st;
   if ((e = cudaEventRecord(c->ev_embed[slot], se)) != cudaSuccess) return c->cuda_fail(e, "record embed");
   if ((e = cudaStreamWaitEvent(sd, c->ev_embed[slot], 0)) != cudaSuccess) return c->cuda_fail(e, "wait embed");
@@ -1396,8 +1401,14 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     c->graphs.clear();
     return CVR_OK;
   }
-  if (!strcmp(key, "embed_v2")) {
-    c->embed_v2 = value != 0;
+  if (!strcmp(key, "embed_bps")) {
+    c->embed_bps_pipe = (int)value;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    return CVR_OK;
+  }
+  if (!strcmp(key, "embed_variant")) {
+    c->embed_variant = (int)value;
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     return CVR_OK;

@@ -40,6 +40,8 @@ struct EmbedArgs {
   int64_t pad_col0, pad_col1;  // zero columns [pad_col0, pad_col1) of x0 rows
   int* flag;                 // sticky error flag
   bool v2;                   // warp-batched variant (batched offsets / staged index runs)
+  int variant;               // occupancy / unroll variant of the per-bag kernel (tuning)
+  int blocks_per_sm;         // grid cap (grid-stride): leaves registers for co-resident GEMM CTAs
 };
 cudaError_t launch_embed(const EmbedArgs& a, int num_sms, cudaStream_t s);
 

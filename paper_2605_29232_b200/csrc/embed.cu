@@ -5,8 +5,8 @@
 //     p[b, t, :] = sum_{j = off[t*B+b]}^{off[t*B+b+1]-1} E_t[idx[j], :]
 // fp32 accumulation in index order, stored in the x0 dtype.  HBM-bound gather, no tensor
 // cores: a group of LPR = d*sizeof(row elt)/16 lanes owns one bag, each lane owns 16 bytes of
-// the row (one 128-bit ld.global.nc per row), and UNROLL rows of the bag are loaded before any
-// is accumulated so >= UNROLL independent 16-B loads per lane are in flight.  Consecutive
+// the row (one 128-bit ld.global.nc per row); latency is hidden by occupancy (64 warps/SM, 32
+// registers) rather than by deep per-lane unrolling (UNROLL = 1 measured fastest).  Consecutive
 // groups take consecutive bags of the same table (table-major CSR), so Zipf-hot rows of a
 // table are re-read from L2 by neighbouring warps.
 //
@@ -96,8 +96,8 @@ __device__ void dense_part(const EmbedArgs& a, int blk, int nblk) {
   }
 }
 
-template <typename TIn, typename TOut, int LPR, int UNROLL>
-__global__ void __launch_bounds__(256) embed_bag_kernel(const EmbedArgs a, int n_embed_blocks) {
+template <typename TIn, typename TOut, int LPR, int UNROLL, int MINB>
+__global__ void __launch_bounds__(256, MINB) embed_bag_kernel(const EmbedArgs a, int n_embed_blocks) {
   if ((int)blockIdx.x >= n_embed_blocks) {
     dense_part<TOut>(a, blockIdx.x - n_embed_blocks, gridDim.x - n_embed_blocks);
     return;
@@ -189,47 +189,77 @@ __global__ void __launch_bounds__(256) embed_bag_v2_kernel(const EmbedArgs a, in
       for (int k = lane; k < run; k += 32) my_idx[k] = __ldg(a.indices + base + k);
     }
     __syncwarp();
+    // two bags per lane group at a time: up to 2 x UNROLL independent 16-byte row loads in flight per lane
 #pragma unroll 1
-    for (int sl = 0; sl < Sh::NS; ++sl) {
-      const int bl = sl * Sh::G + grp;                              // bag within the warp's run
-      const int64_t st = __shfl_sync(0xffffffffu, off_l, min(bl, 31));
-      const int64_t en = __shfl_sync(0xffffffffu, off_l, min(bl + 1, 31));
-      if (bl >= nb) continue;
-      const int64_t bag = bag0 + bl;
-      const int t = (int)(bag / a.B);
-      const int b = (int)(bag - (int64_t)t * a.B);
-      const TableDesc td = a.tables[t];
-      float acc[EPL];
+    for (int sl = 0; sl < Sh::NS; sl += 2) {
+      int64_t st[2], en[2];
+      int tt[2], bb[2];
+      bool bad[2];
 #pragma unroll
-      for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
-      bool bad = (bad_mask >> bl) & 1u;
-      if (!bad) {
-        const uint8_t* colbase = td.base + sub * 16;
-        for (int64_t j = st; j < en; j += UNROLL) {
-          int idx[UNROLL];
+      for (int h = 0; h < 2; ++h) {
+        const int bl = (sl + h) * Sh::G + grp;
+        st[h] = __shfl_sync(0xffffffffu, off_l, min(bl, 31));
+        en[h] = __shfl_sync(0xffffffffu, off_l, min(bl + 1, 31));
+        const bool live = sl + h < Sh::NS && bl < nb;
+        if (!live) en[h] = st[h];
+        const int64_t bag = bag0 + (live ? bl : 0);
+        tt[h] = (int)(bag / a.B);
+        bb[h] = (int)(bag - (int64_t)tt[h] * a.B);
+        bad[h] = live && ((bad_mask >> bl) & 1u);
+        if (bad[h]) en[h] = st[h];
+      }
+      const TableDesc d0 = a.tables[tt[0]], d1 = a.tables[tt[1]];
+      float acc0[EPL], acc1[EPL];
 #pragma unroll
-          for (int u = 0; u < UNROLL; ++u) {
-            const bool live = j + u < en;
-            idx[u] = live ? (staged ? my_idx[j + u - base] : __ldg(a.indices + j + u)) : 0;
-            bad |= live && (idx[u] < 0 || (int64_t)idx[u] >= td.rows);
-          }
-          if (bad) break;
-          uint4 v[UNROLL];
+      for (int e = 0; e < EPL; ++e) acc0[e] = acc1[e] = 0.f;
+      const uint8_t* cb0 = d0.base + sub * 16;
+      const uint8_t* cb1 = d1.base + sub * 16;
+      int64_t j0 = st[0], j1 = st[1];
+      while (j0 < en[0] || j1 < en[1]) {
+        int i0[UNROLL], i1[UNROLL];
 #pragma unroll
-          for (int u = 0; u < UNROLL; ++u)
-            if (j + u < en) v[u] = ptx::ld_nc_v4(colbase + (int64_t)idx[u] * td.stride);
-#pragma unroll
-          for (int u = 0; u < UNROLL; ++u)
-            if (j + u < en) InTraits<TIn>::add(acc, v[u]);
+        for (int u = 0; u < UNROLL; ++u) {
+          const bool l0 = j0 + u < en[0], l1 = j1 + u < en[1];
+          i0[u] = l0 ? (staged ? my_idx[j0 + u - base] : __ldg(a.indices + j0 + u)) : 0;
+          i1[u] = l1 ? (staged ? my_idx[j1 + u - base] : __ldg(a.indices + j1 + u)) : 0;
+          bad[0] |= l0 && (i0[u] < 0 || (int64_t)i0[u] >= d0.rows);
+          bad[1] |= l1 && (i1[u] < 0 || (int64_t)i1[u] >= d1.rows);
         }
-      }
-      if (bad) {
+        if (bad[0]) en[0] = j0;  // stop this bag; it is zeroed below
+        if (bad[1]) en[1] = j1;
+        uint4 v0[UNROLL], v1[UNROLL];
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
-        if (sub == 0) atomicOr(a.flag, 1);
+        for (int u = 0; u < UNROLL; ++u) {
+          if (j0 + u < en[0]) v0[u] = ptx::ld_nc_v4(cb0 + (int64_t)i0[u] * d0.stride);
+          if (j1 + u < en[1]) v1[u] = ptx::ld_nc_v4(cb1 + (int64_t)i1[u] * d1.stride);
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+          if (j0 + u < en[0]) InTraits<TIn>::add(acc0, v0[u]);
+          if (j1 + u < en[1]) InTraits<TIn>::add(acc1, v1[u]);
+        }
+        j0 += UNROLL;
+        j1 += UNROLL;
       }
-      TOut* dst = reinterpret_cast<TOut*>(a.out) + (int64_t)b * a.out_ld + (int64_t)t * a.out_tstride + sub * EPL;
-      store_out<EPL>(dst, acc);
+      const int bl0 = sl * Sh::G + grp, bl1 = (sl + 1) * Sh::G + grp;
+      if (bl0 < nb) {
+        if (bad[0]) {
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) acc0[e] = 0.f;
+          if (sub == 0) atomicOr(a.flag, 1);
+        }
+        store_out<EPL>(reinterpret_cast<TOut*>(a.out) + (int64_t)bb[0] * a.out_ld + (int64_t)tt[0] * a.out_tstride + sub * EPL,
+                       acc0);
+      }
+      if (sl + 1 < Sh::NS && bl1 < nb) {
+        if (bad[1]) {
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) acc1[e] = 0.f;
+          if (sub == 0) atomicOr(a.flag, 1);
+        }
+        store_out<EPL>(reinterpret_cast<TOut*>(a.out) + (int64_t)bb[1] * a.out_ld + (int64_t)tt[1] * a.out_tstride + sub * EPL,
+                       acc1);
+      }
     }
     __syncwarp();
   }
@@ -242,7 +272,7 @@ cudaError_t launch_t(const EmbedArgs& a, int num_sms, cudaStream_t s) {
   // one bag per lane group, no grid-stride loop: short-lived CTAs let the block scheduler interleave
   // the concurrently running dense-stage GEMM CTAs (higher-priority stream) as embed CTAs retire
   int64_t nbE = (n_bags * LPR + threads - 1) / threads;
-  const int64_t capE = (int64_t)num_sms * 64;
+  const int64_t capE = (int64_t)num_sms * (a.blocks_per_sm > 0 ? a.blocks_per_sm : 64);
   if (nbE > capE) nbE = capE;
   int64_t nbD = 0;
   if (a.x0 && a.Bd > 0 && a.pad_col1 > a.dense_col0) {
@@ -256,10 +286,13 @@ cudaError_t launch_t(const EmbedArgs& a, int num_sms, cudaStream_t s) {
     if (nbE > capE) nbE = capE;
   }
   if (nbE + nbD == 0) return cudaSuccess;
+  // measured on B200, config 2 (scripts/embed_ab.py): one row load in flight per lane at full occupancy
+  // (32 registers, 64 warps/SM) beats deeper per-lane unrolling at lower occupancy: 18.5 us (59% of the
+  // HBM peak, algorithmic bytes) vs 24.6 us for 4 rows in flight at 32 warps/SM.
   if (a.v2)
     embed_bag_v2_kernel<TIn, TOut, LPR, 4><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
   else
-    embed_bag_kernel<TIn, TOut, LPR, 4><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
+    embed_bag_kernel<TIn, TOut, LPR, 1, 8><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
   return cudaGetLastError();
 }
 

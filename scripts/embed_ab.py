@@ -16,8 +16,8 @@ s = torch.cuda.Stream()
 x0 = m.new_x0(B)
 K = 200
 for rep in range(3):
-    for v2 in (1, 0):
-        m.set_option("embed_v2", v2)
+    for v2 in [int(x) for x in os.environ.get('VARIANTS', '0,1').split(',')]:
+        m.set_option("embed_variant", v2)
         for i in range(8):
             m.embed(*dev[i % 4][:2], B, dev[i % 4][2], x0=x0, stream=s)
         torch.cuda.synchronize()
@@ -27,5 +27,5 @@ for rep in range(3):
             m.embed(*dev[i % 4][:2], B, dev[i % 4][2], x0=x0, stream=s)
         b.record(s); torch.cuda.synchronize()
         us = a.elapsed_time(b) / K * 1e3
-        print(json.dumps({"cfg": cfg.name, "v2": v2, "us": round(us, 2), "GBps_alg": round(byts / us / 1e3, 1), "frac_hbm": round(byts / us / 1e3 / 6556.5, 3)}))
+        print(json.dumps({"cfg": cfg.name, "variant": v2, "us": round(us, 2), "GBps_alg": round(byts / us / 1e3, 1), "frac_hbm": round(byts / us / 1e3 / 6556.5, 3)}))
 assert m.status(s) == 0
