@@ -162,7 +162,9 @@ def launch_work(cfg, B) -> dict:
         S, D, F, H = cfg.n_tables, cfg.dim, cfg.ffn_dim, cfg.n_heads
         BT = B * S
         w.update({"gemm_ens_qkv": ("tensor", 2 * BT * D * 3 * D), "gemm_ens_oproj": ("tensor", 2 * BT * D * D),
-                  "gemm_ens_ffn1": ("tensor", 2 * BT * D * F), "gemm_ens_ffn2_ln": ("tensor", 2 * BT * F * D),
+                  "gemm_ens_ffn1": ("tensor", 2 * BT * D * F),
+                  # out-projection and FFN2 run as one GEMM over [O | h] (K = D + F)
+                  "gemm_ens_ffn2_ln": ("tensor", 2 * BT * (F + D) * D),
                   "mha64": ("tensor", 4 * B * H * S * S * (D // H))})
     return w
 
@@ -170,7 +172,7 @@ def launch_work(cfg, B) -> dict:
 def dense_flops_per_example(cfg) -> int:
     w = launch_work(cfg, 1)
     # (cross_stack = n_cross x the two cross GEMMs in one launch)
-    layer_roles = ["gemm_xV", "gemm_tU_cross"] + (["gemm_ens_qkv", "gemm_ens_oproj", "gemm_ens_ffn1",
+    layer_roles = ["gemm_xV", "gemm_tU_cross"] + (["gemm_ens_qkv", "gemm_ens_ffn1",
                                                     "gemm_ens_ffn2_ln", "mha64"] if cfg.backbone == "ensemble" else [])
     if cfg.backbone == "dcn_full":
         return int(w["dense_f32_dcn"][1])

@@ -92,10 +92,13 @@ struct cvr_ctx {
   bool fused_cross = false;                       // K5 (r == 256)
   // ensemble (config 4) buffers and maps
   struct Ens {
-    size_t off_S = 0, off_qkv = 0, off_O = 0, off_hf = 0;
+    // cat = [O | FFN hidden] per token: the out-projection and FFN2 become ONE GEMM with K = D + ffn
+    // against [Wo | W2] (their outputs are summed anyway, A20), saving a launch and an fp32 round trip
+    size_t off_S = 0, off_qkv = 0, off_cat = 0;
+    std::vector<size_t> off_catW, off_catb;
     CUtensorMap flat_x0[2], tok_x0[2], flat_xa, flat_xb, tok_xa, tok_xb, sttok_xa, sttok_xb;
-    CUtensorMap st_qkv, tm_O, st_hf, tm_hf;
-    std::vector<CUtensorMap> V, U, Wqkv, Wo, W1, W2;
+    CUtensorMap st_qkv, st_hf, tm_cat;
+    std::vector<CUtensorMap> V, U, Wqkv, W1, Wcat;
     CUtensorMap flat_user, tok_user;
   } ens;
   size_t off_hpart = 0;   // split-head partial dot products [max_batch, last/256]
@@ -398,8 +401,11 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
     c->off_t = carve(cur, (size_t)B * c->r * 2);
     c->ens.off_S = carve(cur, (size_t)B * c->x0_ld * 4);
     c->ens.off_qkv = carve(cur, (size_t)BT * 3 * c->d * 2);
-    c->ens.off_O = carve(cur, (size_t)BT * c->d * 2);
-    c->ens.off_hf = carve(cur, (size_t)BT * c->ffn * 2);
+    c->ens.off_cat = carve(cur, (size_t)BT * (c->d + c->ffn) * 2);
+    for (int l = 0; l < c->n_cross; ++l) {
+      c->ens.off_catW.push_back(carve(cur, (size_t)c->d * (c->d + c->ffn) * 2));
+      c->ens.off_catb.push_back(carve(cur, (size_t)c->d * 4));
+    }
     for (int i = 0; i + 1 < c->n_mlp; ++i) c->off_h.push_back(carve(cur, (size_t)B * c->mlp[i] * 2));
   }
   if (c->backbone != CVR_DCN_FULL) {
@@ -554,9 +560,9 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     ok &= encode_tmap_bf16(&c->tm_t, c->ws + c->off_t, B, c->r, c->r, 128, &er) == 0;
     ok &= encode_tmap_bf16(&c->st_t, c->ws + c->off_t, B, c->r, c->r, 32, &er) == 0;
     ok &= encode_tmap_bf16(&E.st_qkv, c->ws + E.off_qkv, BT, 3 * D, 3 * D, 32, &er) == 0;
-    ok &= encode_tmap_bf16(&E.tm_O, c->ws + E.off_O, BT, D, D, 128, &er) == 0;
-    ok &= encode_tmap_bf16(&E.st_hf, c->ws + E.off_hf, BT, c->ffn, c->ffn, 32, &er) == 0;
-    ok &= encode_tmap_bf16(&E.tm_hf, c->ws + E.off_hf, BT, c->ffn, c->ffn, 128, &er) == 0;
+    const int64_t CW = D + c->ffn;
+    ok &= encode_tmap_bf16(&E.st_hf, c->ws + E.off_cat + D * 2, BT, c->ffn, CW, 32, &er) == 0;
+    ok &= encode_tmap_bf16(&E.tm_cat, c->ws + E.off_cat, BT, CW, CW, 128, &er) == 0;
     c->tm_h.resize(c->off_h.size());
     c->st_h.resize(c->off_h.size());
     for (size_t i = 0; i < c->off_h.size(); ++i) {
@@ -634,18 +640,27 @@ int encode_plan_ensemble(cvr_ctx* c) {
   E.V.assign(c->n_cross, {});
   E.U.assign(c->n_cross, {});
   E.Wqkv.assign(c->n_cross, {});
-  E.Wo.assign(c->n_cross, {});
   E.W1.assign(c->n_cross, {});
-  E.W2.assign(c->n_cross, {});
+  E.Wcat.assign(c->n_cross, {});
   bool ok = true;
   for (int l = 0; l < c->n_cross; ++l) {
     const std::string p = "ens/" + std::to_string(l) + "/";
     ok &= encode_tmap_bf16(&E.V[l], c->wptr(p + "dcn/V"), r, W, W, 128, &er) == 0;
     ok &= encode_tmap_bf16(&E.U[l], c->wptr(p + "dcn/U"), W, r, r, 64, &er) == 0;
     ok &= encode_tmap_bf16(&E.Wqkv[l], c->wptr(p + "mha/Wqkv"), 3 * D, D, D, 256, &er) == 0;
-    ok &= encode_tmap_bf16(&E.Wo[l], c->wptr(p + "mha/Wo"), D, D, D, 128, &er) == 0;
     ok &= encode_tmap_bf16(&E.W1[l], c->wptr(p + "ffn/W1"), F, D, D, 256, &er) == 0;
-    ok &= encode_tmap_bf16(&E.W2[l], c->wptr(p + "ffn/W2"), D, F, F, 256, &er) == 0;
+    // [Wo | W2] and bo + b2, assembled in the workspace from the loaded copies
+    cudaError_t e1 = cudaMemcpy2D(c->ws + E.off_catW[l], (size_t)(D + F) * 2, c->wptr(p + "mha/Wo"), (size_t)D * 2,
+                                  (size_t)D * 2, D, cudaMemcpyDeviceToDevice);
+    cudaError_t e2 = cudaMemcpy2D(c->ws + E.off_catW[l] + (size_t)D * 2, (size_t)(D + F) * 2, c->wptr(p + "ffn/W2"),
+                                  (size_t)F * 2, (size_t)F * 2, D, cudaMemcpyDeviceToDevice);
+    std::vector<float> bo(D), b2(D);
+    cudaError_t e3 = cudaMemcpy(bo.data(), c->wptr(p + "mha/bo"), D * 4, cudaMemcpyDeviceToHost);
+    cudaError_t e4 = cudaMemcpy(b2.data(), c->wptr(p + "ffn/b2"), D * 4, cudaMemcpyDeviceToHost);
+    for (int i = 0; i < D; ++i) bo[i] += b2[i];
+    cudaError_t e5 = cudaMemcpy(c->ws + E.off_catb[l], bo.data(), D * 4, cudaMemcpyHostToDevice);
+    if (e1 || e2 || e3 || e4 || e5) return c->fail(CVR_E_CUDA, "assembling [Wo | W2]");
+    ok &= encode_tmap_bf16(&E.Wcat[l], c->ws + E.off_catW[l], D, D + F, D + F, 256, &er) == 0;
   }
   if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
   // head MLP: same plan as the low-rank path (GemmPlan per mlp layer)
@@ -926,30 +941,25 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     a3.tmOut = &E.st_qkv;
     a3.bias = c->wptr<float>(p + "mha/bqkv");
     if ((e = run_gemm(c, a3, K_ENS_QKV, s)) != cudaSuccess) return c->cuda_fail(e, "ens qkv");
+    __nv_bfloat16* cat = c->at<__nv_bfloat16>(E.off_cat);
     c->pbeg(s);
-    e = launch_mha64(c->at<__nv_bfloat16>(E.off_qkv), c->at<__nv_bfloat16>(E.off_O), B, c->n_heads, s);
+    e = launch_mha64(c->at<__nv_bfloat16>(E.off_qkv), cat, D + c->ffn, B, c->n_heads, s);  // O -> cat[:, :D]
     c->pend(K_MHA, s);
     if (e != cudaSuccess) return c->cuda_fail(e, "mha64");
-    GemmArgs a4 = ga(&E.tm_O, &E.Wo[l], BT, D, D, 128, EPI_BIAS_ADD_F32);
-    a4.bias = c->wptr<float>(p + "mha/bo");
-    a4.in_f32 = S;
-    a4.ld_in = D;
-    a4.out_f32 = S;
-    a4.ld_f32 = D;
-    if ((e = run_gemm(c, a4, K_ENS_OPROJ, s)) != cudaSuccess) return c->cuda_fail(e, "ens oproj");
-    // FFN branch + branch sum + LN: X' = LN(W2 ReLU(W1 X + b1) + b2 + S) * gamma + beta
+    // FFN hidden -> cat[:, D:]
     GemmArgs a5 = ga(tok_xl, &E.W1[l], BT, c->ffn, D, 256, EPI_BIAS_RELU);
     a5.tmOut = &E.st_hf;
     a5.bias = c->wptr<float>(p + "ffn/b1");
     if ((e = run_gemm(c, a5, K_ENS_FFN1, s)) != cudaSuccess) return c->cuda_fail(e, "ens ffn1");
-    GemmArgs a6 = ga(&E.tm_hf, &E.W2[l], BT, D, c->ffn, 256, EPI_SUM_LN);
+    // X' = LN([O | h] [Wo | W2]^T + (bo + b2) + S) * gamma + beta   (S = DCN branch, fp32)
+    GemmArgs a6 = ga(&E.tm_cat, &E.Wcat[l], BT, D, D + c->ffn, 256, EPI_SUM_LN);
     a6.tmOut = even ? &E.sttok_xa : &E.sttok_xb;
-    a6.bias = c->wptr<float>(p + "ffn/b2");
+    a6.bias = c->at<float>(E.off_catb[l]);
     a6.in_f32 = S;
     a6.ld_in = D;
     a6.gamma = c->wptr<float>(p + "ln/gamma");
     a6.beta = c->wptr<float>(p + "ln/beta");
-    if ((e = run_gemm(c, a6, K_ENS_FFN2_LN, s)) != cudaSuccess) return c->cuda_fail(e, "ens ffn2+ln");
+    if ((e = run_gemm(c, a6, K_ENS_FFN2_LN, s)) != cudaSuccess) return c->cuda_fail(e, "ens out-proj+ffn2+ln");
     flat_xl = even ? &E.flat_xa : &E.flat_xb;
     tok_xl = even ? &E.tok_xa : &E.tok_xb;
   }

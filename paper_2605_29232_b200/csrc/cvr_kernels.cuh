@@ -111,7 +111,7 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s);
 
 // ---- K7: multi-head self-attention over the 64 tokens of each example (config 4) ------------------
 // qkv [B*S, 3*D] bf16 (Q | K | V, head h at columns h*64 of each), out [B*S, D] bf16; S = 64, dh = 64.
-cudaError_t launch_mha64(const __nv_bfloat16* qkv, __nv_bfloat16* out, int B, int n_heads, cudaStream_t s);
+cudaError_t launch_mha64(const __nv_bfloat16* qkv, __nv_bfloat16* out, int out_ld, int B, int n_heads, cudaStream_t s);
 // scores[m] = sigmoid(sum_j partial[m][j] + c), j in fixed order (EPI_HEAD_PARTIAL finaliser)
 cudaError_t launch_head_finalize(const float* partial, int n_parts, float c, float* scores, int M, cudaStream_t s);
 

@@ -33,7 +33,7 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
 
 template <int H>
 __global__ void __launch_bounds__(256) mha64_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ out,
-                                                    int B) {
+                                                    int B, int out_ld) {
   constexpr int D = H * DH;           // model width (256 for 4 heads)
   extern __shared__ __align__(16) uint8_t mha_smem[];
   __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(mha_smem);
@@ -134,8 +134,8 @@ __global__ void __launch_bounds__(256) mha64_kernel(const __nv_bfloat16* __restr
         }
       }
       // ---- write O rows r0+g, r0+g+8, columns h*64 + nt*8 + 2t (+1)
-      __nv_bfloat16* o0 = out + ((size_t)b * S + r0 + g) * D + h * DH;
-      __nv_bfloat16* o1 = out + ((size_t)b * S + r0 + g + 8) * D + h * DH;
+      __nv_bfloat16* o0 = out + ((size_t)b * S + r0 + g) * out_ld + h * DH;
+      __nv_bfloat16* o1 = out + ((size_t)b * S + r0 + g + 8) * out_ld + h * DH;
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt) {
         *reinterpret_cast<uint32_t*>(o0 + nt * 8 + 2 * t) = ptx::pack_bf16(oc[nt][0], oc[nt][1]);
@@ -162,7 +162,7 @@ __global__ void head_finalize_kernel(const float* __restrict__ part, int n_parts
 
 }  // namespace
 
-cudaError_t launch_mha64(const __nv_bfloat16* qkv, __nv_bfloat16* out, int B, int n_heads, cudaStream_t s) {
+cudaError_t launch_mha64(const __nv_bfloat16* qkv, __nv_bfloat16* out, int out_ld, int B, int n_heads, cudaStream_t s) {
   if (B <= 0) return cudaSuccess;
   if (n_heads != 4) return cudaErrorInvalidValue;
   constexpr int smem = (2 * S * QK_LD + 4 * DH * VT_LD) * 2;
@@ -172,7 +172,7 @@ cudaError_t launch_mha64(const __nv_bfloat16* qkv, __nv_bfloat16* out, int B, in
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  mha64_kernel<4><<<B, 256, smem, s>>>(qkv, out, B);
+  mha64_kernel<4><<<B, 256, smem, s>>>(qkv, out, B, out_ld);
   return cudaGetLastError();
 }
 
