@@ -112,6 +112,7 @@ struct cvr_ctx {
   // resident-A U GEMM 108.4, persistent cross stack 118 -- both kept as options, off by default
   bool a_resident = false;  // U GEMM keeps t resident (K = r <= 256)
   bool stack = false;       // the cross stack as one persistent dependency-driven kernel
+  int ens_u_bn = 128;       // N tile of the ensemble DCN U GEMM (option "ens_u_bn": 64 | 128)
   int embed_variant = 0;    // 0 per-bag kernel (default), 1 warp-batched (option "embed_variant")
   int embed_bps_pipe = 0;   // embed grid cap (CTAs/SM) in the executor; 0 = none (measured best)
   size_t off_stack_tbl = 0, off_stack_done = 0;
@@ -646,7 +647,7 @@ int encode_plan_ensemble(cvr_ctx* c) {
   for (int l = 0; l < c->n_cross; ++l) {
     const std::string p = "ens/" + std::to_string(l) + "/";
     ok &= encode_tmap_bf16(&E.V[l], c->wptr(p + "dcn/V"), r, W, W, 128, &er) == 0;
-    ok &= encode_tmap_bf16(&E.U[l], c->wptr(p + "dcn/U"), W, r, r, 64, &er) == 0;
+    ok &= encode_tmap_bf16(&E.U[l], c->wptr(p + "dcn/U"), W, r, r, c->ens_u_bn, &er) == 0;
     ok &= encode_tmap_bf16(&E.Wqkv[l], c->wptr(p + "mha/Wqkv"), 3 * D, D, D, 256, &er) == 0;
     ok &= encode_tmap_bf16(&E.W1[l], c->wptr(p + "ffn/W1"), F, D, D, 256, &er) == 0;
     // [Wo | W2] and bo + b2, assembled in the workspace from the loaded copies
@@ -929,7 +930,7 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     GemmArgs a1 = ga(flat_xl, &E.V[l], B, r, W, 128, EPI_STORE);
     a1.tmOut = &c->st_t;
     if ((e = run_gemm(c, a1, K_GEMM_V, s)) != cudaSuccess) return c->cuda_fail(e, "ens V");
-    GemmArgs a2 = ga(&c->tm_t, &E.U[l], B, W, r, 64, EPI_CROSS_F32);
+    GemmArgs a2 = ga(&c->tm_t, &E.U[l], B, W, r, c->ens_u_bn, EPI_CROSS_F32);
     a2.tmX0 = flat_x0;
     a2.tmXl = flat_xl;
     a2.bias = c->wptr<float>(p + "dcn/b");
@@ -1409,6 +1410,14 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     c->fused_cross = value != 0;
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
+    return CVR_OK;
+  }
+  if (!strcmp(key, "ens_u_bn")) {
+    if (value != 64 && value != 128) return c->fail(CVR_E_ARG, "ens_u_bn must be 64 or 128");
+    c->ens_u_bn = (int)value;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    if (c->weights_loaded && c->backbone == CVR_ENSEMBLE) return encode_plan_ensemble(c);
     return CVR_OK;
   }
   if (!strcmp(key, "embed_bps")) {

@@ -396,6 +396,7 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
   CVR_CASE(128, EPI_BIAS)
   CVR_CASE(256, EPI_BIAS)
   CVR_CASE(64, EPI_CROSS_F32)
+  CVR_CASE(128, EPI_CROSS_F32)
   CVR_CASE(64, EPI_BIAS_ADD_F32)
   CVR_CASE(128, EPI_BIAS_ADD_F32)
   CVR_CASE(256, EPI_SUM_LN)
