@@ -188,7 +188,8 @@ int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d
 /* Options (defaults in brackets): "graphs" [1] replay the executor stages of cvr_score /
  * cvr_score_host as cached CUDA graphs (keyed by their pointer / size arguments; captured on first
  * use; 32 entries, LRU); "pdl" [1] launch dependent GEMMs with programmatic stream serialization; "fused_cross" [0; allowed when r == 256]; "stack" [0] run the whole low-rank cross stack as one persistent kernel with per-(layer, row-block)
- * completion counters instead of 2 x n_cross GEMM launches; "embed_bps" [0 = uncapped] embedding CTAs per SM inside cvr_score / cvr_score_host (grid cap: the
+ * completion counters instead of 2 x n_cross GEMM launches; "pair" [1] 2-CTA (cta_group::2, 256-row) tiles for the ensemble path's GEMMs; "ens_u_bn" [128] N tile of the
+ * ensemble DCN U GEMM; "embed_bps" [0 = uncapped] embedding CTAs per SM inside cvr_score / cvr_score_host (grid cap: the
  * embedding stage of batch k+1 then leaves registers for the dense-stage GEMM CTAs of batch k);
  * "embed_variant" [0] 0 = one lane group per bag at full
  * occupancy, 1 = warp-batched bags (coalesced offset / index staging); "a_resident" [0] the U GEMM of a low-rank cross layer keeps
@@ -200,7 +201,8 @@ int cvr_set_option(cvr_ctx* ctx, const char* key, int64_t value);
  * C[M, N] = A[M, K] . B[N, K]^T on the same tcgen05/TMA kernel the dense stage uses (tests and
  * tile tuning): bf16 row-major operands with leading dimensions lda/ldb/ldc (elements, multiples
  * of 8), fp32 accumulation, bf16 output; epi 0 = plain store, 1 = ReLU(C + bias[N]) (fp32 bias).
- * K % 64 == 0, N % bn == 0, bn in {64, 128}.  Enqueued on `stream`. */
+ * K % 64 == 0, N % bn == 0, bn in {64, 128, 256}; epi | 0x100 selects the 2-CTA (cta_group::2, 256-row
+ * tile per CTA pair) variant.  Enqueued on `stream`. */
 int cvr_gemm_bf16(const void* d_A, int64_t lda, const void* d_B, int64_t ldb, void* d_C, int64_t ldc, int M, int N,
                   int K, int epi, const float* d_bias, int bn, cvr_stream_t stream);
 

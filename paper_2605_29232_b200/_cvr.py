@@ -116,13 +116,13 @@ def _stream(s) -> Optional[int]:
 
 
 def gemm_bf16(A: torch.Tensor, B: torch.Tensor, C: Optional[torch.Tensor] = None, bias: Optional[torch.Tensor] = None,
-              bn: int = 64, stream=None) -> torch.Tensor:
+              bn: int = 64, stream=None, pair: bool = False) -> torch.Tensor:
     """C = A @ B^T (bf16, fp32 accumulate) [+ bias, ReLU] on libcvr's tcgen05 GEMM (cvr_gemm_bf16)."""
     M, K = A.shape
     N = B.shape[0]
     C = torch.empty(M, N, dtype=torch.bfloat16, device=A.device) if C is None else C
     st = lib().cvr_gemm_bf16(A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0), C.data_ptr(), C.stride(0), M, N, K,
-                             0 if bias is None else 1, _ptr(bias), bn, _stream(stream))
+                             (0 if bias is None else 1) | (0x100 if pair else 0), _ptr(bias), bn, _stream(stream))
     if st != 0:
         raise CvrError(st, "cvr_gemm_bf16")
     return C

@@ -48,6 +48,7 @@ struct WSlot {
 struct GemmPlan {
   int N, K, BN;
   Epi epi;
+  bool pair = false;  // 2-CTA (cta_group::2) tiles; B map box = BN/2 rows
   const char* wname;  // B operand
   CUtensorMap tmB;
 };
@@ -113,6 +114,7 @@ struct cvr_ctx {
   bool a_resident = false;  // U GEMM keeps t resident (K = r <= 256)
   bool stack = false;       // the cross stack as one persistent dependency-driven kernel
   int ens_u_bn = 128;       // N tile of the ensemble DCN U GEMM (option "ens_u_bn": 64 | 128)
+  bool pair_ens = true;     // 2-CTA tiles for the ensemble path's GEMMs (option "pair")
   int embed_variant = 0;    // 0 per-bag kernel (default), 1 warp-batched (option "embed_variant")
   int embed_bps_pipe = 0;   // embed grid cap (CTAs/SM) in the executor; 0 = none (measured best)
   size_t off_stack_tbl = 0, off_stack_done = 0;
@@ -646,10 +648,11 @@ int encode_plan_ensemble(cvr_ctx* c) {
   bool ok = true;
   for (int l = 0; l < c->n_cross; ++l) {
     const std::string p = "ens/" + std::to_string(l) + "/";
-    ok &= encode_tmap_bf16(&E.V[l], c->wptr(p + "dcn/V"), r, W, W, 128, &er) == 0;
-    ok &= encode_tmap_bf16(&E.U[l], c->wptr(p + "dcn/U"), W, r, r, c->ens_u_bn, &er) == 0;
-    ok &= encode_tmap_bf16(&E.Wqkv[l], c->wptr(p + "mha/Wqkv"), 3 * D, D, D, 256, &er) == 0;
-    ok &= encode_tmap_bf16(&E.W1[l], c->wptr(p + "ffn/W1"), F, D, D, 256, &er) == 0;
+    const int dv = c->pair_ens ? 2 : 1;  // B boxes hold BN/2 rows per CTA of a pair
+    ok &= encode_tmap_bf16(&E.V[l], c->wptr(p + "dcn/V"), r, W, W, 128 / dv, &er) == 0;
+    ok &= encode_tmap_bf16(&E.U[l], c->wptr(p + "dcn/U"), W, r, r, c->ens_u_bn / dv, &er) == 0;
+    ok &= encode_tmap_bf16(&E.Wqkv[l], c->wptr(p + "mha/Wqkv"), 3 * D, D, D, 256 / dv, &er) == 0;
+    ok &= encode_tmap_bf16(&E.W1[l], c->wptr(p + "ffn/W1"), F, D, D, 256 / dv, &er) == 0;
     // [Wo | W2] and bo + b2, assembled in the workspace from the loaded copies
     cudaError_t e1 = cudaMemcpy2D(c->ws + E.off_catW[l], (size_t)(D + F) * 2, c->wptr(p + "mha/Wo"), (size_t)D * 2,
                                   (size_t)D * 2, D, cudaMemcpyDeviceToDevice);
@@ -661,7 +664,7 @@ int encode_plan_ensemble(cvr_ctx* c) {
     for (int i = 0; i < D; ++i) bo[i] += b2[i];
     cudaError_t e5 = cudaMemcpy(c->ws + E.off_catb[l], bo.data(), D * 4, cudaMemcpyHostToDevice);
     if (e1 || e2 || e3 || e4 || e5) return c->fail(CVR_E_CUDA, "assembling [Wo | W2]");
-    ok &= encode_tmap_bf16(&E.Wcat[l], c->ws + E.off_catW[l], D, D + F, D + F, 256, &er) == 0;
+    ok &= encode_tmap_bf16(&E.Wcat[l], c->ws + E.off_catW[l], D, D + F, D + F, 256 / dv, &er) == 0;
   }
   if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
   // head MLP: same plan as the low-rank path (GemmPlan per mlp layer)
@@ -675,7 +678,8 @@ int encode_plan_ensemble(cvr_ctx* c) {
     g.BN = last ? (c->head_parts ? 256 : c->mlp[i]) : pick_bn(c->mlp[i], c->max_batch);
     g.epi = last ? (c->head_parts ? EPI_HEAD_PARTIAL : EPI_HEAD) : EPI_BIAS_RELU;
     g.wname = nullptr;
-    if (encode_tmap_bf16(&g.tmB, c->wptr("mlp/" + std::to_string(i) + "/W"), g.N, K, K, g.BN, &er) != 0)
+    g.pair = c->pair_ens;
+    if (encode_tmap_bf16(&g.tmB, c->wptr("mlp/" + std::to_string(i) + "/W"), g.N, K, K, g.pair ? g.BN / 2 : g.BN, &er) != 0)
       return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
     c->plan.push_back(g);
     K = c->mlp[i];
@@ -855,6 +859,7 @@ GemmArgs gemm_args(cvr_ctx* c, const GemmPlan& g, const CUtensorMap* A, int M) {
   a.epi = g.epi;
   a.num_sms = c->num_sms;
   a.pdl = c->pdl;
+  a.cta_pair = g.pair;
   return a;
 }
 
@@ -920,6 +925,7 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     a.epi = epi;
     a.num_sms = c->num_sms;
     a.pdl = c->pdl;
+    a.cta_pair = c->pair_ens;
     return a;
   };
   (void)gp;
@@ -1369,6 +1375,8 @@ int cvr_profile_end(cvr_ctx* c, cvr_kernel_stat* out, int max_out, int* n_out) {
 
 int cvr_gemm_bf16(const void* d_A, int64_t lda, const void* d_B, int64_t ldb, void* d_C, int64_t ldc, int M, int N,
                   int K, int epi, const float* d_bias, int bn, cvr_stream_t stream) {
+  const bool pair = (epi & 0x100) != 0;
+  epi &= 0xFF;
   if (!d_A || !d_B || !d_C || M < 0 || N <= 0 || K <= 0 || (epi == 1 && !d_bias)) return CVR_E_ARG;
   if (epi != 0 && epi != 1) return CVR_E_ARG;
   if (K % 64 || N % bn || (bn != 64 && bn != 128 && bn != 256) || lda < K || ldb < K || ldc < N || (lda | ldb | ldc) & 7)
@@ -1376,7 +1384,7 @@ int cvr_gemm_bf16(const void* d_A, int64_t lda, const void* d_B, int64_t ldb, vo
   if (M == 0) return CVR_OK;
   const char* er = nullptr;
   CUtensorMap ta, tb, tc;
-  if (encode_tmap_bf16(&ta, d_A, M, K, lda, 128, &er) || encode_tmap_bf16(&tb, d_B, N, K, ldb, bn, &er) ||
+  if (encode_tmap_bf16(&ta, d_A, M, K, lda, 128, &er) || encode_tmap_bf16(&tb, d_B, N, K, ldb, pair ? bn / 2 : bn, &er) ||
       encode_tmap_bf16(&tc, d_C, M, N, ldc, 32, &er))
     return CVR_E_CUDA;
   int dev = 0, sms = 148;
@@ -1394,6 +1402,7 @@ int cvr_gemm_bf16(const void* d_A, int64_t lda, const void* d_B, int64_t ldb, vo
   a.epi = epi == 0 ? EPI_STORE : EPI_BIAS_RELU;
   a.num_sms = sms;
   a.pdl = false;
+  a.cta_pair = pair;
   return launch_gemm_bf16(a, (cudaStream_t)stream) == cudaSuccess ? CVR_OK : CVR_E_CUDA;
 }
 
@@ -1410,6 +1419,13 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     c->fused_cross = value != 0;
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
+    return CVR_OK;
+  }
+  if (!strcmp(key, "pair")) {
+    c->pair_ens = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    if (c->weights_loaded && c->backbone == CVR_ENSEMBLE) return encode_plan_ensemble(c);
     return CVR_OK;
   }
   if (!strcmp(key, "ens_u_bn")) {

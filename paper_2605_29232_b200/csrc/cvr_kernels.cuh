@@ -103,6 +103,7 @@ struct GemmArgs {
   int num_sms;
   bool pdl;                  // launch with programmatic stream serialization
   bool a_resident;           // K <= 256: keep the A block resident, contiguous tile runs per CTA
+  bool cta_pair;             // 2-CTA (cta_group::2) tiles of 256 rows; B box = BN/2 rows
 };
 
 // C[M, N] = epi(A[M, K] . B[N, K]^T).  K % 64 == 0, N % BN == 0, BN in {64, 128, 256};

@@ -44,10 +44,10 @@ struct EpiTraits {
   static constexpr bool kBias = EPI != EPI_STORE;
 };
 
-template <int BN, int EPI, bool AR = false>
+template <int BN, int EPI, bool AR = false, int CG = 1>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;       // 16 KB
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (BN / CG) * BK * 2;  // CG = 2: each CTA of the pair holds half of B
   static constexpr int AR_BYTES = AR ? 4 * A_BYTES : 0;   // resident A block (K <= 256)
   static constexpr int STAGE = (AR ? 0 : A_BYTES) + B_BYTES;
   static constexpr int SUB = BM * 64 * 2;           // one 128 x 64 bf16 sub-tile (16 KB)
@@ -69,13 +69,18 @@ using namespace tile;
 // AR (A resident, K <= 256): each CTA walks a contiguous run of tiles in m-major order and loads the
 // 128 x K A block once per m-block into a resident buffer; the ring only streams B tiles.  This cuts the
 // N/BN-fold re-read of A of a small-K, wide-N GEMM (the U GEMM of a cross layer).
-template <int BN, int EPI, bool AR>
+// CG = 2 (CTA pair, cluster of 2): a 256 x BN tile per pair with tcgen05.mma.cta_group::2 issued by the
+// leader; each CTA loads its own 128 A rows and HALF of the B tile (BN/2 rows), so the bytes each SM must
+// ingest per FLOP drop by (128 + BN/2)/(128 + BN); both CTAs' TMA bytes complete on the leader's full
+// barrier, MMA completion is multicast to both CTAs, and each CTA runs the epilogue of its own 128 rows.
+template <int BN, int EPI, bool AR, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmX0,
                      const __grid_constant__ CUtensorMap tmXl, const GemmArgs g) {
-  using C = Cfg<BN, EPI, AR>;
+  using C = Cfg<BN, EPI, AR, CG>;
   using T = EpiTraits<EPI>;
+  static_assert(CG == 1 || !AR, "the resident-A walk is single-CTA");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sAR = smem;                                  // resident A (AR only)
@@ -96,13 +101,18 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = g.M, N = g.N, K = g.K;
+  constexpr int BMT = BM * CG;  // rows per tile (per CTA pair when CG = 2)
+  const int rank = CG == 2 ? (int)ptx::cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int n_units = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int n_tiles_n = N / BN;
-  const int n_tiles = ((M + BM - 1) / BM) * n_tiles_n;
+  const int n_tiles = ((M + BMT - 1) / BMT) * n_tiles_n;
   const int nk = K / BK;
   // tile walk: strided over the grid, or (AR) a contiguous balanced run per CTA
-  const int t_begin = AR ? (int)((int64_t)n_tiles * blockIdx.x / gridDim.x) : (int)blockIdx.x;
-  const int t_end = AR ? (int)((int64_t)n_tiles * (blockIdx.x + 1) / gridDim.x) : n_tiles;
-  const int t_step = AR ? 1 : (int)gridDim.x;
+  const int t_begin = AR ? (int)((int64_t)n_tiles * unit / n_units) : unit;
+  const int t_end = AR ? (int)((int64_t)n_tiles * (unit + 1) / n_units) : n_tiles;
+  const int t_step = AR ? 1 : n_units;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -111,7 +121,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 4);
+      ptx::mbar_init(&tempty[a], 4 * CG);  // every epilogue warp of the pair
       ptx::mbar_init(&efull[a], 1);
       ptx::mbar_init(&eempty[a], 4);
     }
@@ -128,9 +138,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::prefetch_tmap(&tmXl);
     }
   }
-  if (warp == 1) ptx::tmem_alloc(tmem_holder, C::TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (CG == 2) ptx::tmem_alloc_cg2(tmem_holder, C::TMEM_COLS);
+    else ptx::tmem_alloc(tmem_holder, C::TMEM_COLS);
+  }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) ptx::cluster_sync();  // the peer's barriers exist before any remote arrive
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
   ptx::griddep_wait();  // inputs written by the previous kernel are visible from here on
@@ -141,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int it = 0;
       int cur_m = -1, a_loads = 0;
       for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
-        const int m0 = (tile / n_tiles_n) * BM, n0 = (tile % n_tiles_n) * BN;
+        const int m0 = (tile / n_tiles_n) * BMT + rank * BM, n0 = (tile % n_tiles_n) * BN;
         if constexpr (AR) {
           if (m0 != cur_m) {
             if (a_loads > 0) ptx::mbar_wait(aempty, (a_loads - 1) & 1);
@@ -165,15 +179,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < nk; ++kb, ++gk) {
           const int s = gk % C::STAGES;
           if (gk >= C::STAGES) ptx::mbar_wait(&empty[s], ((gk / C::STAGES) - 1) & 1);
-          ptx::mbar_arrive_expect_tx(&full[s], C::STAGE);
-          if constexpr (!AR) ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
-          ptx::tma_load_2d(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);
+          if constexpr (CG == 2) {
+            if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * C::STAGE);
+            ptx::tma_load_2d_cg2(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
+            ptx::tma_load_2d_cg2(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0 + rank * (BN / 2));
+          } else {
+            ptx::mbar_arrive_expect_tx(&full[s], C::STAGE);
+            if constexpr (!AR) ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
+            ptx::tma_load_2d(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ================= MMA issuer
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN);
+    if (lane == 0 && leader) {  // ================= MMA issuer (the pair's leader when CG = 2)
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BMT, BN);
       int gk = 0, it = 0;
       int cur_m = -1, a_loads = 0;
       for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
@@ -197,11 +217,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               ptx::smem_u32(AR ? sAR + kb * C::A_BYTES : sA + s * C::A_BYTES));
           const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)  // K step 16 = 32 bytes = +2 in the 16-byte address field
-            ptx::umma_bf16_ss(acc, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-          ptx::umma_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
+          for (int k = 0; k < BK / 16; ++k) {  // K step 16 = 32 bytes = +2 in the 16-byte address field
+            if constexpr (CG == 2) ptx::umma_bf16_ss_cg2(acc, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            else ptx::umma_bf16_ss(acc, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          }
+          // frees the smem stage (in both CTAs of a pair) once these MMAs have read it
+          if constexpr (CG == 2) ptx::umma_commit_cg2_mc(&empty[s]);
+          else ptx::umma_commit(&empty[s]);
         }
-        ptx::umma_commit(&tfull[a]);    // accumulator a complete
+        if constexpr (CG == 2) ptx::umma_commit_cg2_mc(&tfull[a]);  // accumulator a complete
+        else ptx::umma_commit(&tfull[a]);
         if constexpr (AR) {             // last tile of this m-block: the resident A may be replaced
           const int nt = tile + t_step;
           if (nt >= t_end || (nt / n_tiles_n) * BM != m0) ptx::umma_commit(aempty);
@@ -213,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = q * 32 + lane;  // row within the tile
     int it = 0;
     for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
-      const int m0 = (tile / n_tiles_n) * BM, tn = tile % n_tiles_n, n0 = tn * BN;
+      const int m0 = (tile / n_tiles_n) * BMT + rank * BM, tn = tile % n_tiles_n, n0 = tn * BN;
       const int m = m0 + r;
       const bool live = m < M;
       const int a = it & 1;
@@ -312,7 +337,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        ptx::mbar_arrive(&tempty[a]);
+        if constexpr (CG == 2) ptx::mbar_arrive_leader(&tempty[a]);
+        else ptx::mbar_arrive(&tempty[a]);
         if constexpr (T::kEin) ptx::mbar_arrive(&eempty[a]);
       }
       if constexpr (EPI == EPI_HEAD) {
@@ -336,33 +362,42 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) ptx::cluster_sync();  // both CTAs are done with the pair's TMEM
+  else __syncthreads();
   ptx::griddep_launch();
-  if (warp == 1) ptx::tmem_dealloc(tmem, C::TMEM_COLS);
+  if (warp == 1) {
+    if constexpr (CG == 2) ptx::tmem_dealloc_cg2(tmem, C::TMEM_COLS);
+    else ptx::tmem_dealloc(tmem, C::TMEM_COLS);
+  }
 }
 
-template <int BN, int EPI, bool AR = false>
+template <int BN, int EPI, bool AR = false, int CG = 1>
 cudaError_t launch_t(const GemmArgs& g, cudaStream_t s) {
-  using C = Cfg<BN, EPI, AR>;
-  auto kern = gemm_bf16_kernel<BN, EPI, AR>;
+  using C = Cfg<BN, EPI, AR, CG>;
+  auto kern = gemm_bf16_kernel<BN, EPI, AR, CG>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  const int n_tiles = ((g.M + BM - 1) / BM) * (g.N / BN);
-  const int grid = n_tiles < g.num_sms ? n_tiles : g.num_sms;
+  const int n_tiles = ((g.M + BM * CG - 1) / (BM * CG)) * (g.N / BN);
+  const int max_units = g.num_sms / CG;
+  const int grid = (n_tiles < max_units ? n_tiles : max_units) * CG;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = g.pdl ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = CG;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = CG == 2 ? 2 : 1;
   const CUtensorMap* dummy = g.tmA;
   return cudaLaunchKernelEx(&cfg, kern, *g.tmA, *g.tmB, *(g.tmOut ? g.tmOut : dummy), *(g.tmX0 ? g.tmX0 : dummy),
                             *(g.tmXl ? g.tmXl : dummy), g);
@@ -381,7 +416,7 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
     return cudaErrorInvalidValue;
   if ((g.epi == EPI_CROSS || g.epi == EPI_CROSS_F32) && (!g.tmX0 || !g.tmXl)) return cudaErrorInvalidValue;
 #define CVR_CASE(BN_, EPI_) \
-  if (g.BN == BN_ && g.epi == EPI_) return launch_t<BN_, EPI_>(g, s);
+  if (g.BN == BN_ && g.epi == EPI_) return g.cta_pair ? launch_t<BN_, EPI_, false, 2>(g, s) : launch_t<BN_, EPI_>(g, s);
   CVR_CASE(64, EPI_STORE)
   CVR_CASE(128, EPI_STORE)
   CVR_CASE(256, EPI_STORE)

@@ -31,9 +31,12 @@ for name, M, N, K in shapes:
     for bn in (64, 128, 256):
         if N % bn == 0:
             row[f"cvr_bn{bn}_us"] = timeit(lambda: gemm_bf16(A, B, C=C, bn=bn))
-    row["cublas_tflops"] = fl / row["cublas_us"] / 1e6
     for bn in (64, 128, 256):
-        if f"cvr_bn{bn}_us" in row:
-            row[f"cvr_bn{bn}_tflops"] = fl / row[f"cvr_bn{bn}_us"] / 1e6
+        if N % bn == 0:
+            row[f"cvr_pair_bn{bn}_us"] = timeit(lambda: gemm_bf16(A, B, C=C, bn=bn, pair=True))
+    row["cublas_tflops"] = fl / row["cublas_us"] / 1e6
+    for k in list(row):
+        if k.startswith("cvr_") and k.endswith("_us"):
+            row[k[:-3] + "_tflops"] = fl / row[k] / 1e6
     res.append(row)
     print(json.dumps(row), flush=True)

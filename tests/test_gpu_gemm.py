@@ -17,13 +17,14 @@ def _build():
 @pytest.mark.parametrize("M,N,K,bn", [(4096, 256, 1728, 64), (300, 1728, 256, 64), (1, 64, 64, 64),
                                       (4096, 1024, 1728, 128), (777, 512, 1024, 128), (129, 128, 4096, 64)])
 @pytest.mark.parametrize("relu", [False, True])
-def test_gemm_vs_fp32_reference(M, N, K, bn, relu):
+@pytest.mark.parametrize("pair", [False, True])
+def test_gemm_vs_fp32_reference(M, N, K, bn, relu, pair):
     from paper_2605_29232_b200 import gemm_bf16
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
     A = (torch.randn(M, K, device="cuda", generator=g) / K ** 0.25).bfloat16()
     B = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.25).bfloat16()
     bias = torch.randn(N, device="cuda", generator=g) if relu else None
-    C = gemm_bf16(A, B, bias=bias, bn=bn)
+    C = gemm_bf16(A, B, bias=bias, bn=bn, pair=pair)
     torch.cuda.synchronize()
     ref = A.float() @ B.float().T
     if relu:
