@@ -138,7 +138,7 @@ def embed_bytes(cfg, bt) -> int:
             + bt.batch * cfg.n_dense * (4 + act))
 
 
-FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965  # FP32 lanes x FMA x max SM clock (GHz) = 74.4 TFLOP/s
+FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965 / 1e3  # FP32 lanes x FMA x max SM clock (GHz) = 74.4 TFLOP/s
 
 
 def launch_work(cfg, B) -> dict:
@@ -426,7 +426,9 @@ def run_cvr(args, cfg):
     roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"],
                 "peak": pk["hbm"] if dk["bound"] == "hbm" else dk["peak"],
                 "unit": dk["unit"], "frac": dk["frac"], "traffic": traffic,
-                "peak_source": f"MEASURED_PEAKS.json ({pk['source']}; bf16 sustained for kernels inside the step)",
+                "peak_source": (f"MEASURED_PEAKS.json ({pk['source']}; bf16 sustained for kernels inside the step)"
+                                if dk["bound"] != "alu" else
+                                "derived: 148 SMs x 128 FP32 lanes x 2 FLOP/FMA x 1.965 GHz (DESIGN.md §6)"),
                 "share_of_kernel_time": share[dom]}
     dense_ms = sum(v["total_ms"] for k, v in kstats.items() if k != "embed_bag_pool") / args.steps
     dense_ach = dense_flops_per_example(cfg) * B / (dense_ms / 1e3) / 1e12

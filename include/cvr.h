@@ -193,8 +193,11 @@ int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d
  * embedding stage of batch k+1 then leaves registers for the dense-stage GEMM CTAs of batch k);
  * "embed_variant" [0] 0 = one lane group per bag at full
  * occupancy, 1 = warp-batched bags (coalesced offset / index staging); "a_resident" [0] the U GEMM of a low-rank cross layer keeps
- * the 128 x r block of t resident in shared memory across its N tiles
- * run each low-rank cross layer as one clustered kernel (K5) instead of two GEMMs. */
+ * the 128 x r block of t resident in shared memory across its N tiles ("fused_cross" = 1 runs each
+ * low-rank cross layer as one clustered kernel (K5) instead of two GEMMs); "mc" [1] clusters of 4 CTAs
+ * over adjacent N tiles with the A tile multicast by TMA: 0 = off, 1 = only the head GEMM (N = 4 x 64,
+ * the sigmoid's dot product summed over the cluster in DSMEM, fixed order), 2 = every GEMM whose N tiles
+ * group by 4.  Unknown key or bad value -> CVR_E_ARG. */
 int cvr_set_option(cvr_ctx* ctx, const char* key, int64_t value);
 
 /* -- utility ----------------------------------------------------------------------------------

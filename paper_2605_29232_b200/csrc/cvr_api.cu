@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -49,6 +50,7 @@ struct GemmPlan {
   int N, K, BN;
   Epi epi;
   bool pair = false;  // 2-CTA (cta_group::2) tiles; B map box = BN/2 rows
+  int cn = 1;         // 4: A multicast across a cluster of 4 N tiles (needs the A operand's quarter map)
   const char* wname;  // B operand
   CUtensorMap tmB;
 };
@@ -133,6 +135,16 @@ struct cvr_ctx {
   int last_x0_rows = -1;
   CUtensorMap tm_x0user;
   std::vector<GemmPlan> plan;  // cross layers (V, U interleaved), then MLP
+  // quarter maps (box {64, 32}) of the A-operand maps, keyed by the full map: A multicast (GemmPlan::cn)
+  std::map<const CUtensorMap*, CUtensorMap> qmaps;
+  int mc = 1;                  // option "mc": 0 off, 1 head only (default), 2 every grouped GEMM
+  int add_q(const CUtensorMap* full, const void* ptr, int64_t rows, int64_t cols, int64_t ld, const char** er) {
+    return encode_tmap_bf16(&qmaps[full], ptr, rows, cols, ld, 32, er);
+  }
+  const CUtensorMap* q(const CUtensorMap* full) {
+    auto it = qmaps.find(full);
+    return it == qmaps.end() ? nullptr : &it->second;
+  }
   // launch accounting + optional per-launch CUDA-event timing (cvr_profile_begin/end)
   int64_t launches = 0;
   bool prof_on = false;
@@ -530,9 +542,14 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     const char* er = nullptr;
     const int64_t B = c->max_batch;
     bool ok = true;
-    for (int i = 0; i < 2; ++i) ok &= encode_tmap_bf16(&c->tm_x0slot[i], c->ws + c->off_x0[i], B, c->x0_ld, c->x0_ld, 128, &er) == 0;
+    for (int i = 0; i < 2; ++i) {
+      ok &= encode_tmap_bf16(&c->tm_x0slot[i], c->ws + c->off_x0[i], B, c->x0_ld, c->x0_ld, 128, &er) == 0;
+      ok &= c->add_q(&c->tm_x0slot[i], c->ws + c->off_x0[i], B, c->x0_ld, c->x0_ld, &er) == 0;
+    }
     ok &= encode_tmap_bf16(&c->tm_xa, c->ws + c->off_xa, B, c->x0_ld, c->x0_ld, 128, &er) == 0;
     ok &= encode_tmap_bf16(&c->tm_xb, c->ws + c->off_xb, B, c->x0_ld, c->x0_ld, 128, &er) == 0;
+    ok &= c->add_q(&c->tm_xa, c->ws + c->off_xa, B, c->x0_ld, c->x0_ld, &er) == 0;
+    ok &= c->add_q(&c->tm_xb, c->ws + c->off_xb, B, c->x0_ld, c->x0_ld, &er) == 0;
     ok &= encode_tmap_bf16(&c->tm_t, c->ws + c->off_t, B, c->r, c->r, 128, &er) == 0;
     ok &= encode_tmap_bf16(&c->st_xa, c->ws + c->off_xa, B, c->x0_ld, c->x0_ld, 32, &er) == 0;
     ok &= encode_tmap_bf16(&c->st_xb, c->ws + c->off_xb, B, c->x0_ld, c->x0_ld, 32, &er) == 0;
@@ -542,6 +559,7 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     for (size_t i = 0; i < c->off_h.size(); ++i) {
       ok &= encode_tmap_bf16(&c->tm_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], 128, &er) == 0;
       ok &= encode_tmap_bf16(&c->st_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], 32, &er) == 0;
+      ok &= c->add_q(&c->tm_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], &er) == 0;
     }
     if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
   }
@@ -615,8 +633,14 @@ int encode_plan(cvr_ctx* c) {
     return true;
   };
   bool ok = true;
+  // Clusters of 4 N tiles with A multicast.  Measured on B200 (scripts/dense_kernels.py, B = 4096): the head
+  // (N = 256 as 4 x 64 tiles, DSMEM dot-product sum) 15.8 -> 13.3 us per launch; multicast alone does not
+  // pay at cluster size 4 (xV 14.7 -> 16.7, MLP 18.4 -> 19.7: unicast reads of a line by <= 4 SMs are
+  // already merged in L2), so option mc = 1 (default) clusters only the head, mc = 2 every grouped GEMM.
+  auto mc4 = [&](int N, int BN) { return c->mc >= 2 && N % (4 * BN) == 0 && N / BN <= 8 ? 4 : 1; };
   for (int l = 0; l < c->n_cross; ++l) {
     ok &= addp("dcn/" + std::to_string(l) + "/V", c->r, (int)c->x0_ld, pick_bn(c->r), EPI_STORE);
+    c->plan.back().cn = mc4(c->r, c->plan.back().BN);
     ok &= addp("dcn/" + std::to_string(l) + "/U", (int)c->x0_ld, c->r, pick_bn((int)c->x0_ld), EPI_CROSS);
   }
   c->tm_v256.assign(c->n_cross, CUtensorMap{});
@@ -627,9 +651,12 @@ int encode_plan(cvr_ctx* c) {
   int K = (int)c->x0_ld;
   for (int i = 0; i < c->n_mlp; ++i) {
     const bool last = i + 1 == c->n_mlp;
-    const int bn = last ? (c->head_parts ? 256 : c->mlp[i]) : pick_bn(c->mlp[i], c->max_batch);
+    int bn = last ? (c->head_parts ? 256 : c->mlp[i]) : pick_bn(c->mlp[i], c->max_batch);
     const Epi ep = last ? (c->head_parts ? EPI_HEAD_PARTIAL : EPI_HEAD) : EPI_BIAS_RELU;
+    const bool head_mc = last && !c->head_parts && c->mc && c->mlp[i] % 256 == 0;
+    if (head_mc) bn = c->mlp[i] / 4;  // the head's dot product spans the cluster's 4 tiles (DSMEM sum)
     ok &= addp("mlp/" + std::to_string(i) + "/W", c->mlp[i], K, bn, ep);
+    c->plan.back().cn = head_mc ? 4 : (!last ? mc4(c->mlp[i], bn) : 1);
     K = c->mlp[i];
   }
   if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
@@ -860,6 +887,10 @@ GemmArgs gemm_args(cvr_ctx* c, const GemmPlan& g, const CUtensorMap* A, int M) {
   a.num_sms = c->num_sms;
   a.pdl = c->pdl;
   a.cta_pair = g.pair;
+  if (g.cn > 1 && c->q(A)) {  // A operands without a quarter map stay unicast
+    a.cn = g.cn;
+    a.tmA = c->q(A);
+  }  // (a cluster-spanning EPI_HEAD without a quarter map fails its launch check: BN * cn != N)
   return a;
 }
 
@@ -1182,6 +1213,7 @@ int cvr_dense(cvr_ctx* c, const void* d_x0, int batch, float* d_scores, cvr_stre
       if (d_x0 != c->last_x0 || batch != c->last_x0_rows) {
         const char* er = nullptr;
         if (encode_tmap_bf16(&c->tm_x0user, d_x0, batch, c->x0_ld, c->x0_ld, 128, &er) != 0 ||
+            c->add_q(&c->tm_x0user, d_x0, batch, c->x0_ld, c->x0_ld, &er) != 0 ||
             (ens && encode_tmap_bf16(&c->ens.tok_user, d_x0, (int64_t)batch * c->T, c->d, c->d, 128, &er) != 0))
           return c->fail(CVR_E_CUDA, "tensor map encode: %s", er);
         c->last_x0 = d_x0;
@@ -1458,6 +1490,14 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     c->a_resident = value != 0;
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
+    return CVR_OK;
+  }
+  if (!strcmp(key, "mc")) {
+    if (value < 0 || value > 2) return c->fail(CVR_E_ARG, "mc must be 0, 1 or 2");
+    c->mc = (int)value;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);
     return CVR_OK;
   }
   if (!strcmp(key, "pdl")) {

@@ -104,10 +104,11 @@ struct GemmArgs {
   bool pdl;                  // launch with programmatic stream serialization
   bool a_resident;           // K <= 256: keep the A block resident, contiguous tile runs per CTA
   bool cta_pair;             // 2-CTA (cta_group::2) tiles of 256 rows; B box = BN/2 rows
+  int cn;                    // 4: clusters of 4 CTAs along N multicast A (tmA box = {64, 32}); 0/1: off
 };
 
 // C[M, N] = epi(A[M, K] . B[N, K]^T).  K % 64 == 0, N % BN == 0, BN in {64, 128, 256};
-// EPI_HEAD needs BN == N.  Persistent: grid = min(tiles, num_sms).
+// EPI_HEAD needs BN * cn == N.  Persistent: grid = min(tiles, num_sms).
 cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s);
 
 // ---- K7: multi-head self-attention over the 64 tokens of each example (config 4) ------------------

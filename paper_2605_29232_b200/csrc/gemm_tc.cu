@@ -44,7 +44,7 @@ struct EpiTraits {
   static constexpr bool kBias = EPI != EPI_STORE;
 };
 
-template <int BN, int EPI, bool AR = false, int CG = 1>
+template <int BN, int EPI, bool AR = false, int CG = 1, int CN = 1>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;       // 16 KB
   static constexpr int B_BYTES = (BN / CG) * BK * 2;  // CG = 2: each CTA of the pair holds half of B
@@ -57,10 +57,12 @@ struct Cfg {
   static constexpr int EIN_BYTES = EpiTraits<EPI>::kEin ? 2 * NSUB * SUB : 0;     // x0 + x_l tiles, per acc
   static constexpr int EPI_BYTES = OUT_BUFS * OUT_BYTES + 2 * EIN_BYTES;
   static constexpr int BAR_BYTES = 256;
-  static constexpr int STAGES_FIT = (kSmemBudget - 1024 - BAR_BYTES - EPI_BYTES - AR_BYTES) / STAGE;
+  // EPI_HEAD across a CN-cluster: per-tile partial dot products gathered in rank 0 ([2][CN][BM] fp32)
+  static constexpr int Z_BYTES = (EPI == EPI_HEAD && CN > 1) ? 2 * CN * BM * 4 : 0;
+  static constexpr int STAGES_FIT = (kSmemBudget - 1024 - BAR_BYTES - EPI_BYTES - AR_BYTES - Z_BYTES) / STAGE;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int TMEM_COLS = 2 * BN;          // two accumulators; BN in {64,128,256}
-  static constexpr int SMEM = 1024 + AR_BYTES + STAGES * STAGE + EPI_BYTES + BAR_BYTES;
+  static constexpr int SMEM = 1024 + AR_BYTES + STAGES * STAGE + EPI_BYTES + Z_BYTES + BAR_BYTES;
   static_assert(STAGES >= 2, "shared memory budget");
 };
 
@@ -73,14 +75,23 @@ using namespace tile;
 // leader; each CTA loads its own 128 A rows and HALF of the B tile (BN/2 rows), so the bytes each SM must
 // ingest per FLOP drop by (128 + BN/2)/(128 + BN); both CTAs' TMA bytes complete on the leader's full
 // barrier, MMA completion is multicast to both CTAs, and each CTA runs the epilogue of its own 128 rows.
-template <int BN, int EPI, bool AR, int CG>
+// CN > 1 (cluster of CN CTAs along N, cta_group::1): the CN CTAs of a cluster work on the CN adjacent N
+// tiles of the same 128-row block in lock step; each loads a BM/CN-row slice of every A k-block and
+// multicasts it to all CN CTAs (tmA then has box {64, BM/CN}), so the L2 serves each A byte once per
+// cluster instead of CN times.  A stage is refilled only after all CN CTAs' MMAs have read it (empty
+// barriers count CN multicast commits).  EPI_HEAD then spans CN tiles: the partial dot products of the
+// CN tiles are gathered in rank 0's shared memory over DSMEM and summed in rank order (fixed order,
+// independent of M: batch invariance).
+template <int BN, int EPI, bool AR, int CG, int CN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmX0,
                      const __grid_constant__ CUtensorMap tmXl, const GemmArgs g) {
-  using C = Cfg<BN, EPI, AR, CG>;
+  using C = Cfg<BN, EPI, AR, CG, CN>;
   using T = EpiTraits<EPI>;
   static_assert(CG == 1 || !AR, "the resident-A walk is single-CTA");
+  static_assert(CN == 1 || (CG == 1 && !AR), "A multicast is cta_group::1 streaming only");
+  static_assert(BM % (8 * CN) == 0, "A slices are whole 8-row swizzle atoms");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sAR = smem;                                  // resident A (AR only)
@@ -88,7 +99,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sB = sA + (AR ? 0 : C::STAGES * C::A_BYTES);
   uint8_t* sOut = sB + C::STAGES * C::B_BYTES;         // [OUT_BUFS][NSUB][SUB]
   uint8_t* sEin = sOut + C::OUT_BUFS * C::OUT_BYTES;   // [2][x0 NSUB subs | x_l NSUB subs]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sEin + 2 * C::EIN_BYTES);
+  float* zbuf = reinterpret_cast<float*>(sEin + 2 * C::EIN_BYTES);  // [2][CN][BM] (EPI_HEAD, CN > 1)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEin + 2 * C::EIN_BYTES + C::Z_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;   // [2] accumulator ready
@@ -97,17 +109,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* eempty = efull + 2;          // [2] epilogue input tiles consumed (4 warps)
   uint64_t* afull = eempty + 2;          // resident A landed (AR)
   uint64_t* aempty = afull + 1;          // resident A no longer read by MMAs (AR)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(aempty + 1);
+  uint64_t* zfull = aempty + 1;          // [2] rank 0: all CN x 4 epilogue warps stored their partials
+  uint64_t* zempty = zfull + 2;          // [2] rank 0's 4 epilogue warps have read buffer a
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(zempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = g.M, N = g.N, K = g.K;
   constexpr int BMT = BM * CG;  // rows per tile (per CTA pair when CG = 2)
   const int rank = CG == 2 ? (int)ptx::cluster_ctarank() : 0;
+  const int crank = CN > 1 ? (int)ptx::cluster_ctarank() : 0;   // N position inside the cluster
+  constexpr uint16_t kMask = (uint16_t)((1u << CN) - 1);
   const bool leader = rank == 0;
-  const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int n_units = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x / CN;
+  const int n_units = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x / CN;
   const int n_tiles_n = N / BN;
-  const int n_tiles = ((M + BMT - 1) / BMT) * n_tiles_n;
+  const int n_groups = n_tiles_n / CN;  // tiles of a cluster: (m-block, group of CN adjacent N tiles)
+  const int n_tiles = ((M + BMT - 1) / BMT) * n_groups;
+  auto tile_m = [&](int tile) { return tile / n_groups; };
+  auto tile_n = [&](int tile) { return (tile % n_groups) * CN + crank; };
   const int nk = K / BK;
   // tile walk: strided over the grid, or (AR) a contiguous balanced run per CTA
   const int t_begin = AR ? (int)((int64_t)n_tiles * unit / n_units) : unit;
@@ -117,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], CN);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
@@ -127,6 +146,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     ptx::mbar_init(afull, 1);
     ptx::mbar_init(aempty, 1);
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(&zfull[a], 4 * CN);
+      ptx::mbar_init(&zempty[a], 4);
+    }
     ptx::fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -143,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     else ptx::tmem_alloc(tmem_holder, C::TMEM_COLS);
   }
   ptx::tc_fence_before();
-  if constexpr (CG == 2) ptx::cluster_sync();  // the peer's barriers exist before any remote arrive
+  if constexpr (CG == 2 || CN > 1) ptx::cluster_sync();  // peers' barriers exist before any remote arrive
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
@@ -155,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int it = 0;
       int cur_m = -1, a_loads = 0;
       for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
-        const int m0 = (tile / n_tiles_n) * BMT + rank * BM, n0 = (tile % n_tiles_n) * BN;
+        const int m0 = tile_m(tile) * BMT + rank * BM, n0 = tile_n(tile) * BN;
         if constexpr (AR) {
           if (m0 != cur_m) {
             if (a_loads > 0) ptx::mbar_wait(aempty, (a_loads - 1) & 1);
@@ -185,7 +208,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tma_load_2d_cg2(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0 + rank * (BN / 2));
           } else {
             ptx::mbar_arrive_expect_tx(&full[s], C::STAGE);
-            if constexpr (!AR) ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
+            if constexpr (CN > 1)
+              ptx::tma_load_2d_mc(sA + s * C::A_BYTES + crank * (BM / CN) * 128, &tmA, &full[s], kb * BK,
+                                  m0 + crank * (BM / CN), kMask);
+            else if constexpr (!AR)
+              ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
             ptx::tma_load_2d(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);
           }
         }
@@ -198,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int cur_m = -1, a_loads = 0;
       for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
         const int a = it & 1;
-        const int m0 = (tile / n_tiles_n) * BM;
+        const int m0 = tile_m(tile) * BM;
         if constexpr (AR) {
           if (m0 != cur_m) {
             ptx::mbar_wait(afull, a_loads & 1);
@@ -223,13 +250,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           // frees the smem stage (in both CTAs of a pair) once these MMAs have read it
           if constexpr (CG == 2) ptx::umma_commit_cg2_mc(&empty[s]);
+          else if constexpr (CN > 1) ptx::umma_commit_mc(&empty[s], kMask);  // frees it in every CTA
           else ptx::umma_commit(&empty[s]);
         }
         if constexpr (CG == 2) ptx::umma_commit_cg2_mc(&tfull[a]);  // accumulator a complete
         else ptx::umma_commit(&tfull[a]);
         if constexpr (AR) {             // last tile of this m-block: the resident A may be replaced
           const int nt = tile + t_step;
-          if (nt >= t_end || (nt / n_tiles_n) * BM != m0) ptx::umma_commit(aempty);
+          if (nt >= t_end || tile_m(nt) * BM != m0) ptx::umma_commit(aempty);
         }
       }
     }
@@ -238,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int r = q * 32 + lane;  // row within the tile
     int it = 0;
     for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
-      const int m0 = (tile / n_tiles_n) * BMT + rank * BM, tn = tile % n_tiles_n, n0 = tn * BN;
+      const int m0 = tile_m(tile) * BMT + rank * BM, tn = tile_n(tile), n0 = tn * BN;
       const int m = m0 + r;
       const bool live = m < M;
       const int a = it & 1;
@@ -341,7 +369,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         else ptx::mbar_arrive(&tempty[a]);
         if constexpr (T::kEin) ptx::mbar_arrive(&eempty[a]);
       }
-      if constexpr (EPI == EPI_HEAD) {
+      if constexpr (EPI == EPI_HEAD && CN > 1) {
+        // gather the CN partial dot products of this row block in rank 0, sum them in rank order
+        if (it >= 2) ptx::mbar_wait_cluster(&zempty[a], ((it >> 1) - 1) & 1);
+        ptx::st_cluster_f32(ptx::mapa(zbuf + (a * CN + crank) * BM + r, 0), z);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(&zfull[a], 0));
+        if (crank == 0) {
+          ptx::mbar_wait_cluster(&zfull[a], (it >> 1) & 1);
+          float zs = 0.f;
+#pragma unroll
+          for (int j = 0; j < CN; ++j) zs += zbuf[(a * CN + j) * BM + r];
+          if (live) g.scores[m] = sigmoid_f32(zs + g.head_b);
+          __syncwarp();
+          if (lane == 0)
+            for (int j = 0; j < CN; ++j) ptx::mbar_arrive_remote(ptx::mapa(&zempty[a], j));
+        }
+      } else if constexpr (EPI == EPI_HEAD) {
         if (live) g.scores[m] = sigmoid_f32(z + g.head_b);
       } else if constexpr (EPI == EPI_HEAD_PARTIAL) {
         if (live) g.partial[(int64_t)m * n_tiles_n + tn] = z;
@@ -362,7 +406,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
   ptx::tc_fence_before();
-  if constexpr (CG == 2) ptx::cluster_sync();  // both CTAs are done with the pair's TMEM
+  // CG = 2: both CTAs are done with the pair's TMEM; CN > 1: no peer still multicasts into / arrives on us
+  if constexpr (CG == 2 || CN > 1) ptx::cluster_sync();
   else __syncthreads();
   ptx::griddep_launch();
   if (warp == 1) {
@@ -371,19 +416,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int BN, int EPI, bool AR = false, int CG = 1>
+template <int BN, int EPI, bool AR = false, int CG = 1, int CN = 1>
 cudaError_t launch_t(const GemmArgs& g, cudaStream_t s) {
-  using C = Cfg<BN, EPI, AR, CG>;
-  auto kern = gemm_bf16_kernel<BN, EPI, AR, CG>;
+  using C = Cfg<BN, EPI, AR, CG, CN>;
+  auto kern = gemm_bf16_kernel<BN, EPI, AR, CG, CN>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  const int n_tiles = ((g.M + BM * CG - 1) / (BM * CG)) * (g.N / BN);
-  const int max_units = g.num_sms / CG;
-  const int grid = (n_tiles < max_units ? n_tiles : max_units) * CG;
+  const int n_tiles = ((g.M + BM * CG - 1) / (BM * CG)) * (g.N / BN / CN);
+  const int max_units = g.num_sms / (CG * CN);
+  const int grid = (n_tiles < max_units ? n_tiles : max_units) * CG * CN;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -393,11 +438,11 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = g.pdl ? 1 : 0;
   attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = CG;
+  attr[1].val.clusterDim.x = CG * CN;
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = CG == 2 ? 2 : 1;
+  cfg.numAttrs = CG * CN > 1 ? 2 : 1;
   const CUtensorMap* dummy = g.tmA;
   return cudaLaunchKernelEx(&cfg, kern, *g.tmA, *g.tmB, *(g.tmOut ? g.tmOut : dummy), *(g.tmX0 ? g.tmX0 : dummy),
                             *(g.tmXl ? g.tmXl : dummy), g);
@@ -410,11 +455,22 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s) {
 cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
   if (g.M <= 0) return cudaSuccess;
   const bool full_row = g.epi == EPI_HEAD || g.epi == EPI_SUM_LN;
-  if (g.K % BK || g.N % g.BN || (full_row && g.BN != g.N)) return cudaErrorInvalidValue;
+  const int cn = g.cn > 1 ? g.cn : 1;
+  if (g.K % BK || g.N % g.BN || (full_row && g.BN * cn != g.N) || (g.N / g.BN) % cn) return cudaErrorInvalidValue;
+  if (cn > 1 && (cn != 4 || g.cta_pair || g.a_resident)) return cudaErrorInvalidValue;
   if ((g.epi == EPI_STORE || g.epi == EPI_BIAS_RELU || g.epi == EPI_CROSS || g.epi == EPI_BIAS ||
        g.epi == EPI_SUM_LN) && !g.tmOut)
     return cudaErrorInvalidValue;
   if ((g.epi == EPI_CROSS || g.epi == EPI_CROSS_F32) && (!g.tmX0 || !g.tmXl)) return cudaErrorInvalidValue;
+  // A-multicast clusters of 4 along N (tmA with box {64, 32})
+#define CVR_MC(BN_, EPI_) \
+  if (cn == 4 && g.BN == BN_ && g.epi == EPI_) return launch_t<BN_, EPI_, false, 1, 4>(g, s);
+  CVR_MC(64, EPI_STORE)
+  CVR_MC(128, EPI_BIAS_RELU)
+  CVR_MC(256, EPI_BIAS_RELU)
+  CVR_MC(64, EPI_HEAD)
+#undef CVR_MC
+  if (cn > 1) return cudaErrorInvalidValue;
 #define CVR_CASE(BN_, EPI_) \
   if (g.BN == BN_ && g.epi == EPI_) return g.cta_pair ? launch_t<BN_, EPI_, false, 2>(g, s) : launch_t<BN_, EPI_>(g, s);
   CVR_CASE(64, EPI_STORE)

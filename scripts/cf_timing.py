@@ -12,6 +12,7 @@ for pdl in (1, 0):
     idx, off, dense = (torch.from_numpy(bt.indices).cuda(), torch.from_numpy(bt.offsets).cuda(), torch.from_numpy(bt.dense).cuda())
     x0 = m.embed(idx, off, 4096, dense)
     m.set_option("pdl", pdl)
+    m.set_option("fused_cross", 1)
     for _ in range(5):
         s = m.dense(x0, 4096)
     torch.cuda.synchronize()

@@ -229,3 +229,27 @@ def test_c2_cross_stack_bitexact(c2, B):
     finally:
         m.set_option("stack", 0)
     assert torch.equal(s_stack, s_plain)
+
+
+@pytest.mark.parametrize("B", [4096, 333])
+def test_c2_multicast_clusters(c2, B):
+    """A-multicast clusters (option "mc"): mc = 2 (every grouped GEMM multicast, same per-tile MMAs and
+    K order) is bit-identical to mc = 1; mc = 0 (head as one 256-wide tile: a different fp32 summation
+    order of the head dot product) meets the oracle and agrees to fp32 rounding."""
+    cfg, m, tabs, w = c2
+    bt = cs.make_batch(cfg, 43, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    s1 = m.dense(x0, B).clone()
+    try:
+        m.set_option("mc", 2)
+        s2 = m.dense(x0, B).clone()
+        m.set_option("mc", 0)
+        s0 = m.dense(x0, B).clone()
+    finally:
+        m.set_option("mc", 1)
+    assert torch.equal(s2, s1)
+    assert (s0 - s1).abs().max().item() <= 1e-5
+    sel = np.arange(B) if B <= 333 else np.random.default_rng(1).choice(B, 256, replace=False)
+    ref = O.score_forward(cfg, cs.table_specs(cfg), w, sub_batch(bt, sel))["scores"]
+    assert np.abs(s1[torch.from_numpy(sel).cuda()].double().cpu().numpy() - ref).max() <= TOL_BF16
