@@ -110,6 +110,10 @@ struct cvr_ctx {
   int dbg_ctas = 0;
   size_t off_part = 0;
   std::vector<CUtensorMap> st_h;
+  // CVR_GEMM_TIMELINE: per-CTA stamps of every GEMM of the last dense stage (printed at cvr_destroy)
+  unsigned long long* gdbg = nullptr;
+  int gdbg_n = 0;
+  std::vector<int> gdbg_kid;
   bool pdl = true;
   // measured on B200 at B = 4096 (scripts/dense_ab.py): separate streaming GEMMs 105.5 us/dense stage,
   // resident-A U GEMM 108.4, persistent cross stack 118 -- both kept as options, off by default
@@ -138,6 +142,7 @@ struct cvr_ctx {
   // quarter maps (box {64, 32}) of the A-operand maps, keyed by the full map: A multicast (GemmPlan::cn)
   std::map<const CUtensorMap*, CUtensorMap> qmaps;
   int mc = 1;                  // option "mc": 0 off, 1 head only (default), 2 every grouped GEMM
+  int u_bn = 192;              // option "u_bn": N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64)
   int add_q(const CUtensorMap* full, const void* ptr, int64_t rows, int64_t cols, int64_t ld, const char** er) {
     return encode_tmap_bf16(&qmaps[full], ptr, rows, cols, ld, 32, er);
   }
@@ -443,6 +448,32 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
 
 int cvr_destroy(cvr_ctx* c) {
   if (!c) return CVR_E_ARG;
+  if (c->gdbg) {  // debug: GEMM timeline of the last dense stage (us from the first GEMM's first CTA entry)
+    std::vector<unsigned long long> h((size_t)32 * 160 * 8);
+    cudaDeviceSynchronize();
+    cudaMemcpy(h.data(), c->gdbg, h.size() * 8, cudaMemcpyDeviceToHost);
+    const int n = std::min<int>((int)c->gdbg_kid.size(), 32);
+    const int first = 0;
+    unsigned long long t0 = ~0ull;
+    for (int b = 0; b < 160; ++b)
+      if (h[((size_t)first * 160 + b) * 8]) t0 = std::min(t0, h[((size_t)first * 160 + b) * 8]);
+    const char* nm[8] = {"entry", "deps", "1st-stage", "last-mma", "1st-acc", "epi-done", "exit", ""};
+    for (int g = first; g < n; ++g) {
+      fprintf(stderr, "gemm %2d %-16s", g - first, kKernelNames[c->gdbg_kid[g]]);
+      for (int i = 0; i < 7; ++i) {
+        double mn = 1e30, mx = 0;
+        for (int b = 0; b < 160; ++b) {
+          const unsigned long long v = h[((size_t)g * 160 + b) * 8 + i];
+          if (!v) continue;
+          mn = std::min(mn, (double)(v - t0) / 1e3);
+          mx = std::max(mx, (double)(v - t0) / 1e3);
+        }
+        fprintf(stderr, " %s %.2f-%.2f", nm[i], mn, mx);
+      }
+      fprintf(stderr, "\n");
+    }
+    cudaFree(c->gdbg);
+  }
   if (c->dbg && c->stack && !c->fused_cross) {  // debug: cross-stack timeline of the last launch
     std::vector<unsigned long long> h(148 * 32);
     cudaDeviceSynchronize();
@@ -530,6 +561,10 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
   // zero the activation slots once so padding columns / tail rows are defined
   if (e == cudaSuccess) e = cudaMemset(c->ws + c->off_x0[0], 0, c->ws_need - c->off_x0[0]);
   if (e != cudaSuccess) return c->cuda_fail(e, "cvr_set_workspace");
+  if (getenv("CVR_GEMM_TIMELINE") && !c->gdbg) {
+    cudaMalloc(&c->gdbg, (size_t)32 * 160 * 8 * 8);
+    cudaMemset(c->gdbg, 0, (size_t)32 * 160 * 8 * 8);
+  }
   if (getenv("CVR_DEBUG_TIMING") && !c->dbg) {
     cudaMalloc(&c->dbg, 160 * 32 * 8 + (size_t)(c->max_batch / 128 + 1) * 4 * 8 * 8);
     cudaMemset(c->dbg, 0, 160 * 32 * 8);
@@ -641,7 +676,11 @@ int encode_plan(cvr_ctx* c) {
   for (int l = 0; l < c->n_cross; ++l) {
     ok &= addp("dcn/" + std::to_string(l) + "/V", c->r, (int)c->x0_ld, pick_bn(c->r), EPI_STORE);
     c->plan.back().cn = mc4(c->r, c->plan.back().BN);
-    ok &= addp("dcn/" + std::to_string(l) + "/U", (int)c->x0_ld, c->r, pick_bn((int)c->x0_ld), EPI_CROSS);
+    // U GEMM: 192-wide tiles (EIN-ring epilogue) when W allows -- 1/3 of the t re-reads of 64-wide tiles
+    // (measured 4096x1728x256: 7.4 us at BN = 192 vs 10.3 at 64); the K5 / stack / resident-A variants
+    // read U through 64-row boxes
+    const bool u192 = c->u_bn == 192 && c->x0_ld % 192 == 0 && !c->fused_cross && !c->stack && !c->a_resident;
+    ok &= addp("dcn/" + std::to_string(l) + "/U", (int)c->x0_ld, c->r, u192 ? 192 : pick_bn((int)c->x0_ld), EPI_CROSS);
   }
   c->tm_v256.assign(c->n_cross, CUtensorMap{});
   if (c->r == 256)
@@ -804,9 +843,11 @@ int cvr_load_weights(cvr_ctx* c, int n, const char* const* names, const void* co
     if (st != CVR_OK) return st;
     CrossStackTables tb;
     memset(&tb, 0, sizeof tb);
-    for (int l = 0; l < c->n_cross; ++l) {
-      tb.V[l] = c->plan[2 * l].tmB;
-      tb.U[l] = c->plan[2 * l + 1].tmB;
+    const char* er = nullptr;
+    for (int l = 0; l < c->n_cross; ++l) {  // the stack kernel reads V and U through 64-row boxes
+      if (encode_tmap_bf16(&tb.V[l], c->wptr("dcn/" + std::to_string(l) + "/V"), c->r, c->x0_ld, c->x0_ld, 64, &er) ||
+          encode_tmap_bf16(&tb.U[l], c->wptr("dcn/" + std::to_string(l) + "/U"), c->x0_ld, c->r, c->r, 64, &er))
+        return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
     }
     tb.xa = c->tm_xa;
     tb.xb = c->tm_xb;
@@ -887,6 +928,7 @@ GemmArgs gemm_args(cvr_ctx* c, const GemmPlan& g, const CUtensorMap* A, int M) {
   a.num_sms = c->num_sms;
   a.pdl = c->pdl;
   a.cta_pair = g.pair;
+  if (c->gdbg && c->gdbg_n < 32) a.dbg = c->gdbg + (size_t)(c->gdbg_n++) * 160 * 8;
   if (g.cn > 1 && c->q(A)) {  // A operands without a quarter map stay unicast
     a.cn = g.cn;
     a.tmA = c->q(A);
@@ -895,6 +937,7 @@ GemmArgs gemm_args(cvr_ctx* c, const GemmPlan& g, const CUtensorMap* A, int M) {
 }
 
 cudaError_t run_gemm(cvr_ctx* c, const GemmArgs& a, int kid, cudaStream_t s) {
+  if (a.dbg) c->gdbg_kid.push_back(kid);
   c->pbeg(s);
   cudaError_t r = launch_gemm_bf16(a, s);
   c->pend(kid, s);
@@ -1007,6 +1050,8 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
 
 int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, const CUtensorMap* tm_x0_tok, int B, float* scores,
              cudaStream_t s) {
+  c->gdbg_n = 0;  // CVR_GEMM_TIMELINE: stamps of this stage's GEMMs start at slot 0
+  c->gdbg_kid.clear();
   cudaError_t e = cudaSuccess;
   if (c->backbone == CVR_DCN_FULL) {
     DenseF32Args a{};
@@ -1411,7 +1456,7 @@ int cvr_gemm_bf16(const void* d_A, int64_t lda, const void* d_B, int64_t ldb, vo
   epi &= 0xFF;
   if (!d_A || !d_B || !d_C || M < 0 || N <= 0 || K <= 0 || (epi == 1 && !d_bias)) return CVR_E_ARG;
   if (epi != 0 && epi != 1) return CVR_E_ARG;
-  if (K % 64 || N % bn || (bn != 64 && bn != 128 && bn != 256) || lda < K || ldb < K || ldc < N || (lda | ldb | ldc) & 7)
+  if (K % 64 || N % bn || (bn != 64 && bn != 128 && bn != 256 && !(bn == 192 && epi == 0 && !pair)) || lda < K || ldb < K || ldc < N || (lda | ldb | ldc) & 7)
     return CVR_E_UNSUPPORTED;
   if (M == 0) return CVR_OK;
   const char* er = nullptr;
@@ -1451,6 +1496,7 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     c->fused_cross = value != 0;
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
+    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);  // U tile width
     return CVR_OK;
   }
   if (!strcmp(key, "pair")) {
@@ -1484,12 +1530,22 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     c->stack = value != 0;
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
+    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);  // U tile width
     return CVR_OK;
   }
   if (!strcmp(key, "a_resident")) {
     c->a_resident = value != 0;
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
+    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);  // U tile width
+    return CVR_OK;
+  }
+  if (!strcmp(key, "u_bn")) {
+    if (value != 64 && value != 192) return c->fail(CVR_E_ARG, "u_bn must be 64 or 192");
+    c->u_bn = (int)value;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);
     return CVR_OK;
   }
   if (!strcmp(key, "mc")) {

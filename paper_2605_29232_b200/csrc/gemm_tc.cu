@@ -18,7 +18,8 @@
 //     tile i+1.  Output tiles are staged in swizzled shared memory and written by TMA stores.
 //   * Tiles are visited n-fastest so CTAs working at the same time share the A row block in L2.
 //   * Programmatic dependent launch: the prologue (barrier init, TMEM alloc, descriptor
-//     prefetch) runs before griddepcontrol.wait, overlapping the previous kernel's tail.
+//     prefetch) runs before griddepcontrol.wait, overlapping the previous kernel's tail; the
+//     dependent launch is triggered right after the wait.
 //   * No split-K: every row's result depends only on that row, in a fixed K order, so scores are
 //     batch-invariant.
 #include <cudaTypedefs.h>
@@ -33,7 +34,9 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 192;
+constexpr int kThreads = 256;   // 8 warps: A producer, MMA, 4 epilogue, B producer, EIN-ring producer
+constexpr int kProducerB = 6;
+constexpr int kProducerE = 7;
 constexpr int kSmemBudget = 225 * 1024;
 
 template <int EPI>
@@ -44,6 +47,12 @@ struct EpiTraits {
   static constexpr bool kBias = EPI != EPI_STORE;
 };
 
+// EIN ring (EPI_CROSS at BN = 192): x0 / x_l come as 64-column sub-tile pairs through a 3-slot ring fed by
+// a dedicated producer warp, and x_{l+1} is written in place over the x_l sub-tile and TMA-stored from there
+// (no separate output staging): 96 KB of epilogue buffers instead of 2 x 96 + 48.
+template <int BN, int EPI, int CG>
+constexpr bool ein_ring() { return EPI == EPI_CROSS && BN == 192 && CG == 1; }
+
 template <int BN, int EPI, bool AR = false, int CG = 1, int CN = 1>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;       // 16 KB
@@ -52,16 +61,18 @@ struct Cfg {
   static constexpr int STAGE = (AR ? 0 : A_BYTES) + B_BYTES;
   static constexpr int SUB = BM * 64 * 2;           // one 128 x 64 bf16 sub-tile (16 KB)
   static constexpr int NSUB = BN / 64;
-  static constexpr int OUT_BUFS = BN == 256 ? 1 : 2;
-  static constexpr int OUT_BYTES = EpiTraits<EPI>::kSmemOut ? NSUB * SUB : 0;     // per buffer
-  static constexpr int EIN_BYTES = EpiTraits<EPI>::kEin ? 2 * NSUB * SUB : 0;     // x0 + x_l tiles, per acc
-  static constexpr int EPI_BYTES = OUT_BUFS * OUT_BYTES + 2 * EIN_BYTES;
-  static constexpr int BAR_BYTES = 256;
+  static constexpr int OUT_BUFS = BN >= 192 ? 1 : 2;
+  static constexpr bool RING = ein_ring<BN, EPI, CG>();
+  static constexpr int RING_SLOTS = 3;
+  static constexpr int OUT_BYTES = EpiTraits<EPI>::kSmemOut && !RING ? NSUB * SUB : 0;     // per buffer
+  static constexpr int EIN_BYTES = EpiTraits<EPI>::kEin && !RING ? 2 * NSUB * SUB : 0;     // x0 + x_l tiles, per acc
+  static constexpr int EPI_BYTES = OUT_BUFS * OUT_BYTES + 2 * EIN_BYTES + (RING ? RING_SLOTS * 2 * SUB : 0);
+  static constexpr int BAR_BYTES = 512;
   // EPI_HEAD across a CN-cluster: per-tile partial dot products gathered in rank 0 ([2][CN][BM] fp32)
   static constexpr int Z_BYTES = (EPI == EPI_HEAD && CN > 1) ? 2 * CN * BM * 4 : 0;
   static constexpr int STAGES_FIT = (kSmemBudget - 1024 - BAR_BYTES - EPI_BYTES - AR_BYTES - Z_BYTES) / STAGE;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
-  static constexpr int TMEM_COLS = 2 * BN;          // two accumulators; BN in {64,128,256}
+  static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);  // 2 accumulators, pow2 alloc
   static constexpr int SMEM = 1024 + AR_BYTES + STAGES * STAGE + EPI_BYTES + Z_BYTES + BAR_BYTES;
   static_assert(STAGES >= 2, "shared memory budget");
 };
@@ -82,6 +93,14 @@ using namespace tile;
 // barriers count CN multicast commits).  EPI_HEAD then spans CN tiles: the partial dot products of the
 // CN tiles are gathered in rank 0's shared memory over DSMEM and summed in rank order (fixed order,
 // independent of M: batch invariance).
+__device__ __forceinline__ void stamp(unsigned long long* dbg, int i) {
+  if (dbg) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    dbg[blockIdx.x * 8 + i] = t;
+  }
+}
+
 template <int BN, int EPI, bool AR, int CG, int CN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -105,9 +124,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;   // [2] accumulator ready
   uint64_t* tempty = tfull + 2;          // [2] accumulator drained (4 epilogue warps)
-  uint64_t* efull = tempty + 2;          // [2] epilogue input tiles landed
-  uint64_t* eempty = efull + 2;          // [2] epilogue input tiles consumed (4 warps)
-  uint64_t* afull = eempty + 2;          // resident A landed (AR)
+  uint64_t* efull = tempty + 2;          // [3] epilogue input tiles (ring slots) landed
+  uint64_t* eempty = efull + 3;          // [3] epilogue input tiles consumed (4 warps)
+  uint64_t* afull = eempty + 3;          // resident A landed (AR)
   uint64_t* aempty = afull + 1;          // resident A no longer read by MMAs (AR)
   uint64_t* zfull = aempty + 1;          // [2] rank 0: all CN x 4 epilogue warps stored their partials
   uint64_t* zempty = zfull + 2;          // [2] rank 0's 4 epilogue warps have read buffer a
@@ -135,14 +154,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&full[s], AR ? 1 : 2);  // one expect_tx arrival per producer stream
       ptx::mbar_init(&empty[s], CN);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
       ptx::mbar_init(&tempty[a], 4 * CG);  // every epilogue warp of the pair
-      ptx::mbar_init(&efull[a], 1);
-      ptx::mbar_init(&eempty[a], 4);
+    }
+    for (int e = 0; e < 3; ++e) {
+      ptx::mbar_init(&efull[e], 1);
+      ptx::mbar_init(&eempty[e], 4);
     }
     ptx::mbar_init(afull, 1);
     ptx::mbar_init(aempty, 1);
@@ -170,50 +191,87 @@ __global__ void __launch_bounds__(kThreads, 1)
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  if (threadIdx.x == 0) stamp(g.dbg, 0);
   ptx::griddep_wait();  // inputs written by the previous kernel are visible from here on
+  if (threadIdx.x == 0) stamp(g.dbg, 1);
+  // Trigger the dependent launch now rather than at exit: its CTAs are then placed on each SM the moment
+  // ours leaves it and run their prologue there, and only their griddepcontrol.wait (full completion +
+  // flush of this grid) orders them after our results.  The grid is persistent (<= 1 CTA per SM, all
+  // resident), so early dependents cannot starve our own CTAs.
+  ptx::griddep_launch();
 
-  if (warp == 0) {
-    if (lane == 0) {  // ================= TMA producer
+  if (warp == 0 || warp == kProducerB) {
+    // ================= TMA producers: warp 0 streams A (and the resident A blocks), warp 6 streams B and the
+    // epilogue input tiles.  One issuing thread per operand stream: a single thread's TMA issue saturates
+    // at ~69 B/clk/SM on B200 while two concurrent streams reach ~120 (scripts/micro/ingest_mix.cu).
+    if (lane == 0) {
+      const bool roleA = warp == 0;
       int gk = 0;     // global k-block counter (ring position)
       int it = 0;
       int cur_m = -1, a_loads = 0;
       for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
         const int m0 = tile_m(tile) * BMT + rank * BM, n0 = tile_n(tile) * BN;
         if constexpr (AR) {
-          if (m0 != cur_m) {
+          if (roleA && m0 != cur_m) {
             if (a_loads > 0) ptx::mbar_wait(aempty, (a_loads - 1) & 1);
             ptx::mbar_arrive_expect_tx(afull, nk * C::A_BYTES);
             for (int kb = 0; kb < nk; ++kb) ptx::tma_load_2d(sAR + kb * C::A_BYTES, &tmA, afull, kb * BK, m0);
             cur_m = m0;
             ++a_loads;
           }
+          if (roleA) continue;  // the ring carries only B
         }
-        if constexpr (T::kEin) {
-          const int a = it & 1;
-          if (it >= 2) ptx::mbar_wait(&eempty[a], ((it >> 1) - 1) & 1);
-          ptx::mbar_arrive_expect_tx(&efull[a], C::EIN_BYTES);
-          uint8_t* base = sEin + a * C::EIN_BYTES;
+        if constexpr (T::kEin && !C::RING) {
+          if (!roleA) {
+            const int a = it & 1;
+            if (it >= 2) ptx::mbar_wait(&eempty[a], ((it >> 1) - 1) & 1);
+            ptx::mbar_arrive_expect_tx(&efull[a], C::EIN_BYTES);
+            uint8_t* base = sEin + a * C::EIN_BYTES;
 #pragma unroll
-          for (int j = 0; j < C::NSUB; ++j) {
-            ptx::tma_load_2d(base + j * C::SUB, &tmX0, &efull[a], n0 + j * 64, m0);
-            ptx::tma_load_2d(base + (C::NSUB + j) * C::SUB, &tmXl, &efull[a], n0 + j * 64, m0);
+            for (int j = 0; j < C::NSUB; ++j) {
+              ptx::tma_load_2d(base + j * C::SUB, &tmX0, &efull[a], n0 + j * 64, m0);
+              ptx::tma_load_2d(base + (C::NSUB + j) * C::SUB, &tmXl, &efull[a], n0 + j * 64, m0);
+            }
           }
         }
         for (int kb = 0; kb < nk; ++kb, ++gk) {
           const int s = gk % C::STAGES;
           if (gk >= C::STAGES) ptx::mbar_wait(&empty[s], ((gk / C::STAGES) - 1) & 1);
           if constexpr (CG == 2) {
-            if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * C::STAGE);
-            ptx::tma_load_2d_cg2(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
-            ptx::tma_load_2d_cg2(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0 + rank * (BN / 2));
-          } else {
-            ptx::mbar_arrive_expect_tx(&full[s], C::STAGE);
+            if (roleA) {
+              if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * C::A_BYTES);
+              ptx::tma_load_2d_cg2(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
+            } else {
+              if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * C::B_BYTES);
+              ptx::tma_load_2d_cg2(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0 + rank * (BN / 2));
+            }
+          } else if (roleA) {
+            ptx::mbar_arrive_expect_tx(&full[s], C::A_BYTES);
             if constexpr (CN > 1)
               ptx::tma_load_2d_mc(sA + s * C::A_BYTES + crank * (BM / CN) * 128, &tmA, &full[s], kb * BK,
                                   m0 + crank * (BM / CN), kMask);
-            else if constexpr (!AR)
+            else
               ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
+          } else {
+            ptx::mbar_arrive_expect_tx(&full[s], C::B_BYTES);
             ptx::tma_load_2d(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);
+          }
+        }
+      }
+    }
+  } else if (warp == kProducerE) {
+    if constexpr (C::RING) {  // ================= EIN ring producer: (x0, x_l) 64-column sub-tile pairs
+      if (lane == 0) {
+        int e = 0;
+        for (int tile = t_begin; tile < t_end; tile += t_step) {
+          const int m0 = tile_m(tile) * BMT, n0 = tile_n(tile) * BN;
+          for (int j = 0; j < C::NSUB; ++j, ++e) {
+            const int sl = e % C::RING_SLOTS;
+            if (e >= C::RING_SLOTS) ptx::mbar_wait(&eempty[sl], ((e / C::RING_SLOTS) - 1) & 1);
+            ptx::mbar_arrive_expect_tx(&efull[sl], 2 * C::SUB);
+            uint8_t* slot = sEin + sl * 2 * C::SUB;
+            ptx::tma_load_2d(slot, &tmX0, &efull[sl], n0 + j * 64, m0);
+            ptx::tma_load_2d(slot + C::SUB, &tmXl, &efull[sl], n0 + j * 64, m0);
           }
         }
       }
@@ -239,6 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < nk; ++kb, ++gk) {
           const int s = gk % C::STAGES;
           ptx::mbar_wait(&full[s], (gk / C::STAGES) & 1);
+          if (gk == 0) stamp(g.dbg, 2);
           ptx::tc_fence_after();
           const uint64_t ad = ptx::sdesc_kmajor_sw128(
               ptx::smem_u32(AR ? sAR + kb * C::A_BYTES : sA + s * C::A_BYTES));
@@ -255,28 +314,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if constexpr (CG == 2) ptx::umma_commit_cg2_mc(&tfull[a]);  // accumulator a complete
         else ptx::umma_commit(&tfull[a]);
+        stamp(g.dbg, 3);
         if constexpr (AR) {             // last tile of this m-block: the resident A may be replaced
           const int nt = tile + t_step;
           if (nt >= t_end || tile_m(nt) * BM != m0) ptx::umma_commit(aempty);
         }
       }
     }
-  } else {  // ================= epilogue warps 2..5: TMEM quadrant q = warp % 4 -> rows 32q .. 32q+31
+  } else if (warp < kProducerB) {  // ======== epilogue warps 2..5: TMEM quadrant q = warp % 4 -> rows 32q..32q+31
     const int q = warp & 3;
     const int r = q * 32 + lane;  // row within the tile
     int it = 0;
+    int g_e = 0;                  // EIN ring: global sub-tile counter (same sequence as the producer)
+    (void)g_e;
     for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
       const int m0 = tile_m(tile) * BMT + rank * BM, tn = tile_n(tile), n0 = tn * BN;
       const int m = m0 + r;
       const bool live = m < M;
       const int a = it & 1;
       ptx::mbar_wait(&tfull[a], (it >> 1) & 1);
+      if (it == 0 && warp == 2 && lane == 0) stamp(g.dbg, 4);
       ptx::tc_fence_after();
       const uint32_t trow = tmem + a * BN + ((uint32_t)(q * 32) << 16);
       const uint32_t out_base = ptx::smem_u32(sOut + (C::OUT_BUFS == 2 ? a : 0) * C::OUT_BYTES);
       const uint32_t ein_base = ptx::smem_u32(sEin + a * C::EIN_BYTES);
-      if constexpr (T::kEin) ptx::mbar_wait(&efull[a], (it >> 1) & 1);
-      if constexpr (T::kSmemOut) {
+      if constexpr (T::kEin && !C::RING) ptx::mbar_wait(&efull[a], (it >> 1) & 1);
+      if constexpr (T::kSmemOut && !C::RING) {
         // the TMA store that last read this staging buffer must have finished reading it
         if (lane == 0) {
           if constexpr (C::OUT_BUFS == 2) ptx::bulk_wait_read<1>();
@@ -285,7 +348,49 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
       float z = 0.f;
-      if constexpr (EPI == EPI_SUM_LN) {
+      if constexpr (C::RING) {
+        // x_{l+1} = x0 * (acc + b) + x_l per 64-column sub-tile, written over x_l in the ring slot and
+        // TMA-stored from there; the previous sub-tile's slot is released once its store has read it
+#pragma unroll 1
+        for (int j = 0; j < C::NSUB; ++j, ++g_e) {
+          const int sl = g_e % C::RING_SLOTS;
+          ptx::mbar_wait(&efull[sl], (g_e / C::RING_SLOTS) & 1);
+          const uint32_t x0b = ptx::smem_u32(sEin + sl * 2 * C::SUB), xlb = x0b + C::SUB;
+#pragma unroll 1
+          for (int c = 0; c < 64; c += 32) {
+            float v[32], x0v[32], xlv[32];
+            ld32_tmem(trow + j * 64 + c, v);
+            lds32_bf16(x0b, r, c >> 3, x0v);
+            lds32_bf16(xlb, r, c >> 3, xlv);
+            const float4* b4 = reinterpret_cast<const float4*>(g.bias + n0 + j * 64 + c);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const float4 bb = __ldg(b4 + u);
+              v[4 * u] = x0v[4 * u] * (v[4 * u] + bb.x) + xlv[4 * u];
+              v[4 * u + 1] = x0v[4 * u + 1] * (v[4 * u + 1] + bb.y) + xlv[4 * u + 1];
+              v[4 * u + 2] = x0v[4 * u + 2] * (v[4 * u + 2] + bb.z) + xlv[4 * u + 2];
+              v[4 * u + 3] = x0v[4 * u + 3] * (v[4 * u + 3] + bb.w) + xlv[4 * u + 3];
+            }
+            sts32_bf16(xlb, r, c >> 3, v);
+          }
+          if (j == C::NSUB - 1) {  // last TMEM read of this accumulator
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[a]);
+          }
+          ptx::fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_2d(&tmOut, sEin + sl * 2 * C::SUB + C::SUB + q * 32 * 128, n0 + j * 64, m0 + q * 32);
+            ptx::bulk_commit();
+            if (g_e > 0) {  // the previous sub-tile's store has read its slot: hand the slot back
+              ptx::bulk_wait_read<1>();
+              ptx::mbar_arrive(&eempty[(g_e - 1) % C::RING_SLOTS]);
+            }
+          }
+          __syncwarp();
+        }
+      } else if constexpr (EPI == EPI_SUM_LN) {
         // pass 1: y = acc + b + in, written back into TMEM; row sum
         float sum = 0.f;
 #pragma unroll 1
@@ -362,12 +467,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       // accumulator (and epilogue inputs) consumed: hand them back
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 2) ptx::mbar_arrive_leader(&tempty[a]);
-        else ptx::mbar_arrive(&tempty[a]);
-        if constexpr (T::kEin) ptx::mbar_arrive(&eempty[a]);
+      if constexpr (!C::RING) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) ptx::mbar_arrive_leader(&tempty[a]);
+          else ptx::mbar_arrive(&tempty[a]);
+          if constexpr (T::kEin) ptx::mbar_arrive(&eempty[a]);
+        }
       }
       if constexpr (EPI == EPI_HEAD && CN > 1) {
         // gather the CN partial dot products of this row block in rank 0, sum them in rank order
@@ -389,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (live) g.scores[m] = sigmoid_f32(z + g.head_b);
       } else if constexpr (EPI == EPI_HEAD_PARTIAL) {
         if (live) g.partial[(int64_t)m * n_tiles_n + tn] = z;
-      } else if constexpr (T::kSmemOut) {
+      } else if constexpr (T::kSmemOut && !C::RING) {
         ptx::fence_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -401,15 +508,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if constexpr (T::kSmemOut) {
+    if constexpr (T::kSmemOut || C::RING) {
       if (lane == 0) ptx::bulk_wait<0>();
     }
+    if (warp == 2 && lane == 0) stamp(g.dbg, 5);
   }
   ptx::tc_fence_before();
   // CG = 2: both CTAs are done with the pair's TMEM; CN > 1: no peer still multicasts into / arrives on us
   if constexpr (CG == 2 || CN > 1) ptx::cluster_sync();
   else __syncthreads();
-  ptx::griddep_launch();
+  if (threadIdx.x == 0) stamp(g.dbg, 6);
   if (warp == 1) {
     if constexpr (CG == 2) ptx::tmem_dealloc_cg2(tmem, C::TMEM_COLS);
     else ptx::tmem_dealloc(tmem, C::TMEM_COLS);
@@ -476,11 +584,13 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
   CVR_CASE(64, EPI_STORE)
   CVR_CASE(128, EPI_STORE)
   CVR_CASE(256, EPI_STORE)
+  CVR_CASE(192, EPI_STORE)
   CVR_CASE(256, EPI_BIAS_RELU)
   CVR_CASE(64, EPI_BIAS_RELU)
   CVR_CASE(128, EPI_BIAS_RELU)
   if (g.BN == 64 && g.epi == EPI_CROSS && g.K <= 256 && g.a_resident) return launch_t<64, EPI_CROSS, true>(g, s);
   CVR_CASE(64, EPI_CROSS)
+  if (g.BN == 192 && g.epi == EPI_CROSS && !g.cta_pair) return launch_t<192, EPI_CROSS>(g, s);
   CVR_CASE(64, EPI_HEAD)
   CVR_CASE(128, EPI_HEAD)
   CVR_CASE(256, EPI_HEAD)

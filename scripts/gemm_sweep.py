@@ -21,14 +21,14 @@ def timeit(fn, iters=20, reps=5):
     return a.elapsed_time(b) / (iters * reps) * 1e3
 
 shapes = [("xV", 4096, 256, 1728), ("tU", 4096, 1728, 256), ("mlp0", 4096, 1024, 1728), ("mlp1", 4096, 512, 1024),
-          ("head", 4096, 256, 512), ("big", 8192, 8192, 8192)]
+          ("head", 4096, 256, 512)] + ([("big", 8192, 8192, 8192)] if os.environ.get("BIG") else [])
 res = []
 for name, M, N, K in shapes:
     A = torch.randn(M, K, device="cuda").bfloat16(); B = torch.randn(N, K, device="cuda").bfloat16()
     C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     fl = 2 * M * N * K
     row = {"gemm": name, "M": M, "N": N, "K": K, "cublas_us": timeit(lambda: torch.matmul(A, B.T, out=C))}
-    for bn in (64, 128, 256):
+    for bn in (64, 128, 192, 256):
         if N % bn == 0:
             row[f"cvr_bn{bn}_us"] = timeit(lambda: gemm_bf16(A, B, C=C, bn=bn))
     for bn in (64, 128, 256):

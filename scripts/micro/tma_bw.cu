@@ -49,30 +49,30 @@ int main() {
     cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
     enc(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, gd, gs, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    const int smem = 8 * 16384 + 2048;
-    cudaFuncSetAttribute(tma_stream<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int smem = 13 * 16384 + 2048;
     cudaFuncSetAttribute(tma_stream<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    for (int grid : {16, 37, 74, 148}) {
-    for (int share : {1}) {
-      for (int st : {8}) {
-        const int tiles = 400;
+    cudaFuncSetAttribute(tma_stream<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(tma_stream<13>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    for (int w = 0; w < 50; ++w) tma_stream<8><<<148, 64, smem>>>(tm, 2000, 1, rr / 128, nullptr);  // warm clocks
+    cudaDeviceSynchronize();
+    for (int grid : {148}) {
+      for (int share : {1, 4, 16, 37, 148}) {
+        const int tiles = 2000, st = 8;
         cudaEvent_t a, b;
         cudaEventCreate(&a);
         cudaEventCreate(&b);
-        for (int w = 0; w < 2; ++w) {
+        for (int w = 0; w < 5; ++w) {
           cudaEventRecord(a);
-          if (st == 8) tma_stream<8><<<grid, 64, smem>>>(tm, tiles, share, rr / 128, nullptr);
-          else tma_stream<4><<<grid, 64, smem>>>(tm, tiles, share, rr / 128, nullptr);
+          tma_stream<8><<<grid, 64, smem>>>(tm, tiles, share, rr / 128, nullptr);
           cudaEventRecord(b);
           cudaEventSynchronize(b);
         }
         float ms;
         cudaEventElapsedTime(&ms, a, b);
         const double bytes = (double)grid * tiles * 16384;
-        printf("rows %5d (%s) grid %3d stages %d: %.2f TB/s delivered to SMs (%.1f GB/s per SM)\n", rr,
-               rr == 4096 ? "L2-resident 14MB" : "113MB > L2", grid, st, bytes / ms / 1e9, bytes / ms / 1e6 / grid);
+        printf("rows %5d grid %3d stages %d share %3d: %.2f TB/s (%.1f GB/s per SM)\n", rr, grid, st, share,
+               bytes / ms / 1e9, bytes / ms / 1e6 / grid);
       }
-    }
     }
     cudaFree(buf);
   }

@@ -253,3 +253,24 @@ def test_c2_multicast_clusters(c2, B):
     sel = np.arange(B) if B <= 333 else np.random.default_rng(1).choice(B, 256, replace=False)
     ref = O.score_forward(cfg, cs.table_specs(cfg), w, sub_batch(bt, sel))["scores"]
     assert np.abs(s1[torch.from_numpy(sel).cuda()].double().cpu().numpy() - ref).max() <= TOL_BF16
+
+
+@pytest.mark.parametrize("B", [4096, 333])
+def test_c2_u_tile_192_bitexact(c2, B):
+    """U GEMM at 192-wide tiles (EIN-ring epilogue, in-place x_{l+1}) vs 64-wide tiles: each output element
+    sees the same MMAs in the same K order and the same fp32 epilogue -> bit-identical scores; both meet the
+    oracle."""
+    cfg, m, tabs, w = c2
+    bt = cs.make_batch(cfg, 47, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    s192 = m.dense(x0, B).clone()
+    m.set_option("u_bn", 64)
+    try:
+        s64 = m.dense(x0, B).clone()
+    finally:
+        m.set_option("u_bn", 192)
+    assert torch.equal(s192, s64)
+    sel = np.arange(B) if B <= 333 else np.random.default_rng(2).choice(B, 256, replace=False)
+    ref = O.score_forward(cfg, cs.table_specs(cfg), w, sub_batch(bt, sel))["scores"]
+    assert np.abs(s192[torch.from_numpy(sel).cuda()].double().cpu().numpy() - ref).max() <= TOL_BF16
