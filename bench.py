@@ -346,13 +346,20 @@ def run_cvr(args, cfg):
 
     # ---- per-kernel attribution: the same K steps again with a CUDA-event pair around every
     # launch on its launching stream (events between kernels also disable PDL overlap, so this
-    # pass is slower than the timed one; it is used only for per-kernel durations / shares)
+    # pass is slower than the timed one; it is used only for per-kernel durations / shares).
+    # Every 16 steps a device-side spin holds both streams while the host enqueues the chunk, so the
+    # GPU then runs it back to back and each pair brackets the kernel, not the host's launch latency.
     torch.cuda.synchronize(dev)
     m.profile_begin(args.steps * launches_per_step + 16)
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p0.record(s_e)
     s_d.wait_event(p0)
+    spin_cycles = int(3e6)  # ~1.5 ms at 1.965 GHz: longer than the host needs to enqueue 16 steps
     for i in range(args.steps):
+        if i % 16 == 0:
+            for st_ in (s_e, s_d):
+                with torch.cuda.stream(st_):
+                    torch.cuda._sleep(spin_cycles)
         step(i)
     p1.record(s_d)
     torch.cuda.synchronize(dev)
@@ -478,8 +485,9 @@ def run_cvr(args, cfg):
         "gpu_launches": int(n_launch),
         "clocks": clocks.summary(),
         "kernels": kernels,
-        "kernel_timing": "separate pass of the same %d steps with a CUDA-event pair around every launch "
-                         "(%.4f ms/step in that pass)" % (args.steps, prof_ms_per_step),
+        "kernel_timing": "separate pass of the same %d steps with a CUDA-event pair around every launch, enqueued "
+                         "ahead behind a device spin every 16 steps (%.4f ms/step in that pass incl. spins)"
+                         % (args.steps, prof_ms_per_step),
         "dense_stage_tflops": dense_ach,
         "stage_isolation": iso,
         "parity": parity,

@@ -143,6 +143,10 @@ struct cvr_ctx {
   std::map<const CUtensorMap*, CUtensorMap> qmaps;
   int mc = 1;                  // option "mc": 0 off, 1 head only (default), 2 every grouped GEMM
   int u_bn = 192;              // option "u_bn": N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64)
+  // option "xv_splitk" [0]: t = x_l V^T as a K-split cluster GEMM (r == 256).  Measured on B200 at B = 4096:
+  // its mainloop halves (3.5 vs 7 us) but the DSMEM exchange of the fp32 partials costs 2-6 us (element-wise
+  // st.shared::cluster or cp.async.bulk shared::cluster alike): 92-100 us per dense stage vs 90 with tiles
+  bool xv_splitk = false;
   int add_q(const CUtensorMap* full, const void* ptr, int64_t rows, int64_t cols, int64_t ld, const char** er) {
     return encode_tmap_bf16(&qmaps[full], ptr, rows, cols, ld, 32, er);
   }
@@ -1137,7 +1141,20 @@ int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, const CUtenso
     }
     GemmArgs av = gemm_args(c, gv, tm_xl, B);
     av.tmOut = &c->st_t;
-    if ((e = run_gemm(c, av, K_GEMM_V, s)) != cudaSuccess) return c->cuda_fail(e, "gemm V launch");
+    if (c->xv_splitk && c->r == 256 && c->x0_ld >= 256) {
+      // one 128 x 256 tile per row block, K split over a 4-CTA cluster (gemm_splitk.cu)
+      av.tmA = tm_xl;
+      av.tmB = &c->tm_v256[l];
+      av.out_bf16 = c->at<__nv_bfloat16>(c->off_t);
+      av.ld_x = c->r;
+      if (av.dbg) c->gdbg_kid.push_back(K_GEMM_V);
+      c->pbeg(s);
+      e = launch_gemm_splitk(av, s);
+      c->pend(K_GEMM_V, s);
+      if (e != cudaSuccess) return c->cuda_fail(e, "gemm V (split-K) launch");
+    } else if ((e = run_gemm(c, av, K_GEMM_V, s)) != cudaSuccess) {
+      return c->cuda_fail(e, "gemm V launch");
+    }
     GemmArgs au = gemm_args(c, gu, &c->tm_t, B);
     au.tmOut = even ? &c->st_xa : &c->st_xb;
     au.tmX0 = tm_x0;
@@ -1423,6 +1440,7 @@ int cvr_profile_begin(cvr_ctx* c, int max_launches) {
 int cvr_profile_end(cvr_ctx* c, cvr_kernel_stat* out, int max_out, int* n_out) {
   if (!c || !n_out || (max_out > 0 && !out)) return CVR_E_ARG;
   c->prof_on = false;
+
   cvr_kernel_stat agg[K_COUNT];
   memset(agg, 0, sizeof agg);
   for (size_t i = 0; i < c->prof_n; ++i) {
@@ -1538,6 +1556,12 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);  // U tile width
+    return CVR_OK;
+  }
+  if (!strcmp(key, "xv_splitk")) {
+    c->xv_splitk = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
     return CVR_OK;
   }
   if (!strcmp(key, "u_bn")) {

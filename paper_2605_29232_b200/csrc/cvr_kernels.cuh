@@ -98,6 +98,8 @@ struct GemmArgs {
   const float* gamma;        // EPI_SUM_LN [N]
   const float* beta;         // EPI_SUM_LN [N]
   float* partial;            // EPI_HEAD_PARTIAL [M, N / BN]
+  __nv_bfloat16* out_bf16;   // launch_gemm_splitk: C [M, ld_x] bf16 (written with plain stores)
+  int64_t ld_x;
   int M, N, K, BN;
   Epi epi;
   int num_sms;
@@ -112,6 +114,11 @@ struct GemmArgs {
 // C[M, N] = epi(A[M, K] . B[N, K]^T).  K % 64 == 0, N % BN == 0, BN in {64, 128, 256};
 // EPI_HEAD needs BN * cn == N.  Persistent: grid = min(tiles, num_sms).
 cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s);
+
+// t = A . B^T with N = 256 as one 128 x 256 tile per row block, K split over a cluster of 4 CTAs and reduced
+// in DSMEM in a fixed order (gemm_splitk.cu).  Uses tmA (box {64, 128}), tmB (box {64, 256}), out_bf16 /
+// ld_x (row stride of t), M, K, pdl.
+cudaError_t launch_gemm_splitk(const GemmArgs& g, cudaStream_t s);
 
 // ---- K7: multi-head self-attention over the 64 tokens of each example (config 4) ------------------
 // qkv [B*S, 3*D] bf16 (Q | K | V, head h at columns h*64 of each), out [B*S, D] bf16; S = 64, dh = 64.

@@ -34,9 +34,7 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 256;   // 8 warps: A producer, MMA, 4 epilogue, B producer, EIN-ring producer
-constexpr int kProducerB = 6;
-constexpr int kProducerE = 7;
+
 constexpr int kSmemBudget = 225 * 1024;
 
 template <int EPI>
@@ -47,9 +45,10 @@ struct EpiTraits {
   static constexpr bool kBias = EPI != EPI_STORE;
 };
 
-// EIN ring (EPI_CROSS at BN = 192): x0 / x_l come as 64-column sub-tile pairs through a 3-slot ring fed by
-// a dedicated producer warp, and x_{l+1} is written in place over the x_l sub-tile and TMA-stored from there
-// (no separate output staging): 96 KB of epilogue buffers instead of 2 x 96 + 48.
+// EIN slots (EPI_CROSS at BN = 192): x0 / x_l come as 64-column sub-tile pairs, one slot per sub-tile
+// position j, fed by a dedicated producer warp; 3 epilogue warps per TMEM lane quadrant, warp part j owning
+// sub-tile j, write x_{l+1} in place over x_l and TMA-store it from there (no separate output staging):
+// 96 KB of epilogue buffers instead of 2 x 96 + 48, and the three sub-tiles are finished in parallel.
 template <int BN, int EPI, int CG>
 constexpr bool ein_ring() { return EPI == EPI_CROSS && BN == 192 && CG == 1; }
 
@@ -64,6 +63,14 @@ struct Cfg {
   static constexpr int OUT_BUFS = BN >= 192 ? 1 : 2;
   static constexpr bool RING = ein_ring<BN, EPI, CG>();
   static constexpr int RING_SLOTS = 3;
+  // epilogue warps per TMEM lane quadrant: the epilogue of a CTA's last tile is exposed (one tile per CTA at
+  // B = 4096), so plain stores split the tile's 64-column sub-tiles over up to 4 warps per quadrant
+  static constexpr bool SPLIT = (EPI == EPI_STORE || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS) && CG == 1 && CN == 1;
+  static constexpr int EPW = RING ? 3 : (SPLIT ? (BN / 64 < 4 ? BN / 64 : 4) : 1);
+  static constexpr int COLS_W = BN / EPW;           // columns per epilogue warp
+  static constexpr int PRODUCER_B = 2 + 4 * EPW;
+  static constexpr int PRODUCER_E = PRODUCER_B + 1;  // EIN producer (RING only)
+  static constexpr int NT = 32 * (PRODUCER_B + (RING ? 2 : 1));
   static constexpr int OUT_BYTES = EpiTraits<EPI>::kSmemOut && !RING ? NSUB * SUB : 0;     // per buffer
   static constexpr int EIN_BYTES = EpiTraits<EPI>::kEin && !RING ? 2 * NSUB * SUB : 0;     // x0 + x_l tiles, per acc
   static constexpr int EPI_BYTES = OUT_BUFS * OUT_BYTES + 2 * EIN_BYTES + (RING ? RING_SLOTS * 2 * SUB : 0);
@@ -102,7 +109,7 @@ __device__ __forceinline__ void stamp(unsigned long long* dbg, int i) {
 }
 
 template <int BN, int EPI, bool AR, int CG, int CN>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN>::NT, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmX0,
                      const __grid_constant__ CUtensorMap tmXl, const GemmArgs g) {
@@ -159,7 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 4 * CG);  // every epilogue warp of the pair
+      ptx::mbar_init(&tempty[a], 4 * C::EPW * CG);  // every epilogue warp of the pair
     }
     for (int e = 0; e < 3; ++e) {
       ptx::mbar_init(&efull[e], 1);
@@ -200,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // resident), so early dependents cannot starve our own CTAs.
   ptx::griddep_launch();
 
-  if (warp == 0 || warp == kProducerB) {
+  if (warp == 0 || warp == C::PRODUCER_B) {
     // ================= TMA producers: warp 0 streams A (and the resident A blocks), warp 6 streams B and the
     // epilogue input tiles.  One issuing thread per operand stream: a single thread's TMA issue saturates
     // at ~69 B/clk/SM on B200 while two concurrent streams reach ~120 (scripts/micro/ingest_mix.cu).
@@ -259,19 +266,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == kProducerE) {
-    if constexpr (C::RING) {  // ================= EIN ring producer: (x0, x_l) 64-column sub-tile pairs
+  } else if (warp == C::PRODUCER_E) {
+    if constexpr (C::RING) {  // ================= EIN producer: (x0, x_l) 64-column sub-tile j -> slot j
       if (lane == 0) {
-        int e = 0;
-        for (int tile = t_begin; tile < t_end; tile += t_step) {
+        int it = 0;
+        for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
           const int m0 = tile_m(tile) * BMT, n0 = tile_n(tile) * BN;
-          for (int j = 0; j < C::NSUB; ++j, ++e) {
-            const int sl = e % C::RING_SLOTS;
-            if (e >= C::RING_SLOTS) ptx::mbar_wait(&eempty[sl], ((e / C::RING_SLOTS) - 1) & 1);
-            ptx::mbar_arrive_expect_tx(&efull[sl], 2 * C::SUB);
-            uint8_t* slot = sEin + sl * 2 * C::SUB;
-            ptx::tma_load_2d(slot, &tmX0, &efull[sl], n0 + j * 64, m0);
-            ptx::tma_load_2d(slot + C::SUB, &tmXl, &efull[sl], n0 + j * 64, m0);
+          for (int j = 0; j < C::NSUB; ++j) {
+            if (it >= 1) ptx::mbar_wait(&eempty[j], (it - 1) & 1);
+            ptx::mbar_arrive_expect_tx(&efull[j], 2 * C::SUB);
+            uint8_t* slot = sEin + j * 2 * C::SUB;
+            ptx::tma_load_2d(slot, &tmX0, &efull[j], n0 + j * 64, m0);
+            ptx::tma_load_2d(slot + C::SUB, &tmXl, &efull[j], n0 + j * 64, m0);
           }
         }
       }
@@ -321,12 +327,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp < kProducerB) {  // ======== epilogue warps 2..5: TMEM quadrant q = warp % 4 -> rows 32q..32q+31
+  } else if (warp < C::PRODUCER_B) {  // ===== epilogue warps: TMEM quadrant q = warp % 4 -> rows 32q..32q+31
     const int q = warp & 3;
+    const int part = (warp - 2) >> 2;  // RING: the 64-column sub-tile this warp finishes
     const int r = q * 32 + lane;  // row within the tile
     int it = 0;
-    int g_e = 0;                  // EIN ring: global sub-tile counter (same sequence as the producer)
-    (void)g_e;
+    (void)part;
     for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
       const int m0 = tile_m(tile) * BMT + rank * BM, tn = tile_n(tile), n0 = tn * BN;
       const int m = m0 + r;
@@ -349,47 +355,42 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       float z = 0.f;
       if constexpr (C::RING) {
-        // x_{l+1} = x0 * (acc + b) + x_l per 64-column sub-tile, written over x_l in the ring slot and
-        // TMA-stored from there; the previous sub-tile's slot is released once its store has read it
-#pragma unroll 1
-        for (int j = 0; j < C::NSUB; ++j, ++g_e) {
-          const int sl = g_e % C::RING_SLOTS;
-          ptx::mbar_wait(&efull[sl], (g_e / C::RING_SLOTS) & 1);
-          const uint32_t x0b = ptx::smem_u32(sEin + sl * 2 * C::SUB), xlb = x0b + C::SUB;
-#pragma unroll 1
-          for (int c = 0; c < 64; c += 32) {
-            float v[32], x0v[32], xlv[32];
-            ld32_tmem(trow + j * 64 + c, v);
-            lds32_bf16(x0b, r, c >> 3, x0v);
-            lds32_bf16(xlb, r, c >> 3, xlv);
-            const float4* b4 = reinterpret_cast<const float4*>(g.bias + n0 + j * 64 + c);
+        // x_{l+1} = x0 * (acc + b) + x_l on sub-tile j = part, written over x_l in slot j and TMA-stored
+        // from there; the slot is handed back once the store has read it
+        const int j = part;
+        ptx::mbar_wait(&efull[j], it & 1);
+        const uint32_t x0b = ptx::smem_u32(sEin + j * 2 * C::SUB), xlb = x0b + C::SUB;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-              const float4 bb = __ldg(b4 + u);
-              v[4 * u] = x0v[4 * u] * (v[4 * u] + bb.x) + xlv[4 * u];
-              v[4 * u + 1] = x0v[4 * u + 1] * (v[4 * u + 1] + bb.y) + xlv[4 * u + 1];
-              v[4 * u + 2] = x0v[4 * u + 2] * (v[4 * u + 2] + bb.z) + xlv[4 * u + 2];
-              v[4 * u + 3] = x0v[4 * u + 3] * (v[4 * u + 3] + bb.w) + xlv[4 * u + 3];
-            }
-            sts32_bf16(xlb, r, c >> 3, v);
-          }
-          if (j == C::NSUB - 1) {  // last TMEM read of this accumulator
+        for (int c = 0; c < 64; c += 32) {
+          float v[32], x0v[32], xlv[32];
+          ld32_tmem(trow + j * 64 + c, v);
+          if (c == 32) {  // last TMEM read of this accumulator by this warp
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tempty[a]);
           }
-          ptx::fence_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            ptx::tma_store_2d(&tmOut, sEin + sl * 2 * C::SUB + C::SUB + q * 32 * 128, n0 + j * 64, m0 + q * 32);
-            ptx::bulk_commit();
-            if (g_e > 0) {  // the previous sub-tile's store has read its slot: hand the slot back
-              ptx::bulk_wait_read<1>();
-              ptx::mbar_arrive(&eempty[(g_e - 1) % C::RING_SLOTS]);
-            }
+          lds32_bf16(x0b, r, c >> 3, x0v);
+          lds32_bf16(xlb, r, c >> 3, xlv);
+          const float4* b4 = reinterpret_cast<const float4*>(g.bias + n0 + j * 64 + c);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float4 bb = __ldg(b4 + u);
+            v[4 * u] = x0v[4 * u] * (v[4 * u] + bb.x) + xlv[4 * u];
+            v[4 * u + 1] = x0v[4 * u + 1] * (v[4 * u + 1] + bb.y) + xlv[4 * u + 1];
+            v[4 * u + 2] = x0v[4 * u + 2] * (v[4 * u + 2] + bb.z) + xlv[4 * u + 2];
+            v[4 * u + 3] = x0v[4 * u + 3] * (v[4 * u + 3] + bb.w) + xlv[4 * u + 3];
           }
-          __syncwarp();
+          sts32_bf16(xlb, r, c >> 3, v);
         }
+        ptx::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::tma_store_2d(&tmOut, sEin + j * 2 * C::SUB + C::SUB + q * 32 * 128, n0 + j * 64, m0 + q * 32);
+          ptx::bulk_commit();
+          ptx::bulk_wait_read<0>();
+          ptx::mbar_arrive(&eempty[j]);
+        }
+        __syncwarp();
       } else if constexpr (EPI == EPI_SUM_LN) {
         // pass 1: y = acc + b + in, written back into TMEM; row sum
         float sum = 0.f;
@@ -427,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       } else {
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = part * C::COLS_W; c < (part + 1) * C::COLS_W; c += 32) {
           float v[32];
           ld32_tmem(trow + c, v);
           const int n = n0 + c;
@@ -503,7 +504,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint8_t* ob = sOut + (C::OUT_BUFS == 2 ? a : 0) * C::OUT_BYTES;
 #pragma unroll
           for (int j = 0; j < C::NSUB; ++j)
-            ptx::tma_store_2d(&tmOut, ob + j * C::SUB + q * 32 * 128, n0 + j * 64, m0 + q * 32);
+            if (j * 64 >= part * C::COLS_W && j * 64 < (part + 1) * C::COLS_W)
+              ptx::tma_store_2d(&tmOut, ob + j * C::SUB + q * 32 * 128, n0 + j * 64, m0 + q * 32);
           ptx::bulk_commit();
         }
       }
@@ -539,7 +541,7 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s) {
   const int grid = (n_tiles < max_units ? n_tiles : max_units) * CG * CN;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(C::NT);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];

@@ -274,3 +274,24 @@ def test_c2_u_tile_192_bitexact(c2, B):
     sel = np.arange(B) if B <= 333 else np.random.default_rng(2).choice(B, 256, replace=False)
     ref = O.score_forward(cfg, cs.table_specs(cfg), w, sub_batch(bt, sel))["scores"]
     assert np.abs(s192[torch.from_numpy(sel).cuda()].double().cpu().numpy() - ref).max() <= TOL_BF16
+
+
+@pytest.mark.parametrize("B", [4096, 333, 1])
+def test_c2_xv_splitk(c2, B):
+    """t = x_l V^T as a K-split cluster GEMM (4 partials summed in DSMEM in a fixed order) vs one 128 x 64
+    tile accumulator: both meet the oracle, and they agree to fp32 summation-order rounding of t."""
+    cfg, m, tabs, w = c2
+    bt = cs.make_batch(cfg, 53, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    s_tile = m.dense(x0, B).clone()
+    m.set_option("xv_splitk", 1)
+    try:
+        s_split = m.dense(x0, B).clone()
+    finally:
+        m.set_option("xv_splitk", 0)
+    assert (s_split - s_tile).abs().max().item() <= 5e-4
+    sel = np.arange(B) if B <= 333 else np.random.default_rng(3).choice(B, 256, replace=False)
+    ref = O.score_forward(cfg, cs.table_specs(cfg), w, sub_batch(bt, sel))["scores"]
+    for s in (s_split, s_tile):
+        assert np.abs(s[torch.from_numpy(sel).cuda()].double().cpu().numpy() - ref).max() <= TOL_BF16
