@@ -54,12 +54,14 @@ class CvrConfig:
     n_dense: int                     # F
     bag: Tuple                       # ('uniform', lo, hi) | ('poisson', lam)
     zipf_a: float
-    backbone: str                    # 'dcn_full' | 'dcn_lowrank' | 'ensemble'
-    n_cross: int
-    cross_rank: int                  # 0 for full rank
+    backbone: str                    # 'dcn_full' | 'dcn_lowrank' | 'ensemble' | 'masknet'
+    n_cross: int                     # cross / ensemble layers; masknet: sequential blocks per branch
+    cross_rank: int                  # 0 for full rank; masknet: mask hidden width r
     mlp_dims: Tuple[int, ...]        # hidden widths after the backbone (head 1 is implicit)
     n_heads: int = 0                 # ensemble only
     ffn_dim: int = 0                 # ensemble only
+    cross_width: int = 0             # masknet: projected cross input width W' (ReLU projection of x0)
+    n_parallel: int = 1              # masknet: parallel branches (outputs concatenated)
     scramble: bool = True            # A3
     zipf_mode: str = "truncated"     # A2 ('truncated' | 'clip')
 
@@ -88,7 +90,12 @@ C3 = CvrConfig("c3", 1003, 65536, 100, (10_000_000,) * 100, 128, "f16", "bf16", 
 C3S = C3.with_(name="c3s", seed=1013, rows=(5_000_000,) * 100)
 C4 = CvrConfig("c4", 1004, 8192, 64, (1_000_000,) * 64, 256, "bf16", "bf16", 0, ("poisson", 3.0), 1.05,
                "ensemble", 4, 512, (2048, 512), n_heads=4, ffn_dim=1024)
-CONFIGS: Dict[str, CvrConfig] = {c.name: c for c in (C1, C2, C3, C3S, C4)}
+# SURVEY.md §8(f) #1 (not a BASELINE.json config): MaskNet on config 2's features, at the paper's default
+# MaskNet scaling factors (Table 1: cross width 2k, deep width 1k, 2 parallel
+# blocks, no sequential blocks); mask hidden width r = 512 (unstated; the DCN configs' low-rank reading).
+C6 = C2.with_(name="c6", seed=1006, backbone="masknet", n_cross=1, cross_rank=512, cross_width=2048,
+              n_parallel=2, mlp_dims=(1024, 512, 256))
+CONFIGS: Dict[str, CvrConfig] = {c.name: c for c in (C1, C2, C3, C3S, C4, C6)}
 
 
 # ---------------------------------------------------------------------------------
@@ -214,6 +221,15 @@ def weight_shapes(cfg: CvrConfig) -> List[Tuple[str, Tuple[int, ...]]]:
                   (f"ens/{l}/ffn/W2", (D, cfg.ffn_dim)), (f"ens/{l}/ffn/b2", (D,)),
                   (f"ens/{l}/ln/gamma", (D,)), (f"ens/{l}/ln/beta", (D,))]
         prev = W
+    elif cfg.backbone == "masknet":
+        Wp = cfg.cross_width or W
+        if cfg.cross_width:
+            s += [("proj/W", (Wp, W)), ("proj/b", (Wp,))]
+        for p in range(cfg.n_parallel):
+            for q in range(cfg.n_cross):
+                s += [(f"mask/{p}/{q}/V", (cfg.cross_rank, Wp)), (f"mask/{p}/{q}/c", (cfg.cross_rank,)),
+                      (f"mask/{p}/{q}/U", (Wp, cfg.cross_rank)), (f"mask/{p}/{q}/b", (Wp,))]
+        prev = cfg.n_parallel * Wp
     else:
         raise ValueError(cfg.backbone)
     for i, h in enumerate(cfg.mlp_dims):
@@ -233,7 +249,8 @@ def make_weights(cfg: CvrConfig) -> Dict[str, torch.Tensor]:
             x = np.full(shape, NORM_MEAN)
         elif name == "norm/std":
             x = np.full(shape, NORM_STD)
-        elif role == "gamma":
+        elif role == "gamma" or (name.startswith("mask/") and role == "b"):
+            # multiplicative parameters start around 1 (A12 for LN gamma; A27 for the MaskNet mask bias)
             x = 1.0 + rng.normal(0.0, 0.1, size=shape)
         elif len(shape) == 1 or role in ("beta",):
             x = rng.normal(0.0, 0.1, size=shape)          # biases: N(0, 0.01) (variance), A12

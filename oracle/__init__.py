@@ -21,6 +21,11 @@ the readings A1..A26 used where the paper is silent, restated in DESIGN.md §3):
   O8 ensemble   Y = LN_token(DCN(X) + MHA(X) + FFN(X))              PAPER.md:243-258, A20
                 (parity unpinned against the paper: the paper gives no formula for the
                  ensemble layer; pinned only to the A20 reading)
+  O10 MaskNet   x0' = ReLU(W_in x0 + b_in)                         PAPER.md:227-228 ("scale the
+                input x0 via one-layer relu projection"); block
+                x_{l+1} = (U_l ReLU(V_l x0' + c_l) + b_l) * x_l      PAPER.md:226 (eq. "MaskNet uses"),
+                no residual; parallel branches concatenated / sequential
+                blocks chained; biases c_l, b_l per reading A27
 
 Parameters are the *stored* (fp32 / bf16 / fp16) values widened exactly to fp64 (A13).
 """
@@ -34,7 +39,8 @@ import numpy as np
 __all__ = [
     "validate_csr", "embedding_bag_sum", "normalize_dense", "concat_x0", "cross_full",
     "cross_lowrank", "mlp_relu", "head_logit", "sigmoid", "layer_norm_tokens", "mha_tokens",
-    "ffn_tokens", "ensemble_layer", "score_forward", "dense_forward", "to_f64",
+    "ffn_tokens", "ensemble_layer", "masknet_project", "masknet_block", "masknet_forward", "score_forward",
+    "dense_forward", "to_f64",
 ]
 
 
@@ -180,6 +186,35 @@ def ensemble_layer(X0: np.ndarray, Xl: np.ndarray, P: Dict[str, np.ndarray], l: 
     return layer_norm_tokens(y, g("ln/gamma"), g("ln/beta")).reshape(B, -1)
 
 
+# -- O10 MaskNet ----------------------------------------------------
+def masknet_project(x0: np.ndarray, W: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """"scale the input x0 via one-layer relu projection": x0' = max(0, W x0 + b),
+    W [W', W] (the cross width W' of Table 1)."""
+    return np.maximum(x0 @ W.T + b, 0.0)
+
+
+def masknet_block(x_in: np.ndarray, x0p: np.ndarray, U: np.ndarray, V: np.ndarray, c: np.ndarray,
+                  b: np.ndarray) -> np.ndarray:
+    """x_{l+1} = U_l(ReLU(V_l x0)) * x_l, biases per A27: (U ReLU(V x0' + c) + b) * x_in.
+    No residual ("omits the residual connection present in DCNv2").  V [r, W'], U [W', r]."""
+    return (np.maximum(x0p @ V.T + c, 0.0) @ U.T + b) * x_in
+
+
+def masknet_forward(cfg, P: Dict[str, np.ndarray], x0: np.ndarray) -> np.ndarray:
+    """n_parallel branches, each a chain of n_cross blocks M(x, x0') starting from x0',
+    concatenated in branch order ("Concat(M_0(x0, x0), ...)" / "M_n(...M_1(x0, x0)..., x0)"; SPEC.md's
+    mixed mode = a sequential chain inside each parallel branch)."""
+    x0p = masknet_project(x0, P["proj/W"], P["proj/b"]) if cfg.cross_width else x0
+    outs = []
+    for p in range(cfg.n_parallel):
+        x = x0p
+        for q in range(cfg.n_cross):
+            g = lambda n: P[f"mask/{p}/{q}/{n}"]
+            x = masknet_block(x, x0p, g("U"), g("V"), g("c"), g("b"))
+        outs.append(x)
+    return np.concatenate(outs, axis=1)
+
+
 # -- whole path -------------------------------------------------------------------------
 def dense_forward(cfg, P: Dict[str, np.ndarray], x0: np.ndarray) -> Dict[str, np.ndarray]:
     """S5-S7 on an fp64 x0 [B, W]: backbone, MLP tower, head, sigmoid."""
@@ -193,6 +228,8 @@ def dense_forward(cfg, P: Dict[str, np.ndarray], x0: np.ndarray) -> Dict[str, np
     elif cfg.backbone == "ensemble":
         for l in range(cfg.n_cross):
             xl = ensemble_layer(x0, xl, P, l, cfg.n_heads, cfg.n_tables)
+    elif cfg.backbone == "masknet":
+        xl = masknet_forward(cfg, P, x0)
     else:
         raise ValueError(cfg.backbone)
     h = xl

@@ -3,7 +3,7 @@
 No numpy matmul, no vectorisation: plain Python floats (IEEE fp64), one loop per index,
 so it checks ``oracle.score_forward`` (P8 of SURVEY.md §8(c)) through an independent
 evaluation order.  Same paper passages as the batched oracle: PAPER.md:96 (pooling),
-95 (standardisation), 116-119 / 225 (DCN-v2 cross), 229-233 (MLP), north star (sigmoid).
+95 (standardisation), 116-119 / 225 (DCN-v2 cross), 226-233 (MaskNet), 229-233 (MLP), north star (sigmoid).
 """
 from __future__ import annotations
 
@@ -53,8 +53,28 @@ def brute_score_one(cfg, tables: Sequence, P: Dict, indices, offsets, dense_row,
             y = _mat_vec(tolist(P[f"dcn/{l}/U"]), t_)
             bb = tolist(P[f"dcn/{l}/b"])
             xl = [x0[i] * (y[i] + bb[i]) + xl[i] for i in range(len(xl))]
+    elif cfg.backbone == "masknet":  # PAPER.md:226-233, biases per A27
+        if cfg.cross_width:
+            y = _mat_vec(tolist(P["proj/W"]), x0)
+            bb = tolist(P["proj/b"])
+            x0p = [max(0.0, y[i] + bb[i]) for i in range(len(y))]
+        else:
+            x0p = list(x0)
+        cat: List[float] = []
+        for p in range(cfg.n_parallel):
+            x = list(x0p)
+            for q in range(cfg.n_cross):
+                g = lambda n: tolist(P[f"mask/{p}/{q}/{n}"])
+                hv = _mat_vec(g("V"), x0p)
+                cv = g("c")
+                hid = [max(0.0, hv[k] + cv[k]) for k in range(len(hv))]
+                mv = _mat_vec(g("U"), hid)
+                bv = g("b")
+                x = [(mv[i] + bv[i]) * x[i] for i in range(len(x))]
+            cat.extend(x)
+        xl = cat
     else:
-        raise NotImplementedError("brute force covers the DCN-v2 configs")
+        raise NotImplementedError("brute force covers the DCN-v2 and MaskNet configs")
     h = xl
     for i in range(len(cfg.mlp_dims)):
         y = _mat_vec(tolist(P[f"mlp/{i}/W"]), h)

@@ -237,3 +237,71 @@ def test_mha_uniform_attention_is_mean():
     o = O.mha_tokens(X, Wqkv, np.zeros(24), np.eye(8), np.zeros(8), 2)
     v = X @ Wqkv[16:].T
     np.testing.assert_allclose(o, np.broadcast_to(v.mean(axis=1, keepdims=True), o.shape), rtol=1e-13, atol=1e-14)
+
+
+# ---- MaskNet: E6 goldens, SPEC.md:259-270 closed forms, brute force -------
+def test_E6_masknet_projection_and_block():
+    g = gold("E6_masknet.json")
+    pj = g["projection"]
+    out = O.masknet_project(np.array([pj["x0"]], float), np.array(pj["W"], float), np.array(pj["b"], float))
+    np.testing.assert_array_equal(out[0], pj["out"])
+    bk = g["block"]
+    args = [np.array(bk[k], float) for k in ("U", "V", "c", "b")]
+    x0p = np.array([bk["x0p"]], float)
+    out = O.masknet_block(np.array([bk["x_in"]], float), x0p, *args)
+    np.testing.assert_array_equal(out[0], bk["out"], err_msg=bk["derivation"])
+    out2 = O.masknet_block(out, x0p, *args)
+    np.testing.assert_array_equal(out2[0], g["sequential2"]["out"], err_msg=g["sequential2"]["derivation"])
+
+
+def _tiny_masknet_cfg(P=2, S=1, width=0):
+    return cs.C2.with_(name="c6tiny", n_tables=1, rows=(4,), dim=2, n_dense=0, backbone="masknet", n_cross=S,
+                       cross_rank=2, cross_width=width, n_parallel=P, mlp_dims=())
+
+
+def test_E6_masknet_forward_parallel_and_sequential():
+    g = gold("E6_masknet.json")
+    bk = g["block"]
+    Pm = {f"mask/{p}/{q}/{k}": np.array(bk[k], float) for p in range(2) for q in range(2) for k in ("U", "V", "c", "b")}
+    x0 = np.array([bk["x0p"]], float)
+    par = O.masknet_forward(_tiny_masknet_cfg(P=2, S=1), Pm, x0)
+    np.testing.assert_array_equal(par[0], g["parallel2"]["out"])
+    seq = O.masknet_forward(_tiny_masknet_cfg(P=1, S=2), Pm, x0)
+    np.testing.assert_array_equal(seq[0], g["sequential2"]["out"])
+
+
+def test_masknet_closed_forms():
+    """ReLU kills the mask -> output = b * x_in (0 when b = 0); unit mask (U = 0, b = 1) ->
+    x_out = x_in; 1 parallel block == 1 sequential block; 2 identical parallel blocks -> duplicated output."""
+    rng = np.random.default_rng(5)
+    B, W, r = 7, 12, 5
+    x0p = np.abs(rng.normal(size=(B, W)))
+    x_in = rng.normal(size=(B, W))
+    V = -np.abs(rng.normal(size=(r, W)))      # V x0p < 0 for a non-negative x0p
+    U = rng.normal(size=(W, r))
+    np.testing.assert_array_equal(O.masknet_block(x_in, x0p, U, V, np.zeros(r), np.zeros(W)), np.zeros((B, W)))
+    b = rng.normal(size=W)
+    np.testing.assert_array_equal(O.masknet_block(x_in, x0p, U, V, np.zeros(r), b), b * x_in)
+    np.testing.assert_array_equal(
+        O.masknet_block(x_in, x0p, np.zeros((W, r)), rng.normal(size=(r, W)), rng.normal(size=r), np.ones(W)), x_in)
+    P = {f"mask/0/0/{k}": v for k, v in zip("UVcb", (U, rng.normal(size=(r, W)), rng.normal(size=r), b))}
+    for k in "UVcb":
+        P[f"mask/1/0/{k}"] = P[f"mask/0/0/{k}"]
+    cfgP1 = _tiny_masknet_cfg(P=1, S=1).with_(dim=W, n_tables=1)
+    one = O.masknet_forward(cfgP1, P, x0p)
+    np.testing.assert_array_equal(one, O.masknet_forward(cfgP1.with_(n_parallel=1, n_cross=1), P, x0p))
+    two = O.masknet_forward(cfgP1.with_(n_parallel=2), P, x0p)
+    np.testing.assert_array_equal(two, np.concatenate([one, one], axis=1))
+
+
+def test_P8_masknet_batched_vs_brute():
+    cfg = cs.C6.with_(name="c6small", n_tables=4, rows=cs.C2.rows[:4], n_dense=8, cross_rank=16, cross_width=48,
+                      n_parallel=2, n_cross=2, mlp_dims=(32, 16, 8), batch=32)
+    tabs = cs.table_specs(cfg)
+    w = cs.make_weights(cfg)
+    bt = cs.make_batch(cfg, 0, batch=32)
+    out = O.score_forward(cfg, tabs, w, bt)
+    P = {k: O.to_f64(v) for k, v in w.items()}
+    for b in (0, 17, 31):
+        s = brute_score_one(cfg, tabs, P, bt.indices, bt.offsets, bt.dense[b], b, 32)
+        assert abs(s - out["scores"][b]) <= 1e-12 * max(1.0, abs(s))
