@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="cvr", choices=["cvr", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4", "c3s"],
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4", "c3s", "c6"],
                     help="workload (default: config 2, the metric's single-GPU config)")
     ap.add_argument("--ring", type=int, default=8, help="distinct pre-uploaded batches cycled through")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -145,7 +145,10 @@ def launch_work(cfg, B) -> dict:
     """Algorithmic work of ONE launch of each kernel role for batch B: (bound, amount), amount in FLOPs
     (2 per MAC) for tensor / alu roles."""
     W, r = cfg.width, cfg.cross_rank
-    dims = [W] + list(cfg.mlp_dims)
+    mask = cfg.backbone == "masknet"
+    Wp = getattr(cfg, "cross_width", 0) or W
+    nb = getattr(cfg, "n_parallel", 1) * cfg.n_cross
+    dims = [getattr(cfg, "n_parallel", 1) * Wp if mask else W] + list(cfg.mlp_dims)
     hidden = [2 * B * dims[i] * dims[i + 1] for i in range(len(cfg.mlp_dims) - 1)]
     w = {"gemm_mlp_relu": ("tensor", sum(hidden) / max(1, len(hidden))),
          "gemm_mlp_head": ("tensor", 2 * B * dims[-2] * dims[-1] + 2 * B * dims[-1]),
@@ -153,6 +156,10 @@ def launch_work(cfg, B) -> dict:
     if cfg.backbone == "dcn_full":
         w["dense_f32_dcn"] = ("alu", 2 * B * (cfg.n_cross * W * W + sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1))
                                               + dims[-1]))
+    elif mask:  # MaskNet: projection, all blocks' mask hiddens, one mask GEMM per block
+        w["gemm_mask_proj"] = ("tensor", 2 * B * W * Wp)
+        w["gemm_mask_hidden"] = ("tensor", 2 * B * Wp * nb * r)
+        w["gemm_mask_mul"] = ("tensor", 2 * B * r * Wp)
     else:
         w["gemm_xV"] = ("tensor", 2 * B * W * r)
         w["gemm_tU_cross"] = ("tensor", 2 * B * r * W)
@@ -177,6 +184,10 @@ def dense_flops_per_example(cfg) -> int:
     if cfg.backbone == "dcn_full":
         return int(w["dense_f32_dcn"][1])
     n_hidden = len(cfg.mlp_dims) - 1
+    if cfg.backbone == "masknet":
+        nb = cfg.n_parallel * cfg.n_cross
+        return int(w["gemm_mask_proj"][1] + w["gemm_mask_hidden"][1] + nb * w["gemm_mask_mul"][1]
+                   + n_hidden * w["gemm_mlp_relu"][1] + w["gemm_mlp_head"][1])
     return int(cfg.n_cross * sum(w[k][1] for k in layer_roles) + n_hidden * w["gemm_mlp_relu"][1] + w["gemm_mlp_head"][1])
 
 
@@ -187,8 +198,10 @@ WORKLOADS = {
     "c3s": "c3-S: BASELINE.json configs[2] strong-scaling variant (100 x 5e6 x 128 fp16 tables, B=65536, W=12864)",
     "c4": "c4: BASELINE.json configs[3] backbone-scaled (64 x 1e6 x 256 bf16, 4 ensemble layers DCN||MHA||FFN + LN, "
           "head 16384-2048-512-1)",
+    "c6": "c6: SURVEY.md §8(f) #1 MaskNet on config 2's features (ReLU projection 1728->2048, 2 parallel mask "
+          "blocks r=512, MLP 4096-1024-512-256-1; PAPER.md Table 1 MaskNet defaults), not a BASELINE.json config",
 }
-TOL = {"c1": 1e-5, "c2": 2e-3, "c3s": 2e-3, "c4": 2e-3}
+TOL = {"c1": 1e-5, "c2": 2e-3, "c3s": 2e-3, "c4": 2e-3, "c6": 2e-3}
 
 
 # ----------------------------------------------------------------------------- distributed

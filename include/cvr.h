@@ -76,7 +76,12 @@ typedef enum { CVR_F32 = 0, CVR_BF16 = 1, CVR_F16 = 2 } cvr_dtype;
 typedef enum {
   CVR_DCN_FULL = 0,     /* full-rank cross with bias, fp32 SIMT path (config 1)      */
   CVR_DCN_LOWRANK = 1,  /* low-rank cross, bf16 tcgen05 path (configs 2, 3, 5)       */
-  CVR_ENSEMBLE = 2      /* DCN || MHA || FFN, summed + layer-normed (config 4)       */
+  CVR_ENSEMBLE = 2,     /* DCN || MHA || FFN, summed + layer-normed (config 4)       */
+  CVR_MASKNET = 3       /* ReLU input projection + instance-guided mask blocks, bf16 tcgen05 path:
+                         *   x0' = ReLU(W_in x0 + b_in)
+                         *   x_{s+1} = (U ReLU(V x0' + c) + b) * x_s     PAPER.md:226 (no residual, :363)
+                         * n_parallel branches of n_cross blocks each (x_0 = x0'), outputs concatenated
+                         * (PAPER.md:229-233), then the MLP tower + head     */
 } cvr_backbone;
 
 /* Model + run description; copied by cvr_create (the arrays need not outlive the call). */
@@ -98,6 +103,8 @@ typedef struct {
   int64_t max_nnz;          /* largest nnz any call will pass (host-fed staging)        */
   int world_size;           /* 1 = unsharded; >1 = table-wise sharding (t -> t % N)     */
   int rank;                 /* this process's rank when world_size > 1                  */
+  int cross_width;          /* MASKNET: projected cross width W' (multiple of 64); else 0 */
+  int n_parallel;           /* MASKNET: parallel branches P (n_cross = blocks per branch); else 0 */
 } cvr_model_desc;
 
 /* -- lifecycle ------------------------------------------------------------------------ */
@@ -131,6 +138,9 @@ int cvr_load_tables(cvr_ctx* ctx, int n, const int* table_ids, const void* const
  *   DCN_LOWRANK: "dcn/<l>/V" [r, W], "dcn/<l>/U" [W, r], "dcn/<l>/b" [W]
  *   ENSEMBLE:    "ens/<l>/dcn/{V,U,b}", "ens/<l>/mha/{Wqkv,bqkv,Wo,bo}",
  *                "ens/<l>/ffn/{W1,b1,W2,b2}", "ens/<l>/ln/{gamma,beta}"
+ *   MASKNET:     "proj/W" [W', W], "proj/b" [W'], for branch p < P and block q < n_cross:
+ *                "mask/<p>/<q>/V" [r, W'], ".../c" [r], ".../U" [W', r], ".../b" [W'];
+ *                the MLP input width is P * W'
  *   "mlp/<i>/W" [h_i, h_{i-1}], "mlp/<i>/b" [h_i], "head/w" [1, h_last], "head/b" [1]
  * shapes is flattened: entry i has ndims[i] extents starting at the running offset.
  * Every expected name must be present exactly once (else CVR_E_SHAPE); dtypes must be

@@ -13,11 +13,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 lib_path = os.path.join(HERE, "libcvr.so")
 
 CVR_F32, CVR_BF16, CVR_F16 = 0, 1, 2
-CVR_DCN_FULL, CVR_DCN_LOWRANK, CVR_ENSEMBLE = 0, 1, 2
+CVR_DCN_FULL, CVR_DCN_LOWRANK, CVR_ENSEMBLE, CVR_MASKNET = 0, 1, 2, 3
 CVR_E_INDEX = 5
 _DT = {"f32": CVR_F32, "bf16": CVR_BF16, "f16": CVR_F16}
 _TORCH_DT = {torch.float32: CVR_F32, torch.bfloat16: CVR_BF16, torch.float16: CVR_F16}
-_BACKBONE = {"dcn_full": CVR_DCN_FULL, "dcn_lowrank": CVR_DCN_LOWRANK, "ensemble": CVR_ENSEMBLE}
+_BACKBONE = {"dcn_full": CVR_DCN_FULL, "dcn_lowrank": CVR_DCN_LOWRANK, "ensemble": CVR_ENSEMBLE,
+             "masknet": CVR_MASKNET}
 
 _c_i64p = ctypes.POINTER(ctypes.c_int64)
 _c_ip = ctypes.POINTER(ctypes.c_int)
@@ -31,6 +32,7 @@ class cvr_model_desc(ctypes.Structure):
         ("n_cross", ctypes.c_int), ("cross_rank", ctypes.c_int), ("n_mlp", ctypes.c_int), ("mlp_dims", _c_ip),
         ("n_heads", ctypes.c_int), ("ffn_dim", ctypes.c_int), ("max_batch", ctypes.c_int),
         ("max_nnz", ctypes.c_int64), ("world_size", ctypes.c_int), ("rank", ctypes.c_int),
+        ("cross_width", ctypes.c_int), ("n_parallel", ctypes.c_int),
     ]
 
 
@@ -144,7 +146,8 @@ class CvrModel:
         self.desc = cvr_model_desc(
             cfg.n_tables, self._rows, cfg.dim, _DT[cfg.emb_dtype], cfg.n_dense, _DT[cfg.act_dtype],
             _BACKBONE[cfg.backbone], cfg.n_cross, cfg.cross_rank, len(cfg.mlp_dims), self._mlp,
-            getattr(cfg, "n_heads", 0), getattr(cfg, "ffn_dim", 0), max_batch, max_nnz, world_size, rank)
+            getattr(cfg, "n_heads", 0), getattr(cfg, "ffn_dim", 0), max_batch, max_nnz, world_size, rank,
+            getattr(cfg, "cross_width", 0), getattr(cfg, "n_parallel", 0))
         self.max_batch, self.max_nnz, self.world_size, self.rank = max_batch, max_nnz, world_size, rank
         h = _vp()
         st = self.L.cvr_create(ctypes.byref(self.desc), ctypes.byref(h))

@@ -25,12 +25,13 @@ using namespace cvr;
 
 enum KernelId {
   K_EMBED = 0, K_GEMM_V, K_GEMM_U, K_GEMM_MLP, K_GEMM_HEAD, K_DENSE_F32, K_UNPACK, K_CROSS_FUSED,
-  K_ENS_QKV, K_MHA, K_ENS_OPROJ, K_ENS_FFN1, K_ENS_FFN2_LN, K_HEAD_FIN, K_CROSS_STACK, K_COUNT
+  K_ENS_QKV, K_MHA, K_ENS_OPROJ, K_ENS_FFN1, K_ENS_FFN2_LN, K_HEAD_FIN, K_CROSS_STACK,
+  K_MASK_PROJ, K_MASK_HIDDEN, K_MASK_MUL, K_COUNT
 };
 static const char* kKernelNames[K_COUNT] = {
     "embed_bag_pool", "gemm_xV",  "gemm_tU_cross",  "gemm_mlp_relu", "gemm_mlp_head", "dense_f32_dcn",
     "shard_unpack",   "cross_fused", "gemm_ens_qkv", "mha64",       "gemm_ens_oproj", "gemm_ens_ffn1",
-    "gemm_ens_ffn2_ln", "head_finalize", "cross_stack"};
+    "gemm_ens_ffn2_ln", "head_finalize", "cross_stack", "gemm_mask_proj", "gemm_mask_hidden", "gemm_mask_mul"};
 
 namespace {
 
@@ -104,6 +105,16 @@ struct cvr_ctx {
     std::vector<CUtensorMap> V, U, Wqkv, W1, Wcat;
     CUtensorMap flat_user, tok_user;
   } ens;
+  // MaskNet: x0' = ReLU(W_in x0 + b_in) [B, Wp]; H = ReLU(x0' V_all^T + c_all)
+  // [B, P*S*r] (every block's mask hidden comes from x0', so one GEMM covers them all);
+  // block (p, q): x <- (H_pq U_pq^T + b_pq) * x, the last block of branch p writing cat[:, p*Wp ..)
+  struct Mask {
+    int Wp = 0, P = 0;
+    size_t off_x0p = 0, off_H = 0, off_cat = 0, off_tmp[2] = {0, 0}, off_Vall = 0, off_call = 0;
+    CUtensorMap tm_x0p, st_x0p, st_H, tm_cat, tm_tmp[2], st_tmp[2], tmB_Vall;
+    std::vector<CUtensorMap> tm_Hblk, st_cat, tmB_U;
+    int bn_proj = 0, bn_h = 0, bn_u = 0;
+  } mk;
   size_t off_hpart = 0;   // split-head partial dot products [max_batch, last/256]
   int head_parts = 0;     // 0: head fused into the last MLP GEMM (last <= 256); else #256-wide parts
   unsigned long long* dbg = nullptr;              // CVR_DEBUG_TIMING: phase stamps of the last fused launch
@@ -246,6 +257,20 @@ void build_weight_slots(cvr_ctx* c) {
       add(p + "ln/beta", {D}, a);
     }
   }
+  if (c->backbone == CVR_MASKNET) {
+    const int Wp = c->mk.Wp;
+    add("proj/W", {Wp, c->W}, a);
+    add("proj/b", {Wp}, a);
+    for (int p = 0; p < c->mk.P; ++p)
+      for (int q = 0; q < c->n_cross; ++q) {
+        const std::string n = "mask/" + std::to_string(p) + "/" + std::to_string(q) + "/";
+        add(n + "V", {c->r, Wp}, a);
+        add(n + "c", {c->r}, a);
+        add(n + "U", {Wp, c->r}, a);
+        add(n + "b", {Wp}, a);
+      }
+    prev = c->mk.P * Wp;
+  }
   for (int i = 0; i < c->n_mlp; ++i) {
     add("mlp/" + std::to_string(i) + "/W", {c->mlp[i], prev}, a);
     add("mlp/" + std::to_string(i) + "/b", {c->mlp[i]}, a);
@@ -266,6 +291,10 @@ size_t packed_bytes(const cvr_ctx* c, const WSlot& s) {
     return (size_t)e * 4;                                              // fp32 copies
   }
   if (c->backbone == CVR_ENSEMBLE) return (size_t)s.shape[0] * s.shape[1] * 2;  // W == x0_ld: no padding
+  if (c->backbone == CVR_MASKNET) {  // only the projection reads x0 (padded to x0_ld)
+    if (n == "proj/W") return (size_t)c->mk.Wp * c->x0_ld * 2;
+    return (size_t)s.shape[0] * s.shape[1] * 2;
+  }
   // bf16 GEMM operands, padded to x0_ld along W
   if (ends("/V")) return (size_t)c->r * c->x0_ld * 2;
   if (ends("/U")) return (size_t)c->x0_ld * c->r * 2;
@@ -317,6 +346,16 @@ int validate_desc(const cvr_model_desc* d, std::string& why) {
       if (d->mlp_dims[i] % 128) return bad("hidden MLP widths must be multiples of 128 on the ensemble path");
     const int last = d->mlp_dims[d->n_mlp - 1];
     if (!(last == 64 || last == 128 || last == 256 || last % 256 == 0)) return bad("last MLP width: 64/128/256 or k*256");
+  } else if (d->backbone == CVR_MASKNET) {
+    if (d->act_dtype != CVR_BF16) return bad("MASKNET runs the bf16 tensor-core path: act_dtype must be CVR_BF16");
+    if (d->cross_width <= 0 || d->cross_width % 128) return bad("MASKNET cross_width must be a positive multiple of 128");
+    if (d->cross_rank <= 0 || d->cross_rank % 64) return bad("MASKNET cross_rank (mask hidden width) must be a multiple of 64");
+    if (d->n_parallel < 1 || d->n_parallel > 8 || d->n_cross < 1) return bad("MASKNET needs n_parallel in [1, 8], n_cross >= 1");
+    for (int i = 0; i < d->n_mlp; ++i)
+      if (d->mlp_dims[i] % 64) return bad("mlp_dims must be multiples of 64 on the bf16 path");
+    const int last = d->mlp_dims[d->n_mlp - 1];
+    if (!(last == 64 || last == 128 || last == 256 || last % 256 == 0))
+      return bad("last MLP width must be 64, 128, 256 (fused head) or a multiple of 256 (split head)");
   } else {
     return CVR_E_UNSUPPORTED;
   }
@@ -390,6 +429,10 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
   c->world = desc->world_size;
   c->rank = desc->rank;
   c->W = c->T * c->d + c->F;
+  if (c->backbone == CVR_MASKNET) {
+    c->mk.Wp = desc->cross_width;
+    c->mk.P = desc->n_parallel;
+  }
   c->x0_ld = c->act == CVR_F32 ? round_up(c->W, 4) : round_up(c->W, 64);
   for (int t = 0; t < c->T; ++t)
     if (t % c->world == c->rank) c->local_tables.push_back(t);
@@ -430,6 +473,17 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
       c->ens.off_catW.push_back(carve(cur, (size_t)c->d * (c->d + c->ffn) * 2));
       c->ens.off_catb.push_back(carve(cur, (size_t)c->d * 4));
     }
+    for (int i = 0; i + 1 < c->n_mlp; ++i) c->off_h.push_back(carve(cur, (size_t)B * c->mlp[i] * 2));
+  } else if (c->backbone == CVR_MASKNET) {
+    auto& K = c->mk;
+    const int nb = K.P * c->n_cross;
+    K.off_x0p = carve(cur, (size_t)B * K.Wp * 2);
+    K.off_H = carve(cur, (size_t)B * nb * c->r * 2);
+    K.off_cat = carve(cur, (size_t)B * K.P * K.Wp * 2);
+    if (c->n_cross > 1)
+      for (int i = 0; i < 2; ++i) K.off_tmp[i] = carve(cur, (size_t)B * K.Wp * 2);
+    K.off_Vall = carve(cur, (size_t)nb * c->r * K.Wp * 2);
+    K.off_call = carve(cur, (size_t)nb * c->r * 4);
     for (int i = 0; i + 1 < c->n_mlp; ++i) c->off_h.push_back(carve(cur, (size_t)B * c->mlp[i] * 2));
   }
   if (c->backbone != CVR_DCN_FULL) {
@@ -602,6 +656,41 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     }
     if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
   }
+  if (c->backbone == CVR_MASKNET) {
+    const char* er = nullptr;
+    const int64_t B = c->max_batch;
+    auto& K = c->mk;
+    const int nb = K.P * c->n_cross, HW = nb * c->r, CW = K.P * K.Wp;
+    bool ok = true;
+    for (int i = 0; i < 2; ++i) {
+      ok &= encode_tmap_bf16(&c->tm_x0slot[i], c->ws + c->off_x0[i], B, c->x0_ld, c->x0_ld, 128, &er) == 0;
+      ok &= c->add_q(&c->tm_x0slot[i], c->ws + c->off_x0[i], B, c->x0_ld, c->x0_ld, &er) == 0;
+    }
+    ok &= encode_tmap_bf16(&K.tm_x0p, c->ws + K.off_x0p, B, K.Wp, K.Wp, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&K.st_x0p, c->ws + K.off_x0p, B, K.Wp, K.Wp, 32, &er) == 0;
+    ok &= encode_tmap_bf16(&K.st_H, c->ws + K.off_H, B, HW, HW, 32, &er) == 0;
+    K.tm_Hblk.assign(nb, CUtensorMap{});
+    for (int j = 0; j < nb; ++j)  // the r columns of block j inside H (row stride P*S*r)
+      ok &= encode_tmap_bf16(&K.tm_Hblk[j], c->ws + K.off_H + (size_t)j * c->r * 2, B, c->r, HW, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&K.tm_cat, c->ws + K.off_cat, B, CW, CW, 128, &er) == 0;
+    ok &= c->add_q(&K.tm_cat, c->ws + K.off_cat, B, CW, CW, &er) == 0;
+    K.st_cat.assign(K.P, CUtensorMap{});
+    for (int p = 0; p < K.P; ++p)
+      ok &= encode_tmap_bf16(&K.st_cat[p], c->ws + K.off_cat + (size_t)p * K.Wp * 2, B, K.Wp, CW, 32, &er) == 0;
+    if (c->n_cross > 1)
+      for (int i = 0; i < 2; ++i) {
+        ok &= encode_tmap_bf16(&K.tm_tmp[i], c->ws + K.off_tmp[i], B, K.Wp, K.Wp, 128, &er) == 0;
+        ok &= encode_tmap_bf16(&K.st_tmp[i], c->ws + K.off_tmp[i], B, K.Wp, K.Wp, 32, &er) == 0;
+      }
+    c->tm_h.resize(c->off_h.size());
+    c->st_h.resize(c->off_h.size());
+    for (size_t i = 0; i < c->off_h.size(); ++i) {
+      ok &= encode_tmap_bf16(&c->tm_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], 128, &er) == 0;
+      ok &= encode_tmap_bf16(&c->st_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], 32, &er) == 0;
+      ok &= c->add_q(&c->tm_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], &er) == 0;
+    }
+    if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
+  }
   if (c->backbone == CVR_ENSEMBLE) {
     const char* er = nullptr;
     const int64_t B = c->max_batch, BT = B * c->T, D = c->d, W = c->x0_ld;
@@ -757,6 +846,65 @@ int encode_plan_ensemble(cvr_ctx* c) {
   return CVR_OK;
 }
 
+// MaskNet plan: V_all / c_all assembled from the loaded blocks (block j = p * S + q), B maps of the
+// projection, the hidden GEMM and every block's U; then the MLP tower as on the low-rank path.
+int encode_plan_masknet(cvr_ctx* c) {
+  const char* er = nullptr;
+  auto& K = c->mk;
+  const int S = c->n_cross, nb = K.P * S, r = c->r, Wp = K.Wp;
+  for (int p = 0; p < K.P; ++p)
+    for (int q = 0; q < S; ++q) {
+      const int j = p * S + q;
+      const std::string n = "mask/" + std::to_string(p) + "/" + std::to_string(q) + "/";
+      cudaError_t e1 = cudaMemcpy(c->ws + K.off_Vall + (size_t)j * r * Wp * 2, c->wptr(n + "V"), (size_t)r * Wp * 2,
+                                  cudaMemcpyDeviceToDevice);
+      cudaError_t e2 = cudaMemcpy(c->ws + K.off_call + (size_t)j * r * 4, c->wptr(n + "c"), (size_t)r * 4,
+                                  cudaMemcpyDeviceToDevice);
+      if (e1 != cudaSuccess || e2 != cudaSuccess) return c->fail(CVR_E_CUDA, "assembling the MaskNet V_all / c_all");
+    }
+  const int64_t M = c->max_batch;
+  K.bn_proj = pick_bn(Wp, M);
+  K.bn_h = pick_bn(nb * r, M);
+  K.bn_u = Wp % 128 == 0 ? 128 : 64;
+  bool ok = true;
+  c->plan.clear();
+  GemmPlan gp;
+  gp.N = Wp;
+  gp.K = (int)c->x0_ld;
+  gp.BN = K.bn_proj;
+  gp.epi = EPI_BIAS_RELU;
+  gp.wname = nullptr;
+  ok &= encode_tmap_bf16(&gp.tmB, c->wptr("proj/W"), Wp, c->x0_ld, c->x0_ld, gp.BN, &er) == 0;
+  c->plan.push_back(gp);  // plan[0]: projection
+  ok &= encode_tmap_bf16(&K.tmB_Vall, c->ws + K.off_Vall, (int64_t)nb * r, Wp, Wp, K.bn_h, &er) == 0;
+  K.tmB_U.assign(nb, CUtensorMap{});
+  for (int p = 0; p < K.P; ++p)
+    for (int q = 0; q < S; ++q)
+      ok &= encode_tmap_bf16(&K.tmB_U[p * S + q],
+                             c->wptr("mask/" + std::to_string(p) + "/" + std::to_string(q) + "/U"), Wp, r, r, K.bn_u,
+                             &er) == 0;
+  int Kd = K.P * Wp;
+  for (int i = 0; i < c->n_mlp; ++i) {
+    const bool last = i + 1 == c->n_mlp;
+    GemmPlan g;
+    g.N = c->mlp[i];
+    g.K = Kd;
+    g.epi = last ? (c->head_parts ? EPI_HEAD_PARTIAL : EPI_HEAD) : EPI_BIAS_RELU;
+    g.BN = last ? (c->head_parts ? 256 : c->mlp[i]) : pick_bn(c->mlp[i], M);
+    const bool head_mc = last && !c->head_parts && c->mc && c->mlp[i] % 256 == 0;
+    if (head_mc) {
+      g.BN = c->mlp[i] / 4;
+      g.cn = 4;
+    }
+    g.wname = nullptr;
+    ok &= encode_tmap_bf16(&g.tmB, c->wptr("mlp/" + std::to_string(i) + "/W"), g.N, Kd, Kd, g.BN, &er) == 0;
+    c->plan.push_back(g);  // plan[1 + i]: MLP
+    Kd = c->mlp[i];
+  }
+  if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
+  return CVR_OK;
+}
+
 // widen a caller weight (fp32 / bf16) to host fp32
 std::vector<float> fetch_f32(const void* d, int dtype, size_t n, cudaError_t& e) {
   std::vector<float> out(n);
@@ -831,7 +979,8 @@ int cvr_load_weights(cvr_ctx* c, int n, const char* const* names, const void* co
       const int64_t O = s.shape[0], I = s.shape[1];
       for (int64_t o = 0; o < O; ++o)
         for (int64_t ii = 0; ii < I; ++ii) pf[ii * O + o] = h[o * I + ii];
-    } else if (ends("/V") || nm == "mlp/0/W") {  // [out, W] -> [out, x0_ld] zero padded
+    } else if ((c->backbone == CVR_MASKNET && nm == "proj/W") ||
+               (c->backbone != CVR_MASKNET && (ends("/V") || nm == "mlp/0/W"))) {  // [out, W] -> [out, x0_ld]
       const int64_t O = s.shape[0], I = s.shape[1];
       for (int64_t o = 0; o < O; ++o)
         for (int64_t ii = 0; ii < I; ++ii) pb[o * c->x0_ld + ii] = bf(h[o * I + ii]);
@@ -860,6 +1009,9 @@ int cvr_load_weights(cvr_ctx* c, int n, const char* const* names, const void* co
     if (e != cudaSuccess) return c->cuda_fail(e, "upload cross-stack tables");
   } else if (c->backbone == CVR_ENSEMBLE) {
     int st = encode_plan_ensemble(c);
+    if (st != CVR_OK) return st;
+  } else if (c->backbone == CVR_MASKNET) {
+    int st = encode_plan_masknet(c);
     if (st != CVR_OK) return st;
   }
   c->weights_loaded = true;
@@ -1052,6 +1204,76 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
   return run_mlp_head(c, flat_xl, 0, B, scores, s);
 }
 
+// MaskNet dense stage: projection, all blocks' mask hiddens in one GEMM, one mask GEMM
+// per block (EPI_MASK: (H U^T + b) * x), then the MLP tower + head on the concatenated branches.
+int do_dense_masknet(cvr_ctx* c, const CUtensorMap* tm_x0, int B, float* scores, cudaStream_t s) {
+  auto& K = c->mk;
+  const int S = c->n_cross, nb = K.P * S;
+  cudaError_t e;
+  GemmArgs a = gemm_args(c, c->plan[0], tm_x0, B);  // x0' = ReLU(x0 W_in^T + b_in)
+  a.bias = c->wptr<float>("proj/b");
+  a.tmOut = &K.st_x0p;
+  if ((e = run_gemm(c, a, K_MASK_PROJ, s)) != cudaSuccess) return c->cuda_fail(e, "MaskNet projection");
+  GemmPlan gh;
+  gh.N = nb * c->r;
+  gh.K = K.Wp;
+  gh.BN = K.bn_h;
+  gh.epi = EPI_BIAS_RELU;
+  GemmArgs ah = gemm_args(c, gh, &K.tm_x0p, B);  // H = ReLU(x0' V_all^T + c_all)
+  ah.tmB = &K.tmB_Vall;
+  ah.bias = c->at<float>(K.off_call);
+  ah.tmOut = &K.st_H;
+  if ((e = run_gemm(c, ah, K_MASK_HIDDEN, s)) != cudaSuccess) return c->cuda_fail(e, "MaskNet mask hidden");
+  for (int p = 0; p < K.P; ++p) {
+    const CUtensorMap* x_in = &K.tm_x0p;
+    for (int q = 0; q < S; ++q) {
+      const int j = p * S + q;
+      GemmPlan gu;
+      gu.N = K.Wp;
+      gu.K = c->r;
+      gu.BN = K.bn_u;
+      gu.epi = EPI_MASK;
+      GemmArgs au = gemm_args(c, gu, &K.tm_Hblk[j], B);
+      au.tmB = &K.tmB_U[j];
+      au.tmXl = x_in;
+      au.bias = c->wptr<float>("mask/" + std::to_string(p) + "/" + std::to_string(q) + "/b");
+      au.tmOut = q + 1 == S ? &K.st_cat[p] : &K.st_tmp[q % 2];
+      if ((e = run_gemm(c, au, K_MASK_MUL, s)) != cudaSuccess) return c->cuda_fail(e, "MaskNet mask block");
+      x_in = &K.tm_tmp[q % 2];
+    }
+  }
+  // MLP tower + head on cat [B, P * Wp]: plan[1..]
+  cudaError_t e2;
+  const CUtensorMap* tm_in = &K.tm_cat;
+  for (int i = 0; i < c->n_mlp; ++i) {
+    const GemmPlan& g = c->plan[1 + i];
+    GemmArgs am = gemm_args(c, g, tm_in, B);
+    am.bias = c->wptr<float>("mlp/" + std::to_string(i) + "/b");
+    int kid = K_GEMM_MLP;
+    if (g.epi == EPI_HEAD) {
+      am.head_w = c->wptr<float>("head/w");
+      am.head_b = c->head_b;
+      am.scores = scores;
+      kid = K_GEMM_HEAD;
+    } else if (g.epi == EPI_HEAD_PARTIAL) {
+      am.head_w = c->wptr<float>("head/w");
+      am.partial = c->at<float>(c->off_hpart);
+      kid = K_GEMM_HEAD;
+    } else {
+      am.tmOut = &c->st_h[i];
+    }
+    if ((e2 = run_gemm(c, am, kid, s)) != cudaSuccess) return c->cuda_fail(e2, "MaskNet MLP launch");
+    if (g.epi == EPI_HEAD_PARTIAL) {
+      c->pbeg(s);
+      e2 = launch_head_finalize(c->at<float>(c->off_hpart), c->head_parts, c->head_b, scores, B, s);
+      c->pend(K_HEAD_FIN, s);
+      if (e2 != cudaSuccess) return c->cuda_fail(e2, "head finalize launch");
+    }
+    if (g.epi == EPI_BIAS_RELU) tm_in = &c->tm_h[i];
+  }
+  return CVR_OK;
+}
+
 int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, const CUtensorMap* tm_x0_tok, int B, float* scores,
              cudaStream_t s) {
   c->gdbg_n = 0;  // CVR_GEMM_TIMELINE: stamps of this stage's GEMMs start at slot 0
@@ -1087,6 +1309,7 @@ int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, const CUtenso
   const float* hb = nullptr;  // (unused; keeps the two backbones' code paths parallel)
   (void)hb;
   if (c->backbone == CVR_ENSEMBLE) return do_dense_ensemble(c, x0, tm_x0, tm_x0_tok, B, scores, s);
+  if (c->backbone == CVR_MASKNET) return do_dense_masknet(c, tm_x0, B, scores, s);
   // ---- bf16 low-rank DCN-v2 on tcgen05
   const CUtensorMap* tm_xl = tm_x0;
   size_t pi = 0;
@@ -1314,7 +1537,8 @@ int cvr_score(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, in
   if ((e = cudaStreamWaitEvent(sd, c->ev_embed[slot], 0)) != cudaSuccess) return c->cuda_fail(e, "wait embed");
   if (batch > 0) {
     const bool ens = c->backbone == CVR_ENSEMBLE;
-    const CUtensorMap* tm = c->backbone == CVR_DCN_LOWRANK ? &c->tm_x0slot[slot] : ens ? &c->ens.flat_x0[slot] : nullptr;
+    const CUtensorMap* tm = (c->backbone == CVR_DCN_LOWRANK || c->backbone == CVR_MASKNET) ? &c->tm_x0slot[slot]
+                            : ens ? &c->ens.flat_x0[slot] : nullptr;
     const CUtensorMap* tmt = ens ? &c->ens.tok_x0[slot] : nullptr;
     const uint64_t kd[7] = {2, u64(x0), (uint64_t)batch, u64(d_scores), 0, 0, 0};
     st = run_stage(c, kd, sd, [&](cudaStream_t s) { return do_dense(c, x0, tm, tmt, batch, d_scores, s); });

@@ -78,7 +78,8 @@ enum Epi {
   EPI_CROSS_F32 = 5,     // fp32 x0 * (C + b) + x_l                      (ensemble DCN branch)
   EPI_BIAS_ADD_F32 = 6,  // fp32 C + b + in_f32                          (ensemble MHA out-proj)
   EPI_SUM_LN = 7,        // bf16 LN_row(C + b + in_f32) * gamma + beta   (ensemble FFN2 + LN, BN == N)
-  EPI_HEAD_PARTIAL = 8   // fp32 partial[m][tile] = ReLU(C + b) . m over the tile's columns
+  EPI_HEAD_PARTIAL = 8,  // fp32 partial[m][tile] = ReLU(C + b) . m over the tile's columns
+  EPI_MASK = 9           // bf16 (C + b) * x_l: MaskNet block, mask applied to x_l (tmXl), no residual
 };
 
 struct GemmArgs {

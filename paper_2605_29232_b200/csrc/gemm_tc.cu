@@ -7,6 +7,8 @@
 //   EPI_BIAS_RELU  C = ReLU(A B^T + b)               MLP tower
 //   EPI_HEAD       s = sigmoid(ReLU(A B^T + b) . m + c)   last MLP layer + head, h never stored
 //                                                    (BASELINE.json north star)
+//   EPI_MASK       C = (A B^T + b) * x_l             MaskNet block x_{l+1} = (U_l h + b_l) * x_l with
+//                                                    h = ReLU(V_l x0' + c_l) (A27)
 //
 // Design (persistent, warp-specialised, one CTA per SM):
 //   * A [M, K] and B [N, K] bf16, K-major, moved by TMA into 128-byte-swizzled shared memory
@@ -40,8 +42,9 @@ constexpr int kSmemBudget = 225 * 1024;
 template <int EPI>
 struct EpiTraits {
   static constexpr bool kSmemOut = EPI == EPI_STORE || EPI == EPI_BIAS_RELU || EPI == EPI_CROSS || EPI == EPI_BIAS ||
-                                   EPI == EPI_SUM_LN;
-  static constexpr bool kEin = EPI == EPI_CROSS || EPI == EPI_CROSS_F32;   // x0 / x_l tiles by TMA
+                                   EPI == EPI_SUM_LN || EPI == EPI_MASK;
+  static constexpr bool kEin = EPI == EPI_CROSS || EPI == EPI_CROSS_F32 || EPI == EPI_MASK;  // x0 / x_l tiles (TMA)
+  static constexpr int kEinTensors = EPI == EPI_MASK ? 1 : 2;                                  // MASK: x_l only
   static constexpr bool kBias = EPI != EPI_STORE;
 };
 
@@ -72,7 +75,7 @@ struct Cfg {
   static constexpr int PRODUCER_E = PRODUCER_B + 1;  // EIN producer (RING only)
   static constexpr int NT = 32 * (PRODUCER_B + (RING ? 2 : 1));
   static constexpr int OUT_BYTES = EpiTraits<EPI>::kSmemOut && !RING ? NSUB * SUB : 0;     // per buffer
-  static constexpr int EIN_BYTES = EpiTraits<EPI>::kEin && !RING ? 2 * NSUB * SUB : 0;     // x0 + x_l tiles, per acc
+  static constexpr int EIN_BYTES = EpiTraits<EPI>::kEin && !RING ? EpiTraits<EPI>::kEinTensors * NSUB * SUB : 0;  // per acc
   static constexpr int EPI_BYTES = OUT_BUFS * OUT_BYTES + 2 * EIN_BYTES + (RING ? RING_SLOTS * 2 * SUB : 0);
   static constexpr int BAR_BYTES = 512;
   // EPI_HEAD across a CN-cluster: per-tile partial dot products gathered in rank 0 ([2][CN][BM] fp32)
@@ -236,8 +239,12 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN>::NT, 1)
             uint8_t* base = sEin + a * C::EIN_BYTES;
 #pragma unroll
             for (int j = 0; j < C::NSUB; ++j) {
-              ptx::tma_load_2d(base + j * C::SUB, &tmX0, &efull[a], n0 + j * 64, m0);
-              ptx::tma_load_2d(base + (C::NSUB + j) * C::SUB, &tmXl, &efull[a], n0 + j * 64, m0);
+              if constexpr (EPI == EPI_MASK) {
+                ptx::tma_load_2d(base + j * C::SUB, &tmXl, &efull[a], n0 + j * 64, m0);
+              } else {
+                ptx::tma_load_2d(base + j * C::SUB, &tmX0, &efull[a], n0 + j * 64, m0);
+                ptx::tma_load_2d(base + (C::NSUB + j) * C::SUB, &tmXl, &efull[a], n0 + j * 64, m0);
+              }
             }
           }
         }
@@ -452,7 +459,12 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN>::NT, 1)
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
             }
-            if constexpr (T::kEin) {
+            if constexpr (EPI == EPI_MASK) {
+              float xlv[32];
+              lds32_bf16(ein_base + (c >> 6) * C::SUB, r, (c & 63) >> 3, xlv);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = v[j] * xlv[j];
+            } else if constexpr (T::kEin) {
               float x0v[32], xlv[32];
               lds32_bf16(ein_base + (c >> 6) * C::SUB, r, (c & 63) >> 3, x0v);
               lds32_bf16(ein_base + (C::NSUB + (c >> 6)) * C::SUB, r, (c & 63) >> 3, xlv);
@@ -572,6 +584,7 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
        g.epi == EPI_SUM_LN) && !g.tmOut)
     return cudaErrorInvalidValue;
   if ((g.epi == EPI_CROSS || g.epi == EPI_CROSS_F32) && (!g.tmX0 || !g.tmXl)) return cudaErrorInvalidValue;
+  if (g.epi == EPI_MASK && (!g.tmXl || !g.tmOut)) return cudaErrorInvalidValue;
   // A-multicast clusters of 4 along N (tmA with box {64, 32})
 #define CVR_MC(BN_, EPI_) \
   if (cn == 4 && g.BN == BN_ && g.epi == EPI_) return launch_t<BN_, EPI_, false, 1, 4>(g, s);
@@ -604,6 +617,8 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
   CVR_CASE(128, EPI_BIAS_ADD_F32)
   CVR_CASE(256, EPI_SUM_LN)
   CVR_CASE(256, EPI_HEAD_PARTIAL)
+  CVR_CASE(64, EPI_MASK)
+  CVR_CASE(128, EPI_MASK)
 #undef CVR_CASE
   return cudaErrorInvalidValue;
 }
