@@ -95,7 +95,7 @@ C4 = CvrConfig("c4", 1004, 8192, 64, (1_000_000,) * 64, 256, "bf16", "bf16", 0, 
 # blocks, no sequential blocks); mask hidden width r = 512 (unstated; the DCN configs' low-rank reading).
 C6 = C2.with_(name="c6", seed=1006, backbone="masknet", n_cross=1, cross_rank=512, cross_width=2048,
               n_parallel=2, mlp_dims=(1024, 512, 256))
-CONFIGS: Dict[str, CvrConfig] = {c.name: c for c in (C1, C2, C3, C3S, C4, C6)}
+CONFIGS: Dict[str, CvrConfig] = {c.name: c for c in (C1, C2, C3, C3S, C4, C6)}  # + C7 (front end) below
 
 
 # ---------------------------------------------------------------------------------
@@ -373,6 +373,79 @@ def make_batch(cfg: CvrConfig, k: int, batch: Optional[int] = None, tables: Opti
     rng = _rng(cfg, STREAM_DENSE, k)
     dense = np.log1p(np.abs(rng.normal(size=(B, cfg.n_dense))) * 10.0).astype(np.float32)
     return Batch(B, len(tl), indices.astype(np.int32), offsets.astype(np.int32), dense, Ls)
+
+
+# ---------------------------------------------------------------------------------
+# feature front end: raw categorical keys, text strings, item histories
+# ---------------------------------------------------------------------------------
+# config c7 = config 2's model on raw features: tables 0..19 categorical (multi-hot 64-bit keys, 1% MISSING,
+# sum), 20..22 text (character 3-grams of 1-4 word queries, 2% empty, mean), 23..25 item histories
+# (Poisson(30) keys, 10% long Poisson(120), truncated to the 50 most recent, mean); every table hashed with
+# vocab = rows - 1 (the last row is the `unseen' row).  Readings A28 (MISSING key), A29 (byte n-grams).
+C7 = C2.with_(name="c7", seed=1007)
+FRONTEND_C7 = {"kinds": ["cat"] * 20 + ["text"] * 3 + ["seq"] * 3, "ngram": 3, "max_len": 50, "missing": 0.01}
+STREAM_FRONTEND = 11
+KEY_MISSING_U64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+CONFIGS["c7"] = C7
+
+
+def _mix64(x: np.ndarray) -> np.ndarray:
+    """splitmix64 finaliser (a PRNG step of the generator, not the method's hash): ranks -> 64-bit ids."""
+    z = x.astype(np.uint64) + np.uint64(0x9E3779B97F4A7C15)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+@dataclass
+class FeatureBatch:
+    """Raw features of one batch: per table either ('keys', keys uint64 [n], offsets int32 [B+1]) for
+    categorical / sequential tables (histories oldest first), or ('text', [bytes] * B)."""
+    batch: int
+    tables: List[Tuple]
+    dense: np.ndarray
+
+
+def make_feature_batch(cfg: CvrConfig, k: int, batch: Optional[int] = None, spec=FRONTEND_C7) -> FeatureBatch:
+    B = cfg.batch if batch is None else batch
+    rng = _rng(cfg, STREAM_FRONTEND, k)
+    words = None
+    out = []
+    for t, kind in enumerate(spec["kinds"]):
+        if kind in ("cat", "seq"):
+            if kind == "cat":
+                L = rng.poisson(3.0, size=B) + 1
+            else:
+                long = rng.random(B) < 0.1
+                L = np.where(long, rng.poisson(120.0, size=B), rng.poisson(30.0, size=B))
+            n = int(L.sum())
+            ranks = sample_zipf_rows(rng, 10 * cfg.rows[t], cfg.zipf_a, n, scramble=False)
+            keys = _mix64(ranks.astype(np.uint64) * np.uint64(4096) + np.uint64(t))
+            if kind == "cat":
+                keys[rng.random(n) < spec["missing"]] = KEY_MISSING_U64
+            off = np.zeros(B + 1, np.int32)
+            off[1:] = np.cumsum(L)
+            out.append(("keys", keys, off))
+        else:
+            if words is None:
+                wl = rng.integers(3, 10, size=5000)
+                letters = rng.integers(97, 123, size=int(wl.sum()))
+                pos = np.concatenate([[0], np.cumsum(wl)])
+                words = [bytes(letters[pos[i]:pos[i + 1]].astype(np.uint8)) for i in range(5000)]
+            texts = []
+            for b in range(B):
+                if rng.random() < 0.02:
+                    texts.append(b"")
+                    continue
+                nw = int(rng.integers(1, 5))
+                ids = sample_zipf_rows(rng, 5000, 1.1, nw, scramble=False)
+                texts.append(b" ".join(words[i] for i in ids))
+            out.append(("text", texts))
+    rngd = _rng(cfg, STREAM_DENSE, 10_000 + k)
+    dense = np.log1p(np.abs(rngd.normal(size=(B, cfg.n_dense))) * 10.0).astype(np.float32)
+    return FeatureBatch(B, out, dense)
 
 
 # ---------------------------------------------------------------------------------

@@ -240,6 +240,33 @@ int cvr_gather_items(int n_tables, int n_dense, int64_t pool_size, const int32_t
                      int32_t* out_offsets, int32_t* out_indices, int64_t out_indices_cap, float* out_dense,
                      int64_t* out_nnz);
 
+/* -- feature front end -----------------------------------------------------
+ * Per model table t (n == T): vocab[t] > 0 puts the table in keys mode -- cvr_embed_keys hashes each raw
+ * 64-bit key on the device, row = FNV-1a 64 over the key's 8 big-endian bytes mod vocab[t] (
+ * PAPER.md:271 "hashing trick"), the MISSING key 0xFFFFFFFFFFFFFFFF maps to the `unseen' row vocab[t]
+ * (PAPER.md:287), so rows[t] >= vocab[t] + 1 is required (else CVR_E_SHAPE); vocab[t] = 0 keeps
+ * row ids.  pool_mode[t] = 1 mean-pools the bag (sum / length, fp32; "average pooling"), 0 sums;
+ * empty bags pool to 0 either way; mean also applies to cvr_embed / cvr_score.  Host call, synchronous. */
+int cvr_set_feature_spec(cvr_ctx* ctx, int n, const int64_t* vocab, const int* pool_mode);
+
+/* S2+S3 in keys mode: d_keys uint64 [nnz] raw keys in the table-major CSR of d_offsets (as cvr_embed's
+ * indices); every table must be in keys mode (CVR_E_STATE otherwise).  Otherwise as cvr_embed. */
+int cvr_embed_keys(cvr_ctx* ctx, const uint64_t* d_keys, const int32_t* d_offsets, int64_t nnz, int batch,
+                   const float* d_dense, void* d_x0, cvr_stream_t stream);
+
+/* Host batch assembly for text features ("tokenized into character n-grams"): the overlapping
+ * n-byte grams (1 <= n <= 8) of each of n_texts byte strings, each packed big-endian into a 64-bit key, into
+ * out_keys (capacity out_cap) with CSR out_offsets [n_texts + 1]; a string shorter than n gives an empty bag.
+ * CVR_E_NOMEM if out_cap is too small. */
+int cvr_text_ngram_keys(int n_texts, const char* const* texts, const int32_t* lens, int n, uint64_t* out_keys,
+                        int64_t out_cap, int32_t* out_offsets, int64_t* out_nnz);
+
+/* Host batch assembly for sequential features: keep the most recent max_len keys of each bag
+ * (bags list oldest first); out_keys needs room for min(len, max_len) per bag.  CVR_E_INDEX on decreasing
+ * offsets. */
+int cvr_truncate_bags(int n_bags, const int32_t* offsets, const uint64_t* keys, int max_len, int32_t* out_offsets,
+                      uint64_t* out_keys, int64_t* out_nnz);
+
 /* -- accounting / measurement -------------------------------------------------------------- */
 /* Number of kernels this ctx has launched since creation (every entry point counts its launches). */
 int cvr_launch_count(const cvr_ctx* ctx, int64_t* n);

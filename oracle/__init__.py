@@ -26,6 +26,11 @@ the readings A1..A26 used where the paper is silent, restated in DESIGN.md §3):
                 x_{l+1} = (U_l ReLU(V_l x0' + c_l) + b_l) * x_l      PAPER.md:226 (eq. "MaskNet uses"),
                 no residual; parallel branches concatenated / sequential
                 blocks chained; biases c_l, b_l per reading A27
+  O11 front end hashed keys -> rows: FNV-1a 64 over the key's 8 big-endian bytes mod vocab,
+                MISSING -> the `unseen' row vocab ("hashing trick", PAPER.md:287
+                "a unique `unseen' placeholder"); text -> character n-gram
+                keys, mean pooled; sequences truncated to the most recent max_len
+                keys, mean pooled; empty bag -> 0
 
 Parameters are the *stored* (fp32 / bf16 / fp16) values widened exactly to fp64 (A13).
 """
@@ -40,7 +45,8 @@ __all__ = [
     "validate_csr", "embedding_bag_sum", "normalize_dense", "concat_x0", "cross_full",
     "cross_lowrank", "mlp_relu", "head_logit", "sigmoid", "layer_norm_tokens", "mha_tokens",
     "ffn_tokens", "ensemble_layer", "masknet_project", "masknet_block", "masknet_forward", "score_forward",
-    "dense_forward", "to_f64",
+    "dense_forward", "to_f64", "fnv1a64", "hash_index", "KEY_MISSING", "ngram_keys", "truncate_recent",
+    "embedding_bag", "frontend_rows",
 ]
 
 
@@ -92,6 +98,59 @@ def embedding_bag_sum(tables: Sequence, indices: np.ndarray, offsets: np.ndarray
         bag_of = np.repeat(np.arange(batch), lens)
         np.add.at(p[t], bag_of, rows)
     return p.transpose(1, 0, 2)  # [B, T, d]
+
+
+def embedding_bag(tables: Sequence, indices: np.ndarray, offsets: np.ndarray, n_tables: int, batch: int, dim: int,
+                  modes: Sequence[str]) -> np.ndarray:
+    """O2 / O11: per-table pooling mode 'sum' (north star (a)) or 'mean' (PAPER.md:97 "average pooling";
+    SPEC.md:169-186): mean = sum / bag length; an empty bag pools to 0 in both modes."""
+    p = embedding_bag_sum(tables, indices, offsets, n_tables, batch, dim)
+    offsets = np.asarray(offsets, dtype=np.int64)
+    for t in range(n_tables):
+        if modes[t] == "mean":
+            L = np.diff(offsets[t * batch:(t + 1) * batch + 1]).astype(np.float64)
+            p[:, t, :] /= np.maximum(L, 1.0)[:, None]
+        elif modes[t] != "sum":
+            raise ValueError(modes[t])
+    return p
+
+
+# -- O11 feature front end ----------------------------------------------------------------
+KEY_MISSING = (1 << 64) - 1   # reading A28: the MISSING categorical value -> the unseen row
+_FNV_OFFSET, _FNV_PRIME, _M64 = 0xCBF29CE484222325, 0x100000001B3, (1 << 64) - 1
+
+
+def fnv1a64(data: bytes) -> int:
+    """FNV-1a, 64 bit: h = offset basis; for each byte: h ^= byte; h *= prime (mod 2^64)."""
+    h = _FNV_OFFSET
+    for byte in data:
+        h ^= byte
+        h = (h * _FNV_PRIME) & _M64
+    return h
+
+
+def hash_index(key: int, vocab: int) -> int:
+    """FNV-1a 64 over the key's 8 big-endian bytes, modulo vocab; KEY_MISSING -> vocab
+    (the appended `unseen' row)."""
+    if vocab < 1:
+        raise ValueError("vocab_size >= 1")
+    if int(key) == KEY_MISSING:
+        return vocab
+    return fnv1a64(int(key).to_bytes(8, "big")) % vocab
+
+
+def ngram_keys(text: bytes, n: int) -> List[int]:
+    """PAPER.md:97 "tokenized into character n-grams": the overlapping n-byte grams of ``text`` (reading A29:
+    bytes), each packed big-endian into a 64-bit key (n <= 8), in order; fewer than n bytes -> no grams."""
+    if not 1 <= n <= 8:
+        raise ValueError("1 <= n <= 8")
+    return [int.from_bytes(text[i:i + n], "big") for i in range(len(text) - n + 1)]
+
+
+def truncate_recent(keys: Sequence[int], max_len: int) -> List[int]:
+    """keep the most recent max_len keys of a history (oldest first, most recent last)."""
+    keys = list(keys)
+    return keys[len(keys) - max_len:] if len(keys) > max_len else keys
 
 
 # -- O3 / O4 ----------------------------------------------------------------------------
@@ -239,14 +298,39 @@ def dense_forward(cfg, P: Dict[str, np.ndarray], x0: np.ndarray) -> Dict[str, np
     return {"xL": xl, "h": h, "logit": z, "scores": sigmoid(z)}
 
 
-def score_forward(cfg, tables: Sequence, weights: Dict, batch, validate: bool = True) -> Dict[str, np.ndarray]:
+def frontend_rows(cfg, fb, spec):
+    """O11 on a raw FeatureBatch (cvr_synth.FeatureBatch): per table, text -> n-gram keys, histories ->
+    the most recent max_len keys, every key -> hash_index(key, rows - 1); returns (row ids int64 [nnz],
+    table-major offsets [T*B + 1], per-table pooling modes)."""
+    rows, lens, modes = [], [], []
+    for t, (kind, tab) in enumerate(zip(spec["kinds"], fb.tables)):
+        vocab = int(cfg.rows[t]) - 1
+        for b in range(fb.batch):
+            if tab[0] == "text":
+                keys = ngram_keys(tab[1][b], spec["ngram"])
+            else:
+                keys = [int(x) for x in tab[1][tab[2][b]:tab[2][b + 1]]]
+                if kind == "seq":
+                    keys = truncate_recent(keys, spec["max_len"])
+            rows.extend(hash_index(k, vocab) for k in keys)
+            lens.append(len(keys))
+        modes.append("sum" if kind == "cat" else "mean")
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    return np.array(rows, np.int64), off, modes
+
+
+def score_forward(cfg, tables: Sequence, weights: Dict, batch, validate: bool = True,
+                  modes: Sequence[str] = None) -> Dict[str, np.ndarray]:
     """S2-S7 of SURVEY.md §8(a) for one batch (``cvr_synth.Batch``): pool -> normalize ->
     concat -> backbone -> MLP -> sigmoid.  Returns scores, x0, xL (fp64)."""
     P = {k: to_f64(v) for k, v in weights.items()}
     B, T = batch.batch, cfg.n_tables
     if validate:
         validate_csr(batch.indices, batch.offsets, cfg.rows, T, B)
-    pooled = embedding_bag_sum(tables, batch.indices, batch.offsets, T, B, cfg.dim)
+    if modes is None:
+        pooled = embedding_bag_sum(tables, batch.indices, batch.offsets, T, B, cfg.dim)
+    else:
+        pooled = embedding_bag(tables, batch.indices, batch.offsets, T, B, cfg.dim, modes)
     if cfg.n_dense:
         z = normalize_dense(batch.dense, P["norm/mean"], P["norm/std"])
     else:

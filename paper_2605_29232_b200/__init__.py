@@ -8,8 +8,8 @@ There is no CPU fallback: if the extension is missing or no CUDA device is prese
 raise.
 """
 from ._cvr import (  # noqa: F401
-    CVR_BF16, CVR_DCN_FULL, CVR_DCN_LOWRANK, CVR_ENSEMBLE, CVR_F16, CVR_F32, CvrError, CvrModel, gemm_bf16, lib, lib_path,
-    status_string,
+    CVR_BF16, CVR_DCN_FULL, CVR_DCN_LOWRANK, CVR_ENSEMBLE, CVR_F16, CVR_F32, CVR_MASKNET, CvrError, CvrModel, gemm_bf16,
+    lib, lib_path, status_string, text_ngram_keys, truncate_bags,
 )
 
-__all__ = ["CvrModel", "CvrError", "lib", "lib_path", "status_string"]
+__all__ = ["CvrModel", "CvrError", "lib", "lib_path", "status_string", "text_ngram_keys", "truncate_bags"]

@@ -71,6 +71,11 @@ _SIGS = [
                                            _c_i64p]),
     ("cvr_gather_items", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, _vp, _vp, _vp, ctypes.c_int, _vp,
                                         _vp, _vp, ctypes.c_int64, _vp, _c_i64p]),
+    ("cvr_set_feature_spec", ctypes.c_int, [_vp, ctypes.c_int, _c_i64p, _c_ip]),
+    ("cvr_embed_keys", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp]),
+    ("cvr_text_ngram_keys", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_char_p), _c_ip, ctypes.c_int, _vp,
+                                           ctypes.c_int64, _vp, _c_i64p]),
+    ("cvr_truncate_bags", ctypes.c_int, [ctypes.c_int, _vp, _vp, ctypes.c_int, _vp, _vp, _c_i64p]),
     ("cvr_launch_count", ctypes.c_int, [_vp, _c_i64p]),
     ("cvr_profile_begin", ctypes.c_int, [_vp, ctypes.c_int]),
     ("cvr_profile_end", ctypes.c_int, [_vp, ctypes.POINTER(cvr_kernel_stat), ctypes.c_int, _c_ip]),
@@ -128,6 +133,37 @@ def gemm_bf16(A: torch.Tensor, B: torch.Tensor, C: Optional[torch.Tensor] = None
     if st != 0:
         raise CvrError(st, "cvr_gemm_bf16")
     return C
+
+
+def text_ngram_keys(texts, n: int):
+    """cvr_text_ngram_keys (host): byte strings -> (keys uint64 ndarray, offsets int32 ndarray)."""
+    import numpy as np
+    cap = sum(max(0, len(t) - n + 1) for t in texts)
+    arr = (ctypes.c_char_p * max(1, len(texts)))(*texts)
+    lens = (ctypes.c_int * max(1, len(texts)))(*[len(t) for t in texts])
+    keys = np.zeros(max(1, cap), np.uint64)
+    off = np.zeros(len(texts) + 1, np.int32)
+    nnz = ctypes.c_int64()
+    st = lib().cvr_text_ngram_keys(len(texts), arr, lens, n, keys.ctypes.data, cap, off.ctypes.data, ctypes.byref(nnz))
+    if st != 0:
+        raise CvrError(st, "cvr_text_ngram_keys")
+    return keys[:nnz.value], off
+
+
+def truncate_bags(keys, offsets, max_len: int):
+    """cvr_truncate_bags (host): keep the most recent max_len keys of each bag."""
+    import numpy as np
+    keys = np.ascontiguousarray(keys, np.uint64)
+    offsets = np.ascontiguousarray(offsets, np.int32)
+    n = len(offsets) - 1
+    out_k = np.zeros(max(1, len(keys)), np.uint64)
+    out_o = np.zeros(n + 1, np.int32)
+    nnz = ctypes.c_int64()
+    st = lib().cvr_truncate_bags(n, offsets.ctypes.data, keys.ctypes.data, max_len, out_o.ctypes.data,
+                                 out_k.ctypes.data, ctypes.byref(nnz))
+    if st != 0:
+        raise CvrError(st, "cvr_truncate_bags")
+    return out_k[:nnz.value], out_o
 
 
 class CvrModel:
@@ -219,6 +255,21 @@ class CvrModel:
         x0 = self.new_x0(batch) if x0 is None else x0
         self._check(self.L.cvr_embed(self.h, _ptr(indices), _ptr(offsets), indices.numel(), batch, _ptr(dense),
                                      _ptr(x0), _stream(stream)))
+        return x0
+
+    def set_feature_spec(self, vocab, pool_mode):
+        """cvr_set_feature_spec: per table hash vocab (0 = row ids) and pooling (0 sum, 1 mean)."""
+        T = self.cfg.n_tables
+        v = (ctypes.c_int64 * T)(*[int(x) for x in vocab])
+        pm = (ctypes.c_int * T)(*[int(x) for x in pool_mode])
+        self._check(self.L.cvr_set_feature_spec(self.h, T, v, pm))
+
+    def embed_keys(self, keys: torch.Tensor, offsets: torch.Tensor, batch: int, dense: Optional[torch.Tensor],
+                   x0: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """cvr_embed_keys: keys is an int64 tensor holding the raw 64-bit keys' bit patterns (MISSING = -1)."""
+        x0 = self.new_x0(batch) if x0 is None else x0
+        self._check(self.L.cvr_embed_keys(self.h, _ptr(keys), _ptr(offsets), keys.numel(), batch, _ptr(dense),
+                                          _ptr(x0), _stream(stream)))
         return x0
 
     def dense(self, x0: torch.Tensor, batch: int, scores: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:

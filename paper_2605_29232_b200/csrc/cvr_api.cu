@@ -78,6 +78,10 @@ struct cvr_ctx {
   std::vector<WSlot> wslots;
   bool tables_loaded = false, weights_loaded = false;
   std::vector<TableDesc> htables;
+  // feature front end (cvr_set_feature_spec): per model table, hash modulus (0 = row ids) and mean pooling
+  std::vector<int64_t> tvocab;
+  std::vector<int> tmean;
+  bool any_mean = false;
   // workspace regions (offsets)
   size_t off_tables = 0, off_flag = 0, off_x0[2] = {0, 0}, off_xa = 0, off_xb = 0, off_t = 0;
   std::vector<size_t> off_h;
@@ -438,6 +442,8 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
     if (t % c->world == c->rank) c->local_tables.push_back(t);
   c->T_pad = (c->T + c->world - 1) / c->world;
   c->htables.resize(c->local_tables.size());
+  c->tvocab.assign(c->T, 0);
+  c->tmean.assign(c->T, 0);
   build_weight_slots(c);
 
   // ---- workspace layout
@@ -736,7 +742,8 @@ int cvr_load_tables(cvr_ctx* c, int n, const int* ids, const void* const* d_rows
     if ((reinterpret_cast<uintptr_t>(d_rows[i]) & 15) || (strides[i] & 15) || strides[i] < row_bytes)
       return c->fail(CVR_E_ARG, "table %d: base and row stride must be 16-byte aligned, stride >= %lld", ids[i],
                      (long long)row_bytes);
-    c->htables[i] = TableDesc{reinterpret_cast<const uint8_t*>(d_rows[i]), strides[i], c->rows[ids[i]]};
+    c->htables[i] = TableDesc{reinterpret_cast<const uint8_t*>(d_rows[i]), strides[i], c->rows[ids[i]],
+                              c->tvocab[ids[i]], c->tmean[ids[i]]};
   }
   cudaError_t e = cudaMemcpy(c->ws + c->off_tables, c->htables.data(), sizeof(TableDesc) * n, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return c->cuda_fail(e, "cvr_load_tables");
@@ -1055,15 +1062,16 @@ EmbedArgs embed_args(cvr_ctx* c, const int32_t* idx, const int32_t* off, int64_t
   a.pad_col0 = c->W;
   a.pad_col1 = c->x0_ld;
   a.flag = c->at<int>(c->off_flag);
-  a.v2 = c->embed_variant == 1;
+  a.v2 = c->embed_variant == 1 && !c->any_mean;  // the warp-batched variant only sums
   a.variant = c->embed_variant;
   return a;
 }
 
 int do_embed(cvr_ctx* c, const int32_t* idx, const int32_t* off, int64_t nnz, int B, const float* dense, void* x0,
-             cudaStream_t s, int blocks_per_sm = 0) {
+             cudaStream_t s, int blocks_per_sm = 0, const uint64_t* keys = nullptr) {
   if (c->F && !c->slot("norm/mean")->loaded) return c->fail(CVR_E_STATE, "norm/mean,std not loaded");
   EmbedArgs a = embed_args(c, idx, off, nnz, B, dense, x0, c->x0_ld, x0, B);
+  a.keys = keys;
   a.blocks_per_sm = blocks_per_sm;
   c->pbeg(s);
   cudaError_t e = launch_embed(a, c->num_sms, s);
@@ -1475,6 +1483,52 @@ int cvr_embed(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, in
   const uint64_t ke[7] = {3, u64(d_indices), u64(d_offsets), (uint64_t)nnz, (uint64_t)batch, u64(d_dense), u64(d_x0)};
   return run_stage(c, ke, (cudaStream_t)stream,
                    [&](cudaStream_t s) { return do_embed(c, d_indices, d_offsets, nnz, batch, d_dense, d_x0, s); });
+}
+
+int cvr_set_feature_spec(cvr_ctx* c, int n, const int64_t* vocab, const int* pool_mode) {
+  if (!c || !vocab || !pool_mode) return CVR_E_ARG;
+  if (n != c->T) return c->fail(CVR_E_SHAPE, "feature spec: expected %d tables, got %d", c->T, n);
+  for (int t = 0; t < n; ++t) {
+    if (pool_mode[t] != 0 && pool_mode[t] != 1) return c->fail(CVR_E_ARG, "table %d: pool_mode must be 0 (sum) or 1 (mean)", t);
+    if (vocab[t] < 0 || (vocab[t] > 0 && vocab[t] + 1 > c->rows[t]))
+      return c->fail(CVR_E_SHAPE, "table %d: vocab %lld needs rows >= vocab + 1 (the unseen row), table has %lld", t,
+                     (long long)vocab[t], (long long)c->rows[t]);
+  }
+  c->any_mean = false;
+  for (int t = 0; t < n; ++t) {
+    c->tvocab[t] = vocab[t];
+    c->tmean[t] = pool_mode[t];
+    c->any_mean |= pool_mode[t] == 1;
+  }
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  c->graphs.clear();
+  if (c->tables_loaded) {
+    for (size_t i = 0; i < c->local_tables.size(); ++i) {
+      c->htables[i].vocab = c->tvocab[c->local_tables[i]];
+      c->htables[i].mean = c->tmean[c->local_tables[i]];
+    }
+    cudaError_t e = cudaMemcpy(c->ws + c->off_tables, c->htables.data(), sizeof(TableDesc) * c->htables.size(),
+                               cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return c->cuda_fail(e, "cvr_set_feature_spec");
+  }
+  return CVR_OK;
+}
+
+int cvr_embed_keys(cvr_ctx* c, const uint64_t* d_keys, const int32_t* d_offsets, int64_t nnz, int batch,
+                   const float* d_dense, void* d_x0, cvr_stream_t stream) {
+  if (!c) return CVR_E_ARG;
+  int st = check_ready(c, true, false);
+  if (st) return st;
+  if (c->world != 1) return c->fail(CVR_E_STATE, "cvr_embed_keys is unsharded");
+  for (int t = 0; t < c->T; ++t)
+    if (c->tvocab[t] <= 0) return c->fail(CVR_E_STATE, "table %d has no hash vocab (cvr_set_feature_spec)", t);
+  if (batch < 0 || batch > c->max_batch) return c->fail(CVR_E_ARG, "batch %d outside [0, %d]", batch, c->max_batch);
+  if (!d_offsets || !d_x0 || (nnz > 0 && !d_keys) || (c->F && batch && !d_dense) || nnz < 0)
+    return c->fail(CVR_E_ARG, "null pointer or negative nnz");
+  const uint64_t ke[7] = {5, u64(d_keys), u64(d_offsets), (uint64_t)nnz, (uint64_t)batch, u64(d_dense), u64(d_x0)};
+  return run_stage(c, ke, (cudaStream_t)stream, [&](cudaStream_t s) {
+    return do_embed(c, nullptr, d_offsets, nnz, batch, d_dense, d_x0, s, 0, d_keys);
+  });
 }
 
 int cvr_dense(cvr_ctx* c, const void* d_x0, int batch, float* d_scores, cvr_stream_t stream) {
@@ -1895,6 +1949,45 @@ int cvr_gather_items(int n_tables, int n_dense, int64_t pool_size, const int32_t
   for (int i = 0; i < (n_dense ? n : 0); ++i)
     memcpy(out_dense + (int64_t)i * n_dense, pool_dense + (int64_t)item_ids[i] * n_dense, (size_t)n_dense * 4);
   *out_nnz = tot[n_tables];
+  return CVR_OK;
+}
+
+int cvr_text_ngram_keys(int n_texts, const char* const* texts, const int32_t* lens, int n, uint64_t* out_keys,
+                        int64_t out_cap, int32_t* out_offsets, int64_t* out_nnz) {
+  if (n_texts < 0 || n < 1 || n > 8 || !out_offsets || !out_nnz || (n_texts > 0 && (!texts || !lens)))
+    return CVR_E_ARG;
+  int64_t pos = 0;
+  out_offsets[0] = 0;
+  for (int i = 0; i < n_texts; ++i) {
+    const int32_t L = lens[i];
+    if (L < 0 || (L > 0 && !texts[i])) return CVR_E_ARG;
+    const unsigned char* t = reinterpret_cast<const unsigned char*>(texts[i]);
+    for (int32_t k = 0; k + n <= L; ++k) {  // overlapping n-byte grams, packed big-endian (A29)
+      if (pos >= out_cap) return CVR_E_NOMEM;
+      uint64_t key = 0;
+      for (int b = 0; b < n; ++b) key = (key << 8) | t[k + b];
+      out_keys[pos++] = key;
+    }
+    if (pos > INT32_MAX) return CVR_E_NOMEM;
+    out_offsets[i + 1] = (int32_t)pos;
+  }
+  *out_nnz = pos;
+  return CVR_OK;
+}
+
+int cvr_truncate_bags(int n_bags, const int32_t* offsets, const uint64_t* keys, int max_len, int32_t* out_offsets,
+                      uint64_t* out_keys, int64_t* out_nnz) {
+  if (n_bags < 0 || max_len < 0 || !offsets || !out_offsets || !out_nnz) return CVR_E_ARG;
+  int64_t pos = 0;
+  out_offsets[0] = 0;
+  for (int i = 0; i < n_bags; ++i) {
+    const int32_t lo = offsets[i], hi = offsets[i + 1];
+    if (hi < lo) return CVR_E_INDEX;
+    const int32_t keep_lo = hi - lo > max_len ? hi - max_len : lo;  // the most recent max_len keys
+    for (int32_t q = keep_lo; q < hi; ++q) out_keys[pos++] = keys[q];
+    out_offsets[i + 1] = (int32_t)pos;
+  }
+  *out_nnz = pos;
   return CVR_OK;
 }
 

@@ -13,12 +13,15 @@ struct TableDesc {
   const uint8_t* base;  // row 0
   int64_t stride;       // bytes between rows
   int64_t rows;
+  int64_t vocab;        // keys mode: hash modulus (row vocab = the `unseen' row); 0 = indices are row ids
+  int mean;             // 1: mean pooling (sum / bag length, empty -> 0); 0: sum pooling
 };
 
 // ---- K1 + K2: embedding-bag sum-pool (+ dense normalisation) --------------------------------
 struct EmbedArgs {
   const TableDesc* tables;   // device array [T_local]
   const int32_t* indices;
+  const uint64_t* keys;      // keys mode (feature front end): raw 64-bit keys instead of indices
   const int32_t* offsets;    // [T_local * B + 1]
   int64_t nnz;
   int B;                     // bags per table (global batch in sharded mode)

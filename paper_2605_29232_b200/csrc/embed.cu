@@ -12,6 +12,12 @@
 //
 // S3 ("normal standardization"): x0[b, T*d + f] = (x[b,f] - mu_f) / sigma_f,
 // computed in fp32 with a correctly rounded division, by extra CTAs of the same grid.
+//
+// Feature front end, fused into the same gather: in keys mode each bag element is a
+// raw 64-bit key, hashed on the fly -- FNV-1a 64 over its 8 big-endian bytes, modulo the table's vocab,
+// the MISSING key (all ones) mapping to the `unseen' row vocab --
+// and tables flagged `mean' divide the fp32 sum by the bag length (PAPER.md:97 average pooling of text
+// n-grams; sequences); empty bags pool to 0 in both modes.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -96,7 +102,18 @@ __device__ void dense_part(const EmbedArgs& a, int blk, int nblk) {
   }
 }
 
-template <typename TIn, typename TOut, int LPR, int UNROLL, int MINB>
+__device__ __forceinline__ int64_t hashed_row(uint64_t key, int64_t vocab) {
+  if (key == ~0ull) return vocab;  // MISSING -> unseen row
+  uint64_t h = 0xCBF29CE484222325ull;
+#pragma unroll
+  for (int i = 7; i >= 0; --i) {  // big-endian byte order
+    h ^= (key >> (8 * i)) & 0xFFull;
+    h *= 0x100000001B3ull;
+  }
+  return (int64_t)(h % (uint64_t)vocab);
+}
+
+template <typename TIn, typename TOut, int LPR, int UNROLL, int MINB, bool KEYS>
 __global__ void __launch_bounds__(256, MINB) embed_bag_kernel(const EmbedArgs a, int n_embed_blocks) {
   if ((int)blockIdx.x >= n_embed_blocks) {
     dense_part<TOut>(a, blockIdx.x - n_embed_blocks, gridDim.x - n_embed_blocks);
@@ -119,18 +136,19 @@ __global__ void __launch_bounds__(256, MINB) embed_bag_kernel(const EmbedArgs a,
     if (!bad) {
       const uint8_t* colbase = td.base + sub * 16;
       for (int64_t j = start; j < end; j += UNROLL) {
-        int idx[UNROLL];
+        int64_t idx[UNROLL];
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) {
           const bool live = j + u < end;
-          idx[u] = live ? __ldg(a.indices + j + u) : 0;
-          bad |= live && (idx[u] < 0 || (int64_t)idx[u] >= td.rows);
+          if constexpr (KEYS) idx[u] = live ? hashed_row(__ldg(a.keys + j + u), td.vocab) : 0;
+          else idx[u] = live ? (int64_t)__ldg(a.indices + j + u) : 0;
+          bad |= live && (idx[u] < 0 || idx[u] >= td.rows);
         }
         if (bad) break;  // uniform within the group: every lane read the same indices
         uint4 v[UNROLL];
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u)
-          if (j + u < end) v[u] = ptx::ld_nc_v4(colbase + (int64_t)idx[u] * td.stride);
+          if (j + u < end) v[u] = ptx::ld_nc_v4(colbase + idx[u] * td.stride);
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u)
           if (j + u < end) InTraits<TIn>::add(acc, v[u]);
@@ -140,6 +158,10 @@ __global__ void __launch_bounds__(256, MINB) embed_bag_kernel(const EmbedArgs a,
 #pragma unroll
       for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
       if (sub == 0) atomicOr(a.flag, 1);
+    } else if (td.mean && end > start) {
+      const float L = (float)(end - start);
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) acc[e] = __fdiv_rn(acc[e], L);
     }
     TOut* dst = reinterpret_cast<TOut*>(a.out) + (int64_t)b * a.out_ld + (int64_t)t * a.out_tstride + sub * EPL;
     store_out<EPL>(dst, acc);
@@ -280,7 +302,7 @@ cudaError_t launch_t(const EmbedArgs& a, int num_sms, cudaStream_t s) {
     nbD = (total + threads - 1) / threads;
     if (nbD > num_sms) nbD = num_sms;
   }
-  if (a.v2) {
+  if (a.v2 && !a.keys) {
     const int64_t warps = (n_bags + V2Shape<LPR>::BPW - 1) / V2Shape<LPR>::BPW;
     nbE = (warps + 7) / 8;
     if (nbE > capE) nbE = capE;
@@ -289,10 +311,12 @@ cudaError_t launch_t(const EmbedArgs& a, int num_sms, cudaStream_t s) {
   // measured on B200, config 2 (scripts/embed_ab.py): one row load in flight per lane at full occupancy
   // (32 registers, 64 warps/SM) beats deeper per-lane unrolling at lower occupancy: 18.5 us (59% of the
   // HBM peak, algorithmic bytes) vs 24.6 us for 4 rows in flight at 32 warps/SM.
-  if (a.v2)
+  if (a.keys)
+    embed_bag_kernel<TIn, TOut, LPR, 1, 8, true><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
+  else if (a.v2)
     embed_bag_v2_kernel<TIn, TOut, LPR, 4><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
   else
-    embed_bag_kernel<TIn, TOut, LPR, 1, 8><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
+    embed_bag_kernel<TIn, TOut, LPR, 1, 8, false><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
   return cudaGetLastError();
 }
 

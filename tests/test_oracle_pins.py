@@ -305,3 +305,35 @@ def test_P8_masknet_batched_vs_brute():
     for b in (0, 17, 31):
         s = brute_score_one(cfg, tabs, P, bt.indices, bt.offsets, bt.dense[b], b, 32)
         assert abs(s - out["scores"][b]) <= 1e-12 * max(1.0, abs(s))
+
+
+# ---- feature front end: FNV-1a reference vectors, SPEC closed forms ------------
+def test_E7_fnv1a_reference_vectors_and_hash_index():
+    g = gold("E7_frontend.json")
+    for v in g["fnv1a64"]:
+        assert O.fnv1a64(v["bytes"].encode()) == int(v["hash"], 16)
+    # vocab 1 -> 0, determinism; key 0 by the closed form of 8 zero bytes
+    for key in (0, 1, 12345678901234567, (1 << 63) + 5):
+        assert O.hash_index(key, 1) == 0
+        assert O.hash_index(key, 1000) == O.hash_index(key, 1000)
+    closed = (0xCBF29CE484222325 * pow(0x100000001B3, 8, 1 << 64)) % (1 << 64)
+    assert O.hash_index(0, 97) == closed % 97
+    # the key's bytes are big-endian: key 0x61 hashes like the byte string 00..00 61
+    assert O.hash_index(0x61, 1 << 62) == O.fnv1a64(bytes(7) + b"a") % (1 << 62)
+    assert O.hash_index(O.KEY_MISSING, 777) == 777  # the unseen row
+
+
+def test_E7_ngrams_mean_pool_truncate():
+    g = gold("E7_frontend.json")
+    for c in g["ngrams"]:
+        assert O.ngram_keys(c["text"].encode(), c["n"]) == c["keys"]
+    mp = g["mean_pool"]
+    tab = np.array(mp["table"], float)
+    idx = np.concatenate([np.array(b, np.int64) for b in mp["bags"]])
+    off = np.concatenate([[0], np.cumsum([len(b) for b in mp["bags"]])])
+    p = O.embedding_bag([tab], idx, off, 1, len(mp["bags"]), 2, ["mean"])
+    np.testing.assert_allclose(p[:, 0, :], np.array(mp["out"]), rtol=0, atol=1e-15)
+    ps = O.embedding_bag([tab], idx, off, 1, len(mp["bags"]), 2, ["sum"])
+    np.testing.assert_array_equal(ps[:, 0, :], O.embedding_bag_sum([tab], idx, off, 1, len(mp["bags"]), 2)[:, 0, :])
+    assert O.truncate_recent(g["truncate"]["keys"], g["truncate"]["max_len"]) == g["truncate"]["out"]
+    assert O.truncate_recent([7], 3) == [7]
