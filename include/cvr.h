@@ -254,6 +254,11 @@ int cvr_set_feature_spec(cvr_ctx* ctx, int n, const int64_t* vocab, const int* p
 int cvr_embed_keys(cvr_ctx* ctx, const uint64_t* d_keys, const int32_t* d_offsets, int64_t nnz, int batch,
                    const float* d_dense, void* d_x0, cvr_stream_t stream);
 
+/* cvr_score in keys mode: the embedding stage hashes d_keys (as cvr_embed_keys); same executor, streams
+ * and ordering as cvr_score. */
+int cvr_score_keys(cvr_ctx* ctx, const uint64_t* d_keys, const int32_t* d_offsets, int64_t nnz, int batch,
+                   const float* d_dense, float* d_scores, cvr_stream_t s_embed, cvr_stream_t s_dense);
+
 /* Host batch assembly for text features ("tokenized into character n-grams"): the overlapping
  * n-byte grams (1 <= n <= 8) of each of n_texts byte strings, each packed big-endian into a 64-bit key, into
  * out_keys (capacity out_cap) with CSR out_offsets [n_texts + 1]; a string shorter than n gives an empty bag.

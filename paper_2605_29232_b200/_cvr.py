@@ -73,6 +73,7 @@ _SIGS = [
                                         _vp, _vp, ctypes.c_int64, _vp, _c_i64p]),
     ("cvr_set_feature_spec", ctypes.c_int, [_vp, ctypes.c_int, _c_i64p, _c_ip]),
     ("cvr_embed_keys", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp]),
+    ("cvr_score_keys", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp, _vp]),
     ("cvr_text_ngram_keys", ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_char_p), _c_ip, ctypes.c_int, _vp,
                                            ctypes.c_int64, _vp, _c_i64p]),
     ("cvr_truncate_bags", ctypes.c_int, [ctypes.c_int, _vp, _vp, ctypes.c_int, _vp, _vp, _c_i64p]),
@@ -271,6 +272,14 @@ class CvrModel:
         self._check(self.L.cvr_embed_keys(self.h, _ptr(keys), _ptr(offsets), keys.numel(), batch, _ptr(dense),
                                           _ptr(x0), _stream(stream)))
         return x0
+
+    def score_keys(self, keys: torch.Tensor, offsets: torch.Tensor, batch: int, dense: Optional[torch.Tensor],
+                   scores: Optional[torch.Tensor] = None, s_embed=None, s_dense=None) -> torch.Tensor:
+        scores = torch.empty(batch, dtype=torch.float32, device=self.device) if scores is None else scores
+        self._check(self.L.cvr_score_keys(self.h, _ptr(keys), _ptr(offsets), keys.numel(), batch, _ptr(dense),
+                                          _ptr(scores), _stream(s_embed),
+                                          _stream(s_dense if s_dense is not None else s_embed)))
+        return scores
 
     def dense(self, x0: torch.Tensor, batch: int, scores: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
         scores = torch.empty(batch, dtype=torch.float32, device=self.device) if scores is None else scores

@@ -742,8 +742,9 @@ int cvr_load_tables(cvr_ctx* c, int n, const int* ids, const void* const* d_rows
     if ((reinterpret_cast<uintptr_t>(d_rows[i]) & 15) || (strides[i] & 15) || strides[i] < row_bytes)
       return c->fail(CVR_E_ARG, "table %d: base and row stride must be 16-byte aligned, stride >= %lld", ids[i],
                      (long long)row_bytes);
-    c->htables[i] = TableDesc{reinterpret_cast<const uint8_t*>(d_rows[i]), strides[i], c->rows[ids[i]],
-                              c->tvocab[ids[i]], c->tmean[ids[i]]};
+    const int64_t v = c->tvocab[ids[i]];
+    c->htables[i] = TableDesc{reinterpret_cast<const uint8_t*>(d_rows[i]), strides[i], c->rows[ids[i]], v,
+                              v > 0 ? ~0ull / (uint64_t)v : 0ull, c->tmean[ids[i]]};
   }
   cudaError_t e = cudaMemcpy(c->ws + c->off_tables, c->htables.data(), sizeof(TableDesc) * n, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return c->cuda_fail(e, "cvr_load_tables");
@@ -1505,6 +1506,7 @@ int cvr_set_feature_spec(cvr_ctx* c, int n, const int64_t* vocab, const int* poo
   if (c->tables_loaded) {
     for (size_t i = 0; i < c->local_tables.size(); ++i) {
       c->htables[i].vocab = c->tvocab[c->local_tables[i]];
+      c->htables[i].magic = c->htables[i].vocab > 0 ? ~0ull / (uint64_t)c->htables[i].vocab : 0ull;
       c->htables[i].mean = c->tmean[c->local_tables[i]];
     }
     cudaError_t e = cudaMemcpy(c->ws + c->off_tables, c->htables.data(), sizeof(TableDesc) * c->htables.size(),
@@ -1567,14 +1569,18 @@ int cvr_dense(cvr_ctx* c, const void* d_x0, int batch, float* d_scores, cvr_stre
                    [&](cudaStream_t s) { return do_dense(c, d_x0, tm, tmt, batch, d_scores, s); });
 }
 
-int cvr_score(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, int64_t nnz, int batch,
-              const float* d_dense, float* d_scores, cvr_stream_t s_embed, cvr_stream_t s_dense) {
+}  // extern "C"
+
+namespace {
+// the two-stream executor behind cvr_score (row ids) and cvr_score_keys (raw keys, hashed in the gather)
+int score_impl(cvr_ctx* c, const int32_t* d_indices, const uint64_t* d_keys, const int32_t* d_offsets, int64_t nnz,
+               int batch, const float* d_dense, float* d_scores, cvr_stream_t s_embed, cvr_stream_t s_dense) {
   if (!c) return CVR_E_ARG;
   int st = check_ready(c, true, true);
   if (st) return st;
   if (c->world != 1) return c->fail(CVR_E_STATE, "cvr_score is unsharded");
   if (batch < 0 || batch > c->max_batch) return c->fail(CVR_E_ARG, "batch %d outside [0, %d]", batch, c->max_batch);
-  if (!d_offsets || !d_scores || (nnz > 0 && !d_indices) || (c->F && batch && !d_dense) || nnz < 0)
+  if (!d_offsets || !d_scores || (nnz > 0 && !d_indices && !d_keys) || (c->F && batch && !d_dense) || nnz < 0)
     return c->fail(CVR_E_ARG, "null pointer or negative nnz");
   cudaStream_t se = (cudaStream_t)s_embed, sd = (cudaStream_t)s_dense;
   const int slot = (int)(c->k & 1);
@@ -1582,9 +1588,10 @@ int cvr_score(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, in
   if (c->k >= 2) e = cudaStreamWaitEvent(se, c->ev_dense[slot], 0);  // dense(k-2) released the slot
   if (e != cudaSuccess) return c->cuda_fail(e, "wait dense(k-2)");
   void* x0 = c->ws + c->off_x0[slot];
-  const uint64_t ke[7] = {1, u64(d_indices), u64(d_offsets), (uint64_t)nnz, (uint64_t)batch, u64(d_dense), u64(x0)};
+  const uint64_t ke[7] = {d_keys ? 6u : 1u, u64(d_keys ? (const void*)d_keys : (const void*)d_indices), u64(d_offsets),
+                          (uint64_t)nnz, (uint64_t)batch, u64(d_dense), u64(x0)};
   st = run_stage(c, ke, se, [&](cudaStream_t s) {
-    return do_embed(c, d_indices, d_offsets, nnz, batch, d_dense, x0, s, c->embed_bps_pipe);
+    return do_embed(c, d_indices, d_offsets, nnz, batch, d_dense, x0, s, c->embed_bps_pipe, d_keys);
   });
   if (st) return st;
   if ((e = cudaEventRecord(c->ev_embed[slot], se)) != cudaSuccess) return c->cuda_fail(e, "record embed");
@@ -1601,6 +1608,23 @@ int cvr_score(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, in
   if ((e = cudaEventRecord(c->ev_dense[slot], sd)) != cudaSuccess) return c->cuda_fail(e, "record dense");
   c->k++;
   return CVR_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int cvr_score(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, int64_t nnz, int batch,
+              const float* d_dense, float* d_scores, cvr_stream_t s_embed, cvr_stream_t s_dense) {
+  return score_impl(c, d_indices, nullptr, d_offsets, nnz, batch, d_dense, d_scores, s_embed, s_dense);
+}
+
+int cvr_score_keys(cvr_ctx* c, const uint64_t* d_keys, const int32_t* d_offsets, int64_t nnz, int batch,
+                   const float* d_dense, float* d_scores, cvr_stream_t s_embed, cvr_stream_t s_dense) {
+  if (!c) return CVR_E_ARG;
+  for (int t = 0; t < c->T; ++t)
+    if (c->tvocab[t] <= 0) return c->fail(CVR_E_STATE, "table %d has no hash vocab (cvr_set_feature_spec)", t);
+  if (nnz > 0 && !d_keys) return c->fail(CVR_E_ARG, "null keys");
+  return score_impl(c, nullptr, d_keys, d_offsets, nnz, batch, d_dense, d_scores, s_embed, s_dense);
 }
 
 int cvr_score_host(cvr_ctx* c, const int32_t* h_indices, const int32_t* h_offsets, int64_t nnz, int batch,

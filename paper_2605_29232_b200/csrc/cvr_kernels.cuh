@@ -14,6 +14,7 @@ struct TableDesc {
   int64_t stride;       // bytes between rows
   int64_t rows;
   int64_t vocab;        // keys mode: hash modulus (row vocab = the `unseen' row); 0 = indices are row ids
+  uint64_t magic;       // floor((2^64 - 1) / vocab): h mod vocab = h - umulhi(h, magic) * vocab (+ <= 2 fixes)
   int mean;             // 1: mean pooling (sum / bag length, empty -> 0); 0: sum pooling
 };
 

@@ -102,7 +102,7 @@ __device__ void dense_part(const EmbedArgs& a, int blk, int nblk) {
   }
 }
 
-__device__ __forceinline__ int64_t hashed_row(uint64_t key, int64_t vocab) {
+__device__ __forceinline__ int64_t hashed_row(uint64_t key, int64_t vocab, uint64_t magic) {
   if (key == ~0ull) return vocab;  // MISSING -> unseen row
   uint64_t h = 0xCBF29CE484222325ull;
 #pragma unroll
@@ -110,7 +110,10 @@ __device__ __forceinline__ int64_t hashed_row(uint64_t key, int64_t vocab) {
     h ^= (key >> (8 * i)) & 0xFFull;
     h *= 0x100000001B3ull;
   }
-  return (int64_t)(h % (uint64_t)vocab);
+  // h mod vocab by a precomputed reciprocal: the quotient estimate is low by at most 2
+  uint64_t r = h - __umul64hi(h, magic) * (uint64_t)vocab;
+  while (r >= (uint64_t)vocab) r -= (uint64_t)vocab;
+  return (int64_t)r;
 }
 
 template <typename TIn, typename TOut, int LPR, int UNROLL, int MINB, bool KEYS>
@@ -135,13 +138,28 @@ __global__ void __launch_bounds__(256, MINB) embed_bag_kernel(const EmbedArgs a,
     bool bad = start < 0 || end < start || end > a.nnz;
     if (!bad) {
       const uint8_t* colbase = td.base + sub * 16;
+      if constexpr (KEYS) {
+        // each lane of the group hashes one key of the next LPR, then the row ids are broadcast in turn
+        const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1) << (threadIdx.x & 31 & ~(LPR - 1)));
+        for (int64_t j0 = start; j0 < end; j0 += LPR) {
+          const int64_t jj = j0 + sub;
+          const int64_t my = jj < end ? hashed_row(__ldg(a.keys + jj), td.vocab, td.magic) : 0;
+          bad |= jj < end && (my < 0 || my >= td.rows);
+          bad = __any_sync(gmask, bad);
+          if (bad) break;
+          const int cnt = (int)((end - j0) < LPR ? (end - j0) : LPR);
+          for (int u = 0; u < cnt; ++u) {
+            const int64_t row = __shfl_sync(gmask, my, u, LPR);
+            InTraits<TIn>::add(acc, ptx::ld_nc_v4(colbase + row * td.stride));
+          }
+        }
+      } else
       for (int64_t j = start; j < end; j += UNROLL) {
         int64_t idx[UNROLL];
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u) {
           const bool live = j + u < end;
-          if constexpr (KEYS) idx[u] = live ? hashed_row(__ldg(a.keys + j + u), td.vocab) : 0;
-          else idx[u] = live ? (int64_t)__ldg(a.indices + j + u) : 0;
+          idx[u] = live ? (int64_t)__ldg(a.indices + j + u) : 0;
           bad |= live && (idx[u] < 0 || idx[u] >= td.rows);
         }
         if (bad) break;  // uniform within the group: every lane read the same indices
