@@ -1,0 +1,88 @@
+#!/usr/bin/env python
+"""Table 6 saturation workload on B200.
+
+For each server-side coalescing window -- none (every request its own batch: Table 6's "0ms (w/o dynamic
+batching)" row), then 0.25 .. 4 ms, scaled to B200 service times as SURVEY.md §8(f) #3 proposes -- the highest
+offered load (queries/s; items/s = x 68.6 mean items per query) whose p99 latency stays under the bound,
+found by geometric bisection (serving.peak_qps_search), with its ratio to the no-batching row.  Config 5
+traffic (Poisson arrivals, lognormal items per query) from the config-2 item pool, served through
+serving.Server (host batch assembly + cvr_score_host).  Prints one JSON line per bound and a summary.
+
+    python bench_saturation.py [--bounds-ms 5 10] [--windows-ms 0.25 0.5 1 2 4] [--duration 0.6]
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import cvr_synth as cs  # noqa: E402
+from paper_2605_29232_b200 import CvrModel  # noqa: E402
+from paper_2605_29232_b200.serving import ItemPoolView, Request, Server, nearest_rank, saturation_table  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--bounds-ms", type=float, nargs="+", default=[5.0, 10.0])
+    ap.add_argument("--windows-ms", type=float, nargs="+", default=[0.25, 0.5, 1.0, 2.0, 4.0])
+    ap.add_argument("--duration", type=float, default=1.0)
+    ap.add_argument("--warmup", type=float, default=0.15)
+    ap.add_argument("--lo", type=float, default=500.0)
+    ap.add_argument("--hi", type=float, default=128000.0)
+    ap.add_argument("--rel-eps", type=float, default=0.07)
+    ap.add_argument("--max-items", type=int, default=8192)
+    ap.add_argument("--pool", type=int, default=1 << 16)
+    args = ap.parse_args()
+    cfg = cs.C2
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    pool = cs.make_item_pool(cfg, args.pool)
+    view = ItemPoolView(pool.offsets, pool.indices, pool.dense, cfg.n_tables)
+    item_nnz = np.diff(pool.offsets).reshape(cfg.n_tables, args.pool).sum(axis=0)
+    max_nnz = int(np.sort(item_nnz)[-args.max_items:].sum())
+    m = CvrModel(cfg, max_batch=args.max_items, max_nnz=max_nnz, device=dev)
+    m.load_tables([s.materialize(device=dev) for s in cs.table_specs(cfg)])
+    m.load_weights({k: v.to(dev) for k, v in cs.make_weights(cfg).items()})
+    log = []
+
+    def p99_for_window(window_s, bound_s):
+        window_ms = None if window_s is None else window_s * 1e3
+
+        def at(qps):
+            trace = cs.make_requests(qps, args.warmup + args.duration, args.pool)
+            reqs = [Request(i, t, len(ids), ids) for i, (t, ids) in enumerate(trace)]
+            srv = Server(m, view, max_items=args.max_items, window_s=0.0 if window_ms is None else window_ms / 1e3,
+                         max_nnz=max_nnz, max_requests=1 if window_ms is None else None)
+            lat, sizes, _ = srv.run(reqs, abort_after_s=4 * bound_s)
+            meas = np.array([r.t_arrival >= args.warmup for r in reqs])
+            p99 = float(nearest_rank(lat[meas], 99)) if meas.any() else float("inf")
+            log.append({"window_ms": window_ms, "qps": round(qps, 1), "p99_ms": p99 * 1e3,
+                        "mean_batch_items": float(sizes.mean()) if len(sizes) else 0.0})
+            return p99
+        return at
+
+    out = []
+    t0 = time.time()
+    for bound in args.bounds_ms:
+        rows = saturation_table(lambda w: p99_for_window(w, bound / 1e3), [None] + [w / 1e3 for w in args.windows_ms],
+                                bound / 1e3, args.lo, args.hi, args.rel_eps, confirm=2)
+        for r in rows:
+            r["peak_items_per_s"] = r["peak_qps"] * 68.6
+        res = {"p99_bound_ms": bound, "rows": rows}
+        out.append(res)
+        print(json.dumps(res), flush=True)
+    print(json.dumps({"metric": "peak offered load under a p99 bound vs coalescing window (Table 6 workload)",
+                      "unit": "queries/s (items/s = x 68.6)", "paper_shape": "Table 6: 3.3-4.4x over no batching at "
+                      "the best window, degrading for longer windows (PAPER.md:1666-1684)",
+                      "results": out, "search": {"lo": args.lo, "hi": args.hi, "rel_eps": args.rel_eps,
+                                                 "duration_s": args.duration, "warmup_s": args.warmup},
+                      "measurements": log, "wall_s": time.time() - t0}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -14,6 +14,9 @@
   them, assembles each batch on the host (libcvr ``cvr_gather_items`` into pinned staging, stage 0),
   scores it through ``cvr_score_host`` (H2D -> embed stream -> dense stream -> D2H, S1-S8) and stamps
   completion when the scores are on the host.  Latency = completion - scheduled arrival.
+* ``simulate_serving`` / ``peak_qps_search`` / ``saturation_table`` -- the Table 6 workload (PAPER.md:1666-1684;
+  SPEC.md:660-668): for each coalescing window, the highest offered load whose p99
+  latency stays under a bound (bisection), and its ratio to the no-batching row.
 
 Host logic only: every score is computed by libcvr's kernels.
 """
@@ -43,10 +46,14 @@ class Request:
 
 
 class DynamicBatcher:
-    def __init__(self, max_items: int = 8192, window_s: float = 0.002, queue_capacity: int = 1 << 16):
-        if max_items < 1 or window_s < 0 or queue_capacity < 1:
-            raise ValueError("max_items >= 1, window_s >= 0, queue_capacity >= 1")
+    def __init__(self, max_items: int = 8192, window_s: float = 0.002, queue_capacity: int = 1 << 16,
+                 max_requests: Optional[int] = None):
+        """``max_requests = 1`` with ``window_s = 0`` is Table 6's "0ms (w/o dynamic batching)" row: every
+        request is its own batch, dispatched as soon as the server can take it."""
+        if max_items < 1 or window_s < 0 or queue_capacity < 1 or (max_requests is not None and max_requests < 1):
+            raise ValueError("max_items >= 1, window_s >= 0, queue_capacity >= 1, max_requests >= 1")
         self.max_items, self.window_s, self.capacity = max_items, window_s, queue_capacity
+        self.max_requests = max_requests
         self.q: Deque[Request] = collections.deque()
         self.items = 0
         self.rejected = 0
@@ -73,7 +80,8 @@ class DynamicBatcher:
         if self.items < self.max_items and now < self.q[0].t_arrival + self.window_s:
             return None
         out, n = [], 0
-        while self.q and (not out or n + self.q[0].n_items <= self.max_items):
+        while self.q and (not out or n + self.q[0].n_items <= self.max_items) and \
+                (self.max_requests is None or len(out) < self.max_requests):
             r = self.q.popleft()
             n += r.n_items
             out.append(r)
@@ -103,6 +111,82 @@ def two_stage_schedule(a_costs: Sequence[float], b_costs: Sequence[float], slots
     return b_done
 
 
+def simulate_serving(arrivals: Sequence[float], n_items: Sequence[int], service, window_s: float,
+                     max_items: int = 8192, max_requests: Optional[int] = None) -> np.ndarray:
+    """Simulated-clock serving: DynamicBatcher in front of ONE server whose batch of n items
+    takes ``service(n)`` seconds; a batch is dispatched when the batcher releases it and the server is free.
+    Returns per-request latency (completion - arrival)."""
+    b = DynamicBatcher(max_items, window_s, queue_capacity=1 << 30, max_requests=max_requests)
+    lat = np.zeros(len(arrivals))
+    i, now, free_at, N = 0, 0.0, 0.0, len(arrivals)
+    done = 0
+    while done < N:
+        # next event: an arrival, the oldest request's window expiring, or the server freeing up
+        cands = []
+        if i < N:
+            cands.append(arrivals[i])
+        if len(b):
+            cands.append(max(b.next_deadline(), free_at) if b.items < max_items else free_at)
+        now = max(now, min(cands))
+        while i < N and arrivals[i] <= now:
+            b.submit(Request(i, arrivals[i], int(n_items[i])))
+            i += 1
+        if now >= free_at:
+            batch = b.poll(now)
+            if batch:
+                n = sum(r.n_items for r in batch)
+                free_at = now + service(n)
+                for r in batch:
+                    lat[r.rid] = free_at - r.t_arrival
+                done += len(batch)
+                continue
+        if i >= N and len(b) and now < free_at:
+            now = free_at
+    return lat
+
+
+def peak_qps_search(p99_at, bound_s: float, lo: float, hi: float, rel_eps: float = 0.05, max_iter: int = 30,
+                    confirm: int = 0):
+    """the highest offered load whose measured p99 <= bound, by bisection (geometric, until
+    hi/lo <= 1 + rel_eps).  ``p99_at(qps) -> seconds``.  Returns (peak, flag): peak 0.0 and flag 'bound
+    violated at minimal load' if even ``lo`` violates the bound; flag 'hi feasible' if the whole range is.
+    ``confirm``: re-measure the result up to that many times, stepping down by (1 + rel_eps) on a violation
+    (measured p99 is noisy, and with long windows it is not monotone in the load: a full batch dispatches
+    before its window expires)."""
+    lo0 = lo
+    if p99_at(lo) > bound_s:
+        return 0.0, "bound violated at minimal load"
+    if p99_at(hi) <= bound_s:
+        return hi, "hi feasible"
+    for _ in range(max_iter):
+        if hi / lo <= 1.0 + rel_eps:
+            break
+        mid = math.sqrt(lo * hi)
+        if p99_at(mid) <= bound_s:
+            lo = mid
+        else:
+            hi = mid
+    for _ in range(confirm):
+        if lo <= lo0 or p99_at(lo) <= bound_s:
+            break
+        lo = max(lo0, lo / (1.0 + rel_eps))
+    return lo, ""
+
+
+def saturation_table(p99_for_window, windows_s: Sequence[Optional[float]], bound_s: float, lo: float, hi: float,
+                     rel_eps: float = 0.05, confirm: int = 0):
+    """Table 6 layout (PAPER.md:1666-1684): one row per window (None = no dynamic batching, the first row);
+    ``p99_for_window(window) -> (qps -> p99 seconds)``; ratio = peak / the no-batching row's peak."""
+    rows = []
+    for w in windows_s:
+        peak, flag = peak_qps_search(p99_for_window(w), bound_s, lo, hi, rel_eps, confirm=confirm)
+        rows.append({"window_ms": None if w is None else w * 1e3, "peak_qps": peak, "flag": flag})
+    base = rows[0]["peak_qps"] if rows else 0.0
+    for r in rows:
+        r["ratio"] = r["peak_qps"] / base if base > 0 else None
+    return rows
+
+
 class ItemPoolView:
     """A host-resident item pool in the library's CSR layout (table-major offsets [T*P+1])."""
 
@@ -130,9 +214,9 @@ class Server:
     """Open-loop serving of a request trace through DynamicBatcher + cvr_score_host."""
 
     def __init__(self, model, pool: ItemPoolView, max_items: int = 8192, window_s: float = 0.002,
-                 host_slots: int = 3, max_nnz: Optional[int] = None):
+                 host_slots: int = 3, max_nnz: Optional[int] = None, max_requests: Optional[int] = None):
         self.m, self.pool = model, pool
-        self.batcher = DynamicBatcher(max_items, window_s)
+        self.batcher = DynamicBatcher(max_items, window_s, max_requests=max_requests)
         dev = model.device
         self.s_copy, self.s_embed = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         self.s_dense = torch.cuda.Stream(dev, priority=-1)
@@ -145,7 +229,9 @@ class Server:
                            ev=torch.cuda.Event(), busy=False)
                       for _ in range(host_slots)]
 
-    def run(self, reqs: List[Request], keep_scores: bool = False):
+    def run(self, reqs: List[Request], keep_scores: bool = False, abort_after_s: Optional[float] = None):
+        """Serve the trace.  ``abort_after_s``: stop early (remaining requests get latency +inf) once the oldest
+        queued request has waited that long -- an overloaded point of a saturation search."""
         lat = np.full(len(reqs), np.nan)
         sizes: List[int] = []
         scores = {} if keep_scores else None
@@ -157,6 +243,9 @@ class Server:
         clock = lambda: time.perf_counter() - t_start
         while done < len(reqs):
             now = clock()
+            if abort_after_s is not None and len(self.batcher) and now - self.batcher.q[0].t_arrival > abort_after_s:
+                lat[np.isnan(lat)] = np.inf
+                break
             while i < len(reqs) and reqs[i].t_arrival <= now:
                 if not self.batcher.submit(reqs[i]):
                     lat[reqs[i].rid] = np.inf

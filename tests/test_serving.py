@@ -141,3 +141,44 @@ def test_request_trace_shapes():
     reqs = cs.make_requests(2000.0, 0.5, 1024)
     assert abs(len(reqs) - 1000) < 5 * 32
     assert all(1 <= len(ids) <= 500 and ids.max() < 1024 for _, ids in reqs)
+
+
+# ---- Table 6 saturation workload on the simulated clock ------------
+def _sim_p99(service, window, max_requests=None, duration=2.0):
+    from paper_2605_29232_b200.serving import nearest_rank, simulate_serving
+
+    def at(qps):
+        t, n = cs.request_trace(qps, duration, seed=77)
+        lat = simulate_serving(t, n, service, 0.0 if window is None else window, max_requests=max_requests)
+        return nearest_rank(lat[t >= 0.25 * duration], 99)
+    return at
+
+
+def test_peak_search_bisection_on_step_function():
+    from paper_2605_29232_b200.serving import peak_qps_search
+    peak, flag = peak_qps_search(lambda q: 0.0 if q <= 1234.0 else 1.0, 0.5, 100.0, 1e5, rel_eps=0.01)
+    assert flag == "" and 1234.0 / 1.01 <= peak <= 1234.0
+    assert peak_qps_search(lambda q: 1.0, 0.5, 100.0, 1e5) == (0.0, "bound violated at minimal load")
+
+
+def test_saturation_no_fixed_cost_no_batching_gain():
+    """zero per-batch fixed cost -> batching does not amortise anything -> ratio ~ 1."""
+    from paper_2605_29232_b200.serving import saturation_table
+    svc = lambda n: 4e-6 * n
+    rows = saturation_table(lambda w: _sim_p99(svc, w, max_requests=1 if w is None else None), [None, 1e-3],
+                            bound_s=10e-3, lo=100.0, hi=20000.0, rel_eps=0.03)
+    assert rows[0]["window_ms"] is None and rows[0]["peak_qps"] > 0
+    assert 0.8 <= rows[1]["ratio"] <= 1.25, rows
+
+
+def test_saturation_fixed_cost_batching_raises_peak():
+    """SPEC.md:667: delay = F + c n with F >> c -> peak strictly increases with batching (Table 6's shape);
+    without batching the server cannot exceed 1 / (F + c E[n]) requests/s."""
+    from paper_2605_29232_b200.serving import saturation_table
+    F, c = 1e-3, 1e-6
+    svc = lambda n: F + c * n
+    rows = saturation_table(lambda w: _sim_p99(svc, w, max_requests=1 if w is None else None), [None, 2e-3],
+                            bound_s=20e-3, lo=50.0, hi=50000.0, rel_eps=0.03)
+    _, n = cs.request_trace(1000.0, 2.0, seed=77)
+    assert rows[0]["peak_qps"] <= 1.0 / (F + c * n.mean()) * 1.05
+    assert rows[1]["ratio"] > 2.0, rows
