@@ -11,6 +11,7 @@ serving.Server (host batch assembly + cvr_score_host).  Prints one JSON line per
     python bench_saturation.py [--bounds-ms 5 10] [--windows-ms 0.25 0.5 1 2 4] [--duration 0.6]
 """
 import argparse
+import gc
 import json
 import os
 import sys
@@ -33,7 +34,7 @@ def main():
     ap.add_argument("--windows-ms", type=float, nargs="+", default=[0.25, 0.5, 1.0, 2.0, 4.0])
     ap.add_argument("--duration", type=float, default=1.0)
     ap.add_argument("--warmup", type=float, default=0.15)
-    ap.add_argument("--lo", type=float, default=500.0)
+    ap.add_argument("--lo", type=float, default=1000.0)
     ap.add_argument("--hi", type=float, default=128000.0)
     ap.add_argument("--rel-eps", type=float, default=0.07)
     ap.add_argument("--max-items", type=int, default=8192)
@@ -54,11 +55,17 @@ def main():
         window_ms = None if window_s is None else window_s * 1e3
 
         def at(qps):
-            trace = cs.make_requests(qps, args.warmup + args.duration, args.pool)
+            # at least ~2000 measured requests per point: the p99 of a few hundred samples is host jitter
+            dur = max(args.duration, 2000.0 / qps)
+            trace = cs.make_requests(qps, args.warmup + dur, args.pool)
             reqs = [Request(i, t, len(ids), ids) for i, (t, ids) in enumerate(trace)]
             srv = Server(m, view, max_items=args.max_items, window_s=0.0 if window_ms is None else window_ms / 1e3,
                          max_nnz=max_nnz, max_requests=1 if window_ms is None else None)
-            lat, sizes, _ = srv.run(reqs, abort_after_s=4 * bound_s)
+            gc.disable()  # a collector pause inside the serving loop would land in the tail
+            try:
+                lat, sizes, _ = srv.run(reqs, abort_after_s=4 * bound_s)
+            finally:
+                gc.enable()
             meas = np.array([r.t_arrival >= args.warmup for r in reqs])
             p99 = float(nearest_rank(lat[meas], 99)) if meas.any() else float("inf")
             log.append({"window_ms": window_ms, "qps": round(qps, 1), "p99_ms": p99 * 1e3,

@@ -63,6 +63,12 @@ _SIGS = [
                                               ctypes.POINTER(ctypes.c_size_t)]),
     ("cvr_embed_shard", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp, _vp]),
     ("cvr_unpack_shard", ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp, _vp]),
+    ("cvr_set_peers", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp]),
+    ("cvr_embed_fused", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, ctypes.c_uint32, _vp]),
+    ("cvr_wait_peers", ctypes.c_int, [_vp, ctypes.c_uint32, _vp]),
+    ("cvr_ipc_get_handle", ctypes.c_int, [_vp, _vp]),
+    ("cvr_ipc_open_handle", ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
+    ("cvr_ipc_close_handle", ctypes.c_int, [_vp]),
     ("cvr_gemm_bf16", ctypes.c_int, [_vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp]),
     ("cvr_set_option", ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int64]),
@@ -134,6 +140,24 @@ def gemm_bf16(A: torch.Tensor, B: torch.Tensor, C: Optional[torch.Tensor] = None
     if st != 0:
         raise CvrError(st, "cvr_gemm_bf16")
     return C
+
+
+def ipc_get_handle(ptr: int) -> bytes:
+    """cvr_ipc_get_handle: the 64-byte CUDA IPC handle of a device allocation."""
+    buf = ctypes.create_string_buffer(64)
+    st = lib().cvr_ipc_get_handle(ptr, buf)
+    if st != 0:
+        raise CvrError(st, "cvr_ipc_get_handle")
+    return buf.raw
+
+
+def ipc_open_handle(handle: bytes) -> int:
+    """cvr_ipc_open_handle: map another process's allocation; returns the device pointer."""
+    p = _vp()
+    st = lib().cvr_ipc_open_handle(ctypes.create_string_buffer(handle, 64), ctypes.byref(p))
+    if st != 0:
+        raise CvrError(st, "cvr_ipc_open_handle")
+    return p.value
 
 
 def text_ngram_keys(texts, n: int):
@@ -319,6 +343,19 @@ class CvrModel:
 
     def unpack_shard(self, recv, batch_global, x0, stream=None):
         self._check(self.L.cvr_unpack_shard(self.h, _ptr(recv), batch_global, _ptr(x0), _stream(stream)))
+
+    def set_peers(self, peer_x0_ptrs, peer_flag_ptrs, local_flags_ptr: int):
+        n = len(peer_x0_ptrs)
+        px = (_vp * n)(*peer_x0_ptrs)
+        pf = (_vp * n)(*peer_flag_ptrs)
+        self._check(self.L.cvr_set_peers(self.h, n, px, pf, local_flags_ptr))
+
+    def embed_fused(self, indices, offsets, batch_global, dense, x0, epoch: int, stream=None):
+        self._check(self.L.cvr_embed_fused(self.h, _ptr(indices), _ptr(offsets), indices.numel(), batch_global,
+                                           _ptr(dense), _ptr(x0), epoch, _stream(stream)))
+
+    def wait_peers(self, epoch: int, stream=None):
+        self._check(self.L.cvr_wait_peers(self.h, epoch, _stream(stream)))
 
     def set_option(self, key: str, value: int):
         self._check(self.L.cvr_set_option(self.h, key.encode(), int(value)))

@@ -46,7 +46,15 @@ struct EmbedArgs {
   bool v2;                   // warp-batched variant (batched offsets / staged index runs)
   int variant;               // occupancy / unroll variant of the per-bag kernel (tuning)
   int blocks_per_sm;         // grid cap (grid-stride): leaves registers for co-resident GEMM CTAs
+  // fused exchange (V3): pooled rows go straight into the owner rank's canonical x0
+  // through peer-mapped pointers: bag (t_local, b) -> peer_x0[b / Bl] row b % Bl, columns (t_local*world+rank)*d
+  void* const* peer_x0;      // device array [world] of destination x0 bases ([Bl, x0_ld] each); null = off
+  int world, rank, Bl;
 };
+// V3 handshake: after the fused gather, rank `rank` sets flags_of[dst][rank] = epoch on every destination
+// (release, system scope); the dense stage of rank dst first waits until its own flags[src] >= epoch for all src.
+cudaError_t launch_peer_signal(uint32_t* const* d_peer_flags, int world, int rank, uint32_t epoch, cudaStream_t s);
+cudaError_t launch_peer_wait(const uint32_t* d_flags, int world, uint32_t epoch, cudaStream_t s);
 cudaError_t launch_embed(const EmbedArgs& a, int num_sms, cudaStream_t s);
 
 // unpack received shard chunks [src][b_local][t_slot][d] into canonical x0 columns

@@ -181,7 +181,14 @@ __global__ void __launch_bounds__(256, MINB) embed_bag_kernel(const EmbedArgs a,
 #pragma unroll
       for (int e = 0; e < EPL; ++e) acc[e] = __fdiv_rn(acc[e], L);
     }
-    TOut* dst = reinterpret_cast<TOut*>(a.out) + (int64_t)b * a.out_ld + (int64_t)t * a.out_tstride + sub * EPL;
+    TOut* dst;
+    if (a.peer_x0) {  // V3: straight into the owner rank's canonical x0 (peer memory over NVLink)
+      const int owner = b / a.Bl, bl = b - owner * a.Bl;
+      dst = reinterpret_cast<TOut*>(a.peer_x0[owner]) + (int64_t)bl * a.x0_ld +
+            (int64_t)(t * a.world + a.rank) * a.d + sub * EPL;
+    } else {
+      dst = reinterpret_cast<TOut*>(a.out) + (int64_t)b * a.out_ld + (int64_t)t * a.out_tstride + sub * EPL;
+    }
     store_out<EPL>(dst, acc);
   }
 }
@@ -329,6 +336,7 @@ cudaError_t launch_t(const EmbedArgs& a, int num_sms, cudaStream_t s) {
   // measured on B200, config 2 (scripts/embed_ab.py): one row load in flight per lane at full occupancy
   // (32 registers, 64 warps/SM) beats deeper per-lane unrolling at lower occupancy: 18.5 us (59% of the
   // HBM peak, algorithmic bytes) vs 24.6 us for 4 rows in flight at 32 warps/SM.
+  if (a.peer_x0 && (a.keys || a.v2)) return cudaErrorInvalidValue;  // V3 uses the row-id per-bag kernel
   if (a.keys)
     embed_bag_kernel<TIn, TOut, LPR, 1, 8, true><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
   else if (a.v2)
@@ -368,7 +376,38 @@ __global__ void unpack_kernel(const uint4* __restrict__ recv, uint8_t* __restric
   }
 }
 
+__global__ void peer_signal_kernel(uint32_t* const* __restrict__ peer_flags, int world, int rank, uint32_t epoch) {
+  // the gather kernel before us on this stream has completed; make its peer stores visible system-wide
+  // before publishing the epoch
+  __threadfence_system();
+  for (int d = threadIdx.x; d < world; d += blockDim.x) {
+    uint32_t* f = peer_flags[d] + rank;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+  }
+}
+
+__global__ void peer_wait_kernel(const uint32_t* __restrict__ flags, int world, uint32_t epoch) {
+  for (int src = threadIdx.x; src < world; src += blockDim.x) {
+    uint32_t v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + src) : "memory");
+    } while ((int32_t)(v - epoch) < 0);
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
 }  // namespace
+
+cudaError_t launch_peer_signal(uint32_t* const* d_peer_flags, int world, int rank, uint32_t epoch, cudaStream_t s) {
+  peer_signal_kernel<<<1, 32, 0, s>>>(d_peer_flags, world, rank, epoch);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_wait(const uint32_t* d_flags, int world, uint32_t epoch, cudaStream_t s) {
+  peer_wait_kernel<<<1, 32, 0, s>>>(d_flags, world, epoch);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_embed(const EmbedArgs& a, int num_sms, cudaStream_t s) {
   if (a.emb_dtype == F32 && a.out_dtype == F32) return launch_lpr<float, float>(a, num_sms, s);

@@ -11,6 +11,9 @@ Tables are placed round-robin (table t on rank t mod N, A18).  Per batch of B_gl
      canonical x0 columns of the local slice (V1 of SURVEY.md §8(e));
   4. the dense stage runs data-parallel on the local slice of B_global / N examples.
 
+``FusedShardedScorer`` is V3: step 1 stores pooled rows straight into the owner's x0 over NVLink and steps 2-3
+become a per-batch flag handshake.
+
 Pooled values are bit-identical to the unsharded path for every N (the exchange is a copy, P11).
 """
 from __future__ import annotations
@@ -36,6 +39,84 @@ def exchange(send: torch.Tensor, recv: torch.Tensor, group=None) -> None:
         dist.all_to_all_single(recv, send, group=group)
     else:
         recv.copy_(send)
+
+
+def exchange_handles(blob: bytes, group=None) -> list:
+    """Every rank's 64-byte IPC handle blob, in rank order (the host side of V3's peer mapping; gloo in the
+    CPU tests, the NCCL group's store-backed object collective on GPUs)."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        out = [None] * dist.get_world_size(group)
+        dist.all_gather_object(out, blob, group=group)
+        return out
+    return [blob]
+
+
+class FusedShardedScorer:
+    """One rank of the V3 sharded path: the gather kernel stores pooled rows
+    straight into the owner rank's canonical x0 over NVLink (cvr_embed_fused), a per-batch epoch flag per
+    (src, dst) pair replaces the all-to-all, and the dense stage waits on the flags (cvr_wait_peers).  No send
+    / receive buffers, no unpack, no NCCL kernel on the data path.
+
+    ``peers=None``: map the other ranks' x0 and flag buffers through CUDA IPC (one process per GPU).
+    ``peers=(x0_list, flags_list)``: use the given device tensors (all ranks' buffers visible in this process,
+    e.g. emulated ranks on one GPU in the tests)."""
+
+    def __init__(self, cfg, world_size: int, rank: int, batch_global: int, max_nnz: int,
+                 device: Optional[torch.device] = None, group=None, x0: Optional[torch.Tensor] = None,
+                 flags: Optional[torch.Tensor] = None):
+        from ._cvr import CvrModel
+        if batch_global % world_size:
+            raise ValueError("batch_global must be a multiple of world_size (A18)")
+        self.cfg, self.N, self.rank, self.group = cfg, world_size, rank, group
+        self.B, self.Bl = batch_global, batch_global // world_size
+        self.model = CvrModel(cfg, max_batch=self.Bl, max_nnz=max_nnz, world_size=world_size, rank=rank,
+                              device=device)
+        self.device = self.model.device
+        self.x0 = self.model.new_x0(self.Bl).zero_() if x0 is None else x0
+        self.flags = torch.zeros(world_size, dtype=torch.int32, device=self.device) if flags is None else flags
+        self.tables = local_tables(cfg.n_tables, world_size, rank)
+        self.epoch = 0
+        self._opened = []
+
+    def connect(self, peers=None):
+        from ._cvr import ipc_get_handle, ipc_open_handle
+        if peers is None:
+            hx = exchange_handles(ipc_get_handle(self.x0.data_ptr()), self.group)
+            hf = exchange_handles(ipc_get_handle(self.flags.data_ptr()), self.group)
+            px, pf = [], []
+            for r in range(self.N):
+                if r == self.rank:
+                    px.append(self.x0.data_ptr())
+                    pf.append(self.flags.data_ptr())
+                else:
+                    px.append(ipc_open_handle(hx[r]))
+                    pf.append(ipc_open_handle(hf[r]))
+                    self._opened += [px[-1], pf[-1]]
+        else:
+            px = [t.data_ptr() for t in peers[0]]
+            pf = [t.data_ptr() for t in peers[1]]
+        self.model.set_peers(px, pf, self.flags.data_ptr())
+
+    def load_tables(self, tables: Sequence[torch.Tensor]):
+        self.model.load_tables(tables, self.tables)
+
+    def load_weights(self, weights):
+        self.model.load_weights(weights)
+
+    def embed(self, indices, offsets, dense_local, stream=None):
+        """Gather + push this rank's tables for the global batch; signals epoch + 1 to every rank."""
+        self.epoch += 1
+        self.model.embed_fused(indices, offsets, self.B, dense_local, self.x0, self.epoch, stream=stream)
+
+    def dense(self, scores: Optional[torch.Tensor] = None, stream=None, wait: bool = True) -> torch.Tensor:
+        scores = torch.empty(self.Bl, dtype=torch.float32, device=self.device) if scores is None else scores
+        if wait:
+            self.model.wait_peers(self.epoch, stream=stream)
+        return self.model.dense(self.x0, self.Bl, scores, stream=stream)
+
+    def score(self, indices, offsets, dense_local, scores=None, stream=None):
+        self.embed(indices, offsets, dense_local, stream)
+        return self.dense(scores, stream)
 
 
 class ShardedScorer:

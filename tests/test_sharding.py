@@ -85,3 +85,27 @@ def test_exchange_gloo_world2():
     for p in ps:
         p.join(timeout=60)
     assert res == {0: True, 1: True}
+
+
+def _handle_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2605_29232_b200.sharded import exchange_handles
+    blob = bytes([rank + 1]) * 64   # stands in for a CUDA IPC handle (64 bytes)
+    got = exchange_handles(blob)
+    q.put((rank, got == [bytes([r + 1]) * 64 for r in range(world)]))
+    dist.destroy_process_group()
+
+
+def test_v3_ipc_handle_exchange_gloo_world2():
+    """V3 host logic (SURVEY.md §8(f) #4): every rank receives every rank's IPC handle blob in rank order."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_handle_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}
