@@ -162,6 +162,7 @@ struct cvr_ctx {
   std::map<const CUtensorMap*, CUtensorMap> qmaps;
   int mc = 1;                  // option "mc": 0 off, 1 head only (default), 2 every grouped GEMM
   int u_bn = 192;              // option "u_bn": N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64)
+  int epw_mode = 2;            // option "epw": split epilogues 0 never, 1 always, 2 when a CTA has one tile
   // option "xv_splitk" [0]: t = x_l V^T as a K-split cluster GEMM (r == 256).  Measured on B200 at B = 4096:
   // its mainloop halves (3.5 vs 7 us) but the DSMEM exchange of the fp32 partials costs 2-6 us (element-wise
   // st.shared::cluster or cp.async.bulk shared::cluster alike): 92-100 us per dense stage vs 90 with tiles
@@ -1098,6 +1099,10 @@ GemmArgs gemm_args(cvr_ctx* c, const GemmPlan& g, const CUtensorMap* A, int M) {
   a.num_sms = c->num_sms;
   a.pdl = c->pdl;
   a.cta_pair = g.pair;
+  {  // several tiles per CTA: the epilogue overlaps the next mainloop, keep the CTA small (Cfg::EPW)
+    const int64_t tiles = (int64_t)((M + 127) / 128) * (g.N / g.BN);
+    a.epw1 = c->epw_mode == 0 || (c->epw_mode == 2 && tiles > c->num_sms);
+  }
   if (c->gdbg && c->gdbg_n < 32) a.dbg = c->gdbg + (size_t)(c->gdbg_n++) * 160 * 8;
   if (g.cn > 1 && c->q(A)) {  // A operands without a quarter map stay unicast
     a.cn = g.cn;
@@ -1170,6 +1175,8 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     a.num_sms = c->num_sms;
     a.pdl = c->pdl;
     a.cta_pair = c->pair_ens;
+    const int64_t tiles = (int64_t)((M + 127) / 128) * (N / BN);
+    a.epw1 = c->epw_mode == 0 || (c->epw_mode == 2 && tiles > c->num_sms);
     return a;
   };
   (void)gp;
@@ -1939,6 +1946,13 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);  // U tile width
+    return CVR_OK;
+  }
+  if (!strcmp(key, "epw")) {
+    if (value < 0 || value > 2) return c->fail(CVR_E_ARG, "epw must be 0, 1 or 2");
+    c->epw_mode = (int)value;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
     return CVR_OK;
   }
   if (!strcmp(key, "xv_splitk")) {

@@ -119,6 +119,7 @@ struct GemmArgs {
   bool pdl;                  // launch with programmatic stream serialization
   bool a_resident;           // K <= 256: keep the A block resident, contiguous tile runs per CTA
   bool cta_pair;             // 2-CTA (cta_group::2) tiles of 256 rows; B box = BN/2 rows
+  bool epw1;                 // one epilogue warp per TMEM quadrant (several tiles per CTA; see Cfg::EPW)
   int cn;                    // 4: clusters of 4 CTAs along N multicast A (tmA box = {64, 32}); 0/1: off
   unsigned long long* dbg;   // optional per-CTA timeline [grid][8] (%globaltimer ns): entry, deps ready,
                              // first stage landed, last MMA issued, first accumulator, epilogue done, exit

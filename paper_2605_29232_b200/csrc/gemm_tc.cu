@@ -55,7 +55,7 @@ struct EpiTraits {
 template <int BN, int EPI, int CG>
 constexpr bool ein_ring() { return EPI == EPI_CROSS && BN == 192 && CG == 1; }
 
-template <int BN, int EPI, bool AR = false, int CG = 1, int CN = 1>
+template <int BN, int EPI, bool AR = false, int CG = 1, int CN = 1, int EW = 4>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;       // 16 KB
   static constexpr int B_BYTES = (BN / CG) * BK * 2;  // CG = 2: each CTA of the pair holds half of B
@@ -69,7 +69,9 @@ struct Cfg {
   // epilogue warps per TMEM lane quadrant: the epilogue of a CTA's last tile is exposed (one tile per CTA at
   // B = 4096), so plain stores split the tile's 64-column sub-tiles over up to 4 warps per quadrant
   static constexpr bool SPLIT = (EPI == EPI_STORE || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS) && CG == 1 && CN == 1;
-  static constexpr int EPW = RING ? 3 : (SPLIT ? (BN / 64 < 4 ? BN / 64 : 4) : 1);
+  // EW caps the split: EW = 1 when each CTA runs several tiles (the epilogue then overlaps the next tile's
+  // mainloop anyway) keeps the CTA at 7 warps, leaving registers for co-resident embedding CTAs
+  static constexpr int EPW = RING ? 3 : (SPLIT ? (BN / 64 < EW ? BN / 64 : EW) : 1);
   static constexpr int COLS_W = BN / EPW;           // columns per epilogue warp
   static constexpr int PRODUCER_B = 2 + 4 * EPW;
   static constexpr int PRODUCER_E = PRODUCER_B + 1;  // EIN producer (RING only)
@@ -111,12 +113,12 @@ __device__ __forceinline__ void stamp(unsigned long long* dbg, int i) {
   }
 }
 
-template <int BN, int EPI, bool AR, int CG, int CN>
-__global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN>::NT, 1)
+template <int BN, int EPI, bool AR, int CG, int CN, int EW>
+__global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW>::NT, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmX0,
                      const __grid_constant__ CUtensorMap tmXl, const GemmArgs g) {
-  using C = Cfg<BN, EPI, AR, CG, CN>;
+  using C = Cfg<BN, EPI, AR, CG, CN, EW>;
   using T = EpiTraits<EPI>;
   static_assert(CG == 1 || !AR, "the resident-A walk is single-CTA");
   static_assert(CN == 1 || (CG == 1 && !AR), "A multicast is cta_group::1 streaming only");
@@ -538,10 +540,10 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN>::NT, 1)
   }
 }
 
-template <int BN, int EPI, bool AR = false, int CG = 1, int CN = 1>
+template <int BN, int EPI, bool AR = false, int CG = 1, int CN = 1, int EW = 4>
 cudaError_t launch_t(const GemmArgs& g, cudaStream_t s) {
-  using C = Cfg<BN, EPI, AR, CG, CN>;
-  auto kern = gemm_bf16_kernel<BN, EPI, AR, CG, CN>;
+  using C = Cfg<BN, EPI, AR, CG, CN, EW>;
+  auto kern = gemm_bf16_kernel<BN, EPI, AR, CG, CN, EW>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -594,6 +596,19 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
   CVR_MC(64, EPI_HEAD)
 #undef CVR_MC
   if (cn > 1) return cudaErrorInvalidValue;
+  // one epilogue warp per quadrant when every CTA runs several tiles (see Cfg::EPW)
+  if (g.epw1 && !g.cta_pair && (g.epi == EPI_STORE || g.epi == EPI_BIAS_RELU || g.epi == EPI_BIAS)) {
+#define CVR_E1(BN_, EPI_) \
+    if (g.BN == BN_ && g.epi == EPI_) return launch_t<BN_, EPI_, false, 1, 1, 1>(g, s);
+    CVR_E1(128, EPI_STORE)
+    CVR_E1(192, EPI_STORE)
+    CVR_E1(256, EPI_STORE)
+    CVR_E1(128, EPI_BIAS_RELU)
+    CVR_E1(256, EPI_BIAS_RELU)
+    CVR_E1(128, EPI_BIAS)
+    CVR_E1(256, EPI_BIAS)
+#undef CVR_E1
+  }
 #define CVR_CASE(BN_, EPI_) \
   if (g.BN == BN_ && g.epi == EPI_) return g.cta_pair ? launch_t<BN_, EPI_, false, 2>(g, s) : launch_t<BN_, EPI_>(g, s);
   CVR_CASE(64, EPI_STORE)

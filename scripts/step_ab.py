@@ -1,10 +1,11 @@
-"""A/B the pipelined cvr_score step (config 2) under executor options, interleaved."""
+"""A/B the pipelined cvr_score step under executor / kernel options, interleaved (CFG=c2|c3s|c4|c6)."""
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, cvr_synth as cs
 from paper_2605_29232_b200 import CvrModel
-cfg = cs.C2; B = cfg.batch
-ring = [cs.make_batch(cfg, 900 + i) for i in range(8)]
+cfg = cs.CONFIGS[os.environ.get("CFG", "c2")]; B = cfg.batch
+NR = int(os.environ.get("RING", "8"))
+ring = [cs.make_batch(cfg, 900 + i) for i in range(NR)]
 m = CvrModel(cfg, max_batch=B, max_nnz=max(b.nnz for b in ring))
 tabs = [s.materialize(device="cuda") for s in cs.table_specs(cfg)]
 m.load_tables(tabs); m.load_weights({k: v.cuda() for k, v in cs.make_weights(cfg).items()})
@@ -13,16 +14,18 @@ outs = [torch.empty(B, device="cuda") for _ in ring]
 se, sd = torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1)
 raw = [(i.data_ptr(), o.data_ptr(), i.numel(), d.data_ptr(), out.data_ptr()) for (i, o, d), out in zip(dev, outs)]
 settings = json.loads(sys.argv[1])
-K = 500
+K = int(os.environ.get("K", "500"))
+DEF = {"u_bn": 192, "epw": 2, "mc": 1, "pdl": 1, "graphs": 1, "xv_splitk": 0, "embed_bps": 0}
 for rep in range(3):
     for st in settings:
         for k, v in st.items(): m.set_option(k, v)
         for i in range(20):
-            ip, op, nnz, dp, sp = raw[i % 8]; m.score_raw(ip, op, nnz, B, dp, sp, se.cuda_stream, sd.cuda_stream)
+            ip, op, nnz, dp, sp = raw[i % NR]; m.score_raw(ip, op, nnz, B, dp, sp, se.cuda_stream, sd.cuda_stream)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(se); sd.wait_event(a)
         for i in range(K):
-            ip, op, nnz, dp, sp = raw[i % 8]; m.score_raw(ip, op, nnz, B, dp, sp, se.cuda_stream, sd.cuda_stream)
+            ip, op, nnz, dp, sp = raw[i % NR]; m.score_raw(ip, op, nnz, B, dp, sp, se.cuda_stream, sd.cuda_stream)
         b.record(sd); torch.cuda.synchronize()
-        print(json.dumps({"rep": rep, "setting": st, "us_per_step": round(a.elapsed_time(b) / K * 1e3, 2)}))
+        print(json.dumps({"cfg": cfg.name, "rep": rep, "setting": st, "us_per_step": round(a.elapsed_time(b) / K * 1e3, 2)}), flush=True)
+        for k in st: m.set_option(k, DEF.get(k, 1))
