@@ -109,7 +109,8 @@ struct cvr_ctx {
     size_t off_S = 0, off_qkv = 0, off_cat = 0;
     std::vector<size_t> off_catW, off_catb;
     CUtensorMap flat_x0[2], tok_x0[2], flat_xa, flat_xb, tok_xa, tok_xb, sttok_xa, sttok_xb;
-    CUtensorMap st_qkv, st_hf, tm_cat;
+    CUtensorMap st_qkv, st_hf, tm_cat, tm_O;           // tm_O: cat[:, :D] (fused FFN kernel's A of Wo)
+    std::vector<CUtensorMap> W1f, Wcf;                 // fused FFN: W1 box {64,128}, [Wo | W2] box {64,256}
     std::vector<CUtensorMap> V, U, Wqkv, W1, Wcat;
     CUtensorMap flat_user, tok_user;
   } ens;
@@ -163,6 +164,11 @@ struct cvr_ctx {
   int mc = 1;                  // option "mc": 0 off, 1 head only (default), 2 every grouped GEMM
   int u_bn = 192;              // option "u_bn": N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64)
   int epw_mode = 2;            // option "epw": split epilogues 0 never, 1 always, 2 when a CTA has one tile
+  // option "ens_fused_ffn" [0]: config 4's FFN + out-projection + LN as one kernel (ens_ffn.cu), bit-identical to
+  // the two GEMMs.  Measured on B200 (B = 8192): 972 us per layer vs 363 + 536 us -- each 128-token tile streams
+  // all 1.15 MB of W1 / W2 / Wo through a 3-deep ring (shared memory is full), so weight streaming, not the
+  // h round trip it removes, bounds it; kept as an option
+  bool ens_fused_ffn = false;
   // option "xv_splitk" [0]: t = x_l V^T as a K-split cluster GEMM (r == 256).  Measured on B200 at B = 4096:
   // its mainloop halves (3.5 vs 7 us) but the DSMEM exchange of the fp32 partials costs 2-6 us (element-wise
   // st.shared::cluster or cp.async.bulk shared::cluster alike): 92-100 us per dense stage vs 90 with tiles
@@ -724,6 +730,7 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     const int64_t CW = D + c->ffn;
     ok &= encode_tmap_bf16(&E.st_hf, c->ws + E.off_cat + D * 2, BT, c->ffn, CW, 32, &er) == 0;
     ok &= encode_tmap_bf16(&E.tm_cat, c->ws + E.off_cat, BT, CW, CW, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&E.tm_O, c->ws + E.off_cat, BT, D, CW, 128, &er) == 0;
     c->tm_h.resize(c->off_h.size());
     c->st_h.resize(c->off_h.size());
     for (size_t i = 0; i < c->off_h.size(); ++i) {
@@ -818,6 +825,8 @@ int encode_plan_ensemble(cvr_ctx* c) {
   E.Wqkv.assign(c->n_cross, {});
   E.W1.assign(c->n_cross, {});
   E.Wcat.assign(c->n_cross, {});
+  E.W1f.assign(c->n_cross, {});
+  E.Wcf.assign(c->n_cross, {});
   bool ok = true;
   for (int l = 0; l < c->n_cross; ++l) {
     const std::string p = "ens/" + std::to_string(l) + "/";
@@ -838,6 +847,8 @@ int encode_plan_ensemble(cvr_ctx* c) {
     cudaError_t e5 = cudaMemcpy(c->ws + E.off_catb[l], bo.data(), D * 4, cudaMemcpyHostToDevice);
     if (e1 || e2 || e3 || e4 || e5) return c->fail(CVR_E_CUDA, "assembling [Wo | W2]");
     ok &= encode_tmap_bf16(&E.Wcat[l], c->ws + E.off_catW[l], D, D + F, D + F, 256 / dv, &er) == 0;
+    ok &= encode_tmap_bf16(&E.W1f[l], c->wptr(p + "ffn/W1"), F, D, D, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&E.Wcf[l], c->ws + E.off_catW[l], D, D + F, D + F, 256, &er) == 0;
   }
   if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
   // head MLP: same plan as the low-rank path (GemmPlan per mlp layer)
@@ -1204,6 +1215,32 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     e = launch_mha64(c->at<__nv_bfloat16>(E.off_qkv), cat, D + c->ffn, B, c->n_heads, s);  // O -> cat[:, :D]
     c->pend(K_MHA, s);
     if (e != cudaSuccess) return c->cuda_fail(e, "mha64");
+    if (c->ens_fused_ffn && D == 256 && c->ffn == 1024) {
+      // FFN + out-projection + branch-sum LN in one kernel: the FFN hidden never leaves the SM (ens_ffn.cu)
+      EnsFfnArgs f{};
+      f.tmX = tok_xl;
+      f.tmO = &E.tm_O;
+      f.tmW1 = &E.W1f[l];
+      f.tmWc = &E.Wcf[l];
+      f.tmY = even ? &E.sttok_xa : &E.sttok_xb;
+      f.b1 = c->wptr<float>(p + "ffn/b1");
+      f.bcat = c->at<float>(E.off_catb[l]);
+      f.S = S;
+      f.gamma = c->wptr<float>(p + "ln/gamma");
+      f.beta = c->wptr<float>(p + "ln/beta");
+      f.M = BT;
+      f.D = D;
+      f.F = c->ffn;
+      f.num_sms = c->num_sms;
+      f.pdl = c->pdl;
+      c->pbeg(s);
+      e = launch_ens_ffn_ln(f, s);
+      c->pend(K_ENS_FFN2_LN, s);
+      if (e != cudaSuccess) return c->cuda_fail(e, "ens fused ffn + ln");
+      flat_xl = even ? &E.flat_xa : &E.flat_xb;
+      tok_xl = even ? &E.tok_xa : &E.tok_xb;
+      continue;
+    }
     // FFN hidden -> cat[:, D:]
     GemmArgs a5 = ga(tok_xl, &E.W1[l], BT, c->ffn, D, 256, EPI_BIAS_RELU);
     a5.tmOut = &E.st_hf;
@@ -1946,6 +1983,12 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);  // U tile width
+    return CVR_OK;
+  }
+  if (!strcmp(key, "ens_fused_ffn")) {
+    c->ens_fused_ffn = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
     return CVR_OK;
   }
   if (!strcmp(key, "epw")) {

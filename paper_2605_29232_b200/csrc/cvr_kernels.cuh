@@ -134,6 +134,19 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s);
 // ld_x (row stride of t), M, K, pdl.
 cudaError_t launch_gemm_splitk(const GemmArgs& g, cudaStream_t s);
 
+// ---- config 4: fused FFN + out-projection + branch-sum LayerNorm (ens_ffn.cu) ------------------------------
+struct EnsFfnArgs {
+  const CUtensorMap* tmX;    // x_l tokens [BT, D] box {64, 128}
+  const CUtensorMap* tmO;    // MHA output O = cat[:, :D] (row stride D + F) box {64, 128}
+  const CUtensorMap* tmW1;   // W1 [F, D] box {64, 128}
+  const CUtensorMap* tmWc;   // [Wo | W2] [D, D + F] box {64, 256}
+  const CUtensorMap* tmY;    // out tokens [BT, D] box {64, 32}
+  const float *b1, *bcat, *S, *gamma, *beta;  // b1 [F], bo + b2 [D], DCN branch S fp32 [BT, D], LN affine [D]
+  int M, D, F, num_sms;
+  bool pdl;
+};
+cudaError_t launch_ens_ffn_ln(const EnsFfnArgs& a, cudaStream_t s);
+
 // ---- K7: multi-head self-attention over the 64 tokens of each example (config 4) ------------------
 // qkv [B*S, 3*D] bf16 (Q | K | V, head h at columns h*64 of each), out [B*S, D] bf16; S = 64, dh = 64.
 cudaError_t launch_mha64(const __nv_bfloat16* qkv, __nv_bfloat16* out, int out_ld, int B, int n_heads, cudaStream_t s);

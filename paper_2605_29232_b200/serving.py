@@ -214,8 +214,13 @@ class Server:
     """Open-loop serving of a request trace through DynamicBatcher + cvr_score_host."""
 
     def __init__(self, model, pool: ItemPoolView, max_items: int = 8192, window_s: float = 0.002,
-                 host_slots: int = 3, max_nnz: Optional[int] = None, max_requests: Optional[int] = None):
+                 host_slots: int = 3, max_nnz: Optional[int] = None, max_requests: Optional[int] = None,
+                 use_graphs: bool = False):
         self.m, self.pool = model, pool
+        # Dynamic batches have (almost) unique sizes: the executor would capture a CUDA graph on the second
+        # sighting of a size (milliseconds of host time inside the serving loop) and rarely replay it, which
+        # showed up as multi-ms p99 spikes at low load; direct launches keep the host cost per batch flat.
+        model.set_option("graphs", 1 if use_graphs else 0)
         self.batcher = DynamicBatcher(max_items, window_s, max_requests=max_requests)
         dev = model.device
         self.s_copy, self.s_embed = torch.cuda.Stream(dev), torch.cuda.Stream(dev)

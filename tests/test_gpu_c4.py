@@ -64,3 +64,21 @@ def test_c4_full_size_sampled():
     assert err.max() <= TOL_BF16, err.max()
     del m, tabs
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("B", [130, 3])
+def test_c4_fused_ffn_bitexact(c4small, B):
+    """The fused FFN + out-projection + LN kernel (ens_ffn.cu) accumulates O Wo^T then h W2^T in the same
+    16-wide K steps as the [O | h] [Wo | W2]^T GEMM and rounds h to bf16 at the same point: bit-identical
+    scores to the two-GEMM path (ragged token tiles included: B * 64 tokens)."""
+    cfg, m, tabs, w = c4small
+    bt = cs.make_batch(cfg, 6, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    s_u = m.dense(x0, B).clone()
+    m.set_option("ens_fused_ffn", 1)
+    try:
+        s_f = m.dense(x0, B).clone()
+    finally:
+        m.set_option("ens_fused_ffn", 0)
+    assert torch.equal(s_f, s_u)
