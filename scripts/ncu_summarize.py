@@ -18,10 +18,12 @@ EPI = {0: "STORE", 1: "BIAS_RELU", 2: "CROSS", 3: "HEAD", 4: "BIAS", 5: "CROSS_F
 
 
 def role(name):
-    m = re.search(r"gemm_bf16_kernel<(\d+), (\d+), (\d+), (\d+), (\d+)>", name)
+    m = re.search(r"gemm_bf16_kernel<(\d+), (\d+), (\d+), (\d+), (\d+)(?:, (\d+))?>", name)
     if m:
-        bn, epi, ar, cg, cn = map(int, m.groups())
-        r = {(0,): "gemm_xV", (2,): "gemm_tU_cross", (1,): "gemm_mlp_relu", (3,): "gemm_mlp_head"}.get((epi,), f"gemm_{EPI.get(epi, epi)}")
+        bn, epi, ar, cg, cn = map(int, m.groups()[:5])
+        # role names of config 2 (for c6: BIAS_RELU = projection / mask hidden / MLP, MASK = mask blocks)
+        r = {(0,): "gemm_xV", (2,): "gemm_tU_cross", (1,): "gemm_mlp_relu", (3,): "gemm_mlp_head",
+             (9,): "gemm_mask_mul"}.get((epi,), f"gemm_{EPI.get(epi, epi)}")
         return f"{r} [BN={bn}{' pair' if cg == 2 else ''}{' cluster%d' % cn if cn > 1 else ''}]"
     for k in ("embed_bag", "gemm_splitk", "dense_f32", "unpack", "mha64", "head_finalize", "cross_stack", "cross_fused"):
         if k in name:
