@@ -120,8 +120,10 @@ struct cvr_ctx {
   struct Mask {
     int Wp = 0, P = 0;
     size_t off_x0p = 0, off_H = 0, off_cat = 0, off_tmp[2] = {0, 0}, off_Vall = 0, off_call = 0;
-    CUtensorMap tm_x0p, st_x0p, st_H, tm_cat, tm_tmp[2], st_tmp[2], tmB_Vall;
+    size_t off_Uall = 0, off_ball = 0;  // parallel-only (S = 1): U_p stacked [P*W', r], b_p stacked [P*W']
+    CUtensorMap tm_x0p, st_x0p, st_H, tm_cat, tm_tmp[2], st_tmp[2], tmB_Vall, tmB_Uall, tm_Hall;
     std::vector<CUtensorMap> tm_Hblk, st_cat, tmB_U;
+    CUtensorMap tm_cat_st;  // store map over the whole cat [B, P*W'] (grouped launch)
     int bn_proj = 0, bn_h = 0, bn_u = 0;
   } mk;
   size_t off_hpart = 0;   // split-head partial dot products [max_batch, last/256]
@@ -169,6 +171,7 @@ struct cvr_ctx {
   // all 1.15 MB of W1 / W2 / Wo through a 3-deep ring (shared memory is full), so weight streaming, not the
   // h round trip it removes, bounds it; kept as an option
   bool ens_fused_ffn = false;
+  bool mask_grouped = true;    // option "mask_grouped": MaskNet parallel blocks as one grouped GEMM launch
   // option "xv_splitk" [0]: t = x_l V^T as a K-split cluster GEMM (r == 256).  Measured on B200 at B = 4096:
   // its mainloop halves (3.5 vs 7 us) but the DSMEM exchange of the fp32 partials costs 2-6 us (element-wise
   // st.shared::cluster or cp.async.bulk shared::cluster alike): 92-100 us per dense stage vs 90 with tiles
@@ -502,6 +505,10 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
       for (int i = 0; i < 2; ++i) K.off_tmp[i] = carve(cur, (size_t)B * K.Wp * 2);
     K.off_Vall = carve(cur, (size_t)nb * c->r * K.Wp * 2);
     K.off_call = carve(cur, (size_t)nb * c->r * 4);
+    if (c->n_cross == 1) {
+      K.off_Uall = carve(cur, (size_t)K.P * K.Wp * c->r * 2);
+      K.off_ball = carve(cur, (size_t)K.P * K.Wp * 4);
+    }
     for (int i = 0; i + 1 < c->n_mlp; ++i) c->off_h.push_back(carve(cur, (size_t)B * c->mlp[i] * 2));
   }
   if (c->backbone != CVR_DCN_FULL) {
@@ -692,6 +699,7 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
       ok &= encode_tmap_bf16(&K.tm_Hblk[j], c->ws + K.off_H + (size_t)j * c->r * 2, B, c->r, HW, 128, &er) == 0;
     ok &= encode_tmap_bf16(&K.tm_cat, c->ws + K.off_cat, B, CW, CW, 128, &er) == 0;
     ok &= c->add_q(&K.tm_cat, c->ws + K.off_cat, B, CW, CW, &er) == 0;
+    ok &= encode_tmap_bf16(&K.tm_cat_st, c->ws + K.off_cat, B, CW, CW, 32, &er) == 0;
     K.st_cat.assign(K.P, CUtensorMap{});
     for (int p = 0; p < K.P; ++p)
       ok &= encode_tmap_bf16(&K.st_cat[p], c->ws + K.off_cat + (size_t)p * K.Wp * 2, B, K.Wp, CW, 32, &er) == 0;
@@ -886,6 +894,13 @@ int encode_plan_masknet(cvr_ctx* c) {
       cudaError_t e2 = cudaMemcpy(c->ws + K.off_call + (size_t)j * r * 4, c->wptr(n + "c"), (size_t)r * 4,
                                   cudaMemcpyDeviceToDevice);
       if (e1 != cudaSuccess || e2 != cudaSuccess) return c->fail(CVR_E_CUDA, "assembling the MaskNet V_all / c_all");
+      if (S == 1) {  // parallel-only: all branches' mask GEMMs run as one grouped launch
+        cudaError_t e3 = cudaMemcpy(c->ws + K.off_Uall + (size_t)p * Wp * r * 2, c->wptr(n + "U"), (size_t)Wp * r * 2,
+                                    cudaMemcpyDeviceToDevice);
+        cudaError_t e4 = cudaMemcpy(c->ws + K.off_ball + (size_t)p * Wp * 4, c->wptr(n + "b"), (size_t)Wp * 4,
+                                    cudaMemcpyDeviceToDevice);
+        if (e3 != cudaSuccess || e4 != cudaSuccess) return c->fail(CVR_E_CUDA, "assembling the MaskNet U_all / b_all");
+      }
     }
   const int64_t M = c->max_batch;
   K.bn_proj = pick_bn(Wp, M);
@@ -902,6 +917,10 @@ int encode_plan_masknet(cvr_ctx* c) {
   ok &= encode_tmap_bf16(&gp.tmB, c->wptr("proj/W"), Wp, c->x0_ld, c->x0_ld, gp.BN, &er) == 0;
   c->plan.push_back(gp);  // plan[0]: projection
   ok &= encode_tmap_bf16(&K.tmB_Vall, c->ws + K.off_Vall, (int64_t)nb * r, Wp, Wp, K.bn_h, &er) == 0;
+  if (S == 1) {
+    ok &= encode_tmap_bf16(&K.tmB_Uall, c->ws + K.off_Uall, (int64_t)K.P * Wp, r, r, K.bn_u, &er) == 0;
+    ok &= encode_tmap_bf16(&K.tm_Hall, c->ws + K.off_H, M, (int64_t)nb * r, (int64_t)nb * r, 128, &er) == 0;
+  }
   K.tmB_U.assign(nb, CUtensorMap{});
   for (int p = 0; p < K.P; ++p)
     for (int q = 0; q < S; ++q)
@@ -1112,7 +1131,7 @@ GemmArgs gemm_args(cvr_ctx* c, const GemmPlan& g, const CUtensorMap* A, int M) {
   a.cta_pair = g.pair;
   {  // several tiles per CTA: the epilogue overlaps the next mainloop, keep the CTA small (Cfg::EPW)
     const int64_t tiles = (int64_t)((M + 127) / 128) * (g.N / g.BN);
-    a.epw1 = c->epw_mode == 0 || (c->epw_mode == 2 && tiles > c->num_sms);
+    a.epw1 = c->epw_mode == 0 || (c->epw_mode == 2 && tiles > 2 * c->num_sms);
   }
   if (c->gdbg && c->gdbg_n < 32) a.dbg = c->gdbg + (size_t)(c->gdbg_n++) * 160 * 8;
   if (g.cn > 1 && c->q(A)) {  // A operands without a quarter map stay unicast
@@ -1187,7 +1206,7 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     a.pdl = c->pdl;
     a.cta_pair = c->pair_ens;
     const int64_t tiles = (int64_t)((M + 127) / 128) * (N / BN);
-    a.epw1 = c->epw_mode == 0 || (c->epw_mode == 2 && tiles > c->num_sms);
+    a.epw1 = c->epw_mode == 0 || (c->epw_mode == 2 && tiles > 2 * c->num_sms);
     return a;
   };
   (void)gp;
@@ -1282,6 +1301,22 @@ int do_dense_masknet(cvr_ctx* c, const CUtensorMap* tm_x0, int B, float* scores,
   ah.bias = c->at<float>(K.off_call);
   ah.tmOut = &K.st_H;
   if ((e = run_gemm(c, ah, K_MASK_HIDDEN, s)) != cudaSuccess) return c->cuda_fail(e, "MaskNet mask hidden");
+  if (S == 1 && c->mask_grouped) {
+    // every branch's block in ONE grouped launch: N = P * W' over cat, branch g = n / W' reads H columns
+    // [g r, (g + 1) r), U rows of branch g (stacked), bias b_g, and x0' columns n - g W'
+    GemmPlan gu;
+    gu.N = K.P * K.Wp;
+    gu.K = c->r;
+    gu.BN = K.bn_u;
+    gu.epi = EPI_MASK;
+    GemmArgs au = gemm_args(c, gu, &K.tm_Hall, B);
+    au.tmB = &K.tmB_Uall;
+    au.tmXl = &K.tm_x0p;
+    au.bias = c->at<float>(K.off_ball);
+    au.tmOut = &K.tm_cat_st;
+    au.group_n = K.Wp;
+    if ((e = run_gemm(c, au, K_MASK_MUL, s)) != cudaSuccess) return c->cuda_fail(e, "MaskNet grouped mask blocks");
+  } else
   for (int p = 0; p < K.P; ++p) {
     const CUtensorMap* x_in = &K.tm_x0p;
     for (int q = 0; q < S; ++q) {
@@ -1983,6 +2018,12 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);  // U tile width
+    return CVR_OK;
+  }
+  if (!strcmp(key, "mask_grouped")) {
+    c->mask_grouped = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
     return CVR_OK;
   }
   if (!strcmp(key, "ens_fused_ffn")) {

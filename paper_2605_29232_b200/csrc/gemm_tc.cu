@@ -223,6 +223,10 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW>::NT, 1)
       int cur_m = -1, a_loads = 0;
       for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
         const int m0 = tile_m(tile) * BMT + rank * BM, n0 = tile_n(tile) * BN;
+        // grouped GEMM (EPI_MASK over several MaskNet branches): N group g = n0 / group_n reads the K range
+        // [g * K, (g + 1) * K) of A and the epilogue input at column n0 - g * group_n
+        const int grp = (EPI == EPI_MASK && g.group_n > 0) ? n0 / g.group_n : 0;
+        const int a_k0 = grp * K, e_n0 = n0 - grp * (EPI == EPI_MASK ? g.group_n : 0);
         if constexpr (AR) {
           if (roleA && m0 != cur_m) {
             if (a_loads > 0) ptx::mbar_wait(aempty, (a_loads - 1) & 1);
@@ -242,7 +246,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW>::NT, 1)
 #pragma unroll
             for (int j = 0; j < C::NSUB; ++j) {
               if constexpr (EPI == EPI_MASK) {
-                ptx::tma_load_2d(base + j * C::SUB, &tmXl, &efull[a], n0 + j * 64, m0);
+                ptx::tma_load_2d(base + j * C::SUB, &tmXl, &efull[a], e_n0 + j * 64, m0);
               } else {
                 ptx::tma_load_2d(base + j * C::SUB, &tmX0, &efull[a], n0 + j * 64, m0);
                 ptx::tma_load_2d(base + (C::NSUB + j) * C::SUB, &tmXl, &efull[a], n0 + j * 64, m0);
@@ -267,7 +271,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW>::NT, 1)
               ptx::tma_load_2d_mc(sA + s * C::A_BYTES + crank * (BM / CN) * 128, &tmA, &full[s], kb * BK,
                                   m0 + crank * (BM / CN), kMask);
             else
-              ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
+              ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], a_k0 + kb * BK, m0);
           } else {
             ptx::mbar_arrive_expect_tx(&full[s], C::B_BYTES);
             ptx::tma_load_2d(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);

@@ -84,3 +84,20 @@ def test_masknet_sequential_and_mixed_vs_oracle():
     ref = O.score_forward(cfg, cs.table_specs(cfg), w, bt)["scores"]
     assert np.abs(s.double().cpu().numpy() - ref).max() <= TOL_BF16
     m.close()
+
+
+@pytest.mark.parametrize("B", [4096, 333])
+def test_c6_grouped_mask_launch_bitexact(c6, B):
+    """The parallel branches' mask GEMMs as one grouped launch (branch g = n / W' reads H columns
+    [g r, (g+1) r) and U_g) vs one launch per branch: same MMAs, same K order -> bit-identical."""
+    cfg, m, tabs, w = c6
+    bt = cs.make_batch(cfg, 17, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    s_g = m.dense(x0, B).clone()
+    m.set_option("mask_grouped", 0)
+    try:
+        s_b = m.dense(x0, B).clone()
+    finally:
+        m.set_option("mask_grouped", 1)
+    assert torch.equal(s_g, s_b)
