@@ -229,7 +229,13 @@ int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d
  * low-rank cross layer as one clustered kernel (K5) instead of two GEMMs); "mc" [1] clusters of 4 CTAs
  * over adjacent N tiles with the A tile multicast by TMA: 0 = off, 1 = only the head GEMM (N = 4 x 64,
  * the sigmoid's dot product summed over the cluster in DSMEM, fixed order), 2 = every GEMM whose N tiles
- * group by 4.  Unknown key or bad value -> CVR_E_ARG. */
+ * group by 4; "u_bn" [192] N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64); "xv_splitk" [0]
+ * t = x_l V^T as a K-split cluster GEMM with a DSMEM reduction; "epw" [2] epilogue warps per TMEM quadrant:
+ * 0 one, 1 up to 4 (one 64-column sub-tile each), 2 split only when a CTA runs <= 2 tiles; "mb" [0] weight
+ * tiles multicast over clusters of 8 row blocks; "ens_fused_ffn" [0] config 4's FFN + out-projection + LN as
+ * one kernel; "mask_grouped" [1] MaskNet's parallel blocks as one grouped GEMM.  Variants are bit-identical
+ * except xv_splitk (fp32 summation order of t) and mc 0 vs 1 (the head's).  Unknown key or bad value ->
+ * CVR_E_ARG. */
 int cvr_set_option(cvr_ctx* ctx, const char* key, int64_t value);
 
 /* -- utility ----------------------------------------------------------------------------------

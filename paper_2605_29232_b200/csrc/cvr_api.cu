@@ -52,6 +52,8 @@ struct GemmPlan {
   Epi epi;
   bool pair = false;  // 2-CTA (cta_group::2) tiles; B map box = BN/2 rows
   int cn = 1;         // 4: A multicast across a cluster of 4 N tiles (needs the A operand's quarter map)
+  bool mb8ok = false; // B multicast across clusters of 8 row blocks is possible (tmB8 encoded)
+  CUtensorMap tmB8;   // B map with box {64, BN/8}
   const char* wname;  // B operand
   CUtensorMap tmB;
 };
@@ -172,6 +174,10 @@ struct cvr_ctx {
   // h round trip it removes, bounds it; kept as an option
   bool ens_fused_ffn = false;
   bool mask_grouped = true;    // option "mask_grouped": MaskNet parallel blocks as one grouped GEMM launch
+  // option "mb" [0]: weight (B) tiles sliced and TMA-multicast over clusters of 8 row blocks (bit-identical).
+  // Measured on B200, c2 dense stage: 176 vs 90 us -- clusters of 8 only start when 8 SMs of a GPC are free
+  // (CTA entry spread over ~10 us behind the previous kernel) and the mainloops got no faster
+  bool mb = false;
   // option "xv_splitk" [0]: t = x_l V^T as a K-split cluster GEMM (r == 256).  Measured on B200 at B = 4096:
   // its mainloop halves (3.5 vs 7 us) but the DSMEM exchange of the fp32 partials costs 2-6 us (element-wise
   // st.shared::cluster or cp.async.bulk shared::cluster alike): 92-100 us per dense stage vs 90 with tiles
@@ -786,6 +792,10 @@ int encode_plan(cvr_ctx* c) {
     g.epi = epi;
     g.wname = nullptr;
     if (encode_tmap_bf16(&g.tmB, c->wptr(wn), N, K, K, BN, &er) != 0) return false;
+    if (BN % 64 == 0 && (epi == EPI_STORE || epi == EPI_BIAS_RELU || (epi == EPI_CROSS && BN == 192))) {
+      if (encode_tmap_bf16(&g.tmB8, c->wptr(wn), N, K, K, BN / 8, &er) != 0) return false;
+      g.mb8ok = true;
+    }
     c->plan.push_back(g);
     return true;
   };
@@ -1134,6 +1144,10 @@ GemmArgs gemm_args(cvr_ctx* c, const GemmPlan& g, const CUtensorMap* A, int M) {
     a.epw1 = c->epw_mode == 0 || (c->epw_mode == 2 && tiles > 2 * c->num_sms);
   }
   if (c->gdbg && c->gdbg_n < 32) a.dbg = c->gdbg + (size_t)(c->gdbg_n++) * 160 * 8;
+  if (c->mb && g.mb8ok && g.cn <= 1 && !g.pair && !c->a_resident) {  // weight tiles multicast over 8 row blocks
+    a.mb8 = true;
+    a.tmB = &g.tmB8;
+  }
   if (g.cn > 1 && c->q(A)) {  // A operands without a quarter map stay unicast
     a.cn = g.cn;
     a.tmA = c->q(A);
@@ -2018,6 +2032,12 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);  // U tile width
+    return CVR_OK;
+  }
+  if (!strcmp(key, "mb")) {
+    c->mb = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
     return CVR_OK;
   }
   if (!strcmp(key, "mask_grouped")) {

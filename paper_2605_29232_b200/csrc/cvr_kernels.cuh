@@ -120,6 +120,7 @@ struct GemmArgs {
   bool a_resident;           // K <= 256: keep the A block resident, contiguous tile runs per CTA
   bool cta_pair;             // 2-CTA (cta_group::2) tiles of 256 rows; B box = BN/2 rows
   bool epw1;                 // one epilogue warp per TMEM quadrant (several tiles per CTA; see Cfg::EPW)
+  bool mb8;                  // clusters of 8 consecutive row blocks multicast the B tile (tmB box {64, BN/8})
   int group_n;               // EPI_MASK grouped over branches: N tiles of group g = n / group_n read A columns
                              // [g K, (g + 1) K) and x_l columns n - g group_n (0 = off)
   int cn;                    // 4: clusters of 4 CTAs along N multicast A (tmA box = {64, 32}); 0/1: off

@@ -55,7 +55,7 @@ struct EpiTraits {
 template <int BN, int EPI, int CG>
 constexpr bool ein_ring() { return EPI == EPI_CROSS && BN == 192 && CG == 1; }
 
-template <int BN, int EPI, bool AR = false, int CG = 1, int CN = 1, int EW = 4>
+template <int BN, int EPI, bool AR = false, int CG = 1, int CN = 1, int EW = 4, bool MB = false>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;       // 16 KB
   static constexpr int B_BYTES = (BN / CG) * BK * 2;  // CG = 2: each CTA of the pair holds half of B
@@ -105,6 +105,9 @@ using namespace tile;
 // barriers count CN multicast commits).  EPI_HEAD then spans CN tiles: the partial dot products of the
 // CN tiles are gathered in rank 0's shared memory over DSMEM and summed in rank order (fixed order,
 // independent of M: batch invariance).
+// MB (with CN > 1): the cluster runs along M instead -- CN consecutive 128-row blocks of the same N tile --
+// and it is the B k-block that is sliced (BN/CN rows per CTA, tmB box {64, BN/CN}) and multicast: every CTA
+// issues 1/CN of the weight bytes and the L2 serves each weight line once per cluster.
 __device__ __forceinline__ void stamp(unsigned long long* dbg, int i) {
   if (dbg) {
     unsigned long long t;
@@ -113,16 +116,17 @@ __device__ __forceinline__ void stamp(unsigned long long* dbg, int i) {
   }
 }
 
-template <int BN, int EPI, bool AR, int CG, int CN, int EW>
-__global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW>::NT, 1)
+template <int BN, int EPI, bool AR, int CG, int CN, int EW, bool MB>
+__global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmX0,
                      const __grid_constant__ CUtensorMap tmXl, const GemmArgs g) {
-  using C = Cfg<BN, EPI, AR, CG, CN, EW>;
+  using C = Cfg<BN, EPI, AR, CG, CN, EW, MB>;
   using T = EpiTraits<EPI>;
   static_assert(CG == 1 || !AR, "the resident-A walk is single-CTA");
+  static_assert(!MB || (CN > 1 && BN % (8 * CN) == 0 && EPI != EPI_HEAD), "B slices are whole 8-row swizzle atoms");
   static_assert(CN == 1 || (CG == 1 && !AR), "A multicast is cta_group::1 streaming only");
-  static_assert(BM % (8 * CN) == 0, "A slices are whole 8-row swizzle atoms");
+  static_assert(MB || BM % (8 * CN) == 0, "A slices are whole 8-row swizzle atoms");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sAR = smem;                                  // resident A (AR only)
@@ -154,10 +158,12 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW>::NT, 1)
   const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x / CN;
   const int n_units = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x / CN;
   const int n_tiles_n = N / BN;
-  const int n_groups = n_tiles_n / CN;  // tiles of a cluster: (m-block, group of CN adjacent N tiles)
-  const int n_tiles = ((M + BMT - 1) / BMT) * n_groups;
-  auto tile_m = [&](int tile) { return tile / n_groups; };
-  auto tile_n = [&](int tile) { return (tile % n_groups) * CN + crank; };
+  // tiles of a cluster: (m-block, group of CN adjacent N tiles), or with MB (group of CN m-blocks, N tile)
+  const int n_groups = MB ? n_tiles_n : n_tiles_n / CN;
+  const int m_units = MB ? ((M + BMT - 1) / BMT + CN - 1) / CN : (M + BMT - 1) / BMT;
+  const int n_tiles = m_units * n_groups;
+  auto tile_m = [&](int tile) { return MB ? (tile / n_groups) * CN + crank : tile / n_groups; };
+  auto tile_n = [&](int tile) { return MB ? tile % n_groups : (tile % n_groups) * CN + crank; };
   const int nk = K / BK;
   // tile walk: strided over the grid, or (AR) a contiguous balanced run per CTA
   const int t_begin = AR ? (int)((int64_t)n_tiles * unit / n_units) : unit;
@@ -267,14 +273,18 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW>::NT, 1)
             }
           } else if (roleA) {
             ptx::mbar_arrive_expect_tx(&full[s], C::A_BYTES);
-            if constexpr (CN > 1)
+            if constexpr (CN > 1 && !MB)
               ptx::tma_load_2d_mc(sA + s * C::A_BYTES + crank * (BM / CN) * 128, &tmA, &full[s], kb * BK,
                                   m0 + crank * (BM / CN), kMask);
             else
               ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], a_k0 + kb * BK, m0);
           } else {
             ptx::mbar_arrive_expect_tx(&full[s], C::B_BYTES);
-            ptx::tma_load_2d(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);
+            if constexpr (MB)
+              ptx::tma_load_2d_mc(sB + s * C::B_BYTES + crank * (BN / CN) * 128, &tmB, &full[s], kb * BK,
+                                  n0 + crank * (BN / CN), kMask);
+            else
+              ptx::tma_load_2d(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);
           }
         }
       }
@@ -544,17 +554,18 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW>::NT, 1)
   }
 }
 
-template <int BN, int EPI, bool AR = false, int CG = 1, int CN = 1, int EW = 4>
+template <int BN, int EPI, bool AR = false, int CG = 1, int CN = 1, int EW = 4, bool MB = false>
 cudaError_t launch_t(const GemmArgs& g, cudaStream_t s) {
-  using C = Cfg<BN, EPI, AR, CG, CN, EW>;
-  auto kern = gemm_bf16_kernel<BN, EPI, AR, CG, CN, EW>;
+  using C = Cfg<BN, EPI, AR, CG, CN, EW, MB>;
+  auto kern = gemm_bf16_kernel<BN, EPI, AR, CG, CN, EW, MB>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  const int n_tiles = ((g.M + BM * CG - 1) / (BM * CG)) * (g.N / BN / CN);
+  const int m_blocks = (g.M + BM * CG - 1) / (BM * CG);
+  const int n_tiles = MB ? (m_blocks + CN - 1) / CN * (g.N / BN) : m_blocks * (g.N / BN / CN);
   const int max_units = g.num_sms / (CG * CN);
   const int grid = (n_tiles < max_units ? n_tiles : max_units) * CG * CN;
   cudaLaunchConfig_t cfg{};
@@ -591,6 +602,18 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
     return cudaErrorInvalidValue;
   if ((g.epi == EPI_CROSS || g.epi == EPI_CROSS_F32) && (!g.tmX0 || !g.tmXl)) return cudaErrorInvalidValue;
   if (g.epi == EPI_MASK && (!g.tmXl || !g.tmOut)) return cudaErrorInvalidValue;
+  // B-multicast clusters of 8 along M (tmB with box {64, BN/8})
+  if (g.mb8) {
+    if (g.cta_pair || g.a_resident || g.cn > 1) return cudaErrorInvalidValue;
+#define CVR_MB(BN_, EPI_) \
+    if (g.BN == BN_ && g.epi == EPI_) return launch_t<BN_, EPI_, false, 1, 8, 1, true>(g, s);
+    CVR_MB(256, EPI_BIAS_RELU)
+    CVR_MB(128, EPI_BIAS_RELU)
+    CVR_MB(192, EPI_CROSS)
+    CVR_MB(64, EPI_STORE)
+#undef CVR_MB
+    return cudaErrorInvalidValue;
+  }
   // A-multicast clusters of 4 along N (tmA with box {64, 32})
 #define CVR_MC(BN_, EPI_) \
   if (cn == 4 && g.BN == BN_ && g.epi == EPI_) return launch_t<BN_, EPI_, false, 1, 4>(g, s);

@@ -15,7 +15,7 @@ se, sd = torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1)
 raw = [(i.data_ptr(), o.data_ptr(), i.numel(), d.data_ptr(), out.data_ptr()) for (i, o, d), out in zip(dev, outs)]
 settings = json.loads(sys.argv[1])
 K = int(os.environ.get("K", "500"))
-DEF = {"u_bn": 192, "epw": 2, "mc": 1, "pdl": 1, "graphs": 1, "xv_splitk": 0, "embed_bps": 0}
+DEF = {"u_bn": 192, "epw": 2, "mc": 1, "pdl": 1, "graphs": 1, "xv_splitk": 0, "embed_bps": 0, "mb": 0}
 for rep in range(3):
     for st in settings:
         for k, v in st.items(): m.set_option(k, v)

@@ -295,3 +295,20 @@ def test_c2_xv_splitk(c2, B):
     ref = O.score_forward(cfg, cs.table_specs(cfg), w, sub_batch(bt, sel))["scores"]
     for s in (s_split, s_tile):
         assert np.abs(s[torch.from_numpy(sel).cuda()].double().cpu().numpy() - ref).max() <= TOL_BF16
+
+
+@pytest.mark.parametrize("B", [4096, 333, 1])
+def test_c2_weight_multicast_bitexact(c2, B):
+    """Option mb: weight tiles sliced and TMA-multicast over clusters of 8 row blocks (padded row-block count
+    for ragged batches).  Only the load routing changes: bit-identical scores."""
+    cfg, m, tabs, w = c2
+    bt = cs.make_batch(cfg, 59, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    s0 = m.dense(x0, B).clone()
+    m.set_option("mb", 1)
+    try:
+        s1 = m.dense(x0, B).clone()
+    finally:
+        m.set_option("mb", 0)
+    assert torch.equal(s0, s1)
