@@ -16,6 +16,8 @@ LIB = os.path.join(HERE, "libcvr.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2,-fopenmp", "--expt-relaxed-constexpr", "-I", INCLUDE]
+# experiments only (e.g. CVR_NVCC_EXTRA="-DCVR_MAX_STAGES=4"); the shipped build sets nothing
+FLAGS += os.environ.get("CVR_NVCC_EXTRA", "").split()
 
 
 def sources():

@@ -116,7 +116,7 @@ __device__ __forceinline__ int64_t hashed_row(uint64_t key, int64_t vocab, uint6
   return (int64_t)r;
 }
 
-template <typename TIn, typename TOut, int LPR, int UNROLL, int MINB, bool KEYS>
+template <typename TIn, typename TOut, int LPR, int UNROLL, int MINB, bool KEYS, bool COOP = false>
 __global__ void __launch_bounds__(256, MINB) embed_bag_kernel(const EmbedArgs a, int n_embed_blocks) {
   if ((int)blockIdx.x >= n_embed_blocks) {
     dense_part<TOut>(a, blockIdx.x - n_embed_blocks, gridDim.x - n_embed_blocks);
@@ -138,19 +138,31 @@ __global__ void __launch_bounds__(256, MINB) embed_bag_kernel(const EmbedArgs a,
     bool bad = start < 0 || end < start || end > a.nnz;
     if (!bad) {
       const uint8_t* colbase = td.base + sub * 16;
-      if constexpr (KEYS) {
-        // each lane of the group hashes one key of the next LPR, then the row ids are broadcast in turn
+      if constexpr (KEYS || COOP) {
+        // each lane of the group fetches (keys: and hashes) one element of the next LPR -- one coalesced
+        // load per group -- then the row ids are broadcast in turn, two row loads in flight per lane
         const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1) << (threadIdx.x & 31 & ~(LPR - 1)));
         for (int64_t j0 = start; j0 < end; j0 += LPR) {
           const int64_t jj = j0 + sub;
-          const int64_t my = jj < end ? hashed_row(__ldg(a.keys + jj), td.vocab, td.magic) : 0;
+          int64_t my = 0;
+          if (jj < end) {
+            if constexpr (KEYS) my = hashed_row(__ldg(a.keys + jj), td.vocab, td.magic);
+            else my = (int64_t)__ldg(a.indices + jj);
+          }
           bad |= jj < end && (my < 0 || my >= td.rows);
           bad = __any_sync(gmask, bad);
           if (bad) break;
           const int cnt = (int)((end - j0) < LPR ? (end - j0) : LPR);
-          for (int u = 0; u < cnt; ++u) {
-            const int64_t row = __shfl_sync(gmask, my, u, LPR);
-            InTraits<TIn>::add(acc, ptx::ld_nc_v4(colbase + row * td.stride));
+          int u = 0;
+          for (; u + 1 < cnt; u += 2) {
+            const int64_t r0 = __shfl_sync(gmask, my, u, LPR), r1 = __shfl_sync(gmask, my, u + 1, LPR);
+            const uint4 v0 = ptx::ld_nc_v4(colbase + r0 * td.stride), v1 = ptx::ld_nc_v4(colbase + r1 * td.stride);
+            InTraits<TIn>::add(acc, v0);
+            InTraits<TIn>::add(acc, v1);
+          }
+          if (u < cnt) {
+            const int64_t r0 = __shfl_sync(gmask, my, u, LPR);
+            InTraits<TIn>::add(acc, ptx::ld_nc_v4(colbase + r0 * td.stride));
           }
         }
       } else
@@ -341,6 +353,8 @@ cudaError_t launch_t(const EmbedArgs& a, int num_sms, cudaStream_t s) {
     embed_bag_kernel<TIn, TOut, LPR, 1, 8, true><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
   else if (a.v2)
     embed_bag_v2_kernel<TIn, TOut, LPR, 4><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
+  else if (a.variant == 2)  // cooperative index fetch + broadcast (option embed_variant = 2)
+    embed_bag_kernel<TIn, TOut, LPR, 1, 8, false, true><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
   else
     embed_bag_kernel<TIn, TOut, LPR, 1, 8, false><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
   return cudaGetLastError();

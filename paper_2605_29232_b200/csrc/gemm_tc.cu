@@ -83,7 +83,10 @@ struct Cfg {
   // EPI_HEAD across a CN-cluster: per-tile partial dot products gathered in rank 0 ([2][CN][BM] fp32)
   static constexpr int Z_BYTES = (EPI == EPI_HEAD && CN > 1) ? 2 * CN * BM * 4 : 0;
   static constexpr int STAGES_FIT = (kSmemBudget - 1024 - BAR_BYTES - EPI_BYTES - AR_BYTES - Z_BYTES) / STAGE;
-  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+#ifndef CVR_MAX_STAGES
+#define CVR_MAX_STAGES 8
+#endif
+  static constexpr int STAGES = STAGES_FIT > CVR_MAX_STAGES ? CVR_MAX_STAGES : STAGES_FIT;
   static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);  // 2 accumulators, pow2 alloc
   static constexpr int SMEM = 1024 + AR_BYTES + STAGES * STAGE + EPI_BYTES + Z_BYTES + BAR_BYTES;
   static_assert(STAGES >= 2, "shared memory budget");
