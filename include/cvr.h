@@ -191,21 +191,27 @@ int cvr_embed_shard(cvr_ctx* ctx, const int32_t* d_indices, const int32_t* d_off
                     cvr_stream_t stream);
 
 /* -- fused exchange (V3 of SURVEY.md §8(e), §8(f) #4): no send / receive buffers, no all-to-all ----------
- * cvr_set_peers: d_peer_x0[dst] is rank dst's x0 buffer ([batch_global / N, x0_ld], the one rank dst passes to
- * cvr_dense) mapped into this process (cvr_ipc_open_handle of its cvr_ipc_get_handle; this rank's own buffer for
- * dst == rank); d_peer_flags[dst] is rank dst's flag array (uint32 [N], zero-initialised once); d_local_flags is
- * this rank's own.  n == world_size > 1.
- * cvr_embed_fused: the gather kernel writes each pooled bag (local table t, global example b) straight into
- * d_peer_x0[b / (B/N)] at row b % (B/N), columns (t*N + rank)*d (the canonical x0 layout, BASELINE.json
- * configs[2] round-robin placement, A18) and the normalised dense features of this rank's slice into d_x0, then
- * stores flags[dst][rank] = epoch on every rank (release, system scope, after a system fence).
- * cvr_wait_peers: enqueues a wait until this rank's flags[src] >= epoch for every src (acquire, system scope);
- * after it, d_x0 holds the complete canonical x0 slice and cvr_dense may run.  epoch must increase per batch.
- * Pooled values are bit-identical to cvr_embed / the NCCL path (same per-bag order, the exchange is a store). */
-int cvr_set_peers(cvr_ctx* ctx, int n, void* const* d_peer_x0, uint32_t* const* d_peer_flags, uint32_t* d_local_flags);
+ * Each rank owns TWO x0 slots ([batch_global / N, x0_ld] each, the buffers it passes to cvr_dense; batch epoch e
+ * uses slot e % 2) and two uint32 [N] flag arrays, zero-initialised once: ready[src] and free[dst].
+ * cvr_set_peers: d_peer_x0[slot * N + dst] is rank dst's x0 slot mapped into this process (cvr_ipc_open_handle
+ * of its cvr_ipc_get_handle; this rank's own buffers for dst == rank), d_peer_ready[dst] / d_peer_free[dst]
+ * rank dst's flag arrays, d_local_ready / d_local_free this rank's.  n == world_size > 1.
+ * cvr_embed_fused (epoch e = 1, 2, ...): waits until free[dst] >= e - 2 for every dst (each owner has finished
+ * the dense stage that read slot e % 2 two batches ago), then the gather kernel writes each pooled bag (local
+ * table t, global example b) straight into d_peer_x0[(e % 2) * N + b / (B/N)] at row b % (B/N), columns
+ * (t*N + rank)*d (the canonical x0 layout; round-robin placement, A18) and the normalised dense features of this
+ * rank's slice into d_x0 (this rank's slot e % 2), then stores ready[rank] = e on every rank (release, system
+ * scope, after a system fence).
+ * cvr_wait_peers(e): enqueues a wait until this rank's ready[src] >= e for every src (acquire, system scope);
+ * after it the slot holds the complete canonical x0 slice and cvr_dense may run on it.
+ * cvr_release_peers(e): after that dense stage, stores free[rank] = e on every rank.
+ * Pooled values are bit-identical to cvr_embed / the NCCL path (same per-bag order; the exchange is a store). */
+int cvr_set_peers(cvr_ctx* ctx, int n, void* const* d_peer_x0, uint32_t* const* d_peer_ready,
+                  uint32_t* const* d_peer_free, uint32_t* d_local_ready, uint32_t* d_local_free);
 int cvr_embed_fused(cvr_ctx* ctx, const int32_t* d_indices, const int32_t* d_offsets, int64_t nnz, int batch_global,
                     const float* d_dense, void* d_x0, uint32_t epoch, cvr_stream_t stream);
 int cvr_wait_peers(cvr_ctx* ctx, uint32_t epoch, cvr_stream_t stream);
+int cvr_release_peers(cvr_ctx* ctx, uint32_t epoch, cvr_stream_t stream);
 /* CUDA IPC for the peer mappings: a 64-byte handle of a device allocation, opened in another process of the
  * node (peer access enabled lazily); close unmaps it. */
 int cvr_ipc_get_handle(const void* d_ptr, void* handle64);

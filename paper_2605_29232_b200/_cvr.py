@@ -63,9 +63,11 @@ _SIGS = [
                                               ctypes.POINTER(ctypes.c_size_t)]),
     ("cvr_embed_shard", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp, _vp]),
     ("cvr_unpack_shard", ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp, _vp]),
-    ("cvr_set_peers", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp]),
+    ("cvr_set_peers", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                                     _vp, _vp]),
     ("cvr_embed_fused", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, ctypes.c_uint32, _vp]),
     ("cvr_wait_peers", ctypes.c_int, [_vp, ctypes.c_uint32, _vp]),
+    ("cvr_release_peers", ctypes.c_int, [_vp, ctypes.c_uint32, _vp]),
     ("cvr_ipc_get_handle", ctypes.c_int, [_vp, _vp]),
     ("cvr_ipc_open_handle", ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
     ("cvr_ipc_close_handle", ctypes.c_int, [_vp]),
@@ -344,11 +346,13 @@ class CvrModel:
     def unpack_shard(self, recv, batch_global, x0, stream=None):
         self._check(self.L.cvr_unpack_shard(self.h, _ptr(recv), batch_global, _ptr(x0), _stream(stream)))
 
-    def set_peers(self, peer_x0_ptrs, peer_flag_ptrs, local_flags_ptr: int):
-        n = len(peer_x0_ptrs)
-        px = (_vp * n)(*peer_x0_ptrs)
-        pf = (_vp * n)(*peer_flag_ptrs)
-        self._check(self.L.cvr_set_peers(self.h, n, px, pf, local_flags_ptr))
+    def set_peers(self, peer_x0_ptrs, peer_ready_ptrs, peer_free_ptrs, local_ready_ptr: int, local_free_ptr: int):
+        """peer_x0_ptrs: 2 * N pointers, slot-major ([slot 0 of ranks 0..N-1, slot 1 of ranks 0..N-1])."""
+        n = len(peer_ready_ptrs)
+        px = (_vp * (2 * n))(*peer_x0_ptrs)
+        pr = (_vp * n)(*peer_ready_ptrs)
+        pf = (_vp * n)(*peer_free_ptrs)
+        self._check(self.L.cvr_set_peers(self.h, n, px, pr, pf, local_ready_ptr, local_free_ptr))
 
     def embed_fused(self, indices, offsets, batch_global, dense, x0, epoch: int, stream=None):
         self._check(self.L.cvr_embed_fused(self.h, _ptr(indices), _ptr(offsets), indices.numel(), batch_global,
@@ -356,6 +360,9 @@ class CvrModel:
 
     def wait_peers(self, epoch: int, stream=None):
         self._check(self.L.cvr_wait_peers(self.h, epoch, _stream(stream)))
+
+    def release_peers(self, epoch: int, stream=None):
+        self._check(self.L.cvr_release_peers(self.h, epoch, _stream(stream)))
 
     def set_option(self, key: str, value: int):
         self._check(self.L.cvr_set_option(self.h, key.encode(), int(value)))

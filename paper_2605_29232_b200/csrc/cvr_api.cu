@@ -74,8 +74,10 @@ struct cvr_ctx {
   std::vector<int> local_tables;
   int T_pad = 0;
   // fused exchange (V3): device arrays [world] of peer x0 bases and peer flag arrays, own flag array
+  // device table: [2][world] peer x0 slot bases, [world] peer ready-flag arrays, [world] peer free-flag arrays
   size_t off_peers = 0;
-  uint32_t* local_flags = nullptr;
+  uint32_t* local_ready = nullptr;  // [world]: ready[src] = last epoch whose rows src stored into our x0 slot
+  uint32_t* local_free = nullptr;   // [world]: free[dst] = last epoch whose dense stage dst has finished
   bool peers_set = false;
   // ---- state
   std::string err;
@@ -476,7 +478,7 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
   const int64_t B = c->max_batch;
   c->off_tables = carve(cur, sizeof(TableDesc) * std::max<size_t>(1, c->local_tables.size()));
   c->off_flag = carve(cur, 256);
-  if (c->world > 1) c->off_peers = carve(cur, (size_t)2 * c->world * sizeof(void*));
+  if (c->world > 1) c->off_peers = carve(cur, (size_t)4 * c->world * sizeof(void*));
   for (int i = 0; i < 2; ++i) c->off_x0[i] = carve(cur, (size_t)B * c->x0_ld * ae);
   if (c->backbone == CVR_DCN_LOWRANK) {
     c->off_xa = carve(cur, (size_t)B * c->x0_ld * 2);
@@ -1803,17 +1805,22 @@ int cvr_embed_shard(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offse
   return CVR_OK;
 }
 
-int cvr_set_peers(cvr_ctx* c, int n, void* const* d_peer_x0, uint32_t* const* d_peer_flags, uint32_t* d_local_flags) {
-  if (!c || !d_peer_x0 || !d_peer_flags || !d_local_flags) return CVR_E_ARG;
+int cvr_set_peers(cvr_ctx* c, int n, void* const* d_peer_x0, uint32_t* const* d_peer_ready,
+                  uint32_t* const* d_peer_free, uint32_t* d_local_ready, uint32_t* d_local_free) {
+  if (!c || !d_peer_x0 || !d_peer_ready || !d_peer_free || !d_local_ready || !d_local_free) return CVR_E_ARG;
   if (!c->cuda_ready) return c->fail(CVR_E_STATE, "cvr_set_peers before cvr_set_workspace");
   if (c->world < 2 || n != c->world) return c->fail(CVR_E_ARG, "cvr_set_peers: n must equal world_size (> 1)");
+  for (int i = 0; i < 2 * n; ++i)
+    if (!d_peer_x0[i]) return c->fail(CVR_E_ARG, "peer x0 slot %d: null pointer", i);
   for (int i = 0; i < n; ++i)
-    if (!d_peer_x0[i] || !d_peer_flags[i]) return c->fail(CVR_E_ARG, "peer %d: null pointer", i);
-  cudaError_t e = cudaMemcpy(c->ws + c->off_peers, d_peer_x0, n * sizeof(void*), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess)
-    e = cudaMemcpy(c->ws + c->off_peers + n * sizeof(void*), d_peer_flags, n * sizeof(void*), cudaMemcpyHostToDevice);
+    if (!d_peer_ready[i] || !d_peer_free[i]) return c->fail(CVR_E_ARG, "peer %d: null flag pointer", i);
+  const size_t P = sizeof(void*);
+  cudaError_t e = cudaMemcpy(c->ws + c->off_peers, d_peer_x0, 2 * n * P, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(c->ws + c->off_peers + 2 * n * P, d_peer_ready, n * P, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(c->ws + c->off_peers + 3 * n * P, d_peer_free, n * P, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return c->cuda_fail(e, "cvr_set_peers");
-  c->local_flags = d_local_flags;
+  c->local_ready = d_local_ready;
+  c->local_free = d_local_free;
   c->peers_set = true;
   return CVR_OK;
 }
@@ -1824,37 +1831,56 @@ int cvr_embed_fused(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offse
   int st = check_ready(c, true, false);
   if (st) return st;
   if (!c->peers_set) return c->fail(CVR_E_STATE, "cvr_embed_fused before cvr_set_peers");
+  if (epoch == 0) return c->fail(CVR_E_ARG, "epoch must start at 1 and increase by one per batch");
   if (batch_global < 0 || batch_global % c->world || batch_global / c->world > c->max_batch)
     return c->fail(CVR_E_ARG, "batch_global %d must be a multiple of world %d with B/N <= max_batch %d", batch_global,
                    c->world, c->max_batch);
   if (!d_offsets || !d_x0 || (nnz > 0 && !d_indices) || (c->F && batch_global && !d_dense) || nnz < 0)
     return c->fail(CVR_E_ARG, "null pointer or negative nnz");
   if (c->F && !c->slot("norm/mean")->loaded) return c->fail(CVR_E_STATE, "norm/mean,std not loaded");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t P = sizeof(void*);
+  cudaError_t e;
+  if (epoch > 2) {  // every owner has finished the dense stage of epoch - 2, which read the slot we now fill
+    e = launch_peer_wait(c->local_free, c->world, epoch - 2, s);
+    ++c->launches;
+    if (e != cudaSuccess) return c->cuda_fail(e, "peer free wait launch");
+  }
   EmbedArgs a = embed_args(c, d_indices, d_offsets, nnz, batch_global, d_dense, d_x0, c->x0_ld, d_x0,
                            batch_global / c->world);
-  a.peer_x0 = reinterpret_cast<void* const*>(c->ws + c->off_peers);
+  a.peer_x0 = reinterpret_cast<void* const*>(c->ws + c->off_peers + (epoch & 1) * c->world * P);
   a.world = c->world;
   a.rank = c->rank;
   a.Bl = batch_global / c->world;
   a.v2 = false;
-  cudaStream_t s = (cudaStream_t)stream;
   c->pbeg(s);
-  cudaError_t e = launch_embed(a, c->num_sms, s);
+  e = launch_embed(a, c->num_sms, s);
   c->pend(K_EMBED, s);
   if (e != cudaSuccess) return c->cuda_fail(e, "embed_fused launch");
-  e = launch_peer_signal(reinterpret_cast<uint32_t* const*>(c->ws + c->off_peers + c->world * sizeof(void*)), c->world,
+  e = launch_peer_signal(reinterpret_cast<uint32_t* const*>(c->ws + c->off_peers + 2 * c->world * P), c->world,
                          c->rank, epoch, s);
   ++c->launches;
-  if (e != cudaSuccess) return c->cuda_fail(e, "peer signal launch");
+  if (e != cudaSuccess) return c->cuda_fail(e, "peer ready signal launch");
   return CVR_OK;
 }
 
 int cvr_wait_peers(cvr_ctx* c, uint32_t epoch, cvr_stream_t stream) {
   if (!c) return CVR_E_ARG;
   if (!c->peers_set) return c->fail(CVR_E_STATE, "cvr_wait_peers before cvr_set_peers");
-  cudaError_t e = launch_peer_wait(c->local_flags, c->world, epoch, (cudaStream_t)stream);
+  cudaError_t e = launch_peer_wait(c->local_ready, c->world, epoch, (cudaStream_t)stream);
   ++c->launches;
   if (e != cudaSuccess) return c->cuda_fail(e, "peer wait launch");
+  return CVR_OK;
+}
+
+int cvr_release_peers(cvr_ctx* c, uint32_t epoch, cvr_stream_t stream) {
+  if (!c) return CVR_E_ARG;
+  if (!c->peers_set) return c->fail(CVR_E_STATE, "cvr_release_peers before cvr_set_peers");
+  const size_t P = sizeof(void*);
+  cudaError_t e = launch_peer_signal(reinterpret_cast<uint32_t* const*>(c->ws + c->off_peers + 3 * c->world * P),
+                                     c->world, c->rank, epoch, (cudaStream_t)stream);
+  ++c->launches;
+  if (e != cudaSuccess) return c->cuda_fail(e, "peer free signal launch");
   return CVR_OK;
 }
 

@@ -53,17 +53,17 @@ def exchange_handles(blob: bytes, group=None) -> list:
 
 class FusedShardedScorer:
     """One rank of the V3 sharded path: the gather kernel stores pooled rows
-    straight into the owner rank's canonical x0 over NVLink (cvr_embed_fused), a per-batch epoch flag per
-    (src, dst) pair replaces the all-to-all, and the dense stage waits on the flags (cvr_wait_peers).  No send
-    / receive buffers, no unpack, no NCCL kernel on the data path.
+    straight into the owner rank's canonical x0 over NVLink (cvr_embed_fused), per-batch epoch flags replace the
+    all-to-all (ready: rows stored; free: the owner's dense stage is done with the slot), and the dense stage waits
+    on the ready flags (cvr_wait_peers).  Two x0 slots per rank (epoch parity), so batch e+1's stores overlap
+    batch e's dense stage.  No send / receive buffers, no unpack, no NCCL kernel on the data path.
 
-    ``peers=None``: map the other ranks' x0 and flag buffers through CUDA IPC (one process per GPU).
-    ``peers=(x0_list, flags_list)``: use the given device tensors (all ranks' buffers visible in this process,
-    e.g. emulated ranks on one GPU in the tests)."""
+    ``connect(peers=None)``: map the other ranks' slots and flag arrays through CUDA IPC (one process per GPU).
+    ``connect(peers=ranks)``: all ranks' FusedShardedScorer objects live in this process (emulated ranks on one
+    GPU in the tests)."""
 
     def __init__(self, cfg, world_size: int, rank: int, batch_global: int, max_nnz: int,
-                 device: Optional[torch.device] = None, group=None, x0: Optional[torch.Tensor] = None,
-                 flags: Optional[torch.Tensor] = None):
+                 device: Optional[torch.device] = None, group=None):
         from ._cvr import CvrModel
         if batch_global % world_size:
             raise ValueError("batch_global must be a multiple of world_size (A18)")
@@ -72,30 +72,31 @@ class FusedShardedScorer:
         self.model = CvrModel(cfg, max_batch=self.Bl, max_nnz=max_nnz, world_size=world_size, rank=rank,
                               device=device)
         self.device = self.model.device
-        self.x0 = self.model.new_x0(self.Bl).zero_() if x0 is None else x0
-        self.flags = torch.zeros(world_size, dtype=torch.int32, device=self.device) if flags is None else flags
+        self.x0 = [self.model.new_x0(self.Bl).zero_() for _ in range(2)]   # slot = epoch % 2
+        self.ready = torch.zeros(world_size, dtype=torch.int32, device=self.device)
+        self.free = torch.zeros(world_size, dtype=torch.int32, device=self.device)
         self.tables = local_tables(cfg.n_tables, world_size, rank)
         self.epoch = 0
-        self._opened = []
+
+    def _buffers(self):
+        return [self.x0[0], self.x0[1], self.ready, self.free]
 
     def connect(self, peers=None):
         from ._cvr import ipc_get_handle, ipc_open_handle
         if peers is None:
-            hx = exchange_handles(ipc_get_handle(self.x0.data_ptr()), self.group)
-            hf = exchange_handles(ipc_get_handle(self.flags.data_ptr()), self.group)
-            px, pf = [], []
+            mine = [ipc_get_handle(t.data_ptr()) for t in self._buffers()]
+            allh = exchange_handles(b"".join(mine), self.group)
+            ptrs = []
             for r in range(self.N):
                 if r == self.rank:
-                    px.append(self.x0.data_ptr())
-                    pf.append(self.flags.data_ptr())
+                    ptrs.append([t.data_ptr() for t in self._buffers()])
                 else:
-                    px.append(ipc_open_handle(hx[r]))
-                    pf.append(ipc_open_handle(hf[r]))
-                    self._opened += [px[-1], pf[-1]]
+                    ptrs.append([ipc_open_handle(allh[r][64 * i:64 * (i + 1)]) for i in range(4)])
         else:
-            px = [t.data_ptr() for t in peers[0]]
-            pf = [t.data_ptr() for t in peers[1]]
-        self.model.set_peers(px, pf, self.flags.data_ptr())
+            ptrs = [[t.data_ptr() for t in p._buffers()] for p in peers]
+        x0_ptrs = [ptrs[r][0] for r in range(self.N)] + [ptrs[r][1] for r in range(self.N)]
+        self.model.set_peers(x0_ptrs, [ptrs[r][2] for r in range(self.N)], [ptrs[r][3] for r in range(self.N)],
+                             self.ready.data_ptr(), self.free.data_ptr())
 
     def load_tables(self, tables: Sequence[torch.Tensor]):
         self.model.load_tables(tables, self.tables)
@@ -104,15 +105,18 @@ class FusedShardedScorer:
         self.model.load_weights(weights)
 
     def embed(self, indices, offsets, dense_local, stream=None):
-        """Gather + push this rank's tables for the global batch; signals epoch + 1 to every rank."""
+        """Gather + push this rank's tables for the global batch of the next epoch; signals ready."""
         self.epoch += 1
-        self.model.embed_fused(indices, offsets, self.B, dense_local, self.x0, self.epoch, stream=stream)
+        self.model.embed_fused(indices, offsets, self.B, dense_local, self.x0[self.epoch % 2], self.epoch,
+                               stream=stream)
 
-    def dense(self, scores: Optional[torch.Tensor] = None, stream=None, wait: bool = True) -> torch.Tensor:
+    def dense(self, scores: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+        """Wait for every rank's rows of this epoch, score the slot, then release it (free flags)."""
         scores = torch.empty(self.Bl, dtype=torch.float32, device=self.device) if scores is None else scores
-        if wait:
-            self.model.wait_peers(self.epoch, stream=stream)
-        return self.model.dense(self.x0, self.Bl, scores, stream=stream)
+        self.model.wait_peers(self.epoch, stream=stream)
+        self.model.dense(self.x0[self.epoch % 2], self.Bl, scores, stream=stream)
+        self.model.release_peers(self.epoch, stream=stream)
+        return scores
 
     def score(self, indices, offsets, dense_local, scores=None, stream=None):
         self.embed(indices, offsets, dense_local, stream)

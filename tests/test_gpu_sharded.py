@@ -66,31 +66,33 @@ def test_sharded_matches_unsharded(c3small, world):
 @pytest.mark.parametrize("world", [2, 4])
 def test_fused_exchange_v3_matches_unsharded(c3small, world):
     """V3 with N ranks emulated on one GPU: every rank's gather stores its pooled rows
-    straight into the owner's x0 through the peer-pointer table and signals the epoch flags; the ranks are
-    launched in sequence and only then wait (no kernel waits on another rank's), so the flags are already
-    set.  Each rank's x0 and scores must be bit-identical to the unsharded path (P11)."""
+    straight into the owner's x0 slot through the peer-pointer table and signals the ready flags; the ranks are
+    launched in sequence and only then wait (no kernel waits on a later launch), so the flags are already set.
+    Four epochs exercise both x0 slots and the free-slot handshake (epochs 3, 4 wait on epochs 1, 2's dense).
+    Each rank's x0 and scores must be bit-identical to the unsharded path (P11)."""
     from paper_2605_29232_b200.sharded import FusedShardedScorer, local_tables
     cfg, tabs, w, ref = c3small
     B = 256
     Bl = B // world
-    bt = cs.make_batch(cfg, 13, batch=B)
-    idx, off, dense = to_dev(bt)
-    x0_ref = ref.embed(idx, off, B, dense)
-    s_ref = ref.dense(x0_ref, B)
     ranks = [FusedShardedScorer(cfg, world, r, B, 1 << 20) for r in range(world)]
     for sc in ranks:
-        sc.connect(peers=([t.x0 for t in ranks], [t.flags for t in ranks]))
+        sc.connect(peers=ranks)
         sc.load_tables([tabs[t] for t in sc.tables])
         sc.load_weights({k: v.cuda() for k, v in w.items()})
-    for epoch in (1, 2):  # two batches: the epoch handshake advances
+    for epoch in (1, 2, 3, 4):
+        bt = cs.make_batch(cfg, 13 + epoch, batch=B)
+        idx, off, dense = to_dev(bt)
+        x0_ref = ref.embed(idx, off, B, dense)
+        s_ref = ref.dense(x0_ref, B)
         for r, sc in enumerate(ranks):
-            lb = cs.make_batch(cfg, 13, batch=B, tables=local_tables(cfg.n_tables, world, r))
+            lb = cs.make_batch(cfg, 13 + epoch, batch=B, tables=local_tables(cfg.n_tables, world, r))
             li, lo, _ = to_dev(lb)
             sc.embed(li, lo, dense[r * Bl:(r + 1) * Bl].contiguous())
         for r, sc in enumerate(ranks):
             s = sc.dense()
             torch.cuda.synchronize()
             assert sc.model.status() == 0
-            assert sc.epoch == epoch and int(sc.flags.min()) == epoch
-            assert torch.equal(sc.x0, x0_ref[r * Bl:(r + 1) * Bl]), f"rank {r}: x0 differs"
-            assert torch.equal(s, s_ref[r * Bl:(r + 1) * Bl]), f"rank {r}: scores differ"
+            assert sc.epoch == epoch and int(sc.ready.min()) == epoch
+            assert torch.equal(sc.x0[epoch % 2], x0_ref[r * Bl:(r + 1) * Bl]), f"epoch {epoch} rank {r}: x0 differs"
+            assert torch.equal(s, s_ref[r * Bl:(r + 1) * Bl]), f"epoch {epoch} rank {r}: scores differ"
+        assert all(int(sc.free.min()) == epoch for sc in ranks)

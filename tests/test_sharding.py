@@ -91,9 +91,9 @@ def _handle_worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2605_29232_b200.sharded import exchange_handles
-    blob = bytes([rank + 1]) * 64   # stands in for a CUDA IPC handle (64 bytes)
+    blob = bytes([rank + 1]) * 256   # stands in for 4 CUDA IPC handles (x0 slots 0/1, ready, free: 64 B each)
     got = exchange_handles(blob)
-    q.put((rank, got == [bytes([r + 1]) * 64 for r in range(world)]))
+    q.put((rank, got == [bytes([r + 1]) * 256 for r in range(world)]))
     dist.destroy_process_group()
 
 
