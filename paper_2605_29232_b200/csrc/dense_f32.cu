@@ -6,7 +6,8 @@
 //
 // True fp32 FFMA (no TF32: SURVEY.md A17, the 1e-5 gate).  One CTA owns R rows, keeps x0, x_l
 // and the next activation in shared memory, and reads the weights as W^T ([in][out], repacked
-// by cvr_load_weights) so the 256 threads of a CTA read one contiguous weight row per k.
+// by cvr_load_weights) so the 256 threads of a CTA read one contiguous weight row per k; each layer's
+// W^T is staged in shared memory by cp.async one layer ahead (double buffer).
 // Per-row work is independent of the batch (batch invariance).
 #include <algorithm>
 
@@ -15,7 +16,7 @@
 namespace cvr {
 namespace {
 
-constexpr int R = 4;  // rows per CTA (B = 256 -> 64 CTAs)
+constexpr int R = 2;  // rows per CTA (B = 256 -> 128 CTAs)
 
 __device__ __forceinline__ float sigmoid_f32(float z) {
   if (z >= 0.f) return 1.f / (1.f + expf(-z));
@@ -23,21 +24,30 @@ __device__ __forceinline__ float sigmoid_f32(float z) {
   return e / (1.f + e);
 }
 
-// out[r][j] = act(sum_k in[r][k] * WT[k][j] + bias[j]) (+ cross epilogue).  The layer's W^T is first
-// staged in shared memory with coalesced loads (one L2 round trip for the whole matrix instead of one
-// dependent load per k), then every thread runs its k loop on shared memory.
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// stage a layer's W^T [n_in][n_out] (workspace: 256-byte aligned) into shared memory with cp.async (one group)
+__device__ void stage(float* __restrict__ ws, const float* __restrict__ WT, int n) {
+  const int n4 = n >> 2;
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) cp_async16(ws + 4 * i, WT + 4 * i);
+  for (int i = 4 * n4 + threadIdx.x; i < n; i += blockDim.x) cp_async4(ws + i, WT + i);
+  cp_commit();
+}
+
+// out[r][j] = act(sum_k in[r][k] * WT[k][j] + bias[j]) (+ cross epilogue) from the staged W^T in ws
 template <bool CROSS>
 __device__ void layer(const float* __restrict__ in, int n_in, float* __restrict__ out, int n_out, int ld,
-                      const float* __restrict__ WT, const float* __restrict__ bias, const float* __restrict__ x0s,
-                      float* __restrict__ ws) {
-  const int n = n_in * n_out;
-  const int n4 = n >> 2;  // float4 body (WT is 256-byte aligned in the workspace), scalar tail
-  const float4* src4 = reinterpret_cast<const float4*>(WT);
-  float4* dst4 = reinterpret_cast<float4*>(ws);
-#pragma unroll 8
-  for (int i = threadIdx.x; i < n4; i += blockDim.x) dst4[i] = __ldg(src4 + i);
-  for (int i = 4 * n4 + threadIdx.x; i < n; i += blockDim.x) ws[i] = __ldg(WT + i);
-  __syncthreads();
+                      const float* __restrict__ ws, const float* __restrict__ bias, const float* __restrict__ x0s) {
   for (int j = threadIdx.x; j < n_out; j += blockDim.x) {
     float acc[R];
 #pragma unroll
@@ -59,12 +69,20 @@ __device__ void layer(const float* __restrict__ in, int n_in, float* __restrict_
   }
 }
 
-__global__ void __launch_bounds__(256) dense_f32_kernel(const DenseF32Args a, int ld) {
+// Weights of layer i + 1 stream into the second shared-memory buffer (cp.async) while layer i computes,
+// so a layer costs max(staging, math) rather than their sum.
+__global__ void __launch_bounds__(256) dense_f32_kernel(const DenseF32Args a, int ld, int wmax) {
   extern __shared__ float sm[];
   float* x0s = sm;
   float* bufA = sm + R * ld;
   float* bufB = sm + 2 * R * ld;
-  float* ws = sm + 3 * R * ld;  // staged weights of the current layer
+  float* wbuf[2] = {sm + 3 * R * ld, sm + 3 * R * ld + wmax};
+  const int n_layers = a.n_cross + a.n_mlp;
+  auto wt = [&](int i) { return i < a.n_cross ? a.WT[i] : a.MT[i - a.n_cross]; };
+  auto wn = [&](int i) {
+    return i < a.n_cross ? a.W * a.W : a.dims[i - a.n_cross] * a.dims[i - a.n_cross + 1];
+  };
+  if (n_layers > 0) stage(wbuf[0], wt(0), wn(0));
   const int row0 = blockIdx.x * R;
   for (int i = threadIdx.x; i < R * a.W; i += blockDim.x) {
     const int r = i / a.W, c = i - r * a.W;
@@ -72,17 +90,23 @@ __global__ void __launch_bounds__(256) dense_f32_kernel(const DenseF32Args a, in
     x0s[r * ld + c] = v;
     bufA[r * ld + c] = v;
   }
-  __syncthreads();
   float* cur = bufA;
   float* nxt = bufB;
-  for (int l = 0; l < a.n_cross; ++l) {
-    layer<true>(cur, a.W, nxt, a.W, ld, a.WT[l], a.bias[l], x0s, ws);
-    __syncthreads();
-    float* t = cur; cur = nxt; nxt = t;
-  }
-  for (int i = 0; i < a.n_mlp; ++i) {
-    layer<false>(cur, a.dims[i], nxt, a.dims[i + 1], ld, a.MT[i], a.mb[i], nullptr, ws);
-    __syncthreads();
+  for (int l = 0; l < n_layers; ++l) {
+    if (l + 1 < n_layers) {
+      stage(wbuf[(l + 1) & 1], wt(l + 1), wn(l + 1));
+      cp_wait<1>();  // this thread's copies of layer l have landed
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();  // everyone's copies of layer l (and the activations) are visible
+    if (l < a.n_cross) {
+      layer<true>(cur, a.W, nxt, a.W, ld, wbuf[l & 1], a.bias[l], x0s);
+    } else {
+      const int i = l - a.n_cross;
+      layer<false>(cur, a.dims[i], nxt, a.dims[i + 1], ld, wbuf[l & 1], a.mb[i], nullptr);
+    }
+    __syncthreads();  // layer l's weights and activations consumed before they are overwritten
     float* t = cur; cur = nxt; nxt = t;
   }
   const int hn = a.dims[a.n_mlp];
@@ -105,7 +129,8 @@ cudaError_t launch_dense_f32(const DenseF32Args& a, cudaStream_t s) {
   for (int i = 0; i <= a.n_mlp; ++i) ld = a.dims[i] > ld ? a.dims[i] : ld;
   for (int i = 0; i < a.n_mlp; ++i) wmax = std::max(wmax, (size_t)a.dims[i] * a.dims[i + 1]);
   ld = (ld + 3) & ~3;
-  const size_t smem = ((size_t)3 * R * ld + wmax) * sizeof(float);
+  wmax = (wmax + 3) & ~(size_t)3;  // keeps the second buffer 16-byte aligned
+  const size_t smem = ((size_t)3 * R * ld + 2 * wmax) * sizeof(float);
   if (smem > 220 * 1024) return cudaErrorInvalidValue;
   static size_t attr_set = 0;
   if (smem > 48 * 1024 && smem > attr_set) {
@@ -113,7 +138,7 @@ cudaError_t launch_dense_f32(const DenseF32Args& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set = smem;
   }
-  dense_f32_kernel<<<(a.B + R - 1) / R, 256, smem, s>>>(a, ld);
+  dense_f32_kernel<<<(a.B + R - 1) / R, 256, smem, s>>>(a, ld, (int)wmax);
   return cudaGetLastError();
 }
 
