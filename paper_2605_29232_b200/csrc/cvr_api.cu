@@ -180,6 +180,7 @@ struct cvr_ctx {
   // Measured on B200, c2 dense stage: 176 vs 90 us -- clusters of 8 only start when 8 SMs of a GPC are free
   // (CTA entry spread over ~10 us behind the previous kernel) and the mainloops got no faster
   bool mb = false;
+  bool pair_mlp = false;       // option "pair_mlp": 2-CTA tiles for the low-rank path's hidden MLP GEMMs
   // option "xv_splitk" [0]: t = x_l V^T as a K-split cluster GEMM (r == 256).  Measured on B200 at B = 4096:
   // its mainloop halves (3.5 vs 7 us) but the DSMEM exchange of the fp32 partials costs 2-6 us (element-wise
   // st.shared::cluster or cp.async.bulk shared::cluster alike): 92-100 us per dense stage vs 90 with tiles
@@ -830,6 +831,11 @@ int encode_plan(cvr_ctx* c) {
     if (head_mc) bn = c->mlp[i] / 4;  // the head's dot product spans the cluster's 4 tiles (DSMEM sum)
     ok &= addp("mlp/" + std::to_string(i) + "/W", c->mlp[i], K, bn, ep);
     c->plan.back().cn = head_mc ? 4 : (!last ? mc4(c->mlp[i], bn) : 1);
+    if (!last && c->pair_mlp && bn >= 128) {  // 2-CTA (cta_group::2) tiles: B box = BN/2 rows per CTA
+      GemmPlan& g = c->plan.back();
+      g.pair = true;
+      ok &= encode_tmap_bf16(&g.tmB, c->wptr("mlp/" + std::to_string(i) + "/W"), g.N, K, K, bn / 2, &er) == 0;
+    }
     K = c->mlp[i];
   }
   if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
@@ -1142,8 +1148,9 @@ GemmArgs gemm_args(cvr_ctx* c, const GemmPlan& g, const CUtensorMap* A, int M) {
   a.pdl = c->pdl;
   a.cta_pair = g.pair;
   {  // several tiles per CTA: the epilogue overlaps the next mainloop, keep the CTA small (Cfg::EPW)
-    const int64_t tiles = (int64_t)((M + 127) / 128) * (g.N / g.BN);
-    a.epw1 = c->epw_mode == 0 || (c->epw_mode == 2 && tiles > 2 * c->num_sms);
+    const int rows = g.pair ? 256 : 128, units = g.pair ? c->num_sms / 2 : c->num_sms;
+    const int64_t tiles = (int64_t)((M + rows - 1) / rows) * (g.N / g.BN);
+    a.epw1 = c->epw_mode == 0 || (c->epw_mode == 2 && tiles > 2 * units);
   }
   if (c->gdbg && c->gdbg_n < 32) a.dbg = c->gdbg + (size_t)(c->gdbg_n++) * 160 * 8;
   if (c->mb && g.mb8ok && g.cn <= 1 && !g.pair && !c->a_resident) {  // weight tiles multicast over 8 row blocks
@@ -1221,8 +1228,9 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     a.num_sms = c->num_sms;
     a.pdl = c->pdl;
     a.cta_pair = c->pair_ens;
-    const int64_t tiles = (int64_t)((M + 127) / 128) * (N / BN);
-    a.epw1 = c->epw_mode == 0 || (c->epw_mode == 2 && tiles > 2 * c->num_sms);
+    const int rows = c->pair_ens ? 256 : 128, units = c->pair_ens ? c->num_sms / 2 : c->num_sms;
+    const int64_t tiles = (int64_t)((M + rows - 1) / rows) * (N / BN);
+    a.epw1 = c->epw_mode == 0 || (c->epw_mode == 2 && tiles > 2 * units);
     return a;
   };
   (void)gp;
@@ -2058,6 +2066,13 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);  // U tile width
+    return CVR_OK;
+  }
+  if (!strcmp(key, "pair_mlp")) {
+    c->pair_mlp = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);
     return CVR_OK;
   }
   if (!strcmp(key, "mb")) {

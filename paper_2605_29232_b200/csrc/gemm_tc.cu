@@ -68,7 +68,7 @@ struct Cfg {
   static constexpr int RING_SLOTS = 3;
   // epilogue warps per TMEM lane quadrant: the epilogue of a CTA's last tile is exposed (one tile per CTA at
   // B = 4096), so plain stores split the tile's 64-column sub-tiles over up to 4 warps per quadrant
-  static constexpr bool SPLIT = (EPI == EPI_STORE || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS) && CG == 1 && CN == 1;
+  static constexpr bool SPLIT = (EPI == EPI_STORE || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS) && CN == 1;
   // EW caps the split: EW = 1 when each CTA runs several tiles (the epilogue then overlaps the next tile's
   // mainloop anyway) keeps the CTA at 7 warps, leaving registers for co-resident embedding CTAs
   static constexpr int EPW = RING ? 3 : (SPLIT ? (BN / 64 < EW ? BN / 64 : EW) : 1);
@@ -627,6 +627,17 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
 #undef CVR_MC
   if (cn > 1) return cudaErrorInvalidValue;
   // one epilogue warp per quadrant when every CTA runs several tiles (see Cfg::EPW)
+  if (g.epw1 && g.cta_pair && (g.epi == EPI_STORE || g.epi == EPI_BIAS_RELU || g.epi == EPI_BIAS)) {
+#define CVR_E1P(BN_, EPI_) \
+    if (g.BN == BN_ && g.epi == EPI_) return launch_t<BN_, EPI_, false, 2, 1, 1>(g, s);
+    CVR_E1P(128, EPI_STORE)
+    CVR_E1P(256, EPI_STORE)
+    CVR_E1P(128, EPI_BIAS_RELU)
+    CVR_E1P(256, EPI_BIAS_RELU)
+    CVR_E1P(128, EPI_BIAS)
+    CVR_E1P(256, EPI_BIAS)
+#undef CVR_E1P
+  }
   if (g.epw1 && !g.cta_pair && (g.epi == EPI_STORE || g.epi == EPI_BIAS_RELU || g.epi == EPI_BIAS)) {
 #define CVR_E1(BN_, EPI_) \
     if (g.BN == BN_ && g.epi == EPI_) return launch_t<BN_, EPI_, false, 1, 1, 1>(g, s);
