@@ -10,7 +10,7 @@ from typing import Dict, Optional, Sequence
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(HERE, "libcvr.so")
+lib_path = os.environ.get("CVR_LIB") or os.path.join(HERE, "libcvr.so")  # CVR_LIB: A/B of two builds (experiments)
 
 CVR_F32, CVR_BF16, CVR_F16 = 0, 1, 2
 CVR_DCN_FULL, CVR_DCN_LOWRANK, CVR_ENSEMBLE, CVR_MASKNET = 0, 1, 2, 3

@@ -181,6 +181,10 @@ struct cvr_ctx {
   // (CTA entry spread over ~10 us behind the previous kernel) and the mainloops got no faster
   bool mb = false;
   bool pair_mlp = false;       // option "pair_mlp": 2-CTA tiles for the low-rank path's hidden MLP GEMMs
+  // option "pair_xv" = BN: t = x_l V^T as 2-CTA 256 x BN tiles (0 = off).  Measured on B200 at B = 4096: 94.2 /
+  // 94.9 / 102.1 us per dense stage at BN = 64 / 128 / 256 vs 90.1 with 128 x 64 single-CTA tiles -- the
+  // mainloop is bound by each SM's TMA ingest (A k-block + B k-block per SM either way), not by MMA shape
+  int pair_xv = 0;
   // option "xv_splitk" [0]: t = x_l V^T as a K-split cluster GEMM (r == 256).  Measured on B200 at B = 4096:
   // its mainloop halves (3.5 vs 7 us) but the DSMEM exchange of the fp32 partials costs 2-6 us (element-wise
   // st.shared::cluster or cp.async.bulk shared::cluster alike): 92-100 us per dense stage vs 90 with tiles
@@ -811,6 +815,14 @@ int encode_plan(cvr_ctx* c) {
   for (int l = 0; l < c->n_cross; ++l) {
     ok &= addp("dcn/" + std::to_string(l) + "/V", c->r, (int)c->x0_ld, pick_bn(c->r), EPI_STORE);
     c->plan.back().cn = mc4(c->r, c->plan.back().BN);
+    if (c->pair_xv && c->r % c->pair_xv == 0) {  // 2-CTA (cta_group::2) tiles: B box = BN/2 rows per CTA
+      GemmPlan& g = c->plan.back();
+      g.pair = true;
+      g.BN = c->pair_xv;
+      g.cn = 1;
+      g.mb8ok = false;
+      ok &= encode_tmap_bf16(&g.tmB, c->wptr("dcn/" + std::to_string(l) + "/V"), g.N, g.K, g.K, g.BN / 2, &er) == 0;
+    }
     // U GEMM: 192-wide tiles (EIN-ring epilogue) when W allows -- 1/3 of the t re-reads of 64-wide tiles
     // (measured 4096x1728x256: 7.4 us at BN = 192 vs 10.3 at 64); the K5 / stack / resident-A variants
     // read U through 64-row boxes
@@ -2066,6 +2078,14 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);  // U tile width
+    return CVR_OK;
+  }
+  if (!strcmp(key, "pair_xv")) {
+    if (value != 0 && value != 64 && value != 128 && value != 256) return c->fail(CVR_E_ARG, "pair_xv: 0, 64, 128 or 256");
+    c->pair_xv = (int)value;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);
     return CVR_OK;
   }
   if (!strcmp(key, "pair_mlp")) {

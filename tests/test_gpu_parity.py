@@ -329,3 +329,22 @@ def test_c2_pair_mlp_bitexact(c2, B):
     finally:
         m.set_option("pair_mlp", 0)
     assert torch.equal(s0, s1)
+
+
+@pytest.mark.parametrize("bn", [64, 128, 256])
+@pytest.mark.parametrize("B", [4096, 333])
+def test_c2_pair_xv_bitexact(c2, B, bn):
+    """Option pair_xv: t = x_l V^T as 2-CTA (cta_group::2) 256 x BN tiles; same MMAs per output element in the
+    same K order -> bit-identical scores."""
+    cfg, m, tabs, w = c2
+    bt = cs.make_batch(cfg, 62, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    s0 = m.dense(x0, B).clone()
+    m.set_option("pair_xv", bn)
+    try:
+        s1 = m.dense(x0, B).clone()
+    finally:
+        m.set_option("pair_xv", 0)
+    assert torch.equal(s0, s1)
+
