@@ -142,38 +142,60 @@ FP32_SIMT_TFLOPS = 148 * 128 * 2 * 1.965 / 1e3  # FP32 lanes x FMA x max SM cloc
 
 
 def launch_work(cfg, B) -> dict:
-    """Algorithmic work of ONE launch of each kernel role for batch B: (bound, amount), amount in FLOPs
-    (2 per MAC) for tensor / alu roles."""
+    """Algorithmic work of ONE launch of each kernel role for batch B: {"flops", "bytes", "alu"}.  FLOPs count
+    2 per MAC; bytes count every operand read once and every output written once (bf16 = 2 B,
+    fp32 biases / LN affine / fp32 partials = 4 B) -- the traffic a kernel cannot avoid.  The roofline bound of a
+    role is the larger of flops / tensor peak and bytes / HBM peak (pick_bound); "alu" roles are fp32 SIMT."""
     W, r = cfg.width, cfg.cross_rank
     mask = cfg.backbone == "masknet"
+    ens = cfg.backbone == "ensemble"
     Wp = getattr(cfg, "cross_width", 0) or W
     nb = getattr(cfg, "n_parallel", 1) * cfg.n_cross
     dims = [getattr(cfg, "n_parallel", 1) * Wp if mask else W] + list(cfg.mlp_dims)
-    hidden = [2 * B * dims[i] * dims[i + 1] for i in range(len(cfg.mlp_dims) - 1)]
-    w = {"gemm_mlp_relu": ("tensor", sum(hidden) / max(1, len(hidden))),
-         "gemm_mlp_head": ("tensor", 2 * B * dims[-2] * dims[-1] + 2 * B * dims[-1]),
-         "head_finalize": ("alu", 2 * B * max(1, dims[-1] // 256))}
+    nh = len(cfg.mlp_dims) - 1
+    hid_f = [2 * B * dims[i] * dims[i + 1] for i in range(nh)]
+    hid_b = [2 * (B * dims[i] + dims[i] * dims[i + 1] + B * dims[i + 1]) + 4 * dims[i + 1] for i in range(nh)]
+    avg = lambda xs: sum(xs) / max(1, len(xs))  # noqa: E731
+
+    def g(flops, nbytes, alu=False):
+        return {"flops": float(flops), "bytes": float(nbytes), "alu": alu}
+
+    w = {"gemm_mlp_relu": g(avg(hid_f), avg(hid_b)),
+         "gemm_mlp_head": g(2 * B * dims[-2] * dims[-1] + 2 * B * dims[-1],
+                            2 * (B * dims[-2] + dims[-2] * dims[-1]) + 8 * dims[-1] + 4 * B),
+         "head_finalize": g(2 * B * max(1, dims[-1] // 256), 4 * B * (max(1, dims[-1] // 256) + 1), alu=True)}
     if cfg.backbone == "dcn_full":
-        w["dense_f32_dcn"] = ("alu", 2 * B * (cfg.n_cross * W * W + sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1))
-                                              + dims[-1]))
+        fl = 2 * B * (cfg.n_cross * W * W + sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1)) + dims[-1])
+        wb = 4 * (cfg.n_cross * (W * W + W) + sum(dims[i] * dims[i + 1] + dims[i + 1] for i in range(len(dims) - 1)))
+        w["dense_f32_dcn"] = g(fl, 4 * B * W + wb + 4 * B, alu=True)
     elif mask:  # MaskNet (SURVEY.md §8(f) #1): projection, all blocks' mask hiddens, one mask GEMM per block
-        w["gemm_mask_proj"] = ("tensor", 2 * B * W * Wp)
-        w["gemm_mask_hidden"] = ("tensor", 2 * B * Wp * nb * r)
-        w["gemm_mask_mul"] = ("tensor", 2 * B * r * Wp)
+        w["gemm_mask_proj"] = g(2 * B * W * Wp, 2 * (B * W + W * Wp + B * Wp) + 4 * Wp)
+        w["gemm_mask_hidden"] = g(2 * B * Wp * nb * r, 2 * (B * Wp + Wp * nb * r + B * nb * r) + 4 * nb * r)
+        w["gemm_mask_mul"] = g(2 * B * r * Wp, 2 * (B * r + r * Wp + 2 * B * Wp) + 4 * Wp)
     else:
-        w["gemm_xV"] = ("tensor", 2 * B * W * r)
-        w["gemm_tU_cross"] = ("tensor", 2 * B * r * W)
-        w["cross_fused"] = ("tensor", 4 * B * W * r)
-        w["cross_stack"] = ("tensor", cfg.n_cross * 4 * B * W * r)
-    if cfg.backbone == "ensemble":
+        out_b = 4 if ens else 2  # c4's DCN branch writes the fp32 branch sum (A26)
+        w["gemm_xV"] = g(2 * B * W * r, 2 * (B * W + r * W + B * r))
+        w["gemm_tU_cross"] = g(2 * B * r * W, 2 * (B * r + W * r + 2 * B * W) + out_b * B * W + 4 * W)
+        w["cross_fused"] = g(4 * B * W * r, 2 * (2 * r * W + 3 * B * W) + 4 * W)
+        w["cross_stack"] = g(cfg.n_cross * 4 * B * W * r, 2 * (cfg.n_cross * 2 * r * W + (cfg.n_cross + 1) * B * W))
+    if ens:
         S, D, F, H = cfg.n_tables, cfg.dim, cfg.ffn_dim, cfg.n_heads
         BT = B * S
-        w.update({"gemm_ens_qkv": ("tensor", 2 * BT * D * 3 * D), "gemm_ens_oproj": ("tensor", 2 * BT * D * D),
-                  "gemm_ens_ffn1": ("tensor", 2 * BT * D * F),
-                  # out-projection and FFN2 run as one GEMM over [O | h] (K = D + F)
-                  "gemm_ens_ffn2_ln": ("tensor", 2 * BT * (F + D) * D),
-                  "mha64": ("tensor", 4 * B * H * S * S * (D // H))})
+        w.update({"gemm_ens_qkv": g(2 * BT * D * 3 * D, 2 * (BT * D + 3 * D * D + 3 * BT * D) + 12 * D),
+                  "gemm_ens_oproj": g(2 * BT * D * D, 2 * (BT * D + D * D) + 8 * BT * D + 4 * D),
+                  "gemm_ens_ffn1": g(2 * BT * D * F, 2 * (BT * D + D * F + BT * F) + 4 * F),
+                  # out-projection and FFN2 run as one GEMM over [O | h] (K = D + F), + fp32 branch sum, LN
+                  "gemm_ens_ffn2_ln": g(2 * BT * (F + D) * D, 2 * (BT * (F + D) + (F + D) * D + BT * D)
+                                        + 4 * BT * D + 12 * D),
+                  "mha64": g(4 * B * H * S * S * (D // H), 2 * (3 * BT * D + BT * D))})
     return w
+
+
+def pick_bound(work: dict, tensor_peak_tflops: float, hbm_gbs: float) -> str:
+    """Roofline bound of one kernel role: the resource whose peak gives the larger minimum time."""
+    if work["alu"]:
+        return "alu"
+    return "tensor" if work["flops"] / (tensor_peak_tflops * 1e12) >= work["bytes"] / (hbm_gbs * 1e9) else "hbm"
 
 
 def dense_flops_per_example(cfg) -> int:
@@ -182,13 +204,14 @@ def dense_flops_per_example(cfg) -> int:
     layer_roles = ["gemm_xV", "gemm_tU_cross"] + (["gemm_ens_qkv", "gemm_ens_ffn1",
                                                     "gemm_ens_ffn2_ln", "mha64"] if cfg.backbone == "ensemble" else [])
     if cfg.backbone == "dcn_full":
-        return int(w["dense_f32_dcn"][1])
+        return int(w["dense_f32_dcn"]["flops"])
     n_hidden = len(cfg.mlp_dims) - 1
     if cfg.backbone == "masknet":
         nb = cfg.n_parallel * cfg.n_cross
-        return int(w["gemm_mask_proj"][1] + w["gemm_mask_hidden"][1] + nb * w["gemm_mask_mul"][1]
-                   + n_hidden * w["gemm_mlp_relu"][1] + w["gemm_mlp_head"][1])
-    return int(cfg.n_cross * sum(w[k][1] for k in layer_roles) + n_hidden * w["gemm_mlp_relu"][1] + w["gemm_mlp_head"][1])
+        return int(w["gemm_mask_proj"]["flops"] + w["gemm_mask_hidden"]["flops"] + nb * w["gemm_mask_mul"]["flops"]
+                   + n_hidden * w["gemm_mlp_relu"]["flops"] + w["gemm_mlp_head"]["flops"])
+    return int(cfg.n_cross * sum(w[k]["flops"] for k in layer_roles) + n_hidden * w["gemm_mlp_relu"]["flops"]
+               + w["gemm_mlp_head"]["flops"])
 
 
 WORKLOADS = {
@@ -429,12 +452,20 @@ def run_cvr(args, cfg):
             kernels[name] = {"bound": "hbm", "avg_us": st["avg_ms"] * 1e3, "launches": st["launches"],
                              "achieved": ach, "unit": "GB/s", "frac": ach / pk["hbm"], "algorithmic_bytes": ebytes}
         else:
-            bound, per = work[name]
-            ach = per / avg_s / 1e12
-            peak = bf16_peak if bound == "tensor" else FP32_SIMT_TFLOPS
-            kernels[name] = {"bound": bound, "avg_us": st["avg_ms"] * 1e3, "launches": st["launches"],
-                             "achieved": ach, "unit": "TFLOP/s", "frac": ach / peak, "flops_per_launch": per,
-                             "peak": peak}
+            wk = work[name]
+            bound = pick_bound(wk, bf16_peak, pk["hbm"])
+            if bound == "hbm":  # arithmetic intensity below the ridge point: bytes / HBM peak bounds it
+                ach = wk["bytes"] / avg_s / 1e9
+                kernels[name] = {"bound": bound, "avg_us": st["avg_ms"] * 1e3, "launches": st["launches"],
+                                 "achieved": ach, "unit": "GB/s", "frac": ach / pk["hbm"], "peak": pk["hbm"],
+                                 "algorithmic_bytes": wk["bytes"], "flops_per_launch": wk["flops"],
+                                 "tensor_frac": wk["flops"] / avg_s / 1e12 / bf16_peak}
+            else:
+                ach = wk["flops"] / avg_s / 1e12
+                peak = bf16_peak if bound == "tensor" else FP32_SIMT_TFLOPS
+                kernels[name] = {"bound": bound, "avg_us": st["avg_ms"] * 1e3, "launches": st["launches"],
+                                 "achieved": ach, "unit": "TFLOP/s", "frac": ach / peak, "peak": peak,
+                                 "flops_per_launch": wk["flops"], "algorithmic_bytes": wk["bytes"]}
     share = {k: v["total_ms"] / max(1e-9, sum(s["total_ms"] for s in kstats.values())) for k, v in kstats.items()}
     dom = max(kstats, key=lambda k: kstats[k]["total_ms"])
     dk = kernels[dom]
@@ -449,7 +480,10 @@ def run_cvr(args, cfg):
                 "peak_source": (f"MEASURED_PEAKS.json ({pk['source']}; bf16 sustained for kernels inside the step)"
                                 if dk["bound"] != "alu" else
                                 "derived: 148 SMs x 128 FP32 lanes x 2 FLOP/FMA x 1.965 GHz (DESIGN.md §6)"),
-                "share_of_kernel_time": share[dom]}
+                "share_of_kernel_time": share[dom],
+                "bound_rule": "roofline: the larger of flops / bf16 peak and algorithmic bytes / HBM peak "
+                              "(bench.launch_work, DESIGN.md §6)",
+                "flops_per_launch": dk.get("flops_per_launch"), "algorithmic_bytes": dk.get("algorithmic_bytes")}
     dense_ms = sum(v["total_ms"] for k, v in kstats.items() if k != "embed_bag_pool") / args.steps
     dense_ach = dense_flops_per_example(cfg) * B / (dense_ms / 1e3) / 1e12
 

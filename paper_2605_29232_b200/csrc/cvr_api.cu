@@ -185,6 +185,7 @@ struct cvr_ctx {
   // 94.9 / 102.1 us per dense stage at BN = 64 / 128 / 256 vs 90.1 with 128 x 64 single-CTA tiles -- the
   // mainloop is bound by each SM's TMA ingest (A k-block + B k-block per SM either way), not by MMA shape
   int pair_xv = 0;
+  int xv_bn = 0;               // option "xv_bn": N tile of t = x_l V^T (0 = by wave count, see pick_bn_xv)
   // option "xv_splitk" [0]: t = x_l V^T as a K-split cluster GEMM (r == 256).  Measured on B200 at B = 4096:
   // its mainloop halves (3.5 vs 7 us) but the DSMEM exchange of the fp32 partials costs 2-6 us (element-wise
   // st.shared::cluster or cp.async.bulk shared::cluster alike): 92-100 us per dense stage vs 90 with tiles
@@ -406,6 +407,27 @@ int pick_bn(int N, int64_t M = 0) {
   if (N % 256 == 0 && N > 256 && mt * (N / 256) >= 100) return 256;
   if (N > 256 && N % 128 == 0) return 128;
   return 64;
+}
+
+// N tile of t = x_l V^T (N = r, small): pick the tile minimising waves x k-block cost.  Measured per 128 x BN x 64
+// k-block on B200 (per-SM ingest / small-N MMA bound): ~211 ns at BN = 64, ~280 ns at 256 -- 64-wide tiles
+// win while they fit one wave (c2: 128 tiles), full-width tiles once the row blocks alone fill the SMs.
+int pick_bn_xv(int N, int64_t M, int num_sms) {
+  const int64_t mt = (M + 127) / 128;
+  double best = 1e30;
+  int bn = 64;
+  const int cand[3] = {64, 128, 256};
+  const double cost[3] = {211, 240, 280};
+  for (int i = 0; i < 3; ++i) {
+    if (N % cand[i]) continue;
+    const int64_t tiles = mt * (N / cand[i]);
+    const double t = (double)((tiles + num_sms - 1) / num_sms) * cost[i];
+    if (t < best - 1e-9) {
+      best = t;
+      bn = cand[i];
+    }
+  }
+  return bn;
 }
 
 }  // namespace
@@ -813,7 +835,8 @@ int encode_plan(cvr_ctx* c) {
   // already merged in L2), so option mc = 1 (default) clusters only the head, mc = 2 every grouped GEMM.
   auto mc4 = [&](int N, int BN) { return c->mc >= 2 && N % (4 * BN) == 0 && N / BN <= 8 ? 4 : 1; };
   for (int l = 0; l < c->n_cross; ++l) {
-    ok &= addp("dcn/" + std::to_string(l) + "/V", c->r, (int)c->x0_ld, pick_bn(c->r), EPI_STORE);
+    const int bn_v = c->xv_bn ? c->xv_bn : pick_bn_xv(c->r, c->max_batch, c->num_sms > 0 ? c->num_sms : 148);
+    ok &= addp("dcn/" + std::to_string(l) + "/V", c->r, (int)c->x0_ld, bn_v, EPI_STORE);
     c->plan.back().cn = mc4(c->r, c->plan.back().BN);
     if (c->pair_xv && c->r % c->pair_xv == 0) {  // 2-CTA (cta_group::2) tiles: B box = BN/2 rows per CTA
       GemmPlan& g = c->plan.back();
@@ -2078,6 +2101,14 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);  // U tile width
+    return CVR_OK;
+  }
+  if (!strcmp(key, "xv_bn")) {
+    if (value != 0 && value != 64 && value != 128 && value != 256) return c->fail(CVR_E_ARG, "xv_bn: 0, 64, 128 or 256");
+    c->xv_bn = (int)value;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);
     return CVR_OK;
   }
   if (!strcmp(key, "pair_xv")) {

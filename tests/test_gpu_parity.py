@@ -348,3 +348,21 @@ def test_c2_pair_xv_bitexact(c2, B, bn):
         m.set_option("pair_xv", 0)
     assert torch.equal(s0, s1)
 
+
+
+@pytest.mark.parametrize("bn", [128, 256])
+def test_c2_xv_bn_bitexact(c2, bn):
+    """Option xv_bn (the xV N tile; the default picks it by wave count, pick_bn_xv): every tile width runs the
+    same K order per output element -> bit-identical scores, ragged batch included."""
+    cfg, m, tabs, w = c2
+    for B in (4096, 333):
+        bt = cs.make_batch(cfg, 64, batch=B)
+        idx, off, dense = to_dev(bt)
+        x0 = m.embed(idx, off, B, dense)
+        s0 = m.dense(x0, B).clone()
+        m.set_option("xv_bn", bn)
+        try:
+            s1 = m.dense(x0, B).clone()
+        finally:
+            m.set_option("xv_bn", 0)
+        assert torch.equal(s0, s1)
