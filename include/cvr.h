@@ -247,7 +247,8 @@ int cvr_set_option(cvr_ctx* ctx, const char* key, int64_t value);
 /* -- utility ----------------------------------------------------------------------------------
  * C[M, N] = A[M, K] . B[N, K]^T on the same tcgen05/TMA kernel the dense stage uses (tests and
  * tile tuning): bf16 row-major operands with leading dimensions lda/ldb/ldc (elements, multiples
- * of 8), fp32 accumulation, bf16 output; epi 0 = plain store, 1 = ReLU(C + bias[N]) (fp32 bias).
+ * of 8), fp32 accumulation, bf16 output; epi 0 = plain store, 1 = ReLU(C + bias[N]) (fp32 bias, 16-byte
+ * aligned, else CVR_E_ARG).
  * K % 64 == 0, N % bn == 0, bn in {64, 128, 256}; epi | 0x100 selects the 2-CTA (cta_group::2, 256-row
  * tile per CTA pair) variant.  Enqueued on `stream`. */
 int cvr_gemm_bf16(const void* d_A, int64_t lda, const void* d_B, int64_t ldb, void* d_C, int64_t ldc, int M, int N,

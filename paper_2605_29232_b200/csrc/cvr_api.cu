@@ -2018,6 +2018,7 @@ int cvr_gemm_bf16(const void* d_A, int64_t lda, const void* d_B, int64_t ldb, vo
   const bool pair = (epi & 0x100) != 0;
   epi &= 0xFF;
   if (!d_A || !d_B || !d_C || M < 0 || N <= 0 || K <= 0 || (epi == 1 && !d_bias)) return CVR_E_ARG;
+  if (d_bias && (reinterpret_cast<uintptr_t>(d_bias) & 15)) return CVR_E_ARG;  // read as float4
   if (epi != 0 && epi != 1) return CVR_E_ARG;
   if (K % 64 || N % bn || (bn != 64 && bn != 128 && bn != 256 && !(bn == 192 && epi == 0 && !pair)) || lda < K || ldb < K || ldc < N || (lda | ldb | ldc) & 7)
     return CVR_E_UNSUPPORTED;

@@ -458,13 +458,27 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
           float v[32];
           ld32_tmem(trow + c, v);
           const int n = n0 + c;
-          if constexpr (T::kBias) {
+          if constexpr (T::kBias) {  // bias / head weights: fp32, 16-byte aligned (workspace slots; cvr.h)
+            const float4* b4 = reinterpret_cast<const float4*>(g.bias + n);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += __ldg(g.bias + n + j);
+            for (int u = 0; u < 8; ++u) {
+              const float4 bb = __ldg(b4 + u);
+              v[4 * u] += bb.x;
+              v[4 * u + 1] += bb.y;
+              v[4 * u + 2] += bb.z;
+              v[4 * u + 3] += bb.w;
+            }
           }
           if constexpr (EPI == EPI_HEAD || EPI == EPI_HEAD_PARTIAL) {
+            const float4* h4 = reinterpret_cast<const float4*>(g.head_w + n);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) z = fmaf(fmaxf(v[j], 0.f), __ldg(g.head_w + n + j), z);
+            for (int u = 0; u < 8; ++u) {
+              const float4 hw = __ldg(h4 + u);
+              z = fmaf(fmaxf(v[4 * u], 0.f), hw.x, z);
+              z = fmaf(fmaxf(v[4 * u + 1], 0.f), hw.y, z);
+              z = fmaf(fmaxf(v[4 * u + 2], 0.f), hw.z, z);
+              z = fmaf(fmaxf(v[4 * u + 3], 0.f), hw.w, z);
+            }
           } else if constexpr (EPI == EPI_BIAS_ADD_F32) {
             if (live) {
               float x[32];
