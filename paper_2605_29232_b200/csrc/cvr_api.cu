@@ -185,11 +185,14 @@ struct cvr_ctx {
   // 94.9 / 102.1 us per dense stage at BN = 64 / 128 / 256 vs 90.1 with 128 x 64 single-CTA tiles -- the
   // mainloop is bound by each SM's TMA ingest (A k-block + B k-block per SM either way), not by MMA shape
   int pair_xv = 0;
-  int xv_bn = 0;               // option "xv_bn": N tile of t = x_l V^T (0 = by wave count, see pick_bn_xv)
+  int xv_bn = 0;
+  bool prefetch_b = true;      // option "prefetch_b": weight k-blocks issued before the dependency wait               // option "xv_bn": N tile of t = x_l V^T (0 = by wave count, see pick_bn_xv)
   // option "xv_splitk" [0]: t = x_l V^T as a K-split cluster GEMM (r == 256).  Measured on B200 at B = 4096:
   // its mainloop halves (3.5 vs 7 us) but the DSMEM exchange of the fp32 partials costs 2-6 us (element-wise
   // st.shared::cluster or cp.async.bulk shared::cluster alike): 92-100 us per dense stage vs 90 with tiles
-  bool xv_splitk = false;
+  // xv_splitk = 2: the same with the partials exchanged through an L2-resident global scratch (off_xchg)
+  int xv_splitk = 0;
+  size_t off_xchg = 0;
   int add_q(const CUtensorMap* full, const void* ptr, int64_t rows, int64_t cols, int64_t ld, const char** er) {
     return encode_tmap_bf16(&qmaps[full], ptr, rows, cols, ld, 32, er);
   }
@@ -515,6 +518,7 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
     c->off_stack_done = carve(cur, sizeof(int) * 2 * kMaxLayers * ((B + 127) / 128));
     if (c->r == 256) {  // K5 scratch; K5 itself is opt-in ("fused_cross"): measured slower than 2 GEMMs at B=4096
       c->off_part = carve(cur, cross_fused_partial_bytes(c->max_batch));
+      c->off_xchg = carve(cur, (size_t)((B + 127) / 128) * 16 * 128 * 64 * 4);  // split-K xV exchange (GX)
     }
     for (int i = 0; i + 1 < c->n_mlp; ++i) c->off_h.push_back(carve(cur, (size_t)B * c->mlp[i] * 2));
   } else if (c->backbone == CVR_ENSEMBLE) {
@@ -1182,6 +1186,7 @@ GemmArgs gemm_args(cvr_ctx* c, const GemmPlan& g, const CUtensorMap* A, int M) {
   a.num_sms = c->num_sms;
   a.pdl = c->pdl;
   a.cta_pair = g.pair;
+  a.no_prefetch_b = !c->prefetch_b;
   {  // several tiles per CTA: the epilogue overlaps the next mainloop, keep the CTA small (Cfg::EPW)
     const int rows = g.pair ? 256 : 128, units = g.pair ? c->num_sms / 2 : c->num_sms;
     const int64_t tiles = (int64_t)((M + rows - 1) / rows) * (g.N / g.BN);
@@ -1255,6 +1260,7 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     GemmArgs a{};
     a.tmA = A;
     a.tmB = Bm;
+    a.no_prefetch_b = !c->prefetch_b;
     a.M = M;
     a.N = N;
     a.K = K;
@@ -1522,6 +1528,7 @@ int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, const CUtenso
       av.tmB = &c->tm_v256[l];
       av.out_bf16 = c->at<__nv_bfloat16>(c->off_t);
       av.ld_x = c->r;
+      av.partial = c->xv_splitk == 2 ? c->at<float>(c->off_xchg) : nullptr;
       if (av.dbg) c->gdbg_kid.push_back(K_GEMM_V);
       c->pbeg(s);
       e = launch_gemm_splitk(av, s);
@@ -2104,6 +2111,12 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);  // U tile width
     return CVR_OK;
   }
+  if (!strcmp(key, "prefetch_b")) {
+    c->prefetch_b = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    return CVR_OK;
+  }
   if (!strcmp(key, "xv_bn")) {
     if (value != 0 && value != 64 && value != 128 && value != 256) return c->fail(CVR_E_ARG, "xv_bn: 0, 64, 128 or 256");
     c->xv_bn = (int)value;
@@ -2153,7 +2166,8 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     return CVR_OK;
   }
   if (!strcmp(key, "xv_splitk")) {
-    c->xv_splitk = value != 0;
+    if (value < 0 || value > 2) return c->fail(CVR_E_ARG, "xv_splitk: 0, 1 (DSMEM) or 2 (L2 exchange)");
+    c->xv_splitk = (int)value;
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     return CVR_OK;

@@ -124,6 +124,7 @@ struct GemmArgs {
   int group_n;               // EPI_MASK grouped over branches: N tiles of group g = n / group_n read A columns
                              // [g K, (g + 1) K) and x_l columns n - g group_n (0 = off)
   int cn;                    // 4: clusters of 4 CTAs along N multicast A (tmA box = {64, 32}); 0/1: off
+  bool no_prefetch_b;        // do not issue the first ring stages' B (weight) loads before griddepcontrol.wait
   unsigned long long* dbg;   // optional per-CTA timeline [grid][8] (%globaltimer ns): entry, deps ready,
                              // first stage landed, last MMA issued, first accumulator, epilogue done, exit
 };

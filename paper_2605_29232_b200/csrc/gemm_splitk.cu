@@ -54,9 +54,15 @@ __device__ __forceinline__ void bulk_s2c(uint32_t dst_cluster, const void* src, 
       : "memory");
 }
 
+// GX (global exchange): the partial slices go through an L2-resident global scratch instead of DSMEM -- each
+// epilogue warp stores its peers' slices straight from registers in a chunk-major layout (coalesced), one
+// cluster barrier (release / acquire, cluster scope) orders them before the owners' loads.
+// xchg layout: [row block][src rank][dst rank][16 float4 chunks][128 rows] (diagonal unused).
+template <bool GX>
 __global__ void __launch_bounds__(NT, 1)
     gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                       __nv_bfloat16* __restrict__ out, int64_t ldo, int M, int K, unsigned long long* dbg) {
+                       __nv_bfloat16* __restrict__ out, int64_t ldo, int M, int K, float4* __restrict__ xchg,
+                       unsigned long long* dbg) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -91,7 +97,7 @@ __global__ void __launch_bounds__(NT, 1)
   ptx::tc_fence_before();
   ptx::cluster_sync();
   ptx::tc_fence_after();
-  if (threadIdx.x == 0) ptx::mbar_arrive_expect_tx(rfull, (KS - 1) * SLOT);
+  if (!GX && threadIdx.x == 0) ptx::mbar_arrive_expect_tx(rfull, (KS - 1) * SLOT);
   const uint32_t tmem = *tmem_holder;
   auto stamp = [&](int i) {
     if (dbg && threadIdx.x == 2 * 32) {
@@ -140,14 +146,35 @@ __global__ void __launch_bounds__(NT, 1)
     ptx::mbar_wait(tfull, 0);  // this CTA's partial is complete (and its ring no longer read)
     stamp(3);
   }
+  const bool epi = warp >= 2 && warp < PRODUCER_B;
+  const int q = warp & 3, part = (warp - 2) >> 2, r = q * 32 + lane;
+  const int64_t rb = blockIdx.x / KS;
+  if constexpr (GX) {
+    // ---------------------------------------------------------------- exchange through L2
+    if (epi && part != j) {
+      float4* dst = xchg + ((rb * KS + j) * KS + part) * (16 * BM);
+      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + part * 64;
+#pragma unroll
+      for (int c = 0; c < 64; c += 32) {
+        float v[32];
+        tile::ld32_tmem(trow + c, v);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          __stcg(dst + ((c >> 2) + u) * BM + r, make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]));
+      }
+    }
+    stamp(2);
+    ptx::tc_fence_before();
+    ptx::cluster_sync();  // release / acquire at cluster scope: every peer's slices are in L2
+    ptx::tc_fence_after();
+    stamp(5);
+  } else {
   ptx::tc_fence_before();
   ptx::cluster_sync();  // every CTA of the cluster has drained its ring: receive slots may be written
   ptx::tc_fence_after();
   stamp(4);
 
   // ---------------------------------------------------------------- exchange: partial columns -> owners
-  const bool epi = warp >= 2 && warp < PRODUCER_B;
-  const int q = warp & 3, part = (warp - 2) >> 2, r = q * 32 + lane;
   if (epi && part != j) {
     // columns [64 part, 64 part + 64) of rows 32q..32q+31 belong to CTA `part`: stage them in send slot part
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + part * 64;
@@ -175,6 +202,7 @@ __global__ void __launch_bounds__(NT, 1)
   stamp(2);
   if (epi) ptx::mbar_wait_cluster(rfull, 0);  // the peers' slices for our columns have landed
   stamp(5);
+  }
 
   // ---------------------------------------------------------------- reduce own 64 columns, bf16 out
   if (epi) {
@@ -198,9 +226,10 @@ __global__ void __launch_bounds__(NT, 1)
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int src = 0; src < KS; ++src) {  // fixed order 0 + 1 + 2 + 3 (the first add is exact)
-          const float4 p = src == j ? own[u]
-                                    : *reinterpret_cast<const float4*>(smem + RECV + slot_of(src, j) * SLOT +
-                                                                       (ch * BM + r) * 16);
+          float4 p;
+          if (src == j) p = own[u];
+          else if constexpr (GX) p = __ldcg(xchg + ((rb * KS + src) * KS + j) * (16 * BM) + ch * BM + r);
+          else p = *reinterpret_cast<const float4*>(smem + RECV + slot_of(src, j) * SLOT + (ch * BM + r) * 16);
           acc.x += p.x;
           acc.y += p.y;
           acc.z += p.z;
@@ -226,7 +255,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
   }
   stamp(6);
-  if (warp == 2 && lane == 0) ptx::bulk_wait_read<0>();  // our outgoing slices have been read
+  if (!GX && warp == 2 && lane == 0) ptx::bulk_wait_read<0>();  // our outgoing slices have been read
   __syncthreads();
   if (warp == 1) ptx::tmem_dealloc(tmem, BN);
 }
@@ -238,7 +267,8 @@ cudaError_t launch_gemm_splitk(const GemmArgs& g, cudaStream_t s) {
   if (g.N != BN || g.K % BK || g.K / BK < KS || !g.out_bf16 || g.ld_x < BN) return cudaErrorInvalidValue;
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_splitk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaError_t e = cudaFuncSetAttribute(gemm_splitk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(gemm_splitk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
@@ -256,7 +286,10 @@ cudaError_t launch_gemm_splitk(const GemmArgs& g, cudaStream_t s) {
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, gemm_splitk_kernel, *g.tmA, *g.tmB, g.out_bf16, g.ld_x, g.M, g.K, g.dbg);
+  float4* xchg = reinterpret_cast<float4*>(g.partial);  // non-null: exchange through L2 (GX)
+  if (xchg)
+    return cudaLaunchKernelEx(&cfg, gemm_splitk_kernel<true>, *g.tmA, *g.tmB, g.out_bf16, g.ld_x, g.M, g.K, xchg, g.dbg);
+  return cudaLaunchKernelEx(&cfg, gemm_splitk_kernel<false>, *g.tmA, *g.tmB, g.out_bf16, g.ld_x, g.M, g.K, xchg, g.dbg);
 }
 
 }  // namespace cvr

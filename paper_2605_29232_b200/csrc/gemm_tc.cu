@@ -213,6 +213,27 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
   if (threadIdx.x == 0) stamp(g.dbg, 0);
+  // B k-blocks of one tile (weights: never written by the previous kernel)
+  auto issue_b = [&](int s, int kb, int n0) {
+    if constexpr (CG == 2) {
+      if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * C::B_BYTES);
+      ptx::tma_load_2d_cg2(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0 + rank * (BN / 2));
+    } else {
+      ptx::mbar_arrive_expect_tx(&full[s], C::B_BYTES);
+      if constexpr (MB)
+        ptx::tma_load_2d_mc(sB + s * C::B_BYTES + crank * (BN / CN) * 128, &tmB, &full[s], kb * BK,
+                            n0 + crank * (BN / CN), kMask);
+      else
+        ptx::tma_load_2d(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);
+    }
+  };
+  // Weight prefetch: the first ring stages' B k-blocks are issued BEFORE griddepcontrol.wait, i.e. while the
+  // previous kernel is still draining; only A (and the epilogue inputs) wait for it
+  int npre = 0;
+  if (!g.no_prefetch_b && !MB && warp == C::PRODUCER_B && lane == 0 && t_begin < t_end) {
+    npre = nk < C::STAGES ? nk : C::STAGES;
+    for (int kb = 0; kb < npre; ++kb) issue_b(kb, kb, tile_n(t_begin) * BN);
+  }
   ptx::griddep_wait();  // inputs written by the previous kernel are visible from here on
   if (threadIdx.x == 0) stamp(g.dbg, 1);
   // Trigger the dependent launch now rather than at exit: its CTAs are then placed on each SM the moment
@@ -266,28 +287,18 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
         for (int kb = 0; kb < nk; ++kb, ++gk) {
           const int s = gk % C::STAGES;
           if (gk >= C::STAGES) ptx::mbar_wait(&empty[s], ((gk / C::STAGES) - 1) & 1);
-          if constexpr (CG == 2) {
-            if (roleA) {
-              if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * C::A_BYTES);
-              ptx::tma_load_2d_cg2(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
-            } else {
-              if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * C::B_BYTES);
-              ptx::tma_load_2d_cg2(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0 + rank * (BN / 2));
-            }
-          } else if (roleA) {
+          if (!roleA) {
+            if (it > 0 || kb >= npre) issue_b(s, kb, n0);  // (first tile: the first npre were prefetched)
+          } else if constexpr (CG == 2) {
+            if (leader) ptx::mbar_arrive_expect_tx(&full[s], 2 * C::A_BYTES);
+            ptx::tma_load_2d_cg2(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
+          } else {
             ptx::mbar_arrive_expect_tx(&full[s], C::A_BYTES);
             if constexpr (CN > 1 && !MB)
               ptx::tma_load_2d_mc(sA + s * C::A_BYTES + crank * (BM / CN) * 128, &tmA, &full[s], kb * BK,
                                   m0 + crank * (BM / CN), kMask);
             else
               ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], a_k0 + kb * BK, m0);
-          } else {
-            ptx::mbar_arrive_expect_tx(&full[s], C::B_BYTES);
-            if constexpr (MB)
-              ptx::tma_load_2d_mc(sB + s * C::B_BYTES + crank * (BN / CN) * 128, &tmB, &full[s], kb * BK,
-                                  n0 + crank * (BN / CN), kMask);
-            else
-              ptx::tma_load_2d(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);
           }
         }
       }

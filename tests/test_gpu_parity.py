@@ -285,11 +285,14 @@ def test_c2_xv_splitk(c2, B):
     idx, off, dense = to_dev(bt)
     x0 = m.embed(idx, off, B, dense)
     s_tile = m.dense(x0, B).clone()
-    m.set_option("xv_splitk", 1)
     try:
+        m.set_option("xv_splitk", 1)
         s_split = m.dense(x0, B).clone()
+        m.set_option("xv_splitk", 2)  # partials exchanged through L2 instead of DSMEM: same sums, same order
+        s_split2 = m.dense(x0, B).clone()
     finally:
         m.set_option("xv_splitk", 0)
+    assert torch.equal(s_split, s_split2)
     assert (s_split - s_tile).abs().max().item() <= 5e-4
     sel = np.arange(B) if B <= 333 else np.random.default_rng(3).choice(B, 256, replace=False)
     ref = O.score_forward(cfg, cs.table_specs(cfg), w, sub_batch(bt, sel))["scores"]
