@@ -18,9 +18,9 @@ EPI = {0: "STORE", 1: "BIAS_RELU", 2: "CROSS", 3: "HEAD", 4: "BIAS", 5: "CROSS_F
 
 
 def role(name):
-    m = re.search(r"gemm_bf16_kernel<(\d+), (\d+), (\d+), (\d+), (\d+)(?:, (\d+))?>", name)
+    m = re.search(r"gemm_bf16_kernel<([\d, ]+)>", name)  # <BN, EPI, AR, CG, CN[, EW[, MB]]>
     if m:
-        bn, epi, ar, cg, cn = map(int, m.groups()[:5])
+        bn, epi, ar, cg, cn = [int(x) for x in m.group(1).split(",")][:5]
         # role names of config 2 (for c6: BIAS_RELU = projection / mask hidden / MLP, MASK = mask blocks)
         r = {(0,): "gemm_xV", (2,): "gemm_tU_cross", (1,): "gemm_mlp_relu", (3,): "gemm_mlp_head",
              (9,): "gemm_mask_mul"}.get((epi,), f"gemm_{EPI.get(epi, epi)}")
