@@ -236,7 +236,11 @@ int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d
  * over adjacent N tiles with the A tile multicast by TMA: 0 = off, 1 = only the head GEMM (N = 4 x 64,
  * the sigmoid's dot product summed over the cluster in DSMEM, fixed order), 2 = every GEMM whose N tiles
  * group by 4; "u_bn" [192] N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64); "xv_splitk" [0]
- * t = x_l V^T as a K-split cluster GEMM with a DSMEM reduction; "epw" [2] epilogue warps per TMEM quadrant:
+ * t = x_l V^T as a K-split cluster GEMM, 1 = partials reduced over DSMEM, 2 = exchanged through an L2-resident
+ * global scratch (same sums, same order); "xv_bn" [0 = by wave count] N tile of t = x_l V^T (64, 128, 256);
+ * "pair_xv" [0] / "pair_mlp" [0] 2-CTA (cta_group::2) tiles for the xV (value = BN) / hidden MLP GEMMs;
+ * "prefetch_b" [1] each GEMM issues its first ring stages' weight loads before waiting for the previous
+ * kernel; "epw" [2] epilogue warps per TMEM quadrant:
  * 0 one, 1 up to 4 (one 64-column sub-tile each), 2 split only when a CTA runs <= 2 tiles; "mb" [0] weight
  * tiles multicast over clusters of 8 row blocks; "ens_fused_ffn" [0] config 4's FFN + out-projection + LN as
  * one kernel; "mask_grouped" [1] MaskNet's parallel blocks as one grouped GEMM.  Variants are bit-identical
