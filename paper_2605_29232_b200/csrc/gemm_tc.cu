@@ -66,6 +66,7 @@ struct Cfg {
   static constexpr int OUT_BUFS = BN >= 192 ? 1 : 2;
   static constexpr bool RING = ein_ring<BN, EPI, CG>();
   static constexpr int RING_SLOTS = 3;
+
   // epilogue warps per TMEM lane quadrant: the epilogue of a CTA's last tile is exposed (one tile per CTA at
   // B = 4096), so plain stores split the tile's 64-column sub-tiles over up to 4 warps per quadrant
   static constexpr bool SPLIT = (EPI == EPI_STORE || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS) && CN == 1;
@@ -87,6 +88,10 @@ struct Cfg {
 #define CVR_MAX_STAGES 8
 #endif
   static constexpr int STAGES = STAGES_FIT > CVR_MAX_STAGES ? CVR_MAX_STAGES : STAGES_FIT;
+  // RING: a CTA's last tile (when it is not also its first) takes its epilogue inputs into the operand ring
+  // instead of the slots -- the ring is free once that tile's MMAs have completed, long before the previous
+  // tile's epilogue hands the slots back (sub-tile j: x0 in A stage j, x_l in B stage j)
+  static constexpr bool RING_ALT = RING && !AR && NSUB <= STAGES && A_BYTES >= SUB && B_BYTES >= SUB;
   static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);  // 2 accumulators, pow2 alloc
   static constexpr int SMEM = 1024 + AR_BYTES + STAGES * STAGE + EPI_BYTES + Z_BYTES + BAR_BYTES;
   static_assert(STAGES >= 2, "shared memory budget");
@@ -309,12 +314,16 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
         int it = 0;
         for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
           const int m0 = tile_m(tile) * BMT, n0 = tile_n(tile) * BN;
+          const bool alt = C::RING_ALT && it >= 1 && tile + t_step >= t_end;
+          // (tfull[a] is at most one phase behind here: tile it-2's epilogue released the slots, see below)
+          if (alt) ptx::mbar_wait(&tfull[it & 1], (it >> 1) & 1);  // last tile's MMAs done: its ring is free
           for (int j = 0; j < C::NSUB; ++j) {
-            if (it >= 1) ptx::mbar_wait(&eempty[j], (it - 1) & 1);
+            uint8_t* x0d = alt ? sA + j * C::A_BYTES : sEin + j * 2 * C::SUB;
+            uint8_t* xld = alt ? sB + j * C::B_BYTES : x0d + C::SUB;
+            if (!alt && it >= 1) ptx::mbar_wait(&eempty[j], (it - 1) & 1);
             ptx::mbar_arrive_expect_tx(&efull[j], 2 * C::SUB);
-            uint8_t* slot = sEin + j * 2 * C::SUB;
-            ptx::tma_load_2d(slot, &tmX0, &efull[j], n0 + j * 64, m0);
-            ptx::tma_load_2d(slot + C::SUB, &tmXl, &efull[j], n0 + j * 64, m0);
+            ptx::tma_load_2d(x0d, &tmX0, &efull[j], n0 + j * 64, m0);
+            ptx::tma_load_2d(xld, &tmXl, &efull[j], n0 + j * 64, m0);
           }
         }
       }
@@ -395,8 +404,10 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
         // x_{l+1} = x0 * (acc + b) + x_l on sub-tile j = part, written over x_l in slot j and TMA-stored
         // from there; the slot is handed back once the store has read it
         const int j = part;
+        const bool alt = C::RING_ALT && it >= 1 && tile + t_step >= t_end;  // inputs in the ring (see producer)
         ptx::mbar_wait(&efull[j], it & 1);
-        const uint32_t x0b = ptx::smem_u32(sEin + j * 2 * C::SUB), xlb = x0b + C::SUB;
+        uint8_t* xl_tile = alt ? sB + j * C::B_BYTES : sEin + j * 2 * C::SUB + C::SUB;
+        const uint32_t x0b = ptx::smem_u32(alt ? sA + j * C::A_BYTES : sEin + j * 2 * C::SUB), xlb = ptx::smem_u32(xl_tile);
 #pragma unroll
         for (int c = 0; c < 64; c += 32) {
           float v[32], x0v[32], xlv[32];
@@ -422,7 +433,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
         ptx::fence_async_smem();
         __syncwarp();
         if (lane == 0) {
-          ptx::tma_store_2d(&tmOut, sEin + j * 2 * C::SUB + C::SUB + q * 32 * 128, n0 + j * 64, m0 + q * 32);
+          ptx::tma_store_2d(&tmOut, xl_tile + q * 32 * 128, n0 + j * 64, m0 + q * 32);
           ptx::bulk_commit();
           ptx::bulk_wait_read<0>();
           ptx::mbar_arrive(&eempty[j]);
