@@ -186,7 +186,10 @@ struct cvr_ctx {
   // mainloop is bound by each SM's TMA ingest (A k-block + B k-block per SM either way), not by MMA shape
   int pair_xv = 0;
   int xv_bn = 0;
-  bool prefetch_b = true;      // option "prefetch_b": weight k-blocks issued before the dependency wait               // option "xv_bn": N tile of t = x_l V^T (0 = by wave count, see pick_bn_xv)
+  bool prefetch_b = true;
+  // option "pair_u": the U GEMM (192-wide EIN-ring tiles) as 2-CTA 256-row tiles, each CTA holding half of the U
+  // tile.  Bit-exact; measured 89.5 vs 86.3 us per c2 dense stage, 726-732 vs 740 us at c3's rank slice (B = 8192)
+  bool pair_u = false;      // option "prefetch_b": weight k-blocks issued before the dependency wait               // option "xv_bn": N tile of t = x_l V^T (0 = by wave count, see pick_bn_xv)
   // option "xv_splitk" [0]: t = x_l V^T as a K-split cluster GEMM (r == 256).  Measured on B200 at B = 4096:
   // its mainloop halves (3.5 vs 7 us) but the DSMEM exchange of the fp32 partials costs 2-6 us (element-wise
   // st.shared::cluster or cp.async.bulk shared::cluster alike): 92-100 us per dense stage vs 90 with tiles
@@ -855,6 +858,12 @@ int encode_plan(cvr_ctx* c) {
     // read U through 64-row boxes
     const bool u192 = c->u_bn == 192 && c->x0_ld % 192 == 0 && !c->fused_cross && !c->stack && !c->a_resident;
     ok &= addp("dcn/" + std::to_string(l) + "/U", (int)c->x0_ld, c->r, u192 ? 192 : pick_bn((int)c->x0_ld), EPI_CROSS);
+    if (u192 && c->pair_u) {  // 2-CTA tiles: each CTA holds half of the U tile (B box = 96 rows)
+      GemmPlan& g = c->plan.back();
+      g.pair = true;
+      g.mb8ok = false;
+      ok &= encode_tmap_bf16(&g.tmB, c->wptr("dcn/" + std::to_string(l) + "/U"), g.N, g.K, g.K, 96, &er) == 0;
+    }
   }
   c->tm_v256.assign(c->n_cross, CUtensorMap{});
   if (c->r == 256)
@@ -2109,6 +2118,13 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);  // U tile width
+    return CVR_OK;
+  }
+  if (!strcmp(key, "pair_u")) {
+    c->pair_u = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);
     return CVR_OK;
   }
   if (!strcmp(key, "prefetch_b")) {

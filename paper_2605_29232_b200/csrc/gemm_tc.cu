@@ -53,7 +53,7 @@ struct EpiTraits {
 // sub-tile j, write x_{l+1} in place over x_l and TMA-store it from there (no separate output staging):
 // 96 KB of epilogue buffers instead of 2 x 96 + 48, and the three sub-tiles are finished in parallel.
 template <int BN, int EPI, int CG>
-constexpr bool ein_ring() { return EPI == EPI_CROSS && BN == 192 && CG == 1; }
+constexpr bool ein_ring() { return EPI == EPI_CROSS && BN == 192; }
 
 template <int BN, int EPI, bool AR = false, int CG = 1, int CN = 1, int EW = 4, bool MB = false>
 struct Cfg {
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
       if (lane == 0) {
         int it = 0;
         for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
-          const int m0 = tile_m(tile) * BMT, n0 = tile_n(tile) * BN;
+          const int m0 = tile_m(tile) * BMT + rank * BM, n0 = tile_n(tile) * BN;  // (CG = 2: this CTA's rows)
           const bool alt = C::RING_ALT && it >= 1 && tile + t_step >= t_end;
           // (tfull[a] is at most one phase behind here: tile it-2's epilogue released the slots, see below)
           if (alt) ptx::mbar_wait(&tfull[it & 1], (it >> 1) & 1);  // last tile's MMAs done: its ring is free
@@ -321,6 +321,9 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
             uint8_t* x0d = alt ? sA + j * C::A_BYTES : sEin + j * 2 * C::SUB;
             uint8_t* xld = alt ? sB + j * C::B_BYTES : x0d + C::SUB;
             if (!alt && it >= 1) ptx::mbar_wait(&eempty[j], (it - 1) & 1);
+            // alt: slot j's previous tile may still be landing -- its efull phase must complete before this
+            // tile's expect_tx re-arms the barrier
+            if (alt) ptx::mbar_wait(&efull[j], (it - 1) & 1);
             ptx::mbar_arrive_expect_tx(&efull[j], 2 * C::SUB);
             ptx::tma_load_2d(x0d, &tmX0, &efull[j], n0 + j * 64, m0);
             ptx::tma_load_2d(xld, &tmXl, &efull[j], n0 + j * 64, m0);
@@ -415,7 +418,10 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
           if (c == 32) {  // last TMEM read of this accumulator by this warp
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[a]);
+            if (lane == 0) {
+              if constexpr (CG == 2) ptx::mbar_arrive_leader(&tempty[a]);
+              else ptx::mbar_arrive(&tempty[a]);
+            }
           }
           lds32_bf16(x0b, r, c >> 3, x0v);
           lds32_bf16(xlb, r, c >> 3, xlv);
@@ -697,7 +703,8 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
   CVR_CASE(128, EPI_BIAS_RELU)
   if (g.BN == 64 && g.epi == EPI_CROSS && g.K <= 256 && g.a_resident) return launch_t<64, EPI_CROSS, true>(g, s);
   CVR_CASE(64, EPI_CROSS)
-  if (g.BN == 192 && g.epi == EPI_CROSS && !g.cta_pair) return launch_t<192, EPI_CROSS>(g, s);
+  if (g.BN == 192 && g.epi == EPI_CROSS) return g.cta_pair ? launch_t<192, EPI_CROSS, false, 2>(g, s)
+                                                           : launch_t<192, EPI_CROSS>(g, s);
   CVR_CASE(64, EPI_HEAD)
   CVR_CASE(128, EPI_HEAD)
   CVR_CASE(256, EPI_HEAD)

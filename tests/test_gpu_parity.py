@@ -369,3 +369,48 @@ def test_c2_xv_bn_bitexact(c2, bn):
         finally:
             m.set_option("xv_bn", 0)
         assert torch.equal(s0, s1)
+
+
+@pytest.mark.parametrize("B", [4096, 333, 1])
+def test_c2_pair_u_bitexact(c2, B):
+    """Option pair_u: the U GEMM's 192-wide EIN-ring tiles as 2-CTA (cta_group::2) 256-row tiles, each CTA
+    holding half of the U tile; same MMAs per output element in the same K order -> bit-identical scores."""
+    cfg, m, tabs, w = c2
+    bt = cs.make_batch(cfg, 65, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    s0 = m.dense(x0, B).clone()
+    m.set_option("pair_u", 1)
+    try:
+        s1 = m.dense(x0, B).clone()
+    finally:
+        m.set_option("pair_u", 0)
+    assert torch.equal(s0, s1)
+
+
+@pytest.mark.parametrize("B", [16384, 12345])
+def test_c2_many_tiles_per_cta_bitexact(B):
+    """Large batches give every persistent GEMM CTA many tiles (the U GEMM's last-tile epilogue inputs go
+    through the operand ring, the slots cycle many times): 192-wide ring tiles == 64-wide tiles bit-exact, and
+    2-CTA U tiles bit-exact, and a sample vs the oracle.  Synthetic x0 (no tables needed for the dense stage)."""
+    from paper_2605_29232_b200 import CvrModel
+    cfg = cs.C2
+    w = cs.make_weights(cfg)
+    m = CvrModel(cfg, max_batch=B, max_nnz=1 << 12)
+    m.load_weights({k: v.cuda() for k, v in w.items()})
+    x0 = m.new_x0(B)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x0[:, :cfg.width] = (torch.randn(B, cfg.width, device="cuda", generator=g) * 0.3).to(x0.dtype)
+    s192 = m.dense(x0, B).clone()
+    m.set_option("u_bn", 64)
+    s64 = m.dense(x0, B).clone()
+    m.set_option("u_bn", 192)
+    m.set_option("pair_u", 1)
+    s_pair = m.dense(x0, B).clone()
+    m.close()
+    assert torch.equal(s192, s64)
+    assert torch.equal(s192, s_pair)
+    sel = np.random.default_rng(4).choice(B, 48, replace=False)
+    xs = x0[torch.from_numpy(sel).cuda(), :cfg.width].double().cpu().numpy()
+    ref = O.dense_forward(cfg, {k: O.to_f64(v) for k, v in w.items()}, xs)["scores"]
+    assert np.abs(s192[torch.from_numpy(sel).cuda()].double().cpu().numpy() - ref).max() <= TOL_BF16
