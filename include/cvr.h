@@ -167,8 +167,11 @@ int cvr_score(cvr_ctx* ctx, const int32_t* d_indices, const int32_t* d_offsets, 
 
 /* Host-fed variant (S1 + S2-S7 + S8): h_* are host buffers (pinned for async copies);
  * the H2D copies of this batch run on s_copy into double-buffered device staging,
- * then as cvr_score, then the D2H of the scores on s_dense.  Returns after enqueueing;
- * h_scores is valid once s_dense has been synchronised. */
+ * then as cvr_score.  S8: when h_scores is page-locked (mapped) memory the head kernel stores
+ * the scores straight into it over PCIe (zero-copy; option "zero_copy_scores" [1]), otherwise
+ * they are copied D2H on s_dense.  Returns after enqueueing; h_scores is valid once s_dense
+ * has been synchronised.  The batch's pinned h_scores must not be reused by another call in
+ * flight (one scores buffer per batch in flight, as for the inputs). */
 int cvr_score_host(cvr_ctx* ctx, const int32_t* h_indices, const int32_t* h_offsets, int64_t nnz,
                    int batch, const float* h_dense, float* h_scores, cvr_stream_t s_copy,
                    cvr_stream_t s_embed, cvr_stream_t s_dense);

@@ -159,6 +159,22 @@ def test_c2_score_pipelined_and_host_fed_match(c2):
     assert m.status(s_d) == 0
     for o, r in zip(houts, refs):
         assert torch.equal(o, r.cpu())
+    # S8 variants: pinned h_scores take the zero-copy store (above); pageable h_scores and the option off take
+    # the D2H copy on s_dense -- same scores
+    pageable = [torch.empty(bt.batch, dtype=torch.float32) for bt in batches]
+    for (idx, off, dense), bt, o in zip(host_in, batches, pageable):
+        m.score_host(idx, off, bt.batch, dense, o, s_copy=s_c, s_embed=s_e, s_dense=s_d)
+    s_d.synchronize()
+    m.set_option("zero_copy_scores", 0)
+    try:
+        houts2 = [torch.empty(bt.batch, dtype=torch.float32).pin_memory() for bt in batches]
+        for (idx, off, dense), bt, o in zip(host_in, batches, houts2):
+            m.score_host(idx, off, bt.batch, dense, o, s_copy=s_c, s_embed=s_e, s_dense=s_d)
+        s_d.synchronize()
+    finally:
+        m.set_option("zero_copy_scores", 1)
+    for o, o2, r in zip(pageable, houts2, refs):
+        assert torch.equal(o, r.cpu()) and torch.equal(o2, r.cpu())
 
 
 def test_c2_zero_weights_closed_form():
