@@ -233,7 +233,8 @@ int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d
  * ensemble DCN U GEMM; "embed_bps" [0 = uncapped] embedding CTAs per SM inside cvr_score / cvr_score_host (grid cap: the
  * embedding stage of batch k+1 then leaves registers for the dense-stage GEMM CTAs of batch k);
  * "embed_variant" [0] 0 = one lane group per bag at full
- * occupancy, 1 = warp-batched bags (coalesced offset / index staging); "a_resident" [0] the U GEMM of a low-rank cross layer keeps
+ * occupancy (rows of <= 128 B loaded without L1 allocation), 1 = warp-batched bags (coalesced offset / index
+ * staging), 2 = cooperative index fetch, 3 = as 0 with L1-allocating row loads; "a_resident" [0] the U GEMM of a low-rank cross layer keeps
  * the 128 x r block of t resident in shared memory across its N tiles ("fused_cross" = 1 runs each
  * low-rank cross layer as one clustered kernel (K5) instead of two GEMMs); "mc" [1] clusters of 4 CTAs
  * over adjacent N tiles with the A tile multicast by TMA: 0 = off, 1 = only the head GEMM (N = 4 x 64,

@@ -116,7 +116,8 @@ __device__ __forceinline__ int64_t hashed_row(uint64_t key, int64_t vocab, uint6
   return (int64_t)r;
 }
 
-template <typename TIn, typename TOut, int LPR, int UNROLL, int MINB, bool KEYS, bool COOP = false>
+// NA: row loads that do not allocate in L1 (rows of <= 128 B, see launch_t)
+template <typename TIn, typename TOut, int LPR, int UNROLL, int MINB, bool KEYS, bool COOP = false, bool NA = false>
 __global__ void __launch_bounds__(256, MINB) embed_bag_kernel(const EmbedArgs a, int n_embed_blocks) {
   if ((int)blockIdx.x >= n_embed_blocks) {
     dense_part<TOut>(a, blockIdx.x - n_embed_blocks, gridDim.x - n_embed_blocks);
@@ -178,7 +179,10 @@ __global__ void __launch_bounds__(256, MINB) embed_bag_kernel(const EmbedArgs a,
         uint4 v[UNROLL];
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u)
-          if (j + u < end) v[u] = ptx::ld_nc_v4(colbase + idx[u] * td.stride);
+          if (j + u < end) {
+            if constexpr (NA) v[u] = ptx::ld_nc_na_v4(colbase + idx[u] * td.stride);
+            else v[u] = ptx::ld_nc_v4(colbase + idx[u] * td.stride);
+          }
 #pragma unroll
         for (int u = 0; u < UNROLL; ++u)
           if (j + u < end) InTraits<TIn>::add(acc, v[u]);
@@ -355,6 +359,11 @@ cudaError_t launch_t(const EmbedArgs& a, int num_sms, cudaStream_t s) {
     embed_bag_v2_kernel<TIn, TOut, LPR, 4><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
   else if (a.variant == 2)  // cooperative index fetch + broadcast (option embed_variant = 2)
     embed_bag_kernel<TIn, TOut, LPR, 1, 8, false, true><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
+  else if (LPR <= 8 && a.variant != 3)
+    // rows of <= 128 B (one line each): row loads skip L1 allocation.  Measured on B200 (scripts/embed_ab.py):
+    // c2 (128-B bf16 rows) 20.3 -> 18.5 us; wider rows keep L1 allocation (c3-S 256-B rows 1.83 -> 2.00 ms,
+    // c4 512-B rows 187 -> 203 us without it); option embed_variant = 3 forces allocating loads
+    embed_bag_kernel<TIn, TOut, LPR, 1, 8, false, false, true><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
   else
     embed_bag_kernel<TIn, TOut, LPR, 1, 8, false><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
   return cudaGetLastError();

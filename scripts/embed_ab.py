@@ -21,11 +21,7 @@ for rep in range(3):
         for i in range(8):
             m.embed(*dev[i % 4][:2], B, dev[i % 4][2], x0=x0, stream=s)
         torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(s)
-        for i in range(K):
-            m.embed(*dev[i % 4][:2], B, dev[i % 4][2], x0=x0, stream=s)
-        b.record(s); torch.cuda.synchronize()
-        us = a.elapsed_time(b) / K * 1e3
+        import bench
+        us = bench.time_enqueued(lambda i: m.embed(*dev[i % 4][:2], B, dev[i % 4][2], x0=x0, stream=s), K, s) * 1e3
         print(json.dumps({"cfg": cfg.name, "variant": v2, "us": round(us, 2), "GBps_alg": round(byts / us / 1e3, 1), "frac_hbm": round(byts / us / 1e3 / 6556.5, 3)}))
 assert m.status(s) == 0
