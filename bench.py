@@ -44,8 +44,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="cvr", choices=["cvr", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c4", "c3s", "c6"],
-                    help="workload (default: config 2, the metric's single-GPU config)")
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c3s", "c6"],
+                    help="workload (default: config 2, the metric's single-GPU config); c3 / c3s with --gpus N > 1 "
+                         "(or --sharded) run the table-sharded path, strong scaling over a fixed global batch")
+    ap.add_argument("--sharded", action="store_true", help="table-sharded path even at N = 1 (c3 always)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
+                    help="sharded path: NCCL all-to-all of pooled rows (V1) or peer-memory stores (V3)")
     ap.add_argument("--ring", type=int, default=8, help="distinct pre-uploaded batches cycled through")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -219,12 +223,14 @@ WORKLOADS = {
     "c2": "c2: BASELINE.json configs[1] single-GPU bf16 DCN-v2 scoring (embed -> 3 low-rank cross -> MLP "
           "1728-1024-512-256-1 -> sigmoid)",
     "c3s": "c3-S: BASELINE.json configs[2] strong-scaling variant (100 x 5e6 x 128 fp16 tables, B=65536, W=12864)",
+    "c3": "c3: BASELINE.json configs[2] embedding-scaled (100 x 1e7 x 128 fp16 tables = 256 GB, table-wise "
+          "round-robin over the GPUs, pooled rows exchanged all-to-all, dense stage data-parallel on B/N)",
     "c4": "c4: BASELINE.json configs[3] backbone-scaled (64 x 1e6 x 256 bf16, 4 ensemble layers DCN||MHA||FFN + LN, "
           "head 16384-2048-512-1)",
     "c6": "c6: SURVEY.md §8(f) #1 MaskNet on config 2's features (ReLU projection 1728->2048, 2 parallel mask "
           "blocks r=512, MLP 4096-1024-512-256-1; PAPER.md Table 1 MaskNet defaults), not a BASELINE.json config",
 }
-TOL = {"c1": 1e-5, "c2": 2e-3, "c3s": 2e-3, "c4": 2e-3, "c6": 2e-3}
+TOL = {"c1": 1e-5, "c2": 2e-3, "c3": 2e-3, "c3s": 2e-3, "c4": 2e-3, "c6": 2e-3}
 
 
 # ----------------------------------------------------------------------------- distributed
@@ -555,11 +561,198 @@ def run_cvr(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, cfg):
+    """Config 3 / 3-S on N GPUs: table t on rank t mod N; every step each rank pools
+    its tables for the GLOBAL batch, the pooled rows are exchanged (NCCL all-to-all, or V3 peer-memory stores),
+    and each rank scores its B/N slice.  value = global examples per second (strong scaling: B fixed)."""
+    from paper_2605_29232_b200.sharded import FusedShardedScorer, ShardedScorer, local_tables
+
+    world, rank, local = dist_setup(args)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    B = cfg.batch
+    Bl = B // world
+    mine = local_tables(cfg.n_tables, world, rank)
+    need = sum(cfg.rows[t] for t in mine) * cfg.dim * 2
+    free, _ = torch.cuda.mem_get_info(dev)
+    if need > free - (8 << 30):
+        raise SystemExit(f"{cfg.name}: this rank's tables need {need / 1e9:.0f} GB, {free / 1e9:.0f} GB free on "
+                         f"the GPU -- run on more GPUs (table-wise sharding divides them by N)")
+    specs = cs.table_specs(cfg)
+    tables = [specs[t].materialize(device=dev) for t in mine]
+    weights = cs.make_weights(cfg)
+    R = max(2, min(args.ring, 2))
+    ring = [cs.make_batch(cfg, 1000 + i, tables=mine) for i in range(R)]
+    max_nnz = max(b.nnz for b in ring)
+    if world == 1:
+        args.exchange = "nccl"  # nothing to exchange at N = 1 (V3 needs peers): the all-to-all is a local copy
+    Sc = FusedShardedScorer if args.exchange == "fused" else ShardedScorer
+    sc = Sc(cfg, world, rank, B, max_nnz, device=dev)
+    if args.exchange == "fused":
+        sc.connect()
+    sc.load_tables(tables)
+    sc.load_weights({k: v.to(dev) for k, v in weights.items()})
+    dev_in = [(torch.from_numpy(b.indices).to(dev), torch.from_numpy(b.offsets).to(dev),
+               torch.from_numpy(b.dense[rank * Bl:(rank + 1) * Bl]).to(dev)) for b in ring]
+    outs = [torch.empty(Bl, dtype=torch.float32, device=dev) for _ in ring]
+    s_e = torch.cuda.Stream(dev, priority=0)   # gather + exchange (+ unpack) of batch k+1
+    s = torch.cuda.Stream(dev, priority=-1)    # dense stage of batch k (higher priority)
+
+    def step(i):
+        idx, off, dn = dev_in[i % R]
+        if args.exchange == "fused":
+            sc.embed(idx, off, dn, stream=s_e)
+            sc.dense(outs[i % R], stream=s)
+        else:
+            sc.score(idx, off, dn, outs[i % R], stream=s_e, s_dense=s)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    clocks = ClockSampler(local)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with clocks:
+        barrier(world)
+        torch.cuda.synchronize(dev)
+        n0 = sc.model.launch_count()
+        ev0.record(s_e)
+        s.wait_event(ev0)
+        for i in range(args.steps):
+            step(i)
+        ev1.record(s)
+        torch.cuda.synchronize(dev)
+        barrier(world)
+    n_launch = sc.model.launch_count() - n0
+    el_ms = max_over_ranks(world, ev0.elapsed_time(ev1), local)
+    assert sc.model.status(s) == 0
+    value = args.steps * B / (el_ms / 1e3)
+
+    # e2e: the same steps fed from pinned host memory (H2D of this rank's inputs, D2H of its scores in the region)
+    host_in = [(torch.from_numpy(b.indices).pin_memory(), torch.from_numpy(b.offsets).pin_memory(),
+                torch.from_numpy(b.dense[rank * Bl:(rank + 1) * Bl]).pin_memory()) for b in ring]
+    stage = [tuple(torch.empty_like(t, device=dev) for t in h) for h in host_in]
+    houts = [torch.empty(Bl, dtype=torch.float32).pin_memory() for _ in ring]
+
+    s_c = torch.cuda.Stream(dev, priority=0)
+    ev_c = [torch.cuda.Event() for _ in range(R)]
+    ev_used = [torch.cuda.Event() for _ in range(R)]
+
+    def hstep(i):  # H2D of batch i on a copy stream (staging slot i % R, free once batch i-R's gather read it)
+        j = i % R
+        if i >= R:
+            s_c.wait_event(ev_used[j])
+        with torch.cuda.stream(s_c):
+            for d, h in zip(stage[j], host_in[j]):
+                d.copy_(h, non_blocking=True)
+        ev_c[j].record(s_c)
+        s_e.wait_event(ev_c[j])
+        idx, off, dn = stage[j]
+        if args.exchange == "fused":
+            sc.embed(idx, off, dn, stream=s_e)
+            sc.dense(outs[j], stream=s)
+        else:
+            sc.score(idx, off, dn, outs[j], stream=s_e, s_dense=s)
+        ev_used[j].record(s_e)
+        with torch.cuda.stream(s):
+            houts[j].copy_(outs[j], non_blocking=True)
+
+    for i in range(min(args.warmup, 3)):
+        hstep(i)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0.record(s_c)
+    s_e.wait_event(h0)
+    s.wait_event(h0)
+    for i in range(args.steps):
+        hstep(i)
+    h1.record(s)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    hel = max_over_ranks(world, h0.elapsed_time(h1), local)
+    h2d = float(np.mean([sum(t.numel() * t.element_size() for t in h) for h in host_in]))
+
+    # per-kernel durations on rank 0 (CUDA-event pairs around its launches; every rank runs the pass, the
+    # exchange needs them all)
+    launches_per_step = 3 + 2 * cfg.n_cross + len(cfg.mlp_dims)
+    sc.model.profile_begin(args.steps * launches_per_step + 16)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    for i in range(args.steps):
+        step(i)
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    kstats = sc.model.profile_end()
+    if rank != 0:
+        return
+    pk = peaks()
+    bf16_peak = pk["bf16_sustained"] or pk["bf16"]
+    work = launch_work(cfg, Bl)
+    kernels = {}
+    for name, st in kstats.items():
+        avg_s = st["avg_ms"] / 1e3
+        if name in work:
+            wk = work[name]
+            bound = pick_bound(wk, bf16_peak, pk["hbm"])
+            ach = (wk["bytes"] / avg_s / 1e9) if bound == "hbm" else (wk["flops"] / avg_s / 1e12)
+            peak = pk["hbm"] if bound == "hbm" else bf16_peak
+            kernels[name] = {"bound": bound, "avg_us": st["avg_ms"] * 1e3, "launches": st["launches"],
+                             "achieved": ach, "unit": "GB/s" if bound == "hbm" else "TFLOP/s", "frac": ach / peak}
+        elif name == "embed_bag_pool":
+            eb = float(np.mean([embed_bytes(cfg, b) for b in ring]))  # this rank's tables, global batch
+            ach = eb / avg_s / 1e9
+            kernels[name] = {"bound": "hbm", "avg_us": st["avg_ms"] * 1e3, "launches": st["launches"],
+                             "achieved": ach, "unit": "GB/s", "frac": ach / pk["hbm"], "algorithmic_bytes": eb}
+        else:
+            kernels[name] = {"avg_us": st["avg_ms"] * 1e3, "launches": st["launches"]}
+    dom = max((k for k in kstats if "frac" in kernels[k]), key=lambda k: kstats[k]["total_ms"])
+    dk = kernels[dom]
+    roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"],
+                "peak": pk["hbm"] if dk["bound"] == "hbm" else bf16_peak, "unit": dk["unit"], "frac": dk["frac"],
+                "traffic": None, "peak_source": f"MEASURED_PEAKS.json ({pk['source']})",
+                "bound_rule": "roofline: the larger of flops / bf16 peak and algorithmic bytes / HBM peak"}
+
+    parity = None
+    try:
+        import oracle as O
+        full = cs.make_batch(cfg, 1000 + (args.steps - 1) % R)
+        sel = np.arange(0, Bl, max(1, Bl // 32))  # rank 0's slice = global rows [0, B/N)
+        ref = O.score_forward(cfg, specs, weights, cs.sub_batch(full, sel))["scores"]
+        got = outs[(args.steps - 1) % R][torch.from_numpy(sel).to(dev)].double().cpu().numpy()
+        parity = {"max_abs_err": float(np.abs(got - ref).max()), "n": int(len(sel)), "tol": TOL[cfg.name]}
+    except Exception as e:  # noqa: BLE001
+        parity = {"error": str(e)}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": el_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (cvr_synth, seeded; fp16 tables materialised on each rank for its tables)",
+        "config": {"workload": WORKLOADS[cfg.name], "global_batch": B, "per_rank_batch": Bl,
+                   "parallelism": f"table-wise sharding over {world} GPU(s) + data-parallel dense",
+                   "exchange": ("NCCL all-to-all of pooled bf16 rows (torch.distributed)" if args.exchange == "nccl"
+                                else "V3: pooled rows stored into the owner's x0 over peer memory"),
+                   "l2": "inputs larger than L2 (tables of %.0f GB per rank)" % (sum(t.numel() * t.element_size()
+                                                                                  for t in tables) / 1e9)},
+        "roofline": roofline,
+        "cpu_baseline": None,
+        "e2e": {"value": args.steps * B / (hel / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+                "d2h_bytes_per_step": B * 4, "ms_per_step": hel / args.steps,
+                "api": "sharded scorer on inputs copied from pinned host memory each step (copy stream, two "
+                       "compute streams)"},
+        "gpu_launches": n_launch, "clocks": clocks.summary(), "kernels": kernels, "parity": parity,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     cfg = cs.CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif cfg.name == "c3" or (cfg.name == "c3s" and world > 1) or args.sharded:
+        run_sharded(args, cfg)
     else:
         run_cvr(args, cfg)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.impl == "cvr":

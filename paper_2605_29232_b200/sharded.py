@@ -137,9 +137,13 @@ class ShardedScorer:
                               device=device)
         self.device = self.model.device
         sb, rb = self.model.shard_buffer_bytes(batch_global)
-        self.send = torch.empty(sb, dtype=torch.uint8, device=self.device)
-        self.recv = torch.empty(rb, dtype=torch.uint8, device=self.device)
-        self.x0 = self.model.new_x0(self.Bl)
+        # two slots of every per-batch buffer: batch k+1's gather / exchange / unpack overlap batch k's dense stage
+        self.send = [torch.empty(sb, dtype=torch.uint8, device=self.device) for _ in range(2)]
+        self.recv = [torch.empty(rb, dtype=torch.uint8, device=self.device) for _ in range(2)]
+        self.x0 = [self.model.new_x0(self.Bl) for _ in range(2)]
+        self.ev_embed = [torch.cuda.Event() for _ in range(2)]
+        self.ev_dense = [torch.cuda.Event() for _ in range(2)]
+        self.k = 0
         self.tables = local_tables(cfg.n_tables, world_size, rank)
 
     def load_tables(self, tables: Sequence[torch.Tensor]):
@@ -149,13 +153,28 @@ class ShardedScorer:
         self.model.load_weights(weights)
 
     def score(self, indices: torch.Tensor, offsets: torch.Tensor, dense_local: torch.Tensor,
-              scores: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-        """indices/offsets: this rank's tables over the global batch; dense_local: [B/N, F]."""
+              scores: Optional[torch.Tensor] = None, stream=None, s_dense=None) -> torch.Tensor:
+        """indices/offsets: this rank's tables over the global batch; dense_local: [B/N, F].
+
+        ``s_dense`` given: the two-stream executor of S9 -- gather, exchange and unpack of this batch on ``stream``
+        into buffer slot k % 2 (after the dense stage of batch k-2 released it), the dense stage on ``s_dense``
+        after them; back-to-back calls overlap batch k+1's exchange with batch k's dense stage.  ``scores`` must
+        stay distinct for the batches in flight.  Without ``s_dense`` everything runs in order on ``stream``."""
         scores = torch.empty(self.Bl, dtype=torch.float32, device=self.device) if scores is None else scores
         s = stream or torch.cuda.current_stream(self.device)
+        slot = self.k % 2 if s_dense is not None else 0
+        if s_dense is not None and self.k >= 2:
+            s.wait_event(self.ev_dense[slot])
         with torch.cuda.stream(s):
-            self.model.embed_shard(indices, offsets, self.B, dense_local, self.send, self.x0, stream=s)
-            exchange(self.send, self.recv, self.group)
-            self.model.unpack_shard(self.recv, self.B, self.x0, stream=s)
-            self.model.dense(self.x0, self.Bl, scores, stream=s)
+            self.model.embed_shard(indices, offsets, self.B, dense_local, self.send[slot], self.x0[slot], stream=s)
+            exchange(self.send[slot], self.recv[slot], self.group)
+            self.model.unpack_shard(self.recv[slot], self.B, self.x0[slot], stream=s)
+        if s_dense is None:
+            self.model.dense(self.x0[slot], self.Bl, scores, stream=s)
+            return scores
+        self.ev_embed[slot].record(s)
+        s_dense.wait_event(self.ev_embed[slot])
+        self.model.dense(self.x0[slot], self.Bl, scores, stream=s_dense)
+        self.ev_dense[slot].record(s_dense)
+        self.k += 1
         return scores

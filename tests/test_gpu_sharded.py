@@ -96,3 +96,28 @@ def test_fused_exchange_v3_matches_unsharded(c3small, world):
             assert torch.equal(sc.x0[epoch % 2], x0_ref[r * Bl:(r + 1) * Bl]), f"epoch {epoch} rank {r}: x0 differs"
             assert torch.equal(s, s_ref[r * Bl:(r + 1) * Bl]), f"epoch {epoch} rank {r}: scores differ"
         assert all(int(sc.free.min()) == epoch for sc in ranks)
+
+
+def test_sharded_scorer_pipelined_world1(c3small):
+    """ShardedScorer's two-stream executor (gather + exchange + unpack of batch k+1 overlapping the dense stage of
+    batch k, double-buffered send / recv / x0) at N = 1 (the all-to-all is a local copy): back-to-back batches give
+    scores bit-identical to the serial call and to the unsharded path."""
+    from paper_2605_29232_b200.sharded import ShardedScorer
+    cfg, tabs, w, ref = c3small
+    B = 384
+    sc = ShardedScorer(cfg, 1, 0, B, 1 << 20)
+    sc.load_tables(tabs)
+    sc.load_weights({k: v.cuda() for k, v in w.items()})
+    batches = [cs.make_batch(cfg, 20 + i, batch=B) for i in range(5)]
+    dev_in = [to_dev(bt) for bt in batches]
+    refs = [ref.dense(ref.embed(i, o, B, d), B).clone() for i, o, d in dev_in]
+    s_e, s_d = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = [torch.empty(B, device="cuda") for _ in batches]
+    for (i, o, d), out in zip(dev_in, outs):
+        sc.score(i, o, d, out, stream=s_e, s_dense=s_d)
+    torch.cuda.synchronize()
+    serial = [sc.score(i, o, d).clone() for i, o, d in dev_in]
+    torch.cuda.synchronize()
+    assert sc.model.status() == 0
+    for out, se, r in zip(outs, serial, refs):
+        assert torch.equal(out, r) and torch.equal(se, r)
