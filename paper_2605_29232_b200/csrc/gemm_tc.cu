@@ -69,7 +69,8 @@ struct Cfg {
 
   // epilogue warps per TMEM lane quadrant: the epilogue of a CTA's last tile is exposed (one tile per CTA at
   // B = 4096), so plain stores split the tile's 64-column sub-tiles over up to 4 warps per quadrant
-  static constexpr bool SPLIT = (EPI == EPI_STORE || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS) && CN == 1;
+  // (EPI_HEAD too: each warp's partial dot product over its 64-column sub-tiles, summed in column order)
+  static constexpr bool SPLIT = (EPI == EPI_STORE || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS || EPI == EPI_HEAD) && CN == 1;
   // EW caps the split: EW = 1 when each CTA runs several tiles (the epilogue then overlaps the next tile's
   // mainloop anyway) keeps the CTA at 7 warps, leaving registers for co-resident embedding CTAs
   static constexpr int EPW = RING ? 3 : (SPLIT ? (BN / 64 < EW ? BN / 64 : EW) : 1);
@@ -82,7 +83,7 @@ struct Cfg {
   static constexpr int EPI_BYTES = OUT_BUFS * OUT_BYTES + 2 * EIN_BYTES + (RING ? RING_SLOTS * 2 * SUB : 0);
   static constexpr int BAR_BYTES = 512;
   // EPI_HEAD across a CN-cluster: per-tile partial dot products gathered in rank 0 ([2][CN][BM] fp32)
-  static constexpr int Z_BYTES = (EPI == EPI_HEAD && CN > 1) ? 2 * CN * BM * 4 : 0;
+  static constexpr int Z_BYTES = (EPI == EPI_HEAD && CN > 1) ? 2 * CN * BM * 4 : (EPI == EPI_HEAD ? EPW * BM * 4 : 0);
   static constexpr int STAGES_FIT = (kSmemBudget - 1024 - BAR_BYTES - EPI_BYTES - AR_BYTES - Z_BYTES) / STAGE;
 #ifndef CVR_MAX_STAGES
 #define CVR_MAX_STAGES 8
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
   uint8_t* sB = sA + (AR ? 0 : C::STAGES * C::A_BYTES);
   uint8_t* sOut = sB + C::STAGES * C::B_BYTES;         // [OUT_BUFS][NSUB][SUB]
   uint8_t* sEin = sOut + C::OUT_BUFS * C::OUT_BYTES;   // [2][x0 NSUB subs | x_l NSUB subs]
-  float* zbuf = reinterpret_cast<float*>(sEin + 2 * C::EIN_BYTES);  // [2][CN][BM] (EPI_HEAD, CN > 1)
+  float* zbuf = reinterpret_cast<float*>(sEin + 2 * C::EIN_BYTES);  // EPI_HEAD: [2][CN][BM] (CN > 1) / [EPW][BM]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sEin + 2 * C::EIN_BYTES + C::Z_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = full + C::STAGES;
@@ -566,6 +567,18 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
           if (lane == 0)
             for (int j = 0; j < CN; ++j) ptx::mbar_arrive_remote(ptx::mapa(&zempty[a], j));
         }
+      } else if constexpr (EPI == EPI_HEAD && C::EPW > 1) {
+        // split epilogue: the quadrant's EPW warps hand their partial dot products to part 0, which sums them in
+        // column order from 0 (as the cluster head sums its CTAs' partials in rank order: same result)
+        zbuf[part * BM + r] = z;
+        ptx::named_bar_sync(1 + q, 32 * C::EPW);
+        if (part == 0) {
+          float zs = 0.f;
+#pragma unroll
+          for (int j = 0; j < C::EPW; ++j) zs += zbuf[j * BM + r];
+          if (live) g.scores[m] = sigmoid_f32(zs + g.head_b);
+        }
+        ptx::named_bar_sync(1 + q, 32 * C::EPW);  // zbuf free for the next tile
       } else if constexpr (EPI == EPI_HEAD) {
         if (live) g.scores[m] = sigmoid_f32(z + g.head_b);
       } else if constexpr (EPI == EPI_HEAD_PARTIAL) {
