@@ -359,6 +359,7 @@ def run_cvr(args, cfg):
         ip, op, nnz, dp, sp = raw[i % R]
         m.score_raw(ip, op, nnz, B, dp, sp, hse, hsd)
 
+    torch.cuda.synchronize(dev)  # the inputs were copied on the current stream; the executor's streams start now
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize(dev)
@@ -597,6 +598,8 @@ def run_sharded(args, cfg):
     outs = [torch.empty(Bl, dtype=torch.float32, device=dev) for _ in ring]
     s_e = torch.cuda.Stream(dev, priority=0)   # gather + exchange (+ unpack) of batch k+1
     s = torch.cuda.Stream(dev, priority=-1)    # dense stage of batch k (higher priority)
+
+    torch.cuda.synchronize(dev)  # inputs / buffers of the current stream are ready before the side streams start
 
     def step(i):
         idx, off, dn = dev_in[i % R]

@@ -143,8 +143,9 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
   uint8_t* sB = sA + (AR ? 0 : C::STAGES * C::A_BYTES);
   uint8_t* sOut = sB + C::STAGES * C::B_BYTES;         // [OUT_BUFS][NSUB][SUB]
   uint8_t* sEin = sOut + C::OUT_BUFS * C::OUT_BYTES;   // [2][x0 NSUB subs | x_l NSUB subs]
-  float* zbuf = reinterpret_cast<float*>(sEin + 2 * C::EIN_BYTES);  // EPI_HEAD: [2][CN][BM] (CN > 1) / [EPW][BM]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sEin + 2 * C::EIN_BYTES + C::Z_BYTES);
+  // (ring slots / staging live in [sOut, sOut + EPI_BYTES); the head partials and the barriers follow them)
+  float* zbuf = reinterpret_cast<float*>(sOut + C::EPI_BYTES);  // EPI_HEAD: [2][CN][BM] (CN > 1) / [EPW][BM]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + C::EPI_BYTES + C::Z_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;   // [2] accumulator ready

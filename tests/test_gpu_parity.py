@@ -145,6 +145,7 @@ def test_c2_score_pipelined_and_host_fed_match(c2):
     torch.cuda.synchronize()
     dev_in = [to_dev(bt) for bt in batches]
     outs = [torch.empty(bt.batch, device="cuda") for bt in batches]
+    torch.cuda.synchronize()  # the side streams do not order after the current stream's copies
     for (idx, off, dense), bt, o in zip(dev_in, batches, outs):
         m.score(idx, off, bt.batch, dense, o, s_embed=s_e, s_dense=s_d)
     s_d.synchronize()
