@@ -191,7 +191,10 @@ def launch_work(cfg, B) -> dict:
                   # out-projection and FFN2 run as one GEMM over [O | h] (K = D + F), + fp32 branch sum, LN
                   "gemm_ens_ffn2_ln": g(2 * BT * (F + D) * D, 2 * (BT * (F + D) + (F + D) * D + BT * D)
                                         + 4 * BT * D + 12 * D),
-                  "mha64": g(4 * B * H * S * S * (D // H), 2 * (3 * BT * D + BT * D))})
+                  "mha64": g(4 * B * H * S * S * (D // H), 2 * (3 * BT * D + BT * D)),
+                  # QKV projection + attention in one GEMM (option ens_fused_attn): X in, O out, qkv never stored
+                  "gemm_ens_qkv_attn": g(2 * BT * D * 3 * D + 4 * B * H * S * S * (D // H),
+                                         2 * (BT * D + 3 * D * D + BT * D) + 12 * D)})
     return w
 
 

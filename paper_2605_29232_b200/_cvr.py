@@ -391,9 +391,9 @@ class CvrModel:
         self._check(self.L.cvr_profile_begin(self.h, max_launches))
 
     def profile_end(self) -> Dict[str, dict]:
-        buf = (cvr_kernel_stat * 16)()
+        buf = (cvr_kernel_stat * 32)()
         n = ctypes.c_int()
-        self._check(self.L.cvr_profile_end(self.h, buf, 16, ctypes.byref(n)))
+        self._check(self.L.cvr_profile_end(self.h, buf, 32, ctypes.byref(n)))
         return {buf[i].name.decode(): {"launches": buf[i].launches, "total_ms": buf[i].total_ms,
                                         "avg_ms": buf[i].total_ms / max(1, buf[i].launches),
                                         "min_ms": buf[i].min_ms, "max_ms": buf[i].max_ms}

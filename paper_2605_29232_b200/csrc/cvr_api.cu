@@ -26,12 +26,13 @@ using namespace cvr;
 enum KernelId {
   K_EMBED = 0, K_GEMM_V, K_GEMM_U, K_GEMM_MLP, K_GEMM_HEAD, K_DENSE_F32, K_UNPACK, K_CROSS_FUSED,
   K_ENS_QKV, K_MHA, K_ENS_OPROJ, K_ENS_FFN1, K_ENS_FFN2_LN, K_HEAD_FIN, K_CROSS_STACK,
-  K_MASK_PROJ, K_MASK_HIDDEN, K_MASK_MUL, K_COUNT
+  K_MASK_PROJ, K_MASK_HIDDEN, K_MASK_MUL, K_ENS_QKV_ATTN, K_COUNT
 };
 static const char* kKernelNames[K_COUNT] = {
     "embed_bag_pool", "gemm_xV",  "gemm_tU_cross",  "gemm_mlp_relu", "gemm_mlp_head", "dense_f32_dcn",
     "shard_unpack",   "cross_fused", "gemm_ens_qkv", "mha64",       "gemm_ens_oproj", "gemm_ens_ffn1",
-    "gemm_ens_ffn2_ln", "head_finalize", "cross_stack", "gemm_mask_proj", "gemm_mask_hidden", "gemm_mask_mul"};
+    "gemm_ens_ffn2_ln", "head_finalize", "cross_stack", "gemm_mask_proj", "gemm_mask_hidden", "gemm_mask_mul",
+    "gemm_ens_qkv_attn"};
 
 namespace {
 
@@ -112,6 +113,8 @@ struct cvr_ctx {
     // against [Wo | W2] (their outputs are summed anyway, A20), saving a launch and an fp32 round trip
     size_t off_S = 0, off_qkv = 0, off_cat = 0;
     std::vector<size_t> off_catW, off_catb;
+    std::vector<size_t> off_qkvh, off_bqkvh;           // Wqkv / bqkv repacked head-major: head h = rows [192 h, +192)
+    std::vector<CUtensorMap> Wqkvh;                    //   = [q_h | k_h | v_h] (the fused QKV + attention GEMM's B)
     CUtensorMap flat_x0[2], tok_x0[2], flat_xa, flat_xb, tok_xa, tok_xb, sttok_xa, sttok_xb;
     CUtensorMap st_qkv, st_hf, tm_cat, tm_O;           // tm_O: cat[:, :D] (fused FFN kernel's A of Wo)
     std::vector<CUtensorMap> W1f, Wcf;                 // fused FFN: W1 box {64,128}, [Wo | W2] box {64,256}
@@ -187,6 +190,7 @@ struct cvr_ctx {
   int pair_xv = 0;
   int xv_bn = 0;
   bool prefetch_b = true;
+  bool ens_fused_attn = false;  // option "ens_fused_attn": config 4's QKV projection + attention as one GEMM
   bool zero_copy_scores = true;  // option "zero_copy_scores": cvr_score_host writes scores into pinned h_scores
   // option "pair_u": the U GEMM (192-wide EIN-ring tiles) as 2-CTA 256-row tiles, each CTA holding half of the U
   // tile.  Bit-exact; measured 89.5 vs 86.3 us per c2 dense stage, 726-732 vs 740 us at c3's rank slice (B = 8192)
@@ -536,6 +540,8 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
     for (int l = 0; l < c->n_cross; ++l) {
       c->ens.off_catW.push_back(carve(cur, (size_t)c->d * (c->d + c->ffn) * 2));
       c->ens.off_catb.push_back(carve(cur, (size_t)c->d * 4));
+      c->ens.off_qkvh.push_back(carve(cur, (size_t)3 * c->d * c->d * 2));
+      c->ens.off_bqkvh.push_back(carve(cur, (size_t)3 * c->d * 4));
     }
     for (int i = 0; i + 1 < c->n_mlp; ++i) c->off_h.push_back(carve(cur, (size_t)B * c->mlp[i] * 2));
   } else if (c->backbone == CVR_MASKNET) {
@@ -898,6 +904,7 @@ int encode_plan_ensemble(cvr_ctx* c) {
   E.V.assign(c->n_cross, {});
   E.U.assign(c->n_cross, {});
   E.Wqkv.assign(c->n_cross, {});
+  E.Wqkvh.assign(c->n_cross, {});
   E.W1.assign(c->n_cross, {});
   E.Wcat.assign(c->n_cross, {});
   E.W1f.assign(c->n_cross, {});
@@ -924,6 +931,21 @@ int encode_plan_ensemble(cvr_ctx* c) {
     ok &= encode_tmap_bf16(&E.Wcat[l], c->ws + E.off_catW[l], D, D + F, D + F, 256 / dv, &er) == 0;
     ok &= encode_tmap_bf16(&E.W1f[l], c->wptr(p + "ffn/W1"), F, D, D, 128, &er) == 0;
     ok &= encode_tmap_bf16(&E.Wcf[l], c->ws + E.off_catW[l], D, D + F, D + F, 256, &er) == 0;
+    // head-major [q_h | k_h | v_h] copies of Wqkv / bqkv for the fused QKV + attention GEMM (EPI_ATTN)
+    if (D == 64 * c->n_heads) {
+      std::vector<float> bq(3 * D), bh(3 * D);
+      cudaError_t e6 = cudaMemcpy(bq.data(), c->wptr(p + "mha/bqkv"), 3 * D * 4, cudaMemcpyDeviceToHost);
+      for (int h = 0; h < c->n_heads && e6 == cudaSuccess; ++h)
+        for (int m = 0; m < 3; ++m) {
+          e6 = cudaMemcpy(c->ws + E.off_qkvh[l] + ((size_t)h * 192 + m * 64) * D * 2,
+                          c->wptr<uint8_t>(p + "mha/Wqkv") + ((size_t)m * D + h * 64) * D * 2, (size_t)64 * D * 2,
+                          cudaMemcpyDeviceToDevice);
+          for (int j = 0; j < 64; ++j) bh[h * 192 + m * 64 + j] = bq[m * D + h * 64 + j];
+        }
+      if (e6 == cudaSuccess) e6 = cudaMemcpy(c->ws + E.off_bqkvh[l], bh.data(), 3 * D * 4, cudaMemcpyHostToDevice);
+      if (e6 != cudaSuccess) return c->fail(CVR_E_CUDA, "assembling the head-major Wqkv");
+      ok &= encode_tmap_bf16(&E.Wqkvh[l], c->ws + E.off_qkvh[l], 3 * D, D, D, 192, &er) == 0;
+    }
   }
   if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
   // head MLP: same plan as the low-rank path (GemmPlan per mlp layer)
@@ -1300,15 +1322,26 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     a2.ld_f32 = W;
     if ((e = run_gemm(c, a2, K_GEMM_U, s)) != cudaSuccess) return c->cuda_fail(e, "ens U");
     // MHA branch: qkv = X Wqkv^T + b ; O = attention ; S += O Wo^T + bo
-    GemmArgs a3 = ga(tok_xl, &E.Wqkv[l], BT, 3 * D, D, 256, EPI_BIAS);
-    a3.tmOut = &E.st_qkv;
-    a3.bias = c->wptr<float>(p + "mha/bqkv");
-    if ((e = run_gemm(c, a3, K_ENS_QKV, s)) != cudaSuccess) return c->cuda_fail(e, "ens qkv");
     __nv_bfloat16* cat = c->at<__nv_bfloat16>(E.off_cat);
-    c->pbeg(s);
-    e = launch_mha64(c->at<__nv_bfloat16>(E.off_qkv), cat, D + c->ffn, B, c->n_heads, s);  // O -> cat[:, :D]
-    c->pend(K_MHA, s);
-    if (e != cudaSuccess) return c->cuda_fail(e, "mha64");
+    if (c->ens_fused_attn && D == 64 * c->n_heads) {
+      // one GEMM: each 128-token x 192 tile [q_h | k_h | v_h] (+ b) is attended in its epilogue, O -> cat[:, 64 h ..]
+      // (the qkv tensor never reaches HBM; same bf16 roundings and attention core as qkv GEMM + mha64)
+      GemmArgs a3 = ga(tok_xl, &E.Wqkvh[l], BT, 3 * D, D, 192, EPI_ATTN);
+      a3.cta_pair = false;
+      a3.bias = c->at<float>(E.off_bqkvh[l]);
+      a3.out_bf16 = cat;
+      a3.ld_x = D + c->ffn;
+      if ((e = run_gemm(c, a3, K_ENS_QKV_ATTN, s)) != cudaSuccess) return c->cuda_fail(e, "ens qkv + attention");
+    } else {
+      GemmArgs a3 = ga(tok_xl, &E.Wqkv[l], BT, 3 * D, D, 256, EPI_BIAS);
+      a3.tmOut = &E.st_qkv;
+      a3.bias = c->wptr<float>(p + "mha/bqkv");
+      if ((e = run_gemm(c, a3, K_ENS_QKV, s)) != cudaSuccess) return c->cuda_fail(e, "ens qkv");
+      c->pbeg(s);
+      e = launch_mha64(c->at<__nv_bfloat16>(E.off_qkv), cat, D + c->ffn, B, c->n_heads, s);  // O -> cat[:, :D]
+      c->pend(K_MHA, s);
+      if (e != cudaSuccess) return c->cuda_fail(e, "mha64");
+    }
     if (c->ens_fused_ffn && D == 256 && c->ffn == 1024) {
       // FFN + out-projection + branch-sum LN in one kernel: the FFN hidden never leaves the SM (ens_ffn.cu)
       EnsFfnArgs f{};
@@ -2140,6 +2173,12 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);
+    return CVR_OK;
+  }
+  if (!strcmp(key, "ens_fused_attn")) {
+    c->ens_fused_attn = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
     return CVR_OK;
   }
   if (!strcmp(key, "prefetch_b")) {

@@ -91,7 +91,9 @@ enum Epi {
   EPI_BIAS_ADD_F32 = 6,  // fp32 C + b + in_f32                          (ensemble MHA out-proj)
   EPI_SUM_LN = 7,        // bf16 LN_row(C + b + in_f32) * gamma + beta   (ensemble FFN2 + LN, BN == N)
   EPI_HEAD_PARTIAL = 8,  // fp32 partial[m][tile] = ReLU(C + b) . m over the tile's columns
-  EPI_MASK = 9           // bf16 (C + b) * x_l: MaskNet block, mask applied to x_l (tmXl), no residual
+  EPI_MASK = 9,          // bf16 (C + b) * x_l: MaskNet block, mask applied to x_l (tmXl), no residual
+  EPI_ATTN = 10          // config 4: the 128 x 192 tile [q_h | k_h | v_h] (+ b) of 2 examples' tokens -> attention of
+                         // head h = N tile -> O (bf16) at out_bf16[token, 64 h ..] (row stride ld_x); BN = 192
 };
 
 struct GemmArgs {

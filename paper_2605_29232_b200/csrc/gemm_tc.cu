@@ -27,6 +27,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include "cvr_attn.cuh"
 #include "cvr_kernels.cuh"
 #include "cvr_ptx.cuh"
 #include "cvr_tile.cuh"
@@ -73,14 +74,18 @@ struct Cfg {
   static constexpr bool SPLIT = (EPI == EPI_STORE || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS || EPI == EPI_HEAD) && CN == 1;
   // EW caps the split: EW = 1 when each CTA runs several tiles (the epilogue then overlaps the next tile's
   // mainloop anyway) keeps the CTA at 7 warps, leaving registers for co-resident embedding CTAs
-  static constexpr int EPW = RING ? 3 : (SPLIT ? (BN / 64 < EW ? BN / 64 : EW) : 1);
+  // EPI_ATTN: 8 epilogue warps = 2 examples x 4 groups of 16 query rows (one attention warp each)
+  static constexpr bool ATTN = EPI == EPI_ATTN;
+  static constexpr int EPW = RING ? 3 : (ATTN ? 2 : (SPLIT ? (BN / 64 < EW ? BN / 64 : EW) : 1));
   static constexpr int COLS_W = BN / EPW;           // columns per epilogue warp
   static constexpr int PRODUCER_B = 2 + 4 * EPW;
   static constexpr int PRODUCER_E = PRODUCER_B + 1;  // EIN producer (RING only)
   static constexpr int NT = 32 * (PRODUCER_B + (RING ? 2 : 1));
   static constexpr int OUT_BYTES = EpiTraits<EPI>::kSmemOut && !RING ? NSUB * SUB : 0;     // per buffer
   static constexpr int EIN_BYTES = EpiTraits<EPI>::kEin && !RING ? EpiTraits<EPI>::kEinTensors * NSUB * SUB : 0;  // per acc
-  static constexpr int EPI_BYTES = OUT_BUFS * OUT_BYTES + 2 * EIN_BYTES + (RING ? RING_SLOTS * 2 * SUB : 0);
+  static constexpr int ATT_LD = 72;  // EPI_ATTN staging row stride (elements): conflict-free ldmatrix
+  static constexpr int ATT_BYTES = ATTN ? 3 * BM * ATT_LD * 2 : 0;  // Q | K | V of the tile's 128 tokens, bf16
+  static constexpr int EPI_BYTES = OUT_BUFS * OUT_BYTES + 2 * EIN_BYTES + (RING ? RING_SLOTS * 2 * SUB : 0) + ATT_BYTES;
   static constexpr int BAR_BYTES = 512;
   // EPI_HEAD across a CN-cluster: per-tile partial dot products gathered in rank 0 ([2][CN][BM] fp32)
   static constexpr int Z_BYTES = (EPI == EPI_HEAD && CN > 1) ? 2 * CN * BM * 4 : (EPI == EPI_HEAD ? EPW * BM * 4 : 0);
@@ -447,6 +452,56 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
           ptx::mbar_arrive(&eempty[j]);
         }
         __syncwarp();
+      } else if constexpr (C::ATTN) {
+        // ---- fused QKV projection + attention (config 4, SURVEY.md §8(a) S5', A20): this tile is rows [m0, m0+128)
+        // = two examples' 64 tokens, columns [q_h | k_h | v_h] of head h = tn (weights repacked head-major at load)
+        __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(sOut);  // [3][128][ATT_LD]
+        constexpr int LDA = C::ATT_LD;
+        // (1) accumulator + bias -> bf16 Q / K / V rows (the QKV GEMM's EPI_BIAS rounding); warp (q, part) converts
+        //     its TMEM quadrant's 32 rows, columns [96 part, 96 part + 96)
+#pragma unroll 1
+        for (int cc = 0; cc < 3; ++cc) {
+          const int c = part * 96 + cc * 32;
+          float v[32];
+          ld32_tmem(trow + c, v);
+          const float4* b4 = reinterpret_cast<const float4*>(g.bias + n0 + c);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float4 bb = __ldg(b4 + u);
+            v[4 * u] += bb.x;
+            v[4 * u + 1] += bb.y;
+            v[4 * u + 2] += bb.z;
+            v[4 * u + 3] += bb.w;
+          }
+          __nv_bfloat16* dst = qs + ((c >> 6) * BM + r) * LDA + (c & 63);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint4 o;
+            o.x = ptx::pack_bf16(v[8 * u], v[8 * u + 1]);
+            o.y = ptx::pack_bf16(v[8 * u + 2], v[8 * u + 3]);
+            o.z = ptx::pack_bf16(v[8 * u + 4], v[8 * u + 5]);
+            o.w = ptx::pack_bf16(v[8 * u + 6], v[8 * u + 7]);
+            *reinterpret_cast<uint4*>(dst + 8 * u) = o;
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tempty[a]);  // the accumulator is free for the tile after next
+        ptx::named_bar_sync(1, 32 * 4 * C::EPW);     // every token's Q / K / V is staged
+        // (2) attention (cvr_attn.cuh, the mha64 core): warp ew = 4 part + q -> example ew / 4, query rows 16 (ew % 4)
+        const int ew = part * 4 + q, ex = ew >> 2, r0 = (ew & 3) * 16;
+        __nv_bfloat16* Qs = qs + (ex * 64) * LDA;
+        attn::rows16<LDA>(Qs, qs + (BM + ex * 64) * LDA, qs + (2 * BM + ex * 64) * LDA, r0, lane);
+        __syncwarp();
+        // (3) O rows -> out (16 rows x 128 B, coalesced 16-byte chunks)
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const int row = p * 4 + (lane >> 3), ch = lane & 7, tok = m0 + ex * 64 + r0 + row;
+          if (tok < M)
+            *reinterpret_cast<uint4*>(g.out_bf16 + (int64_t)tok * g.ld_x + tn * 64 + ch * 8) =
+                *reinterpret_cast<const uint4*>(Qs + (r0 + row) * LDA + ch * 8);
+        }
+        ptx::named_bar_sync(1, 32 * 4 * C::EPW);  // the staging buffer is free for the next tile
       } else if constexpr (EPI == EPI_SUM_LN) {
         // pass 1: y = acc + b + in, written back into TMEM; row sum
         float sum = 0.f;
@@ -542,8 +597,8 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
           }
         }
       }
-      // accumulator (and epilogue inputs) consumed: hand them back
-      if constexpr (!C::RING) {
+      // accumulator (and epilogue inputs) consumed: hand them back (RING / ATTN warps did so themselves)
+      if constexpr (!C::RING && !C::ATTN) {
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -705,6 +760,10 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
     CVR_E1(128, EPI_BIAS)
     CVR_E1(256, EPI_BIAS)
 #undef CVR_E1
+  }
+  if (g.epi == EPI_ATTN) {
+    if (g.BN != 192 || g.N % 192 || g.cta_pair || !g.out_bf16 || !g.bias || g.ld_x % 8) return cudaErrorInvalidValue;
+    return launch_t<192, EPI_ATTN>(g, s);
   }
 #define CVR_CASE(BN_, EPI_) \
   if (g.BN == BN_ && g.epi == EPI_) return g.cta_pair ? launch_t<BN_, EPI_, false, 2>(g, s) : launch_t<BN_, EPI_>(g, s);

@@ -22,7 +22,7 @@ for st in settings:
         m.dense(x0, B, sc, stream=s)
     torch.cuda.synchronize()
     m.profile_begin(4000)
-    for _ in range(100):
+    for _ in range(int(os.environ.get("K", "100"))):
         m.dense(x0, B, sc, stream=s)
     torch.cuda.synchronize()
     prof = m.profile_end()

@@ -82,3 +82,23 @@ def test_c4_fused_ffn_bitexact(c4small, B):
     finally:
         m.set_option("ens_fused_ffn", 0)
     assert torch.equal(s_f, s_u)
+
+
+@pytest.mark.parametrize("B", [131, 512])
+def test_c4_fused_qkv_attention_bitexact(c4small, B):
+    """Option ens_fused_attn: the QKV projection and the 64-token attention as ONE GEMM (EPI_ATTN: each 128-token x
+    192 tile [q_h | k_h | v_h] + b is rounded to bf16 in shared memory and attended in the epilogue with the
+    mha64 core) -- the same roundings and the same attention code, so scores are bit-identical to QKV GEMM +
+    mha64.  B = 131: the last tile holds one example (its second half is out of range and never stored)."""
+    cfg, m, tabs, w = c4small
+    bt = cs.make_batch(cfg, 8, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    s0 = m.dense(x0, B).clone()
+    m.set_option("ens_fused_attn", 1)
+    try:
+        s1 = m.dense(x0, B).clone()
+    finally:
+        m.set_option("ens_fused_attn", 0)
+    assert m.status() == 0
+    assert torch.equal(s0, s1)
