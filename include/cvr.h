@@ -244,7 +244,9 @@ int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d
  * global scratch (same sums, same order); "xv_bn" [0 = by wave count] N tile of t = x_l V^T (64, 128, 256);
  * "pair_xv" [0] / "pair_mlp" [0] 2-CTA (cta_group::2) tiles for the xV (value = BN) / hidden MLP GEMMs;
  * "prefetch_b" [1] each GEMM issues its first ring stages' weight loads before waiting for the previous
- * kernel; "epw" [2] epilogue warps per TMEM quadrant:
+ * kernel; "ens_fused_attn" [1] config 4's QKV projection + attention as one GEMM (attention in the epilogue);
+ * "pair_u" [0] 2-CTA tiles for the low-rank U GEMM; "zero_copy_scores" [1] cvr_score_host stores the scores
+ * straight into page-locked h_scores; "epw" [2] epilogue warps per TMEM quadrant:
  * 0 one, 1 up to 4 (one 64-column sub-tile each), 2 split only when a CTA runs <= 2 tiles; "mb" [0] weight
  * tiles multicast over clusters of 8 row blocks; "ens_fused_ffn" [0] config 4's FFN + out-projection + LN as
  * one kernel; "mask_grouped" [1] MaskNet's parallel blocks as one grouped GEMM.  Variants are bit-identical

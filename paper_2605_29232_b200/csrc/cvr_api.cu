@@ -190,7 +190,10 @@ struct cvr_ctx {
   int pair_xv = 0;
   int xv_bn = 0;
   bool prefetch_b = true;
-  bool ens_fused_attn = false;  // option "ens_fused_attn": config 4's QKV projection + attention as one GEMM
+  // option "ens_fused_attn" [1]: config 4's QKV projection + attention as one GEMM (EPI_ATTN; the qkv tensor,
+  // 805 MB per layer at B = 8192, never reaches HBM).  Bit-identical to QKV GEMM + mha64; measured per layer
+  // 381 us vs 257 + 247 (two epilogue groups; one group: 519 -- the attention warps' latency bounds each tile)
+  bool ens_fused_attn = true;
   bool zero_copy_scores = true;  // option "zero_copy_scores": cvr_score_host writes scores into pinned h_scores
   // option "pair_u": the U GEMM (192-wide EIN-ring tiles) as 2-CTA 256-row tiles, each CTA holding half of the U
   // tile.  Bit-exact; measured 89.5 vs 86.3 us per c2 dense stage, 726-732 vs 740 us at c3's rank slice (B = 8192)

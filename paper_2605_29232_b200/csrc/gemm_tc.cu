@@ -76,7 +76,10 @@ struct Cfg {
   // mainloop anyway) keeps the CTA at 7 warps, leaving registers for co-resident embedding CTAs
   // EPI_ATTN: 8 epilogue warps = 2 examples x 4 groups of 16 query rows (one attention warp each)
   static constexpr bool ATTN = EPI == EPI_ATTN;
-  static constexpr int EPW = RING ? 3 : (ATTN ? 2 : (SPLIT ? (BN / 64 < EW ? BN / 64 : EW) : 1));
+  // ATTN: two groups of 8 epilogue warps take alternate tiles (accumulator a = group), each with its own staging,
+  // so one tile's attention overlaps the next one's
+  static constexpr int ATT_GROUPS = 2;
+  static constexpr int EPW = RING ? 3 : (ATTN ? 2 * ATT_GROUPS : (SPLIT ? (BN / 64 < EW ? BN / 64 : EW) : 1));
   static constexpr int COLS_W = BN / EPW;           // columns per epilogue warp
   static constexpr int PRODUCER_B = 2 + 4 * EPW;
   static constexpr int PRODUCER_E = PRODUCER_B + 1;  // EIN producer (RING only)
@@ -84,7 +87,8 @@ struct Cfg {
   static constexpr int OUT_BYTES = EpiTraits<EPI>::kSmemOut && !RING ? NSUB * SUB : 0;     // per buffer
   static constexpr int EIN_BYTES = EpiTraits<EPI>::kEin && !RING ? EpiTraits<EPI>::kEinTensors * NSUB * SUB : 0;  // per acc
   static constexpr int ATT_LD = 72;  // EPI_ATTN staging row stride (elements): conflict-free ldmatrix
-  static constexpr int ATT_BYTES = ATTN ? 3 * BM * ATT_LD * 2 : 0;  // Q | K | V of the tile's 128 tokens, bf16
+  static constexpr int ATT_BUF = 3 * BM * ATT_LD * 2;                 // Q | K | V of a tile's 128 tokens, bf16
+  static constexpr int ATT_BYTES = ATTN ? ATT_GROUPS * ATT_BUF : 0;
   static constexpr int EPI_BYTES = OUT_BUFS * OUT_BYTES + 2 * EIN_BYTES + (RING ? RING_SLOTS * 2 * SUB : 0) + ATT_BYTES;
   static constexpr int BAR_BYTES = 512;
   // EPI_HEAD across a CN-cluster: per-tile partial dot products gathered in rank 0 ([2][CN][BM] fp32)
@@ -192,7 +196,8 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 4 * C::EPW * CG);  // every epilogue warp of the pair
+      ptx::mbar_init(&tempty[a], C::ATTN ? 4 * C::EPW / C::ATT_GROUPS : 4 * C::EPW * CG);  // every epilogue warp
+                                                                                           // (ATTN: of one group)
     }
     for (int e = 0; e < 3; ++e) {
       ptx::mbar_init(&efull[e], 1);
@@ -394,6 +399,9 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
       const int m = m0 + r;
       const bool live = m < M;
       const int a = it & 1;
+      if constexpr (C::ATTN) {
+        if (a != (part >> 1)) continue;  // the other group's tile (its accumulator index)
+      }
       ptx::mbar_wait(&tfull[a], (it >> 1) & 1);
       if (it == 0 && warp == 2 && lane == 0) stamp(g.dbg, 4);
       ptx::tc_fence_after();
@@ -455,13 +463,14 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
       } else if constexpr (C::ATTN) {
         // ---- fused QKV projection + attention (config 4, SURVEY.md §8(a) S5', A20): this tile is rows [m0, m0+128)
         // = two examples' 64 tokens, columns [q_h | k_h | v_h] of head h = tn (weights repacked head-major at load)
-        __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(sOut);  // [3][128][ATT_LD]
+        const int grp = part >> 1, gpart = part & 1;  // group = accumulator of its tiles; 2 warps per quadrant
+        __nv_bfloat16* qs = reinterpret_cast<__nv_bfloat16*>(sOut + grp * C::ATT_BUF);  // [3][128][ATT_LD]
         constexpr int LDA = C::ATT_LD;
         // (1) accumulator + bias -> bf16 Q / K / V rows (the QKV GEMM's EPI_BIAS rounding); warp (q, part) converts
         //     its TMEM quadrant's 32 rows, columns [96 part, 96 part + 96)
 #pragma unroll 1
         for (int cc = 0; cc < 3; ++cc) {
-          const int c = part * 96 + cc * 32;
+          const int c = gpart * 96 + cc * 32;
           float v[32];
           ld32_tmem(trow + c, v);
           const float4* b4 = reinterpret_cast<const float4*>(g.bias + n0 + c);
@@ -487,9 +496,9 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&tempty[a]);  // the accumulator is free for the tile after next
-        ptx::named_bar_sync(1, 32 * 4 * C::EPW);     // every token's Q / K / V is staged
-        // (2) attention (cvr_attn.cuh, the mha64 core): warp ew = 4 part + q -> example ew / 4, query rows 16 (ew % 4)
-        const int ew = part * 4 + q, ex = ew >> 2, r0 = (ew & 3) * 16;
+        ptx::named_bar_sync(1 + grp, 32 * 8);     // every token's Q / K / V is staged
+        // (2) attention (cvr_attn.cuh, the mha64 core): warp ew = 4 gpart + q -> example ew / 4, query rows 16 (ew % 4)
+        const int ew = gpart * 4 + q, ex = ew >> 2, r0 = (ew & 3) * 16;
         __nv_bfloat16* Qs = qs + (ex * 64) * LDA;
         attn::rows16<LDA>(Qs, qs + (BM + ex * 64) * LDA, qs + (2 * BM + ex * 64) * LDA, r0, lane);
         __syncwarp();
@@ -501,7 +510,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
             *reinterpret_cast<uint4*>(g.out_bf16 + (int64_t)tok * g.ld_x + tn * 64 + ch * 8) =
                 *reinterpret_cast<const uint4*>(Qs + (r0 + row) * LDA + ch * 8);
         }
-        ptx::named_bar_sync(1, 32 * 4 * C::EPW);  // the staging buffer is free for the next tile
+        ptx::named_bar_sync(1 + grp, 32 * 8);  // the group's staging buffer is free for its next tile
       } else if constexpr (EPI == EPI_SUM_LN) {
         // pass 1: y = acc + b + in, written back into TMEM; row sum
         float sum = 0.f;

@@ -94,11 +94,11 @@ def test_c4_fused_qkv_attention_bitexact(c4small, B):
     bt = cs.make_batch(cfg, 8, batch=B)
     idx, off, dense = to_dev(bt)
     x0 = m.embed(idx, off, B, dense)
-    s0 = m.dense(x0, B).clone()
-    m.set_option("ens_fused_attn", 1)
+    s1 = m.dense(x0, B).clone()  # fused (default)
+    m.set_option("ens_fused_attn", 0)
     try:
-        s1 = m.dense(x0, B).clone()
+        s0 = m.dense(x0, B).clone()
     finally:
-        m.set_option("ens_fused_attn", 0)
+        m.set_option("ens_fused_attn", 1)
     assert m.status() == 0
     assert torch.equal(s0, s1)
