@@ -14,7 +14,7 @@ src = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "gpurun_out")
 
 # kernel template -> role (gemm_bf16_kernel<BN, EPI, AR, CG, CN>; Epi enum in cvr_kernels.cuh)
 EPI = {0: "STORE", 1: "BIAS_RELU", 2: "CROSS", 3: "HEAD", 4: "BIAS", 5: "CROSS_F32", 6: "BIAS_ADD_F32", 7: "SUM_LN",
-       8: "HEAD_PARTIAL", 9: "MASK"}
+       8: "HEAD_PARTIAL", 9: "MASK", 10: "ATTN"}
 
 
 def role(name):
@@ -23,7 +23,7 @@ def role(name):
         bn, epi, ar, cg, cn = [int(x) for x in m.group(1).split(",")][:5]
         # role names of config 2 (for c6: BIAS_RELU = projection / mask hidden / MLP, MASK = mask blocks)
         r = {(0,): "gemm_xV", (2,): "gemm_tU_cross", (1,): "gemm_mlp_relu", (3,): "gemm_mlp_head",
-             (9,): "gemm_mask_mul"}.get((epi,), f"gemm_{EPI.get(epi, epi)}")
+             (9,): "gemm_mask_mul", (10,): "gemm_ens_qkv_attn"}.get((epi,), f"gemm_{EPI.get(epi, epi)}")
         return f"{r} [BN={bn}{' pair' if cg == 2 else ''}{' cluster%d' % cn if cn > 1 else ''}]"
     for k in ("embed_bag", "gemm_splitk", "dense_f32", "unpack", "mha64", "head_finalize", "cross_stack", "cross_fused"):
         if k in name:
