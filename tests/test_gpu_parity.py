@@ -431,3 +431,34 @@ def test_c2_many_tiles_per_cta_bitexact(B):
     xs = x0[torch.from_numpy(sel).cuda(), :cfg.width].double().cpu().numpy()
     ref = O.dense_forward(cfg, {k: O.to_f64(v) for k, v in w.items()}, xs)["scores"]
     assert np.abs(s192[torch.from_numpy(sel).cuda()].double().cpu().numpy() - ref).max() <= TOL_BF16
+
+
+def test_c2_api_error_paths(c2):
+    """The boundary's error convention (cvr.h): host-side validation returns a status and never
+    launches -- batch > max_batch and unknown options -> CVR_E_ARG, a weight of the wrong shape / an unknown name ->
+    CVR_E_SHAPE -- and batch 0 is a no-op; the context stays usable afterwards (scores unchanged)."""
+    from paper_2605_29232_b200._cvr import CvrError
+    cfg, m, tabs, w = c2
+    bt = cs.make_batch(cfg, 70, batch=64)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, 64, dense)
+    s_before = m.dense(x0, 64).clone()
+    big = torch.zeros(4097, 1792, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(CvrError) as e:
+        m.dense(big, 4097)
+    assert e.value.status == 1                                   # CVR_E_ARG
+    with pytest.raises(CvrError) as e:
+        m.set_option("no_such_option", 1)
+    assert e.value.status == 1
+    bad = {"mlp/0/W": torch.zeros(1024, 1000, dtype=torch.bfloat16, device="cuda")}
+    with pytest.raises(CvrError) as e:
+        m.load_weights(bad)
+    assert e.value.status == 2                                   # CVR_E_SHAPE
+    with pytest.raises(CvrError) as e:
+        m.load_weights({"mlp/9/W": torch.zeros(8, 8, dtype=torch.bfloat16, device="cuda")})
+    assert e.value.status == 2
+    sc = torch.full((4,), -1.0, device="cuda")
+    m.dense(x0, 0, scores=sc)                                    # batch 0: nothing to do (pointers still checked)
+    assert torch.all(sc == -1.0)
+    assert m.status() == 0
+    assert torch.equal(m.dense(x0, 64), s_before)
