@@ -194,6 +194,7 @@ struct cvr_ctx {
   // 805 MB per layer at B = 8192, never reaches HBM).  Bit-identical to QKV GEMM + mha64; measured per layer
   // 381 us vs 257 + 247 (two epilogue groups; one group: 519 -- the attention warps' latency bounds each tile)
   bool ens_fused_attn = true;
+  bool ens_attn_ar = false;     // option "ens_attn_ar": the fused QKV + attention GEMM with a resident X tile
   bool zero_copy_scores = true;  // option "zero_copy_scores": cvr_score_host writes scores into pinned h_scores
   // option "pair_u": the U GEMM (192-wide EIN-ring tiles) as 2-CTA 256-row tiles, each CTA holding half of the U
   // tile.  Bit-exact; measured 89.5 vs 86.3 us per c2 dense stage, 726-732 vs 740 us at c3's rank slice (B = 8192)
@@ -1331,6 +1332,7 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
       // (the qkv tensor never reaches HBM; same bf16 roundings and attention core as qkv GEMM + mha64)
       GemmArgs a3 = ga(tok_xl, &E.Wqkvh[l], BT, 3 * D, D, 192, EPI_ATTN);
       a3.cta_pair = false;
+      a3.a_resident = c->ens_attn_ar;  // the 128-token X tile stays resident across its 4 heads' tiles
       a3.bias = c->at<float>(E.off_bqkvh[l]);
       a3.out_bf16 = cat;
       a3.ld_x = D + c->ffn;
@@ -2176,6 +2178,12 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);
+    return CVR_OK;
+  }
+  if (!strcmp(key, "ens_attn_ar")) {
+    c->ens_attn_ar = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
     return CVR_OK;
   }
   if (!strcmp(key, "ens_fused_attn")) {
