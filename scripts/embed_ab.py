@@ -12,6 +12,16 @@ ring = [cs.make_batch(cfg, 700 + i, index_mode=os.environ.get("IDX")) for i in r
 dev = [(torch.from_numpy(b.indices).cuda(), torch.from_numpy(b.offsets).cuda(), torch.from_numpy(b.dense).cuda()) for b in ring]
 row = cfg.dim * (4 if cfg.emb_dtype == "f32" else 2); act = 4 if cfg.act_dtype == "f32" else 2
 byts = sum(b.nnz * (row + 4) + (cfg.n_tables * B + 1) * 4 + B * cfg.n_tables * cfg.dim * act + B * cfg.n_dense * (4 + act) for b in ring) / len(ring)
+import numpy as np
+
+
+def distinct_rows(b):  # compulsory traffic: every distinct (table, row) once
+    offs = b.offsets.astype(np.int64)
+    return sum(len(np.unique(b.indices[offs[t * B]:offs[(t + 1) * B]])) for t in range(cfg.n_tables))
+
+
+cbyts = sum(distinct_rows(b) * row + b.nnz * 4 + (cfg.n_tables * B + 1) * 4 + B * cfg.n_tables * cfg.dim * act
+            + B * cfg.n_dense * (4 + act) for b in ring) / len(ring)
 s = torch.cuda.Stream()
 x0 = m.new_x0(B)
 K = 200
@@ -23,5 +33,8 @@ for rep in range(3):
         torch.cuda.synchronize()
         import bench
         us = bench.time_enqueued(lambda i: m.embed(*dev[i % 4][:2], B, dev[i % 4][2], x0=x0, stream=s), K, s) * 1e3
-        print(json.dumps({"cfg": cfg.name, "variant": v2, "us": round(us, 2), "GBps_alg": round(byts / us / 1e3, 1), "frac_hbm": round(byts / us / 1e3 / 6556.5, 3)}))
+        print(json.dumps({"cfg": cfg.name, "index_mode": os.environ.get("IDX") or cfg.zipf_mode, "variant": v2,
+                          "us": round(us, 2), "GBps_alg": round(byts / us / 1e3, 1),
+                          "frac_hbm": round(byts / us / 1e3 / 6556.5, 3),
+                          "frac_hbm_compulsory": round(cbyts / us / 1e3 / 6556.5, 3)}))
 assert m.status(s) == 0
