@@ -144,7 +144,7 @@ int cvr_load_tables(cvr_ctx* ctx, int n, const int* table_ids, const void* const
  *   "mlp/<i>/W" [h_i, h_{i-1}], "mlp/<i>/b" [h_i], "head/w" [1, h_last], "head/b" [1]
  * shapes is flattened: entry i has ndims[i] extents starting at the running offset.
  * Every expected name must be present exactly once (else CVR_E_SHAPE); dtypes must be
- * act_dtype (norm/* fp32).  Synchronous; the caller may free its tensors afterwards. */
+ * act_dtype (the norm/ entries fp32).  Synchronous; the caller may free its tensors afterwards. */
 int cvr_load_weights(cvr_ctx* ctx, int n, const char* const* names, const void* const* d_ptrs,
                      const int* dtypes, const int* ndims, const int64_t* shapes);
 

@@ -1512,8 +1512,6 @@ int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, const CUtenso
     if (e != cudaSuccess) return c->cuda_fail(e, "dense_f32 launch");
     return CVR_OK;
   }
-  const float* hb = nullptr;  // (unused; keeps the two backbones' code paths parallel)
-  (void)hb;
   if (c->backbone == CVR_ENSEMBLE) return do_dense_ensemble(c, x0, tm_x0, tm_x0_tok, B, scores, s);
   if (c->backbone == CVR_MASKNET) return do_dense_masknet(c, tm_x0, B, scores, s);
   // ---- bf16 low-rank DCN-v2 on tcgen05
