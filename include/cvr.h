@@ -236,10 +236,10 @@ int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d
  * occupancy (rows of <= 128 B loaded without L1 allocation), 1 = warp-batched bags (coalesced offset / index
  * staging), 2 = cooperative index fetch, 3 = as 0 with L1-allocating row loads; "a_resident" [0] the U GEMM of a low-rank cross layer keeps
  * the 128 x r block of t resident in shared memory across its N tiles ("fused_cross" = 1 runs each
- * low-rank cross layer as one clustered kernel (K5) instead of two GEMMs); "mc" [1] clusters of 4 CTAs
- * over adjacent N tiles with the A tile multicast by TMA: 0 = off, 1 = only the head GEMM (N = 4 x 64,
- * the sigmoid's dot product summed over the cluster in DSMEM, fixed order), 2 = every GEMM whose N tiles
- * group by 4; "u_bn" [192] N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64); "xv_splitk" [0]
+ * low-rank cross layer as one clustered kernel (K5) instead of two GEMMs); "mc" [0] clusters of 4 CTAs
+ * over adjacent N tiles with the A tile multicast by TMA: 0 = off (the head as one 256-wide tile per row block,
+ * split epilogue), 1 = only the head GEMM (N = 4 x 64, the sigmoid's dot product summed over the cluster in
+ * DSMEM; same order, same result), 2 = every GEMM whose N tiles group by 4; "u_bn" [192] N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64); "xv_splitk" [0]
  * t = x_l V^T as a K-split cluster GEMM, 1 = partials reduced over DSMEM, 2 = exchanged through an L2-resident
  * global scratch (same sums, same order); "xv_bn" [0 = by wave count] N tile of t = x_l V^T (64, 128, 256);
  * "pair_xv" [0] / "pair_mlp" [0] 2-CTA (cta_group::2) tiles for the xV (value = BN) / hidden MLP GEMMs;
@@ -250,7 +250,7 @@ int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d
  * 0 one, 1 up to 4 (one 64-column sub-tile each), 2 split only when a CTA runs <= 2 tiles; "mb" [0] weight
  * tiles multicast over clusters of 8 row blocks; "ens_fused_ffn" [0] config 4's FFN + out-projection + LN as
  * one kernel; "mask_grouped" [1] MaskNet's parallel blocks as one grouped GEMM.  Variants are bit-identical
- * except xv_splitk (fp32 summation order of t) and mc 0 vs 1 (the head's).  Unknown key or bad value ->
+ * except xv_splitk (fp32 summation order of t).  Unknown key or bad value ->
  * CVR_E_ARG. */
 int cvr_set_option(cvr_ctx* ctx, const char* key, int64_t value);
 

@@ -170,7 +170,7 @@ struct cvr_ctx {
   std::vector<GemmPlan> plan;  // cross layers (V, U interleaved), then MLP
   // quarter maps (box {64, 32}) of the A-operand maps, keyed by the full map: A multicast (GemmPlan::cn)
   std::map<const CUtensorMap*, CUtensorMap> qmaps;
-  int mc = 1;                  // option "mc": 0 off, 1 head only (default), 2 every grouped GEMM
+  int mc = 0;                  // option "mc": 0 off (default), 1 head only, 2 every grouped GEMM
   int u_bn = 192;              // option "u_bn": N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64)
   int epw_mode = 2;            // option "epw": split epilogues 0 never, 1 always, 2 when a CTA has one tile
   // option "ens_fused_ffn" [0]: config 4's FFN + out-projection + LN as one kernel (ens_ffn.cu), bit-identical to
@@ -850,7 +850,9 @@ int encode_plan(cvr_ctx* c) {
   // Clusters of 4 N tiles with A multicast.  Measured on B200 (scripts/dense_kernels.py, B = 4096): the head
   // (N = 256 as 4 x 64 tiles, DSMEM dot-product sum) 15.8 -> 13.3 us per launch; multicast alone does not
   // pay at cluster size 4 (xV 14.7 -> 16.7, MLP 18.4 -> 19.7: unicast reads of a line by <= 4 SMs are
-  // already merged in L2), so option mc = 1 (default) clusters only the head, mc = 2 every grouped GEMM.
+  // already merged in L2); mc = 1 clusters only the head, mc = 2 every grouped GEMM.  Default mc = 0: the head as
+  // one 256-wide tile per row block with a split epilogue, bit-identical to the cluster head and no slower (c2 dense
+  // stage 85.97 vs 86.3 us; pipelined step equal within noise over 1000-step runs), without cluster scheduling.
   auto mc4 = [&](int N, int BN) { return c->mc >= 2 && N % (4 * BN) == 0 && N / BN <= 8 ? 4 : 1; };
   for (int l = 0; l < c->n_cross; ++l) {
     const int bn_v = c->xv_bn ? c->xv_bn : pick_bn_xv(c->r, c->max_batch, c->num_sms > 0 ? c->num_sms : 148);

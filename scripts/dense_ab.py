@@ -31,6 +31,6 @@ for rep in range(3):
         b.record(s); torch.cuda.synchronize()
         res[i].append(a.elapsed_time(b) / K * 1e3)
         for k in st:  # restore defaults
-            m.set_option(k, {"a_resident": 0, "pdl": 1, "fused_cross": 0, "graphs": 1, "stack": 0, "ens_u_bn": 128, "pair": 1, "u_bn": 192, "mc": 1, "mb": 0, "pair_mlp": 0, "pair_xv": 0}.get(k, 1))
+            m.set_option(k, {"a_resident": 0, "pdl": 1, "fused_cross": 0, "graphs": 1, "stack": 0, "ens_u_bn": 128, "pair": 1, "u_bn": 192, "mc": 0, "mb": 0, "pair_mlp": 0, "pair_xv": 0}.get(k, 1))
 for i, st in enumerate(settings):
     print(json.dumps({"setting": st, "us_per_dense": [round(x, 2) for x in res[i]], "min": round(min(res[i]), 2)}))
