@@ -245,6 +245,8 @@ int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d
  * "pair_xv" [0] / "pair_mlp" [0] 2-CTA (cta_group::2) tiles for the xV (value = BN) / hidden MLP GEMMs;
  * "prefetch_b" [1] each GEMM issues its first ring stages' weight loads before waiting for the previous
  * kernel; "ens_fused_attn" [1] config 4's QKV projection + attention as one GEMM (attention in the epilogue);
+ * "f32_tma_store" [1] config 4's fp32 DCN-branch output through staged TMA stores; "ens_attn_ar" [0] the fused
+ * QKV + attention GEMM with its X tile resident across the 4 heads;
  * "pair_u" [0] 2-CTA tiles for the low-rank U GEMM; "zero_copy_scores" [1] cvr_score_host stores the scores
  * straight into page-locked h_scores; "epw" [2] epilogue warps per TMEM quadrant:
  * 0 one, 1 up to 4 (one 64-column sub-tile each), 2 split only when a CTA runs <= 2 tiles; "mb" [0] weight

@@ -117,6 +117,8 @@ struct cvr_ctx {
     std::vector<CUtensorMap> Wqkvh;                    //   = [q_h | k_h | v_h] (the fused QKV + attention GEMM's B)
     CUtensorMap flat_x0[2], tok_x0[2], flat_xa, flat_xb, tok_xa, tok_xb, sttok_xa, sttok_xb;
     CUtensorMap st_qkv, st_hf, tm_cat, tm_O;           // tm_O: cat[:, :D] (fused FFN kernel's A of Wo)
+    CUtensorMap st_S;                                  // fp32 branch sum S [B, W]: staged TMA stores (box 32 x 32)
+    bool st_S_ok = false;
     std::vector<CUtensorMap> W1f, Wcf;                 // fused FFN: W1 box {64,128}, [Wo | W2] box {64,256}
     std::vector<CUtensorMap> V, U, Wqkv, W1, Wcat;
     CUtensorMap flat_user, tok_user;
@@ -190,6 +192,7 @@ struct cvr_ctx {
   int pair_xv = 0;
   int xv_bn = 0;
   bool prefetch_b = true;
+  bool f32_tma_store = true;    // option "f32_tma_store": config 4's fp32 DCN-branch output through staged TMA stores
   // option "ens_fused_attn" [1]: config 4's QKV projection + attention as one GEMM (EPI_ATTN; the qkv tensor,
   // 805 MB per layer at B = 8192, never reaches HBM).  Bit-identical to QKV GEMM + mha64; measured per layer
   // 381 us vs 257 + 247 (two epilogue groups; one group: 519 -- the attention warps' latency bounds each tile)
@@ -788,6 +791,8 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     ok &= encode_tmap_bf16(&c->tm_t, c->ws + c->off_t, B, c->r, c->r, 128, &er) == 0;
     ok &= encode_tmap_bf16(&c->st_t, c->ws + c->off_t, B, c->r, c->r, 32, &er) == 0;
     ok &= encode_tmap_bf16(&E.st_qkv, c->ws + E.off_qkv, BT, 3 * D, 3 * D, 32, &er) == 0;
+    E.st_S_ok = encode_tmap_f32_store(&E.st_S, c->ws + E.off_S, B, W, W, &er) == 0;
+    ok &= E.st_S_ok;
     const int64_t CW = D + c->ffn;
     ok &= encode_tmap_bf16(&E.st_hf, c->ws + E.off_cat + D * 2, BT, c->ffn, CW, 32, &er) == 0;
     ok &= encode_tmap_bf16(&E.tm_cat, c->ws + E.off_cat, BT, CW, CW, 128, &er) == 0;
@@ -1326,6 +1331,7 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     a2.bias = c->wptr<float>(p + "dcn/b");
     a2.out_f32 = S;
     a2.ld_f32 = W;
+    if (c->f32_tma_store && E.st_S_ok) a2.tmOut = &E.st_S;  // staged, coalesced TMA stores of S
     if ((e = run_gemm(c, a2, K_GEMM_U, s)) != cudaSuccess) return c->cuda_fail(e, "ens U");
     // MHA branch: qkv = X Wqkv^T + b ; O = attention ; S += O Wo^T + bo
     __nv_bfloat16* cat = c->at<__nv_bfloat16>(E.off_cat);
@@ -2178,6 +2184,12 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);
+    return CVR_OK;
+  }
+  if (!strcmp(key, "f32_tma_store")) {
+    c->f32_tma_store = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
     return CVR_OK;
   }
   if (!strcmp(key, "ens_attn_ar")) {

@@ -198,6 +198,9 @@ cudaError_t launch_cross_stack(const CUtensorMap* tmX0, const CrossStackTables* 
 
 // host: encode a 2-D bf16 K-major tensor map [rows, cols] (row stride ld elements) with box
 // {64, box_rows} and 128-byte swizzle.
+// fp32 [rows, cols] (row stride ld elements), box {32 columns, 32 rows}, 128-byte swizzle: the staged fp32 epilogue
+// stores (EPI_CROSS_F32)
+int encode_tmap_f32_store(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols, int64_t ld, const char** err);
 int encode_tmap_bf16(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                      const char** err);
 

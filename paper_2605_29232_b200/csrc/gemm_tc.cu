@@ -91,7 +91,12 @@ struct Cfg {
   static constexpr int ATT_LD = 72;
   static constexpr int ATT_BUF = 3 * BM * ATT_LD * 2;
   static constexpr int ATT_BYTES = ATTN ? ATT_GROUPS * ATT_BUF : 0;
-  static constexpr int EPI_BYTES = OUT_BUFS * OUT_BYTES + 2 * EIN_BYTES + (RING ? RING_SLOTS * 2 * SUB : 0) + ATT_BYTES;
+  // EPI_CROSS_F32 with a tmOut map: fp32 32 x 32 chunks staged per epilogue warp (double-buffered) and TMA-stored
+  // (coalesced) instead of per-thread row stores
+  static constexpr int F32_NBUF = CG == 2 ? 2 : 1;  // (single-CTA tiles: the ring needs the room)
+  static constexpr int F32_BYTES = EPI == EPI_CROSS_F32 ? 4 * EPW * F32_NBUF * 32 * 32 * 4 : 0;
+  static constexpr int EPI_BYTES =
+      OUT_BUFS * OUT_BYTES + 2 * EIN_BYTES + (RING ? RING_SLOTS * 2 * SUB : 0) + ATT_BYTES + F32_BYTES;
   static constexpr int BAR_BYTES = 512;
   // EPI_HEAD across a CN-cluster: per-tile partial dot products gathered in rank 0 ([2][CN][BM] fp32)
   static constexpr int Z_BYTES = (EPI == EPI_HEAD && CN > 1) ? 2 * CN * BM * 4 : (EPI == EPI_HEAD ? EPW * BM * 4 : 0);
@@ -600,7 +605,27 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
               for (int j = 0; j < 32; ++j) v[j] = x0v[j] * v[j] + xlv[j];
             }
             if constexpr (EPI == EPI_CROSS_F32) {
-              if (live) st32_f32(g.out_f32 + (int64_t)m * g.ld_f32 + n, v);
+              if (g.tmOut) {  // (the launch passed a store map: use its kernel-parameter copy)
+                // stage this warp's 32 rows x 32 columns (swizzled 16-byte chunks), one TMA store per chunk
+                const int buf = (c >> 5) % C::F32_NBUF;
+                uint8_t* sb = sEin + 2 * C::EIN_BYTES + ((warp - 2) * C::F32_NBUF + buf) * 4096;
+                if (lane == 0) ptx::bulk_wait_read<C::F32_NBUF - 1>();  // the last store from this buffer read it
+                __syncwarp();
+                const uint32_t sbu = ptx::smem_u32(sb);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                  sts128(sbu + lane * 128 + ((u ^ (lane & 7)) << 4),
+                         make_uint4(__float_as_uint(v[4 * u]), __float_as_uint(v[4 * u + 1]),
+                                    __float_as_uint(v[4 * u + 2]), __float_as_uint(v[4 * u + 3])));
+                ptx::fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                  ptx::tma_store_2d(&tmOut, sb, n, m0 + q * 32);
+                  ptx::bulk_commit();
+                }
+              } else if (live) {
+                st32_f32(g.out_f32 + (int64_t)m * g.ld_f32 + n, v);
+              }
             } else {
               sts32_bf16(out_base + (c >> 6) * C::SUB, r, (c & 63) >> 3, v);
             }
@@ -662,7 +687,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
         }
       }
     }
-    if constexpr (T::kSmemOut || C::RING) {
+    if constexpr (T::kSmemOut || C::RING || EPI == EPI_CROSS_F32) {
       if (lane == 0) ptx::bulk_wait<0>();
     }
     if (warp == 2 && lane == 0) stamp(g.dbg, 5);
@@ -803,6 +828,31 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
   CVR_CASE(128, EPI_MASK)
 #undef CVR_CASE
   return cudaErrorInvalidValue;
+}
+
+int encode_tmap_f32_store(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols, int64_t ld, const char** err) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+      *err = "cuTensorMapEncodeTiled entry point unavailable";
+      return -1;
+    }
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), gdim, gstride, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    *err = "cuTensorMapEncodeTiled (fp32) failed";
+    return -1;
+  }
+  return 0;
 }
 
 int encode_tmap_bf16(CUtensorMap* tm, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,

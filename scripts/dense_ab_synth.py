@@ -18,7 +18,7 @@ sc = torch.empty(B, device="cuda")
 settings = json.loads(sys.argv[1]) if len(sys.argv) > 1 else [{}]
 K = int(os.environ.get("K", "20"))
 defaults = {"a_resident": 0, "pdl": 1, "fused_cross": 0, "graphs": 1, "stack": 0, "ens_u_bn": 128, "pair": 1,
-            "u_bn": 192, "mc": 0, "mb": 0, "pair_mlp": 0, "pair_xv": 0, "xv_bn": 0, "xv_splitk": 0, "prefetch_b": 1, "pair_u": 0, "ens_fused_attn": 1, "ens_attn_ar": 0}
+            "u_bn": 192, "mc": 0, "mb": 0, "pair_mlp": 0, "pair_xv": 0, "xv_bn": 0, "xv_splitk": 0, "prefetch_b": 1, "pair_u": 0, "ens_fused_attn": 1, "ens_attn_ar": 0, "f32_tma_store": 1}
 res = {i: [] for i in range(len(settings))}
 ref = None
 for rep in range(3):

@@ -102,3 +102,24 @@ def test_c4_fused_qkv_attention_bitexact(c4small, B):
         m.set_option("ens_fused_attn", 1)
     assert m.status() == 0
     assert torch.equal(s0, s1)
+
+
+@pytest.mark.parametrize("pair", [1, 0])
+def test_c4_f32_tma_store_bitexact(c4small, pair):
+    """Option f32_tma_store: the DCN branch's fp32 output S written through per-warp 32 x 32 staged TMA stores
+    instead of per-thread row stores -- the same values, bit-identical scores (2-CTA and single-CTA tiles)."""
+    cfg, m, tabs, w = c4small
+    B = 131
+    bt = cs.make_batch(cfg, 9, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    m.set_option("pair", pair)
+    try:
+        s1 = m.dense(x0, B).clone()
+        m.set_option("f32_tma_store", 0)
+        s0 = m.dense(x0, B).clone()
+    finally:
+        m.set_option("f32_tma_store", 1)
+        m.set_option("pair", 1)
+    assert m.status() == 0
+    assert torch.equal(s0, s1)
