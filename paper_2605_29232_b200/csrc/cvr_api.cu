@@ -118,6 +118,7 @@ struct cvr_ctx {
     CUtensorMap flat_x0[2], tok_x0[2], flat_xa, flat_xb, tok_xa, tok_xb, sttok_xa, sttok_xb;
     CUtensorMap st_qkv, st_hf, tm_cat, tm_O;           // tm_O: cat[:, :D] (fused FFN kernel's A of Wo)
     CUtensorMap st_S;                                  // fp32 branch sum S [B, W]: staged TMA stores (box 32 x 32)
+    CUtensorMap ld_Stok;                               // the same S as tokens [B*T, D]: the FFN2 + LN input loads
     bool st_S_ok = false;
     std::vector<CUtensorMap> W1f, Wcf;                 // fused FFN: W1 box {64,128}, [Wo | W2] box {64,256}
     std::vector<CUtensorMap> V, U, Wqkv, W1, Wcat;
@@ -791,7 +792,8 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     ok &= encode_tmap_bf16(&c->tm_t, c->ws + c->off_t, B, c->r, c->r, 128, &er) == 0;
     ok &= encode_tmap_bf16(&c->st_t, c->ws + c->off_t, B, c->r, c->r, 32, &er) == 0;
     ok &= encode_tmap_bf16(&E.st_qkv, c->ws + E.off_qkv, BT, 3 * D, 3 * D, 32, &er) == 0;
-    E.st_S_ok = encode_tmap_f32_store(&E.st_S, c->ws + E.off_S, B, W, W, &er) == 0;
+    E.st_S_ok = encode_tmap_f32_store(&E.st_S, c->ws + E.off_S, B, W, W, &er) == 0 &&
+                encode_tmap_f32_store(&E.ld_Stok, c->ws + E.off_S, BT, D, D, &er) == 0;
     ok &= E.st_S_ok;
     const int64_t CW = D + c->ffn;
     ok &= encode_tmap_bf16(&E.st_hf, c->ws + E.off_cat + D * 2, BT, c->ffn, CW, 32, &er) == 0;
@@ -1392,6 +1394,7 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     a6.bias = c->at<float>(E.off_catb[l]);
     a6.in_f32 = S;
     a6.ld_in = D;
+    a6.tmX0 = &E.ld_Stok;  // S chunks by TMA (EPI_SUM_LN's input ring)
     a6.gamma = c->wptr<float>(p + "ln/gamma");
     a6.beta = c->wptr<float>(p + "ln/beta");
     if ((e = run_gemm(c, a6, K_ENS_FFN2_LN, s)) != cudaSuccess) return c->cuda_fail(e, "ens out-proj+ffn2+ln");

@@ -94,7 +94,9 @@ struct Cfg {
   // EPI_CROSS_F32 with a tmOut map: fp32 32 x 32 chunks staged per epilogue warp (double-buffered) and TMA-stored
   // (coalesced) instead of per-thread row stores
   static constexpr int F32_NBUF = CG == 2 ? 2 : 1;  // (single-CTA tiles: the ring needs the room)
-  static constexpr int F32_BYTES = EPI == EPI_CROSS_F32 ? 4 * EPW * F32_NBUF * 32 * 32 * 4 : 0;
+  static constexpr int SLN_BUFS = 3;                 // EPI_SUM_LN: fp32 input chunks in flight per epilogue warp
+  static constexpr int F32_BYTES = EPI == EPI_CROSS_F32 ? 4 * EPW * F32_NBUF * 32 * 32 * 4
+                                  : (EPI == EPI_SUM_LN ? 4 * EPW * SLN_BUFS * 32 * 32 * 4 : 0);  // SUM_LN input ring
   static constexpr int EPI_BYTES =
       OUT_BUFS * OUT_BYTES + 2 * EIN_BYTES + (RING ? RING_SLOTS * 2 * SUB : 0) + ATT_BYTES + F32_BYTES;
   static constexpr int BAR_BYTES = 512;
@@ -172,7 +174,8 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
   uint64_t* aempty = afull + 1;          // resident A no longer read by MMAs (AR)
   uint64_t* zfull = aempty + 1;          // [2] rank 0: all CN x 4 epilogue warps stored their partials
   uint64_t* zempty = zfull + 2;          // [2] rank 0's 4 epilogue warps have read buffer a
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(zempty + 2);
+  uint64_t* sfull = zempty + 2;          // [4 warps][SLN_BUFS] EPI_SUM_LN fp32 input chunk landed
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sfull + 4 * 3);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int M = g.M, N = g.N, K = g.K;
@@ -216,6 +219,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
       ptx::mbar_init(&zfull[a], 4 * CN);
       ptx::mbar_init(&zempty[a], 4);
     }
+    for (int i = 0; i < 4 * 3; ++i) ptx::mbar_init(&sfull[i], 1);
     ptx::fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -399,8 +403,9 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
     const int q = warp & 3;
     const int part = (warp - 2) >> 2;  // RING: the 64-column sub-tile this warp finishes
     const int r = q * 32 + lane;  // row within the tile
-    int it = 0;
+    int it = 0, sln_k = 0;  // sln_k: EPI_SUM_LN fp32 input chunks consumed so far (ring position / parity)
     (void)part;
+    (void)sln_k;
     for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
       const int m0 = tile_m(tile) * BMT + rank * BM, tn = tile_n(tile), n0 = tn * BN;
       const int m = m0 + r;
@@ -408,6 +413,18 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
       const int a = it & 1;
       if constexpr (C::ATTN) {
         if (a != (part >> 1)) continue;  // the other group's tile (its accumulator index)
+      }
+      if constexpr (EPI == EPI_SUM_LN) {  // the tile's first fp32 input chunks (independent of the accumulator)
+        if (lane == 0) {
+          const int wq = warp - 2;
+          ptx::fence_async_smem();  // this warp's reads of the ring (previous tile) before the TMA overwrites
+          for (int i = 0; i < C::SLN_BUFS && 32 * i < BN; ++i) {
+            const int b = (sln_k + i) % C::SLN_BUFS;
+            ptx::mbar_arrive_expect_tx(&sfull[wq * 3 + b], 4096);
+            ptx::tma_load_2d(sEin + 2 * C::EIN_BYTES + (wq * C::SLN_BUFS + b) * 4096, &tmX0, &sfull[wq * 3 + b],
+                             n0 + 32 * i, m0 + q * 32);
+          }
+        }
       }
       ptx::mbar_wait(&tfull[a], (it >> 1) & 1);
       if (it == 0 && warp == 2 && lane == 0) stamp(g.dbg, 4);
@@ -518,13 +535,34 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
         }
         ptx::named_bar_sync(1 + grp, 32 * 8);  // the group's staging buffer is free for its next tile
       } else if constexpr (EPI == EPI_SUM_LN) {
-        // pass 1: y = acc + b + in, written back into TMEM; row sum
+        // pass 1: y = acc + b + in, written back into TMEM; row sum.  The fp32 input (this warp's 32 rows x 32-column
+        // chunks) arrives by TMA into a per-warp ring of SLN_BUFS swizzled 4 KB buffers, the first chunks issued
+        // before the accumulator is ready (per-lane row reads touched 32 lines per instruction and exposed the
+        // memory latency of every chunk: 1.5x slower kernel)
         float sum = 0.f;
+        const int wq = warp - 2;  // (EPW = 1: one warp per quadrant)
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
+          const int k = sln_k + (c >> 5), b = k % C::SLN_BUFS;
           float v[32], x[32];
           ld32_tmem(trow + c, v);
-          if (live) ld32_f32(g.in_f32 + (int64_t)m * g.ld_in + n0 + c, x);
+          ptx::mbar_wait(&sfull[wq * 3 + b], (k / C::SLN_BUFS) & 1);
+          const uint32_t xt = ptx::smem_u32(sEin + 2 * C::EIN_BYTES + (wq * C::SLN_BUFS + b) * 4096);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint4 w4 = lds128(xt + lane * 128 + ((u ^ (lane & 7)) << 4));
+            x[4 * u] = __uint_as_float(w4.x);
+            x[4 * u + 1] = __uint_as_float(w4.y);
+            x[4 * u + 2] = __uint_as_float(w4.z);
+            x[4 * u + 3] = __uint_as_float(w4.w);
+          }
+          __syncwarp();
+          if (lane == 0 && c + 32 * C::SLN_BUFS < BN) {  // refill this buffer with chunk c + SLN_BUFS of the tile
+            ptx::fence_async_smem();
+            ptx::mbar_arrive_expect_tx(&sfull[wq * 3 + b], 4096);
+            ptx::tma_load_2d(sEin + 2 * C::EIN_BYTES + (wq * C::SLN_BUFS + b) * 4096, &tmX0, &sfull[wq * 3 + b],
+                             n0 + c + 32 * C::SLN_BUFS, m0 + q * 32);
+          }
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             v[j] = v[j] + __ldg(g.bias + n0 + c + j) + (live ? x[j] : 0.f);
@@ -532,6 +570,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
           }
           st32_tmem(trow + c, v);
         }
+        sln_k += BN / 32;
         ptx::tmem_wait_st();
         const float mean = sum / (float)BN;
         float var = 0.f;  // pass 2: centred second moment (biased variance, A20)
@@ -750,6 +789,7 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
        g.epi == EPI_SUM_LN) && !g.tmOut)
     return cudaErrorInvalidValue;
   if ((g.epi == EPI_CROSS || g.epi == EPI_CROSS_F32) && (!g.tmX0 || !g.tmXl)) return cudaErrorInvalidValue;
+  if (g.epi == EPI_SUM_LN && !g.tmX0) return cudaErrorInvalidValue;  // the fp32 input's TMA load map
   if (g.epi == EPI_MASK && (!g.tmXl || !g.tmOut)) return cudaErrorInvalidValue;
   // B-multicast clusters of 8 along M (tmB with box {64, BN/8})
   if (g.mb8) {
