@@ -122,6 +122,7 @@ struct cvr_ctx {
     bool st_S_ok = false;
     std::vector<CUtensorMap> W1f, Wcf;                 // fused FFN: W1 box {64,128}, [Wo | W2] box {64,256}
     std::vector<CUtensorMap> V, U, Wqkv, W1, Wcat;
+    std::vector<CUtensorMap> V256;                     // V with 256-row boxes: t = X V^T as one-wave 128 x 256 tiles
     CUtensorMap flat_user, tok_user;
   } ens;
   // MaskNet: x0' = ReLU(W_in x0 + b_in) [B, Wp]; H = ReLU(x0' V_all^T + c_all)
@@ -198,7 +199,8 @@ struct cvr_ctx {
   // 805 MB per layer at B = 8192, never reaches HBM).  Bit-identical to QKV GEMM + mha64; measured per layer
   // 381 us vs 257 + 247 (two epilogue groups; one group: 519 -- the attention warps' latency bounds each tile)
   bool ens_fused_attn = true;
-  bool ens_attn_ar = false;     // option "ens_attn_ar": the fused QKV + attention GEMM with a resident X tile
+  bool ens_attn_ar = false;
+  bool ens_xv_wave = true;      // option "ens_xv_wave": config 4's t = X V^T as one wave of 128 x 256 tiles     // option "ens_attn_ar": the fused QKV + attention GEMM with a resident X tile
   bool zero_copy_scores = true;  // option "zero_copy_scores": cvr_score_host writes scores into pinned h_scores
   // option "pair_u": the U GEMM (192-wide EIN-ring tiles) as 2-CTA 256-row tiles, each CTA holding half of the U
   // tile.  Bit-exact; measured 89.5 vs 86.3 us per c2 dense stage, 726-732 vs 740 us at c3's rank slice (B = 8192)
@@ -918,6 +920,7 @@ int encode_plan_ensemble(cvr_ctx* c) {
   E.U.assign(c->n_cross, {});
   E.Wqkv.assign(c->n_cross, {});
   E.Wqkvh.assign(c->n_cross, {});
+  E.V256.assign(c->n_cross, {});
   E.W1.assign(c->n_cross, {});
   E.Wcat.assign(c->n_cross, {});
   E.W1f.assign(c->n_cross, {});
@@ -927,6 +930,7 @@ int encode_plan_ensemble(cvr_ctx* c) {
     const std::string p = "ens/" + std::to_string(l) + "/";
     const int dv = c->pair_ens ? 2 : 1;  // B boxes hold BN/2 rows per CTA of a pair
     ok &= encode_tmap_bf16(&E.V[l], c->wptr(p + "dcn/V"), r, W, W, 128 / dv, &er) == 0;
+    if (r % 256 == 0) ok &= encode_tmap_bf16(&E.V256[l], c->wptr(p + "dcn/V"), r, W, W, 256, &er) == 0;
     ok &= encode_tmap_bf16(&E.U[l], c->wptr(p + "dcn/U"), W, r, r, c->ens_u_bn / dv, &er) == 0;
     ok &= encode_tmap_bf16(&E.Wqkv[l], c->wptr(p + "mha/Wqkv"), 3 * D, D, D, 256 / dv, &er) == 0;
     ok &= encode_tmap_bf16(&E.W1[l], c->wptr(p + "ffn/W1"), F, D, D, 256 / dv, &er) == 0;
@@ -1317,6 +1321,7 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     const int rows = c->pair_ens ? 256 : 128, units = c->pair_ens ? c->num_sms / 2 : c->num_sms;
     const int64_t tiles = (int64_t)((M + rows - 1) / rows) * (N / BN);
     a.epw1 = c->epw_mode == 0 || (c->epw_mode == 2 && tiles > 2 * units);
+    if (c->gdbg && c->gdbg_n < 32) a.dbg = c->gdbg + (size_t)(c->gdbg_n++) * 160 * 8;  // CVR_GEMM_TIMELINE
     return a;
   };
   (void)gp;
@@ -1325,6 +1330,15 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     const bool even = l % 2 == 0;
     // DCN branch: t = X V^T ; S = x0 * (t U^T + b) + X   (fp32, A26)
     GemmArgs a1 = ga(flat_xl, &E.V[l], B, r, W, 128, EPI_STORE);
+    // t = X V^T has only (B / 128) x (r / 128) tiles of a very long K (W = 16384): 2-CTA 256 x 128 tiles give
+    // 1.73 waves (the second wave 73% full: measured 164 us, every CTA's tile ~82 us); 128 x 256 single-CTA tiles
+    // fit one wave when (B / 128) (r / 256) <= #SMs
+    if (c->ens_xv_wave && r % 256 == 0 && (int64_t)((B + 127) / 128) * (r / 256) <= c->num_sms) {
+      a1.BN = 256;
+      a1.cta_pair = false;
+      a1.tmB = &E.V256[l];
+      a1.epw1 = false;
+    }
     a1.tmOut = &c->st_t;
     if ((e = run_gemm(c, a1, K_GEMM_V, s)) != cudaSuccess) return c->cuda_fail(e, "ens V");
     GemmArgs a2 = ga(&c->tm_t, &E.U[l], B, W, r, c->ens_u_bn, EPI_CROSS_F32);
@@ -2191,6 +2205,12 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
   }
   if (!strcmp(key, "f32_tma_store")) {
     c->f32_tma_store = value != 0;
+    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    return CVR_OK;
+  }
+  if (!strcmp(key, "ens_xv_wave")) {
+    c->ens_xv_wave = value != 0;
     for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
     c->graphs.clear();
     return CVR_OK;

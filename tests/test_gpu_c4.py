@@ -123,3 +123,20 @@ def test_c4_f32_tma_store_bitexact(c4small, pair):
         m.set_option("pair", 1)
     assert m.status() == 0
     assert torch.equal(s0, s1)
+
+
+def test_c4_xv_one_wave_bitexact(c4small):
+    """Option ens_xv_wave: t = X V^T as one wave of single-CTA 128 x 256 tiles instead of 2-CTA 256 x 128 tiles --
+    every element of t accumulates the same K order, so scores are bit-identical."""
+    cfg, m, tabs, w = c4small
+    B = 300
+    bt = cs.make_batch(cfg, 10, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    s1 = m.dense(x0, B).clone()
+    m.set_option("ens_xv_wave", 0)
+    try:
+        s0 = m.dense(x0, B).clone()
+    finally:
+        m.set_option("ens_xv_wave", 1)
+    assert torch.equal(s0, s1)
