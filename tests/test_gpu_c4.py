@@ -84,8 +84,8 @@ def test_c4_fused_ffn_bitexact(c4small, B):
     assert torch.equal(s_f, s_u)
 
 
-@pytest.mark.parametrize("B", [131, 512])
-def test_c4_fused_qkv_attention_bitexact(c4small, B):
+@pytest.mark.parametrize("B,ar", [(131, 0), (512, 0), (512, 1)])
+def test_c4_fused_qkv_attention_bitexact(c4small, B, ar):
     """Option ens_fused_attn: the QKV projection and the 64-token attention as ONE GEMM (EPI_ATTN: each 128-token x
     192 tile [q_h | k_h | v_h] + b is rounded to bf16 in shared memory and attended in the epilogue with the
     mha64 core) -- the same roundings and the same attention code, so scores are bit-identical to QKV GEMM +
@@ -94,12 +94,14 @@ def test_c4_fused_qkv_attention_bitexact(c4small, B):
     bt = cs.make_batch(cfg, 8, batch=B)
     idx, off, dense = to_dev(bt)
     x0 = m.embed(idx, off, B, dense)
-    s1 = m.dense(x0, B).clone()  # fused (default)
-    m.set_option("ens_fused_attn", 0)
+    m.set_option("ens_attn_ar", ar)  # ar = 1: the X tile resident across its 4 heads' tiles
     try:
+        s1 = m.dense(x0, B).clone()  # fused (default)
+        m.set_option("ens_fused_attn", 0)
         s0 = m.dense(x0, B).clone()
     finally:
         m.set_option("ens_fused_attn", 1)
+        m.set_option("ens_attn_ar", 0)
     assert m.status() == 0
     assert torch.equal(s0, s1)
 
