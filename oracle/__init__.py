@@ -19,8 +19,10 @@ the readings A1..A26 used where the paper is silent, restated in DESIGN.md §3):
   O6 MLP        h_{i+1} = max(0, M_i h_i + c_i)                     PAPER.md:229-233, A10/A11
   O7 head       s = sigmoid(m . h + c)                              BASELINE.json north star, A16
   O8 ensemble   Y = LN_token(DCN(X) + MHA(X) + FFN(X))              PAPER.md:243-258, A20
-                (parity unpinned against the paper: the paper gives no formula for the
-                 ensemble layer; pinned only to the A20 reading)
+                (the paper gives no formula for the ensemble layer: pinned to the A20 reading by the
+                 hand-derived goldens E8 -- two-head attention with 1/sqrt(dh) != 1/dh, non-uniform
+                 softmax, per-token queries; FFN with live ReLU and b2; a layer with X0 != X_l --
+                 P16, and P8 scalar brute force, tests/test_oracle_pins.py)
   O10 MaskNet   x0' = ReLU(W_in x0 + b_in)                         PAPER.md:227-228 ("scale the
                 input x0 via one-layer relu projection"); block
                 x_{l+1} = (U_l ReLU(V_l x0' + c_l) + b_l) * x_l      PAPER.md:226 (eq. "MaskNet uses"),

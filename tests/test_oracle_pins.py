@@ -337,3 +337,69 @@ def test_E7_ngrams_mean_pool_truncate():
     np.testing.assert_array_equal(ps[:, 0, :], O.embedding_bag_sum([tab], idx, off, 1, len(mp["bags"]), 2)[:, 0, :])
     assert O.truncate_recent(g["truncate"]["keys"], g["truncate"]["max_len"]) == g["truncate"]["out"]
     assert O.truncate_recent([7], 3) == [7]
+
+
+# ---- E8: hand-derived attention / FFN / ensemble-layer goldens (A20; VERDICT r1 "c4 under-pinned") -------
+def _shift_matrix(n):
+    W = np.zeros((n, n))
+    for i in range(n):
+        W[i, (i + 1) % n] = 1.0
+    return W
+
+
+def test_E8_attention_two_heads():
+    c = gold("E8_attention.json")["cases"][0]
+    D, H = c["D"], c["n_heads"]
+    X = np.array(c["X"], float)[None]                      # [1, S=2, D]
+    l3 = math.log(3.0)
+    Wqkv = np.concatenate([np.zeros((D, D)), np.eye(D), np.eye(D)])
+    bqkv = np.concatenate([[2 * l3, 0, 0, 0, 2 * l3, 0, 0, 0], np.zeros(D), np.zeros(D)])
+    out = O.mha_tokens(X, Wqkv, bqkv, _shift_matrix(D), np.array(c["bo"], float), H)
+    np.testing.assert_allclose(out[0], np.array(c["out"], float), rtol=0, atol=1e-14, err_msg=c["derivation"])
+
+
+def test_E8_attention_token_queries_softmax_axis():
+    a, b = math.sqrt(2 * math.log(3.0)), math.sqrt(2 * math.log(7.0))
+    X = np.array([[[a, 0, 0, 0], [0, b, 0, 0]]])
+    Wqkv = np.concatenate([np.eye(4)] * 3)
+    out = O.mha_tokens(X, Wqkv, np.zeros(12), np.eye(4), np.zeros(4), 1)
+    ref = np.array([[3 * a / 4, b / 4, 0, 0], [a / 8, 7 * b / 8, 0, 0]])  # E8_attention.json cases[1]
+    np.testing.assert_allclose(out[0], ref, rtol=0, atol=1e-14)
+
+
+def test_E8_ffn():
+    g = gold("E8_ffn_ensemble.json")["ffn"]
+    out = O.ffn_tokens(np.array([[g["x"]]], float), np.array(g["W1"], float), np.array(g["b1"], float),
+                       np.array(g["W2"], float), np.array(g["b2"], float))
+    np.testing.assert_array_equal(out[0, 0], np.array(g["out"], float), err_msg=g["derivation"])
+
+
+def test_E8_ensemble_layer_x0_differs_from_xl():
+    g = gold("E8_ffn_ensemble.json")["ensemble"]
+    S, D = g["tokens"], g["D"]
+    P = {"ens/0/dcn/V": np.array(g["dcn_V"], float), "ens/0/dcn/U": np.array(g["dcn_U"], float),
+         "ens/0/dcn/b": np.array(g["dcn_b"], float),
+         "ens/0/mha/Wqkv": np.zeros((3 * D, D)), "ens/0/mha/bqkv": np.zeros(3 * D),
+         "ens/0/mha/Wo": np.zeros((D, D)), "ens/0/mha/bo": np.array([1.0, -1.0]),
+         "ens/0/ffn/W1": np.zeros((4, D)), "ens/0/ffn/b1": np.zeros(4), "ens/0/ffn/W2": np.zeros((D, 4)),
+         "ens/0/ffn/b2": np.zeros(D), "ens/0/ln/gamma": np.array(g["gamma"], float),
+         "ens/0/ln/beta": np.array(g["beta"], float)}
+    Y = O.ensemble_layer(np.array([g["X0"]], float), np.array([g["Xl"]], float), P, 0, g["n_heads"], S)
+    r0, r1 = 0.75 / math.sqrt(0.5625 + 1e-5), 3 / math.sqrt(9 + 1e-5)
+    np.testing.assert_allclose(Y[0], [r0, 0.5 - 2 * r0, r1, 0.5 - 2 * r1], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(Y[0], g["out"], rtol=0, atol=1e-15, err_msg=g["derivation"])
+
+
+def test_P8_ensemble_batched_vs_brute():
+    """P8 on a tiny config-4 structure (2 ensemble layers, 2 heads, 4 tokens): the batched oracle against the
+    scalar loops of oracle/brute.py (independent evaluation order)."""
+    cfg = cs.C4.with_(name="c4tiny", n_tables=4, rows=(64,) * 4, dim=8, cross_rank=4, ffn_dim=16, n_heads=2,
+                      n_cross=2, mlp_dims=(16, 8), batch=6)
+    tabs = cs.table_specs(cfg)
+    w = cs.make_weights(cfg)
+    bt = cs.make_batch(cfg, 0, batch=6)
+    out = O.score_forward(cfg, tabs, w, bt)
+    P = {k: O.to_f64(v) for k, v in w.items()}
+    for b in range(6):
+        s = brute_score_one(cfg, tabs, P, bt.indices, bt.offsets, bt.dense[b] if bt.dense.size else [], b, 6)
+        assert abs(s - out["scores"][b]) <= 1e-12 * max(1.0, abs(s))
