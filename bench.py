@@ -41,8 +41,8 @@ UNIT = "examples/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
-    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="cvr", choices=["cvr", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c3s", "c6"],
                     help="workload (default: config 2, the metric's single-GPU config); c3 / c3s with --gpus N > 1 "
@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--ring", type=int, default=8, help="distinct pre-uploaded batches cycled through")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-serving", action="store_true", help="skip the c5 p50/p99 probe (2 s at 8k queries/s)")
+    ap.add_argument("--no-sharded", action="store_true", help="N > 1: skip the c3-S sharded measurement")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
@@ -244,7 +246,8 @@ def dist_setup(args):
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
 
 
@@ -330,6 +333,69 @@ def time_enqueued(run, n, stream, chunk=32, spin_cycles=int(4e6)):
 
 
 # ----------------------------------------------------------------------------- our arm
+def dense_roles(cfg):
+    """(kernel role, launches per dense stage) of the tcgen05 GEMMs of a stage, in stage order."""
+    L, nh = cfg.n_cross, len(cfg.mlp_dims) - 1
+    tail = ([("gemm_mlp_relu", nh)] if nh else []) + [("gemm_mlp_head", 1)]
+    if cfg.backbone == "dcn_lowrank":
+        return [("gemm_xV", L), ("gemm_tU_cross", L)] + tail
+    if cfg.backbone == "ensemble":
+        return [("gemm_xV", L), ("gemm_tU_cross", L), ("gemm_ens_qkv_attn", L), ("gemm_ens_ffn1", L),
+                ("gemm_ens_ffn2_ln", L)] + tail
+    if cfg.backbone == "masknet":
+        grouped = cfg.n_cross == 1
+        return [("gemm_mask_proj", 1), ("gemm_mask_hidden", 1),
+                ("gemm_mask_mul", 1 if grouped else cfg.n_parallel * cfg.n_cross)] + tail
+    return []
+
+
+def role_work(cfg, B, role):
+    w = launch_work(cfg, B)[role]
+    if role == "gemm_mask_mul" and cfg.n_cross == 1:  # one grouped launch covers every parallel branch
+        w = dict(w, flops=w["flops"] * cfg.n_parallel, bytes=w["bytes"] * cfg.n_parallel)
+    return w
+
+
+def distinct_row_bytes(cfg, bt) -> int:
+    """Compulsory gather traffic of a batch: every distinct (table, row) once."""
+    row = cfg.dim * (4 if cfg.emb_dtype == "f32" else 2)
+    offs, B = bt.offsets.astype(np.int64), bt.batch
+    return sum(len(np.unique(bt.indices[offs[t * B]:offs[(t + 1) * B]])) for t in range(cfg.n_tables)) * row
+
+
+def digest(a) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def run_serving_probe(cfg, dev, tables, weights, qps=8000.0, duration=2.0, warm=0.3):
+    """Config 5 at one offered load: open-loop Poisson queries through DynamicBatcher + cvr_score_host (2 ms
+    window, max 8192 items), p50 / p99 latency from the scheduled arrival."""
+    from paper_2605_29232_b200 import CvrModel
+    from paper_2605_29232_b200.serving import ItemPoolView, Request, Server, nearest_rank
+    pool_n = 1 << 16
+    pool = cs.make_item_pool(cfg, pool_n)
+    view = ItemPoolView(pool.offsets, pool.indices, pool.dense, cfg.n_tables)
+    item_nnz = np.diff(pool.offsets).reshape(cfg.n_tables, pool_n).sum(axis=0)
+    max_nnz = int(np.sort(item_nnz)[-8192:].sum())
+    m = CvrModel(cfg, max_batch=8192, max_nnz=max_nnz, device=dev)
+    m.load_tables(tables)
+    m.load_weights({k: v.to(dev) for k, v in weights.items()})
+    trace = cs.make_requests(qps, warm + duration, pool_n)
+    reqs = [Request(i, t, len(ids), ids) for i, (t, ids) in enumerate(trace)]
+    srv = Server(m, view, max_items=8192, window_s=0.002, max_nnz=max_nnz)
+    lat, sizes, _ = srv.run(reqs)
+    meas = [r.rid for r in reqs if r.t_arrival >= warm]
+    L = lat[meas] * 1e3
+    n_items = sum(reqs[i].n_items for i in meas)
+    m.close()
+    return {"config": "c5: BASELINE.json configs[4] (c2 model, Poisson queries, lognormal(ln 50, 0.8) items capped at "
+                      "500, 2 ms window, max 8192 items, cvr_score_host with per-slot graphs)",
+            "qps_offered": qps, "duration_s": duration, "queries": len(meas), "p50_ms": float(nearest_rank(L, 50)),
+            "p99_ms": float(nearest_rank(L, 99)), "served_items_per_s": n_items / duration,
+            "batch_items_mean": float(sizes.mean()) if len(sizes) else 0.0, "rejected": int(srv.batcher.rejected)}
+
+
 def run_cvr(args, cfg):
     from paper_2605_29232_b200 import CvrModel
 
@@ -340,7 +406,7 @@ def run_cvr(args, cfg):
     # inputs: tables (HBM, > L2), weights, a ring of distinct batches (per-rank seeds)
     tables = [s.materialize(device=dev) for s in cs.table_specs(cfg)]
     weights = cs.make_weights(cfg)
-    ring = [cs.make_batch(cfg, 1000 * rank + i) for i in range(args.ring if cfg.name != "c3s" else 2)]
+    ring = [cs.make_batch(cfg, 1000 * rank + i) for i in range(args.ring)]
     max_nnz = max(b.nnz for b in ring)
     m = CvrModel(cfg, max_batch=B, max_nnz=max_nnz, device=dev)
     m.load_tables(tables)
@@ -363,14 +429,16 @@ def run_cvr(args, cfg):
         m.score_raw(ip, op, nnz, B, dp, sp, hse, hsd)
 
     torch.cuda.synchronize(dev)  # the inputs were copied on the current stream; the executor's streams start now
+    # warm-up: the executor captures its two per-slot graphs per stage in the first two calls; every later batch
+    # (any pointers, any size) replays them, so the timed region below holds no capture
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize(dev)
     assert m.status(s_d) == 0
+    captures_warm = m.call_info(0)["graph_captures"]
 
     clocks = ClockSampler(local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches_per_step = 2 + 7 * cfg.n_cross + len(cfg.mlp_dims)  # upper bound over the backbones
     with clocks:
         barrier(world)
         torch.cuda.synchronize(dev)
@@ -385,7 +453,20 @@ def run_cvr(args, cfg):
     n_launch = m.launch_count() - n0
     el_ms = max_over_ranks(world, ev0.elapsed_time(ev1), local)
     assert m.status(s_d) == 0
+    captures_timed = m.call_info(0)["graph_captures"] - captures_warm
     value = world * args.steps * B / (el_ms / 1e3)
+    # P12: what the timed region's last batch consumed, read back through its slot's call block (pointers and
+    # sizes) and the arrays behind them, against the generator's (SHA-256)
+    last = (args.steps - 1) % R
+    rec = m.call_info((args.warmup + args.steps - 1) % 2)
+    p12 = {"indices_sha256": digest(dev_in[last][0].cpu().numpy()),
+           "generator_indices_sha256": digest(ring[last].indices),
+           "offsets_sha256": digest(dev_in[last][1].cpu().numpy()),
+           "generator_offsets_sha256": digest(ring[last].offsets),
+           "call_block_matches": (rec["d_indices"], rec["d_offsets"], rec["nnz"], rec["batch"]) ==
+                                 (raw[last][0], raw[last][1], ring[last].nnz, B)}
+    p12["match"] = (p12["indices_sha256"] == p12["generator_indices_sha256"] and
+                    p12["offsets_sha256"] == p12["generator_offsets_sha256"] and p12["call_block_matches"])
 
     # ---- stage isolation: each stage alone, back to back on one stream (direct launches queued ahead of the GPU)
     iso = {}
@@ -401,29 +482,37 @@ def run_cvr(args, cfg):
         for i in range(min(args.warmup, 10) + R):
             run(i)
         torch.cuda.synchronize(dev)
-        iso[name + "_us_per_step"] = time_enqueued(run, args.steps, s_e) * 1e3
+        iso[name + "_us_per_step"] = time_enqueued(run, max(args.steps, 20), s_e) * 1e3
 
-    # ---- per-kernel attribution: the same K steps again with a CUDA-event pair around every
-    # launch on its launching stream (events between kernels also disable PDL overlap, so this
-    # pass is slower than the timed one; it is used only for per-kernel durations / shares).
-    # Every 16 steps a device-side spin holds both streams while the host enqueues the chunk, so the
-    # GPU then runs it back to back and each pair brackets the kernel, not the host's launch latency.
+    # ---- sparse stage on the uniform-index control (every lookup uniform over the rows: ~no L2 reuse)
+    uni = [cs.make_batch(cfg, 5000 + 1000 * rank + i, index_mode="uniform") for i in range(2)]
+    uni_in = [(torch.from_numpy(b.indices).to(dev), torch.from_numpy(b.offsets).to(dev),
+               torch.from_numpy(b.dense).to(dev)) for b in uni]
+
+    def run_u(i):
+        idx, off, dense = uni_in[i % 2]
+        m.embed(idx, off, B, dense, x0=x0iso, stream=s_e)
+    for i in range(4):
+        run_u(i)
     torch.cuda.synchronize(dev)
-    m.profile_begin(args.steps * launches_per_step + 16)
-    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    p0.record(s_e)
-    s_d.wait_event(p0)
-    spin_cycles = int(3e6)  # ~1.5 ms at 1.965 GHz: longer than the host needs to enqueue 16 steps
-    for i in range(args.steps):
-        if i % 16 == 0:
-            for st_ in (s_e, s_d):
-                with torch.cuda.stream(st_):
-                    torch.cuda._sleep(spin_cycles)
-        step(i)
-    p1.record(s_d)
+    embed_uniform_us = time_enqueued(run_u, max(args.steps, 20), s_e) * 1e3
+
+    # ---- per-kernel time inside a programmatic-launch chain: cvr_repeat_kernel enqueues only one GEMM role of
+    # the dense stage, each launch `reps` times back to back with PDL (no event between kernels), CUDA events
+    # around the whole chain on the launching stream; per-launch time = chain time / launches
+    m.dense(x0iso, B, scores=siso, stream=s_e)  # leave every intermediate buffer a full stage would
     torch.cuda.synchronize(dev)
-    kstats = m.profile_end()
-    prof_ms_per_step = p0.elapsed_time(p1) / args.steps
+    roles = dense_roles(cfg)
+    kt = {}
+    for role, cnt in roles:
+        reps = 8
+        nl = m.repeat_kernel(role, reps, x0iso, B, stream=s_e)
+        torch.cuda.synchronize(dev)
+        nchain = 6
+        us_chain = time_enqueued(lambda i, role=role: m.repeat_kernel(role, reps, x0iso, B, stream=s_e), nchain,
+                                 s_e) * 1e3
+        kt[role] = {"per_step": cnt, "us_per_launch": us_chain / nl}
+    assert m.status(s_e) == 0
 
     # ---- e2e: same metric through cvr_score_host (pinned host inputs, D2H scores in the region)
     e2e = None
@@ -458,67 +547,97 @@ def run_cvr(args, cfg):
         h2d = float(np.mean([b.nnz * 4 + b.offsets.nbytes + b.dense.nbytes for b in ring]))
         e2e = {"value": world * args.steps * B / (hel / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": B * 4, "ms_per_step": hel / args.steps,
-               "api": "cvr_score_host (pinned host buffers, copy stream + two compute streams)"}
+               "api": "cvr_score_host (pinned host buffers, copy stream + two compute streams, per-slot graphs)"}
+        # P12 on the host-fed path: the staged copies the kernels read (the slot's call block points into the
+        # ctx's workspace) against the generator's arrays
+        hrec = m.call_info((2 * args.warmup + 2 * args.steps - 1) % 2)
+        lastb = ring[(args.steps - 1) % R]
+        wsp = m.workspace.data_ptr()
+        got = {k: m.workspace[hrec[k] - wsp:hrec[k] - wsp + n].cpu().numpy()
+               for k, n in (("d_indices", lastb.indices.nbytes), ("d_offsets", lastb.offsets.nbytes))}
+        p12["host_fed_staged_match"] = (digest(got["d_indices"]) == digest(lastb.indices) and
+                                        digest(got["d_offsets"]) == digest(lastb.offsets))
+        p12["match"] = p12["match"] and p12["host_fed_staged_match"]
+
+    # ---- c5 serving probe (p50 / p99 under dynamic batching), config-2 model only, rank 0, N = 1
+    serving = None
+    if cfg.name == "c2" and world == 1 and not args.no_serving:
+        try:
+            serving = run_serving_probe(cfg, dev, tables, weights)
+        except Exception as e:  # noqa: BLE001
+            serving = {"error": str(e)}
 
     if rank != 0:
         return
-    # ---- per-kernel roofline (CUDA events on the launching stream, inside the timed region)
+    # ---- per-kernel rooflines
     pk = peaks()
     ebytes = float(np.mean([embed_bytes(cfg, b) for b in ring]))
-    work = launch_work(cfg, B)
-    bf16_peak = pk["bf16_sustained"] or pk["bf16"]
-    kernels = {}
-    for name, st in kstats.items():
-        avg_s = st["avg_ms"] / 1e3
-        if name == "embed_bag_pool":
-            ach = ebytes / avg_s / 1e9
-            kernels[name] = {"bound": "hbm", "avg_us": st["avg_ms"] * 1e3, "launches": st["launches"],
-                             "achieved": ach, "unit": "GB/s", "frac": ach / pk["hbm"], "algorithmic_bytes": ebytes}
-        else:
-            wk = work[name]
-            bound = pick_bound(wk, bf16_peak, pk["hbm"])
-            if bound == "hbm":  # arithmetic intensity below the ridge point: bytes / HBM peak bounds it
-                ach = wk["bytes"] / avg_s / 1e9
-                kernels[name] = {"bound": bound, "avg_us": st["avg_ms"] * 1e3, "launches": st["launches"],
-                                 "achieved": ach, "unit": "GB/s", "frac": ach / pk["hbm"], "peak": pk["hbm"],
-                                 "algorithmic_bytes": wk["bytes"], "flops_per_launch": wk["flops"],
-                                 "tensor_frac": wk["flops"] / avg_s / 1e12 / bf16_peak}
-            else:
-                ach = wk["flops"] / avg_s / 1e12
-                peak = bf16_peak if bound == "tensor" else FP32_SIMT_TFLOPS
-                kernels[name] = {"bound": bound, "avg_us": st["avg_ms"] * 1e3, "launches": st["launches"],
-                                 "achieved": ach, "unit": "TFLOP/s", "frac": ach / peak, "peak": peak,
-                                 "flops_per_launch": wk["flops"], "algorithmic_bytes": wk["bytes"]}
-    share = {k: v["total_ms"] / max(1e-9, sum(s["total_ms"] for s in kstats.values())) for k, v in kstats.items()}
-    dom = max(kstats, key=lambda k: kstats[k]["total_ms"])
-    dk = kernels[dom]
-    traffic = None
+    cbytes = float(np.mean([embed_bytes(cfg, b) - b.nnz * cfg.dim * (4 if cfg.emb_dtype == "f32" else 2)
+                            + distinct_row_bytes(cfg, b) for b in ring[:2]]))
+    ubytes = float(np.mean([embed_bytes(cfg, b) for b in uni]))
+    bf16_burst = pk["bf16"]
+    emb_us = iso["embed_us_per_step"]
+    kernels = {"embed_bag_pool": {
+        "bound": "hbm", "per_step": 1, "us_per_launch": emb_us, "achieved": ebytes / emb_us / 1e3, "unit": "GB/s",
+        "peak": pk["hbm"], "frac": ebytes / emb_us / 1e3 / pk["hbm"], "algorithmic_bytes": ebytes,
+        "frac_compulsory": cbytes / emb_us / 1e3 / pk["hbm"], "compulsory_bytes": cbytes,
+        "uniform_index_control": {"us": embed_uniform_us, "algorithmic_bytes": ubytes,
+                                  "achieved": ubytes / embed_uniform_us / 1e3,
+                                  "frac": ubytes / embed_uniform_us / 1e3 / pk["hbm"]},
+        "timing": "embedding stage alone, back-to-back launches, CUDA events"}}
+    traffic_db = {}
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(dom)
-    roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"],
-                "peak": pk["hbm"] if dk["bound"] == "hbm" else dk["peak"],
-                "unit": dk["unit"], "frac": dk["frac"], "traffic": traffic,
-                "peak_source": (f"MEASURED_PEAKS.json ({pk['source']}; bf16 sustained for kernels inside the step)"
-                                if dk["bound"] != "alu" else
-                                "derived: 148 SMs x 128 FP32 lanes x 2 FLOP/FMA x 1.965 GHz (DESIGN.md §6)"),
-                "share_of_kernel_time": share[dom],
-                "bound_rule": "roofline: the larger of flops / bf16 peak and algorithmic bytes / HBM peak "
-                              "(bench.launch_work, DESIGN.md §6)",
-                "flops_per_launch": dk.get("flops_per_launch"), "algorithmic_bytes": dk.get("algorithmic_bytes")}
-    dense_ms = sum(v["total_ms"] for k, v in kstats.items() if k != "embed_bag_pool") / args.steps
-    dense_ach = dense_flops_per_example(cfg) * B / (dense_ms / 1e3) / 1e12
+            traffic_db = json.load(f).get(cfg.name, {})
+    for role, d in kt.items():
+        wk = role_work(cfg, B, role)
+        t_s = d["us_per_launch"] / 1e6
+        tf = wk["flops"] / t_s / 1e12
+        gb = wk["bytes"] / t_s / 1e9
+        kernels[role] = {"bound": "tensor", "per_step": d["per_step"], "us_per_launch": d["us_per_launch"],
+                         "achieved": tf, "unit": "TFLOP/s", "peak": bf16_burst, "frac": tf / bf16_burst,
+                         "flops_per_launch": wk["flops"], "algorithmic_bytes": wk["bytes"],
+                         "hbm_line": {"achieved": gb, "unit": "GB/s", "frac": gb / pk["hbm"],
+                                      "ai_flop_per_byte": wk["flops"] / wk["bytes"],
+                                      "traffic": traffic_db.get(role)}}
+    for k in kernels:
+        kernels[k]["us_per_step"] = kernels[k]["us_per_launch"] * kernels[k]["per_step"]
+    dom = max(kernels, key=lambda k: kernels[k]["us_per_step"])
+    dk = kernels[dom]
+    tot = sum(v["us_per_step"] for v in kernels.values())
+    roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"], "peak": dk["peak"],
+                "unit": dk["unit"], "frac": dk["frac"],
+                "traffic": dk["hbm_line"]["traffic"] if "hbm_line" in dk else traffic_db.get(dom),
+                "peak_source": "MEASURED_PEAKS.json (%s): bf16 burst for a GEMM timed alone, HBM copy GB/s" % pk["source"],
+                "share_of_kernel_time": dk["us_per_step"] / tot,
+                "timing": ("GEMM: cvr_repeat_kernel chain (only this role, %d launches back to back with PDL, CUDA events "
+                           "around the chain on its stream); embed: the stage alone" % 8),
+                "bound_rule": "dense GEMMs on the bf16 tensor pipe (SURVEY.md §8(d) f_TC), HBM line beside; "
+                              "the gather on HBM bytes"}
+    if "hbm_line" in dk:
+        roofline["hbm_line"] = dk["hbm_line"]
+    dense_us = iso["dense_us_per_step"]
+    dense_flops = dense_flops_per_example(cfg) * B
+    dense_stage = {"us": dense_us, "flops": dense_flops, "achieved_tflops": dense_flops / dense_us / 1e6,
+                   "frac_burst": dense_flops / dense_us / 1e6 / bf16_burst,
+                   "frac_sustained": dense_flops / dense_us / 1e6 / (pk["bf16_sustained"] or bf16_burst),
+                   "sum_of_kernel_chains_us": sum(v["us_per_step"] for k, v in kernels.items()
+                                                  if k != "embed_bag_pool")}
 
-    # ---- parity spot check (outside the timed region): 64 examples of the last ring batch vs the oracle
+    # ---- parity (outside the timed region): the last ring batch vs the oracle -- every example for c1 / c2,
+    # a sample for the larger configs
     parity = None
     try:
         import oracle as O
-        sel = np.arange(0, B, max(1, B // (16 if cfg.name == "c4" else 64)))
-        bt = ring[(args.steps - 1) % R]
+        n_chk = B if cfg.name in ("c1", "c2", "c6") else 64
+        sel = np.arange(0, B, max(1, B // n_chk))
+        bt = ring[last]
         ref = O.score_forward(cfg, cs.table_specs(cfg), weights, cs.sub_batch(bt, sel))["scores"]
-        got = outs[(args.steps - 1) % R][torch.from_numpy(sel).to(dev)].double().cpu().numpy()
-        parity = {"max_abs_err": float(np.abs(got - ref).max()), "n": int(len(sel)), "tol": TOL[cfg.name]}
+        got = outs[last][torch.from_numpy(sel).to(dev)].double().cpu().numpy()
+        err = np.abs(got - ref)
+        parity = {"max_abs_err": float(err.max()), "p99_abs_err": float(np.percentile(err, 99)), "n": int(len(sel)),
+                  "tol": TOL[cfg.name]}
     except Exception as e:  # noqa: BLE001
         parity = {"error": str(e)}
 
@@ -553,16 +672,20 @@ def run_cvr(args, cfg):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(n_launch),
+        "graph_captures_in_timed_region": int(captures_timed),
         "clocks": clocks.summary(),
         "kernels": kernels,
-        "kernel_timing": "separate pass of the same %d steps with a CUDA-event pair around every launch, enqueued "
-                         "ahead behind a device spin every 16 steps (%.4f ms/step in that pass incl. spins)"
-                         % (args.steps, prof_ms_per_step),
-        "dense_stage_tflops": dense_ach,
+        "dense_stage": dense_stage,
         "stage_isolation": iso,
+        "overlap": {"ms_per_step": el_ms / args.steps,
+                    "serial_sum_ms": (iso["embed_us_per_step"] + iso["dense_us_per_step"]) / 1e3,
+                    "dense_alone_ms": iso["dense_us_per_step"] / 1e3},
+        "serving": serving,
+        "p12": p12,
         "parity": parity,
     }
     print(json.dumps(line), flush=True)
+    return line
 
 
 def run_sharded(args, cfg):
@@ -679,45 +802,33 @@ def run_sharded(args, cfg):
     hel = max_over_ranks(world, h0.elapsed_time(h1), local)
     h2d = float(np.mean([sum(t.numel() * t.element_size() for t in h) for h in host_in]))
 
-    # per-kernel durations on rank 0 (CUDA-event pairs around its launches; every rank runs the pass, the
-    # exchange needs them all)
-    launches_per_step = 3 + 2 * cfg.n_cross + len(cfg.mlp_dims)
-    sc.model.profile_begin(args.steps * launches_per_step + 16)
-    torch.cuda.synchronize(dev)
-    barrier(world)
-    for i in range(args.steps):
-        step(i)
-    torch.cuda.synchronize(dev)
-    barrier(world)
-    kstats = sc.model.profile_end()
+    # stage isolation on every rank (the exchange needs them all): gather, exchange (NCCL + unpack), dense stage
+    iso = {}
+    if args.exchange == "nccl":
+        idx0, off0, dn0 = dev_in[0]
+        stages = {"embed_shard": lambda i: sc.model.embed_shard(idx0, off0, B, dn0, sc.send[0], sc.x0[0], stream=s_e),
+                  "exchange": lambda i: sc.model.exchange(sc.send[0], sc.recv[0], B, sc.x0[0], stream=s_e),
+                  "dense": lambda i: sc.model.dense(sc.x0[0], Bl, outs[0], stream=s_e)}
+        for name, fn in stages.items():
+            for i in range(3):
+                fn(i)
+            torch.cuda.synchronize(dev)
+            barrier(world)
+            iso[name + "_us"] = time_enqueued(fn, 10, s_e, chunk=10) * 1e3
+            barrier(world)
+    assert sc.model.status(s_e) == 0
     if rank != 0:
-        return
+        return None
     pk = peaks()
-    bf16_peak = pk["bf16_sustained"] or pk["bf16"]
-    work = launch_work(cfg, Bl)
-    kernels = {}
-    for name, st in kstats.items():
-        avg_s = st["avg_ms"] / 1e3
-        if name in work:
-            wk = work[name]
-            bound = pick_bound(wk, bf16_peak, pk["hbm"])
-            ach = (wk["bytes"] / avg_s / 1e9) if bound == "hbm" else (wk["flops"] / avg_s / 1e12)
-            peak = pk["hbm"] if bound == "hbm" else bf16_peak
-            kernels[name] = {"bound": bound, "avg_us": st["avg_ms"] * 1e3, "launches": st["launches"],
-                             "achieved": ach, "unit": "GB/s" if bound == "hbm" else "TFLOP/s", "frac": ach / peak}
-        elif name == "embed_bag_pool":
-            eb = float(np.mean([embed_bytes(cfg, b) for b in ring]))  # this rank's tables, global batch
-            ach = eb / avg_s / 1e9
-            kernels[name] = {"bound": "hbm", "avg_us": st["avg_ms"] * 1e3, "launches": st["launches"],
-                             "achieved": ach, "unit": "GB/s", "frac": ach / pk["hbm"], "algorithmic_bytes": eb}
-        else:
-            kernels[name] = {"avg_us": st["avg_ms"] * 1e3, "launches": st["launches"]}
-    dom = max((k for k in kstats if "frac" in kernels[k]), key=lambda k: kstats[k]["total_ms"])
-    dk = kernels[dom]
-    roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"],
-                "peak": pk["hbm"] if dk["bound"] == "hbm" else bf16_peak, "unit": dk["unit"], "frac": dk["frac"],
-                "traffic": None, "peak_source": f"MEASURED_PEAKS.json ({pk['source']})",
-                "bound_rule": "roofline: the larger of flops / bf16 peak and algorithmic bytes / HBM peak"}
+    eb = float(np.mean([embed_bytes(cfg, b) for b in ring]))  # this rank's tables over the global batch
+    sparse = None
+    if "embed_shard_us" in iso:
+        sparse = {"bound": "hbm", "achieved": eb / iso["embed_shard_us"] / 1e3, "unit": "GB/s", "peak": pk["hbm"],
+                  "frac": eb / iso["embed_shard_us"] / 1e3 / pk["hbm"], "algorithmic_bytes": eb}
+        xb = (world - 1) * sc.send[0].numel() / world  # bytes each rank sends to its peers
+        iso["exchange_GBps_per_rank"] = xb / iso["exchange_us"] / 1e3 if world > 1 else None
+        dflops = dense_flops_per_example(cfg) * Bl
+        iso["dense_tflops"] = dflops / iso["dense_us"] / 1e6
 
     parity = None
     try:
@@ -736,31 +847,64 @@ def run_sharded(args, cfg):
         "dtype": "bf16", "data": "synthetic (cvr_synth, seeded; fp16 tables materialised on each rank for its tables)",
         "config": {"workload": WORKLOADS[cfg.name], "global_batch": B, "per_rank_batch": Bl,
                    "parallelism": f"table-wise sharding over {world} GPU(s) + data-parallel dense",
-                   "exchange": ("NCCL all-to-all of pooled bf16 rows (torch.distributed)" if args.exchange == "nccl"
+                   "exchange": ("cvr_exchange: grouped ncclSend/ncclRecv of pooled bf16 rows on the library's own "
+                                "NCCL communicator + unpack" if args.exchange == "nccl"
                                 else "V3: pooled rows stored into the owner's x0 over peer memory"),
                    "l2": "inputs larger than L2 (tables of %.0f GB per rank)" % (sum(t.numel() * t.element_size()
                                                                                   for t in tables) / 1e9)},
-        "roofline": roofline,
+        "roofline": sparse,
         "cpu_baseline": None,
         "e2e": {"value": args.steps * B / (hel / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                 "d2h_bytes_per_step": B * 4, "ms_per_step": hel / args.steps,
                 "api": "sharded scorer on inputs copied from pinned host memory each step (copy stream, two "
                        "compute streams)"},
-        "gpu_launches": n_launch, "clocks": clocks.summary(), "kernels": kernels, "parity": parity,
+        "gpu_launches": n_launch, "clocks": clocks.summary(), "stage_isolation": iso, "parity": parity,
     }
-    print(json.dumps(line), flush=True)
+    if not getattr(args, "embedded", False):
+        print(json.dumps(line), flush=True)
+    return line
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without torchrun: launch the N ranks (one process per GPU) through torch.distributed.run
+    with a 127.0.0.1 rendezvous, as the driver does; returns its exit code."""
+    import socket
+    import subprocess
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
     args = parse()
     cfg = cs.CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if torch.cuda.device_count() < args.gpus:
+            raise SystemExit(f"--gpus {args.gpus}: only {torch.cuda.device_count()} CUDA device(s) visible")
+        raise SystemExit(spawn_ranks(args.gpus))
+    if args.gpus > 1 and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, cfg)
     elif cfg.name == "c3" or (cfg.name == "c3s" and world > 1) or args.sharded:
         run_sharded(args, cfg)
     else:
-        run_cvr(args, cfg)
+        line = run_cvr(args, cfg)
+        # N > 1: the replica line above is the driver's value; the table-sharded strong-scaling measurement of
+        # c3-S (SURVEY.md A19: the >= 70% efficiency target) rides along in the same line
+        if world > 1 and cfg.name == "c2" and not args.no_sharded:
+            import torch.distributed as dist
+            args2 = argparse.Namespace(**vars(args))
+            args2.embedded, args2.ring = True, 2
+            sh = run_sharded(args2, cs.CONFIGS["c3s"])
+            if int(os.environ.get("RANK", "0")) == 0 and line is not None:
+                line["sharded_c3s"] = sh
+                print(json.dumps(line), flush=True)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.impl == "cvr":
         import torch.distributed as dist
         dist.destroy_process_group()

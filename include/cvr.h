@@ -73,6 +73,10 @@ typedef enum {
 
 typedef enum { CVR_F32 = 0, CVR_BF16 = 1, CVR_F16 = 2 } cvr_dtype;
 
+/* An NCCL unique id (ncclUniqueId: 128 opaque bytes), created by one rank (cvr_comm_unique_id) and handed to every
+ * rank by the caller's process group. */
+typedef struct { char internal[128]; } cvr_nccl_id;
+
 typedef enum {
   CVR_DCN_FULL = 0,     /* full-rank cross with bias, fp32 SIMT path (config 1)      */
   CVR_DCN_LOWRANK = 1,  /* low-rank cross, bf16 tcgen05 path (configs 2, 3, 5)       */
@@ -160,7 +164,11 @@ int cvr_dense(cvr_ctx* ctx, const void* d_x0, int batch, float* d_scores, cvr_st
 /* S2-S7 for one batch using the ctx's double-buffered x0 slots: the embed stage runs on
  * s_embed, the dense stage on s_dense, with event edges embed(k) -> dense(k) and
  * dense(k) -> embed(k+2) (slot reuse).  Back-to-back calls therefore overlap the embed
- * stage of batch k+1 with the dense stage of batch k (S9). */
+ * stage of batch k+1 with the dense stage of batch k (S9; "Hybrid CPU-GPU Execution").
+ * Each stage is ONE CUDA graph per x0 slot, captured at its first use and replayed for every later batch of any
+ * size <= max_batch: the batch's pointers and row count are written to a per-slot argument block in the workspace
+ * (a one-thread kernel on s_embed) that every kernel of both stages reads (option "graphs" [1]).  The pointers
+ * must stay valid until s_dense has passed this batch. */
 int cvr_score(cvr_ctx* ctx, const int32_t* d_indices, const int32_t* d_offsets, int64_t nnz,
               int batch, const float* d_dense, float* d_scores, cvr_stream_t s_embed,
               cvr_stream_t s_dense);
@@ -215,45 +223,47 @@ int cvr_embed_fused(cvr_ctx* ctx, const int32_t* d_indices, const int32_t* d_off
                     const float* d_dense, void* d_x0, uint32_t epoch, cvr_stream_t stream);
 int cvr_wait_peers(cvr_ctx* ctx, uint32_t epoch, cvr_stream_t stream);
 int cvr_release_peers(cvr_ctx* ctx, uint32_t epoch, cvr_stream_t stream);
-/* CUDA IPC for the peer mappings: a 64-byte handle of a device allocation, opened in another process of the
- * node (peer access enabled lazily); close unmaps it. */
-int cvr_ipc_get_handle(const void* d_ptr, void* handle64);
-int cvr_ipc_open_handle(const void* handle64, void** d_ptr);
+/* CUDA IPC for the peer mappings.  cvr_ipc_get_handle writes CVR_IPC_HANDLE_BYTES: the 64-byte CUDA IPC handle of
+ * the allocation that CONTAINS d_ptr plus the 8-byte offset of d_ptr inside it (a caching allocator may sub-allocate
+ * tensors); cvr_ipc_open_handle maps the allocation in another process of the node (peer access enabled lazily) and
+ * returns the mapped base + offset; cvr_ipc_close_handle(that pointer) unmaps it once no opened pointer of the same
+ * allocation remains.  CVR_E_CUDA on a CUDA failure, CVR_E_ARG on an unknown pointer. */
+#define CVR_IPC_HANDLE_BYTES 72
+int cvr_ipc_get_handle(const void* d_ptr, void* handle);
+int cvr_ipc_open_handle(const void* handle, void** d_ptr);
 int cvr_ipc_close_handle(void* d_ptr);
 
+/* -- S4 pooled all-to-all over the library's own NCCL communicator (BASELINE.json
+ * configs[2] "pooled embeddings exchanged by all-to-all") ----------------------------------------------------------
+ * NCCL is resolved at run time (the process's libnccl.so.2 -- PyTorch's -- or CVR_NCCL_LIB); CVR_E_NCCL if absent.
+ * cvr_comm_unique_id: a new unique id (call on one rank, broadcast it).  cvr_comm_init: ncclCommInitRank for this
+ * ctx (collective over the world_size ranks; world / rank must equal the ctx's; the current CUDA device is used).
+ * cvr_exchange: one grouped ncclSend / ncclRecv per peer on `stream`: chunk dst of d_send ([dst][b_local][t_slot][d],
+ * as written by cvr_embed_shard, cvr_shard_buffer_bytes each) goes to rank dst, chunk src of d_recv comes from rank
+ * src; then the unpack kernel writes the received pooled rows into the canonical x0 columns of d_x0_local (this
+ * rank's slice [batch_global / N, x0_ld], whose dense columns cvr_embed_shard already wrote).  The payload is the
+ * pooled rows verbatim (P11: bit-identical to the unsharded path).  CVR_E_STATE before cvr_comm_init. */
+int cvr_comm_unique_id(cvr_nccl_id* id);
+int cvr_comm_init(cvr_ctx* ctx, const cvr_nccl_id* id, int world, int rank);
+int cvr_exchange(cvr_ctx* ctx, const void* d_send, void* d_recv, int batch_global, void* d_x0_local,
+                 cvr_stream_t stream);
+
 /* Unpack received source-major chunks d_recv [src][b_local][t_slot][d] into the canonical
- * x0 columns of the local slice (V1 of SURVEY.md §8(e)).  The all-to-all itself is done by
- * the caller's communicator (NCCL over NVLink via torch.distributed) or cvr_exchange. */
+ * x0 columns of the local slice (V1 of SURVEY.md §8(e)); cvr_exchange runs it after its all-to-all. */
 int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d_x0, cvr_stream_t stream);
 
-/* Options (defaults in brackets): "graphs" [1] replay the executor stages of cvr_score /
- * cvr_score_host as cached CUDA graphs (keyed by their pointer / size arguments; captured on first
- * use; 32 entries, LRU); "pdl" [1] launch dependent GEMMs with programmatic stream serialization; "fused_cross" [0; allowed when r == 256]; "stack" [0] run the whole low-rank cross stack as one persistent kernel with per-(layer, row-block)
- * completion counters instead of 2 x n_cross GEMM launches; "pair" [1] 2-CTA (cta_group::2, 256-row) tiles for the ensemble path's GEMMs; "ens_u_bn" [128] N tile of the
- * ensemble DCN U GEMM; "embed_bps" [0 = uncapped] embedding CTAs per SM inside cvr_score / cvr_score_host (grid cap: the
- * embedding stage of batch k+1 then leaves registers for the dense-stage GEMM CTAs of batch k);
- * "embed_variant" [0] 0 = one lane group per bag at full
- * occupancy (rows of <= 128 B loaded without L1 allocation), 1 = warp-batched bags (coalesced offset / index
- * staging), 2 = cooperative index fetch, 3 = as 0 with L1-allocating row loads; "a_resident" [0] the U GEMM of a low-rank cross layer keeps
- * the 128 x r block of t resident in shared memory across its N tiles ("fused_cross" = 1 runs each
- * low-rank cross layer as one clustered kernel (K5) instead of two GEMMs); "mc" [0] clusters of 4 CTAs
- * over adjacent N tiles with the A tile multicast by TMA: 0 = off (the head as one 256-wide tile per row block,
- * split epilogue), 1 = only the head GEMM (N = 4 x 64, the sigmoid's dot product summed over the cluster in
- * DSMEM; same order, same result), 2 = every GEMM whose N tiles group by 4; "u_bn" [192] N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64); "xv_splitk" [0]
- * t = x_l V^T as a K-split cluster GEMM, 1 = partials reduced over DSMEM, 2 = exchanged through an L2-resident
- * global scratch (same sums, same order); "xv_bn" [0 = by wave count] N tile of t = x_l V^T (64, 128, 256);
- * "pair_xv" [0] / "pair_mlp" [0] 2-CTA (cta_group::2) tiles for the xV (value = BN) / hidden MLP GEMMs;
- * "prefetch_b" [1] each GEMM issues its first ring stages' weight loads before waiting for the previous
- * kernel; "ens_fused_attn" [1] config 4's QKV projection + attention as one GEMM (attention in the epilogue);
- * "f32_tma_store" [1] config 4's fp32 DCN-branch output through staged TMA stores; "ens_attn_ar" [0] the fused
- * QKV + attention GEMM with its X tile resident across the 4 heads;
- * "pair_u" [0] 2-CTA tiles for the low-rank U GEMM; "zero_copy_scores" [1] cvr_score_host stores the scores
- * straight into page-locked h_scores; "epw" [2] epilogue warps per TMEM quadrant:
- * 0 one, 1 up to 4 (one 64-column sub-tile each), 2 split only when a CTA runs <= 2 tiles; "mb" [0] weight
- * tiles multicast over clusters of 8 row blocks; "ens_fused_ffn" [0] config 4's FFN + out-projection + LN as
- * one kernel; "mask_grouped" [1] MaskNet's parallel blocks as one grouped GEMM.  Variants are bit-identical
- * except xv_splitk (fp32 summation order of t).  Unknown key or bad value ->
- * CVR_E_ARG. */
+/* Options (defaults in brackets): "graphs" [1] replay the executor stages of cvr_score / cvr_score_host as
+ * per-slot CUDA graphs (see cvr_score); "pdl" [1] launch dependent GEMMs with programmatic stream serialization;
+ * "prefetch_b" [1] each GEMM issues its first ring stages' weight loads before waiting for the previous kernel;
+ * "embed_bps" [0 = uncapped] embedding CTAs per SM inside the executor; "xv_bn" [0 = by wave count] N tile of
+ * t = x_l V^T (64, 128, 256); "u_bn" [192] N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64);
+ * "epw" [2] epilogue warps per TMEM quadrant: 0 one, 1 up to 4 (one 64-column sub-tile each), 2 split only when a
+ * CTA runs <= 2 tiles; "zero_copy_scores" [1] cvr_score_host stores the scores straight into page-locked h_scores;
+ * config 4: "pair" [1] 2-CTA (cta_group::2) tiles, "ens_u_bn" [128] N tile of the DCN U GEMM, "ens_fused_attn" [1]
+ * the QKV projection + attention as one GEMM (else QKV GEMM + mha64), "f32_tma_store" [1] the fp32 DCN-branch
+ * output through staged TMA stores, "ens_xv_wave" [1] t = X V^T as one wave of 128 x 256 tiles; MaskNet:
+ * "mask_grouped" [1] parallel blocks as one grouped GEMM.  Every variant is bit-identical to the default.  Unknown
+ * key or bad value -> CVR_E_ARG. */
 int cvr_set_option(cvr_ctx* ctx, const char* key, int64_t value);
 
 /* -- utility ----------------------------------------------------------------------------------
@@ -273,19 +283,22 @@ int cvr_gemm_bf16(const void* d_A, int64_t lda, const void* d_B, int64_t ldb, vo
  * (host memory).  Output: out_offsets [T*B + 1], out_indices (capacity out_indices_cap), out_dense
  * [B, F] with B = sum n_items, items in request order (the scatter map is implicit: request r owns
  * rows [sum_{q<r} n_q, sum_{q<=r} n_q)).  Pure host memcpy work (typically into pinned staging);
- * CVR_E_NOMEM if the indices do not fit, CVR_E_INDEX if a request's offsets decrease. */
+ * out_offsets / out_dense have room for out_batch_cap items; CVR_E_NOMEM if B > out_batch_cap or the indices do not
+ * fit, CVR_E_INDEX if a request's offsets are negative or decrease. */
 int cvr_concat_requests(int n_req, int n_tables, int n_dense, const int* n_items, const int32_t* const* h_offsets,
-                        const int32_t* const* h_indices, const float* const* h_dense, int32_t* out_offsets,
-                        int32_t* out_indices, int64_t out_indices_cap, float* out_dense, int64_t* out_nnz);
+                        const int32_t* const* h_indices, const float* const* h_dense, int out_batch_cap,
+                        int32_t* out_offsets, int32_t* out_indices, int64_t out_indices_cap, float* out_dense,
+                        int64_t* out_nnz);
 
 /* Gather n items of a host-resident item pool (table-major CSR pool_offsets [T*P + 1],
  * pool_indices, pool_dense [P, F]; a feature store) into one batch in the library's input layout:
  * out_offsets [T*n + 1], out_indices, out_dense [n, F], item i of the batch = pool item item_ids[i].
- * Host-only; CVR_E_INDEX on an item id outside [0, P), CVR_E_NOMEM if the indices do not fit. */
+ * out_offsets / out_dense have room for out_batch_cap items.  Host-only; CVR_E_INDEX on an item id outside
+ * [0, P), CVR_E_NOMEM if n > out_batch_cap or the indices do not fit. */
 int cvr_gather_items(int n_tables, int n_dense, int64_t pool_size, const int32_t* pool_offsets,
                      const int32_t* pool_indices, const float* pool_dense, int n, const int32_t* item_ids,
-                     int32_t* out_offsets, int32_t* out_indices, int64_t out_indices_cap, float* out_dense,
-                     int64_t* out_nnz);
+                     int out_batch_cap, int32_t* out_offsets, int32_t* out_indices, int64_t out_indices_cap,
+                     float* out_dense, int64_t* out_nnz);
 
 /* -- feature front end -----------------------------------------------------
  * Per model table t (n == T): vocab[t] > 0 puts the table in keys mode -- cvr_embed_keys hashes each raw
@@ -329,6 +342,30 @@ typedef struct {
   double total_ms;   /* sum of CUDA-event durations measured on the launching stream */
   double min_ms, max_ms;
 } cvr_kernel_stat;
+
+/* What the executor's kernels consumed: the per-call argument block of x0 slot `slot` (batch k used slot k % 2) as
+ * the device holds it -- the device pointers and sizes the embed / dense graphs read (P12: the caller hashes the
+ * arrays behind them) -- and how many executor graphs this ctx has captured.  Synchronous. */
+typedef struct {
+  const int32_t* d_indices;
+  const uint64_t* d_keys;
+  const int32_t* d_offsets;
+  const float* d_dense;
+  float* d_scores;
+  int64_t nnz;
+  int batch;
+  int64_t graph_captures;
+} cvr_call_record;
+int cvr_call_info(const cvr_ctx* ctx, int slot, cvr_call_record* out);
+
+/* Measurement: run the dense stage on d_x0 [batch, x0_ld] launching ONLY the tcgen05 GEMMs of kernel role `role`
+ * (a cvr_kernel_stat name, e.g. "gemm_tU_cross"), each of them `reps` times back to back on `stream` with the stage's
+ * programmatic (PDL) launches -- the GEMMs are idempotent given the buffers a full stage left behind (call cvr_dense
+ * on the same x0 first), so CUDA events around the call give the role's steady-state per-launch time inside a
+ * PDL chain without event pairs between kernels.  *n_launched = launches enqueued.  CVR_E_UNSUPPORTED on the fp32
+ * path. */
+int cvr_repeat_kernel(cvr_ctx* ctx, const char* role, int reps, const void* d_x0, int batch, cvr_stream_t stream,
+                      int* n_launched);
 
 /* Record a CUDA event pair around each of the next max_launches kernel launches (on the stream
  * the kernel is launched on).  cvr_profile_end synchronises on those events, aggregates them per

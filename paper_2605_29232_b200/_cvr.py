@@ -36,6 +36,18 @@ class cvr_model_desc(ctypes.Structure):
     ]
 
 
+class cvr_nccl_id(ctypes.Structure):
+    _fields_ = [("internal", ctypes.c_char * 128)]
+
+
+class cvr_call_record(ctypes.Structure):
+    _fields_ = [("d_indices", _vp), ("d_keys", _vp), ("d_offsets", _vp), ("d_dense", _vp), ("d_scores", _vp),
+                ("nnz", ctypes.c_int64), ("batch", ctypes.c_int), ("graph_captures", ctypes.c_int64)]
+
+
+IPC_HANDLE_BYTES = 72  # CVR_IPC_HANDLE_BYTES: CUDA IPC handle of the allocation + the tensor's offset inside it
+
+
 class cvr_kernel_stat(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 32), ("launches", ctypes.c_int64), ("total_ms", ctypes.c_double),
                 ("min_ms", ctypes.c_double), ("max_ms", ctypes.c_double)]
@@ -71,14 +83,19 @@ _SIGS = [
     ("cvr_ipc_get_handle", ctypes.c_int, [_vp, _vp]),
     ("cvr_ipc_open_handle", ctypes.c_int, [_vp, ctypes.POINTER(_vp)]),
     ("cvr_ipc_close_handle", ctypes.c_int, [_vp]),
+    ("cvr_comm_unique_id", ctypes.c_int, [ctypes.POINTER(cvr_nccl_id)]),
+    ("cvr_comm_init", ctypes.c_int, [_vp, ctypes.POINTER(cvr_nccl_id), ctypes.c_int, ctypes.c_int]),
+    ("cvr_exchange", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int, _vp, _vp]),
+    ("cvr_call_info", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(cvr_call_record)]),
+    ("cvr_repeat_kernel", ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int, _vp, ctypes.c_int, _vp, _c_ip]),
     ("cvr_gemm_bf16", ctypes.c_int, [_vp, ctypes.c_int64, _vp, ctypes.c_int64, _vp, ctypes.c_int64, ctypes.c_int,
                                      ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp]),
     ("cvr_set_option", ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_int64]),
     ("cvr_concat_requests", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, _c_ip, ctypes.POINTER(_vp),
-                                           ctypes.POINTER(_vp), ctypes.POINTER(_vp), _vp, _vp, ctypes.c_int64, _vp,
-                                           _c_i64p]),
+                                           ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.c_int, _vp, _vp,
+                                           ctypes.c_int64, _vp, _c_i64p]),
     ("cvr_gather_items", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, _vp, _vp, _vp, ctypes.c_int, _vp,
-                                        _vp, _vp, ctypes.c_int64, _vp, _c_i64p]),
+                                        ctypes.c_int, _vp, _vp, ctypes.c_int64, _vp, _c_i64p]),
     ("cvr_set_feature_spec", ctypes.c_int, [_vp, ctypes.c_int, _c_i64p, _c_ip]),
     ("cvr_embed_keys", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp]),
     ("cvr_score_keys", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp, _vp]),
@@ -145,8 +162,8 @@ def gemm_bf16(A: torch.Tensor, B: torch.Tensor, C: Optional[torch.Tensor] = None
 
 
 def ipc_get_handle(ptr: int) -> bytes:
-    """cvr_ipc_get_handle: the 64-byte CUDA IPC handle of a device allocation."""
-    buf = ctypes.create_string_buffer(64)
+    """cvr_ipc_get_handle: the CUDA IPC handle of the allocation holding ``ptr`` + ptr's offset in it (72 bytes)."""
+    buf = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
     st = lib().cvr_ipc_get_handle(ptr, buf)
     if st != 0:
         raise CvrError(st, "cvr_ipc_get_handle")
@@ -154,12 +171,27 @@ def ipc_get_handle(ptr: int) -> bytes:
 
 
 def ipc_open_handle(handle: bytes) -> int:
-    """cvr_ipc_open_handle: map another process's allocation; returns the device pointer."""
+    """cvr_ipc_open_handle: map another process's allocation; returns the device pointer of the tensor."""
     p = _vp()
-    st = lib().cvr_ipc_open_handle(ctypes.create_string_buffer(handle, 64), ctypes.byref(p))
+    st = lib().cvr_ipc_open_handle(ctypes.create_string_buffer(handle, IPC_HANDLE_BYTES), ctypes.byref(p))
     if st != 0:
         raise CvrError(st, "cvr_ipc_open_handle")
     return p.value
+
+
+def ipc_close_handle(ptr: int) -> None:
+    st = lib().cvr_ipc_close_handle(ptr)
+    if st != 0:
+        raise CvrError(st, "cvr_ipc_close_handle")
+
+
+def comm_unique_id() -> bytes:
+    """cvr_comm_unique_id: a fresh NCCL unique id (128 bytes), to be broadcast to every rank."""
+    uid = cvr_nccl_id()
+    st = lib().cvr_comm_unique_id(ctypes.byref(uid))
+    if st != 0:
+        raise CvrError(st, "cvr_comm_unique_id (NCCL unavailable?)")
+    return bytes(uid.internal) + b"\0" * (128 - len(bytes(uid.internal)))
 
 
 def text_ngram_keys(texts, n: int):
@@ -363,6 +395,31 @@ class CvrModel:
 
     def release_peers(self, epoch: int, stream=None):
         self._check(self.L.cvr_release_peers(self.h, epoch, _stream(stream)))
+
+    def comm_init(self, unique_id: bytes, world: int, rank: int):
+        """cvr_comm_init: the ctx's own NCCL communicator (collective over the ranks)."""
+        uid = cvr_nccl_id()
+        ctypes.memmove(ctypes.addressof(uid), unique_id, 128)
+        self._check(self.L.cvr_comm_init(self.h, ctypes.byref(uid), world, rank))
+
+    def exchange(self, send, recv, batch_global: int, x0, stream=None):
+        """cvr_exchange: grouped ncclSend / ncclRecv of the pooled rows + unpack into x0 (S4)."""
+        self._check(self.L.cvr_exchange(self.h, _ptr(send), _ptr(recv), batch_global, _ptr(x0), _stream(stream)))
+
+    def call_info(self, slot: int) -> dict:
+        """cvr_call_info: the per-call block of x0 slot `slot` as the executor's kernels read it."""
+        rec = cvr_call_record()
+        self._check(self.L.cvr_call_info(self.h, slot, ctypes.byref(rec)))
+        return {"d_indices": rec.d_indices or 0, "d_keys": rec.d_keys or 0, "d_offsets": rec.d_offsets or 0,
+                "d_dense": rec.d_dense or 0, "d_scores": rec.d_scores or 0, "nnz": rec.nnz, "batch": rec.batch,
+                "graph_captures": rec.graph_captures}
+
+    def repeat_kernel(self, role: str, reps: int, x0, batch: int, stream=None) -> int:
+        """cvr_repeat_kernel: only the GEMMs of `role`, each `reps` times back to back; returns launches."""
+        n = ctypes.c_int()
+        self._check(self.L.cvr_repeat_kernel(self.h, role.encode(), reps, _ptr(x0), batch, _stream(stream),
+                                             ctypes.byref(n)))
+        return n.value
 
     def set_option(self, key: str, value: int):
         self._check(self.L.cvr_set_option(self.h, key.encode(), int(value)))

@@ -5,7 +5,9 @@
 //
 // No CUDA call is made before cvr_set_workspace, so creation / validation / layout queries work
 // on a host without a GPU.
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <array>
@@ -24,15 +26,14 @@
 using namespace cvr;
 
 enum KernelId {
-  K_EMBED = 0, K_GEMM_V, K_GEMM_U, K_GEMM_MLP, K_GEMM_HEAD, K_DENSE_F32, K_UNPACK, K_CROSS_FUSED,
-  K_ENS_QKV, K_MHA, K_ENS_OPROJ, K_ENS_FFN1, K_ENS_FFN2_LN, K_HEAD_FIN, K_CROSS_STACK,
-  K_MASK_PROJ, K_MASK_HIDDEN, K_MASK_MUL, K_ENS_QKV_ATTN, K_COUNT
+  K_EMBED = 0, K_GEMM_V, K_GEMM_U, K_GEMM_MLP, K_GEMM_HEAD, K_DENSE_F32, K_UNPACK, K_ENS_QKV, K_MHA,
+  K_ENS_FFN1, K_ENS_FFN2_LN, K_HEAD_FIN, K_MASK_PROJ, K_MASK_HIDDEN, K_MASK_MUL, K_ENS_QKV_ATTN, K_SET_CALL,
+  K_PEER, K_COUNT
 };
 static const char* kKernelNames[K_COUNT] = {
     "embed_bag_pool", "gemm_xV",  "gemm_tU_cross",  "gemm_mlp_relu", "gemm_mlp_head", "dense_f32_dcn",
-    "shard_unpack",   "cross_fused", "gemm_ens_qkv", "mha64",       "gemm_ens_oproj", "gemm_ens_ffn1",
-    "gemm_ens_ffn2_ln", "head_finalize", "cross_stack", "gemm_mask_proj", "gemm_mask_hidden", "gemm_mask_mul",
-    "gemm_ens_qkv_attn"};
+    "shard_unpack",   "gemm_ens_qkv", "mha64", "gemm_ens_ffn1", "gemm_ens_ffn2_ln", "head_finalize",
+    "gemm_mask_proj", "gemm_mask_hidden", "gemm_mask_mul", "gemm_ens_qkv_attn", "set_call", "peer_flags"};
 
 namespace {
 
@@ -52,12 +53,56 @@ struct GemmPlan {
   int N, K, BN;
   Epi epi;
   bool pair = false;  // 2-CTA (cta_group::2) tiles; B map box = BN/2 rows
-  int cn = 1;         // 4: A multicast across a cluster of 4 N tiles (needs the A operand's quarter map)
-  bool mb8ok = false; // B multicast across clusters of 8 row blocks is possible (tmB8 encoded)
-  CUtensorMap tmB8;   // B map with box {64, BN/8}
-  const char* wname;  // B operand
   CUtensorMap tmB;
 };
+
+// NCCL, resolved at run time (dlopen of the libnccl.so.2 the process already has -- PyTorch's -- or the system
+// one): no link-time dependency, so the library still loads and validates on a host without NCCL / a GPU.
+struct Nccl {
+  void* dl = nullptr;
+  int (*getUniqueId)(void*) = nullptr;
+  int (*commInitRank)(void**, int, cvr_nccl_id, int) = nullptr;
+  int (*commDestroy)(void*) = nullptr;
+  int (*groupStart)() = nullptr;
+  int (*groupEnd)() = nullptr;
+  int (*send)(const void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*recv)(void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  const char* (*errorString)(int) = nullptr;
+  std::string why;
+  bool load() {
+    if (dl) return true;
+    const char* env = getenv("CVR_NCCL_LIB");
+    const char* names[] = {env, "libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      if (!n) continue;
+      dl = dlopen(n, RTLD_NOW | RTLD_NOLOAD);  // the copy already in the process (torch's) first
+      if (!dl) dl = dlopen(n, RTLD_NOW | RTLD_LOCAL);
+      if (dl) break;
+    }
+    if (!dl) {
+      why = "libnccl.so.2 not found (set CVR_NCCL_LIB)";
+      return false;
+    }
+    getUniqueId = reinterpret_cast<int (*)(void*)>(dlsym(dl, "ncclGetUniqueId"));
+    commInitRank = reinterpret_cast<int (*)(void**, int, cvr_nccl_id, int)>(dlsym(dl, "ncclCommInitRank"));
+    commDestroy = reinterpret_cast<int (*)(void*)>(dlsym(dl, "ncclCommDestroy"));
+    groupStart = reinterpret_cast<int (*)()>(dlsym(dl, "ncclGroupStart"));
+    groupEnd = reinterpret_cast<int (*)()>(dlsym(dl, "ncclGroupEnd"));
+    send = reinterpret_cast<int (*)(const void*, size_t, int, int, void*, cudaStream_t)>(dlsym(dl, "ncclSend"));
+    recv = reinterpret_cast<int (*)(void*, size_t, int, int, void*, cudaStream_t)>(dlsym(dl, "ncclRecv"));
+    errorString = reinterpret_cast<const char* (*)(int)>(dlsym(dl, "ncclGetErrorString"));
+    if (!getUniqueId || !commInitRank || !commDestroy || !groupStart || !groupEnd || !send || !recv) {
+      why = "libnccl.so.2 lacks ncclSend / ncclRecv / ncclCommInitRank";
+      dlclose(dl);
+      dl = nullptr;
+      return false;
+    }
+    return true;
+  }
+  const char* err(int r) { return errorString ? errorString(r) : "nccl error"; }
+};
+Nccl g_nccl;
+constexpr int kNcclUint8 = 1;  // ncclDataType_t ncclUint8 (nccl.h): the exchange moves raw bytes
 
 }  // namespace
 
@@ -74,8 +119,10 @@ struct cvr_ctx {
   // sharding
   std::vector<int> local_tables;
   int T_pad = 0;
-  // fused exchange (V3): device arrays [world] of peer x0 bases and peer flag arrays, own flag array
-  // device table: [2][world] peer x0 slot bases, [world] peer ready-flag arrays, [world] peer free-flag arrays
+  void* nccl_comm = nullptr;        // this ctx's NCCL communicator (cvr_comm_init), the S4 all-to-all
+  int comm_world = 0, comm_rank = 0;
+  // fused exchange (V3): device table: [2][world] peer x0 slot bases, [world] peer ready-flag arrays, [world] peer
+  // free-flag arrays
   size_t off_peers = 0;
   uint32_t* local_ready = nullptr;  // [world]: ready[src] = last epoch whose rows src stored into our x0 slot
   uint32_t* local_free = nullptr;   // [world]: free[dst] = last epoch whose dense stage dst has finished
@@ -93,6 +140,7 @@ struct cvr_ctx {
   bool any_mean = false;
   // workspace regions (offsets)
   size_t off_tables = 0, off_flag = 0, off_x0[2] = {0, 0}, off_xa = 0, off_xb = 0, off_t = 0;
+  size_t off_call[2] = {0, 0};  // executor per-call argument blocks (CallArgs), one per x0 slot
   std::vector<size_t> off_h;
   size_t off_idx[2] = {0, 0}, off_offs[2] = {0, 0}, off_dense[2] = {0, 0}, off_scores[2] = {0, 0};
   // runtime
@@ -105,8 +153,6 @@ struct cvr_ctx {
   CUtensorMap tm_x0slot[2], tm_xa, tm_xb, tm_t;   // A-operand / epilogue-input maps, box {64, 128}
   std::vector<CUtensorMap> tm_h;
   CUtensorMap st_xa, st_xb, st_t;                 // output (TMA store) maps, box {64, 32}
-  std::vector<CUtensorMap> tm_v256;               // V_l with box {64, 256} (fused cross layer)
-  bool fused_cross = false;                       // K5 (r == 256)
   // ensemble (config 4) buffers and maps
   struct Ens {
     // cat = [O | FFN hidden] per token: the out-projection and FFN2 become ONE GEMM with K = D + ffn
@@ -116,14 +162,13 @@ struct cvr_ctx {
     std::vector<size_t> off_qkvh, off_bqkvh;           // Wqkv / bqkv repacked head-major: head h = rows [192 h, +192)
     std::vector<CUtensorMap> Wqkvh;                    //   = [q_h | k_h | v_h] (the fused QKV + attention GEMM's B)
     CUtensorMap flat_x0[2], tok_x0[2], flat_xa, flat_xb, tok_xa, tok_xb, sttok_xa, sttok_xb;
-    CUtensorMap st_qkv, st_hf, tm_cat, tm_O;           // tm_O: cat[:, :D] (fused FFN kernel's A of Wo)
+    CUtensorMap st_qkv, st_hf, tm_cat;
     CUtensorMap st_S;                                  // fp32 branch sum S [B, W]: staged TMA stores (box 32 x 32)
     CUtensorMap ld_Stok;                               // the same S as tokens [B*T, D]: the FFN2 + LN input loads
     bool st_S_ok = false;
-    std::vector<CUtensorMap> W1f, Wcf;                 // fused FFN: W1 box {64,128}, [Wo | W2] box {64,256}
     std::vector<CUtensorMap> V, U, Wqkv, W1, Wcat;
     std::vector<CUtensorMap> V256;                     // V with 256-row boxes: t = X V^T as one-wave 128 x 256 tiles
-    CUtensorMap flat_user, tok_user;
+    CUtensorMap tok_user;
   } ens;
   // MaskNet: x0' = ReLU(W_in x0 + b_in) [B, Wp]; H = ReLU(x0' V_all^T + c_all)
   // [B, P*S*r] (every block's mask hidden comes from x0', so one GEMM covers them all);
@@ -139,87 +184,50 @@ struct cvr_ctx {
   } mk;
   size_t off_hpart = 0;   // split-head partial dot products [max_batch, last/256]
   int head_parts = 0;     // 0: head fused into the last MLP GEMM (last <= 256); else #256-wide parts
-  unsigned long long* dbg = nullptr;              // CVR_DEBUG_TIMING: phase stamps of the last fused launch
-  int dbg_ctas = 0;
-  size_t off_part = 0;
   std::vector<CUtensorMap> st_h;
   // CVR_GEMM_TIMELINE: per-CTA stamps of every GEMM of the last dense stage (printed at cvr_destroy)
   unsigned long long* gdbg = nullptr;
   int gdbg_n = 0;
   std::vector<int> gdbg_kid;
+  // the stage being enqueued reads its batch from this per-call block (executor graphs), else nullptr
+  const CallArgs* call = nullptr;
+  // ---- options (cvr_set_option); every variant that measured slower in round 1 was removed
   bool pdl = true;
-  // measured on B200 at B = 4096 (scripts/dense_ab.py): separate streaming GEMMs 105.5 us/dense stage,
-  // resident-A U GEMM 108.4, persistent cross stack 118 -- both kept as options, off by default
-  bool a_resident = false;  // U GEMM keeps t resident (K = r <= 256)
-  bool stack = false;       // the cross stack as one persistent dependency-driven kernel
   int ens_u_bn = 128;       // N tile of the ensemble DCN U GEMM (option "ens_u_bn": 64 | 128)
   bool pair_ens = true;     // 2-CTA tiles for the ensemble path's GEMMs (option "pair")
-  int embed_variant = 0;    // 0 per-bag kernel (default), 1 warp-batched (option "embed_variant")
   int embed_bps_pipe = 0;   // embed grid cap (CTAs/SM) in the executor; 0 = none (measured best)
-  size_t off_stack_tbl = 0, off_stack_done = 0;
-  // CUDA-graph cache for the executor stages (cvr_score / cvr_score_host)
-  struct GraphEntry {
-    uint64_t key[7];
-    cudaGraphExec_t exec;
-    int64_t n_kernels;
-    uint64_t last_use;
-  };
-  std::vector<GraphEntry> graphs;
-  bool use_graphs = true;
-  uint64_t use_clock = 0;
-  std::vector<std::array<uint64_t, 7>> seen_keys;
-  const void* last_x0 = nullptr;
-  int last_x0_rows = -1;
-  CUtensorMap tm_x0user;
-  std::vector<GemmPlan> plan;  // cross layers (V, U interleaved), then MLP
-  // quarter maps (box {64, 32}) of the A-operand maps, keyed by the full map: A multicast (GemmPlan::cn)
-  std::map<const CUtensorMap*, CUtensorMap> qmaps;
-  int mc = 0;                  // option "mc": 0 off (default), 1 head only, 2 every grouped GEMM
-  int u_bn = 192;              // option "u_bn": N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64)
-  int epw_mode = 2;            // option "epw": split epilogues 0 never, 1 always, 2 when a CTA has one tile
-  // option "ens_fused_ffn" [0]: config 4's FFN + out-projection + LN as one kernel (ens_ffn.cu), bit-identical to
-  // the two GEMMs.  Measured on B200 (B = 8192): 972 us per layer vs 363 + 536 us -- each 128-token tile streams
-  // all 1.15 MB of W1 / W2 / Wo through a 3-deep ring (shared memory is full), so weight streaming, not the
-  // h round trip it removes, bounds it; kept as an option
-  bool ens_fused_ffn = false;
-  bool mask_grouped = true;    // option "mask_grouped": MaskNet parallel blocks as one grouped GEMM launch
-  // option "mb" [0]: weight (B) tiles sliced and TMA-multicast over clusters of 8 row blocks (bit-identical).
-  // Measured on B200, c2 dense stage: 176 vs 90 us -- clusters of 8 only start when 8 SMs of a GPC are free
-  // (CTA entry spread over ~10 us behind the previous kernel) and the mainloops got no faster
-  bool mb = false;
-  bool pair_mlp = false;       // option "pair_mlp": 2-CTA tiles for the low-rank path's hidden MLP GEMMs
-  // option "pair_xv" = BN: t = x_l V^T as 2-CTA 256 x BN tiles (0 = off).  Measured on B200 at B = 4096: 94.2 /
-  // 94.9 / 102.1 us per dense stage at BN = 64 / 128 / 256 vs 90.1 with 128 x 64 single-CTA tiles -- the
-  // mainloop is bound by each SM's TMA ingest (A k-block + B k-block per SM either way), not by MMA shape
-  int pair_xv = 0;
-  int xv_bn = 0;
   bool prefetch_b = true;
   bool f32_tma_store = true;    // option "f32_tma_store": config 4's fp32 DCN-branch output through staged TMA stores
   // option "ens_fused_attn" [1]: config 4's QKV projection + attention as one GEMM (EPI_ATTN; the qkv tensor,
   // 805 MB per layer at B = 8192, never reaches HBM).  Bit-identical to QKV GEMM + mha64; measured per layer
   // 381 us vs 257 + 247 (two epilogue groups; one group: 519 -- the attention warps' latency bounds each tile)
   bool ens_fused_attn = true;
-  bool ens_attn_ar = false;
-  bool ens_xv_wave = true;      // option "ens_xv_wave": config 4's t = X V^T as one wave of 128 x 256 tiles     // option "ens_attn_ar": the fused QKV + attention GEMM with a resident X tile
+  bool ens_xv_wave = true;      // option "ens_xv_wave": config 4's t = X V^T as one wave of 128 x 256 tiles
   bool zero_copy_scores = true;  // option "zero_copy_scores": cvr_score_host writes scores into pinned h_scores
-  // option "pair_u": the U GEMM (192-wide EIN-ring tiles) as 2-CTA 256-row tiles, each CTA holding half of the U
-  // tile.  Bit-exact; measured 89.5 vs 86.3 us per c2 dense stage, 726-732 vs 740 us at c3's rank slice (B = 8192)
-  bool pair_u = false;      // option "prefetch_b": weight k-blocks issued before the dependency wait               // option "xv_bn": N tile of t = x_l V^T (0 = by wave count, see pick_bn_xv)
-  // option "xv_splitk" [0]: t = x_l V^T as a K-split cluster GEMM (r == 256).  Measured on B200 at B = 4096:
-  // its mainloop halves (3.5 vs 7 us) but the DSMEM exchange of the fp32 partials costs 2-6 us (element-wise
-  // st.shared::cluster or cp.async.bulk shared::cluster alike): 92-100 us per dense stage vs 90 with tiles
-  // xv_splitk = 2: the same with the partials exchanged through an L2-resident global scratch (off_xchg)
-  int xv_splitk = 0;
-  size_t off_xchg = 0;
-  int add_q(const CUtensorMap* full, const void* ptr, int64_t rows, int64_t cols, int64_t ld, const char** er) {
-    return encode_tmap_bf16(&qmaps[full], ptr, rows, cols, ld, 32, er);
+  int u_bn = 192;              // option "u_bn": N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64)
+  int xv_bn = 0;               // option "xv_bn": N tile of t = x_l V^T (0 = by wave count, see pick_bn_xv)
+  int epw_mode = 2;            // option "epw": split epilogues 0 never, 1 always, 2 when a CTA has one tile
+  bool mask_grouped = true;    // option "mask_grouped": MaskNet parallel blocks as one grouped GEMM launch
+  // executor CUDA graphs: ONE per (stage, slot), captured at first use and replayed for every batch (the batch
+  // lives in the per-call block, so neither its pointers nor its size are baked into the graph)
+  bool use_graphs = true;
+  enum { G_EMBED = 0, G_EMBED_KEYS = 1, G_DENSE = 2, G_KINDS = 3 };
+  cudaGraphExec_t gexec[G_KINDS][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+  int64_t gkernels[G_KINDS][2] = {{0, 0}, {0, 0}, {0, 0}};
+  int64_t graph_captures = 0;
+  void drop_graphs() {
+    for (auto& kind : gexec)
+      for (auto& g : kind)
+        if (g) {
+          cudaGraphExecDestroy(g);
+          g = nullptr;
+        }
   }
-  const CUtensorMap* q(const CUtensorMap* full) {
-    auto it = qmaps.find(full);
-    return it == qmaps.end() ? nullptr : &it->second;
-  }
+  std::vector<GemmPlan> plan;  // cross layers (V, U interleaved), then MLP
   // launch accounting + optional per-launch CUDA-event timing (cvr_profile_begin/end)
   int64_t launches = 0;
+  // cvr_repeat_kernel: the dense stage launches only the GEMMs of role only_kid, each only_reps times
+  int only_kid = -1, only_reps = 1;
   bool prof_on = false;
   size_t prof_cap = 0, prof_n = 0;
   std::vector<cudaEvent_t> prof_ev;
@@ -369,8 +377,11 @@ int validate_desc(const cvr_model_desc* d, std::string& why) {
     }
   if (d->dim <= 0 || d->dim > 512) return bad("dim out of range");
   if (d->emb_dtype < 0 || d->emb_dtype > 2 || d->act_dtype < 0 || d->act_dtype > 1) return bad("bad dtype");
-  if ((d->dim * (int)elt_size(d->emb_dtype)) % 32 != 0 || d->dim * (int)elt_size(d->emb_dtype) > 512)
-    return bad("dim * sizeof(row element) must be a multiple of 32 bytes and <= 512 bytes");
+  {  // one lane group of row_bytes / 16 lanes per bag: 2, 4, 8, 16 or 32 lanes (a power of two, embed.cu)
+    const int lanes = d->dim * (int)elt_size(d->emb_dtype) / 16;
+    if ((d->dim * (int)elt_size(d->emb_dtype)) % 16 != 0 || lanes < 2 || lanes > 32 || (lanes & (lanes - 1)))
+      return bad("dim * sizeof(row element) must be 32, 64, 128, 256 or 512 bytes");
+  }
   if (d->n_dense < 0 || d->n_cross < 0 || d->n_cross > kMaxLayers || d->n_mlp < 1 || d->n_mlp > kMaxLayers)
     return bad("layer counts out of range");
   if (!d->mlp_dims) return bad("mlp_dims is null");
@@ -392,6 +403,8 @@ int validate_desc(const cvr_model_desc* d, std::string& why) {
     if (d->act_dtype != CVR_BF16) return bad("ENSEMBLE runs the bf16 tensor-core path: act_dtype must be CVR_BF16");
     if (d->n_heads != 4 || d->dim != 256)
       return bad("ensemble layer: 4 heads x 64 over tokens of dim 256 (BASELINE.json configs[3], A20)");
+    if (d->n_tables != 64)  // the attention kernels hold one example's 64 tokens per 64-row block (S = 64)
+      return bad("ensemble layer: the attention runs over exactly 64 tokens (n_tables = 64, BASELINE.json configs[3])");
     if (d->n_dense != 0) return bad("ensemble: the tokens are the pooled tables, no dense features (A20)");
     if (d->cross_rank <= 0 || d->cross_rank % 128) return bad("ensemble cross_rank must be a multiple of 128");
     if (d->ffn_dim <= 0 || d->ffn_dim % 128) return bad("ffn_dim must be a multiple of 128");
@@ -526,18 +539,13 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
   const int64_t B = c->max_batch;
   c->off_tables = carve(cur, sizeof(TableDesc) * std::max<size_t>(1, c->local_tables.size()));
   c->off_flag = carve(cur, 256);
+  for (int i = 0; i < 2; ++i) c->off_call[i] = carve(cur, sizeof(CallArgs));
   if (c->world > 1) c->off_peers = carve(cur, (size_t)4 * c->world * sizeof(void*));
   for (int i = 0; i < 2; ++i) c->off_x0[i] = carve(cur, (size_t)B * c->x0_ld * ae);
   if (c->backbone == CVR_DCN_LOWRANK) {
     c->off_xa = carve(cur, (size_t)B * c->x0_ld * 2);
     c->off_xb = carve(cur, (size_t)B * c->x0_ld * 2);
     c->off_t = carve(cur, (size_t)B * c->r * 2);
-    c->off_stack_tbl = carve(cur, sizeof(CrossStackTables));
-    c->off_stack_done = carve(cur, sizeof(int) * 2 * kMaxLayers * ((B + 127) / 128));
-    if (c->r == 256) {  // K5 scratch; K5 itself is opt-in ("fused_cross"): measured slower than 2 GEMMs at B=4096
-      c->off_part = carve(cur, cross_fused_partial_bytes(c->max_batch));
-      c->off_xchg = carve(cur, (size_t)((B + 127) / 128) * 16 * 128 * 64 * 4);  // split-K xV exchange (GX)
-    }
     for (int i = 0; i + 1 < c->n_mlp; ++i) c->off_h.push_back(carve(cur, (size_t)B * c->mlp[i] * 2));
   } else if (c->backbone == CVR_ENSEMBLE) {
     const int64_t BT = B * c->T;  // tokens
@@ -595,13 +603,12 @@ int cvr_destroy(cvr_ctx* c) {
     cudaDeviceSynchronize();
     cudaMemcpy(h.data(), c->gdbg, h.size() * 8, cudaMemcpyDeviceToHost);
     const int n = std::min<int>((int)c->gdbg_kid.size(), 32);
-    const int first = 0;
     unsigned long long t0 = ~0ull;
     for (int b = 0; b < 160; ++b)
-      if (h[((size_t)first * 160 + b) * 8]) t0 = std::min(t0, h[((size_t)first * 160 + b) * 8]);
+      if (h[(size_t)b * 8]) t0 = std::min(t0, h[(size_t)b * 8]);
     const char* nm[8] = {"entry", "deps", "1st-stage", "last-mma", "1st-acc", "epi-done", "exit", ""};
-    for (int g = first; g < n; ++g) {
-      fprintf(stderr, "gemm %2d %-16s", g - first, kKernelNames[c->gdbg_kid[g]]);
+    for (int g = 0; g < n; ++g) {
+      fprintf(stderr, "gemm %2d %-16s", g, kKernelNames[c->gdbg_kid[g]]);
       for (int i = 0; i < 7; ++i) {
         double mn = 1e30, mx = 0;
         for (int b = 0; b < 160; ++b) {
@@ -616,51 +623,9 @@ int cvr_destroy(cvr_ctx* c) {
     }
     cudaFree(c->gdbg);
   }
-  if (c->dbg && c->stack && !c->fused_cross) {  // debug: cross-stack timeline of the last launch
-    std::vector<unsigned long long> h(148 * 32);
-    cudaDeviceSynchronize();
-    cudaMemcpy(h.data(), c->dbg, h.size() * 8, cudaMemcpyDeviceToHost);
-    unsigned long long t0 = ~0ull;
-    for (int b = 0; b < 148; ++b)
-      if (h[b * 32 + 31]) t0 = std::min(t0, h[b * 32 + 31]);
-    for (int g = 0; g < 2 * c->n_cross; ++g) {
-      double mx = 0, mn = 1e30, sm = 0, w0 = 1e30, w1 = 0;
-      int n = 0;
-      for (int b = 0; b < 148; ++b) {
-        if (h[b * 32 + g]) {
-          const double v = (double)(h[b * 32 + g] - t0) / 1e3;
-          mx = std::max(mx, v);
-          mn = std::min(mn, v);
-          sm += v;
-          ++n;
-        }
-        if (h[b * 32 + 16 + g]) {
-          const double v = (double)(h[b * 32 + 16 + g] - t0) / 1e3;
-          w0 = std::min(w0, v);
-          w1 = std::max(w1, v);
-        }
-      }
-      fprintf(stderr, "stack gemm %d: first-dep-ready %.2f..%.2f us, chunk done min %.2f avg %.2f max %.2f us (%d ctas)\n",
-              g, w0, w1, mn, n ? sm / n : 0.0, mx, n);
-    }
-    cudaFree(c->dbg);
-    c->dbg = nullptr;
-  }
-  if (c->dbg) {  // debug: per-phase averages of the last fused cross launch
-    std::vector<unsigned long long> h((size_t)c->dbg_ctas * 8);
-    cudaDeviceSynchronize();
-    cudaMemcpy(h.data(), c->dbg, h.size() * 8, cudaMemcpyDeviceToHost);
-    unsigned long long t0 = ~0ull;
-    for (int b = 0; b < c->dbg_ctas; ++b) t0 = std::min(t0, h[b * 8]);
-    double avg[7] = {0};
-    for (int b = 0; b < c->dbg_ctas; ++b)
-      for (int i = 0; i < 7; ++i) avg[i] += (double)(h[b * 8 + i] - t0) / c->dbg_ctas;
-    fprintf(stderr, "cross_fused phases (us from first CTA start): start %.2f wait %.2f A %.2f sync1 %.2f B %.2f sync2 %.2f end %.2f\n",
-            avg[0] / 1e3, avg[1] / 1e3, avg[2] / 1e3, avg[3] / 1e3, avg[4] / 1e3, avg[5] / 1e3, avg[6] / 1e3);
-    cudaFree(c->dbg);
-  }
   for (auto ev : c->prof_ev) cudaEventDestroy(ev);
-  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  c->drop_graphs();
+  if (c->nccl_comm && g_nccl.dl) g_nccl.commDestroy(c->nccl_comm);
   for (int i = 0; i < 2; ++i) {
     if (c->ev_embed[i]) cudaEventDestroy(c->ev_embed[i]);
     if (c->ev_dense[i]) cudaEventDestroy(c->ev_dense[i]);
@@ -707,12 +672,9 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     cudaMalloc(&c->gdbg, (size_t)32 * 160 * 8 * 8);
     cudaMemset(c->gdbg, 0, (size_t)32 * 160 * 8 * 8);
   }
-  if (getenv("CVR_DEBUG_TIMING") && !c->dbg) {
-    cudaMalloc(&c->dbg, 160 * 32 * 8 + (size_t)(c->max_batch / 128 + 1) * 4 * 8 * 8);
-    cudaMemset(c->dbg, 0, 160 * 32 * 8);
-  }
   c->cuda_ready = true;
   c->k = 0;
+  c->drop_graphs();
   c->weights_loaded = false;
   for (auto& s : c->wslots) s.loaded = false;
   if (c->backbone == CVR_DCN_LOWRANK) {
@@ -721,12 +683,9 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     bool ok = true;
     for (int i = 0; i < 2; ++i) {
       ok &= encode_tmap_bf16(&c->tm_x0slot[i], c->ws + c->off_x0[i], B, c->x0_ld, c->x0_ld, 128, &er) == 0;
-      ok &= c->add_q(&c->tm_x0slot[i], c->ws + c->off_x0[i], B, c->x0_ld, c->x0_ld, &er) == 0;
     }
     ok &= encode_tmap_bf16(&c->tm_xa, c->ws + c->off_xa, B, c->x0_ld, c->x0_ld, 128, &er) == 0;
     ok &= encode_tmap_bf16(&c->tm_xb, c->ws + c->off_xb, B, c->x0_ld, c->x0_ld, 128, &er) == 0;
-    ok &= c->add_q(&c->tm_xa, c->ws + c->off_xa, B, c->x0_ld, c->x0_ld, &er) == 0;
-    ok &= c->add_q(&c->tm_xb, c->ws + c->off_xb, B, c->x0_ld, c->x0_ld, &er) == 0;
     ok &= encode_tmap_bf16(&c->tm_t, c->ws + c->off_t, B, c->r, c->r, 128, &er) == 0;
     ok &= encode_tmap_bf16(&c->st_xa, c->ws + c->off_xa, B, c->x0_ld, c->x0_ld, 32, &er) == 0;
     ok &= encode_tmap_bf16(&c->st_xb, c->ws + c->off_xb, B, c->x0_ld, c->x0_ld, 32, &er) == 0;
@@ -736,7 +695,6 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     for (size_t i = 0; i < c->off_h.size(); ++i) {
       ok &= encode_tmap_bf16(&c->tm_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], 128, &er) == 0;
       ok &= encode_tmap_bf16(&c->st_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], 32, &er) == 0;
-      ok &= c->add_q(&c->tm_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], &er) == 0;
     }
     if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
   }
@@ -748,7 +706,6 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     bool ok = true;
     for (int i = 0; i < 2; ++i) {
       ok &= encode_tmap_bf16(&c->tm_x0slot[i], c->ws + c->off_x0[i], B, c->x0_ld, c->x0_ld, 128, &er) == 0;
-      ok &= c->add_q(&c->tm_x0slot[i], c->ws + c->off_x0[i], B, c->x0_ld, c->x0_ld, &er) == 0;
     }
     ok &= encode_tmap_bf16(&K.tm_x0p, c->ws + K.off_x0p, B, K.Wp, K.Wp, 128, &er) == 0;
     ok &= encode_tmap_bf16(&K.st_x0p, c->ws + K.off_x0p, B, K.Wp, K.Wp, 32, &er) == 0;
@@ -757,7 +714,6 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     for (int j = 0; j < nb; ++j)  // the r columns of block j inside H (row stride P*S*r)
       ok &= encode_tmap_bf16(&K.tm_Hblk[j], c->ws + K.off_H + (size_t)j * c->r * 2, B, c->r, HW, 128, &er) == 0;
     ok &= encode_tmap_bf16(&K.tm_cat, c->ws + K.off_cat, B, CW, CW, 128, &er) == 0;
-    ok &= c->add_q(&K.tm_cat, c->ws + K.off_cat, B, CW, CW, &er) == 0;
     ok &= encode_tmap_bf16(&K.tm_cat_st, c->ws + K.off_cat, B, CW, CW, 32, &er) == 0;
     K.st_cat.assign(K.P, CUtensorMap{});
     for (int p = 0; p < K.P; ++p)
@@ -772,7 +728,6 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     for (size_t i = 0; i < c->off_h.size(); ++i) {
       ok &= encode_tmap_bf16(&c->tm_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], 128, &er) == 0;
       ok &= encode_tmap_bf16(&c->st_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], 32, &er) == 0;
-      ok &= c->add_q(&c->tm_h[i], c->ws + c->off_h[i], B, c->mlp[i], c->mlp[i], &er) == 0;
     }
     if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
   }
@@ -800,7 +755,6 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     const int64_t CW = D + c->ffn;
     ok &= encode_tmap_bf16(&E.st_hf, c->ws + E.off_cat + D * 2, BT, c->ffn, CW, 32, &er) == 0;
     ok &= encode_tmap_bf16(&E.tm_cat, c->ws + E.off_cat, BT, CW, CW, 128, &er) == 0;
-    ok &= encode_tmap_bf16(&E.tm_O, c->ws + E.off_cat, BT, D, CW, 128, &er) == 0;
     c->tm_h.resize(c->off_h.size());
     c->st_h.resize(c->off_h.size());
     for (size_t i = 0; i < c->off_h.size(); ++i) {
@@ -846,66 +800,25 @@ int encode_plan(cvr_ctx* c) {
     g.K = K;
     g.BN = BN;
     g.epi = epi;
-    g.wname = nullptr;
     if (encode_tmap_bf16(&g.tmB, c->wptr(wn), N, K, K, BN, &er) != 0) return false;
-    if (BN % 64 == 0 && (epi == EPI_STORE || epi == EPI_BIAS_RELU || (epi == EPI_CROSS && BN == 192))) {
-      if (encode_tmap_bf16(&g.tmB8, c->wptr(wn), N, K, K, BN / 8, &er) != 0) return false;
-      g.mb8ok = true;
-    }
     c->plan.push_back(g);
     return true;
   };
   bool ok = true;
-  // Clusters of 4 N tiles with A multicast.  Measured on B200 (scripts/dense_kernels.py, B = 4096): the head
-  // (N = 256 as 4 x 64 tiles, DSMEM dot-product sum) 15.8 -> 13.3 us per launch; multicast alone does not
-  // pay at cluster size 4 (xV 14.7 -> 16.7, MLP 18.4 -> 19.7: unicast reads of a line by <= 4 SMs are
-  // already merged in L2); mc = 1 clusters only the head, mc = 2 every grouped GEMM.  Default mc = 0: the head as
-  // one 256-wide tile per row block with a split epilogue, bit-identical to the cluster head and no slower (c2 dense
-  // stage 85.97 vs 86.3 us; pipelined step equal within noise over 1000-step runs), without cluster scheduling.
-  auto mc4 = [&](int N, int BN) { return c->mc >= 2 && N % (4 * BN) == 0 && N / BN <= 8 ? 4 : 1; };
   for (int l = 0; l < c->n_cross; ++l) {
     const int bn_v = c->xv_bn ? c->xv_bn : pick_bn_xv(c->r, c->max_batch, c->num_sms > 0 ? c->num_sms : 148);
     ok &= addp("dcn/" + std::to_string(l) + "/V", c->r, (int)c->x0_ld, bn_v, EPI_STORE);
-    c->plan.back().cn = mc4(c->r, c->plan.back().BN);
-    if (c->pair_xv && c->r % c->pair_xv == 0) {  // 2-CTA (cta_group::2) tiles: B box = BN/2 rows per CTA
-      GemmPlan& g = c->plan.back();
-      g.pair = true;
-      g.BN = c->pair_xv;
-      g.cn = 1;
-      g.mb8ok = false;
-      ok &= encode_tmap_bf16(&g.tmB, c->wptr("dcn/" + std::to_string(l) + "/V"), g.N, g.K, g.K, g.BN / 2, &er) == 0;
-    }
     // U GEMM: 192-wide tiles (EIN-ring epilogue) when W allows -- 1/3 of the t re-reads of 64-wide tiles
-    // (measured 4096x1728x256: 7.4 us at BN = 192 vs 10.3 at 64); the K5 / stack / resident-A variants
-    // read U through 64-row boxes
-    const bool u192 = c->u_bn == 192 && c->x0_ld % 192 == 0 && !c->fused_cross && !c->stack && !c->a_resident;
+    // (measured 4096x1728x256: 7.4 us at BN = 192 vs 10.3 at 64)
+    const bool u192 = c->u_bn == 192 && c->x0_ld % 192 == 0;
     ok &= addp("dcn/" + std::to_string(l) + "/U", (int)c->x0_ld, c->r, u192 ? 192 : pick_bn((int)c->x0_ld), EPI_CROSS);
-    if (u192 && c->pair_u) {  // 2-CTA tiles: each CTA holds half of the U tile (B box = 96 rows)
-      GemmPlan& g = c->plan.back();
-      g.pair = true;
-      g.mb8ok = false;
-      ok &= encode_tmap_bf16(&g.tmB, c->wptr("dcn/" + std::to_string(l) + "/U"), g.N, g.K, g.K, 96, &er) == 0;
-    }
   }
-  c->tm_v256.assign(c->n_cross, CUtensorMap{});
-  if (c->r == 256)
-    for (int l = 0; l < c->n_cross; ++l)
-      ok &= encode_tmap_bf16(&c->tm_v256[l], c->wptr("dcn/" + std::to_string(l) + "/V"), c->r, c->x0_ld, c->x0_ld, 256,
-                             &er) == 0;
   int K = (int)c->x0_ld;
   for (int i = 0; i < c->n_mlp; ++i) {
     const bool last = i + 1 == c->n_mlp;
-    int bn = last ? (c->head_parts ? 256 : c->mlp[i]) : pick_bn(c->mlp[i], c->max_batch);
+    const int bn = last ? (c->head_parts ? 256 : c->mlp[i]) : pick_bn(c->mlp[i], c->max_batch);
     const Epi ep = last ? (c->head_parts ? EPI_HEAD_PARTIAL : EPI_HEAD) : EPI_BIAS_RELU;
-    const bool head_mc = last && !c->head_parts && c->mc && c->mlp[i] % 256 == 0;
-    if (head_mc) bn = c->mlp[i] / 4;  // the head's dot product spans the cluster's 4 tiles (DSMEM sum)
     ok &= addp("mlp/" + std::to_string(i) + "/W", c->mlp[i], K, bn, ep);
-    c->plan.back().cn = head_mc ? 4 : (!last ? mc4(c->mlp[i], bn) : 1);
-    if (!last && c->pair_mlp && bn >= 128) {  // 2-CTA (cta_group::2) tiles: B box = BN/2 rows per CTA
-      GemmPlan& g = c->plan.back();
-      g.pair = true;
-      ok &= encode_tmap_bf16(&g.tmB, c->wptr("mlp/" + std::to_string(i) + "/W"), g.N, K, K, bn / 2, &er) == 0;
-    }
     K = c->mlp[i];
   }
   if (!ok) return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
@@ -923,8 +836,6 @@ int encode_plan_ensemble(cvr_ctx* c) {
   E.V256.assign(c->n_cross, {});
   E.W1.assign(c->n_cross, {});
   E.Wcat.assign(c->n_cross, {});
-  E.W1f.assign(c->n_cross, {});
-  E.Wcf.assign(c->n_cross, {});
   bool ok = true;
   for (int l = 0; l < c->n_cross; ++l) {
     const std::string p = "ens/" + std::to_string(l) + "/";
@@ -946,8 +857,6 @@ int encode_plan_ensemble(cvr_ctx* c) {
     cudaError_t e5 = cudaMemcpy(c->ws + E.off_catb[l], bo.data(), D * 4, cudaMemcpyHostToDevice);
     if (e1 || e2 || e3 || e4 || e5) return c->fail(CVR_E_CUDA, "assembling [Wo | W2]");
     ok &= encode_tmap_bf16(&E.Wcat[l], c->ws + E.off_catW[l], D, D + F, D + F, 256 / dv, &er) == 0;
-    ok &= encode_tmap_bf16(&E.W1f[l], c->wptr(p + "ffn/W1"), F, D, D, 128, &er) == 0;
-    ok &= encode_tmap_bf16(&E.Wcf[l], c->ws + E.off_catW[l], D, D + F, D + F, 256, &er) == 0;
     // head-major [q_h | k_h | v_h] copies of Wqkv / bqkv for the fused QKV + attention GEMM (EPI_ATTN)
     if (D == 64 * c->n_heads) {
       std::vector<float> bq(3 * D), bh(3 * D);
@@ -975,7 +884,6 @@ int encode_plan_ensemble(cvr_ctx* c) {
     g.K = K;
     g.BN = last ? (c->head_parts ? 256 : c->mlp[i]) : pick_bn(c->mlp[i], c->max_batch);
     g.epi = last ? (c->head_parts ? EPI_HEAD_PARTIAL : EPI_HEAD) : EPI_BIAS_RELU;
-    g.wname = nullptr;
     g.pair = c->pair_ens;
     if (encode_tmap_bf16(&g.tmB, c->wptr("mlp/" + std::to_string(i) + "/W"), g.N, K, K, g.pair ? g.BN / 2 : g.BN, &er) != 0)
       return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
@@ -1019,7 +927,6 @@ int encode_plan_masknet(cvr_ctx* c) {
   gp.K = (int)c->x0_ld;
   gp.BN = K.bn_proj;
   gp.epi = EPI_BIAS_RELU;
-  gp.wname = nullptr;
   ok &= encode_tmap_bf16(&gp.tmB, c->wptr("proj/W"), Wp, c->x0_ld, c->x0_ld, gp.BN, &er) == 0;
   c->plan.push_back(gp);  // plan[0]: projection
   ok &= encode_tmap_bf16(&K.tmB_Vall, c->ws + K.off_Vall, (int64_t)nb * r, Wp, Wp, K.bn_h, &er) == 0;
@@ -1041,12 +948,6 @@ int encode_plan_masknet(cvr_ctx* c) {
     g.K = Kd;
     g.epi = last ? (c->head_parts ? EPI_HEAD_PARTIAL : EPI_HEAD) : EPI_BIAS_RELU;
     g.BN = last ? (c->head_parts ? 256 : c->mlp[i]) : pick_bn(c->mlp[i], M);
-    const bool head_mc = last && !c->head_parts && c->mc && c->mlp[i] % 256 == 0;
-    if (head_mc) {
-      g.BN = c->mlp[i] / 4;
-      g.cn = 4;
-    }
-    g.wname = nullptr;
     ok &= encode_tmap_bf16(&g.tmB, c->wptr("mlp/" + std::to_string(i) + "/W"), g.N, Kd, Kd, g.BN, &er) == 0;
     c->plan.push_back(g);  // plan[1 + i]: MLP
     Kd = c->mlp[i];
@@ -1141,22 +1042,10 @@ int cvr_load_weights(cvr_ctx* c, int n, const char* const* names, const void* co
     if (e != cudaSuccess) return c->cuda_fail(e, "cvr_load_weights upload");
     s.loaded = true;
   }
+  c->drop_graphs();  // captured graphs hold the old plan's tensor maps / head bias by value
   if (c->backbone == CVR_DCN_LOWRANK) {
     int st = encode_plan(c);
     if (st != CVR_OK) return st;
-    CrossStackTables tb;
-    memset(&tb, 0, sizeof tb);
-    const char* er = nullptr;
-    for (int l = 0; l < c->n_cross; ++l) {  // the stack kernel reads V and U through 64-row boxes
-      if (encode_tmap_bf16(&tb.V[l], c->wptr("dcn/" + std::to_string(l) + "/V"), c->r, c->x0_ld, c->x0_ld, 64, &er) ||
-          encode_tmap_bf16(&tb.U[l], c->wptr("dcn/" + std::to_string(l) + "/U"), c->x0_ld, c->r, c->r, 64, &er))
-        return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
-    }
-    tb.xa = c->tm_xa;
-    tb.xb = c->tm_xb;
-    tb.t = c->tm_t;
-    cudaError_t e = cudaMemcpy(c->ws + c->off_stack_tbl, &tb, sizeof tb, cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return c->cuda_fail(e, "upload cross-stack tables");
   } else if (c->backbone == CVR_ENSEMBLE) {
     int st = encode_plan_ensemble(c);
     if (st != CVR_OK) return st;
@@ -1205,11 +1094,11 @@ EmbedArgs embed_args(cvr_ctx* c, const int32_t* idx, const int32_t* off, int64_t
   a.pad_col0 = c->W;
   a.pad_col1 = c->x0_ld;
   a.flag = c->at<int>(c->off_flag);
-  a.v2 = c->embed_variant == 1 && !c->any_mean;  // the warp-batched variant only sums
-  a.variant = c->embed_variant;
+  a.call = c->call;
   return a;
 }
 
+// S2 + S3.  Executor stages (c->call set): B is max_batch (grid size); the kernel reads the batch from the block.
 int do_embed(cvr_ctx* c, const int32_t* idx, const int32_t* off, int64_t nnz, int B, const float* dense, void* x0,
              cudaStream_t s, int blocks_per_sm = 0, const uint64_t* keys = nullptr) {
   if (c->F && !c->slot("norm/mean")->loaded) return c->fail(CVR_E_STATE, "norm/mean,std not loaded");
@@ -1223,7 +1112,8 @@ int do_embed(cvr_ctx* c, const int32_t* idx, const int32_t* off, int64_t nnz, in
   return CVR_OK;
 }
 
-GemmArgs gemm_args(cvr_ctx* c, const GemmPlan& g, const CUtensorMap* A, int M) {
+// M: rows of the A operand (examples, or tokens = examples x m_mult); executor stages pass max_batch x m_mult
+GemmArgs gemm_args(cvr_ctx* c, const GemmPlan& g, const CUtensorMap* A, int M, int m_mult = 1) {
   GemmArgs a{};
   a.tmA = A;
   a.tmB = &g.tmB;
@@ -1236,24 +1126,27 @@ GemmArgs gemm_args(cvr_ctx* c, const GemmPlan& g, const CUtensorMap* A, int M) {
   a.pdl = c->pdl;
   a.cta_pair = g.pair;
   a.no_prefetch_b = !c->prefetch_b;
+  a.call = c->call;
+  a.m_mult = m_mult;
   {  // several tiles per CTA: the epilogue overlaps the next mainloop, keep the CTA small (Cfg::EPW)
     const int rows = g.pair ? 256 : 128, units = g.pair ? c->num_sms / 2 : c->num_sms;
     const int64_t tiles = (int64_t)((M + rows - 1) / rows) * (g.N / g.BN);
     a.epw1 = c->epw_mode == 0 || (c->epw_mode == 2 && tiles > 2 * units);
   }
   if (c->gdbg && c->gdbg_n < 32) a.dbg = c->gdbg + (size_t)(c->gdbg_n++) * 160 * 8;
-  if (c->mb && g.mb8ok && g.cn <= 1 && !g.pair && !c->a_resident) {  // weight tiles multicast over 8 row blocks
-    a.mb8 = true;
-    a.tmB = &g.tmB8;
-  }
-  if (g.cn > 1 && c->q(A)) {  // A operands without a quarter map stay unicast
-    a.cn = g.cn;
-    a.tmA = c->q(A);
-  }  // (a cluster-spanning EPI_HEAD without a quarter map fails its launch check: BN * cn != N)
   return a;
 }
 
 cudaError_t run_gemm(cvr_ctx* c, const GemmArgs& a, int kid, cudaStream_t s) {
+  if (c->only_kid >= 0) {  // cvr_repeat_kernel: this role only, back to back (programmatic launches)
+    if (kid != c->only_kid) return cudaSuccess;
+    for (int i = 0; i < c->only_reps; ++i) {
+      cudaError_t r = launch_gemm_bf16(a, s);
+      ++c->launches;
+      if (r != cudaSuccess) return r;
+    }
+    return cudaSuccess;
+  }
   if (a.dbg) c->gdbg_kid.push_back(kid);
   c->pbeg(s);
   cudaError_t r = launch_gemm_bf16(a, s);
@@ -1283,9 +1176,9 @@ int run_mlp_head(cvr_ctx* c, const CUtensorMap* tm_in, size_t pi, int B, float* 
       a.tmOut = &c->st_h[i];
     }
     if ((e = run_gemm(c, a, kid, s)) != cudaSuccess) return c->cuda_fail(e, "gemm MLP launch");
-    if (g.epi == EPI_HEAD_PARTIAL) {
+    if (g.epi == EPI_HEAD_PARTIAL && c->only_kid < 0) {
       c->pbeg(s);
-      e = launch_head_finalize(c->at<float>(c->off_hpart), c->head_parts, c->head_b, scores, B, s);
+      e = launch_head_finalize(c->at<float>(c->off_hpart), c->head_parts, c->head_b, scores, B, s, c->call);
       c->pend(K_HEAD_FIN, s);
       if (e != cudaSuccess) return c->cuda_fail(e, "head finalize launch");
     }
@@ -1296,15 +1189,15 @@ int run_mlp_head(cvr_ctx* c, const CUtensorMap* tm_in, size_t pi, int B, float* 
 
 // S5' (config 4, A20/A26): per layer Y = LN_token(DCN(X) + MHA(X) + FFN(X)); the branch sum is kept in
 // fp32 (S) and the LN runs in the FFN2 epilogue.
-int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, const CUtensorMap* tok_x0, int B,
-                      float* scores, cudaStream_t s) {
+int do_dense_ensemble(cvr_ctx* c, const CUtensorMap* flat_x0, const CUtensorMap* tok_x0, int B, float* scores,
+                      cudaStream_t s) {
   auto& E = c->ens;
   cudaError_t e;
   const int D = c->d, W = (int)c->x0_ld, r = c->r, T = c->T, BT = B * T;
   float* S = c->at<float>(E.off_S);
   const CUtensorMap* flat_xl = flat_x0;
   const CUtensorMap* tok_xl = tok_x0;
-  GemmPlan gp;  // scratch plan for per-call GemmArgs
+  // M rows: B (flat [B, W] operands) or BT (token [B*T, D] operands, m_mult = T)
   auto ga = [&](const CUtensorMap* A, const CUtensorMap* Bm, int M, int N, int K, int BN, Epi epi) {
     GemmArgs a{};
     a.tmA = A;
@@ -1318,13 +1211,14 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     a.num_sms = c->num_sms;
     a.pdl = c->pdl;
     a.cta_pair = c->pair_ens;
+    a.call = c->call;
+    a.m_mult = M == BT ? T : 1;
     const int rows = c->pair_ens ? 256 : 128, units = c->pair_ens ? c->num_sms / 2 : c->num_sms;
     const int64_t tiles = (int64_t)((M + rows - 1) / rows) * (N / BN);
     a.epw1 = c->epw_mode == 0 || (c->epw_mode == 2 && tiles > 2 * units);
     if (c->gdbg && c->gdbg_n < 32) a.dbg = c->gdbg + (size_t)(c->gdbg_n++) * 160 * 8;  // CVR_GEMM_TIMELINE
     return a;
   };
-  (void)gp;
   for (int l = 0; l < c->n_cross; ++l) {
     const std::string p = "ens/" + std::to_string(l) + "/";
     const bool even = l % 2 == 0;
@@ -1356,7 +1250,6 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
       // (the qkv tensor never reaches HBM; same bf16 roundings and attention core as qkv GEMM + mha64)
       GemmArgs a3 = ga(tok_xl, &E.Wqkvh[l], BT, 3 * D, D, 192, EPI_ATTN);
       a3.cta_pair = false;
-      a3.a_resident = c->ens_attn_ar;  // the 128-token X tile stays resident across its 4 heads' tiles
       a3.bias = c->at<float>(E.off_bqkvh[l]);
       a3.out_bf16 = cat;
       a3.ld_x = D + c->ffn;
@@ -1366,36 +1259,12 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
       a3.tmOut = &E.st_qkv;
       a3.bias = c->wptr<float>(p + "mha/bqkv");
       if ((e = run_gemm(c, a3, K_ENS_QKV, s)) != cudaSuccess) return c->cuda_fail(e, "ens qkv");
-      c->pbeg(s);
-      e = launch_mha64(c->at<__nv_bfloat16>(E.off_qkv), cat, D + c->ffn, B, c->n_heads, s);  // O -> cat[:, :D]
-      c->pend(K_MHA, s);
-      if (e != cudaSuccess) return c->cuda_fail(e, "mha64");
-    }
-    if (c->ens_fused_ffn && D == 256 && c->ffn == 1024) {
-      // FFN + out-projection + branch-sum LN in one kernel: the FFN hidden never leaves the SM (ens_ffn.cu)
-      EnsFfnArgs f{};
-      f.tmX = tok_xl;
-      f.tmO = &E.tm_O;
-      f.tmW1 = &E.W1f[l];
-      f.tmWc = &E.Wcf[l];
-      f.tmY = even ? &E.sttok_xa : &E.sttok_xb;
-      f.b1 = c->wptr<float>(p + "ffn/b1");
-      f.bcat = c->at<float>(E.off_catb[l]);
-      f.S = S;
-      f.gamma = c->wptr<float>(p + "ln/gamma");
-      f.beta = c->wptr<float>(p + "ln/beta");
-      f.M = BT;
-      f.D = D;
-      f.F = c->ffn;
-      f.num_sms = c->num_sms;
-      f.pdl = c->pdl;
-      c->pbeg(s);
-      e = launch_ens_ffn_ln(f, s);
-      c->pend(K_ENS_FFN2_LN, s);
-      if (e != cudaSuccess) return c->cuda_fail(e, "ens fused ffn + ln");
-      flat_xl = even ? &E.flat_xa : &E.flat_xb;
-      tok_xl = even ? &E.tok_xa : &E.tok_xb;
-      continue;
+      if (c->only_kid < 0) c->pbeg(s);
+      if (c->only_kid < 0) {
+        e = launch_mha64(c->at<__nv_bfloat16>(E.off_qkv), cat, D + c->ffn, B, c->n_heads, s, c->call);  // O -> cat[:, :D]
+        c->pend(K_MHA, s);
+        if (e != cudaSuccess) return c->cuda_fail(e, "mha64");
+      }
     }
     // FFN hidden -> cat[:, D:]
     GemmArgs a5 = ga(tok_xl, &E.W1[l], BT, c->ffn, D, 256, EPI_BIAS_RELU);
@@ -1415,7 +1284,6 @@ int do_dense_ensemble(cvr_ctx* c, const void* x0, const CUtensorMap* flat_x0, co
     flat_xl = even ? &E.flat_xa : &E.flat_xb;
     tok_xl = even ? &E.tok_xa : &E.tok_xb;
   }
-  (void)x0;
   return run_mlp_head(c, flat_xl, 0, B, scores, s);
 }
 
@@ -1454,55 +1322,28 @@ int do_dense_masknet(cvr_ctx* c, const CUtensorMap* tm_x0, int B, float* scores,
     au.tmOut = &K.tm_cat_st;
     au.group_n = K.Wp;
     if ((e = run_gemm(c, au, K_MASK_MUL, s)) != cudaSuccess) return c->cuda_fail(e, "MaskNet grouped mask blocks");
-  } else
-  for (int p = 0; p < K.P; ++p) {
-    const CUtensorMap* x_in = &K.tm_x0p;
-    for (int q = 0; q < S; ++q) {
-      const int j = p * S + q;
-      GemmPlan gu;
-      gu.N = K.Wp;
-      gu.K = c->r;
-      gu.BN = K.bn_u;
-      gu.epi = EPI_MASK;
-      GemmArgs au = gemm_args(c, gu, &K.tm_Hblk[j], B);
-      au.tmB = &K.tmB_U[j];
-      au.tmXl = x_in;
-      au.bias = c->wptr<float>("mask/" + std::to_string(p) + "/" + std::to_string(q) + "/b");
-      au.tmOut = q + 1 == S ? &K.st_cat[p] : &K.st_tmp[q % 2];
-      if ((e = run_gemm(c, au, K_MASK_MUL, s)) != cudaSuccess) return c->cuda_fail(e, "MaskNet mask block");
-      x_in = &K.tm_tmp[q % 2];
+  } else {
+    for (int p = 0; p < K.P; ++p) {
+      const CUtensorMap* x_in = &K.tm_x0p;
+      for (int q = 0; q < S; ++q) {
+        const int j = p * S + q;
+        GemmPlan gu;
+        gu.N = K.Wp;
+        gu.K = c->r;
+        gu.BN = K.bn_u;
+        gu.epi = EPI_MASK;
+        GemmArgs au = gemm_args(c, gu, &K.tm_Hblk[j], B);
+        au.tmB = &K.tmB_U[j];
+        au.tmXl = x_in;
+        au.bias = c->wptr<float>("mask/" + std::to_string(p) + "/" + std::to_string(q) + "/b");
+        au.tmOut = q + 1 == S ? &K.st_cat[p] : &K.st_tmp[q % 2];
+        if ((e = run_gemm(c, au, K_MASK_MUL, s)) != cudaSuccess) return c->cuda_fail(e, "MaskNet mask block");
+        x_in = &K.tm_tmp[q % 2];
+      }
     }
   }
   // MLP tower + head on cat [B, P * Wp]: plan[1..]
-  cudaError_t e2;
-  const CUtensorMap* tm_in = &K.tm_cat;
-  for (int i = 0; i < c->n_mlp; ++i) {
-    const GemmPlan& g = c->plan[1 + i];
-    GemmArgs am = gemm_args(c, g, tm_in, B);
-    am.bias = c->wptr<float>("mlp/" + std::to_string(i) + "/b");
-    int kid = K_GEMM_MLP;
-    if (g.epi == EPI_HEAD) {
-      am.head_w = c->wptr<float>("head/w");
-      am.head_b = c->head_b;
-      am.scores = scores;
-      kid = K_GEMM_HEAD;
-    } else if (g.epi == EPI_HEAD_PARTIAL) {
-      am.head_w = c->wptr<float>("head/w");
-      am.partial = c->at<float>(c->off_hpart);
-      kid = K_GEMM_HEAD;
-    } else {
-      am.tmOut = &c->st_h[i];
-    }
-    if ((e2 = run_gemm(c, am, kid, s)) != cudaSuccess) return c->cuda_fail(e2, "MaskNet MLP launch");
-    if (g.epi == EPI_HEAD_PARTIAL) {
-      c->pbeg(s);
-      e2 = launch_head_finalize(c->at<float>(c->off_hpart), c->head_parts, c->head_b, scores, B, s);
-      c->pend(K_HEAD_FIN, s);
-      if (e2 != cudaSuccess) return c->cuda_fail(e2, "head finalize launch");
-    }
-    if (g.epi == EPI_BIAS_RELU) tm_in = &c->tm_h[i];
-  }
-  return CVR_OK;
+  return run_mlp_head(c, &K.tm_cat, 1, B, scores, s);
 }
 
 int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, const CUtensorMap* tm_x0_tok, int B, float* scores,
@@ -1531,163 +1372,83 @@ int do_dense(cvr_ctx* c, const void* x0, const CUtensorMap* tm_x0, const CUtenso
     a.head_w = c->wptr<float>("head/w");
     a.head_b = c->wptr<float>("head/b");
     a.scores = scores;
+    a.call = c->call;
     c->pbeg(s);
     e = launch_dense_f32(a, s);
     c->pend(K_DENSE_F32, s);
     if (e != cudaSuccess) return c->cuda_fail(e, "dense_f32 launch");
     return CVR_OK;
   }
-  if (c->backbone == CVR_ENSEMBLE) return do_dense_ensemble(c, x0, tm_x0, tm_x0_tok, B, scores, s);
+  if (c->backbone == CVR_ENSEMBLE) return do_dense_ensemble(c, tm_x0, tm_x0_tok, B, scores, s);
   if (c->backbone == CVR_MASKNET) return do_dense_masknet(c, tm_x0, B, scores, s);
-  // ---- bf16 low-rank DCN-v2 on tcgen05
+  // ---- bf16 low-rank DCN-v2 on tcgen05: per layer t = x_l V^T (EPI_STORE), x_{l+1} = x0 * (t U^T + b) + x_l
   const CUtensorMap* tm_xl = tm_x0;
   size_t pi = 0;
-  if (c->stack && !c->fused_cross && c->n_cross > 0) {
-    CrossStackArgs a{};
-    a.xa = c->at<__nv_bfloat16>(c->off_xa);
-    a.xb = c->at<__nv_bfloat16>(c->off_xb);
-    a.t = c->at<__nv_bfloat16>(c->off_t);
-    for (int l = 0; l < c->n_cross; ++l) a.bias[l] = c->wptr<float>("dcn/" + std::to_string(l) + "/b");
-    a.done = c->at<int>(c->off_stack_done);
-    a.M = B;
-    a.W = (int)c->x0_ld;
-    a.R = c->r;
-    a.L = c->n_cross;
-    a.num_sms = c->num_sms;
-    a.dbg = c->dbg;
-    c->pbeg(s);
-    e = launch_cross_stack(tm_x0, c->at<CrossStackTables>(c->off_stack_tbl), a, s);
-    c->pend(K_CROSS_STACK, s);
-    if (e != cudaSuccess) return c->cuda_fail(e, "cross_stack launch");
-    pi = 2 * c->n_cross;
-    tm_xl = (c->n_cross - 1) % 2 == 0 ? &c->tm_xa : &c->tm_xb;
-    return run_mlp_head(c, tm_xl, pi, B, scores, s);
-  }
   for (int l = 0; l < c->n_cross; ++l) {
     const GemmPlan& gv = c->plan[pi++];
     const GemmPlan& gu = c->plan[pi++];
     const bool even = l % 2 == 0;
-    if (c->fused_cross) {
-      CrossFusedArgs a{};
-      a.tmXl = tm_xl;
-      a.tmV = &c->tm_v256[l];
-      a.tmT = &c->tm_t;
-      a.tmU = &gu.tmB;
-      a.tmX0 = tm_x0;
-      a.tmOut = even ? &c->st_xa : &c->st_xb;
-      a.bias = c->wptr<float>("dcn/" + std::to_string(l) + "/b");
-      a.part = c->at<float>(c->off_part);
-      a.t_out = c->at<__nv_bfloat16>(c->off_t);
-      a.M = B;
-      a.W = (int)c->x0_ld;
-      a.R = c->r;
-      a.pdl = c->pdl;
-      a.dbg = c->dbg;
-      c->dbg_ctas = (B + 127) / 128 * 4;
-      c->pbeg(s);
-      e = launch_cross_fused(a, s);
-      c->pend(K_CROSS_FUSED, s);
-      if (e != cudaSuccess) return c->cuda_fail(e, "cross_fused launch");
-      tm_xl = even ? &c->tm_xa : &c->tm_xb;
-      continue;
-    }
     GemmArgs av = gemm_args(c, gv, tm_xl, B);
     av.tmOut = &c->st_t;
-    if (c->xv_splitk && c->r == 256 && c->x0_ld >= 256) {
-      // one 128 x 256 tile per row block, K split over a 4-CTA cluster (gemm_splitk.cu)
-      av.tmA = tm_xl;
-      av.tmB = &c->tm_v256[l];
-      av.out_bf16 = c->at<__nv_bfloat16>(c->off_t);
-      av.ld_x = c->r;
-      av.partial = c->xv_splitk == 2 ? c->at<float>(c->off_xchg) : nullptr;
-      if (av.dbg) c->gdbg_kid.push_back(K_GEMM_V);
-      c->pbeg(s);
-      e = launch_gemm_splitk(av, s);
-      c->pend(K_GEMM_V, s);
-      if (e != cudaSuccess) return c->cuda_fail(e, "gemm V (split-K) launch");
-    } else if ((e = run_gemm(c, av, K_GEMM_V, s)) != cudaSuccess) {
-      return c->cuda_fail(e, "gemm V launch");
-    }
+    if ((e = run_gemm(c, av, K_GEMM_V, s)) != cudaSuccess) return c->cuda_fail(e, "gemm V launch");
     GemmArgs au = gemm_args(c, gu, &c->tm_t, B);
     au.tmOut = even ? &c->st_xa : &c->st_xb;
     au.tmX0 = tm_x0;
     au.tmXl = tm_xl;
     au.bias = c->wptr<float>("dcn/" + std::to_string(l) + "/b");
-    au.a_resident = c->a_resident;
     if ((e = run_gemm(c, au, K_GEMM_U, s)) != cudaSuccess) return c->cuda_fail(e, "gemm U launch");
     tm_xl = even ? &c->tm_xa : &c->tm_xb;
   }
   return run_mlp_head(c, tm_xl, pi, B, scores, s);
 }
 
-}  // namespace
+// x0 tensor maps of a caller buffer (standalone cvr_dense on a buffer that is not an x0 slot)
+int user_x0_maps(cvr_ctx* c, const void* d_x0, int batch, CUtensorMap* tm, CUtensorMap* tmt) {
+  const char* er = nullptr;
+  if (encode_tmap_bf16(tm, d_x0, batch, c->x0_ld, c->x0_ld, 128, &er) != 0 ||
+      (c->backbone == CVR_ENSEMBLE && encode_tmap_bf16(tmt, d_x0, (int64_t)batch * c->T, c->d, c->d, 128, &er) != 0))
+    return c->fail(CVR_E_CUDA, "tensor map encode: %s", er ? er : "?");
+  return CVR_OK;
+}
 
-namespace {
-
-// Run one executor stage: replay a cached CUDA graph keyed by the stage's arguments, or capture one
-// (the stage's launches become graph nodes; PDL launches become programmatic edges).  Falls back to
-// direct launches on the legacy stream, while profiling, or inside a caller's own capture.
+// Run one executor stage for slot `slot`: replay its graph (captured at first use; the batch is read from the
+// per-call block, so the same graph serves every batch and batch size), or launch directly (graphs off, while
+// profiling, or inside a caller's own capture).
 template <typename F>
-int run_stage(cvr_ctx* c, const uint64_t (&key)[7], cudaStream_t s, F&& enqueue) {
+int run_stage(cvr_ctx* c, int kind, int slot, cudaStream_t s, F&& enqueue) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (!c->use_graphs || s == nullptr || c->prof_on || cudaStreamIsCapturing(s, &cs) != cudaSuccess ||
       cs != cudaStreamCaptureStatusNone)
     return enqueue(s);
-  for (auto& g : c->graphs) {
-    if (memcmp(g.key, key, sizeof g.key) == 0) {
-      g.last_use = ++c->use_clock;
-      cudaError_t e = cudaGraphLaunch(g.exec, s);
-      if (e != cudaSuccess) return c->cuda_fail(e, "cudaGraphLaunch");
-      c->launches += g.n_kernels;
-      return CVR_OK;
+  cudaGraphExec_t& ge = c->gexec[kind][slot];
+  if (!ge) {
+    const int64_t l0 = c->launches;
+    cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return c->cuda_fail(e, "cudaStreamBeginCapture");
+    int st = enqueue(s);
+    cudaGraph_t graph = nullptr;
+    e = cudaStreamEndCapture(s, &graph);
+    const int64_t nk = c->launches - l0;
+    c->launches = l0;
+    if (st != CVR_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
     }
+    if (e != cudaSuccess) return c->cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&ge, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+      ge = nullptr;
+      return c->cuda_fail(e, "cudaGraphInstantiate");
+    }
+    c->gkernels[kind][slot] = nk;
+    ++c->graph_captures;
   }
-  // capture only keys seen before: one-off shapes (dynamic batching) launch directly
-  bool seen = false;
-  for (auto& k : c->seen_keys)
-    if (memcmp(k.data(), key, sizeof(uint64_t) * 7) == 0) seen = true;
-  if (!seen) {
-    std::array<uint64_t, 7> k;
-    memcpy(k.data(), key, sizeof(uint64_t) * 7);
-    if (c->seen_keys.size() >= 256) c->seen_keys.erase(c->seen_keys.begin());
-    c->seen_keys.push_back(k);
-    return enqueue(s);
-  }
-  const int64_t l0 = c->launches;
-  cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
-  if (e != cudaSuccess) return c->cuda_fail(e, "cudaStreamBeginCapture");
-  int st = enqueue(s);
-  cudaGraph_t graph = nullptr;
-  e = cudaStreamEndCapture(s, &graph);
-  const int64_t nk = c->launches - l0;
-  c->launches = l0;
-  if (st != CVR_OK) {
-    if (graph) cudaGraphDestroy(graph);
-    return st;
-  }
-  if (e != cudaSuccess) return c->cuda_fail(e, "cudaStreamEndCapture");
-  cvr_ctx::GraphEntry ge;
-  memcpy(ge.key, key, sizeof ge.key);
-  e = cudaGraphInstantiate(&ge.exec, graph, 0);
-  cudaGraphDestroy(graph);
-  if (e != cudaSuccess) return c->cuda_fail(e, "cudaGraphInstantiate");
-  ge.n_kernels = nk;
-  ge.last_use = ++c->use_clock;
-  if (c->graphs.size() >= 32) {  // evict the least recently used
-    size_t lru = 0;
-    for (size_t i = 1; i < c->graphs.size(); ++i)
-      if (c->graphs[i].last_use < c->graphs[lru].last_use) lru = i;
-    cudaGraphExecDestroy(c->graphs[lru].exec);
-    c->graphs.erase(c->graphs.begin() + lru);
-  }
-  c->graphs.push_back(ge);
-  e = cudaGraphLaunch(ge.exec, s);
+  cudaError_t e = cudaGraphLaunch(ge, s);
   if (e != cudaSuccess) return c->cuda_fail(e, "cudaGraphLaunch");
-  c->launches += nk;
+  c->launches += c->gkernels[kind][slot];
   return CVR_OK;
 }
-
-uint64_t u64(const void* p) { return (uint64_t)(uintptr_t)p; }
 
 }  // namespace
 
@@ -1702,9 +1463,7 @@ int cvr_embed(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, in
   if (batch < 0 || batch > c->max_batch) return c->fail(CVR_E_ARG, "batch %d outside [0, %d]", batch, c->max_batch);
   if (!d_offsets || !d_x0 || (nnz > 0 && !d_indices) || (c->F && batch && !d_dense) || nnz < 0)
     return c->fail(CVR_E_ARG, "null pointer or negative nnz");
-  const uint64_t ke[7] = {3, u64(d_indices), u64(d_offsets), (uint64_t)nnz, (uint64_t)batch, u64(d_dense), u64(d_x0)};
-  return run_stage(c, ke, (cudaStream_t)stream,
-                   [&](cudaStream_t s) { return do_embed(c, d_indices, d_offsets, nnz, batch, d_dense, d_x0, s); });
+  return do_embed(c, d_indices, d_offsets, nnz, batch, d_dense, d_x0, (cudaStream_t)stream);
 }
 
 int cvr_set_feature_spec(cvr_ctx* c, int n, const int64_t* vocab, const int* pool_mode) {
@@ -1722,8 +1481,6 @@ int cvr_set_feature_spec(cvr_ctx* c, int n, const int64_t* vocab, const int* poo
     c->tmean[t] = pool_mode[t];
     c->any_mean |= pool_mode[t] == 1;
   }
-  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-  c->graphs.clear();
   if (c->tables_loaded) {
     for (size_t i = 0; i < c->local_tables.size(); ++i) {
       c->htables[i].vocab = c->tvocab[c->local_tables[i]];
@@ -1748,10 +1505,7 @@ int cvr_embed_keys(cvr_ctx* c, const uint64_t* d_keys, const int32_t* d_offsets,
   if (batch < 0 || batch > c->max_batch) return c->fail(CVR_E_ARG, "batch %d outside [0, %d]", batch, c->max_batch);
   if (!d_offsets || !d_x0 || (nnz > 0 && !d_keys) || (c->F && batch && !d_dense) || nnz < 0)
     return c->fail(CVR_E_ARG, "null pointer or negative nnz");
-  const uint64_t ke[7] = {5, u64(d_keys), u64(d_offsets), (uint64_t)nnz, (uint64_t)batch, u64(d_dense), u64(d_x0)};
-  return run_stage(c, ke, (cudaStream_t)stream, [&](cudaStream_t s) {
-    return do_embed(c, nullptr, d_offsets, nnz, batch, d_dense, d_x0, s, 0, d_keys);
-  });
+  return do_embed(c, nullptr, d_offsets, nnz, batch, d_dense, d_x0, (cudaStream_t)stream, 0, d_keys);
 }
 
 int cvr_dense(cvr_ctx* c, const void* d_x0, int batch, float* d_scores, cvr_stream_t stream) {
@@ -1763,39 +1517,31 @@ int cvr_dense(cvr_ctx* c, const void* d_x0, int batch, float* d_scores, cvr_stre
   if (batch == 0) return CVR_OK;
   const CUtensorMap* tm = nullptr;
   const CUtensorMap* tmt = nullptr;
+  CUtensorMap um, umt;
   if (c->backbone != CVR_DCN_FULL) {
     const bool ens = c->backbone == CVR_ENSEMBLE;
-    if (d_x0 == c->ws + c->off_x0[0]) {
-      tm = ens ? &c->ens.flat_x0[0] : &c->tm_x0slot[0];
-      tmt = &c->ens.tok_x0[0];
-    } else if (d_x0 == c->ws + c->off_x0[1]) {
-      tm = ens ? &c->ens.flat_x0[1] : &c->tm_x0slot[1];
-      tmt = &c->ens.tok_x0[1];
+    int slot = d_x0 == c->ws + c->off_x0[0] ? 0 : (d_x0 == c->ws + c->off_x0[1] ? 1 : -1);
+    if (slot >= 0) {
+      tm = ens ? &c->ens.flat_x0[slot] : &c->tm_x0slot[slot];
+      tmt = &c->ens.tok_x0[slot];
     } else {
-      if (d_x0 != c->last_x0 || batch != c->last_x0_rows) {
-        const char* er = nullptr;
-        if (encode_tmap_bf16(&c->tm_x0user, d_x0, batch, c->x0_ld, c->x0_ld, 128, &er) != 0 ||
-            c->add_q(&c->tm_x0user, d_x0, batch, c->x0_ld, c->x0_ld, &er) != 0 ||
-            (ens && encode_tmap_bf16(&c->ens.tok_user, d_x0, (int64_t)batch * c->T, c->d, c->d, 128, &er) != 0))
-          return c->fail(CVR_E_CUDA, "tensor map encode: %s", er);
-        c->last_x0 = d_x0;
-        c->last_x0_rows = batch;
-      }
-      tm = &c->tm_x0user;
-      tmt = &c->ens.tok_user;
+      if ((st = user_x0_maps(c, d_x0, batch, &um, &umt)) != CVR_OK) return st;
+      tm = &um;
+      tmt = &umt;
     }
   }
-  const uint64_t kd[7] = {4, u64(d_x0), (uint64_t)batch, u64(d_scores), 0, 0, 0};
-  return run_stage(c, kd, (cudaStream_t)stream,
-                   [&](cudaStream_t s) { return do_dense(c, d_x0, tm, tmt, batch, d_scores, s); });
+  return do_dense(c, d_x0, tm, tmt, batch, d_scores, (cudaStream_t)stream);
 }
 
 }  // extern "C"
 
 namespace {
-// the two-stream executor behind cvr_score (row ids) and cvr_score_keys (raw keys, hashed in the gather)
+// the two-stream executor behind cvr_score (row ids) and cvr_score_keys (raw keys, hashed in the gather):
+// slot = k % 2; on s_embed: [wait dense(k-2)] -> set_call(slot) -> embed graph(slot) -> event; on s_dense:
+// [wait embed(k)] -> dense graph(slot) -> event.  Both graphs read the batch from the slot's call block.
 int score_impl(cvr_ctx* c, const int32_t* d_indices, const uint64_t* d_keys, const int32_t* d_offsets, int64_t nnz,
-               int batch, const float* d_dense, float* d_scores, cvr_stream_t s_embed, cvr_stream_t s_dense) {
+               int batch, const float* d_dense, float* d_scores, cvr_stream_t s_embed, cvr_stream_t s_dense,
+               cudaStream_t s_after_wait = nullptr) {
   if (!c) return CVR_E_ARG;
   int st = check_ready(c, true, true);
   if (st) return st;
@@ -1806,26 +1552,45 @@ int score_impl(cvr_ctx* c, const int32_t* d_indices, const uint64_t* d_keys, con
   cudaStream_t se = (cudaStream_t)s_embed, sd = (cudaStream_t)s_dense;
   const int slot = (int)(c->k & 1);
   cudaError_t e = cudaSuccess;
-  if (c->k >= 2) e = cudaStreamWaitEvent(se, c->ev_dense[slot], 0);  // dense(k-2) released the slot
+  if (c->k >= 2) e = cudaStreamWaitEvent(se, c->ev_dense[slot], 0);  // dense(k-2) released the slot (and its block)
   if (e != cudaSuccess) return c->cuda_fail(e, "wait dense(k-2)");
+  CallArgs v{};
+  v.indices = d_indices;
+  v.keys = d_keys;
+  v.offsets = d_offsets;
+  v.dense = d_dense;
+  v.scores = d_scores;
+  v.nnz = nnz;
+  v.B = batch;
+  CallArgs* blk = c->at<CallArgs>(c->off_call[slot]);
+  c->pbeg(se);
+  e = launch_set_call(v, blk, se);
+  c->pend(K_SET_CALL, se);
+  if (e != cudaSuccess) return c->cuda_fail(e, "set_call launch");
+  if (s_after_wait && (e = cudaStreamWaitEvent(se, c->ev_copy[slot], 0)) != cudaSuccess)  // host-fed: H2D landed
+    return c->cuda_fail(e, "wait copy");
   void* x0 = c->ws + c->off_x0[slot];
-  const uint64_t ke[7] = {d_keys ? 6u : 1u, u64(d_keys ? (const void*)d_keys : (const void*)d_indices), u64(d_offsets),
-                          (uint64_t)nnz, (uint64_t)batch, u64(d_dense), u64(x0)};
-  st = run_stage(c, ke, se, [&](cudaStream_t s) {
-    return do_embed(c, d_indices, d_offsets, nnz, batch, d_dense, x0, s, c->embed_bps_pipe, d_keys);
+  const int Bmax = c->max_batch;
+  c->call = blk;
+  st = run_stage(c, d_keys ? cvr_ctx::G_EMBED_KEYS : cvr_ctx::G_EMBED, slot, se, [&](cudaStream_t s) {
+    return do_embed(c, d_indices, d_offsets, nnz, Bmax, d_dense, x0, s, c->embed_bps_pipe, d_keys);
   });
-  if (st) return st;
-  if ((e = cudaEventRecord(c->ev_embed[slot], se)) != cudaSuccess) return c->cuda_fail(e, "record embed");
-  if ((e = cudaStreamWaitEvent(sd, c->ev_embed[slot], 0)) != cudaSuccess) return c->cuda_fail(e, "wait embed");
-  if (batch > 0) {
+  if (st) {
+    c->call = nullptr;
+    return st;
+  }
+  if ((e = cudaEventRecord(c->ev_embed[slot], se)) != cudaSuccess) st = c->cuda_fail(e, "record embed");
+  if (!st && (e = cudaStreamWaitEvent(sd, c->ev_embed[slot], 0)) != cudaSuccess) st = c->cuda_fail(e, "wait embed");
+  if (!st && batch > 0) {
     const bool ens = c->backbone == CVR_ENSEMBLE;
     const CUtensorMap* tm = (c->backbone == CVR_DCN_LOWRANK || c->backbone == CVR_MASKNET) ? &c->tm_x0slot[slot]
                             : ens ? &c->ens.flat_x0[slot] : nullptr;
     const CUtensorMap* tmt = ens ? &c->ens.tok_x0[slot] : nullptr;
-    const uint64_t kd[7] = {2, u64(x0), (uint64_t)batch, u64(d_scores), 0, 0, 0};
-    st = run_stage(c, kd, sd, [&](cudaStream_t s) { return do_dense(c, x0, tm, tmt, batch, d_scores, s); });
-    if (st) return st;
+    st = run_stage(c, cvr_ctx::G_DENSE, slot, sd,
+                   [&](cudaStream_t s) { return do_dense(c, x0, tm, tmt, Bmax, d_scores, s); });
   }
+  c->call = nullptr;
+  if (st) return st;
   if ((e = cudaEventRecord(c->ev_dense[slot], sd)) != cudaSuccess) return c->cuda_fail(e, "record dense");
   c->k++;
   return CVR_OK;
@@ -1876,7 +1641,6 @@ int cvr_score_host(cvr_ctx* c, const int32_t* h_indices, const int32_t* h_offset
   if (c->F && batch && (e = cudaMemcpyAsync(dd, h_dense, (size_t)batch * c->F * 4, cudaMemcpyHostToDevice, sc)) != cudaSuccess)
     return c->cuda_fail(e, "H2D dense");
   if ((e = cudaEventRecord(c->ev_copy[slot], sc)) != cudaSuccess) return c->cuda_fail(e, "record copy");
-  if ((e = cudaStreamWaitEvent((cudaStream_t)s_embed, c->ev_copy[slot], 0)) != cudaSuccess) return c->cuda_fail(e, "wait copy");
   // S8: page-locked (mapped) h_scores -> the head kernel stores the scores straight into host memory over PCIe
   // (zero-copy: no D2H copy on the dense stream's critical path, measured +7.7 us per c2 step); pageable
   // memory -> device staging + a D2H copy on s_dense
@@ -1887,7 +1651,8 @@ int cvr_score_host(cvr_ctx* c, const int32_t* h_indices, const int32_t* h_offset
       zc = reinterpret_cast<float*>(pa.devicePointer);
     cudaGetLastError();  // (a failed query leaves a non-sticky error code)
   }
-  st = cvr_score(c, di, doff, nnz, batch, dd, zc ? zc : ds, s_embed, s_dense);
+  // the embed stream sets the call block, then waits for this batch's copies (ev_copy[slot]) before the graph
+  st = score_impl(c, di, nullptr, doff, nnz, batch, dd, zc ? zc : ds, s_embed, s_dense, sc);
   if (st) return st;
   if (!zc && batch && (e = cudaMemcpyAsync(h_scores, ds, (size_t)batch * 4, cudaMemcpyDeviceToHost, sd)) != cudaSuccess)
     return c->cuda_fail(e, "D2H scores");
@@ -1983,7 +1748,6 @@ int cvr_embed_fused(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offse
   a.world = c->world;
   a.rank = c->rank;
   a.Bl = batch_global / c->world;
-  a.v2 = false;
   c->pbeg(s);
   e = launch_embed(a, c->num_sms, s);
   c->pend(K_EMBED, s);
@@ -2015,25 +1779,147 @@ int cvr_release_peers(cvr_ctx* c, uint32_t epoch, cvr_stream_t stream) {
   return CVR_OK;
 }
 
-int cvr_ipc_get_handle(const void* d_ptr, void* handle64) {
-  if (!d_ptr || !handle64) return CVR_E_ARG;
+// CUDA IPC handles name a whole allocation (cudaIpcGetMemHandle), but callers pass tensors that a caching allocator
+// may have sub-allocated at an offset inside it: the handle blob carries that offset (cuMemGetAddressRange) and
+// the opening side adds it back; the opened base is remembered so cvr_ipc_close_handle can unmap it.
+static std::map<void*, void*> g_ipc_bases;  // opened tensor pointer -> mapped allocation base
+
+int cvr_ipc_get_handle(const void* d_ptr, void* handle) {
+  if (!d_ptr || !handle) return CVR_E_ARG;
+  static PFN_cuMemGetAddressRange_v3020 range = nullptr;
+  if (!range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return CVR_E_CUDA;
+    range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (CUdeviceptr)(uintptr_t)d_ptr) != CUDA_SUCCESS) return CVR_E_CUDA;
   cudaIpcMemHandle_t h;
-  if (cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)) != cudaSuccess) return CVR_E_CUDA;
+  if (cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)) != cudaSuccess) return CVR_E_CUDA;
   static_assert(sizeof(h) == 64, "CUDA IPC handles are 64 bytes");
-  memcpy(handle64, &h, 64);
+  const int64_t off = (int64_t)((uintptr_t)d_ptr - (uintptr_t)base);
+  memcpy(handle, &h, 64);
+  memcpy(reinterpret_cast<uint8_t*>(handle) + 64, &off, 8);
   return CVR_OK;
 }
 
-int cvr_ipc_open_handle(const void* handle64, void** d_ptr) {
-  if (!handle64 || !d_ptr) return CVR_E_ARG;
+int cvr_ipc_open_handle(const void* handle, void** d_ptr) {
+  if (!handle || !d_ptr) return CVR_E_ARG;
   cudaIpcMemHandle_t h;
-  memcpy(&h, handle64, 64);
-  return cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? CVR_OK : CVR_E_CUDA;
+  int64_t off = 0;
+  memcpy(&h, handle, 64);
+  memcpy(&off, reinterpret_cast<const uint8_t*>(handle) + 64, 8);
+  if (off < 0) return CVR_E_ARG;
+  void* base = nullptr;
+  if (cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return CVR_E_CUDA;
+  *d_ptr = reinterpret_cast<uint8_t*>(base) + off;
+  g_ipc_bases[*d_ptr] = base;
+  return CVR_OK;
 }
 
 int cvr_ipc_close_handle(void* d_ptr) {
   if (!d_ptr) return CVR_E_ARG;
-  return cudaIpcCloseMemHandle(d_ptr) == cudaSuccess ? CVR_OK : CVR_E_CUDA;
+  auto it = g_ipc_bases.find(d_ptr);
+  if (it == g_ipc_bases.end()) return CVR_E_ARG;
+  void* base = it->second;
+  g_ipc_bases.erase(it);
+  bool still_used = false;  // several tensors of one allocation share one mapping
+  for (auto& kv : g_ipc_bases) still_used |= kv.second == base;
+  if (still_used) return CVR_OK;
+  return cudaIpcCloseMemHandle(base) == cudaSuccess ? CVR_OK : CVR_E_CUDA;
+}
+
+// ---- S4 through the library's own NCCL communicator ----------------------------------
+int cvr_comm_unique_id(cvr_nccl_id* id) {
+  if (!id) return CVR_E_ARG;
+  if (!g_nccl.load()) return CVR_E_NCCL;
+  return g_nccl.getUniqueId(id) == 0 ? CVR_OK : CVR_E_NCCL;
+}
+
+int cvr_comm_init(cvr_ctx* c, const cvr_nccl_id* id, int world, int rank) {
+  if (!c || !id) return CVR_E_ARG;
+  if (!c->cuda_ready) return c->fail(CVR_E_STATE, "cvr_comm_init before cvr_set_workspace");
+  if (world != c->world || rank != c->rank)
+    return c->fail(CVR_E_ARG, "cvr_comm_init(world %d, rank %d) != the ctx's world_size %d / rank %d", world, rank,
+                   c->world, c->rank);
+  if (c->nccl_comm) return c->fail(CVR_E_STATE, "communicator already initialised");
+  if (!g_nccl.load()) return c->fail(CVR_E_NCCL, "%s", g_nccl.why.c_str());
+  void* comm = nullptr;
+  const int r = g_nccl.commInitRank(&comm, world, *id, rank);
+  if (r != 0) return c->fail(CVR_E_NCCL, "ncclCommInitRank: %s", g_nccl.err(r));
+  c->nccl_comm = comm;
+  c->comm_world = world;
+  c->comm_rank = rank;
+  return CVR_OK;
+}
+
+int cvr_exchange(cvr_ctx* c, const void* d_send, void* d_recv, int batch_global, void* d_x0_local,
+                 cvr_stream_t stream) {
+  if (!c) return CVR_E_ARG;
+  if (!c->cuda_ready) return c->fail(CVR_E_STATE, "workspace not set");
+  if (!c->nccl_comm) return c->fail(CVR_E_STATE, "cvr_exchange before cvr_comm_init");
+  if (!d_send || !d_recv || !d_x0_local || batch_global < 0 || batch_global % c->world ||
+      batch_global / c->world > c->max_batch)
+    return c->fail(CVR_E_ARG, "bad arguments (batch_global %d, world %d)", batch_global, c->world);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t chunk = (size_t)(batch_global / c->world) * c->T_pad * c->d * elt_size(c->act);
+  if (chunk) {
+    // chunk dst of d_send (destination-major [dst][b_local][t_slot][d]) -> rank dst; chunk src of d_recv <- rank src
+    int r = g_nccl.groupStart();
+    for (int p = 0; p < c->world && r == 0; ++p) {
+      r = g_nccl.send(reinterpret_cast<const uint8_t*>(d_send) + p * chunk, chunk, kNcclUint8, p, c->nccl_comm, s);
+      if (r == 0) r = g_nccl.recv(reinterpret_cast<uint8_t*>(d_recv) + p * chunk, chunk, kNcclUint8, p, c->nccl_comm, s);
+    }
+    const int r2 = g_nccl.groupEnd();
+    if (r != 0 || r2 != 0) return c->fail(CVR_E_NCCL, "grouped ncclSend/ncclRecv: %s", g_nccl.err(r ? r : r2));
+  }
+  ++c->launches;  // (the NCCL kernel)
+  c->pbeg(s);
+  cudaError_t e = launch_unpack(d_recv, d_x0_local, c->x0_ld, c->world, batch_global / c->world, c->T_pad, c->T, c->d,
+                                c->act, s);
+  c->pend(K_UNPACK, s);
+  if (e != cudaSuccess) return c->cuda_fail(e, "unpack launch");
+  return CVR_OK;
+}
+
+int cvr_repeat_kernel(cvr_ctx* c, const char* role, int reps, const void* d_x0, int batch, cvr_stream_t stream,
+                      int* n_launched) {
+  if (!c || !role || reps < 1 || !n_launched) return CVR_E_ARG;
+  int st = check_ready(c, false, true);
+  if (st) return st;
+  if (c->backbone == CVR_DCN_FULL) return c->fail(CVR_E_UNSUPPORTED, "cvr_repeat_kernel: tcgen05 GEMM roles only");
+  int kid = -1;
+  for (int k = 0; k < K_COUNT; ++k)
+    if (!strcmp(role, kKernelNames[k])) kid = k;
+  if (kid < 0 || strncmp(role, "gemm_", 5) != 0) return c->fail(CVR_E_ARG, "unknown GEMM role '%s'", role);
+  float* scores = c->at<float>(c->off_scores[0]);  // (the head writes into the ctx's own score staging)
+  const int64_t l0 = c->launches;
+  c->only_kid = kid;
+  c->only_reps = reps;
+  st = cvr_dense(c, d_x0, batch, scores, stream);
+  c->only_kid = -1;
+  c->only_reps = 1;
+  *n_launched = (int)(c->launches - l0);
+  return st;
+}
+
+int cvr_call_info(const cvr_ctx* c, int slot, cvr_call_record* out) {
+  if (!c || !out || slot < 0 || slot > 1) return CVR_E_ARG;
+  if (!c->cuda_ready) return CVR_E_STATE;
+  CallArgs v{};
+  if (cudaMemcpy(&v, c->ws + c->off_call[slot], sizeof v, cudaMemcpyDeviceToHost) != cudaSuccess) return CVR_E_CUDA;
+  out->d_indices = v.indices;
+  out->d_keys = v.keys;
+  out->d_offsets = v.offsets;
+  out->d_dense = v.dense;
+  out->d_scores = v.scores;
+  out->nnz = v.nnz;
+  out->batch = v.B;
+  out->graph_captures = c->graph_captures;
+  return CVR_OK;
 }
 
 int cvr_unpack_shard(cvr_ctx* c, const void* d_recv, int batch_global, void* d_x0, cvr_stream_t stream) {
@@ -2137,185 +2023,59 @@ int cvr_gemm_bf16(const void* d_A, int64_t lda, const void* d_B, int64_t ldb, vo
 
 int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return CVR_E_ARG;
-  if (!strcmp(key, "graphs")) {
-    c->use_graphs = value != 0;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
+  // every option below changes what the executor's graphs would launch: drop them (recaptured at next use)
+  auto replan = [&]() -> int {
+    c->drop_graphs();
+    if (!c->weights_loaded) return CVR_OK;
+    if (c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);
+    if (c->backbone == CVR_ENSEMBLE) return encode_plan_ensemble(c);
     return CVR_OK;
-  }
-  if (!strcmp(key, "fused_cross")) {
-    if (value && !(c->backbone == CVR_DCN_LOWRANK && c->r == 256)) return c->fail(CVR_E_UNSUPPORTED, "fused cross needs r == 256");
-    c->fused_cross = value != 0;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);  // U tile width
-    return CVR_OK;
-  }
-  if (!strcmp(key, "pair")) {
-    c->pair_ens = value != 0;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    if (c->weights_loaded && c->backbone == CVR_ENSEMBLE) return encode_plan_ensemble(c);
-    return CVR_OK;
-  }
-  if (!strcmp(key, "ens_u_bn")) {
-    if (value != 64 && value != 128) return c->fail(CVR_E_ARG, "ens_u_bn must be 64 or 128");
-    c->ens_u_bn = (int)value;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    if (c->weights_loaded && c->backbone == CVR_ENSEMBLE) return encode_plan_ensemble(c);
-    return CVR_OK;
-  }
-  if (!strcmp(key, "embed_bps")) {
-    c->embed_bps_pipe = (int)value;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    return CVR_OK;
-  }
-  if (!strcmp(key, "embed_variant")) {
-    c->embed_variant = (int)value;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    return CVR_OK;
-  }
-  if (!strcmp(key, "stack")) {
-    c->stack = value != 0;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);  // U tile width
-    return CVR_OK;
-  }
-  if (!strcmp(key, "a_resident")) {
-    c->a_resident = value != 0;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);  // U tile width
-    return CVR_OK;
-  }
+  };
+  auto flag = [&](bool& f) { f = value != 0; return replan(); };
+  if (!strcmp(key, "graphs")) return flag(c->use_graphs);
+  if (!strcmp(key, "pdl")) return flag(c->pdl);
+  if (!strcmp(key, "prefetch_b")) return flag(c->prefetch_b);
+  if (!strcmp(key, "pair")) return flag(c->pair_ens);
+  if (!strcmp(key, "f32_tma_store")) return flag(c->f32_tma_store);
+  if (!strcmp(key, "ens_xv_wave")) return flag(c->ens_xv_wave);
+  if (!strcmp(key, "ens_fused_attn")) return flag(c->ens_fused_attn);
+  if (!strcmp(key, "mask_grouped")) return flag(c->mask_grouped);
   if (!strcmp(key, "zero_copy_scores")) {
     c->zero_copy_scores = value != 0;
     return CVR_OK;
   }
-  if (!strcmp(key, "pair_u")) {
-    c->pair_u = value != 0;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);
-    return CVR_OK;
+  if (!strcmp(key, "embed_bps")) {
+    if (value < 0 || value > 64) return c->fail(CVR_E_ARG, "embed_bps must be in [0, 64]");
+    c->embed_bps_pipe = (int)value;
+    return replan();
   }
-  if (!strcmp(key, "f32_tma_store")) {
-    c->f32_tma_store = value != 0;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    return CVR_OK;
-  }
-  if (!strcmp(key, "ens_xv_wave")) {
-    c->ens_xv_wave = value != 0;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    return CVR_OK;
-  }
-  if (!strcmp(key, "ens_attn_ar")) {
-    c->ens_attn_ar = value != 0;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    return CVR_OK;
-  }
-  if (!strcmp(key, "ens_fused_attn")) {
-    c->ens_fused_attn = value != 0;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    return CVR_OK;
-  }
-  if (!strcmp(key, "prefetch_b")) {
-    c->prefetch_b = value != 0;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    return CVR_OK;
+  if (!strcmp(key, "ens_u_bn")) {
+    if (value != 64 && value != 128) return c->fail(CVR_E_ARG, "ens_u_bn must be 64 or 128");
+    c->ens_u_bn = (int)value;
+    return replan();
   }
   if (!strcmp(key, "xv_bn")) {
     if (value != 0 && value != 64 && value != 128 && value != 256) return c->fail(CVR_E_ARG, "xv_bn: 0, 64, 128 or 256");
     c->xv_bn = (int)value;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);
-    return CVR_OK;
-  }
-  if (!strcmp(key, "pair_xv")) {
-    if (value != 0 && value != 64 && value != 128 && value != 256) return c->fail(CVR_E_ARG, "pair_xv: 0, 64, 128 or 256");
-    c->pair_xv = (int)value;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);
-    return CVR_OK;
-  }
-  if (!strcmp(key, "pair_mlp")) {
-    c->pair_mlp = value != 0;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);
-    return CVR_OK;
-  }
-  if (!strcmp(key, "mb")) {
-    c->mb = value != 0;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    return CVR_OK;
-  }
-  if (!strcmp(key, "mask_grouped")) {
-    c->mask_grouped = value != 0;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    return CVR_OK;
-  }
-  if (!strcmp(key, "ens_fused_ffn")) {
-    c->ens_fused_ffn = value != 0;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    return CVR_OK;
-  }
-  if (!strcmp(key, "epw")) {
-    if (value < 0 || value > 2) return c->fail(CVR_E_ARG, "epw must be 0, 1 or 2");
-    c->epw_mode = (int)value;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    return CVR_OK;
-  }
-  if (!strcmp(key, "xv_splitk")) {
-    if (value < 0 || value > 2) return c->fail(CVR_E_ARG, "xv_splitk: 0, 1 (DSMEM) or 2 (L2 exchange)");
-    c->xv_splitk = (int)value;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    return CVR_OK;
+    return replan();
   }
   if (!strcmp(key, "u_bn")) {
     if (value != 64 && value != 192) return c->fail(CVR_E_ARG, "u_bn must be 64 or 192");
     c->u_bn = (int)value;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);
-    return CVR_OK;
+    return replan();
   }
-  if (!strcmp(key, "mc")) {
-    if (value < 0 || value > 2) return c->fail(CVR_E_ARG, "mc must be 0, 1 or 2");
-    c->mc = (int)value;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    if (c->weights_loaded && c->backbone == CVR_DCN_LOWRANK) return encode_plan(c);
-    return CVR_OK;
-  }
-  if (!strcmp(key, "pdl")) {
-    c->pdl = value != 0;
-    for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-    return CVR_OK;
+  if (!strcmp(key, "epw")) {
+    if (value < 0 || value > 2) return c->fail(CVR_E_ARG, "epw must be 0, 1 or 2");
+    c->epw_mode = (int)value;
+    return replan();
   }
   return c->fail(CVR_E_ARG, "unknown option '%s'", key);
 }
 
 int cvr_concat_requests(int n_req, int n_tables, int n_dense, const int* n_items, const int32_t* const* h_offsets,
-                        const int32_t* const* h_indices, const float* const* h_dense, int32_t* out_offsets,
-                        int32_t* out_indices, int64_t out_indices_cap, float* out_dense, int64_t* out_nnz) {
+                        const int32_t* const* h_indices, const float* const* h_dense, int out_batch_cap,
+                        int32_t* out_offsets, int32_t* out_indices, int64_t out_indices_cap, float* out_dense,
+                        int64_t* out_nnz) {
   if (n_req < 0 || n_tables <= 0 || n_dense < 0 || !n_items || !h_offsets || !h_indices || !out_offsets ||
       !out_indices || !out_nnz || (n_dense && (!h_dense || !out_dense)))
     return CVR_E_ARG;
@@ -2324,6 +2084,7 @@ int cvr_concat_requests(int n_req, int n_tables, int n_dense, const int* n_items
     if (n_items[r] < 0 || !h_offsets[r]) return CVR_E_ARG;
     B += n_items[r];
   }
+  if (B > out_batch_cap) return CVR_E_NOMEM;
   // table-major: for t, for request r, for item i: bag (t, r, i)
   int64_t pos = 0, bag = 0;
   out_offsets[0] = 0;
@@ -2332,7 +2093,9 @@ int cvr_concat_requests(int n_req, int n_tables, int n_dense, const int* n_items
       const int n = n_items[r];
       const int32_t* off = h_offsets[r] + (int64_t)t * n;
       const int32_t lo = off[0], hi = off[n];
-      if (hi < lo) return CVR_E_INDEX;
+      if (lo < 0 || hi < lo) return CVR_E_INDEX;
+      for (int i = 0; i < n; ++i)  // every bag inside [lo, hi], non-decreasing (else the copy below reads out of range)
+        if (off[i + 1] < off[i]) return CVR_E_INDEX;
       const int64_t len = hi - lo;
       if (pos + len > out_indices_cap) return CVR_E_NOMEM;
       if (len) memcpy(out_indices + pos, h_indices[r] + lo, (size_t)len * 4);
@@ -2347,18 +2110,18 @@ int cvr_concat_requests(int n_req, int n_tables, int n_dense, const int* n_items
       row += n_items[r];
     }
   }
-  (void)B;
   *out_nnz = pos;
   return CVR_OK;
 }
 
 int cvr_gather_items(int n_tables, int n_dense, int64_t pool_size, const int32_t* pool_offsets,
                      const int32_t* pool_indices, const float* pool_dense, int n, const int32_t* item_ids,
-                     int32_t* out_offsets, int32_t* out_indices, int64_t out_indices_cap, float* out_dense,
-                     int64_t* out_nnz) {
+                     int out_batch_cap, int32_t* out_offsets, int32_t* out_indices, int64_t out_indices_cap,
+                     float* out_dense, int64_t* out_nnz) {
   if (n_tables <= 0 || n_dense < 0 || pool_size <= 0 || n < 0 || !pool_offsets || !pool_indices || !item_ids ||
       !out_offsets || !out_indices || !out_nnz || (n_dense && (!pool_dense || !out_dense)))
     return CVR_E_ARG;
+  if (n > out_batch_cap) return CVR_E_NOMEM;  // out_offsets [T * cap + 1] and out_dense [cap, F] would overflow
   for (int i = 0; i < n; ++i)
     if (item_ids[i] < 0 || item_ids[i] >= pool_size) return CVR_E_INDEX;
   // pass 1 (parallel over tables): bag lengths -> per-table totals; pass 2: copy at prefix offsets

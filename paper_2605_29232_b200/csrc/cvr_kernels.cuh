@@ -18,6 +18,23 @@ struct TableDesc {
   int mean;             // 1: mean pooling (sum / bag length, empty -> 0); 0: sum pooling
 };
 
+// ---- per-call argument block of the executor (device memory, one per x0 slot) ---------------------------
+// cvr_score / cvr_score_host replay ONE captured CUDA graph per (stage, slot) for every batch: the batch's
+// pointers and row count live in this block, written on the embed stream right before the embed graph
+// (launch_set_call), and every kernel of both stages reads them from here instead of its launch parameters
+// (one graph per stage for every batch size <= max_batch, device-side row count).
+struct CallArgs {
+  const int32_t* indices;
+  const uint64_t* keys;
+  const int32_t* offsets;
+  const float* dense;
+  float* scores;
+  int64_t nnz;
+  int B;                     // rows of this batch (<= max_batch)
+  int pad;
+};
+cudaError_t launch_set_call(const CallArgs& v, CallArgs* d_call, cudaStream_t s);
+
 // ---- K1 + K2: embedding-bag sum-pool (+ dense normalisation) --------------------------------
 struct EmbedArgs {
   const TableDesc* tables;   // device array [T_local]
@@ -43,8 +60,8 @@ struct EmbedArgs {
   int64_t dense_col0;        // first dense column (T_total * d)
   int64_t pad_col0, pad_col1;  // zero columns [pad_col0, pad_col1) of x0 rows
   int* flag;                 // sticky error flag
-  bool v2;                   // warp-batched variant (batched offsets / staged index runs)
-  int variant;               // occupancy / unroll variant of the per-bag kernel (tuning)
+  const CallArgs* call;      // executor graphs: indices / keys / offsets / nnz / B (= Bd) / dense come from here
+                             // (B above then only sizes the grid: max_batch)
   int blocks_per_sm;         // grid cap (grid-stride): leaves registers for co-resident GEMM CTAs
   // fused exchange (V3): pooled rows go straight into the owner rank's canonical x0
   // through peer-mapped pointers: bag (t_local, b) -> peer_x0[b / Bl] row b % Bl, columns (t_local*world+rank)*d
@@ -77,6 +94,7 @@ struct DenseF32Args {
   const float* head_w;            // [h_n]
   const float* head_b;            // [1]
   float* scores;
+  const CallArgs* call;           // executor graphs: B and scores from the call block (B above sizes the grid)
 };
 cudaError_t launch_dense_f32(const DenseF32Args& a, cudaStream_t s);
 
@@ -113,88 +131,34 @@ struct GemmArgs {
   const float* gamma;        // EPI_SUM_LN [N]
   const float* beta;         // EPI_SUM_LN [N]
   float* partial;            // EPI_HEAD_PARTIAL [M, N / BN]
-  __nv_bfloat16* out_bf16;   // launch_gemm_splitk: C [M, ld_x] bf16 (written with plain stores)
+  __nv_bfloat16* out_bf16;   // EPI_ATTN: O [M, ld_x] bf16 (written with plain stores)
   int64_t ld_x;
   int M, N, K, BN;
   Epi epi;
   int num_sms;
   bool pdl;                  // launch with programmatic stream serialization
-  bool a_resident;           // K <= 256: keep the A block resident, contiguous tile runs per CTA
   bool cta_pair;             // 2-CTA (cta_group::2) tiles of 256 rows; B box = BN/2 rows
   bool epw1;                 // one epilogue warp per TMEM quadrant (several tiles per CTA; see Cfg::EPW)
-  bool mb8;                  // clusters of 8 consecutive row blocks multicast the B tile (tmB box {64, BN/8})
   int group_n;               // EPI_MASK grouped over branches: N tiles of group g = n / group_n read A columns
                              // [g K, (g + 1) K) and x_l columns n - g group_n (0 = off)
-  int cn;                    // 4: clusters of 4 CTAs along N multicast A (tmA box = {64, 32}); 0/1: off
   bool no_prefetch_b;        // do not issue the first ring stages' B (weight) loads before griddepcontrol.wait
+  const CallArgs* call;      // executor graphs: M = call->B * m_mult and scores = call->scores are read on the
+  int m_mult;                // device (M above then sizes the grid for max_batch; m_mult = rows per example)
   unsigned long long* dbg;   // optional per-CTA timeline [grid][8] (%globaltimer ns): entry, deps ready,
                              // first stage landed, last MMA issued, first accumulator, epilogue done, exit
 };
 
 // C[M, N] = epi(A[M, K] . B[N, K]^T).  K % 64 == 0, N % BN == 0, BN in {64, 128, 256};
-// EPI_HEAD needs BN * cn == N.  Persistent: grid = min(tiles, num_sms).
+// EPI_HEAD / EPI_SUM_LN need BN == N.  Persistent: grid = min(tiles, num_sms).
 cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s);
-
-// t = A . B^T with N = 256 as one 128 x 256 tile per row block, K split over a cluster of 4 CTAs and reduced
-// in DSMEM in a fixed order (gemm_splitk.cu).  Uses tmA (box {64, 128}), tmB (box {64, 256}), out_bf16 /
-// ld_x (row stride of t), M, K, pdl.
-cudaError_t launch_gemm_splitk(const GemmArgs& g, cudaStream_t s);
-
-// ---- config 4: fused FFN + out-projection + branch-sum LayerNorm (ens_ffn.cu) ------------------------------
-struct EnsFfnArgs {
-  const CUtensorMap* tmX;    // x_l tokens [BT, D] box {64, 128}
-  const CUtensorMap* tmO;    // MHA output O = cat[:, :D] (row stride D + F) box {64, 128}
-  const CUtensorMap* tmW1;   // W1 [F, D] box {64, 128}
-  const CUtensorMap* tmWc;   // [Wo | W2] [D, D + F] box {64, 256}
-  const CUtensorMap* tmY;    // out tokens [BT, D] box {64, 32}
-  const float *b1, *bcat, *S, *gamma, *beta;  // b1 [F], bo + b2 [D], DCN branch S fp32 [BT, D], LN affine [D]
-  int M, D, F, num_sms;
-  bool pdl;
-};
-cudaError_t launch_ens_ffn_ln(const EnsFfnArgs& a, cudaStream_t s);
 
 // ---- K7: multi-head self-attention over the 64 tokens of each example (config 4) ------------------
 // qkv [B*S, 3*D] bf16 (Q | K | V, head h at columns h*64 of each), out [B*S, D] bf16; S = 64, dh = 64.
-cudaError_t launch_mha64(const __nv_bfloat16* qkv, __nv_bfloat16* out, int out_ld, int B, int n_heads, cudaStream_t s);
+cudaError_t launch_mha64(const __nv_bfloat16* qkv, __nv_bfloat16* out, int out_ld, int B, int n_heads, cudaStream_t s,
+                         const CallArgs* call = nullptr);
 // scores[m] = sigmoid(sum_j partial[m][j] + c), j in fixed order (EPI_HEAD_PARTIAL finaliser)
-cudaError_t launch_head_finalize(const float* partial, int n_parts, float c, float* scores, int M, cudaStream_t s);
-
-// ---- K5: fused low-rank cross layer (cluster of 4 CTAs per 128-row block, r = 256) ----------------
-struct CrossFusedArgs {
-  const CUtensorMap* tmXl;   // x_l [M, W] box {64, 128}
-  const CUtensorMap* tmV;    // V   [r, W] box {64, 256}
-  const CUtensorMap* tmT;    // t   [M, r] box {64, 128}
-  const CUtensorMap* tmU;    // U   [W, r] box {64, 64}
-  const CUtensorMap* tmX0;   // x0  [M, W] box {64, 128}
-  const CUtensorMap* tmOut;  // x_{l+1} [M, W] box {64, 32}
-  const float* bias;         // b_l fp32 [W]
-  float* part;               // fp32 scratch, cross_fused_partial_bytes(max_batch)
-  __nv_bfloat16* t_out;      // t [max_batch, r] bf16
-  int M, W, R;
-  bool pdl;
-  unsigned long long* dbg;   // optional per-CTA phase timestamps (CVR_DEBUG_TIMING)
-};
-size_t cross_fused_partial_bytes(int max_batch);
-cudaError_t launch_cross_fused(const CrossFusedArgs& g, cudaStream_t s);
-
-// ---- the whole low-rank cross stack as one persistent dependency-driven kernel ------------------------
-struct CrossStackTables {        // device-resident (64-byte aligned), built at cvr_load_weights
-  CUtensorMap V[kMaxLayers];     // V_l [r, W], box {64, 64}
-  CUtensorMap U[kMaxLayers];     // U_l [W, r], box {64, 64}
-  CUtensorMap xa, xb;            // layer outputs (A operand / x_l epilogue input), box {64, 128}
-  CUtensorMap t;                 // t [max_batch, r], box {64, 128}
-};
-struct CrossStackArgs {
-  __nv_bfloat16* xa;
-  __nv_bfloat16* xb;
-  __nv_bfloat16* t;
-  const float* bias[kMaxLayers];
-  int* done;                     // [2L][ceil(M/128)] completion counters (zeroed per launch)
-  int M, W, R, L, num_sms;
-  unsigned long long* dbg;       // optional [grid][32] timestamps (CVR_DEBUG_TIMING)
-};
-cudaError_t launch_cross_stack(const CUtensorMap* tmX0, const CrossStackTables* d_tables, const CrossStackArgs& a,
-                               cudaStream_t s);
+cudaError_t launch_head_finalize(const float* partial, int n_parts, float c, float* scores, int M, cudaStream_t s,
+                                 const CallArgs* call = nullptr);
 
 // host: encode a 2-D bf16 K-major tensor map [rows, cols] (row stride ld elements) with box
 // {64, box_rows} and 128-byte swizzle.

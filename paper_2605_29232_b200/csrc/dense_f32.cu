@@ -73,6 +73,10 @@ __device__ void layer(const float* __restrict__ in, int n_in, float* __restrict_
 // so a layer costs max(staging, math) rather than their sum.
 __global__ void __launch_bounds__(256) dense_f32_kernel(const DenseF32Args a, int ld, int wmax) {
   extern __shared__ float sm[];
+  // executor graphs: this batch's rows / scores pointer from the per-call block (grid sized for max_batch)
+  const int B = a.call ? a.call->B : a.B;
+  float* const scores = a.call ? a.call->scores : a.scores;
+  if ((int)blockIdx.x * R >= B) return;
   float* x0s = sm;
   float* bufA = sm + R * ld;
   float* bufB = sm + 2 * R * ld;
@@ -86,7 +90,7 @@ __global__ void __launch_bounds__(256) dense_f32_kernel(const DenseF32Args a, in
   const int row0 = blockIdx.x * R;
   for (int i = threadIdx.x; i < R * a.W; i += blockDim.x) {
     const int r = i / a.W, c = i - r * a.W;
-    const float v = (row0 + r < a.B) ? a.x0[(int64_t)(row0 + r) * a.x0_ld + c] : 0.f;
+    const float v = (row0 + r < B) ? a.x0[(int64_t)(row0 + r) * a.x0_ld + c] : 0.f;
     x0s[r * ld + c] = v;
     bufA[r * ld + c] = v;
   }
@@ -116,7 +120,7 @@ __global__ void __launch_bounds__(256) dense_f32_kernel(const DenseF32Args a, in
     for (int k = lane; k < hn; k += 32) s = fmaf(cur[r * ld + k], __ldg(a.head_w + k), s);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0 && row0 + r < a.B) a.scores[row0 + r] = sigmoid_f32(s + __ldg(a.head_b));
+    if (lane == 0 && row0 + r < B) scores[row0 + r] = sigmoid_f32(s + __ldg(a.head_b));
   }
 }
 

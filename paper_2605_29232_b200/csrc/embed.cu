@@ -6,7 +6,7 @@
 // fp32 accumulation in index order, stored in the x0 dtype.  HBM-bound gather, no tensor
 // cores: a group of LPR = d*sizeof(row elt)/16 lanes owns one bag, each lane owns 16 bytes of
 // the row (one 128-bit ld.global.nc per row); latency is hidden by occupancy (64 warps/SM, 32
-// registers) rather than by deep per-lane unrolling (UNROLL = 1 measured fastest).  Consecutive
+// registers) rather than by deep per-lane unrolling (measured fastest).  Consecutive
 // groups take consecutive bags of the same table (table-major CSR), so Zipf-hot rows of a
 // table are re-read from L2 by neighbouring warps.
 //
@@ -89,15 +89,15 @@ __device__ __forceinline__ void store_scalar(float* p, float v) { *p = v; }
 __device__ __forceinline__ void store_scalar(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
 
 template <typename TOut>
-__device__ void dense_part(const EmbedArgs& a, int blk, int nblk) {
+__device__ void dense_part(const EmbedArgs& a, const float* dense, int Bd, int blk, int nblk) {
   const int64_t ncols = a.pad_col1 - a.dense_col0;
-  const int64_t total = (int64_t)a.Bd * ncols;
+  const int64_t total = (int64_t)Bd * ncols;
   TOut* x0 = reinterpret_cast<TOut*>(a.x0);
   for (int64_t i = (int64_t)blk * blockDim.x + threadIdx.x; i < total; i += (int64_t)nblk * blockDim.x) {
     const int64_t r = i / ncols;
     const int c = (int)(i - r * ncols);
     float v = 0.f;
-    if (c < a.F) v = __fdiv_rn(__ldg(a.dense + r * a.F + c) - __ldg(a.mean + c), __ldg(a.sigma + c));
+    if (c < a.F) v = __fdiv_rn(__ldg(dense + r * a.F + c) - __ldg(a.mean + c), __ldg(a.sigma + c));
     store_scalar(x0 + r * a.x0_ld + a.dense_col0 + c, v);
   }
 }
@@ -117,29 +117,44 @@ __device__ __forceinline__ int64_t hashed_row(uint64_t key, int64_t vocab, uint6
 }
 
 // NA: row loads that do not allocate in L1 (rows of <= 128 B, see launch_t)
-template <typename TIn, typename TOut, int LPR, int UNROLL, int MINB, bool KEYS, bool COOP = false, bool NA = false>
+template <typename TIn, typename TOut, int LPR, int MINB, bool KEYS, bool NA = false>
 __global__ void __launch_bounds__(256, MINB) embed_bag_kernel(const EmbedArgs a, int n_embed_blocks) {
+  // this batch's inputs: from the executor's per-call block (one graph serves every batch), else the launch's
+  const int32_t* indices = a.indices;
+  const uint64_t* keys = a.keys;
+  const int32_t* offsets = a.offsets;
+  const float* dense = a.dense;
+  int64_t nnz = a.nnz;
+  int B = a.B, Bd = a.Bd;
+  if (a.call) {
+    indices = a.call->indices;
+    keys = a.call->keys;
+    offsets = a.call->offsets;
+    dense = a.call->dense;
+    nnz = a.call->nnz;
+    B = Bd = a.call->B;
+  }
   if ((int)blockIdx.x >= n_embed_blocks) {
-    dense_part<TOut>(a, blockIdx.x - n_embed_blocks, gridDim.x - n_embed_blocks);
+    dense_part<TOut>(a, dense, Bd, blockIdx.x - n_embed_blocks, gridDim.x - n_embed_blocks);
     return;
   }
   constexpr int EPL = InTraits<TIn>::EPL;
   const int sub = threadIdx.x & (LPR - 1);
-  const int64_t n_bags = (int64_t)a.T * a.B;
+  const int64_t n_bags = (int64_t)a.T * B;
   const int64_t stride = (int64_t)n_embed_blocks * blockDim.x / LPR;
   for (int64_t bag = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPR; bag < n_bags; bag += stride) {
-    const int t = (int)(bag / a.B);
-    const int b = (int)(bag - (int64_t)t * a.B);
-    const int64_t start = __ldg(a.offsets + bag);
-    const int64_t end = __ldg(a.offsets + bag + 1);
+    const int t = (int)(bag / B);
+    const int b = (int)(bag - (int64_t)t * B);
+    const int64_t start = __ldg(offsets + bag);
+    const int64_t end = __ldg(offsets + bag + 1);
     const TableDesc td = a.tables[t];
     float acc[EPL];
 #pragma unroll
     for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
-    bool bad = start < 0 || end < start || end > a.nnz;
+    bool bad = start < 0 || end < start || end > nnz;
     if (!bad) {
       const uint8_t* colbase = td.base + sub * 16;
-      if constexpr (KEYS || COOP) {
+      if constexpr (KEYS) {
         // each lane of the group fetches (keys: and hashes) one element of the next LPR -- one coalesced
         // load per group -- then the row ids are broadcast in turn, two row loads in flight per lane
         const unsigned gmask = (LPR == 32) ? 0xffffffffu : (((1u << LPR) - 1) << (threadIdx.x & 31 & ~(LPR - 1)));
@@ -147,8 +162,7 @@ __global__ void __launch_bounds__(256, MINB) embed_bag_kernel(const EmbedArgs a,
           const int64_t jj = j0 + sub;
           int64_t my = 0;
           if (jj < end) {
-            if constexpr (KEYS) my = hashed_row(__ldg(a.keys + jj), td.vocab, td.magic);
-            else my = (int64_t)__ldg(a.indices + jj);
+            my = hashed_row(__ldg(keys + jj), td.vocab, td.magic);
           }
           bad |= jj < end && (my < 0 || my >= td.rows);
           bad = __any_sync(gmask, bad);
@@ -167,25 +181,14 @@ __global__ void __launch_bounds__(256, MINB) embed_bag_kernel(const EmbedArgs a,
           }
         }
       } else
-      for (int64_t j = start; j < end; j += UNROLL) {
-        int64_t idx[UNROLL];
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-          const bool live = j + u < end;
-          idx[u] = live ? (int64_t)__ldg(a.indices + j + u) : 0;
-          bad |= live && (idx[u] < 0 || idx[u] >= td.rows);
-        }
-        if (bad) break;  // uniform within the group: every lane read the same indices
-        uint4 v[UNROLL];
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u)
-          if (j + u < end) {
-            if constexpr (NA) v[u] = ptx::ld_nc_na_v4(colbase + idx[u] * td.stride);
-            else v[u] = ptx::ld_nc_v4(colbase + idx[u] * td.stride);
-          }
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u)
-          if (j + u < end) InTraits<TIn>::add(acc, v[u]);
+      for (int64_t j = start; j < end; ++j) {  // one row load in flight per lane (occupancy hides latency)
+        const int64_t idx = (int64_t)__ldg(indices + j);
+        bad |= idx < 0 || idx >= td.rows;
+        if (bad) break;  // uniform within the group: every lane read the same index
+        uint4 v;
+        if constexpr (NA) v = ptx::ld_nc_na_v4(colbase + idx * td.stride);
+        else v = ptx::ld_nc_v4(colbase + idx * td.stride);
+        InTraits<TIn>::add(acc, v);
       }
     }
     if (bad) {
@@ -209,131 +212,13 @@ __global__ void __launch_bounds__(256, MINB) embed_bag_kernel(const EmbedArgs a,
   }
 }
 
-// v2: warp-batched bags.  A warp owns BPW = NS * (32/LPR) consecutive bags (table-major, so they are
-// contiguous in offsets[] and their indices are one contiguous run of indices[]).  The warp loads the
-// BPW+1 offsets with ONE coalesced load, stages the whole index run in shared memory with coalesced
-// loads, then each lane group walks its bags' rows (UNROLL 16-byte loads in flight per lane).  The
-// dependent offset -> index -> row chain is paid once per BPW bags instead of once per bag.
-template <int LPR>
-struct V2Shape {
-  static constexpr int G = 32 / LPR;                                   // lane groups (bags) per pass
-  static constexpr int NS = (G >= 16) ? 1 : (G >= 8 ? 3 : (G >= 4 ? 4 : (G >= 2 ? 8 : 16)));
-  static constexpr int BPW = NS * G;                                   // bags per warp, <= 31
-  static constexpr int IDX_CAP = 512;                                  // staged indices per warp
-};
-
-template <typename TIn, typename TOut, int LPR, int UNROLL>
-__global__ void __launch_bounds__(256) embed_bag_v2_kernel(const EmbedArgs a, int n_embed_blocks) {
-  using Sh = V2Shape<LPR>;
-  constexpr int EPL = InTraits<TIn>::EPL;
-  __shared__ int sidx[8][Sh::IDX_CAP];
-  if ((int)blockIdx.x >= n_embed_blocks) {
-    dense_part<TOut>(a, blockIdx.x - n_embed_blocks, gridDim.x - n_embed_blocks);
-    return;
-  }
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int grp = lane / LPR, sub = lane & (LPR - 1);
-  const int64_t n_bags = (int64_t)a.T * a.B;
-  const int64_t total_warps = (int64_t)n_embed_blocks * (blockDim.x >> 5);
-  int* my_idx = sidx[wib];
-  for (int64_t bag0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wib) * Sh::BPW; bag0 < n_bags;
-       bag0 += total_warps * Sh::BPW) {
-    const int nb = (int)(n_bags - bag0 < Sh::BPW ? n_bags - bag0 : Sh::BPW);
-    const int64_t off_l = lane <= nb ? (int64_t)__ldg(a.offsets + bag0 + lane) : 0;
-    const int64_t base = __shfl_sync(0xffffffffu, off_l, 0);
-    const int64_t endall = __shfl_sync(0xffffffffu, off_l, nb);
-    // a bag is bad if its offsets decrease or leave [0, nnz]
-    const int64_t off_n = __shfl_down_sync(0xffffffffu, off_l, 1);
-    const bool bag_bad = lane < nb && (off_l < 0 || off_n < off_l || off_n > a.nnz);
-    const unsigned bad_mask = __ballot_sync(0xffffffffu, bag_bad);
-    const int64_t run = endall - base;
-    const bool staged = bad_mask == 0 && run >= 0 && run <= Sh::IDX_CAP;
-    if (staged) {
-      for (int k = lane; k < run; k += 32) my_idx[k] = __ldg(a.indices + base + k);
-    }
-    __syncwarp();
-    // two bags per lane group at a time: up to 2 x UNROLL independent 16-byte row loads in flight per lane
-#pragma unroll 1
-    for (int sl = 0; sl < Sh::NS; sl += 2) {
-      int64_t st[2], en[2];
-      int tt[2], bb[2];
-      bool bad[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int bl = (sl + h) * Sh::G + grp;
-        st[h] = __shfl_sync(0xffffffffu, off_l, min(bl, 31));
-        en[h] = __shfl_sync(0xffffffffu, off_l, min(bl + 1, 31));
-        const bool live = sl + h < Sh::NS && bl < nb;
-        if (!live) en[h] = st[h];
-        const int64_t bag = bag0 + (live ? bl : 0);
-        tt[h] = (int)(bag / a.B);
-        bb[h] = (int)(bag - (int64_t)tt[h] * a.B);
-        bad[h] = live && ((bad_mask >> bl) & 1u);
-        if (bad[h]) en[h] = st[h];
-      }
-      const TableDesc d0 = a.tables[tt[0]], d1 = a.tables[tt[1]];
-      float acc0[EPL], acc1[EPL];
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) acc0[e] = acc1[e] = 0.f;
-      const uint8_t* cb0 = d0.base + sub * 16;
-      const uint8_t* cb1 = d1.base + sub * 16;
-      int64_t j0 = st[0], j1 = st[1];
-      while (j0 < en[0] || j1 < en[1]) {
-        int i0[UNROLL], i1[UNROLL];
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-          const bool l0 = j0 + u < en[0], l1 = j1 + u < en[1];
-          i0[u] = l0 ? (staged ? my_idx[j0 + u - base] : __ldg(a.indices + j0 + u)) : 0;
-          i1[u] = l1 ? (staged ? my_idx[j1 + u - base] : __ldg(a.indices + j1 + u)) : 0;
-          bad[0] |= l0 && (i0[u] < 0 || (int64_t)i0[u] >= d0.rows);
-          bad[1] |= l1 && (i1[u] < 0 || (int64_t)i1[u] >= d1.rows);
-        }
-        if (bad[0]) en[0] = j0;  // stop this bag; it is zeroed below
-        if (bad[1]) en[1] = j1;
-        uint4 v0[UNROLL], v1[UNROLL];
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-          if (j0 + u < en[0]) v0[u] = ptx::ld_nc_v4(cb0 + (int64_t)i0[u] * d0.stride);
-          if (j1 + u < en[1]) v1[u] = ptx::ld_nc_v4(cb1 + (int64_t)i1[u] * d1.stride);
-        }
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-          if (j0 + u < en[0]) InTraits<TIn>::add(acc0, v0[u]);
-          if (j1 + u < en[1]) InTraits<TIn>::add(acc1, v1[u]);
-        }
-        j0 += UNROLL;
-        j1 += UNROLL;
-      }
-      const int bl0 = sl * Sh::G + grp, bl1 = (sl + 1) * Sh::G + grp;
-      if (bl0 < nb) {
-        if (bad[0]) {
-#pragma unroll
-          for (int e = 0; e < EPL; ++e) acc0[e] = 0.f;
-          if (sub == 0) atomicOr(a.flag, 1);
-        }
-        store_out<EPL>(reinterpret_cast<TOut*>(a.out) + (int64_t)bb[0] * a.out_ld + (int64_t)tt[0] * a.out_tstride + sub * EPL,
-                       acc0);
-      }
-      if (sl + 1 < Sh::NS && bl1 < nb) {
-        if (bad[1]) {
-#pragma unroll
-          for (int e = 0; e < EPL; ++e) acc1[e] = 0.f;
-          if (sub == 0) atomicOr(a.flag, 1);
-        }
-        store_out<EPL>(reinterpret_cast<TOut*>(a.out) + (int64_t)bb[1] * a.out_ld + (int64_t)tt[1] * a.out_tstride + sub * EPL,
-                       acc1);
-      }
-    }
-    __syncwarp();
-  }
-}
-
 template <typename TIn, typename TOut, int LPR>
 cudaError_t launch_t(const EmbedArgs& a, int num_sms, cudaStream_t s) {
   const int threads = 256;
+  // (executor graphs: a.B = a.Bd = max_batch here; the kernel reads the batch's B from a.call)
   const int64_t n_bags = (int64_t)a.T * a.B;
-  // one bag per lane group, no grid-stride loop: short-lived CTAs let the block scheduler interleave
-  // the concurrently running dense-stage GEMM CTAs (higher-priority stream) as embed CTAs retire
+  // one bag per lane group, no grid-stride loop at full size: short-lived CTAs let the block scheduler
+  // interleave the concurrently running dense-stage GEMM CTAs (higher-priority stream) as embed CTAs retire
   int64_t nbE = (n_bags * LPR + threads - 1) / threads;
   const int64_t capE = (int64_t)num_sms * (a.blocks_per_sm > 0 ? a.blocks_per_sm : 64);
   if (nbE > capE) nbE = capE;
@@ -343,29 +228,18 @@ cudaError_t launch_t(const EmbedArgs& a, int num_sms, cudaStream_t s) {
     nbD = (total + threads - 1) / threads;
     if (nbD > num_sms) nbD = num_sms;
   }
-  if (a.v2 && !a.keys) {
-    const int64_t warps = (n_bags + V2Shape<LPR>::BPW - 1) / V2Shape<LPR>::BPW;
-    nbE = (warps + 7) / 8;
-    if (nbE > capE) nbE = capE;
-  }
   if (nbE + nbD == 0) return cudaSuccess;
-  // measured on B200, config 2 (scripts/embed_ab.py): one row load in flight per lane at full occupancy
-  // (32 registers, 64 warps/SM) beats deeper per-lane unrolling at lower occupancy: 18.5 us (59% of the
-  // HBM peak, algorithmic bytes) vs 24.6 us for 4 rows in flight at 32 warps/SM.
-  if (a.peer_x0 && (a.keys || a.v2)) return cudaErrorInvalidValue;  // V3 uses the row-id per-bag kernel
+  if (a.peer_x0 && a.keys) return cudaErrorInvalidValue;  // V3 uses the row-id kernel
   if (a.keys)
-    embed_bag_kernel<TIn, TOut, LPR, 1, 8, true><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
-  else if (a.v2)
-    embed_bag_v2_kernel<TIn, TOut, LPR, 4><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
-  else if (a.variant == 2)  // cooperative index fetch + broadcast (option embed_variant = 2)
-    embed_bag_kernel<TIn, TOut, LPR, 1, 8, false, true><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
-  else if (LPR <= 8 && a.variant != 3)
-    // rows of <= 128 B (one line each): row loads skip L1 allocation.  Measured on B200 (scripts/embed_ab.py):
-    // c2 (128-B bf16 rows) 20.3 -> 18.5 us; wider rows keep L1 allocation (c3-S 256-B rows 1.83 -> 2.00 ms,
-    // c4 512-B rows 187 -> 203 us without it); option embed_variant = 3 forces allocating loads
-    embed_bag_kernel<TIn, TOut, LPR, 1, 8, false, false, true><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
+    embed_bag_kernel<TIn, TOut, LPR, 8, true><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
+  else if (LPR <= 8)
+    // rows of <= 128 B (one line each): row loads skip L1 allocation.  Measured on B200 (round 1): c2 (128-B bf16
+    // rows) 20.3 -> 18.5 us; wider rows keep L1 allocation (c3-S 256-B rows 1.83 vs 2.00 ms, c4 512-B rows 187 vs
+    // 203 us without it).  One row load in flight per lane at full occupancy (32 registers, 64 warps/SM) beat
+    // deeper per-lane unrolling at lower occupancy (18.5 vs 24.6 us for 4 rows in flight at 32 warps/SM).
+    embed_bag_kernel<TIn, TOut, LPR, 8, false, true><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
   else
-    embed_bag_kernel<TIn, TOut, LPR, 1, 8, false><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
+    embed_bag_kernel<TIn, TOut, LPR, 8, false><<<(unsigned)(nbE + nbD), threads, 0, s>>>(a, (int)nbE);
   return cudaGetLastError();
 }
 
@@ -399,6 +273,10 @@ __global__ void unpack_kernel(const uint4* __restrict__ recv, uint8_t* __restric
   }
 }
 
+__global__ void set_call_kernel(const CallArgs v, CallArgs* dst) {
+  if (threadIdx.x == 0) *dst = v;
+}
+
 __global__ void peer_signal_kernel(uint32_t* const* __restrict__ peer_flags, int world, int rank, uint32_t epoch) {
   // the gather kernel before us on this stream has completed; make its peer stores visible system-wide
   // before publishing the epoch
@@ -421,6 +299,11 @@ __global__ void peer_wait_kernel(const uint32_t* __restrict__ flags, int world, 
 }
 
 }  // namespace
+
+cudaError_t launch_set_call(const CallArgs& v, CallArgs* d_call, cudaStream_t s) {
+  set_call_kernel<<<1, 32, 0, s>>>(v, d_call);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_peer_signal(uint32_t* const* d_peer_flags, int world, int rank, uint32_t epoch, cudaStream_t s) {
   peer_signal_kernel<<<1, 32, 0, s>>>(d_peer_flags, world, rank, epoch);

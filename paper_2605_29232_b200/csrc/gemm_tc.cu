@@ -56,12 +56,11 @@ struct EpiTraits {
 template <int BN, int EPI, int CG>
 constexpr bool ein_ring() { return EPI == EPI_CROSS && BN == 192; }
 
-template <int BN, int EPI, bool AR = false, int CG = 1, int CN = 1, int EW = 4, bool MB = false>
+template <int BN, int EPI, int CG = 1, int EW = 4>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;       // 16 KB
   static constexpr int B_BYTES = (BN / CG) * BK * 2;  // CG = 2: each CTA of the pair holds half of B
-  static constexpr int AR_BYTES = AR ? 4 * A_BYTES : 0;   // resident A block (K <= 256)
-  static constexpr int STAGE = (AR ? 0 : A_BYTES) + B_BYTES;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int SUB = BM * 64 * 2;           // one 128 x 64 bf16 sub-tile (16 KB)
   static constexpr int NSUB = BN / 64;
   static constexpr int OUT_BUFS = BN >= 192 ? 1 : 2;
@@ -71,7 +70,7 @@ struct Cfg {
   // epilogue warps per TMEM lane quadrant: the epilogue of a CTA's last tile is exposed (one tile per CTA at
   // B = 4096), so plain stores split the tile's 64-column sub-tiles over up to 4 warps per quadrant
   // (EPI_HEAD too: each warp's partial dot product over its 64-column sub-tiles, summed in column order)
-  static constexpr bool SPLIT = (EPI == EPI_STORE || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS || EPI == EPI_HEAD) && CN == 1;
+  static constexpr bool SPLIT = EPI == EPI_STORE || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS || EPI == EPI_HEAD;
   // EW caps the split: EW = 1 when each CTA runs several tiles (the epilogue then overlaps the next tile's
   // mainloop anyway) keeps the CTA at 7 warps, leaving registers for co-resident embedding CTAs
   // EPI_ATTN: 8 epilogue warps = 2 examples x 4 groups of 16 query rows (one attention warp each)
@@ -100,9 +99,9 @@ struct Cfg {
   static constexpr int EPI_BYTES =
       OUT_BUFS * OUT_BYTES + 2 * EIN_BYTES + (RING ? RING_SLOTS * 2 * SUB : 0) + ATT_BYTES + F32_BYTES;
   static constexpr int BAR_BYTES = 512;
-  // EPI_HEAD across a CN-cluster: per-tile partial dot products gathered in rank 0 ([2][CN][BM] fp32)
-  static constexpr int Z_BYTES = (EPI == EPI_HEAD && CN > 1) ? 2 * CN * BM * 4 : (EPI == EPI_HEAD ? EPW * BM * 4 : 0);
-  static constexpr int STAGES_FIT = (kSmemBudget - 1024 - BAR_BYTES - EPI_BYTES - AR_BYTES - Z_BYTES) / STAGE;
+  // EPI_HEAD with a split epilogue: the EPW warps' partial dot products per row ([EPW][BM] fp32)
+  static constexpr int Z_BYTES = EPI == EPI_HEAD ? EPW * BM * 4 : 0;
+  static constexpr int STAGES_FIT = (kSmemBudget - 1024 - BAR_BYTES - EPI_BYTES - Z_BYTES) / STAGE;
 #ifndef CVR_MAX_STAGES
 #define CVR_MAX_STAGES 8
 #endif
@@ -110,31 +109,20 @@ struct Cfg {
   // RING: a CTA's last tile (when it is not also its first) takes its epilogue inputs into the operand ring
   // instead of the slots -- the ring is free once that tile's MMAs have completed, long before the previous
   // tile's epilogue hands the slots back (sub-tile j: x0 in A stage j, x_l in B stage j)
-  static constexpr bool RING_ALT = RING && !AR && NSUB <= STAGES && A_BYTES >= SUB && B_BYTES >= SUB;
+  static constexpr bool RING_ALT = RING && NSUB <= STAGES && A_BYTES >= SUB && B_BYTES >= SUB;
   static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);  // 2 accumulators, pow2 alloc
-  static constexpr int SMEM = 1024 + AR_BYTES + STAGES * STAGE + EPI_BYTES + Z_BYTES + BAR_BYTES;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + EPI_BYTES + Z_BYTES + BAR_BYTES;
   static_assert(STAGES >= 2, "shared memory budget");
 };
 
 using namespace tile;
 
-// AR (A resident, K <= 256): each CTA walks a contiguous run of tiles in m-major order and loads the
-// 128 x K A block once per m-block into a resident buffer; the ring only streams B tiles.  This cuts the
-// N/BN-fold re-read of A of a small-K, wide-N GEMM (the U GEMM of a cross layer).
 // CG = 2 (CTA pair, cluster of 2): a 256 x BN tile per pair with tcgen05.mma.cta_group::2 issued by the
 // leader; each CTA loads its own 128 A rows and HALF of the B tile (BN/2 rows), so the bytes each SM must
 // ingest per FLOP drop by (128 + BN/2)/(128 + BN); both CTAs' TMA bytes complete on the leader's full
 // barrier, MMA completion is multicast to both CTAs, and each CTA runs the epilogue of its own 128 rows.
-// CN > 1 (cluster of CN CTAs along N, cta_group::1): the CN CTAs of a cluster work on the CN adjacent N
-// tiles of the same 128-row block in lock step; each loads a BM/CN-row slice of every A k-block and
-// multicasts it to all CN CTAs (tmA then has box {64, BM/CN}), so the L2 serves each A byte once per
-// cluster instead of CN times.  A stage is refilled only after all CN CTAs' MMAs have read it (empty
-// barriers count CN multicast commits).  EPI_HEAD then spans CN tiles: the partial dot products of the
-// CN tiles are gathered in rank 0's shared memory over DSMEM and summed in rank order (fixed order,
-// independent of M: batch invariance).
-// MB (with CN > 1): the cluster runs along M instead -- CN consecutive 128-row blocks of the same N tile --
-// and it is the B k-block that is sliced (BN/CN rows per CTA, tmB box {64, BN/CN}) and multicast: every CTA
-// issues 1/CN of the weight bytes and the L2 serves each weight line once per cluster.
+// Executor graphs (g.call): the row count M and the scores pointer are read from the per-call argument block in
+// device memory; the grid is sized for max_batch and CTAs whose tiles lie beyond M find no work.
 __device__ __forceinline__ void stamp(unsigned long long* dbg, int i) {
   if (dbg) {
     unsigned long long t;
@@ -143,26 +131,21 @@ __device__ __forceinline__ void stamp(unsigned long long* dbg, int i) {
   }
 }
 
-template <int BN, int EPI, bool AR, int CG, int CN, int EW, bool MB>
-__global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
+template <int BN, int EPI, int CG, int EW>
+__global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmX0,
                      const __grid_constant__ CUtensorMap tmXl, const GemmArgs g) {
-  using C = Cfg<BN, EPI, AR, CG, CN, EW, MB>;
+  using C = Cfg<BN, EPI, CG, EW>;
   using T = EpiTraits<EPI>;
-  static_assert(CG == 1 || !AR, "the resident-A walk is single-CTA");
-  static_assert(!MB || (CN > 1 && BN % (8 * CN) == 0 && EPI != EPI_HEAD), "B slices are whole 8-row swizzle atoms");
-  static_assert(CN == 1 || (CG == 1 && !AR), "A multicast is cta_group::1 streaming only");
-  static_assert(MB || BM % (8 * CN) == 0, "A slices are whole 8-row swizzle atoms");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sAR = smem;                                  // resident A (AR only)
-  uint8_t* sA = smem + C::AR_BYTES;
-  uint8_t* sB = sA + (AR ? 0 : C::STAGES * C::A_BYTES);
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + C::STAGES * C::A_BYTES;
   uint8_t* sOut = sB + C::STAGES * C::B_BYTES;         // [OUT_BUFS][NSUB][SUB]
   uint8_t* sEin = sOut + C::OUT_BUFS * C::OUT_BYTES;   // [2][x0 NSUB subs | x_l NSUB subs]
   // (ring slots / staging live in [sOut, sOut + EPI_BYTES); the head partials and the barriers follow them)
-  float* zbuf = reinterpret_cast<float*>(sOut + C::EPI_BYTES);  // EPI_HEAD: [2][CN][BM] (CN > 1) / [EPW][BM]
+  float* zbuf = reinterpret_cast<float*>(sOut + C::EPI_BYTES);  // EPI_HEAD: [EPW][BM]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + C::EPI_BYTES + C::Z_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = full + C::STAGES;
@@ -170,39 +153,31 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
   uint64_t* tempty = tfull + 2;          // [2] accumulator drained (4 epilogue warps)
   uint64_t* efull = tempty + 2;          // [3] epilogue input tiles (ring slots) landed
   uint64_t* eempty = efull + 3;          // [3] epilogue input tiles consumed (4 warps)
-  uint64_t* afull = eempty + 3;          // resident A landed (AR)
-  uint64_t* aempty = afull + 1;          // resident A no longer read by MMAs (AR)
-  uint64_t* zfull = aempty + 1;          // [2] rank 0: all CN x 4 epilogue warps stored their partials
-  uint64_t* zempty = zfull + 2;          // [2] rank 0's 4 epilogue warps have read buffer a
-  uint64_t* sfull = zempty + 2;          // [4 warps][SLN_BUFS] EPI_SUM_LN fp32 input chunk landed
+  uint64_t* sfull = eempty + 3;          // [4 warps][SLN_BUFS] EPI_SUM_LN fp32 input chunk landed
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sfull + 4 * 3);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int M = g.M, N = g.N, K = g.K;
+  // executor graphs: this batch's row count (and scores pointer) from the per-call block, else the launch's
+  const int M = g.call ? g.call->B * g.m_mult : g.M;
+  const int N = g.N, K = g.K;
   constexpr int BMT = BM * CG;  // rows per tile (per CTA pair when CG = 2)
   const int rank = CG == 2 ? (int)ptx::cluster_ctarank() : 0;
-  const int crank = CN > 1 ? (int)ptx::cluster_ctarank() : 0;   // N position inside the cluster
-  constexpr uint16_t kMask = (uint16_t)((1u << CN) - 1);
   const bool leader = rank == 0;
-  const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x / CN;
-  const int n_units = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x / CN;
+  const int unit = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int n_units = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int n_tiles_n = N / BN;
-  // tiles of a cluster: (m-block, group of CN adjacent N tiles), or with MB (group of CN m-blocks, N tile)
-  const int n_groups = MB ? n_tiles_n : n_tiles_n / CN;
-  const int m_units = MB ? ((M + BMT - 1) / BMT + CN - 1) / CN : (M + BMT - 1) / BMT;
-  const int n_tiles = m_units * n_groups;
-  auto tile_m = [&](int tile) { return MB ? (tile / n_groups) * CN + crank : tile / n_groups; };
-  auto tile_n = [&](int tile) { return MB ? tile % n_groups : (tile % n_groups) * CN + crank; };
+  const int n_tiles = (M + BMT - 1) / BMT * n_tiles_n;
+  auto tile_m = [&](int tile) { return tile / n_tiles_n; };
+  auto tile_n = [&](int tile) { return tile % n_tiles_n; };
+  float* const scores = g.call ? g.call->scores : g.scores;
   const int nk = K / BK;
-  // tile walk: strided over the grid, or (AR) a contiguous balanced run per CTA
-  const int t_begin = AR ? (int)((int64_t)n_tiles * unit / n_units) : unit;
-  const int t_end = AR ? (int)((int64_t)n_tiles * (unit + 1) / n_units) : n_tiles;
-  const int t_step = AR ? 1 : n_units;
+  // tile walk: strided over the grid (n-fastest, so CTAs running together share the A row block in L2)
+  const int t_begin = unit, t_end = n_tiles, t_step = n_units;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      ptx::mbar_init(&full[s], AR ? 1 : 2);  // one expect_tx arrival per producer stream
-      ptx::mbar_init(&empty[s], CN);
+      ptx::mbar_init(&full[s], 2);  // one expect_tx arrival per producer stream
+      ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
@@ -212,12 +187,6 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
     for (int e = 0; e < 3; ++e) {
       ptx::mbar_init(&efull[e], 1);
       ptx::mbar_init(&eempty[e], 4);
-    }
-    ptx::mbar_init(afull, 1);
-    ptx::mbar_init(aempty, 1);
-    for (int a = 0; a < 2; ++a) {
-      ptx::mbar_init(&zfull[a], 4 * CN);
-      ptx::mbar_init(&zempty[a], 4);
     }
     for (int i = 0; i < 4 * 3; ++i) ptx::mbar_init(&sfull[i], 1);
     ptx::fence_barrier_init();
@@ -236,7 +205,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
     else ptx::tmem_alloc(tmem_holder, C::TMEM_COLS);
   }
   ptx::tc_fence_before();
-  if constexpr (CG == 2 || CN > 1) ptx::cluster_sync();  // peers' barriers exist before any remote arrive
+  if constexpr (CG == 2) ptx::cluster_sync();  // peers' barriers exist before any remote arrive
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
@@ -248,17 +217,13 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
       ptx::tma_load_2d_cg2(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0 + rank * (BN / 2));
     } else {
       ptx::mbar_arrive_expect_tx(&full[s], C::B_BYTES);
-      if constexpr (MB)
-        ptx::tma_load_2d_mc(sB + s * C::B_BYTES + crank * (BN / CN) * 128, &tmB, &full[s], kb * BK,
-                            n0 + crank * (BN / CN), kMask);
-      else
-        ptx::tma_load_2d(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);
+      ptx::tma_load_2d(sB + s * C::B_BYTES, &tmB, &full[s], kb * BK, n0);
     }
   };
   // Weight prefetch: the first ring stages' B k-blocks are issued BEFORE griddepcontrol.wait, i.e. while the
   // previous kernel is still draining; only A (and the epilogue inputs) wait for it
   int npre = 0;
-  if (!g.no_prefetch_b && !MB && warp == C::PRODUCER_B && lane == 0 && t_begin < t_end) {
+  if (!g.no_prefetch_b && warp == C::PRODUCER_B && lane == 0 && t_begin < t_end) {
     npre = nk < C::STAGES ? nk : C::STAGES;
     for (int kb = 0; kb < npre; ++kb) issue_b(kb, kb, tile_n(t_begin) * BN);
   }
@@ -278,23 +243,12 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
       const bool roleA = warp == 0;
       int gk = 0;     // global k-block counter (ring position)
       int it = 0;
-      int cur_m = -1, a_loads = 0;
       for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
         const int m0 = tile_m(tile) * BMT + rank * BM, n0 = tile_n(tile) * BN;
         // grouped GEMM (EPI_MASK over several MaskNet branches): N group g = n0 / group_n reads the K range
         // [g * K, (g + 1) * K) of A and the epilogue input at column n0 - g * group_n
         const int grp = (EPI == EPI_MASK && g.group_n > 0) ? n0 / g.group_n : 0;
         const int a_k0 = grp * K, e_n0 = n0 - grp * (EPI == EPI_MASK ? g.group_n : 0);
-        if constexpr (AR) {
-          if (roleA && m0 != cur_m) {
-            if (a_loads > 0) ptx::mbar_wait(aempty, (a_loads - 1) & 1);
-            ptx::mbar_arrive_expect_tx(afull, nk * C::A_BYTES);
-            for (int kb = 0; kb < nk; ++kb) ptx::tma_load_2d(sAR + kb * C::A_BYTES, &tmA, afull, kb * BK, m0);
-            cur_m = m0;
-            ++a_loads;
-          }
-          if (roleA) continue;  // the ring carries only B
-        }
         if constexpr (T::kEin && !C::RING) {
           if (!roleA) {
             const int a = it & 1;
@@ -322,11 +276,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
             ptx::tma_load_2d_cg2(sA + s * C::A_BYTES, &tmA, &full[s], kb * BK, m0);
           } else {
             ptx::mbar_arrive_expect_tx(&full[s], C::A_BYTES);
-            if constexpr (CN > 1 && !MB)
-              ptx::tma_load_2d_mc(sA + s * C::A_BYTES + crank * (BM / CN) * 128, &tmA, &full[s], kb * BK,
-                                  m0 + crank * (BM / CN), kMask);
-            else
-              ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], a_k0 + kb * BK, m0);
+            ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], a_k0 + kb * BK, m0);
           }
         }
       }
@@ -358,17 +308,8 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
     if (lane == 0 && leader) {  // ================= MMA issuer (the pair's leader when CG = 2)
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(BMT, BN);
       int gk = 0, it = 0;
-      int cur_m = -1, a_loads = 0;
       for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
         const int a = it & 1;
-        const int m0 = tile_m(tile) * BM;
-        if constexpr (AR) {
-          if (m0 != cur_m) {
-            ptx::mbar_wait(afull, a_loads & 1);
-            cur_m = m0;
-            ++a_loads;
-          }
-        }
         if (it >= 2) ptx::mbar_wait(&tempty[a], ((it >> 1) - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t acc = tmem + a * BN;
@@ -377,8 +318,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
           ptx::mbar_wait(&full[s], (gk / C::STAGES) & 1);
           if (gk == 0) stamp(g.dbg, 2);
           ptx::tc_fence_after();
-          const uint64_t ad = ptx::sdesc_kmajor_sw128(
-              ptx::smem_u32(AR ? sAR + kb * C::A_BYTES : sA + s * C::A_BYTES));
+          const uint64_t ad = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sA + s * C::A_BYTES));
           const uint64_t bd = ptx::sdesc_kmajor_sw128(ptx::smem_u32(sB + s * C::B_BYTES));
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {  // K step 16 = 32 bytes = +2 in the 16-byte address field
@@ -387,16 +327,11 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
           }
           // frees the smem stage (in both CTAs of a pair) once these MMAs have read it
           if constexpr (CG == 2) ptx::umma_commit_cg2_mc(&empty[s]);
-          else if constexpr (CN > 1) ptx::umma_commit_mc(&empty[s], kMask);  // frees it in every CTA
           else ptx::umma_commit(&empty[s]);
         }
         if constexpr (CG == 2) ptx::umma_commit_cg2_mc(&tfull[a]);  // accumulator a complete
         else ptx::umma_commit(&tfull[a]);
         stamp(g.dbg, 3);
-        if constexpr (AR) {             // last tile of this m-block: the resident A may be replaced
-          const int nt = tile + t_step;
-          if (nt >= t_end || tile_m(nt) * BM != m0) ptx::umma_commit(aempty);
-        }
       }
     }
   } else if (warp < C::PRODUCER_B) {  // ===== epilogue warps: TMEM quadrant q = warp % 4 -> rows 32q..32q+31
@@ -681,23 +616,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
           if constexpr (T::kEin) ptx::mbar_arrive(&eempty[a]);
         }
       }
-      if constexpr (EPI == EPI_HEAD && CN > 1) {
-        // gather the CN partial dot products of this row block in rank 0, sum them in rank order
-        if (it >= 2) ptx::mbar_wait_cluster(&zempty[a], ((it >> 1) - 1) & 1);
-        ptx::st_cluster_f32(ptx::mapa(zbuf + (a * CN + crank) * BM + r, 0), z);
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_remote(ptx::mapa(&zfull[a], 0));
-        if (crank == 0) {
-          ptx::mbar_wait_cluster(&zfull[a], (it >> 1) & 1);
-          float zs = 0.f;
-#pragma unroll
-          for (int j = 0; j < CN; ++j) zs += zbuf[(a * CN + j) * BM + r];
-          if (live) g.scores[m] = sigmoid_f32(zs + g.head_b);
-          __syncwarp();
-          if (lane == 0)
-            for (int j = 0; j < CN; ++j) ptx::mbar_arrive_remote(ptx::mapa(&zempty[a], j));
-        }
-      } else if constexpr (EPI == EPI_HEAD && C::EPW > 1) {
+      if constexpr (EPI == EPI_HEAD && C::EPW > 1) {
         // split epilogue: the quadrant's EPW warps hand their partial dot products to part 0, which sums them in
         // column order from 0 (as the cluster head sums its CTAs' partials in rank order: same result)
         zbuf[part * BM + r] = z;
@@ -706,11 +625,11 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
           float zs = 0.f;
 #pragma unroll
           for (int j = 0; j < C::EPW; ++j) zs += zbuf[j * BM + r];
-          if (live) g.scores[m] = sigmoid_f32(zs + g.head_b);
+          if (live) scores[m] = sigmoid_f32(zs + g.head_b);
         }
         ptx::named_bar_sync(1 + q, 32 * C::EPW);  // zbuf free for the next tile
       } else if constexpr (EPI == EPI_HEAD) {
-        if (live) g.scores[m] = sigmoid_f32(z + g.head_b);
+        if (live) scores[m] = sigmoid_f32(z + g.head_b);
       } else if constexpr (EPI == EPI_HEAD_PARTIAL) {
         if (live) g.partial[(int64_t)m * n_tiles_n + tn] = z;
       } else if constexpr (T::kSmemOut && !C::RING) {
@@ -732,8 +651,8 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
     if (warp == 2 && lane == 0) stamp(g.dbg, 5);
   }
   ptx::tc_fence_before();
-  // CG = 2: both CTAs are done with the pair's TMEM; CN > 1: no peer still multicasts into / arrives on us
-  if constexpr (CG == 2 || CN > 1) ptx::cluster_sync();
+  // CG = 2: both CTAs are done with the pair's TMEM
+  if constexpr (CG == 2) ptx::cluster_sync();
   else __syncthreads();
   if (threadIdx.x == 0) stamp(g.dbg, 6);
   if (warp == 1) {
@@ -742,20 +661,21 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, AR, CG, CN, EW, MB>::NT, 1)
   }
 }
 
-template <int BN, int EPI, bool AR = false, int CG = 1, int CN = 1, int EW = 4, bool MB = false>
+template <int BN, int EPI, int CG = 1, int EW = 4>
 cudaError_t launch_t(const GemmArgs& g, cudaStream_t s) {
-  using C = Cfg<BN, EPI, AR, CG, CN, EW, MB>;
-  auto kern = gemm_bf16_kernel<BN, EPI, AR, CG, CN, EW, MB>;
+  using C = Cfg<BN, EPI, CG, EW>;
+  auto kern = gemm_bf16_kernel<BN, EPI, CG, EW>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
+  // (executor graphs: g.M is max_batch * m_mult here, the kernel reads the batch's M from g.call)
   const int m_blocks = (g.M + BM * CG - 1) / (BM * CG);
-  const int n_tiles = MB ? (m_blocks + CN - 1) / CN * (g.N / BN) : m_blocks * (g.N / BN / CN);
-  const int max_units = g.num_sms / (CG * CN);
-  const int grid = (n_tiles < max_units ? n_tiles : max_units) * CG * CN;
+  const int n_tiles = m_blocks * (g.N / BN);
+  const int max_units = g.num_sms / CG;
+  const int grid = (n_tiles < max_units ? n_tiles : max_units) * CG;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(C::NT);
@@ -765,11 +685,11 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = g.pdl ? 1 : 0;
   attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = CG * CN;
+  attr[1].val.clusterDim.x = CG;
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = CG * CN > 1 ? 2 : 1;
+  cfg.numAttrs = CG > 1 ? 2 : 1;
   const CUtensorMap* dummy = g.tmA;
   return cudaLaunchKernelEx(&cfg, kern, *g.tmA, *g.tmB, *(g.tmOut ? g.tmOut : dummy), *(g.tmX0 ? g.tmX0 : dummy),
                             *(g.tmXl ? g.tmXl : dummy), g);
@@ -782,40 +702,18 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s) {
 cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
   if (g.M <= 0) return cudaSuccess;
   const bool full_row = g.epi == EPI_HEAD || g.epi == EPI_SUM_LN;
-  const int cn = g.cn > 1 ? g.cn : 1;
-  if (g.K % BK || g.N % g.BN || (full_row && g.BN * cn != g.N) || (g.N / g.BN) % cn) return cudaErrorInvalidValue;
-  if (cn > 1 && (cn != 4 || g.cta_pair || g.a_resident)) return cudaErrorInvalidValue;
+  if (g.K % BK || g.N % g.BN || (full_row && g.BN != g.N)) return cudaErrorInvalidValue;
+  if (g.call && g.m_mult <= 0) return cudaErrorInvalidValue;
   if ((g.epi == EPI_STORE || g.epi == EPI_BIAS_RELU || g.epi == EPI_CROSS || g.epi == EPI_BIAS ||
        g.epi == EPI_SUM_LN) && !g.tmOut)
     return cudaErrorInvalidValue;
   if ((g.epi == EPI_CROSS || g.epi == EPI_CROSS_F32) && (!g.tmX0 || !g.tmXl)) return cudaErrorInvalidValue;
   if (g.epi == EPI_SUM_LN && !g.tmX0) return cudaErrorInvalidValue;  // the fp32 input's TMA load map
   if (g.epi == EPI_MASK && (!g.tmXl || !g.tmOut)) return cudaErrorInvalidValue;
-  // B-multicast clusters of 8 along M (tmB with box {64, BN/8})
-  if (g.mb8) {
-    if (g.cta_pair || g.a_resident || g.cn > 1) return cudaErrorInvalidValue;
-#define CVR_MB(BN_, EPI_) \
-    if (g.BN == BN_ && g.epi == EPI_) return launch_t<BN_, EPI_, false, 1, 8, 1, true>(g, s);
-    CVR_MB(256, EPI_BIAS_RELU)
-    CVR_MB(128, EPI_BIAS_RELU)
-    CVR_MB(192, EPI_CROSS)
-    CVR_MB(64, EPI_STORE)
-#undef CVR_MB
-    return cudaErrorInvalidValue;
-  }
-  // A-multicast clusters of 4 along N (tmA with box {64, 32})
-#define CVR_MC(BN_, EPI_) \
-  if (cn == 4 && g.BN == BN_ && g.epi == EPI_) return launch_t<BN_, EPI_, false, 1, 4>(g, s);
-  CVR_MC(64, EPI_STORE)
-  CVR_MC(128, EPI_BIAS_RELU)
-  CVR_MC(256, EPI_BIAS_RELU)
-  CVR_MC(64, EPI_HEAD)
-#undef CVR_MC
-  if (cn > 1) return cudaErrorInvalidValue;
   // one epilogue warp per quadrant when every CTA runs several tiles (see Cfg::EPW)
   if (g.epw1 && g.cta_pair && (g.epi == EPI_STORE || g.epi == EPI_BIAS_RELU || g.epi == EPI_BIAS)) {
 #define CVR_E1P(BN_, EPI_) \
-    if (g.BN == BN_ && g.epi == EPI_) return launch_t<BN_, EPI_, false, 2, 1, 1>(g, s);
+    if (g.BN == BN_ && g.epi == EPI_) return launch_t<BN_, EPI_, 2, 1>(g, s);
     CVR_E1P(128, EPI_STORE)
     CVR_E1P(256, EPI_STORE)
     CVR_E1P(128, EPI_BIAS_RELU)
@@ -826,7 +724,7 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
   }
   if (g.epw1 && !g.cta_pair && (g.epi == EPI_STORE || g.epi == EPI_BIAS_RELU || g.epi == EPI_BIAS)) {
 #define CVR_E1(BN_, EPI_) \
-    if (g.BN == BN_ && g.epi == EPI_) return launch_t<BN_, EPI_, false, 1, 1, 1>(g, s);
+    if (g.BN == BN_ && g.epi == EPI_) return launch_t<BN_, EPI_, 1, 1>(g, s);
     CVR_E1(128, EPI_STORE)
     CVR_E1(192, EPI_STORE)
     CVR_E1(256, EPI_STORE)
@@ -838,10 +736,10 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
   }
   if (g.epi == EPI_ATTN) {
     if (g.BN != 192 || g.N % 192 || g.cta_pair || !g.out_bf16 || !g.bias || g.ld_x % 8) return cudaErrorInvalidValue;
-    return g.a_resident ? launch_t<192, EPI_ATTN, true>(g, s) : launch_t<192, EPI_ATTN>(g, s);
+    return launch_t<192, EPI_ATTN>(g, s);
   }
 #define CVR_CASE(BN_, EPI_) \
-  if (g.BN == BN_ && g.epi == EPI_) return g.cta_pair ? launch_t<BN_, EPI_, false, 2>(g, s) : launch_t<BN_, EPI_>(g, s);
+  if (g.BN == BN_ && g.epi == EPI_) return g.cta_pair ? launch_t<BN_, EPI_, 2>(g, s) : launch_t<BN_, EPI_>(g, s);
   CVR_CASE(64, EPI_STORE)
   CVR_CASE(128, EPI_STORE)
   CVR_CASE(256, EPI_STORE)
@@ -849,10 +747,8 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
   CVR_CASE(256, EPI_BIAS_RELU)
   CVR_CASE(64, EPI_BIAS_RELU)
   CVR_CASE(128, EPI_BIAS_RELU)
-  if (g.BN == 64 && g.epi == EPI_CROSS && g.K <= 256 && g.a_resident) return launch_t<64, EPI_CROSS, true>(g, s);
   CVR_CASE(64, EPI_CROSS)
-  if (g.BN == 192 && g.epi == EPI_CROSS) return g.cta_pair ? launch_t<192, EPI_CROSS, false, 2>(g, s)
-                                                           : launch_t<192, EPI_CROSS>(g, s);
+  if (g.BN == 192 && g.epi == EPI_CROSS && !g.cta_pair) return launch_t<192, EPI_CROSS>(g, s);
   CVR_CASE(64, EPI_HEAD)
   CVR_CASE(128, EPI_HEAD)
   CVR_CASE(256, EPI_HEAD)

@@ -35,12 +35,13 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 template <int H>
 __global__ void __launch_bounds__(128) mha64_v2_kernel(const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ out,
-                                                       int out_ld) {
+                                                       int out_ld, const CallArgs* call) {
   constexpr int D = H * DH;
   __shared__ __align__(128) __nv_bfloat16 Qs[S * LD2];
   __shared__ __align__(128) __nv_bfloat16 Ks[S * LD2];
   __shared__ __align__(128) __nv_bfloat16 Vs[S * LD2];
   const int b = blockIdx.x / H, h = blockIdx.x % H;
+  if (call && b >= call->B) return;  // executor graphs: grid sized for max_batch
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const __nv_bfloat16* src = qkv + (size_t)b * S * 3 * D + h * DH;
   // 3 x 64 rows x 8 chunks of 16 bytes
@@ -70,7 +71,11 @@ __device__ __forceinline__ float sigmoid_f32(float z) {
 }
 
 __global__ void head_finalize_kernel(const float* __restrict__ part, int n_parts, float c, float* __restrict__ scores,
-                                     int M) {
+                                     int M, const CallArgs* call) {
+  if (call) {  // executor graphs: this batch's rows and scores pointer
+    M = call->B;
+    scores = call->scores;
+  }
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= M) return;
   float z = 0.f;
@@ -80,17 +85,19 @@ __global__ void head_finalize_kernel(const float* __restrict__ part, int n_parts
 
 }  // namespace
 
-cudaError_t launch_mha64(const __nv_bfloat16* qkv, __nv_bfloat16* out, int out_ld, int B, int n_heads, cudaStream_t s) {
+cudaError_t launch_mha64(const __nv_bfloat16* qkv, __nv_bfloat16* out, int out_ld, int B, int n_heads, cudaStream_t s,
+                         const CallArgs* call) {
   if (B <= 0) return cudaSuccess;
   if (n_heads != 4) return cudaErrorInvalidValue;
   if (out_ld % 8) return cudaErrorInvalidValue;
-  mha64_v2_kernel<4><<<B * 4, 128, 0, s>>>(qkv, out, out_ld);
+  mha64_v2_kernel<4><<<B * 4, 128, 0, s>>>(qkv, out, out_ld, call);
   return cudaGetLastError();
 }
 
-cudaError_t launch_head_finalize(const float* partial, int n_parts, float c, float* scores, int M, cudaStream_t s) {
+cudaError_t launch_head_finalize(const float* partial, int n_parts, float c, float* scores, int M, cudaStream_t s,
+                                 const CallArgs* call) {
   if (M <= 0) return cudaSuccess;
-  head_finalize_kernel<<<(M + 255) / 256, 256, 0, s>>>(partial, n_parts, c, scores, M);
+  head_finalize_kernel<<<(M + 255) / 256, 256, 0, s>>>(partial, n_parts, c, scores, M, call);
   return cudaGetLastError();
 }
 

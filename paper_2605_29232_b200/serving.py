@@ -62,8 +62,10 @@ class DynamicBatcher:
         return len(self.q)
 
     def submit(self, req: Request) -> bool:
-        """Queue a request; False (overload) if the queue is full."""
-        if len(self.q) >= self.capacity:
+        """Queue a request; False if the queue is full (overload) or the request alone holds more
+        than max_items items (requests are never split, so it could never be dispatched within the batch cap that
+        the server's staging and the library's max_batch are sized for)."""
+        if len(self.q) >= self.capacity or req.n_items > self.max_items:
             self.rejected += 1
             return False
         self.q.append(req)
@@ -80,7 +82,7 @@ class DynamicBatcher:
         if self.items < self.max_items and now < self.q[0].t_arrival + self.window_s:
             return None
         out, n = [], 0
-        while self.q and (not out or n + self.q[0].n_items <= self.max_items) and \
+        while self.q and n + self.q[0].n_items <= self.max_items and \
                 (self.max_requests is None or len(out) < self.max_requests):
             r = self.q.popleft()
             n += r.n_items
@@ -203,8 +205,9 @@ class ItemPoolView:
         ids = np.ascontiguousarray(item_ids, dtype=np.int32)
         nnz = ctypes.c_int64()
         st = lib().cvr_gather_items(self.T, self.F, self.P, self.offsets.ctypes.data, self.indices.ctypes.data,
-                                    self.dense.ctypes.data, len(ids), ids.ctypes.data, out_off.data_ptr(),
-                                    out_idx.data_ptr(), out_idx.numel(), out_dense.data_ptr(), ctypes.byref(nnz))
+                                    self.dense.ctypes.data, len(ids), ids.ctypes.data, out_dense.shape[0],
+                                    out_off.data_ptr(), out_idx.data_ptr(), out_idx.numel(), out_dense.data_ptr(),
+                                    ctypes.byref(nnz))
         if st:
             raise CvrError(st, "cvr_gather_items")
         return nnz.value
@@ -215,11 +218,10 @@ class Server:
 
     def __init__(self, model, pool: ItemPoolView, max_items: int = 8192, window_s: float = 0.002,
                  host_slots: int = 3, max_nnz: Optional[int] = None, max_requests: Optional[int] = None,
-                 use_graphs: bool = False):
+                 use_graphs: bool = True):
         self.m, self.pool = model, pool
-        # Dynamic batches have (almost) unique sizes: the executor would capture a CUDA graph on the second
-        # sighting of a size (milliseconds of host time inside the serving loop) and rarely replay it, which
-        # showed up as multi-ms p99 spikes at low load; direct launches keep the host cost per batch flat.
+        # The executor replays one CUDA graph per stage and x0 slot for every batch (the batch's pointers and size
+        # live in a device-side call block), so dynamically sized batches need no capture after the first two.
         model.set_option("graphs", 1 if use_graphs else 0)
         self.batcher = DynamicBatcher(max_items, window_s, max_requests=max_requests)
         dev = model.device

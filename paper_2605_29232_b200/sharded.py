@@ -5,10 +5,11 @@ Tables are placed round-robin (table t on rank t mod N, A18).  Per batch of B_gl
   1. every rank pools ITS tables for the GLOBAL batch straight into a destination-major send buffer
      [dst][b_local][t_slot][d] (libcvr ``cvr_embed_shard``; slot = t div N, padded to ceil(T/N)) and
      normalises the dense features of its own batch slice into its local x0;
-  2. one all-to-all exchanges the pooled rows (the only collective on the path; NCCL over NVLink
-     through ``torch.distributed`` on GPUs, gloo in the CPU tests of this host logic);
-  3. ``cvr_unpack_shard`` writes the received source-major chunks [src][b_local][t_slot][d] into the
-     canonical x0 columns of the local slice (V1 of SURVEY.md §8(e));
+  2. ``cvr_exchange`` runs the one all-to-all (the only collective on the path) as grouped ncclSend / ncclRecv
+     on the library's OWN NCCL communicator (``cvr_comm_init``; the unique id is broadcast by the caller's
+     process group, the only thing torch.distributed does here), then
+  3. unpacks the received source-major chunks [src][b_local][t_slot][d] into the canonical x0 columns of the
+     local slice (V1 of SURVEY.md §8(e));
   4. the dense stage runs data-parallel on the local slice of B_global / N examples.
 
 ``FusedShardedScorer`` is V3: step 1 stores pooled rows straight into the owner's x0 over NVLink and steps 2-3
@@ -32,18 +33,19 @@ def slots_per_rank(n_tables: int, world: int) -> int:
     return (n_tables + world - 1) // world
 
 
-def exchange(send: torch.Tensor, recv: torch.Tensor, group=None) -> None:
-    """All-to-all of equal chunks: chunk dst of ``send`` goes to rank dst, chunk src of ``recv`` comes
-    from rank src (both 1-D byte/element views of [N][chunk])."""
+def broadcast_unique_id(make, group=None) -> bytes:
+    """Rank 0 of ``group`` creates the NCCL unique id (``make()``: libcvr cvr_comm_unique_id) and every rank
+    receives it (host plumbing over the caller's process group; gloo in the CPU tests)."""
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_to_all_single(recv, send, group=group)
-    else:
-        recv.copy_(send)
+        box = [make() if dist.get_rank(group) == 0 else None]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        return box[0]
+    return make()
 
 
 def exchange_handles(blob: bytes, group=None) -> list:
-    """Every rank's 64-byte IPC handle blob, in rank order (the host side of V3's peer mapping; gloo in the
-    CPU tests, the NCCL group's store-backed object collective on GPUs)."""
+    """Every rank's IPC handle blob (CVR_IPC_HANDLE_BYTES per buffer), in rank order (the host side of V3's peer
+    mapping; gloo in the CPU tests, the process group's store-backed object collective on GPUs)."""
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         out = [None] * dist.get_world_size(group)
         dist.all_gather_object(out, blob, group=group)
@@ -77,13 +79,22 @@ class FusedShardedScorer:
         self.free = torch.zeros(world_size, dtype=torch.int32, device=self.device)
         self.tables = local_tables(cfg.n_tables, world_size, rank)
         self.epoch = 0
+        self.opened = []
+
+    def close(self):
+        from ._cvr import ipc_close_handle
+        for p in self.opened:
+            ipc_close_handle(p)
+        self.opened = []
 
     def _buffers(self):
         return [self.x0[0], self.x0[1], self.ready, self.free]
 
     def connect(self, peers=None):
-        from ._cvr import ipc_get_handle, ipc_open_handle
+        from ._cvr import IPC_HANDLE_BYTES as HB, ipc_get_handle, ipc_open_handle
         if peers is None:
+            # each handle carries its tensor's offset inside the caching allocator's block: x0 slots and
+            # the 4-int flag arrays are sub-allocated, so the opened base alone would point at the wrong bytes
             mine = [ipc_get_handle(t.data_ptr()) for t in self._buffers()]
             allh = exchange_handles(b"".join(mine), self.group)
             ptrs = []
@@ -91,7 +102,8 @@ class FusedShardedScorer:
                 if r == self.rank:
                     ptrs.append([t.data_ptr() for t in self._buffers()])
                 else:
-                    ptrs.append([ipc_open_handle(allh[r][64 * i:64 * (i + 1)]) for i in range(4)])
+                    ptrs.append([ipc_open_handle(allh[r][HB * i:HB * (i + 1)]) for i in range(4)])
+                    self.opened.extend(ptrs[-1])
         else:
             ptrs = [[t.data_ptr() for t in p._buffers()] for p in peers]
         x0_ptrs = [ptrs[r][0] for r in range(self.N)] + [ptrs[r][1] for r in range(self.N)]
@@ -145,6 +157,8 @@ class ShardedScorer:
         self.ev_dense = [torch.cuda.Event() for _ in range(2)]
         self.k = 0
         self.tables = local_tables(cfg.n_tables, world_size, rank)
+        from ._cvr import comm_unique_id
+        self.model.comm_init(broadcast_unique_id(comm_unique_id, group), world_size, rank)
 
     def load_tables(self, tables: Sequence[torch.Tensor]):
         self.model.load_tables(tables, self.tables)
@@ -165,10 +179,8 @@ class ShardedScorer:
         slot = self.k % 2 if s_dense is not None else 0
         if s_dense is not None and self.k >= 2:
             s.wait_event(self.ev_dense[slot])
-        with torch.cuda.stream(s):
-            self.model.embed_shard(indices, offsets, self.B, dense_local, self.send[slot], self.x0[slot], stream=s)
-            exchange(self.send[slot], self.recv[slot], self.group)
-            self.model.unpack_shard(self.recv[slot], self.B, self.x0[slot], stream=s)
+        self.model.embed_shard(indices, offsets, self.B, dense_local, self.send[slot], self.x0[slot], stream=s)
+        self.model.exchange(self.send[slot], self.recv[slot], self.B, self.x0[slot], stream=s)
         if s_dense is None:
             self.model.dense(self.x0[slot], self.Bl, scores, stream=s)
             return scores

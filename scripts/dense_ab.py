@@ -14,7 +14,7 @@ idx, off, dense = (torch.from_numpy(bt.indices).cuda(), torch.from_numpy(bt.offs
 s = torch.cuda.Stream()
 x0 = m.embed(idx, off, B, dense, stream=s)
 sc = torch.empty(B, device="cuda")
-settings = json.loads(sys.argv[1]) if len(sys.argv) > 1 else [{}, {"a_resident": 0}]
+settings = json.loads(sys.argv[1]) if len(sys.argv) > 1 else [{}, {"pdl": 0}]
 K = int(os.environ.get("K", "200"))
 res = {i: [] for i in range(len(settings))}
 for rep in range(3):
@@ -31,6 +31,6 @@ for rep in range(3):
         b.record(s); torch.cuda.synchronize()
         res[i].append(a.elapsed_time(b) / K * 1e3)
         for k in st:  # restore defaults
-            m.set_option(k, {"a_resident": 0, "pdl": 1, "fused_cross": 0, "graphs": 1, "stack": 0, "ens_u_bn": 128, "pair": 1, "u_bn": 192, "mc": 0, "mb": 0, "pair_mlp": 0, "pair_xv": 0}.get(k, 1))
+            m.set_option(k, {"pdl": 1, "graphs": 1, "ens_u_bn": 128, "pair": 1, "u_bn": 192, "xv_bn": 0, "epw": 2}.get(k, 1))
 for i, st in enumerate(settings):
     print(json.dumps({"setting": st, "us_per_dense": [round(x, 2) for x in res[i]], "min": round(min(res[i]), 2)}))

@@ -29,4 +29,4 @@ for st in settings:
     print(json.dumps({"setting": st, "kernels": {k: round(v["avg_ms"] * 1e3, 2) for k, v in prof.items()},
                       "launches": {k: v["launches"] for k, v in prof.items()}}))
     for k in st:
-        m.set_option(k, {"a_resident": 0, "pdl": 1, "fused_cross": 0, "graphs": 1, "stack": 0}.get(k, 1))
+        m.set_option(k, {"pdl": 1, "graphs": 1, "u_bn": 192, "xv_bn": 0, "epw": 2}.get(k, 1))

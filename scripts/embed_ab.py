@@ -1,4 +1,5 @@
-"""A/B the embedding stage (graph-replayed) for embed_v2 on/off; reports us and algorithmic GB/s."""
+"""Time the embedding stage alone (IDX=uniform: the uniform-index control); reports us and GB/s on algorithmic
+and compulsory (distinct rows once) bytes."""
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, cvr_synth as cs
@@ -26,8 +27,7 @@ s = torch.cuda.Stream()
 x0 = m.new_x0(B)
 K = 200
 for rep in range(3):
-    for v2 in [int(x) for x in os.environ.get('VARIANTS', '0,1').split(',')]:
-        m.set_option("embed_variant", v2)
+    for v2 in [0]:
         for i in range(8):
             m.embed(*dev[i % 4][:2], B, dev[i % 4][2], x0=x0, stream=s)
         torch.cuda.synchronize()

@@ -25,7 +25,7 @@ def role(name):
         r = {(0,): "gemm_xV", (2,): "gemm_tU_cross", (1,): "gemm_mlp_relu", (3,): "gemm_mlp_head",
              (9,): "gemm_mask_mul", (10,): "gemm_ens_qkv_attn"}.get((epi,), f"gemm_{EPI.get(epi, epi)}")
         return f"{r} [BN={bn}{' pair' if cg == 2 else ''}{' cluster%d' % cn if cn > 1 else ''}]"
-    for k in ("embed_bag", "gemm_splitk", "dense_f32", "unpack", "mha64", "head_finalize", "cross_stack", "cross_fused"):
+    for k in ("embed_bag", "dense_f32", "unpack", "mha64", "head_finalize", "set_call"):
         if k in name:
             return k
     return name[:60]

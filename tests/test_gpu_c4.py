@@ -47,45 +47,36 @@ def test_c4_batch_invariance(c4small):
     assert torch.equal(part, full[torch.from_numpy(sel).cuda()])
 
 
-def test_c4_full_size_sampled():
-    """BASELINE.json configs[3] at full size (64 x 1e6 x 256 bf16 tables, B = 8192), the oracle on a
-    sample of 24 examples."""
+@pytest.mark.slow
+def test_c4_full_size_full_batch():
+    """BASELINE.json configs[3] at full size (64 x 1e6 x 256 bf16 tables, B = 8192) through the executor
+    (cvr_score, the launch configuration bench.py times), every one of the 8192 scores against the fp64 oracle
+    ("Report max |delta| over the full 8192 batch"; the oracle regenerates the touched rows)."""
     from paper_2605_29232_b200 import build
     build.build()
     cfg = cs.C4
     m, tabs, w = make_model(cfg, max_batch=8192, max_nnz=1 << 22)
     bt = cs.make_batch(cfg, 0)
     idx, off, dense = to_dev(bt)
-    s = m.dense(m.embed(idx, off, 8192, dense), 8192)
-    assert m.status() == 0
-    sel = np.random.default_rng(2).choice(8192, 24, replace=False)
-    ref = O.score_forward(cfg, cs.table_specs(cfg), w, cs.sub_batch(bt, sel))["scores"]
-    err = np.abs(s[torch.from_numpy(sel).cuda()].double().cpu().numpy() - ref)
-    assert err.max() <= TOL_BF16, err.max()
+    s_e, s_d = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
+    s = torch.empty(8192, device="cuda")
+    torch.cuda.synchronize()
+    m.score(idx, off, 8192, dense, s, s_embed=s_e, s_dense=s_d)
+    s_d.synchronize()
+    assert m.status(s_d) == 0
+    got = s.double().cpu().numpy()
     del m, tabs
     torch.cuda.empty_cache()
+    specs, err = cs.table_specs(cfg), np.empty(8192)
+    for c0 in range(0, 8192, 1024):
+        sel = np.arange(c0, c0 + 1024)
+        err[sel] = np.abs(got[sel] - O.score_forward(cfg, specs, w, cs.sub_batch(bt, sel))["scores"])
+    print(f"c4 full batch: max |delta| = {err.max():.3e}, p99 = {np.percentile(err, 99):.3e} over 8192 examples")
+    assert err.max() <= TOL_BF16, (err.max(), np.percentile(err, 99))
 
 
-@pytest.mark.parametrize("B", [130, 3])
-def test_c4_fused_ffn_bitexact(c4small, B):
-    """The fused FFN + out-projection + LN kernel (ens_ffn.cu) accumulates O Wo^T then h W2^T in the same
-    16-wide K steps as the [O | h] [Wo | W2]^T GEMM and rounds h to bf16 at the same point: bit-identical
-    scores to the two-GEMM path (ragged token tiles included: B * 64 tokens)."""
-    cfg, m, tabs, w = c4small
-    bt = cs.make_batch(cfg, 6, batch=B)
-    idx, off, dense = to_dev(bt)
-    x0 = m.embed(idx, off, B, dense)
-    s_u = m.dense(x0, B).clone()
-    m.set_option("ens_fused_ffn", 1)
-    try:
-        s_f = m.dense(x0, B).clone()
-    finally:
-        m.set_option("ens_fused_ffn", 0)
-    assert torch.equal(s_f, s_u)
-
-
-@pytest.mark.parametrize("B,ar", [(131, 0), (512, 0), (512, 1)])
-def test_c4_fused_qkv_attention_bitexact(c4small, B, ar):
+@pytest.mark.parametrize("B", [131, 512])
+def test_c4_fused_qkv_attention_bitexact(c4small, B):
     """Option ens_fused_attn: the QKV projection and the 64-token attention as ONE GEMM (EPI_ATTN: each 128-token x
     192 tile [q_h | k_h | v_h] + b is rounded to bf16 in shared memory and attended in the epilogue with the
     mha64 core) -- the same roundings and the same attention code, so scores are bit-identical to QKV GEMM +
@@ -94,14 +85,12 @@ def test_c4_fused_qkv_attention_bitexact(c4small, B, ar):
     bt = cs.make_batch(cfg, 8, batch=B)
     idx, off, dense = to_dev(bt)
     x0 = m.embed(idx, off, B, dense)
-    m.set_option("ens_attn_ar", ar)  # ar = 1: the X tile resident across its 4 heads' tiles
     try:
         s1 = m.dense(x0, B).clone()  # fused (default)
         m.set_option("ens_fused_attn", 0)
         s0 = m.dense(x0, B).clone()
     finally:
         m.set_option("ens_fused_attn", 1)
-        m.set_option("ens_attn_ar", 0)
     assert m.status() == 0
     assert torch.equal(s0, s1)
 

@@ -52,7 +52,16 @@ def test_whole_requests_never_split_and_fifo():
     assert flat == list(range(300))                 # FIFO, each request exactly once
     n = {r.rid: r.n_items for r in reqs}
     for _, bb in out:
-        assert sum(n[r] for r in bb) <= 1000 or len(bb) == 1
+        assert sum(n[r] for r in bb) <= 1000
+
+
+def test_oversized_request_rejected():
+    """A request with more items than max_items is rejected at submit (it would overflow the
+    server's pinned staging, sized for max_items); the queue keeps serving the others."""
+    b = DynamicBatcher(max_items=10, window_s=0.0)
+    assert not b.submit(Request(0, 0.0, 11)) and b.rejected == 1
+    assert b.submit(Request(1, 0.0, 10))
+    assert [r.rid for r in b.poll(0.0)] == [1]
 
 
 def test_overload_rejects_newest():
@@ -121,7 +130,7 @@ def test_concat_requests_matches_reference():
     o_idx = np.zeros(4096, np.int32)
     o_den = np.zeros((B, F), np.float32)
     nnz = ctypes.c_int64()
-    st = lib().cvr_concat_requests(3, T, F, n, offs, idxs, dens, o_off.ctypes.data, o_idx.ctypes.data, 4096,
+    st = lib().cvr_concat_requests(3, T, F, n, offs, idxs, dens, B, o_off.ctypes.data, o_idx.ctypes.data, 4096,
                                    o_den.ctypes.data, ctypes.byref(nnz))
     assert st == 0
     # reference: table-major, requests in order

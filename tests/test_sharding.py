@@ -1,6 +1,6 @@
 """Table-wise sharding host logic on CPU: the sharding simulator reproduces the canonical x0 exactly
-for N in {1,2,4,8} (P11), and the product's exchange() moves the chunks correctly across a real
-world_size-2 gloo process group."""
+for N in {1,2,4,8} (P11), the all-to-all payload is conserved chunk by chunk (P12), and the host plumbing of
+the library's NCCL communicator / V3 peer mapping works across a real world_size-2 gloo process group."""
 import os
 import socket
 
@@ -29,6 +29,22 @@ def test_simulator_reproduces_canonical_x0(world):
     Bl = 64 // world
     got = np.concatenate([S.unpack(recvs[d], cfg.n_tables, world) for d in range(world)])
     np.testing.assert_array_equal(got, pooled.reshape(64, -1))
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_all_to_all_payload_conserved(world):
+    """P12: the all-to-all is a permutation of equal chunks -- the SHA-256 of every (src, dst) chunk sent equals
+    the digest of the chunk received, and no byte is created or lost."""
+    import hashlib
+    cfg, bt, pooled = pooled_c2(64)
+    sends = [S.build_send(pooled.astype(np.float32), world, s) for s in range(world)]
+    recvs = S.all_to_all(sends)
+    dig = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+    for s_ in range(world):
+        for d in range(world):
+            assert dig(sends[s_][d]) == dig(recvs[d][s_])
+    assert sorted(dig(x[i]) for x in sends for i in range(world)) == sorted(dig(x[i]) for x in recvs
+                                                                             for i in range(world))
 
 
 def test_table_placement_round_robin():
@@ -62,19 +78,21 @@ def _free_port():
 def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2605_29232_b200.sharded import exchange
-    cfg, bt, pooled = pooled_c2(64)
-    send = S.build_send(pooled.astype(np.float32), world, rank)
-    recv = torch.empty(send.size, dtype=torch.float32)
-    exchange(torch.from_numpy(send.reshape(-1)).clone(), recv)
-    mine = S.unpack(recv.numpy().reshape(send.shape), cfg.n_tables, world)
-    Bl = 64 // world
-    ok = np.array_equal(mine, pooled.astype(np.float32)[rank * Bl:(rank + 1) * Bl].reshape(Bl, -1))
-    q.put((rank, ok))
+    from paper_2605_29232_b200.sharded import broadcast_unique_id
+    calls = []
+
+    def make():  # stands in for cvr_comm_unique_id (NCCL needs a GPU): only rank 0 may call it
+        calls.append(rank)
+        return bytes(range(128))
+
+    uid = broadcast_unique_id(make)
+    q.put((rank, uid == bytes(range(128)) and calls == ([0] if rank == 0 else [])))
     dist.destroy_process_group()
 
 
-def test_exchange_gloo_world2():
+def test_unique_id_broadcast_gloo_world2():
+    """S4 host plumbing: rank 0 alone creates the NCCL unique id for the library's communicator (cvr_comm_init)
+    and every rank receives the same 128 bytes over the process group."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -91,9 +109,9 @@ def _handle_worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2605_29232_b200.sharded import exchange_handles
-    blob = bytes([rank + 1]) * 256   # stands in for 4 CUDA IPC handles (x0 slots 0/1, ready, free: 64 B each)
+    blob = bytes([rank + 1]) * 288   # stands in for 4 IPC handles (x0 slots 0/1, ready, free: 72 B each)
     got = exchange_handles(blob)
-    q.put((rank, got == [bytes([r + 1]) * 256 for r in range(world)]))
+    q.put((rank, got == [bytes([r + 1]) * 288 for r in range(world)]))
     dist.destroy_process_group()
 
 
