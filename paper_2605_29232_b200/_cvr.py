@@ -191,7 +191,7 @@ def comm_unique_id() -> bytes:
     st = lib().cvr_comm_unique_id(ctypes.byref(uid))
     if st != 0:
         raise CvrError(st, "cvr_comm_unique_id (NCCL unavailable?)")
-    return bytes(uid.internal) + b"\0" * (128 - len(bytes(uid.internal)))
+    return ctypes.string_at(ctypes.addressof(uid), 128)  # (uid.internal would stop at the first NUL byte)
 
 
 def text_ngram_keys(texts, n: int):
