@@ -390,7 +390,7 @@ def run_serving_probe(cfg, dev, tables, weights, qps=8000.0, duration=2.0, warm=
     n_items = sum(reqs[i].n_items for i in meas)
     m.close()
     return {"config": "c5: BASELINE.json configs[4] (c2 model, Poisson queries, lognormal(ln 50, 0.8) items capped at "
-                      "500, 2 ms window, max 8192 items, cvr_score_host with per-slot graphs)",
+                      "500, 2 ms window, max 8192 items, cvr_score_host with executor graphs, native serving loop)",
             "qps_offered": qps, "duration_s": duration, "queries": len(meas), "p50_ms": float(nearest_rank(L, 50)),
             "p99_ms": float(nearest_rank(L, 99)), "served_items_per_s": n_items / duration,
             "batch_items_mean": float(sizes.mean()) if len(sizes) else 0.0, "rejected": int(srv.batcher.rejected)}
@@ -429,8 +429,8 @@ def run_cvr(args, cfg):
         m.score_raw(ip, op, nnz, B, dp, sp, hse, hsd)
 
     torch.cuda.synchronize(dev)  # the inputs were copied on the current stream; the executor's streams start now
-    # warm-up: the executor captures its two per-slot graphs per stage in the first two calls; every later batch
-    # (any pointers, any size) replays them, so the timed region below holds no capture
+    # warm-up: the executor captures one graph per stage for each of its two x0 slots in the first two calls; every
+    # later batch (any pointers; any size in the same grid bucket) replays them, so the timed region holds no capture
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize(dev)
@@ -547,7 +547,7 @@ def run_cvr(args, cfg):
         h2d = float(np.mean([b.nnz * 4 + b.offsets.nbytes + b.dense.nbytes for b in ring]))
         e2e = {"value": world * args.steps * B / (hel / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": B * 4, "ms_per_step": hel / args.steps,
-               "api": "cvr_score_host (pinned host buffers, copy stream + two compute streams, per-slot graphs)"}
+               "api": "cvr_score_host (pinned host buffers, copy stream + two compute streams, executor graphs)"}
         # P12 on the host-fed path: the staged copies the kernels read (the slot's call block points into the
         # ctx's workspace) against the generator's arrays
         hrec = m.call_info((2 * args.warmup + 2 * args.steps - 1) % 2)

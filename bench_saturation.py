@@ -6,12 +6,11 @@ batching)" row), then 0.25 .. 4 ms, scaled to B200 service times as SURVEY.md §
 offered load (queries/s; items/s = x 68.6 mean items per query) whose p99 latency stays under the bound,
 found by geometric bisection (serving.peak_qps_search), with its ratio to the no-batching row.  Config 5
 traffic (Poisson arrivals, lognormal items per query) from the config-2 item pool, served through
-serving.Server (host batch assembly + cvr_score_host).  Prints one JSON line per bound and a summary.
+the native serving loop (libcvr cvr_serve_trace: C++ batcher, host batch assembly, cvr_score_host).  Prints one JSON line per bound and a summary.
 
     python bench_saturation.py [--bounds-ms 5 10] [--windows-ms 0.25 0.5 1 2 4] [--duration 0.6]
 """
 import argparse
-import gc
 import json
 import os
 import sys
@@ -25,17 +24,17 @@ sys.path.insert(0, ROOT)
 
 import cvr_synth as cs  # noqa: E402
 from paper_2605_29232_b200 import CvrModel  # noqa: E402
-from paper_2605_29232_b200.serving import ItemPoolView, Request, Server, nearest_rank, saturation_table  # noqa: E402
+from paper_2605_29232_b200.serving import ItemPoolView, Server, nearest_rank, saturation_table  # noqa: E402
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--bounds-ms", type=float, nargs="+", default=[5.0, 10.0])
-    ap.add_argument("--windows-ms", type=float, nargs="+", default=[0.25, 0.5, 1.0, 2.0, 4.0])
-    ap.add_argument("--duration", type=float, default=1.0)
+    ap.add_argument("--windows-ms", type=float, nargs="+", default=[0.1, 0.25, 0.5, 1.0, 2.0, 4.0, 8.0])
+    ap.add_argument("--duration", type=float, default=0.5)
     ap.add_argument("--warmup", type=float, default=0.15)
-    ap.add_argument("--lo", type=float, default=1000.0)
-    ap.add_argument("--hi", type=float, default=128000.0)
+    ap.add_argument("--lo", type=float, default=500.0)
+    ap.add_argument("--hi", type=float, default=4.0e6)
     ap.add_argument("--rel-eps", type=float, default=0.07)
     ap.add_argument("--max-items", type=int, default=8192)
     ap.add_argument("--pool", type=int, default=1 << 16)
@@ -57,16 +56,11 @@ def main():
         def at(qps):
             # at least ~2000 measured requests per point: the p99 of a few hundred samples is host jitter
             dur = max(args.duration, 2000.0 / qps)
-            trace = cs.make_requests(qps, args.warmup + dur, args.pool)
-            reqs = [Request(i, t, len(ids), ids) for i, (t, ids) in enumerate(trace)]
+            t, n, start, ids = cs.make_requests_flat(qps, args.warmup + dur, args.pool)
             srv = Server(m, view, max_items=args.max_items, window_s=0.0 if window_ms is None else window_ms / 1e3,
                          max_nnz=max_nnz, max_requests=1 if window_ms is None else None)
-            gc.disable()  # a collector pause inside the serving loop would land in the tail
-            try:
-                lat, sizes, _ = srv.run(reqs, abort_after_s=4 * bound_s)
-            finally:
-                gc.enable()
-            meas = np.array([r.t_arrival >= args.warmup for r in reqs])
+            lat, sizes, _ = srv.run_arrays(t, n, start, ids, abort_after_s=4 * bound_s)  # native loop
+            meas = t >= args.warmup
             p99 = float(nearest_rank(lat[meas], 99)) if meas.any() else float("inf")
             log.append({"window_ms": window_ms, "qps": round(qps, 1), "p99_ms": p99 * 1e3,
                         "mean_batch_items": float(sizes.mean()) if len(sizes) else 0.0})

@@ -472,6 +472,16 @@ def make_item_pool(cfg: CvrConfig, pool_size: int = 1 << 16, k: int = 5000) -> B
     return make_batch(cfg, k, batch=pool_size)
 
 
+def make_requests_flat(qps: float, duration_s: float, pool_size: int, seed: int = 1005):
+    """Config 5 trace as flat arrays for the native serving loop (large offered loads): (t_arrival [s], n_items,
+    item_start [n+1], item_ids) -- the same arrivals and sizes as make_requests, item ids drawn in one call."""
+    t, n = request_trace(qps, duration_s, seed=seed)
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence(seed, spawn_key=(STREAM_TRACE, 8, int(qps)))))
+    start = np.zeros(len(n) + 1, np.int64)
+    start[1:] = np.cumsum(n)
+    return t, n.astype(np.int32), start, rng.integers(0, pool_size, int(start[-1])).astype(np.int32)
+
+
 def make_requests(qps: float, duration_s: float, pool_size: int, seed: int = 1005):
     """Config 5 request trace: [(t_arrival, item_ids)], Poisson arrivals at ``qps`` queries/s, items per
     query clip(rint(lognormal(ln 50, 0.8)), 1, 500) drawn uniformly from the pool (A21)."""

@@ -165,10 +165,11 @@ int cvr_dense(cvr_ctx* ctx, const void* d_x0, int batch, float* d_scores, cvr_st
  * s_embed, the dense stage on s_dense, with event edges embed(k) -> dense(k) and
  * dense(k) -> embed(k+2) (slot reuse).  Back-to-back calls therefore overlap the embed
  * stage of batch k+1 with the dense stage of batch k (S9; "Hybrid CPU-GPU Execution").
- * Each stage is ONE CUDA graph per x0 slot, captured at its first use and replayed for every later batch of any
- * size <= max_batch: the batch's pointers and row count are written to a per-slot argument block in the workspace
- * (a one-thread kernel on s_embed) that every kernel of both stages reads (option "graphs" [1]).  The pointers
- * must stay valid until s_dense has passed this batch. */
+ * Each stage is one CUDA graph per (x0 slot, grid-size bucket), captured at its first use and replayed for every
+ * later batch: the batch's pointers and row count are written to a per-slot argument block in the workspace (a
+ * one-thread kernel on s_embed) that every kernel of both stages reads, so no pointer or size is baked into a graph;
+ * the bucket (batch rounded up to a power of two >= 128, capped at max_batch) only sizes the grids (option
+ * "graphs" [1]).  The pointers must stay valid until s_dense has passed this batch. */
 int cvr_score(cvr_ctx* ctx, const int32_t* d_indices, const int32_t* d_offsets, int64_t nnz,
               int batch, const float* d_dense, float* d_scores, cvr_stream_t s_embed,
               cvr_stream_t s_dense);
@@ -253,7 +254,7 @@ int cvr_exchange(cvr_ctx* ctx, const void* d_send, void* d_recv, int batch_globa
 int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d_x0, cvr_stream_t stream);
 
 /* Options (defaults in brackets): "graphs" [1] replay the executor stages of cvr_score / cvr_score_host as
- * per-slot CUDA graphs (see cvr_score); "pdl" [1] launch dependent GEMMs with programmatic stream serialization;
+ * CUDA graphs (see cvr_score); "pdl" [1] launch dependent GEMMs with programmatic stream serialization;
  * "prefetch_b" [1] each GEMM issues its first ring stages' weight loads before waiting for the previous kernel;
  * "embed_bps" [0 = uncapped] embedding CTAs per SM inside the executor; "xv_bn" [0 = by wave count] N tile of
  * t = x_l V^T (64, 128, 256); "u_bn" [192] N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64);
@@ -299,6 +300,55 @@ int cvr_gather_items(int n_tables, int n_dense, int64_t pool_size, const int32_t
                      const int32_t* pool_indices, const float* pool_dense, int n, const int32_t* item_ids,
                      int out_batch_cap, int32_t* out_offsets, int32_t* out_indices, int64_t out_indices_cap,
                      float* out_dense, int64_t* out_nnz);
+
+/* -- serving: the native dynamic-batching loop (SURVEY.md §8(a) S0 + S9; "Server-Side Batching",
+ * Table 6) ------------------------------------------------------------------
+ * Batcher rule (identical to serving.DynamicBatcher): requests are never split; a request with more than max_items
+ * items or arriving at a full queue (queue_capacity requests) is rejected (latency +inf); a batch is
+ * dispatched when the queued items reach max_items or the OLDEST queued request has waited window_s, and holds the
+ * longest FIFO prefix of whole requests with sum(items) <= max_items (and <= max_requests requests when > 0;
+ * max_requests = 1 with window_s = 0 is Table 6's "w/o dynamic batching" row). */
+typedef struct {
+  double window_s;        /* coalescing window, anchored at the oldest queued request                         */
+  int max_items;          /* batch cap (<= the ctx's max_batch)                                               */
+  int max_requests;       /* 0 = no limit                                                                     */
+  int queue_capacity;     /* queued requests before overload rejection                                       */
+  int host_slots;         /* batches in flight (pinned staging slots), 1..16                                  */
+  int64_t max_nnz;        /* index capacity of a slot (<= the ctx's max_nnz)                                  */
+  double abort_after_s;   /* > 0: stop once the oldest queued request has waited this long (overload probe)    */
+} cvr_serve_config;
+
+typedef struct {
+  int64_t rejected;       /* requests rejected at admission                                                   */
+  int aborted;            /* 1 if abort_after_s stopped the run (unserved requests keep latency +inf)          */
+  int64_t items_served;
+  double host_dispatch_s; /* host time spent assembling + enqueueing batches                                  */
+  double wall_s;          /* from the trace's time origin to the last completion                              */
+} cvr_serve_stats;
+
+/* Serve an open-loop trace on ONE host thread: request r arrives at t_arrival[r] seconds (non-decreasing; the
+ * origin is 10 ms after the call starts) with n_items[r] candidate items, pool item ids
+ * item_ids[item_start[r] .. item_start[r] + n_items[r]) of the host item pool (table-major CSR pool_offsets
+ * [T*P + 1], pool_indices, pool_dense [P, F], as cvr_gather_items).  Each dispatched batch is assembled into one of
+ * host_slots page-locked staging slots (cvr_gather_items) and enqueued with cvr_score_host on the three streams
+ * (the scores are stored straight into the slot's mapped buffer); a CUDA event per slot marks completion, polled
+ * without blocking.  Outputs: latency[r] = completion seen on the host - t_arrival[r] (s; +inf if rejected or not
+ * served), scores_out (optional, [sum n_items]) at item_start[r], batch_sizes[b] (capacity n_req) and *n_batches,
+ * stats.  Synchronous (returns when every batch has completed). */
+int cvr_serve_trace(cvr_ctx* ctx, const cvr_serve_config* cfg, int n_tables, int n_dense, int64_t pool_size,
+                    const int32_t* pool_offsets, const int32_t* pool_indices, const float* pool_dense, int n_req,
+                    const double* t_arrival, const int32_t* n_items, const int64_t* item_start,
+                    const int32_t* item_ids, double* latency, float* scores_out, int32_t* batch_sizes,
+                    int* n_batches, cvr_serve_stats* stats, cvr_stream_t s_copy, cvr_stream_t s_embed,
+                    cvr_stream_t s_dense);
+
+/* The same batcher on a simulated clock: one server whose batch of n items takes
+ * service_fixed_s + service_per_item_s * n seconds; a batch is dispatched when the batcher releases it and the
+ * server is free.  latency[r] (+inf if rejected), batch_of[r] (-1 if rejected), dispatch_time[b] (capacity n_req),
+ * *n_batches.  Host only (tests). */
+int cvr_batcher_simulate(int n_req, const double* t_arrival, const int32_t* n_items, double window_s, int max_items,
+                         int max_requests, int queue_capacity, double service_fixed_s, double service_per_item_s,
+                         double* latency, int32_t* batch_of, double* dispatch_time, int* n_batches);
 
 /* -- feature front end -----------------------------------------------------
  * Per model table t (n == T): vocab[t] > 0 puts the table in keys mode -- cvr_embed_keys hashes each raw

@@ -45,6 +45,17 @@ class cvr_call_record(ctypes.Structure):
                 ("nnz", ctypes.c_int64), ("batch", ctypes.c_int), ("graph_captures", ctypes.c_int64)]
 
 
+class cvr_serve_config(ctypes.Structure):
+    _fields_ = [("window_s", ctypes.c_double), ("max_items", ctypes.c_int), ("max_requests", ctypes.c_int),
+                ("queue_capacity", ctypes.c_int), ("host_slots", ctypes.c_int), ("max_nnz", ctypes.c_int64),
+                ("abort_after_s", ctypes.c_double)]
+
+
+class cvr_serve_stats(ctypes.Structure):
+    _fields_ = [("rejected", ctypes.c_int64), ("aborted", ctypes.c_int), ("items_served", ctypes.c_int64),
+                ("host_dispatch_s", ctypes.c_double), ("wall_s", ctypes.c_double)]
+
+
 IPC_HANDLE_BYTES = 72  # CVR_IPC_HANDLE_BYTES: CUDA IPC handle of the allocation + the tensor's offset inside it
 
 
@@ -96,6 +107,11 @@ _SIGS = [
                                            ctypes.c_int64, _vp, _c_i64p]),
     ("cvr_gather_items", ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int64, _vp, _vp, _vp, ctypes.c_int, _vp,
                                         ctypes.c_int, _vp, _vp, ctypes.c_int64, _vp, _c_i64p]),
+    ("cvr_serve_trace", ctypes.c_int, [_vp, ctypes.POINTER(cvr_serve_config), ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_int64, _vp, _vp, _vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                       _c_ip, ctypes.POINTER(cvr_serve_stats), _vp, _vp, _vp]),
+    ("cvr_batcher_simulate", ctypes.c_int, [ctypes.c_int, _vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_int, ctypes.c_double, ctypes.c_double, _vp, _vp, _vp, _c_ip]),
     ("cvr_set_feature_spec", ctypes.c_int, [_vp, ctypes.c_int, _c_i64p, _c_ip]),
     ("cvr_embed_keys", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp]),
     ("cvr_score_keys", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp, _vp]),

@@ -208,20 +208,33 @@ struct cvr_ctx {
   int xv_bn = 0;               // option "xv_bn": N tile of t = x_l V^T (0 = by wave count, see pick_bn_xv)
   int epw_mode = 2;            // option "epw": split epilogues 0 never, 1 always, 2 when a CTA has one tile
   bool mask_grouped = true;    // option "mask_grouped": MaskNet parallel blocks as one grouped GEMM launch
-  // executor CUDA graphs: ONE per (stage, slot), captured at first use and replayed for every batch (the batch
-  // lives in the per-call block, so neither its pointers nor its size are baked into the graph)
+  // executor CUDA graphs: one per (stage, slot, size bucket), captured at first use and replayed for every batch
+  // (the batch lives in the per-call block, so neither its pointers nor its row count are baked into the graph;
+  // the bucket -- the batch size rounded up to a power of two >= 128, capped at max_batch -- only sizes the grids,
+  // so a 68-item request does not launch the grids of a max_batch one)
   bool use_graphs = true;
-  enum { G_EMBED = 0, G_EMBED_KEYS = 1, G_DENSE = 2, G_KINDS = 3 };
-  cudaGraphExec_t gexec[G_KINDS][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
-  int64_t gkernels[G_KINDS][2] = {{0, 0}, {0, 0}, {0, 0}};
+  enum { G_EMBED = 0, G_EMBED_KEYS = 1, G_DENSE = 2, G_KINDS = 3, G_BUCKETS = 24 };
+  cudaGraphExec_t gexec[G_KINDS][2][G_BUCKETS] = {};
+  int64_t gkernels[G_KINDS][2][G_BUCKETS] = {};
   int64_t graph_captures = 0;
   void drop_graphs() {
     for (auto& kind : gexec)
-      for (auto& g : kind)
-        if (g) {
-          cudaGraphExecDestroy(g);
-          g = nullptr;
-        }
+      for (auto& sl : kind)
+        for (auto& g : sl)
+          if (g) {
+            cudaGraphExecDestroy(g);
+            g = nullptr;
+          }
+  }
+  // grid size of an executor batch of `batch` rows: the next power of two >= 128, capped at max_batch
+  int bucket_rows(int batch, int* idx) const {
+    int b = 128, i = 0;
+    while (b < batch && b < max_batch) {
+      b <<= 1;
+      ++i;
+    }
+    *idx = i;
+    return b < max_batch ? b : max_batch;
   }
   std::vector<GemmPlan> plan;  // cross layers (V, U interleaved), then MLP
   // launch accounting + optional per-launch CUDA-event timing (cvr_profile_begin/end)
@@ -1415,12 +1428,12 @@ int user_x0_maps(cvr_ctx* c, const void* d_x0, int batch, CUtensorMap* tm, CUten
 // per-call block, so the same graph serves every batch and batch size), or launch directly (graphs off, while
 // profiling, or inside a caller's own capture).
 template <typename F>
-int run_stage(cvr_ctx* c, int kind, int slot, cudaStream_t s, F&& enqueue) {
+int run_stage(cvr_ctx* c, int kind, int slot, int bucket, cudaStream_t s, F&& enqueue) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (!c->use_graphs || s == nullptr || c->prof_on || cudaStreamIsCapturing(s, &cs) != cudaSuccess ||
       cs != cudaStreamCaptureStatusNone)
     return enqueue(s);
-  cudaGraphExec_t& ge = c->gexec[kind][slot];
+  cudaGraphExec_t& ge = c->gexec[kind][slot][bucket];
   if (!ge) {
     const int64_t l0 = c->launches;
     cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
@@ -1441,12 +1454,12 @@ int run_stage(cvr_ctx* c, int kind, int slot, cudaStream_t s, F&& enqueue) {
       ge = nullptr;
       return c->cuda_fail(e, "cudaGraphInstantiate");
     }
-    c->gkernels[kind][slot] = nk;
+    c->gkernels[kind][slot][bucket] = nk;
     ++c->graph_captures;
   }
   cudaError_t e = cudaGraphLaunch(ge, s);
   if (e != cudaSuccess) return c->cuda_fail(e, "cudaGraphLaunch");
-  c->launches += c->gkernels[kind][slot];
+  c->launches += c->gkernels[kind][slot][bucket];
   return CVR_OK;
 }
 
@@ -1570,9 +1583,10 @@ int score_impl(cvr_ctx* c, const int32_t* d_indices, const uint64_t* d_keys, con
   if (s_after_wait && (e = cudaStreamWaitEvent(se, c->ev_copy[slot], 0)) != cudaSuccess)  // host-fed: H2D landed
     return c->cuda_fail(e, "wait copy");
   void* x0 = c->ws + c->off_x0[slot];
-  const int Bmax = c->max_batch;
+  int bucket = 0;
+  const int Bmax = c->bucket_rows(batch, &bucket);  // grid sizing only: the kernels read `batch` from the block
   c->call = blk;
-  st = run_stage(c, d_keys ? cvr_ctx::G_EMBED_KEYS : cvr_ctx::G_EMBED, slot, se, [&](cudaStream_t s) {
+  st = run_stage(c, d_keys ? cvr_ctx::G_EMBED_KEYS : cvr_ctx::G_EMBED, slot, bucket, se, [&](cudaStream_t s) {
     return do_embed(c, d_indices, d_offsets, nnz, Bmax, d_dense, x0, s, c->embed_bps_pipe, d_keys);
   });
   if (st) {
@@ -1586,7 +1600,7 @@ int score_impl(cvr_ctx* c, const int32_t* d_indices, const uint64_t* d_keys, con
     const CUtensorMap* tm = (c->backbone == CVR_DCN_LOWRANK || c->backbone == CVR_MASKNET) ? &c->tm_x0slot[slot]
                             : ens ? &c->ens.flat_x0[slot] : nullptr;
     const CUtensorMap* tmt = ens ? &c->ens.tok_x0[slot] : nullptr;
-    st = run_stage(c, cvr_ctx::G_DENSE, slot, sd,
+    st = run_stage(c, cvr_ctx::G_DENSE, slot, bucket, sd,
                    [&](cudaStream_t s) { return do_dense(c, x0, tm, tmt, Bmax, d_scores, s); });
   }
   c->call = nullptr;

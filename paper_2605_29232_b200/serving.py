@@ -10,10 +10,11 @@
 * ``nearest_rank`` -- percentile by nearest rank.
 * ``two_stage_schedule`` -- the simulated-clock model of the decoupled two-stage executor (S9):
   stage A of batch k+1 overlaps stage B of batch k, with ``slots`` x0 buffers.
-* ``Server`` -- the real loop: admits requests at their scheduled (open-loop) arrival times, batches
-  them, assembles each batch on the host (libcvr ``cvr_gather_items`` into pinned staging, stage 0),
-  scores it through ``cvr_score_host`` (H2D -> embed stream -> dense stream -> D2H, S1-S8) and stamps
-  completion when the scores are on the host.  Latency = completion - scheduled arrival.
+* ``Server`` -- the real loop, native (libcvr ``cvr_serve_trace``): admits requests at their scheduled (open-loop)
+  arrival times into the same batcher (C++), assembles each batch on the host (``cvr_gather_items`` into pinned
+  staging, stage 0), scores it through ``cvr_score_host`` (H2D -> embed stream -> dense stream -> zero-copy
+  scores, S1-S8) and stamps completion when the batch's event has fired.  Latency = completion - scheduled arrival.
+  ``batcher_simulate`` replays the native batcher on a simulated clock (tests pin it to DynamicBatcher).
 * ``simulate_serving`` / ``peak_qps_search`` / ``saturation_table`` -- the Table 6 workload (PAPER.md:1666-1684;
   SPEC.md:660-668): for each coalescing window, the highest offered load whose p99
   latency stays under a bound (bisection), and its ratio to the no-batching row.
@@ -213,74 +214,89 @@ class ItemPoolView:
         return nnz.value
 
 
+def batcher_simulate(t_arrival, n_items, window_s: float, max_items: int = 8192, max_requests: int = 0,
+                     queue_capacity: int = 1 << 30, service_fixed_s: float = 0.0, service_per_item_s: float = 0.0):
+    """libcvr cvr_batcher_simulate: the native batcher on a simulated clock -> (latency, batch_of, dispatch_times)."""
+    t = np.ascontiguousarray(t_arrival, dtype=np.float64)
+    n = np.ascontiguousarray(n_items, dtype=np.int32)
+    N = len(t)
+    lat, bof, disp = np.zeros(N), np.zeros(N, np.int32), np.zeros(max(N, 1))
+    nb = ctypes.c_int()
+    st = lib().cvr_batcher_simulate(N, t.ctypes.data, n.ctypes.data, window_s, max_items, max_requests or 0,
+                                    queue_capacity, service_fixed_s, service_per_item_s, lat.ctypes.data,
+                                    bof.ctypes.data, disp.ctypes.data, ctypes.byref(nb))
+    if st:
+        raise CvrError(st, "cvr_batcher_simulate")
+    return lat, bof, disp[:nb.value]
+
+
 class Server:
-    """Open-loop serving of a request trace through DynamicBatcher + cvr_score_host."""
+    """Open-loop serving of a request trace: libcvr's native loop (cvr_serve_trace: the batcher above in C++,
+    host batch assembly into page-locked slots, cvr_score_host on three streams, completion by CUDA events, one
+    busy-polling host thread).  This class only marshals the trace and the results."""
 
     def __init__(self, model, pool: ItemPoolView, max_items: int = 8192, window_s: float = 0.002,
                  host_slots: int = 3, max_nnz: Optional[int] = None, max_requests: Optional[int] = None,
-                 use_graphs: bool = True):
+                 use_graphs: bool = True, queue_capacity: int = 1 << 16):
         self.m, self.pool = model, pool
         # The executor replays one CUDA graph per stage and x0 slot for every batch (the batch's pointers and size
         # live in a device-side call block), so dynamically sized batches need no capture after the first two.
         model.set_option("graphs", 1 if use_graphs else 0)
-        self.batcher = DynamicBatcher(max_items, window_s, max_requests=max_requests)
+        if max_items > model.max_batch:
+            raise ValueError(f"max_items {max_items} > the model's max_batch {model.max_batch}")
+        from ._cvr import cvr_serve_config
+        self.cfg = cvr_serve_config(window_s, max_items, max_requests or 0, queue_capacity, host_slots,
+                                    max_nnz or model.max_nnz, 0.0)
+        self.max_items = max_items
+        self.batcher = type("BatcherStats", (), {"rejected": 0})()
         dev = model.device
         self.s_copy, self.s_embed = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         self.s_dense = torch.cuda.Stream(dev, priority=-1)
-        T, F = pool.T, pool.F
-        cap = max_nnz or model.max_nnz
-        self.slots = [dict(off=torch.empty(T * max_items + 1, dtype=torch.int32).pin_memory(),
-                           idx=torch.empty(cap, dtype=torch.int32).pin_memory(),
-                           dense=torch.empty(max_items, F, dtype=torch.float32).pin_memory(),
-                           scores=torch.empty(max_items, dtype=torch.float32).pin_memory(),
-                           ev=torch.cuda.Event(), busy=False)
-                      for _ in range(host_slots)]
+        self.stats = None
 
     def run(self, reqs: List[Request], keep_scores: bool = False, abort_after_s: Optional[float] = None):
-        """Serve the trace.  ``abort_after_s``: stop early (remaining requests get latency +inf) once the oldest
-        queued request has waited that long -- an overloaded point of a saturation search."""
-        lat = np.full(len(reqs), np.nan)
-        sizes: List[int] = []
-        scores = {} if keep_scores else None
-        inflight: Deque = collections.deque()
-        free = collections.deque(range(len(self.slots)))
-        i, done = 0, 0
-        h_c, h_e, h_d = self.s_copy.cuda_stream, self.s_embed.cuda_stream, self.s_dense.cuda_stream
-        t_start = time.perf_counter() + 0.01
-        clock = lambda: time.perf_counter() - t_start
-        while done < len(reqs):
-            now = clock()
-            if abort_after_s is not None and len(self.batcher) and now - self.batcher.q[0].t_arrival > abort_after_s:
-                lat[np.isnan(lat)] = np.inf
-                break
-            while i < len(reqs) and reqs[i].t_arrival <= now:
-                if not self.batcher.submit(reqs[i]):
-                    lat[reqs[i].rid] = np.inf
-                    done += 1
-                i += 1
-            while inflight and inflight[0][1]["ev"].query():
-                batch, slot, si = inflight.popleft()
-                t_done = clock()
-                row = 0
-                for r in batch:
-                    lat[r.rid] = t_done - r.t_arrival
-                    if keep_scores:
-                        scores[r.rid] = slot["scores"][row:row + r.n_items].numpy().copy()
-                    row += r.n_items
-                done += len(batch)
-                free.append(si)
-            if free:
-                batch = self.batcher.poll(clock())
-                if batch:
-                    si = free.popleft()
-                    slot = self.slots[si]
-                    ids = np.concatenate([r.item_ids for r in batch])
-                    B = len(ids)
-                    nnz = self.pool.gather(ids, slot["off"], slot["idx"], slot["dense"])
-                    self.m.score_host_raw(slot["idx"].data_ptr(), slot["off"].data_ptr(), nnz, B,
-                                          slot["dense"].data_ptr(), slot["scores"].data_ptr(), h_c, h_e, h_d)
-                    slot["ev"].record(self.s_dense)
-                    inflight.append((batch, slot, si))
-                    sizes.append(B)
+        """Serve the trace; returns (latency [s] per request id, batch sizes, {rid: scores} or None).
+        ``abort_after_s``: stop early (remaining requests get latency +inf) once the oldest queued request has
+        waited that long -- an overloaded point of a saturation search."""
+        reqs = sorted(reqs, key=lambda r: r.rid)
+        N = len(reqs)
+        t = np.array([r.t_arrival for r in reqs], np.float64)
+        n = np.array([r.n_items for r in reqs], np.int32)
+        start = np.zeros(N + 1, np.int64)
+        start[1:] = np.cumsum(n)
+        ids = np.concatenate([np.asarray(r.item_ids, np.int32) for r in reqs]) if N else np.zeros(1, np.int32)
+        lat, sizes, scores = self.run_arrays(t, n, start, ids, keep_scores, abort_after_s)
+        out = None
+        if keep_scores:
+            out = {r.rid: scores[start[i]:start[i + 1]].copy() for i, r in enumerate(reqs)}
+        return lat, sizes, out
+
+    def run_arrays(self, t, n, start, ids, keep_scores: bool = False, abort_after_s: Optional[float] = None):
+        """The trace as flat arrays (t_arrival, n_items, item_start [N+1], item_ids): (latency, batch sizes,
+        scores [sum n] or None)."""
+        from ._cvr import cvr_serve_stats
+        t = np.ascontiguousarray(t, np.float64)
+        n = np.ascontiguousarray(n, np.int32)
+        start = np.ascontiguousarray(start, np.int64)
+        ids = np.ascontiguousarray(ids, np.int32) if len(ids) else np.zeros(1, np.int32)
+        N = len(t)
+        lat = np.zeros(N)
+        sizes = np.zeros(max(N, 1), np.int32)
+        scores = np.zeros(max(int(start[-1]), 1), np.float32) if keep_scores else None
+        nb = ctypes.c_int()
+        stats = cvr_serve_stats()
+        self.cfg.abort_after_s = abort_after_s or 0.0
         torch.cuda.synchronize()
-        return lat, np.array(sizes), scores
+        p = self.pool
+        st = lib().cvr_serve_trace(self.m.h, ctypes.byref(self.cfg), p.T, p.F, p.P, p.offsets.ctypes.data,
+                                   p.indices.ctypes.data, p.dense.ctypes.data, N, t.ctypes.data, n.ctypes.data,
+                                   start.ctypes.data, ids.ctypes.data, lat.ctypes.data,
+                                   scores.ctypes.data if keep_scores else None, sizes.ctypes.data, ctypes.byref(nb),
+                                   ctypes.byref(stats), self.s_copy.cuda_stream, self.s_embed.cuda_stream,
+                                   self.s_dense.cuda_stream)
+        if st:
+            self.m._check(st)
+        self.batcher.rejected = stats.rejected
+        self.stats = {"rejected": stats.rejected, "aborted": bool(stats.aborted), "items_served": stats.items_served,
+                      "host_dispatch_s": stats.host_dispatch_s, "wall_s": stats.wall_s}
+        return lat, sizes[:nb.value], scores

@@ -6,12 +6,12 @@ set -u
 OUT=gpurun_out
 mkdir -p $OUT
 CFG=${CFG:-c2}
-CMD="python bench.py --config $CFG --steps 5 --warmup 3 --no-cpu-baseline --no-e2e"
+CMD="python bench.py --config $CFG --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-serving"
 timeout 300 $CMD > $OUT/plain_$CFG.log 2>&1
 rc=$?
 echo "plain_exit=$rc"
 if [ $rc -ne 0 ]; then tail -20 $OUT/plain_$CFG.log; exit 1; fi
-KRE='regex:embed_bag|gemm_bf16|gemm_splitk|dense_f32|unpack|mha64|head_finalize'
+KRE='regex:embed_bag|gemm_bf16|dense_f32|unpack|mha64|head_finalize|set_call'
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KRE" --csv \
   --log-file $OUT/launches_$CFG.csv $CMD > $OUT/ncu_launches_$CFG.log 2>&1
 echo "ncu_launches_exit=$?"

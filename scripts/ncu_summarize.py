@@ -18,13 +18,14 @@ EPI = {0: "STORE", 1: "BIAS_RELU", 2: "CROSS", 3: "HEAD", 4: "BIAS", 5: "CROSS_F
 
 
 def role(name):
-    m = re.search(r"gemm_bf16_kernel<([\d, ]+)>", name)  # <BN, EPI, AR, CG, CN[, EW[, MB]]>
+    m = re.search(r"gemm_bf16_kernel<([\d, ]+)>", name)  # <BN, EPI, CG, EW>
     if m:
-        bn, epi, ar, cg, cn = [int(x) for x in m.group(1).split(",")][:5]
+        bn, epi, cg = [int(x) for x in m.group(1).split(",")][:3]
         # role names of config 2 (for c6: BIAS_RELU = projection / mask hidden / MLP, MASK = mask blocks)
         r = {(0,): "gemm_xV", (2,): "gemm_tU_cross", (1,): "gemm_mlp_relu", (3,): "gemm_mlp_head",
-             (9,): "gemm_mask_mul", (10,): "gemm_ens_qkv_attn"}.get((epi,), f"gemm_{EPI.get(epi, epi)}")
-        return f"{r} [BN={bn}{' pair' if cg == 2 else ''}{' cluster%d' % cn if cn > 1 else ''}]"
+             (9,): "gemm_mask_mul", (10,): "gemm_ens_qkv_attn", (5,): "gemm_tU_cross", (7,): "gemm_ens_ffn2_ln",
+             (8,): "gemm_mlp_head"}.get((epi,), f"gemm_{EPI.get(epi, epi)}")
+        return f"{r} [BN={bn}{' pair' if cg == 2 else ''}]"
     for k in ("embed_bag", "dense_f32", "unpack", "mha64", "head_finalize", "set_call"):
         if k in name:
             return k
@@ -53,7 +54,7 @@ tot = sum(v[1] for v in agg.values())
 out = os.path.join(ROOT, "profiles", f"{tag}_launches_{cfg}.csv")
 with open(out, "w") as f:
     f.write("# ncu launch list: gpu__time_duration.sum --clock-control none (serialised, cold cache: compare SHARES)\n")
-    f.write(f"# command: python bench.py --config {cfg} --steps 5 --warmup 3 --no-cpu-baseline --no-e2e (scripts/gpu_profile.sh)\n")
+    f.write(f"# command: python bench.py --config {cfg} --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-serving (scripts/gpu_profile.sh)\n")
     f.write("kernel, launches, avg_us, share_of_kernel_time\n")
     for k, (n, t) in agg.items():
         f.write(f"{k}, {n}, {t / n:.2f}, {t / tot:.3f}\n")
@@ -102,11 +103,10 @@ with open(out, "w") as f:
 print(open(out).read())
 tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 old = json.load(open(tp)) if os.path.exists(tp) else {}
-new = {("embed_bag_pool" if k == "embed_bag" else k): sum(v) / len(v) for k, v in traffic.items()}
-key = {"c2": "", "c4": "c4:", "c1": "c1:", "c6": "c6:"}.get(cfg, cfg + ":")
-for k, v in new.items():
-    old[key + k] = v
-old["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, mean over captured launches of the role "
-                "(keys prefixed by config except c2); ncu --set full replays with caches flushed (cold L2), so "
-                "L2-resident activations count as DRAM traffic here")
+if not isinstance(old.get(cfg, {}), dict) or "_note" not in old or "by_config" not in old.get("_format", ""):
+    old = {"_format": "by_config: {config: {kernel role: bytes per launch}}"}
+old[cfg] = {("embed_bag_pool" if k == "embed_bag" else k): sum(v) / len(v) for k, v in traffic.items()}
+old["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch, mean over the captured launches of the "
+                "role; ncu --set full replays with caches flushed (cold L2), so L2-resident activations count as DRAM "
+                "traffic here (tag %s)" % tag)
 json.dump(old, open(tp, "w"), indent=1)

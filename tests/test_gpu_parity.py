@@ -199,10 +199,10 @@ def _small(name):
 
 @pytest.mark.parametrize("name", ["c1", "c4", "c6"])
 def test_executor_graphs_every_backbone(name):
-    """The executor's per-slot graphs (one captured graph per stage and slot, the batch read from the per-call
-    block) on every backbone: batches of changing size through the same graphs are bit-identical to embed + dense,
-    only 2 x 2 graphs are captured, and the call block holds exactly the pointers / sizes of the last batch (P12:
-    what the kernels consumed)."""
+    """The executor's graphs (one captured graph per stage, slot and grid-size bucket, the batch read from the
+    per-call block) on every backbone: batches of changing size through the same graphs are bit-identical to embed +
+    dense, graphs are captured once per (stage, slot, bucket), and the call block holds exactly the pointers / sizes
+    of the last batch (P12: what the kernels consumed)."""
     cfg = _small(name)
     Bmax = 256 if name == "c1" else 384
     m, tabs, w = make_model(cfg, max_batch=Bmax, max_nnz=1 << 20)
@@ -224,7 +224,13 @@ def test_executor_graphs_every_backbone(name):
     assert (last["d_indices"], last["d_offsets"], last["nnz"], last["batch"]) == \
         (i.data_ptr(), o.data_ptr(), i.numel(), sizes[-1])
     assert last["d_scores"] == outs[-1].data_ptr()
-    assert last["graph_captures"] == 4
+    def bucket(b):  # grid-size bucket: next power of two >= 128, capped at max_batch (cvr_ctx::bucket_rows)
+        r = 128
+        while r < b and r < Bmax:
+            r *= 2
+        return min(r, Bmax)
+    # one graph per (stage, slot, bucket): embed + dense for every distinct (slot, bucket) seen, nothing more
+    assert last["graph_captures"] == 2 * len({(k % 2, bucket(b)) for k, b in enumerate(sizes)})
     m.close()
 
 

@@ -191,3 +191,36 @@ def test_saturation_fixed_cost_batching_raises_peak():
     _, n = cs.request_trace(1000.0, 2.0, seed=77)
     assert rows[0]["peak_qps"] <= 1.0 / (F + c * n.mean()) * 1.05
     assert rows[1]["ratio"] > 2.0, rows
+
+
+# ---- the native batcher (libcvr cvr_batcher_simulate / cvr_serve_trace) pinned to the same contract ---------------
+def test_native_batcher_spec_goldens():
+    """SPEC.md:639-641 on the native batcher (simulated clock, zero service time)."""
+    from paper_2605_29232_b200.serving import batcher_simulate
+    # passthrough: window 0, max 1 -> every request its own batch at its arrival
+    lat, bof, disp = batcher_simulate([0.000, 0.001, 0.002, 0.003, 0.004], [1] * 5, 0.0, max_items=1)
+    assert list(bof) == [0, 1, 2, 3, 4] and np.allclose(disp, [0, 0.001, 0.002, 0.003, 0.004])
+    # three requests inside one window -> one batch at t0 + window
+    lat, bof, disp = batcher_simulate([0.0, 0.0005, 0.0012], [1, 1, 1], 0.002, max_items=8)
+    assert list(bof) == [0, 0, 0] and disp[0] == 0.002
+    # cap 2 splits FIFO [2, 1]: the full batch leaves at once, the third at its window
+    lat, bof, disp = batcher_simulate([0.0, 0.0, 0.0], [1, 1, 1], 0.002, max_items=2)
+    assert list(bof) == [0, 0, 1] and list(disp) == [0.0, 0.002]
+    # oversized request and a full queue are rejected (latency +inf, batch -1)
+    lat, bof, disp = batcher_simulate([0.0, 0.0, 0.0, 0.0], [11, 1, 1, 1], 0.001, max_items=10, queue_capacity=2)
+    assert list(bof) == [-1, 0, 0, -1] and np.isinf(lat[0]) and np.isinf(lat[3])
+
+
+@pytest.mark.parametrize("window,max_requests", [(0.0, 1), (0.5e-3, 0), (2e-3, 0), (4e-3, 0)])
+def test_native_batcher_matches_python_on_traces(window, max_requests):
+    """The C++ batcher and serving.DynamicBatcher (via simulate_serving) give the same latency for every request of
+    a config-5 trace under a fixed + per-item service model (same rule, same clock arithmetic)."""
+    from paper_2605_29232_b200.serving import batcher_simulate, simulate_serving
+    t, n = cs.request_trace(20000.0, 0.3, seed=5)
+    F, c = 150e-6, 0.02e-6
+    ref = simulate_serving(t, n, lambda k: F + c * k, window, max_items=8192,
+                           max_requests=max_requests if max_requests else None)
+    lat, bof, disp = batcher_simulate(t, n, window, max_items=8192, max_requests=max_requests,
+                                      service_fixed_s=F, service_per_item_s=c)
+    assert (bof >= 0).all()
+    np.testing.assert_array_equal(lat, ref)
