@@ -31,8 +31,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--bounds-ms", type=float, nargs="+", default=[5.0, 10.0])
     ap.add_argument("--windows-ms", type=float, nargs="+", default=[0.1, 0.25, 0.5, 1.0, 2.0, 4.0, 8.0])
-    ap.add_argument("--duration", type=float, default=0.5)
-    ap.add_argument("--warmup", type=float, default=0.15)
+    ap.add_argument("--duration", type=float, default=1.5)
+    ap.add_argument("--warmup", type=float, default=0.2)
     ap.add_argument("--lo", type=float, default=500.0)
     ap.add_argument("--hi", type=float, default=4.0e6)
     ap.add_argument("--rel-eps", type=float, default=0.07)

@@ -174,6 +174,12 @@ int cvr_score(cvr_ctx* ctx, const int32_t* d_indices, const int32_t* d_offsets, 
               int batch, const float* d_dense, float* d_scores, cvr_stream_t s_embed,
               cvr_stream_t s_dense);
 
+/* Capture (without running anything) the executor graphs of every grid-size bucket up to max_rows, for both x0
+ * slots and both stages (and the keys-mode embed stage when every table has a hash vocab), so that no batch of a
+ * serving run pays a capture; the graphs read their batch from the call block at replay time.  Streams are only
+ * used to capture on (non-NULL).  CVR_E_ARG if max_rows is outside [1, max_batch]. */
+int cvr_warm_graphs(cvr_ctx* ctx, int max_rows, cvr_stream_t s_embed, cvr_stream_t s_dense);
+
 /* Host-fed variant (S1 + S2-S7 + S8): h_* are host buffers (pinned for async copies);
  * the H2D copies of this batch run on s_copy into double-buffered device staging,
  * then as cvr_score.  S8: when h_scores is page-locked (mapped) memory the head kernel stores
@@ -261,7 +267,8 @@ int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d
  * "epw" [2] epilogue warps per TMEM quadrant: 0 one, 1 up to 4 (one 64-column sub-tile each), 2 split only when a
  * CTA runs <= 2 tiles; "zero_copy_scores" [1] cvr_score_host stores the scores straight into page-locked h_scores;
  * config 4: "pair" [1] 2-CTA (cta_group::2) tiles, "ens_u_bn" [128] N tile of the DCN U GEMM, "ens_fused_attn" [1]
- * the QKV projection + attention as one GEMM (else QKV GEMM + mha64), "f32_tma_store" [1] the fp32 DCN-branch
+ * the QKV projection + attention as one GEMM (else QKV GEMM + mha64), "ens_attn_tc" [1] that GEMM's attention on
+ * tcgen05 (S = Q K^T, O = P V as UMMAs in TMEM; else mma.sync in the epilogue), "f32_tma_store" [1] the fp32 DCN-branch
  * output through staged TMA stores, "ens_xv_wave" [1] t = X V^T as one wave of 128 x 256 tiles; MaskNet:
  * "mask_grouped" [1] parallel blocks as one grouped GEMM.  Every variant is bit-identical to the default.  Unknown
  * key or bad value -> CVR_E_ARG. */

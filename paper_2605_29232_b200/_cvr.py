@@ -80,6 +80,7 @@ _SIGS = [
     ("cvr_embed", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp]),
     ("cvr_dense", ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp, _vp]),
     ("cvr_score", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp, _vp]),
+    ("cvr_warm_graphs", ctypes.c_int, [_vp, ctypes.c_int, _vp, _vp]),
     ("cvr_score_host", ctypes.c_int, [_vp, _vp, _vp, ctypes.c_int64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp]),
     ("cvr_get_status", ctypes.c_int, [_vp, _vp]),
     ("cvr_shard_buffer_bytes", ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t),
@@ -373,6 +374,10 @@ class CvrModel:
         self._check(self.L.cvr_score_host(self.h, _ptr(indices), _ptr(offsets), indices.numel(), batch, _ptr(dense),
                                           _ptr(scores), _stream(s_copy), _stream(s_embed), _stream(s_dense)))
         return scores
+
+    def warm_graphs(self, max_rows: int, s_embed, s_dense):
+        """cvr_warm_graphs: capture every executor graph up to max_rows (nothing runs)."""
+        self._check(self.L.cvr_warm_graphs(self.h, max_rows, _stream(s_embed), _stream(s_dense)))
 
     def status(self, stream=None) -> int:
         """Synchronise ``stream`` and return the sticky device status (raises on CUDA errors)."""

@@ -202,6 +202,12 @@ struct cvr_ctx {
   // 805 MB per layer at B = 8192, never reaches HBM).  Bit-identical to QKV GEMM + mha64; measured per layer
   // 381 us vs 257 + 247 (two epilogue groups; one group: 519 -- the attention warps' latency bounds each tile)
   bool ens_fused_attn = true;
+  // option "ens_attn_tc" [1]: the fused QKV + attention GEMM with the attention itself on tcgen05 (EPI_ATTN_TC:
+  // S = Q K^T and O = P V as UMMAs into the drained accumulator's TMEM columns, thread-per-row softmax from TMEM, P
+  // written back to TMEM as the A operand of P V, two groups of 4 epilogue warps on alternate tiles).  Measured on
+  // B200 at B = 8192: 340 us per launch vs 472 with the mma.sync core (0 = the mma.sync epilogue, EPI_ATTN); a first
+  // version with P staged in shared memory and one epilogue group ran 597 us
+  bool ens_attn_tc = true;
   bool ens_xv_wave = true;      // option "ens_xv_wave": config 4's t = X V^T as one wave of 128 x 256 tiles
   bool zero_copy_scores = true;  // option "zero_copy_scores": cvr_score_host writes scores into pinned h_scores
   int u_bn = 192;              // option "u_bn": N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64)
@@ -1261,11 +1267,12 @@ int do_dense_ensemble(cvr_ctx* c, const CUtensorMap* flat_x0, const CUtensorMap*
     if (c->ens_fused_attn && D == 64 * c->n_heads) {
       // one GEMM: each 128-token x 192 tile [q_h | k_h | v_h] (+ b) is attended in its epilogue, O -> cat[:, 64 h ..]
       // (the qkv tensor never reaches HBM; same bf16 roundings and attention core as qkv GEMM + mha64)
-      GemmArgs a3 = ga(tok_xl, &E.Wqkvh[l], BT, 3 * D, D, 192, EPI_ATTN);
+      GemmArgs a3 = ga(tok_xl, &E.Wqkvh[l], BT, 3 * D, D, 192, c->ens_attn_tc ? EPI_ATTN_TC : EPI_ATTN);
       a3.cta_pair = false;
       a3.bias = c->at<float>(E.off_bqkvh[l]);
       a3.out_bf16 = cat;
       a3.ld_x = D + c->ffn;
+      if (c->ens_attn_tc) a3.tmOut = &E.tm_cat;  // O: 128 x 64 boxes at cat[m0.., 64 h] (TMA store)
       if ((e = run_gemm(c, a3, K_ENS_QKV_ATTN, s)) != cudaSuccess) return c->cuda_fail(e, "ens qkv + attention");
     } else {
       GemmArgs a3 = ga(tok_xl, &E.Wqkv[l], BT, 3 * D, D, 256, EPI_BIAS);
@@ -1428,11 +1435,11 @@ int user_x0_maps(cvr_ctx* c, const void* d_x0, int batch, CUtensorMap* tm, CUten
 // per-call block, so the same graph serves every batch and batch size), or launch directly (graphs off, while
 // profiling, or inside a caller's own capture).
 template <typename F>
-int run_stage(cvr_ctx* c, int kind, int slot, int bucket, cudaStream_t s, F&& enqueue) {
+int run_stage(cvr_ctx* c, int kind, int slot, int bucket, cudaStream_t s, F&& enqueue, bool launch = true) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (!c->use_graphs || s == nullptr || c->prof_on || cudaStreamIsCapturing(s, &cs) != cudaSuccess ||
       cs != cudaStreamCaptureStatusNone)
-    return enqueue(s);
+    return launch ? enqueue(s) : CVR_OK;
   cudaGraphExec_t& ge = c->gexec[kind][slot][bucket];
   if (!ge) {
     const int64_t l0 = c->launches;
@@ -1457,6 +1464,7 @@ int run_stage(cvr_ctx* c, int kind, int slot, int bucket, cudaStream_t s, F&& en
     c->gkernels[kind][slot][bucket] = nk;
     ++c->graph_captures;
   }
+  if (!launch) return CVR_OK;  // (capture only: cvr_warm_graphs)
   cudaError_t e = cudaGraphLaunch(ge, s);
   if (e != cudaSuccess) return c->cuda_fail(e, "cudaGraphLaunch");
   c->launches += c->gkernels[kind][slot][bucket];
@@ -1612,6 +1620,44 @@ int score_impl(cvr_ctx* c, const int32_t* d_indices, const uint64_t* d_keys, con
 }  // namespace
 
 extern "C" {
+
+int cvr_warm_graphs(cvr_ctx* c, int max_rows, cvr_stream_t s_embed, cvr_stream_t s_dense) {
+  if (!c || !s_embed || !s_dense) return CVR_E_ARG;
+  int st = check_ready(c, true, true);
+  if (st) return st;
+  if (c->world != 1) return c->fail(CVR_E_STATE, "the executor is unsharded");
+  if (max_rows < 1 || max_rows > c->max_batch) return c->fail(CVR_E_ARG, "max_rows %d outside [1, %d]", max_rows, c->max_batch);
+  if (!c->use_graphs) return CVR_OK;
+  bool keys = true;
+  for (int t = 0; t < c->T; ++t) keys &= c->tvocab[t] > 0;
+  int last = 0;
+  c->bucket_rows(max_rows, &last);
+  for (int slot = 0; slot < 2 && !st; ++slot) {
+    void* x0 = c->ws + c->off_x0[slot];
+    c->call = c->at<CallArgs>(c->off_call[slot]);
+    const bool ens = c->backbone == CVR_ENSEMBLE;
+    const CUtensorMap* tm = (c->backbone == CVR_DCN_LOWRANK || c->backbone == CVR_MASKNET) ? &c->tm_x0slot[slot]
+                            : ens ? &c->ens.flat_x0[slot] : nullptr;
+    const CUtensorMap* tmt = ens ? &c->ens.tok_x0[slot] : nullptr;
+    for (int b = 0; b <= last && !st; ++b) {
+      const int rows = std::min<int64_t>((int64_t)128 << b, c->max_batch);
+      // the captured kernels read their batch from the slot's call block at execution time: placeholders here
+      st = run_stage(c, cvr_ctx::G_EMBED, slot, b, (cudaStream_t)s_embed, [&](cudaStream_t s) {
+        return do_embed(c, nullptr, nullptr, 0, rows, nullptr, x0, s, c->embed_bps_pipe, nullptr);
+      }, false);
+      if (!st && keys)
+        st = run_stage(c, cvr_ctx::G_EMBED_KEYS, slot, b, (cudaStream_t)s_embed, [&](cudaStream_t s) {
+          return do_embed(c, nullptr, nullptr, 0, rows, nullptr, x0, s, c->embed_bps_pipe,
+                          reinterpret_cast<const uint64_t*>(16));
+        }, false);
+      if (!st)
+        st = run_stage(c, cvr_ctx::G_DENSE, slot, b, (cudaStream_t)s_dense,
+                       [&](cudaStream_t s) { return do_dense(c, x0, tm, tmt, rows, nullptr, s); }, false);
+    }
+  }
+  c->call = nullptr;
+  return st;
+}
 
 int cvr_score(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, int64_t nnz, int batch,
               const float* d_dense, float* d_scores, cvr_stream_t s_embed, cvr_stream_t s_dense) {
@@ -2053,6 +2099,7 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
   if (!strcmp(key, "f32_tma_store")) return flag(c->f32_tma_store);
   if (!strcmp(key, "ens_xv_wave")) return flag(c->ens_xv_wave);
   if (!strcmp(key, "ens_fused_attn")) return flag(c->ens_fused_attn);
+  if (!strcmp(key, "ens_attn_tc")) return flag(c->ens_attn_tc);
   if (!strcmp(key, "mask_grouped")) return flag(c->mask_grouped);
   if (!strcmp(key, "zero_copy_scores")) {
     c->zero_copy_scores = value != 0;

@@ -110,8 +110,10 @@ enum Epi {
   EPI_SUM_LN = 7,        // bf16 LN_row(C + b + in_f32) * gamma + beta   (ensemble FFN2 + LN, BN == N)
   EPI_HEAD_PARTIAL = 8,  // fp32 partial[m][tile] = ReLU(C + b) . m over the tile's columns
   EPI_MASK = 9,          // bf16 (C + b) * x_l: MaskNet block, mask applied to x_l (tmXl), no residual
-  EPI_ATTN = 10          // config 4: the 128 x 192 tile [q_h | k_h | v_h] (+ b) of 2 examples' tokens -> attention of
+  EPI_ATTN = 10,         // config 4: the 128 x 192 tile [q_h | k_h | v_h] (+ b) of 2 examples' tokens -> attention of
                          // head h = N tile -> O (bf16) at out_bf16[token, 64 h ..] (row stride ld_x); BN = 192
+  EPI_ATTN_TC = 11       // the same on tcgen05: S = Q K^T and O = P V as UMMAs into the drained accumulator's TMEM
+                         // columns, softmax thread-per-row from TMEM; O TMA-stored through tmOut (box {64, 128})
 };
 
 struct GemmArgs {

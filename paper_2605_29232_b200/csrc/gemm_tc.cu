@@ -75,21 +75,26 @@ struct Cfg {
   // mainloop anyway) keeps the CTA at 7 warps, leaving registers for co-resident embedding CTAs
   // EPI_ATTN: 8 epilogue warps = 2 examples x 4 groups of 16 query rows (one attention warp each)
   static constexpr bool ATTN = EPI == EPI_ATTN;
+  // EPI_ATTN_TC: two groups of 4 epilogue warps (one per TMEM lane quadrant) take alternate tiles (group = the
+  // tile's accumulator), each with its own attention-MMA warp and its own Q | K | V staging [3][128 x 64] bf16 in the
+  // 128-byte-swizzled UMMA layout (Q doubles as the O staging of the TMA store); P never touches shared memory:
+  // the softmax writes it back into TMEM as the A operand of O = P V
+  static constexpr bool ATTN_TC = EPI == EPI_ATTN_TC;
   // ATTN: two groups of 8 epilogue warps take alternate tiles (accumulator a = group), each with its own staging,
   // so one tile's attention overlaps the next one's
   static constexpr int ATT_GROUPS = 2;
-  static constexpr int EPW = RING ? 3 : (ATTN ? 2 * ATT_GROUPS : (SPLIT ? (BN / 64 < EW ? BN / 64 : EW) : 1));
+  static constexpr int EPW = RING ? 3 : (ATTN ? 2 * ATT_GROUPS : (ATTN_TC ? 2 : (SPLIT ? (BN / 64 < EW ? BN / 64 : EW) : 1)));
   static constexpr int COLS_W = BN / EPW;           // columns per epilogue warp
   static constexpr int PRODUCER_B = 2 + 4 * EPW;
-  static constexpr int PRODUCER_E = PRODUCER_B + 1;  // EIN producer (RING only)
-  static constexpr int NT = 32 * (PRODUCER_B + (RING ? 2 : 1));
+  static constexpr int PRODUCER_E = PRODUCER_B + 1;  // EIN producer (RING) / attention-MMA warps (ATTN_TC: +0, +1)
+  static constexpr int NT = 32 * (PRODUCER_B + (RING ? 2 : (ATTN_TC ? 3 : 1)));
   static constexpr int OUT_BYTES = EpiTraits<EPI>::kSmemOut && !RING ? NSUB * SUB : 0;     // per buffer
   static constexpr int EIN_BYTES = EpiTraits<EPI>::kEin && !RING ? EpiTraits<EPI>::kEinTensors * NSUB * SUB : 0;  // per acc
   // EPI_ATTN staging: Q | K | V of a tile's 128 tokens, bf16, row stride ATT_LD (padded: conflict-free ldmatrix).
   // (An unpadded XOR-swizzled layout freed a third ring stage but measured slower: 469 vs 381 us per layer.)
   static constexpr int ATT_LD = 72;
   static constexpr int ATT_BUF = 3 * BM * ATT_LD * 2;
-  static constexpr int ATT_BYTES = ATTN ? ATT_GROUPS * ATT_BUF : 0;
+  static constexpr int ATT_BYTES = ATTN ? ATT_GROUPS * ATT_BUF : (ATTN_TC ? 2 * 3 * SUB : 0);  // TC: [group][Q K V]
   // EPI_CROSS_F32 with a tmOut map: fp32 32 x 32 chunks staged per epilogue warp (double-buffered) and TMA-stored
   // (coalesced) instead of per-thread row stores
   static constexpr int F32_NBUF = CG == 2 ? 2 : 1;  // (single-CTA tiles: the ring needs the room)
@@ -154,7 +159,8 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
   uint64_t* efull = tempty + 2;          // [3] epilogue input tiles (ring slots) landed
   uint64_t* eempty = efull + 3;          // [3] epilogue input tiles consumed (4 warps)
   uint64_t* sfull = eempty + 3;          // [4 warps][SLN_BUFS] EPI_SUM_LN fp32 input chunk landed
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sfull + 4 * 3);
+  uint64_t* abar = sfull + 4 * 3;        // [2 groups][4] EPI_ATTN_TC handshakes
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(abar + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // executor graphs: this batch's row count (and scores pointer) from the per-call block, else the launch's
@@ -181,13 +187,14 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], C::ATTN ? 4 * C::EPW / C::ATT_GROUPS : 4 * C::EPW * CG);  // every epilogue warp
+      ptx::mbar_init(&tempty[a], C::ATTN ? 4 * C::EPW / C::ATT_GROUPS : (C::ATTN_TC ? 4 : 4 * C::EPW * CG));
                                                                                            // (ATTN: of one group)
     }
     for (int e = 0; e < 3; ++e) {
       ptx::mbar_init(&efull[e], 1);
       ptx::mbar_init(&eempty[e], 4);
     }
+    for (int i = 0; i < 8; ++i) ptx::mbar_init(&abar[i], 1);  // ATTN_TC: [group][qkv staged, S, P staged, O]
     for (int i = 0; i < 4 * 3; ++i) ptx::mbar_init(&sfull[i], 1);
     ptx::fence_barrier_init();
   }
@@ -281,8 +288,8 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
         }
       }
     }
-  } else if (warp == C::PRODUCER_E) {
-    if constexpr (C::RING) {  // ================= EIN producer: (x0, x_l) 64-column sub-tile j -> slot j
+  } else if (warp == C::PRODUCER_E && !C::ATTN_TC) {
+    if constexpr (C::RING) {    } else if constexpr (C::RING) {  // ================= EIN producer: (x0, x_l) 64-column sub-tile j -> slot j
       if (lane == 0) {
         int it = 0;
         for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
@@ -302,6 +309,28 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
             ptx::tma_load_2d(xld, &tmXl, &efull[j], n0 + j * 64, m0);
           }
         }
+      }
+    }
+  } else if (C::ATTN_TC && warp >= C::PRODUCER_E) {
+    if (lane == 0) {  // ================= attention MMAs of group grp's tiles (the tiles on accumulator grp)
+      const int grp = warp - C::PRODUCER_E;
+      const uint32_t sq = ptx::smem_u32(sOut + grp * 3 * C::SUB), sk = sq + C::SUB, sv = sq + 2 * C::SUB;
+      const uint32_t acc = tmem + grp * BN;  // S in [0, 128), P (bf16 pairs) in [0, 64), O in [128, 192)
+      constexpr uint32_t id_s = ptx::idesc_bf16_f32(128, 128), id_o = ptx::idesc_bf16_f32_bmn(128, 64);
+      int j = 0;  // this group's tile count (barrier phase)
+      for (int tile = t_begin + grp * t_step; tile < t_end; tile += 2 * t_step, ++j) {
+        ptx::mbar_wait(&abar[grp * 4 + 0], j & 1);  // Q, K, V staged
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 4; ++k)  // S = Q K^T over dh = 64: both examples' 128 x 128 (cross blocks unused)
+          ptx::umma_bf16_ss(acc, ptx::sdesc_kmajor_sw128(sq) + 2 * k, ptx::sdesc_kmajor_sw128(sk) + 2 * k, id_s, k);
+        ptx::umma_commit(&abar[grp * 4 + 1]);
+        ptx::mbar_wait(&abar[grp * 4 + 2], j & 1);  // P in TMEM (block diagonal over the 128 keys)
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < 8; ++k)  // O = P V: A = P from TMEM (8 columns per 16 keys), V MN-major (2048 B per 16 keys)
+          ptx::umma_bf16_ts(acc + 128, acc + 8 * k, ptx::sdesc_kmajor_sw128(sv) + 128 * k, id_o, k);
+        ptx::umma_commit(&abar[grp * 4 + 3]);
       }
     }
   } else if (warp == 1) {
@@ -348,6 +377,9 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
       const int a = it & 1;
       if constexpr (C::ATTN) {
         if (a != (part >> 1)) continue;  // the other group's tile (its accumulator index)
+      }
+      if constexpr (C::ATTN_TC) {
+        if (a != part) continue;  // the other group's tile
       }
       if constexpr (EPI == EPI_SUM_LN) {  // the tile's first fp32 input chunks (independent of the accumulator)
         if (lane == 0) {
@@ -419,6 +451,100 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
           ptx::mbar_arrive(&eempty[j]);
         }
         __syncwarp();
+      } else if constexpr (C::ATTN_TC) {
+        // ---- fused QKV projection + attention on tcgen05 (config 4, SURVEY.md §8(a) S5', A20): rows [m0, m0 + 128) =
+        // two examples' 64 tokens, columns [q_h | k_h | v_h] of head h = tn.  Same roundings as EPI_ATTN / mha64: q, k,
+        // v + bias rounded to bf16, S = Q K^T fp32, softmax(S / 8) fp32 (exact scale), P rounded to bf16, O fp32 -> bf16.
+        const int grp = a;  // this warp's group owns the tiles on accumulator `grp`
+        uint64_t* ab = abar + grp * 4;
+        const int j = it >> 1;  // the group's tile count (barrier phase)
+        const uint32_t sq = ptx::smem_u32(sOut + grp * 3 * C::SUB);
+        const uint32_t acc = tmem + a * BN + ((uint32_t)(q * 32) << 16);
+        const bool lead = q == 0 && lane == 0;
+        // (0) the previous O store of this group has read the staging (Q doubles as O)
+        if (lead) ptx::bulk_wait_read<0>();
+        ptx::named_bar_sync(1 + grp, 32 * 4);
+        // (1) accumulator + bias -> bf16 Q | K | V rows
+#pragma unroll 1
+        for (int c = 0; c < 192; c += 32) {
+          float v[32];
+          ld32_tmem(trow + c, v);
+          const float4* b4 = reinterpret_cast<const float4*>(g.bias + n0 + c);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float4 bb = __ldg(b4 + u);
+            v[4 * u] += bb.x;
+            v[4 * u + 1] += bb.y;
+            v[4 * u + 2] += bb.z;
+            v[4 * u + 3] += bb.w;
+          }
+          sts32_bf16(sq + (c >> 6) * C::SUB, r, (c & 63) >> 3, v);
+        }
+        ptx::fence_async_smem();  // generic-proxy staging writes -> visible to the tensor core's reads
+        ptx::tc_fence_before();
+        ptx::named_bar_sync(1 + grp, 32 * 4);
+        if (lead) ptx::mbar_arrive(&ab[0]);
+        // (2) softmax of this row over its example's 64 keys (columns [64 e, 64 e + 64) of S); P (bf16) back into TMEM
+        // columns [0, 64) as pairs (keys 2i, 2i + 1 in column i), the other example's 32 columns zero
+        ptx::mbar_wait(&ab[1], j & 1);
+        ptx::tc_fence_after();
+        {
+          const int e = r >> 6;
+          float s0[32], s1[32];
+          ld32_tmem(acc + 64 * e, s0);
+          ld32_tmem(acc + 64 * e + 32, s1);
+          float mx = -INFINITY;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            s0[i] *= 0.125f;
+            s1[i] *= 0.125f;
+            mx = fmaxf(mx, fmaxf(s0[i], s1[i]));
+          }
+          float sum = 0.f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            s0[i] = expf(s0[i] - mx);
+            s1[i] = expf(s1[i] - mx);
+            sum += s0[i];
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) sum += s1[i];
+          const float inv = 1.f / sum;
+          uint32_t pk[16], z[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            pk[i] = ptx::pack_bf16(s0[2 * i] * inv, s0[2 * i + 1] * inv);
+            z[i] = 0u;
+          }
+          ptx::tmem_st_32x32b_x16(acc + 32 * e, pk);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[i] = ptx::pack_bf16(s1[2 * i] * inv, s1[2 * i + 1] * inv);
+          ptx::tmem_st_32x32b_x16(acc + 32 * e + 16, pk);
+          ptx::tmem_st_32x32b_x16(acc + 32 * (1 - e), z);
+          ptx::tmem_st_32x32b_x16(acc + 32 * (1 - e) + 16, z);
+          ptx::tmem_wait_st();
+        }
+        ptx::tc_fence_before();
+        ptx::named_bar_sync(1 + grp, 32 * 4);
+        if (lead) ptx::mbar_arrive(&ab[2]);
+        // (3) O rows -> bf16 staging (over Q) -> one TMA store of the 128 x 64 box at cat[m0.., 64 h]
+        ptx::mbar_wait(&ab[3], j & 1);
+        ptx::tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 64; c += 32) {
+          float o[32];
+          ld32_tmem(acc + 128 + c, o);
+          sts32_bf16(sq, r, c >> 3, o);
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tempty[a]);  // accumulator a (QKV, S, P, O columns) free for its next tile
+        ptx::fence_async_smem();
+        ptx::named_bar_sync(1 + grp, 32 * 4);
+        if (lead) {
+          ptx::tma_store_2d(&tmOut, sOut + grp * 3 * C::SUB, tn * 64, m0);
+          ptx::bulk_commit();
+        }
       } else if constexpr (C::ATTN) {
         // ---- fused QKV projection + attention (config 4, SURVEY.md §8(a) S5', A20): this tile is rows [m0, m0+128)
         // = two examples' 64 tokens, columns [q_h | k_h | v_h] of head h = tn (weights repacked head-major at load)
@@ -607,7 +733,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
         }
       }
       // accumulator (and epilogue inputs) consumed: hand them back (RING / ATTN warps did so themselves)
-      if constexpr (!C::RING && !C::ATTN) {
+      if constexpr (!C::RING && !C::ATTN && !C::ATTN_TC) {
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -645,7 +771,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
         }
       }
     }
-    if constexpr (T::kSmemOut || C::RING || EPI == EPI_CROSS_F32) {
+    if constexpr (T::kSmemOut || C::RING || EPI == EPI_CROSS_F32 || C::ATTN_TC) {
       if (lane == 0) ptx::bulk_wait<0>();
     }
     if (warp == 2 && lane == 0) stamp(g.dbg, 5);
@@ -737,6 +863,10 @@ cudaError_t launch_gemm_bf16(const GemmArgs& g, cudaStream_t s) {
   if (g.epi == EPI_ATTN) {
     if (g.BN != 192 || g.N % 192 || g.cta_pair || !g.out_bf16 || !g.bias || g.ld_x % 8) return cudaErrorInvalidValue;
     return launch_t<192, EPI_ATTN>(g, s);
+  }
+  if (g.epi == EPI_ATTN_TC) {
+    if (g.BN != 192 || g.N % 192 || g.cta_pair || !g.tmOut || !g.bias) return cudaErrorInvalidValue;
+    return launch_t<192, EPI_ATTN_TC>(g, s);
   }
 #define CVR_CASE(BN_, EPI_) \
   if (g.BN == BN_ && g.epi == EPI_) return g.cta_pair ? launch_t<BN_, EPI_, 2>(g, s) : launch_t<BN_, EPI_>(g, s);

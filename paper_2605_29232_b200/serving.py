@@ -253,6 +253,8 @@ class Server:
         self.s_copy, self.s_embed = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         self.s_dense = torch.cuda.Stream(dev, priority=-1)
         self.stats = None
+        if use_graphs:  # capture every grid-size bucket's graphs now: no batch of a run pays a capture
+            model.warm_graphs(max_items, self.s_embed, self.s_dense)
 
     def run(self, reqs: List[Request], keep_scores: bool = False, abort_after_s: Optional[float] = None):
         """Serve the trace; returns (latency [s] per request id, batch sizes, {rid: scores} or None).

@@ -31,6 +31,23 @@ for rep in range(3):
         b.record(s); torch.cuda.synchronize()
         res[i].append(a.elapsed_time(b) / K * 1e3)
         for k in st:  # restore defaults
-            m.set_option(k, {"pdl": 1, "graphs": 1, "ens_u_bn": 128, "pair": 1, "u_bn": 192, "xv_bn": 0, "epw": 2}.get(k, 1))
+            m.set_option(k, {"pdl": 1, "graphs": 1, "ens_u_bn": 128, "pair": 1, "u_bn": 192, "xv_bn": 0, "epw": 2,
+                             "ens_attn_tc": 1}.get(k, 1))
+roles = [r for r in os.environ.get("ROLES", "").split(",") if r]
 for i, st in enumerate(settings):
-    print(json.dumps({"setting": st, "us_per_dense": [round(x, 2) for x in res[i]], "min": round(min(res[i]), 2)}))
+    out = {"setting": st, "us_per_dense": [round(x, 2) for x in res[i]], "min": round(min(res[i]), 2)}
+    for k, v in st.items():
+        m.set_option(k, v)
+    m.dense(x0, B, sc, stream=s)
+    for role in roles:  # per-launch time of one GEMM role in a PDL chain of its own launches (cvr_repeat_kernel)
+        n = m.repeat_kernel(role, 4, x0, B, stream=s)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        for _ in range(3):
+            m.repeat_kernel(role, 4, x0, B, stream=s)
+        b.record(s); torch.cuda.synchronize()
+        out[role + "_us"] = round(a.elapsed_time(b) * 1e3 / (3 * n), 2)
+    for k in st:
+        m.set_option(k, {"ens_attn_tc": 1}.get(k, 1))
+    print(json.dumps(out))

@@ -1,6 +1,7 @@
-"""Serving on the GPU (config 5 machinery): a short open-loop run through DynamicBatcher + host batch
-assembly + cvr_score_host; every served score must be bit-identical to scoring the same request alone
-(batching transparency, SPEC.md:672 / SURVEY.md P10), and every request must complete."""
+"""Serving on the GPU (config 5 machinery): a short open-loop run through the native serving loop (C++ batcher +
+host batch assembly + cvr_score_host, libcvr cvr_serve_trace); every served score must be bit-identical to scoring
+the same request alone (batching transparency, SPEC.md:672 / SURVEY.md P10), every request must complete, and no
+executor graph is captured during the run (all grid-size buckets were captured up front by cvr_warm_graphs)."""
 import numpy as np
 import pytest
 import torch
@@ -25,7 +26,11 @@ def test_served_scores_equal_offline():
     trace = cs.make_requests(4000.0, 0.25, 4096, seed=77)
     reqs = [Request(i, t, len(ids), ids) for i, (t, ids) in enumerate(trace)]
     srv = Server(m, view, max_items=2048, window_s=0.002, max_nnz=2048 * 26 * 16)
+    captured = m.call_info(0)["graph_captures"]
+    assert captured == 2 * 2 * 5          # 2 slots x (embed, dense) x buckets 128 .. 2048
     lat, sizes, scores = srv.run(reqs, keep_scores=True)
+    assert m.call_info(0)["graph_captures"] == captured
+    assert srv.stats["rejected"] == 0 and not srv.stats["aborted"]
     assert np.all(np.isfinite(lat)) and sizes.sum() == sum(r.n_items for r in reqs)
     assert sizes.max() <= 2048
     for r in reqs[:: max(1, len(reqs) // 12)]:
