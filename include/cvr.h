@@ -331,6 +331,8 @@ typedef struct {
   int64_t items_served;
   double host_dispatch_s; /* host time spent assembling + enqueueing batches                                  */
   double wall_s;          /* from the trace's time origin to the last completion                              */
+  double max_dispatch_s;  /* the longest single batch assembly + enqueue                                     */
+  int64_t loop_gaps_1ms;  /* polling-loop iterations that took > 1 ms (the host thread was held up)           */
 } cvr_serve_stats;
 
 /* Serve an open-loop trace on ONE host thread: request r arrives at t_arrival[r] seconds (non-decreasing; the

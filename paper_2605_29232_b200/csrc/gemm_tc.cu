@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
       }
     }
   } else if (warp == C::PRODUCER_E && !C::ATTN_TC) {
-    if constexpr (C::RING) {    } else if constexpr (C::RING) {  // ================= EIN producer: (x0, x_l) 64-column sub-tile j -> slot j
+    if constexpr (C::RING) {  // ================= EIN producer: (x0, x_l) 64-column sub-tile j -> slot j
       if (lane == 0) {
         int it = 0;
         for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {

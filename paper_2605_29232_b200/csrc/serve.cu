@@ -164,11 +164,13 @@ int cvr_serve_trace(cvr_ctx* ctx, const cvr_serve_config* cfg, int n_tables, int
   const auto t0 = clk::now() + std::chrono::milliseconds(10);
   auto now_s = [&]() { return std::chrono::duration<double>(clk::now() - t0).count(); };
   int i = 0, done = 0, nb = 0, st = CVR_OK;
-  double busy_host = 0.0;
-  int64_t items_served = 0;
+  double busy_host = 0.0, max_dispatch = 0.0, last_iter = -1.0;
+  int64_t items_served = 0, gaps = 0;
   bool aborted = false;
   while (done < n_req) {
     double now = now_s();
+    if (last_iter >= 0.0 && now - last_iter > 1e-3) ++gaps;
+    last_iter = now;
     if (cfg->abort_after_s > 0 && !b.q.empty() && now - t_arrival[b.q.front()] > cfg->abort_after_s) {
       aborted = true;  // overloaded: the oldest request has waited too long -- stop this point
       break;
@@ -218,7 +220,10 @@ int cvr_serve_trace(cvr_ctx* ctx, const cvr_serve_config* cfg, int n_tables, int
       batch_sizes[nb++] = (int32_t)ids.size();
       items_served += (int64_t)ids.size();
       inflight.push_back(s);
-      busy_host += std::chrono::duration<double>(clk::now() - h0).count();
+      const double dt = std::chrono::duration<double>(clk::now() - h0).count();
+      busy_host += dt;
+      max_dispatch = std::max(max_dispatch, dt);
+      last_iter = now_s();
       continue;
     }
     if (i >= n_req && b.q.empty() && inflight.empty()) break;
@@ -232,6 +237,8 @@ int cvr_serve_trace(cvr_ctx* ctx, const cvr_serve_config* cfg, int n_tables, int
   stats->items_served = items_served;
   stats->host_dispatch_s = busy_host;
   stats->wall_s = now_s();
+  stats->max_dispatch_s = max_dispatch;
+  stats->loop_gaps_1ms = gaps;
   release();
   return st;
 }

@@ -36,13 +36,17 @@ for B in (68, 512, 4096):
     t_host = (time.perf_counter() - t0) / n
     torch.cuda.synchronize()
     print(json.dumps({"B": B, "device_us_per_batch": e0.elapsed_time(e1) / n * 1e3, "host_enqueue_us": t_host * 1e6}), flush=True)
-for qps in (2000.0, 4000.0, 6000.0, 10000.0):
-    t, nn, start, ids = cs.make_requests_flat(qps, 2.0, pool_n)
-    srv = Server(m, view, max_items=8192, window_s=0.0, max_nnz=max_nnz, max_requests=1)
+for window, qps, mr in [(0.0, 2000.0, 1), (0.0, 10000.0, 1), (0.5e-3, 500.0, 0), (4e-3, 500.0, 0), (0.5e-3, 500.0, 0),
+                        (4e-3, 500.0, 0), (1e-3, 200000.0, 0), (1e-3, 300000.0, 0)]:
+    t, nn, start, ids = cs.make_requests_flat(qps, 3.0 if qps < 1e4 else 1.0, pool_n)
+    srv = Server(m, view, max_items=8192, window_s=window, max_nnz=max_nnz, max_requests=mr or None)
     lat, sizes, _ = srv.run_arrays(t, nn, start, ids, abort_after_s=0.05)
     meas = t >= 0.3
     st = srv.stats
-    print(json.dumps({"qps": qps, "p99_ms": float(nearest_rank(lat[meas], 99)) * 1e3,
-                      "p50_ms": float(nearest_rank(lat[meas], 50)) * 1e3, "batches": int(len(sizes)),
-                      "host_dispatch_us_per_batch": st["host_dispatch_s"] / max(1, len(sizes)) * 1e6,
-                      "aborted": st["aborted"], "wall_s": st["wall_s"]}), flush=True)
+    L = lat[meas]
+    worst = np.argsort(-np.where(np.isfinite(lat), lat, 1e9))[:5]
+    print(json.dumps({"window_ms": window * 1e3, "qps": qps, "p50_ms": float(nearest_rank(L, 50)) * 1e3,
+                      "p99_ms": float(nearest_rank(L, 99)) * 1e3, "max_ms": float(np.max(L)) * 1e3,
+                      "batches": int(len(sizes)), "host_dispatch_us_per_batch": st["host_dispatch_s"] / max(1, len(sizes)) * 1e6,
+                      "max_dispatch_ms": st["max_dispatch_s"] * 1e3, "loop_gaps_1ms": st["loop_gaps_1ms"],
+                      "aborted": st["aborted"], "worst_at_s": [round(float(t[i]), 4) for i in worst]}), flush=True)

@@ -343,3 +343,25 @@ def test_c2_api_error_paths(c2):
     assert torch.all(sc == -1.0)
     assert m.status() == 0
     assert torch.equal(m.dense(x0, 64), s_before)
+
+
+def test_c3_rank_slice_dense_stage_vs_oracle():
+    """The dense stage of one c3 rank at N = 8 (W = 12,864, B/N = 8,192 rows: many tiles per persistent CTA on every
+    GEMM) against the oracle on a sample of 64 rows; synthetic x0 (the dense stage needs no tables)."""
+    from paper_2605_29232_b200 import CvrModel
+    cfg = cs.C3
+    B = 8192
+    w = cs.make_weights(cfg)
+    m = CvrModel(cfg, max_batch=B, max_nnz=1 << 12)
+    m.load_weights({k: v.cuda() for k, v in w.items()})
+    x0 = m.new_x0(B).zero_()
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x0[:, :cfg.width] = (torch.randn(B, cfg.width, device="cuda", generator=g) * 0.3).to(x0.dtype)
+    s = m.dense(x0, B)
+    assert m.status() == 0
+    sel = np.random.default_rng(5).choice(B, 64, replace=False)
+    xs = x0[torch.from_numpy(sel).cuda(), :cfg.width].double().cpu().numpy()
+    ref = O.dense_forward(cfg, {k: O.to_f64(v) for k, v in w.items()}, xs)["scores"]
+    err = np.abs(s[torch.from_numpy(sel).cuda()].double().cpu().numpy() - ref)
+    m.close()
+    assert err.max() <= TOL_BF16, err.max()
