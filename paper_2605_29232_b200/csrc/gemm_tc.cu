@@ -89,7 +89,11 @@ struct Cfg {
   static constexpr int PRODUCER_E = PRODUCER_B + 1;  // EIN producer (RING) / attention-MMA warps (ATTN_TC: +0, +1)
   static constexpr int NT = 32 * (PRODUCER_B + (RING ? 2 : (ATTN_TC ? 3 : 1)));
   static constexpr int OUT_BYTES = EpiTraits<EPI>::kSmemOut && !RING ? NSUB * SUB : 0;     // per buffer
-  static constexpr int EIN_BYTES = EpiTraits<EPI>::kEin && !RING ? EpiTraits<EPI>::kEinTensors * NSUB * SUB : 0;  // per acc
+  static constexpr int EIN_BYTES = EpiTraits<EPI>::kEin && !RING ? EpiTraits<EPI>::kEinTensors * NSUB * SUB : 0;  // per buf
+  // EIN buffers: 2 (one per accumulator) by default; config 4's DCN U GEMM (fp32 output, 2-CTA 128-wide tiles) keeps
+  // ONE, which frees three more operand ring stages (2 -> 5) -- its B producer then issues a tile's x0 / x_l loads
+  // after the tile's weight k-blocks, once the previous tile's epilogue has released the buffer
+  static constexpr int EIN_NBUF = EPI == EPI_CROSS_F32 ? 1 : 2;
   // EPI_ATTN staging: Q | K | V of a tile's 128 tokens, bf16, row stride ATT_LD (padded: conflict-free ldmatrix).
   // (An unpadded XOR-swizzled layout freed a third ring stage but measured slower: 469 vs 381 us per layer.)
   static constexpr int ATT_LD = 72;
@@ -102,7 +106,7 @@ struct Cfg {
   static constexpr int F32_BYTES = EPI == EPI_CROSS_F32 ? 4 * EPW * F32_NBUF * 32 * 32 * 4
                                   : (EPI == EPI_SUM_LN ? 4 * EPW * SLN_BUFS * 32 * 32 * 4 : 0);  // SUM_LN input ring
   static constexpr int EPI_BYTES =
-      OUT_BUFS * OUT_BYTES + 2 * EIN_BYTES + (RING ? RING_SLOTS * 2 * SUB : 0) + ATT_BYTES + F32_BYTES;
+      OUT_BUFS * OUT_BYTES + EIN_NBUF * EIN_BYTES + (RING ? RING_SLOTS * 2 * SUB : 0) + ATT_BYTES + F32_BYTES;
   static constexpr int BAR_BYTES = 512;
   // EPI_HEAD with a split epilogue: the EPW warps' partial dot products per row ([EPW][BM] fp32)
   static constexpr int Z_BYTES = EPI == EPI_HEAD ? EPW * BM * 4 : 0;
@@ -256,22 +260,24 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
         // [g * K, (g + 1) * K) of A and the epilogue input at column n0 - g * group_n
         const int grp = (EPI == EPI_MASK && g.group_n > 0) ? n0 / g.group_n : 0;
         const int a_k0 = grp * K, e_n0 = n0 - grp * (EPI == EPI_MASK ? g.group_n : 0);
-        if constexpr (T::kEin && !C::RING) {
-          if (!roleA) {
-            const int a = it & 1;
-            if (it >= 2) ptx::mbar_wait(&eempty[a], ((it >> 1) - 1) & 1);
-            ptx::mbar_arrive_expect_tx(&efull[a], C::EIN_BYTES);
-            uint8_t* base = sEin + a * C::EIN_BYTES;
+        auto issue_ein = [&]() {  // this tile's epilogue inputs (x0 / x_l tiles) into EIN buffer it % EIN_NBUF
+          const int a = it % C::EIN_NBUF;
+          if (it >= C::EIN_NBUF) ptx::mbar_wait(&eempty[a], ((it / C::EIN_NBUF) - 1) & 1);
+          ptx::mbar_arrive_expect_tx(&efull[a], C::EIN_BYTES);
+          uint8_t* base = sEin + a * C::EIN_BYTES;
 #pragma unroll
-            for (int j = 0; j < C::NSUB; ++j) {
-              if constexpr (EPI == EPI_MASK) {
-                ptx::tma_load_2d(base + j * C::SUB, &tmXl, &efull[a], e_n0 + j * 64, m0);
-              } else {
-                ptx::tma_load_2d(base + j * C::SUB, &tmX0, &efull[a], n0 + j * 64, m0);
-                ptx::tma_load_2d(base + (C::NSUB + j) * C::SUB, &tmXl, &efull[a], n0 + j * 64, m0);
-              }
+          for (int j = 0; j < C::NSUB; ++j) {
+            if constexpr (EPI == EPI_MASK) {
+              ptx::tma_load_2d(base + j * C::SUB, &tmXl, &efull[a], e_n0 + j * 64, m0);
+            } else {
+              ptx::tma_load_2d(base + j * C::SUB, &tmX0, &efull[a], n0 + j * 64, m0);
+              ptx::tma_load_2d(base + (C::NSUB + j) * C::SUB, &tmXl, &efull[a], n0 + j * 64, m0);
             }
           }
+        };
+        (void)issue_ein;
+        if constexpr (T::kEin && !C::RING && C::EIN_NBUF == 2) {
+          if (!roleA) issue_ein();
         }
         for (int kb = 0; kb < nk; ++kb, ++gk) {
           const int s = gk % C::STAGES;
@@ -285,6 +291,9 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
             ptx::mbar_arrive_expect_tx(&full[s], C::A_BYTES);
             ptx::tma_load_2d(sA + s * C::A_BYTES, &tmA, &full[s], a_k0 + kb * BK, m0);
           }
+        }
+        if constexpr (T::kEin && !C::RING && C::EIN_NBUF == 1) {
+          if (!roleA) issue_ein();  // (single EIN buffer: after the tile's weight k-blocks, see Cfg::EIN_NBUF)
         }
       }
     }
@@ -388,7 +397,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
           for (int i = 0; i < C::SLN_BUFS && 32 * i < BN; ++i) {
             const int b = (sln_k + i) % C::SLN_BUFS;
             ptx::mbar_arrive_expect_tx(&sfull[wq * 3 + b], 4096);
-            ptx::tma_load_2d(sEin + 2 * C::EIN_BYTES + (wq * C::SLN_BUFS + b) * 4096, &tmX0, &sfull[wq * 3 + b],
+            ptx::tma_load_2d(sEin + C::EIN_NBUF * C::EIN_BYTES + (wq * C::SLN_BUFS + b) * 4096, &tmX0, &sfull[wq * 3 + b],
                              n0 + 32 * i, m0 + q * 32);
           }
         }
@@ -398,8 +407,8 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
       ptx::tc_fence_after();
       const uint32_t trow = tmem + a * BN + ((uint32_t)(q * 32) << 16);
       const uint32_t out_base = ptx::smem_u32(sOut + (C::OUT_BUFS == 2 ? a : 0) * C::OUT_BYTES);
-      const uint32_t ein_base = ptx::smem_u32(sEin + a * C::EIN_BYTES);
-      if constexpr (T::kEin && !C::RING) ptx::mbar_wait(&efull[a], (it >> 1) & 1);
+      const uint32_t ein_base = ptx::smem_u32(sEin + (it % C::EIN_NBUF) * C::EIN_BYTES);
+      if constexpr (T::kEin && !C::RING) ptx::mbar_wait(&efull[it % C::EIN_NBUF], (it / C::EIN_NBUF) & 1);
       if constexpr (T::kSmemOut && !C::RING) {
         // the TMA store that last read this staging buffer must have finished reading it
         if (lane == 0) {
@@ -608,7 +617,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
           float v[32], x[32];
           ld32_tmem(trow + c, v);
           ptx::mbar_wait(&sfull[wq * 3 + b], (k / C::SLN_BUFS) & 1);
-          const uint32_t xt = ptx::smem_u32(sEin + 2 * C::EIN_BYTES + (wq * C::SLN_BUFS + b) * 4096);
+          const uint32_t xt = ptx::smem_u32(sEin + C::EIN_NBUF * C::EIN_BYTES + (wq * C::SLN_BUFS + b) * 4096);
 #pragma unroll
           for (int u = 0; u < 8; ++u) {
             const uint4 w4 = lds128(xt + lane * 128 + ((u ^ (lane & 7)) << 4));
@@ -621,7 +630,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
           if (lane == 0 && c + 32 * C::SLN_BUFS < BN) {  // refill this buffer with chunk c + SLN_BUFS of the tile
             ptx::fence_async_smem();
             ptx::mbar_arrive_expect_tx(&sfull[wq * 3 + b], 4096);
-            ptx::tma_load_2d(sEin + 2 * C::EIN_BYTES + (wq * C::SLN_BUFS + b) * 4096, &tmX0, &sfull[wq * 3 + b],
+            ptx::tma_load_2d(sEin + C::EIN_NBUF * C::EIN_BYTES + (wq * C::SLN_BUFS + b) * 4096, &tmX0, &sfull[wq * 3 + b],
                              n0 + c + 32 * C::SLN_BUFS, m0 + q * 32);
           }
 #pragma unroll
@@ -708,7 +717,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
               if (g.tmOut) {  // (the launch passed a store map: use its kernel-parameter copy)
                 // stage this warp's 32 rows x 32 columns (swizzled 16-byte chunks), one TMA store per chunk
                 const int buf = (c >> 5) % C::F32_NBUF;
-                uint8_t* sb = sEin + 2 * C::EIN_BYTES + ((warp - 2) * C::F32_NBUF + buf) * 4096;
+                uint8_t* sb = sEin + C::EIN_NBUF * C::EIN_BYTES + ((warp - 2) * C::F32_NBUF + buf) * 4096;
                 if (lane == 0) ptx::bulk_wait_read<C::F32_NBUF - 1>();  // the last store from this buffer read it
                 __syncwarp();
                 const uint32_t sbu = ptx::smem_u32(sb);
@@ -739,7 +748,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
         if (lane == 0) {
           if constexpr (CG == 2) ptx::mbar_arrive_leader(&tempty[a]);
           else ptx::mbar_arrive(&tempty[a]);
-          if constexpr (T::kEin) ptx::mbar_arrive(&eempty[a]);
+          if constexpr (T::kEin) ptx::mbar_arrive(&eempty[it % C::EIN_NBUF]);
         }
       }
       if constexpr (EPI == EPI_HEAD && C::EPW > 1) {
