@@ -70,7 +70,8 @@ struct Cfg {
   // epilogue warps per TMEM lane quadrant: the epilogue of a CTA's last tile is exposed (one tile per CTA at
   // B = 4096), so plain stores split the tile's 64-column sub-tiles over up to 4 warps per quadrant
   // (EPI_HEAD too: each warp's partial dot product over its 64-column sub-tiles, summed in column order)
-  static constexpr bool SPLIT = EPI == EPI_STORE || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS || EPI == EPI_HEAD;
+  static constexpr bool SPLIT = EPI == EPI_STORE || EPI == EPI_BIAS_RELU || EPI == EPI_BIAS || EPI == EPI_HEAD ||
+                                EPI == EPI_CROSS_F32;
   // EW caps the split: EW = 1 when each CTA runs several tiles (the epilogue then overlaps the next tile's
   // mainloop anyway) keeps the CTA at 7 warps, leaving registers for co-resident embedding CTAs
   // EPI_ATTN: 8 epilogue warps = 2 examples x 4 groups of 16 query rows (one attention warp each)
@@ -83,6 +84,8 @@ struct Cfg {
   // ATTN: two groups of 8 epilogue warps take alternate tiles (accumulator a = group), each with its own staging,
   // so one tile's attention overlaps the next one's
   static constexpr int ATT_GROUPS = 2;
+  // (EPI_CROSS_F32, config 4's DCN branch with fp32 output: 2 epilogue warps per quadrant at BN = 128 measured 354 ->
+  // 320 us per launch; 4 warps of 32 columns each, 335)
   static constexpr int EPW = RING ? 3 : (ATTN ? 2 * ATT_GROUPS : (ATTN_TC ? 2 : (SPLIT ? (BN / 64 < EW ? BN / 64 : EW) : 1)));
   static constexpr int COLS_W = BN / EPW;           // columns per epilogue warp
   static constexpr int PRODUCER_B = 2 + 4 * EPW;
@@ -91,8 +94,10 @@ struct Cfg {
   static constexpr int OUT_BYTES = EpiTraits<EPI>::kSmemOut && !RING ? NSUB * SUB : 0;     // per buffer
   static constexpr int EIN_BYTES = EpiTraits<EPI>::kEin && !RING ? EpiTraits<EPI>::kEinTensors * NSUB * SUB : 0;  // per buf
   // EIN buffers: 2 (one per accumulator) by default; config 4's DCN U GEMM (fp32 output, 2-CTA 128-wide tiles) keeps
-  // ONE, which frees three more operand ring stages (2 -> 5) -- its B producer then issues a tile's x0 / x_l loads
-  // after the tile's weight k-blocks, once the previous tile's epilogue has released the buffer
+  // ONE, which leaves room for its split epilogue's fp32 staging and 4 operand ring stages (with 2 buffers and one
+  // epilogue warp per quadrant it had 2 stages: 348-354 us; one buffer alone, 5 stages: no change; + the split
+  // epilogue: 320 us) -- its B producer then issues a tile's x0 / x_l loads after the tile's weight k-blocks, once the
+  // previous tile's epilogue has released the buffer
   static constexpr int EIN_NBUF = EPI == EPI_CROSS_F32 ? 1 : 2;
   // EPI_ATTN staging: Q | K | V of a tile's 128 tokens, bf16, row stride ATT_LD (padded: conflict-free ldmatrix).
   // (An unpadded XOR-swizzled layout freed a third ring stage but measured slower: 469 vs 381 us per layer.)
@@ -196,7 +201,7 @@ __global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
     }
     for (int e = 0; e < 3; ++e) {
       ptx::mbar_init(&efull[e], 1);
-      ptx::mbar_init(&eempty[e], 4);
+      ptx::mbar_init(&eempty[e], C::RING ? 4 : 4 * C::EPW);  // RING: one warp per quadrant and sub-tile slot
     }
     for (int i = 0; i < 8; ++i) ptx::mbar_init(&abar[i], 1);  // ATTN_TC: [group][qkv staged, S, P staged, O]
     for (int i = 0; i < 4 * 3; ++i) ptx::mbar_init(&sfull[i], 1);
