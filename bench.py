@@ -468,6 +468,27 @@ def run_cvr(args, cfg):
     p12["match"] = (p12["indices_sha256"] == p12["generator_indices_sha256"] and
                     p12["offsets_sha256"] == p12["generator_offsets_sha256"] and p12["call_block_matches"])
 
+    # ---- S9 overlap evidence: timing events on both executor streams around 6 consecutive steps (events only
+    # BETWEEN the stages, never inside a graph): embed(k) runs in [e0(k), e1(k)], dense(k) in [max(d0(k), e1(k)),
+    # d1(k)]; embed(k+1) overlapping dense(k) shows as e1(k+1) < d1(k)
+    torch.cuda.synchronize(dev)
+    marks = []
+    for i in range(6):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record(s_e)
+        ev[2].record(s_d)
+        step(i)
+        ev[1].record(s_e)
+        ev[3].record(s_d)
+        marks.append(ev)
+    torch.cuda.synchronize(dev)
+    t0m = marks[0][0]
+    timeline = []
+    for k, ev in enumerate(marks):
+        e0, e1, d0, d1 = (t0m.elapsed_time(x) * 1e3 for x in ev)
+        timeline.append({"k": k, "embed_us": [round(e0, 1), round(e1, 1)], "dense_us": [round(max(d0, e1), 1), round(d1, 1)]})
+    overlapped = sum(1 for k in range(len(timeline) - 1) if timeline[k + 1]["embed_us"][1] < timeline[k]["dense_us"][1])
+
     # ---- stage isolation: each stage alone, back to back on one stream (direct launches queued ahead of the GPU)
     iso = {}
     x0iso = m.new_x0(B)
@@ -679,7 +700,8 @@ def run_cvr(args, cfg):
         "stage_isolation": iso,
         "overlap": {"ms_per_step": el_ms / args.steps,
                     "serial_sum_ms": (iso["embed_us_per_step"] + iso["dense_us_per_step"]) / 1e3,
-                    "dense_alone_ms": iso["dense_us_per_step"] / 1e3},
+                    "dense_alone_ms": iso["dense_us_per_step"] / 1e3,
+                    "timeline": timeline, "embed_k1_done_before_dense_k_done": f"{overlapped}/{len(timeline) - 1}"},
         "serving": serving,
         "p12": p12,
         "parity": parity,
