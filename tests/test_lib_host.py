@@ -73,3 +73,38 @@ def test_shard_layout_host(L):
     s, r = m.shard_buffer_bytes(65536)
     assert s == r == 65536 * 13 * 128 * 2                    # T_pad = ceil(100/8) = 13 slots
     m.close()
+
+
+def test_nccl_boundary_host(L):
+    """S4's boundary on a host without a GPU: the library resolves NCCL at run time (the process's libnccl.so.2)
+    and hands out 128-byte unique ids; cvr_comm_init / cvr_exchange before a workspace are state errors."""
+    import ctypes as C
+    from paper_2605_29232_b200 import CvrModel
+    from paper_2605_29232_b200._cvr import comm_unique_id, cvr_nccl_id
+    a, b = comm_unique_id(), comm_unique_id()
+    assert len(a) == 128 and a != b
+    m = CvrModel(cs.C3S, max_batch=64, max_nnz=1, world_size=2, rank=1, allocate=False)
+    uid = cvr_nccl_id()
+    C.memmove(C.addressof(uid), a, 128)
+    assert L.cvr_comm_init(m.h, C.byref(uid), 2, 1) == 4                      # CVR_E_STATE (no workspace)
+    assert L.cvr_exchange(m.h, 16, 16, 128, 16, None) == 4
+    m.close()
+
+
+def test_executor_and_serving_args_host(L):
+    """Host-side validation of the executor / serving entry points (no GPU needed to reject bad arguments)."""
+    import ctypes as C
+    import numpy as np
+    from paper_2605_29232_b200 import CvrModel
+    m = CvrModel(cs.C2, max_batch=64, max_nnz=1, allocate=False)
+    assert L.cvr_warm_graphs(m.h, 64, 16, 16) == 4                           # CVR_E_STATE (no workspace)
+    from paper_2605_29232_b200._cvr import cvr_call_record
+    rec = cvr_call_record()
+    assert L.cvr_call_info(m.h, 0, C.byref(rec)) == 4
+    m.close()
+    t = np.array([0.0, 0.1, 0.05])                                            # arrivals must not decrease
+    n = np.ones(3, np.int32)
+    lat, bof, disp = np.zeros(3), np.zeros(3, np.int32), np.zeros(3)
+    nb = C.c_int()
+    assert L.cvr_batcher_simulate(3, t.ctypes.data, n.ctypes.data, 0.001, 8, 0, 16, 0.0, 0.0, lat.ctypes.data,
+                                  bof.ctypes.data, disp.ctypes.data, C.byref(nb)) == 1   # CVR_E_ARG
