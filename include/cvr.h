@@ -332,6 +332,7 @@ typedef struct {
   double host_dispatch_s; /* host time spent assembling + enqueueing batches                                  */
   double wall_s;          /* from the trace's time origin to the last completion                              */
   double max_dispatch_s;  /* the longest single batch assembly + enqueue                                     */
+  double max_gather_s;    /* the longest single batch assembly (cvr_gather_items)                             */
   int64_t loop_gaps_1ms;  /* polling-loop iterations that took > 1 ms (the host thread was held up)           */
 } cvr_serve_stats;
 

@@ -54,6 +54,7 @@ class cvr_serve_config(ctypes.Structure):
 class cvr_serve_stats(ctypes.Structure):
     _fields_ = [("rejected", ctypes.c_int64), ("aborted", ctypes.c_int), ("items_served", ctypes.c_int64),
                 ("host_dispatch_s", ctypes.c_double), ("wall_s", ctypes.c_double), ("max_dispatch_s", ctypes.c_double),
+                ("max_gather_s", ctypes.c_double),
                 ("loop_gaps_1ms", ctypes.c_int64)]
 
 

@@ -2186,11 +2186,15 @@ int cvr_gather_items(int n_tables, int n_dense, int64_t pool_size, const int32_t
   if (n > out_batch_cap) return CVR_E_NOMEM;  // out_offsets [T * cap + 1] and out_dense [cap, F] would overflow
   for (int i = 0; i < n; ++i)
     if (item_ids[i] < 0 || item_ids[i] >= pool_size) return CVR_E_INDEX;
-  // pass 1 (parallel over tables): bag lengths -> per-table totals; pass 2: copy at prefix offsets.  The random
-  // pool reads are latency-bound, so the whole OpenMP team pays even for small batches (measured on the GPU box: a
-  // 68-item batch 25 us with the team vs 100 us on one thread; 8192 items 0.93 ms on 8 threads vs ~0.25 ms on all)
-  const bool par = true;
-  const int nth = std::max(1, omp_get_max_threads());
+  // pass 1: bag lengths -> per-table totals; pass 2: copy at the prefix offsets.  The pool reads are random
+  // (item ids) and latency-bound, so both passes prefetch the offsets PF items ahead (and pass 2 the index runs of
+  // items PF/2 ahead, whose offsets are cached by then).  Batches below 2048 items stay on the calling thread: an
+  // OpenMP region's barrier waits for its slowest member, and on the 16-core GPU host a team member descheduled
+  // for a few ms showed up as 2-11 ms outliers of single gathers (cvr_serve_stats.max_gather_s) at low load
+  constexpr int PF = 16;
+  const bool par = n >= 2048;
+  // (large batches: the team leaves 4 cores to the polling thread's neighbours -- CUDA driver threads, the OS)
+  const int nth = std::max(1, omp_get_max_threads() - 4);
   std::vector<int64_t> tot(n_tables + 1, 0);
   int bad = 0;
 #pragma omp parallel for schedule(static) reduction(| : bad) if (par) num_threads(nth)
@@ -2198,6 +2202,7 @@ int cvr_gather_items(int n_tables, int n_dense, int64_t pool_size, const int32_t
     const int32_t* off = pool_offsets + (int64_t)t * pool_size;
     int64_t s = 0;
     for (int i = 0; i < n; ++i) {
+      if (i + PF < n) __builtin_prefetch(off + item_ids[i + PF]);
       const int64_t it = item_ids[i];
       const int32_t len = off[it + 1] - off[it];
       bad |= len < 0;
@@ -2214,6 +2219,8 @@ int cvr_gather_items(int n_tables, int n_dense, int64_t pool_size, const int32_t
     const int32_t* off = pool_offsets + (int64_t)t * pool_size;
     int64_t pos = tot[t];
     for (int i = 0; i < n; ++i) {
+      if (i + PF < n) __builtin_prefetch(off + item_ids[i + PF]);
+      if (i + PF / 2 < n) __builtin_prefetch(pool_indices + off[item_ids[i + PF / 2]]);
       const int64_t it = item_ids[i];
       const int32_t lo = off[it], hi = off[it + 1];
       for (int32_t q = lo; q < hi; ++q) out_indices[pos++] = pool_indices[q];
@@ -2221,8 +2228,10 @@ int cvr_gather_items(int n_tables, int n_dense, int64_t pool_size, const int32_t
     }
   }
 #pragma omp parallel for schedule(static) if (par) num_threads(nth)
-  for (int i = 0; i < (n_dense ? n : 0); ++i)
+  for (int i = 0; i < (n_dense ? n : 0); ++i) {
+    if (i + PF < n) __builtin_prefetch(pool_dense + (int64_t)item_ids[i + PF] * n_dense);
     memcpy(out_dense + (int64_t)i * n_dense, pool_dense + (int64_t)item_ids[i] * n_dense, (size_t)n_dense * 4);
+  }
   *out_nnz = tot[n_tables];
   return CVR_OK;
 }

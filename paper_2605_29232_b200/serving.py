@@ -301,5 +301,5 @@ class Server:
         self.batcher.rejected = stats.rejected
         self.stats = {"rejected": stats.rejected, "aborted": bool(stats.aborted), "items_served": stats.items_served,
                       "host_dispatch_s": stats.host_dispatch_s, "wall_s": stats.wall_s,
-                      "max_dispatch_s": stats.max_dispatch_s, "loop_gaps_1ms": stats.loop_gaps_1ms}
+                      "max_dispatch_s": stats.max_dispatch_s, "max_gather_s": stats.max_gather_s, "loop_gaps_1ms": stats.loop_gaps_1ms}
         return lat, sizes[:nb.value], scores

@@ -48,5 +48,5 @@ for window, qps, mr in [(0.0, 2000.0, 1), (0.0, 10000.0, 1), (0.5e-3, 500.0, 0),
     print(json.dumps({"window_ms": window * 1e3, "qps": qps, "p50_ms": float(nearest_rank(L, 50)) * 1e3,
                       "p99_ms": float(nearest_rank(L, 99)) * 1e3, "max_ms": float(np.max(L)) * 1e3,
                       "batches": int(len(sizes)), "host_dispatch_us_per_batch": st["host_dispatch_s"] / max(1, len(sizes)) * 1e6,
-                      "max_dispatch_ms": st["max_dispatch_s"] * 1e3, "loop_gaps_1ms": st["loop_gaps_1ms"],
+                      "max_dispatch_ms": st["max_dispatch_s"] * 1e3, "max_gather_ms": st["max_gather_s"] * 1e3, "loop_gaps_1ms": st["loop_gaps_1ms"],
                       "aborted": st["aborted"], "worst_at_s": [round(float(t[i]), 4) for i in worst]}), flush=True)
