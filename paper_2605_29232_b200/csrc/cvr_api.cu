@@ -18,6 +18,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -1843,7 +1844,9 @@ int cvr_release_peers(cvr_ctx* c, uint32_t epoch, cvr_stream_t stream) {
 // CUDA IPC handles name a whole allocation (cudaIpcGetMemHandle), but callers pass tensors that a caching allocator
 // may have sub-allocated at an offset inside it: the handle blob carries that offset (cuMemGetAddressRange) and
 // the opening side adds it back; the opened base is remembered so cvr_ipc_close_handle can unmap it.
-static std::map<void*, void*> g_ipc_bases;  // opened tensor pointer -> mapped allocation base
+static std::map<void*, void*> g_ipc_bases;          // opened tensor pointer -> mapped allocation base
+static std::map<std::string, std::pair<void*, int>> g_ipc_maps;  // allocation handle -> (mapped base, opened tensors)
+static std::mutex g_ipc_mu;                         // (the IPC entry points take no ctx: any thread may call them)
 
 int cvr_ipc_get_handle(const void* d_ptr, void* handle) {
   if (!d_ptr || !handle) return CVR_E_ARG;
@@ -1874,8 +1877,17 @@ int cvr_ipc_open_handle(const void* handle, void** d_ptr) {
   memcpy(&h, handle, 64);
   memcpy(&off, reinterpret_cast<const uint8_t*>(handle) + 64, 8);
   if (off < 0) return CVR_E_ARG;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
+  const std::string key(reinterpret_cast<const char*>(&h), 64);
+  auto it = g_ipc_maps.find(key);
   void* base = nullptr;
-  if (cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return CVR_E_CUDA;
+  if (it != g_ipc_maps.end()) {  // several tensors of one allocation: one mapping, reference-counted
+    base = it->second.first;
+    ++it->second.second;
+  } else {
+    if (cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) return CVR_E_CUDA;
+    g_ipc_maps[key] = {base, 1};
+  }
   *d_ptr = reinterpret_cast<uint8_t*>(base) + off;
   g_ipc_bases[*d_ptr] = base;
   return CVR_OK;
@@ -1883,14 +1895,18 @@ int cvr_ipc_open_handle(const void* handle, void** d_ptr) {
 
 int cvr_ipc_close_handle(void* d_ptr) {
   if (!d_ptr) return CVR_E_ARG;
+  std::lock_guard<std::mutex> lk(g_ipc_mu);
   auto it = g_ipc_bases.find(d_ptr);
   if (it == g_ipc_bases.end()) return CVR_E_ARG;
   void* base = it->second;
   g_ipc_bases.erase(it);
-  bool still_used = false;  // several tensors of one allocation share one mapping
-  for (auto& kv : g_ipc_bases) still_used |= kv.second == base;
-  if (still_used) return CVR_OK;
-  return cudaIpcCloseMemHandle(base) == cudaSuccess ? CVR_OK : CVR_E_CUDA;
+  for (auto m = g_ipc_maps.begin(); m != g_ipc_maps.end(); ++m) {
+    if (m->second.first != base) continue;
+    if (--m->second.second > 0) return CVR_OK;
+    g_ipc_maps.erase(m);
+    return cudaIpcCloseMemHandle(base) == cudaSuccess ? CVR_OK : CVR_E_CUDA;
+  }
+  return CVR_E_ARG;
 }
 
 // ---- S4 through the library's own NCCL communicator ----------------------------------
