@@ -264,8 +264,8 @@ int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d
  * "prefetch_b" [1] each GEMM issues its first ring stages' weight loads before waiting for the previous kernel;
  * "embed_bps" [0 = uncapped] embedding CTAs per SM inside the executor; "xv_bn" [0 = by wave count] N tile of
  * t = x_l V^T (64, 128, 256); "u_bn" [192] N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64);
- * "epw" [2] epilogue warps per TMEM quadrant: 0 one, 1 up to 4 (one 64-column sub-tile each), 2 split only when a
- * CTA runs <= 2 tiles; "zero_copy_scores" [1] cvr_score_host stores the scores straight into page-locked h_scores;
+ * "epw" [0 for DCN_LOWRANK, else 2] epilogue warps per TMEM quadrant: 0 one, 1 up to 4 (one 64-column sub-tile
+ * each), 2 split only when a CTA runs <= 2 tiles; "zero_copy_scores" [1] cvr_score_host stores the scores straight into page-locked h_scores;
  * config 4: "pair" [1] 2-CTA (cta_group::2) tiles, "ens_u_bn" [128] N tile of the DCN U GEMM, "ens_fused_attn" [1]
  * the QKV projection + attention as one GEMM (else QKV GEMM + mha64), "ens_attn_tc" [1] that GEMM's attention on
  * tcgen05 (S = Q K^T, O = P V as UMMAs in TMEM; else mma.sync in the epilogue), "f32_tma_store" [1] the fp32 DCN-branch

@@ -214,7 +214,11 @@ struct cvr_ctx {
   bool zero_copy_scores = true;  // option "zero_copy_scores": cvr_score_host writes scores into pinned h_scores
   int u_bn = 192;              // option "u_bn": N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64)
   int xv_bn = 0;               // option "xv_bn": N tile of t = x_l V^T (0 = by wave count, see pick_bn_xv)
-  int epw_mode = 2;            // option "epw": split epilogues 0 never, 1 always, 2 when a CTA has one tile
+  // option "epw": split epilogues 0 never, 1 always, 2 when a CTA has <= 2 tiles; default by backbone (set at create):
+  // 0 for the low-rank DCN -- its MLP GEMMs then run 7-warp CTAs whose registers leave room for the next batch's
+  // gather CTAs: c2's pipelined step 99.8 -> 97.6 us although the dense stage alone slows 87.0 -> 89.9 us -- and
+  // 2 elsewhere (c6: 139-141 vs 142-145 us per step with 0; c4 neutral)
+  int epw_mode = 2;
   bool mask_grouped = true;    // option "mask_grouped": MaskNet parallel blocks as one grouped GEMM launch
   // executor CUDA graphs: one per (stage, slot, size bucket), captured at first use and replayed for every batch
   // (the batch lives in the per-call block, so neither its pointers nor its row count are baked into the graph;
@@ -541,6 +545,7 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
     c->mk.Wp = desc->cross_width;
     c->mk.P = desc->n_parallel;
   }
+  c->epw_mode = c->backbone == CVR_DCN_LOWRANK ? 0 : 2;
   c->x0_ld = c->act == CVR_F32 ? round_up(c->W, 4) : round_up(c->W, 64);
   for (int t = 0; t < c->T; ++t)
     if (t % c->world == c->rank) c->local_tables.push_back(t);

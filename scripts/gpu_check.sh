@@ -1,3 +1,2 @@
 cd $GRAFT_REPO_ROOT
-timeout 300 python -u scripts/embed_wb_ab.py 2>&1 | tail -8
-CFG=c4 timeout 300 python -u scripts/embed_wb_ab.py 2>&1 | tail -8
+timeout 600 python -u scripts/step_ab.py '[{}, {"u_bn": 64}, {"xv_bn": 128}, {"prefetch_b": 0}]' 2>&1 | tail -12

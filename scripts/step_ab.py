@@ -15,7 +15,7 @@ se, sd = torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1)
 raw = [(i.data_ptr(), o.data_ptr(), i.numel(), d.data_ptr(), out.data_ptr()) for (i, o, d), out in zip(dev, outs)]
 settings = json.loads(sys.argv[1])
 K = int(os.environ.get("K", "500"))
-DEF = {"u_bn": 192, "epw": 2, "pdl": 1, "graphs": 1, "embed_bps": 0, "xv_bn": 0, "prefetch_b": 1,
+DEF = {"u_bn": 192, "epw": 0, "pdl": 1, "graphs": 1, "embed_bps": 0, "xv_bn": 0, "prefetch_b": 1,
        "ens_fused_attn": 1, "zero_copy_scores": 1}
 for rep in range(3):
     for st in settings:
