@@ -470,7 +470,7 @@ def run_cvr(args, cfg):
 
     # ---- S9 overlap evidence: timing events on both executor streams around 6 consecutive steps (events only
     # BETWEEN the stages, never inside a graph): embed(k) runs in [e0(k), e1(k)], dense(k) in [max(d0(k), e1(k)),
-    # d1(k)]; embed(k+1) overlapping dense(k) shows as e1(k+1) < d1(k)
+    # d1(k)]; the gap between dense(k) and dense(k+1) is the part of embed(k+1) not hidden under dense(k)
     torch.cuda.synchronize(dev)
     marks = []
     for i in range(6):
@@ -487,7 +487,8 @@ def run_cvr(args, cfg):
     for k, ev in enumerate(marks):
         e0, e1, d0, d1 = (t0m.elapsed_time(x) * 1e3 for x in ev)
         timeline.append({"k": k, "embed_us": [round(e0, 1), round(e1, 1)], "dense_us": [round(max(d0, e1), 1), round(d1, 1)]})
-    overlapped = sum(1 for k in range(len(timeline) - 1) if timeline[k + 1]["embed_us"][1] < timeline[k]["dense_us"][1])
+    # the dense stream's bubble between dense(k) and dense(k+1) is the part of embed(k+1) NOT hidden under dense(k)
+    bubbles = [timeline[k + 1]["dense_us"][0] - timeline[k]["dense_us"][1] for k in range(1, len(timeline) - 1)]
 
     # ---- stage isolation: each stage alone, back to back on one stream (direct launches queued ahead of the GPU)
     iso = {}
@@ -701,7 +702,8 @@ def run_cvr(args, cfg):
         "overlap": {"ms_per_step": el_ms / args.steps,
                     "serial_sum_ms": (iso["embed_us_per_step"] + iso["dense_us_per_step"]) / 1e3,
                     "dense_alone_ms": iso["dense_us_per_step"] / 1e3,
-                    "timeline": timeline, "embed_k1_done_before_dense_k_done": f"{overlapped}/{len(timeline) - 1}"},
+                    "timeline": timeline, "dense_stream_bubble_us": float(np.mean(bubbles)),
+                    "embed_hidden_frac": 1.0 - float(np.mean(bubbles)) / iso["embed_us_per_step"]},
         "serving": serving,
         "p12": p12,
         "parity": parity,
