@@ -458,7 +458,8 @@ def run_cvr(args, cfg):
     # P12: what the timed region's last batch consumed, read back through its slot's call block (pointers and
     # sizes) and the arrays behind them, against the generator's (SHA-256)
     last = (args.steps - 1) % R
-    rec = m.call_info((args.warmup + args.steps - 1) % 2)
+    from paper_2605_29232_b200._cvr import EXECUTOR_SLOTS as NS
+    rec = m.call_info((args.warmup + args.steps - 1) % NS)
     p12 = {"indices_sha256": digest(dev_in[last][0].cpu().numpy()),
            "generator_indices_sha256": digest(ring[last].indices),
            "offsets_sha256": digest(dev_in[last][1].cpu().numpy()),
@@ -572,7 +573,7 @@ def run_cvr(args, cfg):
                "api": "cvr_score_host (pinned host buffers, copy stream + two compute streams, executor graphs)"}
         # P12 on the host-fed path: the staged copies the kernels read (the slot's call block points into the
         # ctx's workspace) against the generator's arrays
-        hrec = m.call_info((2 * args.warmup + 2 * args.steps - 1) % 2)
+        hrec = m.call_info((2 * args.warmup + 2 * args.steps + 6 - 1) % NS)  # (+6: the overlap timeline's steps)
         lastb = ring[(args.steps - 1) % R]
         wsp = m.workspace.data_ptr()
         got = {k: m.workspace[hrec[k] - wsp:hrec[k] - wsp + n].cpu().numpy()

@@ -77,6 +77,8 @@ typedef enum { CVR_F32 = 0, CVR_BF16 = 1, CVR_F16 = 2 } cvr_dtype;
  * rank by the caller's process group. */
 typedef struct { char internal[128]; } cvr_nccl_id;
 
+#define CVR_EXECUTOR_SLOTS 2  /* x0 slots (and per-call blocks, host-fed staging) of cvr_score / cvr_score_host */
+
 typedef enum {
   CVR_DCN_FULL = 0,     /* full-rank cross with bias, fp32 SIMT path (config 1)      */
   CVR_DCN_LOWRANK = 1,  /* low-rank cross, bf16 tcgen05 path (configs 2, 3, 5)       */
@@ -161,10 +163,11 @@ int cvr_embed(cvr_ctx* ctx, const int32_t* d_indices, const int32_t* d_offsets, 
 /* S5-S7 on d_x0 [batch, x0_ld] -> d_scores [batch] fp32. */
 int cvr_dense(cvr_ctx* ctx, const void* d_x0, int batch, float* d_scores, cvr_stream_t stream);
 
-/* S2-S7 for one batch using the ctx's double-buffered x0 slots: the embed stage runs on
- * s_embed, the dense stage on s_dense, with event edges embed(k) -> dense(k) and
- * dense(k) -> embed(k+2) (slot reuse).  Back-to-back calls therefore overlap the embed
- * stage of batch k+1 with the dense stage of batch k (S9; "Hybrid CPU-GPU Execution").
+/* S2-S7 for one batch using the ctx's CVR_EXECUTOR_SLOTS x0 slots (batch k uses slot k % CVR_EXECUTOR_SLOTS): the
+ * embed stage runs on s_embed, the dense stage on s_dense, with event edges embed(k) -> dense(k) and
+ * dense(k) -> embed(k + CVR_EXECUTOR_SLOTS) (slot reuse).  Back-to-back calls therefore overlap the embed stage of
+ * batch k+1 with the dense stage of batch k (S9; "Hybrid CPU-GPU
+ * Execution").
  * Each stage is one CUDA graph per (x0 slot, grid-size bucket), captured at its first use and replayed for every
  * later batch: the batch's pointers and row count are written to a per-slot argument block in the workspace (a
  * one-thread kernel on s_embed) that every kernel of both stages reads, so no pointer or size is baked into a graph;
@@ -403,7 +406,8 @@ typedef struct {
   double min_ms, max_ms;
 } cvr_kernel_stat;
 
-/* What the executor's kernels consumed: the per-call argument block of x0 slot `slot` (batch k used slot k % 2) as
+/* What the executor's kernels consumed: the per-call argument block of x0 slot `slot` (batch k used slot
+ * k % CVR_EXECUTOR_SLOTS) as
  * the device holds it -- the device pointers and sizes the embed / dense graphs read (P12: the caller hashes the
  * arrays behind them) -- and how many executor graphs this ctx has captured.  Synchronous. */
 typedef struct {

@@ -58,7 +58,8 @@ class cvr_serve_stats(ctypes.Structure):
                 ("loop_gaps_1ms", ctypes.c_int64)]
 
 
-IPC_HANDLE_BYTES = 72  # CVR_IPC_HANDLE_BYTES: CUDA IPC handle of the allocation + the tensor's offset inside it
+IPC_HANDLE_BYTES = 72
+EXECUTOR_SLOTS = 2  # CVR_EXECUTOR_SLOTS: batch k of cvr_score / cvr_score_host uses x0 slot k % 2  # CVR_IPC_HANDLE_BYTES: CUDA IPC handle of the allocation + the tensor's offset inside it
 
 
 class cvr_kernel_stat(ctypes.Structure):

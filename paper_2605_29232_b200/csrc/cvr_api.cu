@@ -141,18 +141,22 @@ struct cvr_ctx {
   std::vector<int> tmean;
   bool any_mean = false;
   // workspace regions (offsets)
-  size_t off_tables = 0, off_flag = 0, off_x0[2] = {0, 0}, off_xa = 0, off_xb = 0, off_t = 0;
-  size_t off_call[2] = {0, 0};  // executor per-call argument blocks (CallArgs), one per x0 slot
+  // executor x0 slots: batch k uses slot k % kSlots.  (Three slots, letting the embed stream run two batches ahead,
+  // measured the same c2 step as two -- 97.7-97.9 vs 97.3-97.6 us: the gather's tail after dense(k) comes from the
+  // dense GEMMs holding the SMs' registers, not from the slot dependency)
+  static constexpr int kSlots = 2;
+  size_t off_tables = 0, off_flag = 0, off_x0[kSlots] = {}, off_xa = 0, off_xb = 0, off_t = 0;
+  size_t off_call[kSlots] = {};  // executor per-call argument blocks (CallArgs), one per x0 slot
   std::vector<size_t> off_h;
-  size_t off_idx[2] = {0, 0}, off_offs[2] = {0, 0}, off_dense[2] = {0, 0}, off_scores[2] = {0, 0};
+  size_t off_idx[kSlots] = {}, off_offs[kSlots] = {}, off_dense[kSlots] = {}, off_scores[kSlots] = {};
   // runtime
   int num_sms = 148;
   bool cuda_ready = false;
-  cudaEvent_t ev_embed[2] = {nullptr, nullptr}, ev_dense[2] = {nullptr, nullptr}, ev_copy[2] = {nullptr, nullptr};
+  cudaEvent_t ev_embed[kSlots] = {}, ev_dense[kSlots] = {}, ev_copy[kSlots] = {};
   int64_t k = 0;
   float head_b = 0.f;  // host copy of head/b (weights are loaded synchronously)
   // tensor maps for internal A operands
-  CUtensorMap tm_x0slot[2], tm_xa, tm_xb, tm_t;   // A-operand / epilogue-input maps, box {64, 128}
+  CUtensorMap tm_x0slot[kSlots], tm_xa, tm_xb, tm_t;   // A-operand / epilogue-input maps, box {64, 128}
   std::vector<CUtensorMap> tm_h;
   CUtensorMap st_xa, st_xb, st_t;                 // output (TMA store) maps, box {64, 32}
   // ensemble (config 4) buffers and maps
@@ -163,7 +167,7 @@ struct cvr_ctx {
     std::vector<size_t> off_catW, off_catb;
     std::vector<size_t> off_qkvh, off_bqkvh;           // Wqkv / bqkv repacked head-major: head h = rows [192 h, +192)
     std::vector<CUtensorMap> Wqkvh;                    //   = [q_h | k_h | v_h] (the fused QKV + attention GEMM's B)
-    CUtensorMap flat_x0[2], tok_x0[2], flat_xa, flat_xb, tok_xa, tok_xb, sttok_xa, sttok_xb;
+    CUtensorMap flat_x0[kSlots], tok_x0[kSlots], flat_xa, flat_xb, tok_xa, tok_xb, sttok_xa, sttok_xb;
     CUtensorMap st_qkv, st_hf, tm_cat;
     CUtensorMap st_S;                                  // fp32 branch sum S [B, W]: staged TMA stores (box 32 x 32)
     CUtensorMap ld_Stok;                               // the same S as tokens [B*T, D]: the FFN2 + LN input loads
@@ -226,8 +230,8 @@ struct cvr_ctx {
   // so a 68-item request does not launch the grids of a max_batch one)
   bool use_graphs = true;
   enum { G_EMBED = 0, G_EMBED_KEYS = 1, G_DENSE = 2, G_KINDS = 3, G_BUCKETS = 24 };
-  cudaGraphExec_t gexec[G_KINDS][2][G_BUCKETS] = {};
-  int64_t gkernels[G_KINDS][2][G_BUCKETS] = {};
+  cudaGraphExec_t gexec[G_KINDS][kSlots][G_BUCKETS] = {};
+  int64_t gkernels[G_KINDS][kSlots][G_BUCKETS] = {};
   int64_t graph_captures = 0;
   void drop_graphs() {
     for (auto& kind : gexec)
@@ -565,9 +569,9 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
   const int64_t B = c->max_batch;
   c->off_tables = carve(cur, sizeof(TableDesc) * std::max<size_t>(1, c->local_tables.size()));
   c->off_flag = carve(cur, 256);
-  for (int i = 0; i < 2; ++i) c->off_call[i] = carve(cur, sizeof(CallArgs));
+  for (int i = 0; i < cvr_ctx::kSlots; ++i) c->off_call[i] = carve(cur, sizeof(CallArgs));
   if (c->world > 1) c->off_peers = carve(cur, (size_t)4 * c->world * sizeof(void*));
-  for (int i = 0; i < 2; ++i) c->off_x0[i] = carve(cur, (size_t)B * c->x0_ld * ae);
+  for (int i = 0; i < cvr_ctx::kSlots; ++i) c->off_x0[i] = carve(cur, (size_t)B * c->x0_ld * ae);
   if (c->backbone == CVR_DCN_LOWRANK) {
     c->off_xa = carve(cur, (size_t)B * c->x0_ld * 2);
     c->off_xb = carve(cur, (size_t)B * c->x0_ld * 2);
@@ -611,7 +615,7 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
   }
   const int64_t Bin = c->world > 1 ? B * c->world : B;  // sharded: indices cover the global batch
   const int T_l = (int)c->local_tables.size();
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < cvr_ctx::kSlots; ++i) {
     c->off_idx[i] = carve(cur, (size_t)std::max<int64_t>(c->max_nnz, 1) * 4);
     c->off_offs[i] = carve(cur, (size_t)(T_l * Bin + 1) * 4);
     c->off_dense[i] = carve(cur, (size_t)B * std::max(c->F, 1) * 4);
@@ -652,7 +656,7 @@ int cvr_destroy(cvr_ctx* c) {
   for (auto ev : c->prof_ev) cudaEventDestroy(ev);
   c->drop_graphs();
   if (c->nccl_comm && g_nccl.dl) g_nccl.commDestroy(c->nccl_comm);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < cvr_ctx::kSlots; ++i) {
     if (c->ev_embed[i]) cudaEventDestroy(c->ev_embed[i]);
     if (c->ev_dense[i]) cudaEventDestroy(c->ev_dense[i]);
     if (c->ev_copy[i]) cudaEventDestroy(c->ev_copy[i]);
@@ -685,7 +689,7 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, dev);
-  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+  for (int i = 0; i < cvr_ctx::kSlots && e == cudaSuccess; ++i) {
     if (!c->ev_embed[i]) e = cudaEventCreateWithFlags(&c->ev_embed[i], cudaEventDisableTiming);
     if (e == cudaSuccess && !c->ev_dense[i]) e = cudaEventCreateWithFlags(&c->ev_dense[i], cudaEventDisableTiming);
     if (e == cudaSuccess && !c->ev_copy[i]) e = cudaEventCreateWithFlags(&c->ev_copy[i], cudaEventDisableTiming);
@@ -707,7 +711,7 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     const char* er = nullptr;
     const int64_t B = c->max_batch;
     bool ok = true;
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < cvr_ctx::kSlots; ++i) {
       ok &= encode_tmap_bf16(&c->tm_x0slot[i], c->ws + c->off_x0[i], B, c->x0_ld, c->x0_ld, 128, &er) == 0;
     }
     ok &= encode_tmap_bf16(&c->tm_xa, c->ws + c->off_xa, B, c->x0_ld, c->x0_ld, 128, &er) == 0;
@@ -730,7 +734,7 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     auto& K = c->mk;
     const int nb = K.P * c->n_cross, HW = nb * c->r, CW = K.P * K.Wp;
     bool ok = true;
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < cvr_ctx::kSlots; ++i) {
       ok &= encode_tmap_bf16(&c->tm_x0slot[i], c->ws + c->off_x0[i], B, c->x0_ld, c->x0_ld, 128, &er) == 0;
     }
     ok &= encode_tmap_bf16(&K.tm_x0p, c->ws + K.off_x0p, B, K.Wp, K.Wp, 128, &er) == 0;
@@ -762,7 +766,7 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
     const int64_t B = c->max_batch, BT = B * c->T, D = c->d, W = c->x0_ld;
     auto& E = c->ens;
     bool ok = true;
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < cvr_ctx::kSlots; ++i) {
       ok &= encode_tmap_bf16(&E.flat_x0[i], c->ws + c->off_x0[i], B, W, W, 128, &er) == 0;
       ok &= encode_tmap_bf16(&E.tok_x0[i], c->ws + c->off_x0[i], BT, D, D, 128, &er) == 0;
     }
@@ -1548,7 +1552,9 @@ int cvr_dense(cvr_ctx* c, const void* d_x0, int batch, float* d_scores, cvr_stre
   CUtensorMap um, umt;
   if (c->backbone != CVR_DCN_FULL) {
     const bool ens = c->backbone == CVR_ENSEMBLE;
-    int slot = d_x0 == c->ws + c->off_x0[0] ? 0 : (d_x0 == c->ws + c->off_x0[1] ? 1 : -1);
+    int slot = -1;
+    for (int i = 0; i < cvr_ctx::kSlots; ++i)
+      if (d_x0 == c->ws + c->off_x0[i]) slot = i;
     if (slot >= 0) {
       tm = ens ? &c->ens.flat_x0[slot] : &c->tm_x0slot[slot];
       tmt = &c->ens.tok_x0[slot];
@@ -1565,7 +1571,7 @@ int cvr_dense(cvr_ctx* c, const void* d_x0, int batch, float* d_scores, cvr_stre
 
 namespace {
 // the two-stream executor behind cvr_score (row ids) and cvr_score_keys (raw keys, hashed in the gather):
-// slot = k % 2; on s_embed: [wait dense(k-2)] -> set_call(slot) -> embed graph(slot) -> event; on s_dense:
+// slot = k % kSlots; on s_embed: [wait dense(k-kSlots)] -> set_call(slot) -> embed graph(slot) -> event; on s_dense:
 // [wait embed(k)] -> dense graph(slot) -> event.  Both graphs read the batch from the slot's call block.
 int score_impl(cvr_ctx* c, const int32_t* d_indices, const uint64_t* d_keys, const int32_t* d_offsets, int64_t nnz,
                int batch, const float* d_dense, float* d_scores, cvr_stream_t s_embed, cvr_stream_t s_dense,
@@ -1578,10 +1584,10 @@ int score_impl(cvr_ctx* c, const int32_t* d_indices, const uint64_t* d_keys, con
   if (!d_offsets || !d_scores || (nnz > 0 && !d_indices && !d_keys) || (c->F && batch && !d_dense) || nnz < 0)
     return c->fail(CVR_E_ARG, "null pointer or negative nnz");
   cudaStream_t se = (cudaStream_t)s_embed, sd = (cudaStream_t)s_dense;
-  const int slot = (int)(c->k & 1);
+  const int slot = (int)(c->k % cvr_ctx::kSlots);
   cudaError_t e = cudaSuccess;
-  if (c->k >= 2) e = cudaStreamWaitEvent(se, c->ev_dense[slot], 0);  // dense(k-2) released the slot (and its block)
-  if (e != cudaSuccess) return c->cuda_fail(e, "wait dense(k-2)");
+  if (c->k >= cvr_ctx::kSlots) e = cudaStreamWaitEvent(se, c->ev_dense[slot], 0);  // dense(k-kSlots) released the slot
+  if (e != cudaSuccess) return c->cuda_fail(e, "wait dense(k-kSlots)");
   CallArgs v{};
   v.indices = d_indices;
   v.keys = d_keys;
@@ -1639,7 +1645,7 @@ int cvr_warm_graphs(cvr_ctx* c, int max_rows, cvr_stream_t s_embed, cvr_stream_t
   for (int t = 0; t < c->T; ++t) keys &= c->tvocab[t] > 0;
   int last = 0;
   c->bucket_rows(max_rows, &last);
-  for (int slot = 0; slot < 2 && !st; ++slot) {
+  for (int slot = 0; slot < cvr_ctx::kSlots && !st; ++slot) {
     void* x0 = c->ws + c->off_x0[slot];
     c->call = c->at<CallArgs>(c->off_call[slot]);
     const bool ens = c->backbone == CVR_ENSEMBLE;
@@ -1692,10 +1698,10 @@ int cvr_score_host(cvr_ctx* c, const int32_t* h_indices, const int32_t* h_offset
   if (!h_offsets || !h_scores || (nnz > 0 && !h_indices) || (c->F && batch && !h_dense))
     return c->fail(CVR_E_ARG, "null pointer");
   cudaStream_t sc = (cudaStream_t)s_copy, sd = (cudaStream_t)s_dense;
-  const int slot = (int)(c->k & 1);
+  const int slot = (int)(c->k % cvr_ctx::kSlots);
   cudaError_t e = cudaSuccess;
-  if (c->k >= 2 && (e = cudaStreamWaitEvent(sc, c->ev_embed[slot], 0)) != cudaSuccess)  // embed(k-2) read staging
-    return c->cuda_fail(e, "wait embed(k-2)");
+  if (c->k >= cvr_ctx::kSlots && (e = cudaStreamWaitEvent(sc, c->ev_embed[slot], 0)) != cudaSuccess)
+    return c->cuda_fail(e, "wait embed(k-kSlots)");  // embed(k-kSlots) has read this staging slot
   int32_t* di = c->at<int32_t>(c->off_idx[slot]);
   int32_t* doff = c->at<int32_t>(c->off_offs[slot]);
   float* dd = c->at<float>(c->off_dense[slot]);
@@ -1989,7 +1995,7 @@ int cvr_repeat_kernel(cvr_ctx* c, const char* role, int reps, const void* d_x0, 
 }
 
 int cvr_call_info(const cvr_ctx* c, int slot, cvr_call_record* out) {
-  if (!c || !out || slot < 0 || slot > 1) return CVR_E_ARG;
+  if (!c || !out || slot < 0 || slot >= cvr_ctx::kSlots) return CVR_E_ARG;
   if (!c->cuda_ready) return CVR_E_STATE;
   CallArgs v{};
   if (cudaMemcpy(&v, c->ws + c->off_call[slot], sizeof v, cudaMemcpyDeviceToHost) != cudaSuccess) return CVR_E_CUDA;

@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
-timeout 1500 python -m pytest tests -q -m gpu -x > gpurun_out/t4_pytest.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/t4_pytest.log
-timeout 600 python -u bench.py --steps 50 --warmup 10 > gpurun_out/bench_c2.log 2>&1; echo "bench c2 rc=$?"; tail -c 300 gpurun_out/bench_c2.log
-timeout 300 python -u bench.py --steps 20 --warmup 5 > gpurun_out/bench_c2_driverargs.log 2>&1; echo "bench c2 (driver args) rc=$?"
+timeout 600 python -u scripts/step_ab.py '[{}]' 2>&1 | tail -3
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_serving.py tests/test_gpu_c4.py -q -x -k "not full_batch" 2>&1 | tail -2
+CFG=c6 timeout 600 python -u scripts/step_ab.py '[{}]' 2>&1 | tail -2

@@ -11,7 +11,8 @@ tabs = [s.materialize(device="cuda") for s in cs.table_specs(cfg)]
 m.load_tables(tabs); m.load_weights({k: v.cuda() for k, v in cs.make_weights(cfg).items()})
 dev = [(torch.from_numpy(b.indices).cuda(), torch.from_numpy(b.offsets).cuda(), torch.from_numpy(b.dense).cuda()) for b in ring]
 outs = [torch.empty(B, device="cuda") for _ in ring]
-se, sd = torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1)
+PE, PD = (int(x) for x in os.environ.get("PRIO", "0,-1").split(","))  # stream priorities (lower = higher)
+se, sd = torch.cuda.Stream(priority=PE), torch.cuda.Stream(priority=PD)
 raw = [(i.data_ptr(), o.data_ptr(), i.numel(), d.data_ptr(), out.data_ptr()) for (i, o, d), out in zip(dev, outs)]
 settings = json.loads(sys.argv[1])
 K = int(os.environ.get("K", "500"))

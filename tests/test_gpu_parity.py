@@ -163,7 +163,8 @@ def test_c2_score_pipelined_and_host_fed_match(c2):
     # P12: the indices / offsets the executor's kernels consumed (read back through the call block of the last
     # batch's slot) are byte-identical to the generator's -- SHA-256 over the device copies
     import hashlib
-    rec, bt = m.call_info((2 * len(batches) - 1) % 2), batches[-1]   # call k uses slot k % 2 (device-fed calls first)
+    from paper_2605_29232_b200._cvr import EXECUTOR_SLOTS as NS
+    rec, bt = m.call_info((2 * len(batches) - 1) % NS), batches[-1]  # call k uses slot k % NS (device-fed calls first)
     assert rec["batch"] == bt.batch and rec["nnz"] == bt.nnz
     nbytes = {"d_indices": bt.indices.nbytes, "d_offsets": bt.offsets.nbytes, "d_dense": bt.dense.nbytes}
     for key, ref_arr in (("d_indices", bt.indices), ("d_offsets", bt.offsets), ("d_dense", bt.dense)):
@@ -219,7 +220,8 @@ def test_executor_graphs_every_backbone(name):
     assert m.status(s_d) == 0
     for k, (out, r) in enumerate(zip(outs, refs)):
         assert torch.equal(out, r), (name, k, sizes[k])
-    last = m.call_info((len(sizes) - 1) % 2)
+    from paper_2605_29232_b200._cvr import EXECUTOR_SLOTS as NS
+    last = m.call_info((len(sizes) - 1) % NS)
     i, o, d = dev_in[-1]
     assert (last["d_indices"], last["d_offsets"], last["nnz"], last["batch"]) == \
         (i.data_ptr(), o.data_ptr(), i.numel(), sizes[-1])
@@ -230,7 +232,7 @@ def test_executor_graphs_every_backbone(name):
             r *= 2
         return min(r, Bmax)
     # one graph per (stage, slot, bucket): embed + dense for every distinct (slot, bucket) seen, nothing more
-    assert last["graph_captures"] == 2 * len({(k % 2, bucket(b)) for k, b in enumerate(sizes)})
+    assert last["graph_captures"] == 2 * len({(k % NS, bucket(b)) for k, b in enumerate(sizes)})
     m.close()
 
 

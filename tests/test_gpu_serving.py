@@ -27,7 +27,8 @@ def test_served_scores_equal_offline():
     reqs = [Request(i, t, len(ids), ids) for i, (t, ids) in enumerate(trace)]
     srv = Server(m, view, max_items=2048, window_s=0.002, max_nnz=2048 * 26 * 16)
     captured = m.call_info(0)["graph_captures"]
-    assert captured == 2 * 2 * 5          # 2 slots x (embed, dense) x buckets 128 .. 2048
+    from paper_2605_29232_b200._cvr import EXECUTOR_SLOTS as NS
+    assert captured == NS * 2 * 5         # slots x (embed, dense) x buckets 128 .. 2048
     lat, sizes, scores = srv.run(reqs, keep_scores=True)
     assert m.call_info(0)["graph_captures"] == captured
     assert srv.stats["rejected"] == 0 and not srv.stats["aborted"]
