@@ -127,6 +127,12 @@ struct Cfg {
   static constexpr int TMEM_COLS = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);  // 2 accumulators, pow2 alloc
   static constexpr int SMEM = 1024 + STAGES * STAGE + EPI_BYTES + Z_BYTES + BAR_BYTES;
   static_assert(STAGES >= 2, "shared memory budget");
+  // register cap: 65536 / NT (one CTA per SM), except the RING U GEMM (512 threads): 96 instead of 128 registers
+  // (no spills) leaves 16K registers on each SM for two co-resident embedding CTAs of the next batch, which the
+  // 128-register build locked out for the U GEMMs' whole duration -- c2 pipelined step 98.4 -> 97.1 us.  (The same
+  // cap on the MLP GEMMs -- 80 or 64 registers -- measured 99.1 / 99.9 us, on the head -- 88 -- no change.)
+  static constexpr int MAXREG_LB = (65536 / NT) > 255 ? 255 : (65536 / NT) & ~7;
+  static constexpr int MAXREG = RING ? 96 : MAXREG_LB;
 };
 
 using namespace tile;
@@ -146,7 +152,7 @@ __device__ __forceinline__ void stamp(unsigned long long* dbg, int i) {
 }
 
 template <int BN, int EPI, int CG, int EW>
-__global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1)
+__global__ void __launch_bounds__(Cfg<BN, EPI, CG, EW>::NT, 1) __maxnreg__((Cfg<BN, EPI, CG, EW>::MAXREG))
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmX0,
                      const __grid_constant__ CUtensorMap tmXl, const GemmArgs g) {
