@@ -266,6 +266,29 @@ def max_over_ranks(world, x: float, local) -> float:
     return float(t.item())
 
 
+FP32_ALU_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # derived FP32 FFMA peak (c1's SIMT dense kernel), DESIGN.md §8
+
+
+def cpu_host_info():
+    """CPU model and BLAS vendor of the oracle's host."""
+    info = {}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    info["cpu_model"] = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+        info["blas"] = sorted({"%s %s" % (i.get("internal_api"), i.get("version")) for i in threadpool_info()
+                               if i.get("user_api") == "blas"})
+    except Exception:  # noqa: BLE001
+        pass
+    return info
+
+
 def host_cores():
     try:
         from threadpoolctl import threadpool_info
@@ -624,6 +647,18 @@ def run_cvr(args, cfg):
                          "hbm_line": {"achieved": gb, "unit": "GB/s", "frac": gb / pk["hbm"],
                                       "ai_flop_per_byte": wk["flops"] / wk["bytes"],
                                       "traffic": traffic_db.get(role)}}
+    if cfg.backbone == "dcn_full":  # c1: one fp32 SIMT launch per dense stage (K3), timed as the stage alone
+        wk = launch_work(cfg, B)["dense_f32_dcn"]
+        t_s = iso["dense_us_per_step"] / 1e6
+        tf = wk["flops"] / t_s / 1e12
+        kernels["dense_f32_dcn"] = {"bound": "alu", "per_step": 1, "us_per_launch": iso["dense_us_per_step"],
+                                    "achieved": tf, "unit": "TFLOP/s", "peak": FP32_ALU_TFLOPS,
+                                    "frac": tf / FP32_ALU_TFLOPS, "flops_per_launch": wk["flops"],
+                                    "peak_source": "derived (DESIGN.md §8): 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz",
+                                    "hbm_line": {"achieved": wk["bytes"] / t_s / 1e9, "unit": "GB/s",
+                                                 "frac": wk["bytes"] / t_s / 1e9 / pk["hbm"],
+                                                 "traffic": traffic_db.get("dense_f32_dcn")},
+                                    "timing": "dense stage alone (one launch), back-to-back, CUDA events"}
     for k in kernels:
         kernels[k]["us_per_step"] = kernels[k]["us_per_launch"] * kernels[k]["per_step"]
     dom = max(kernels, key=lambda k: kernels[k]["us_per_step"])
@@ -632,7 +667,8 @@ def run_cvr(args, cfg):
     roofline = {"kernel": dom, "bound": dk["bound"], "achieved": dk["achieved"], "peak": dk["peak"],
                 "unit": dk["unit"], "frac": dk["frac"],
                 "traffic": dk["hbm_line"]["traffic"] if "hbm_line" in dk else traffic_db.get(dom),
-                "peak_source": "MEASURED_PEAKS.json (%s): bf16 burst for a GEMM timed alone, HBM copy GB/s" % pk["source"],
+                "peak_source": dk.get("peak_source") or
+                "MEASURED_PEAKS.json (%s): bf16 burst for a GEMM timed alone, HBM copy GB/s" % pk["source"],
                 "share_of_kernel_time": dk["us_per_step"] / tot,
                 "timing": ("GEMM: cvr_repeat_kernel chain (only this role, %d launches back to back with PDL, CUDA events "
                            "around the chain on its stream); embed: the stage alone" % 8),
@@ -647,6 +683,21 @@ def run_cvr(args, cfg):
                    "frac_sustained": dense_flops / dense_us / 1e6 / (pk["bf16_sustained"] or bf16_burst),
                    "sum_of_kernel_chains_us": sum(v["us_per_step"] for k, v in kernels.items()
                                                   if k != "embed_bag_pool")}
+
+    # ---- SURVEY.md §8(d) "End-to-end ex/s / roofline ex/s": the examples/s each stage's peak allows (sparse on
+    # algorithmic bytes / HBM, dense on FLOPs / the bf16 burst peak, or the derived FP32 ALU peak for c1), serial
+    # (sum of the two) and overlapped (the slower one)
+    dense_peak = FP32_ALU_TFLOPS if cfg.backbone == "dcn_full" else bf16_burst
+    ex_sparse = B / (ebytes / (pk["hbm"] * 1e9))
+    ex_dense = B / (dense_flops / (dense_peak * 1e12))
+    ex_serial = 1.0 / (1.0 / ex_sparse + 1.0 / ex_dense)
+    ex_over = min(ex_sparse, ex_dense)
+    vs_roof = {"sparse_only_ex_s": ex_sparse, "dense_only_ex_s": ex_dense, "serial_ex_s": ex_serial,
+               "overlapped_ex_s": ex_over, "frac_of_serial": value / world / ex_serial,
+               "frac_of_overlapped": value / world / ex_over,
+               "peaks": "HBM %.1f GB/s, dense %.1f TFLOP/s (%s)" % (pk["hbm"], dense_peak,
+                                                                  "FP32 ALU, derived" if cfg.backbone == "dcn_full"
+                                                                  else "bf16 burst, measured")}
 
     # ---- parity (outside the timed region): the last ring batch vs the oracle -- every example for c1 / c2,
     # a sample for the larger configs
@@ -682,6 +733,21 @@ def run_cvr(args, cfg):
         cpu = {"value": n_ex / el, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
                "sample": f"{k} x {sub} examples of {cfg.name} ({n_ex} examples, {el:.1f} s) through "
                          f"oracle.score_forward (numpy fp64, table rows regenerated on demand)"}
+        cpu.update(cpu_host_info())
+        try:  # plus a 1-thread run (a shorter sample of the same batches)
+            from threadpoolctl import threadpool_limits
+            with threadpool_limits(limits=1):
+                n1, t1, k1 = 0, time.perf_counter(), 0
+                while True:
+                    bt = ring[k1 % R] if sub == B else cs.sub_batch(ring[k1 % R], np.arange(sub))
+                    O.score_forward(cfg, tabs, weights, bt)
+                    n1 += sub
+                    k1 += 1
+                    if time.perf_counter() - t1 >= args.cpu_seconds / 3:
+                        break
+                cpu["one_thread"] = {"value": n1 / (time.perf_counter() - t1), "unit": UNIT, "examples": n1}
+        except Exception as e:  # noqa: BLE001
+            cpu["one_thread"] = {"error": str(e)}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -699,6 +765,7 @@ def run_cvr(args, cfg):
         "clocks": clocks.summary(),
         "kernels": kernels,
         "dense_stage": dense_stage,
+        "vs_roofline_ex_s": vs_roof,
         "stage_isolation": iso,
         "overlap": {"ms_per_step": el_ms / args.steps,
                     "serial_sum_ms": (iso["embed_us_per_step"] + iso["dense_us_per_step"]) / 1e3,
