@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-serving", action="store_true", help="skip the c5 p50/p99 probe (2 s at 8k queries/s)")
     ap.add_argument("--no-sharded", action="store_true", help="N > 1: skip the c3-S sharded measurement")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--lanes", type=int, default=0, help="executor lanes (0 = the config's default, LANES)")
     return ap.parse_args()
 
 
@@ -235,6 +236,9 @@ WORKLOADS = {
     "c6": "c6: SURVEY.md §8(f) #1 MaskNet on config 2's features (ReLU projection 1728->2048, 2 parallel mask "
           "blocks r=512, MLP 4096-1024-512-256-1; PAPER.md Table 1 MaskNet defaults), not a BASELINE.json config",
 }
+# executor lanes per config (cvr.h option "lanes"): c2 86.3 vs 97.0 us per batch with two pipelines dealt batches
+# round-robin (scripts/two_exec.py); c6 no gain (137-143 vs 140-141); the others one
+LANES = {"c2": 2}
 TOL = {"c1": 1e-5, "c2": 2e-3, "c3": 2e-3, "c3s": 2e-3, "c4": 2e-3, "c6": 2e-3}
 
 
@@ -431,9 +435,11 @@ def run_cvr(args, cfg):
     weights = cs.make_weights(cfg)
     ring = [cs.make_batch(cfg, 1000 * rank + i) for i in range(args.ring)]
     max_nnz = max(b.nnz for b in ring)
-    m = CvrModel(cfg, max_batch=B, max_nnz=max_nnz, device=dev)
+    lanes = args.lanes if args.lanes else LANES.get(cfg.name, 1)
+    m = CvrModel(cfg, max_batch=B, max_nnz=max_nnz, device=dev, lanes=lanes)
     m.load_tables(tables)
     m.load_weights({k: v.to(dev) for k, v in weights.items()})
+    ncall = [0]  # executor calls made on m (cvr_call_info slot of call n: m.executor_slot(n))
     dev_in = [(torch.from_numpy(b.indices).to(dev), torch.from_numpy(b.offsets).to(dev),
                torch.from_numpy(b.dense).to(dev)) for b in ring]
     outs = [torch.empty(B, dtype=torch.float32, device=dev) for _ in ring]
@@ -447,13 +453,16 @@ def run_cvr(args, cfg):
            for (idx, off, dense), o in zip(dev_in, outs)]
     hse, hsd, hsc = s_e.cuda_stream, s_d.cuda_stream, s_c.cuda_stream
 
-    def step(i):
+    def step(i, mm=m):
         ip, op, nnz, dp, sp = raw[i % R]
-        m.score_raw(ip, op, nnz, B, dp, sp, hse, hsd)
+        mm.score_raw(ip, op, nnz, B, dp, sp, hse, hsd)
+        if mm is m:
+            ncall[0] += 1
 
     torch.cuda.synchronize(dev)  # the inputs were copied on the current stream; the executor's streams start now
-    # warm-up: the executor captures one graph per stage for each of its two x0 slots in the first two calls; every
-    # later batch (any pointers; any size in the same grid bucket) replays them, so the timed region holds no capture
+    # every executor graph (each lane's slots x stages x grid buckets up to B) captured up front, nothing run; every
+    # batch (any pointers; any size in a captured bucket) replays them, so the timed region holds no capture
+    m.warm_graphs(B, s_e, s_d)
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize(dev)
@@ -481,8 +490,7 @@ def run_cvr(args, cfg):
     # P12: what the timed region's last batch consumed, read back through its slot's call block (pointers and
     # sizes) and the arrays behind them, against the generator's (SHA-256)
     last = (args.steps - 1) % R
-    from paper_2605_29232_b200._cvr import EXECUTOR_SLOTS as NS
-    rec = m.call_info((args.warmup + args.steps - 1) % NS)
+    rec = m.call_info(m.executor_slot(ncall[0] - 1))
     p12 = {"indices_sha256": digest(dev_in[last][0].cpu().numpy()),
            "generator_indices_sha256": digest(ring[last].indices),
            "offsets_sha256": digest(dev_in[last][1].cpu().numpy()),
@@ -492,16 +500,40 @@ def run_cvr(args, cfg):
     p12["match"] = (p12["indices_sha256"] == p12["generator_indices_sha256"] and
                     p12["offsets_sha256"] == p12["generator_offsets_sha256"] and p12["call_block_matches"])
 
+    # ---- one pipeline alone (lanes = 1): with L > 1 lanes the line's value comes from L pipelines dealt batches
+    # round-robin; this is the single pipeline's step (per-batch latency view) and the one the timeline below shows
+    m1 = m
+    single = None
+    if lanes > 1:
+        m1 = CvrModel(cfg, max_batch=B, max_nnz=max_nnz, device=dev)
+        m1.load_tables(tables)
+        m1.load_weights({k: v.to(dev) for k, v in weights.items()})
+        m1.warm_graphs(B, s_e, s_d)
+        for i in range(args.warmup):
+            step(i, m1)
+        torch.cuda.synchronize(dev)
+        a1, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a1.record(s_e)
+        s_d.wait_event(a1)
+        for i in range(args.steps):
+            step(i, m1)
+        b1.record(s_d)
+        torch.cuda.synchronize(dev)
+        assert m1.status(s_d) == 0
+        el1 = a1.elapsed_time(b1)
+        single = {"lanes": 1, "ms_per_step": el1 / args.steps, "value": args.steps * B / (el1 / 1e3)}
+
     # ---- S9 overlap evidence: timing events on both executor streams around 6 consecutive steps (events only
     # BETWEEN the stages, never inside a graph): embed(k) runs in [e0(k), e1(k)], dense(k) in [max(d0(k), e1(k)),
     # d1(k)]; the gap between dense(k) and dense(k+1) is the part of embed(k+1) not hidden under dense(k)
+    # (one pipeline: m1)
     torch.cuda.synchronize(dev)
     marks = []
     for i in range(6):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         ev[0].record(s_e)
         ev[2].record(s_d)
-        step(i)
+        step(i, m1)
         ev[1].record(s_e)
         ev[3].record(s_d)
         marks.append(ev)
@@ -573,6 +605,7 @@ def run_cvr(args, cfg):
         def hstep(i):
             ip, op, nnz, dp, sp = hraw[i % R]
             m.score_host_raw(ip, op, nnz, B, dp, sp, hsc, hse, hsd)
+            ncall[0] += 1
 
         for i in range(args.warmup):
             hstep(i)
@@ -596,7 +629,7 @@ def run_cvr(args, cfg):
                "api": "cvr_score_host (pinned host buffers, copy stream + two compute streams, executor graphs)"}
         # P12 on the host-fed path: the staged copies the kernels read (the slot's call block points into the
         # ctx's workspace) against the generator's arrays
-        hrec = m.call_info((2 * args.warmup + 2 * args.steps + 6 - 1) % NS)  # (+6: the overlap timeline's steps)
+        hrec = m.call_info(m.executor_slot(ncall[0] - 1))
         lastb = ring[(args.steps - 1) % R]
         wsp = m.workspace.data_ptr()
         got = {k: m.workspace[hrec[k] - wsp:hrec[k] - wsp + n].cpu().numpy()
@@ -754,7 +787,10 @@ def run_cvr(args, cfg):
         "ms_per_step": el_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32" if cfg.act_dtype == "f32" else "bf16", "data": "synthetic (cvr_synth: seeded, BASELINE.json configs[1] shapes/distributions)",
         "config": {"workload": WORKLOADS[cfg.name], "global_batch": B * world, "batch_per_gpu": B,
-                   "parallelism": f"replicas x{world} (two-stream decoupled executor per GPU)",
+                   "parallelism": f"replicas x{world} (two-stream decoupled executor per GPU"
+                                  + (f", {lanes} executor lanes: batches dealt round-robin to {lanes} pipelines)"
+                                     if lanes > 1 else ")"),
+                   "lanes": lanes,
                    "l2": "inputs larger than L2 (%.2f GB of tables, ring of %d distinct batches)" % (
                        sum(t.numel() * t.element_size() for t in tables) / 1e9, R)},
         "roofline": roofline,
@@ -767,7 +803,9 @@ def run_cvr(args, cfg):
         "dense_stage": dense_stage,
         "vs_roofline_ex_s": vs_roof,
         "stage_isolation": iso,
-        "overlap": {"ms_per_step": el_ms / args.steps,
+        "single_pipeline": single,
+        "overlap": {"ms_per_step": single["ms_per_step"] if single else el_ms / args.steps,
+                    "pipeline": "one lane (lanes = 1)",
                     "serial_sum_ms": (iso["embed_us_per_step"] + iso["dense_us_per_step"]) / 1e3,
                     "dense_alone_ms": iso["dense_us_per_step"] / 1e3,
                     "timeline": timeline, "dense_stream_bubble_us": float(np.mean(bubbles)),

@@ -122,7 +122,8 @@ const char* cvr_status_string(int status);
 const char* cvr_version(void);
 
 /* Device workspace (weights, x0 slots, intermediates, staging, flags); caller-allocated,
- * >= 256-byte aligned.  Must be set before cvr_load_weights. */
+ * >= 256-byte aligned.  Must be set before cvr_load_weights.  With option "lanes" L > 1 (set before this call) the
+ * size covers every lane (each lane holds its own copy of everything but the borrowed tables). */
 int cvr_workspace_bytes(const cvr_ctx* ctx, size_t* bytes);
 int cvr_set_workspace(cvr_ctx* ctx, void* d_ws, size_t bytes);
 
@@ -172,7 +173,12 @@ int cvr_dense(cvr_ctx* ctx, const void* d_x0, int batch, float* d_scores, cvr_st
  * later batch: the batch's pointers and row count are written to a per-slot argument block in the workspace (a
  * one-thread kernel on s_embed) that every kernel of both stages reads, so no pointer or size is baked into a graph;
  * the bucket (batch rounded up to a power of two >= 128, capped at max_batch) only sizes the grids (option
- * "graphs" [1]).  The pointers must stay valid until s_dense has passed this batch. */
+ * "graphs" [1]).  The pointers must stay valid until s_dense has passed this batch.
+ * Executor lanes (option "lanes" = L > 1): consecutive calls are dealt round-robin to L independent pipelines of
+ * the model (each with its own slots, intermediates and graphs, on its own pair of library streams created with
+ * the priorities of s_embed / s_dense): the call's work starts after everything enqueued on s_embed so far (the
+ * inputs AND d_scores must be ready there) and s_dense waits for its end, so the dense stages of consecutive
+ * batches may run concurrently (throughput up, per-batch latency up). */
 int cvr_score(cvr_ctx* ctx, const int32_t* d_indices, const int32_t* d_offsets, int64_t nnz,
               int batch, const float* d_dense, float* d_scores, cvr_stream_t s_embed,
               cvr_stream_t s_dense);
@@ -273,8 +279,10 @@ int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d
  * the QKV projection + attention as one GEMM (else QKV GEMM + mha64), "ens_attn_tc" [1] that GEMM's attention on
  * tcgen05 (S = Q K^T, O = P V as UMMAs in TMEM; else mma.sync in the epilogue), "f32_tma_store" [1] the fp32 DCN-branch
  * output through staged TMA stores, "ens_xv_wave" [1] t = X V^T as one wave of 128 x 256 tiles; MaskNet:
- * "mask_grouped" [1] parallel blocks as one grouped GEMM.  Every variant is bit-identical to the default.  Unknown
- * key or bad value -> CVR_E_ARG. */
+ * "mask_grouped" [1] parallel blocks as one grouped GEMM.  Every variant is bit-identical to the default.
+ * "lanes" [1] executor lanes (1-4, see cvr_score): only before cvr_set_workspace (else CVR_E_STATE), unsharded
+ * only; sub-contexts are created here and every later option, table, weight and feature-spec call is applied to
+ * all lanes.  Unknown key or bad value -> CVR_E_ARG. */
 int cvr_set_option(cvr_ctx* ctx, const char* key, int64_t value);
 
 /* -- utility ----------------------------------------------------------------------------------
@@ -407,9 +415,10 @@ typedef struct {
 } cvr_kernel_stat;
 
 /* What the executor's kernels consumed: the per-call argument block of x0 slot `slot` (batch k used slot
- * k % CVR_EXECUTOR_SLOTS) as
+ * k % CVR_EXECUTOR_SLOTS; with L lanes slot is in [0, L * CVR_EXECUTOR_SLOTS): call n ran on lane n % L, in that
+ * lane's slot (n / L) % CVR_EXECUTOR_SLOTS, flat index lane * CVR_EXECUTOR_SLOTS + slot) as
  * the device holds it -- the device pointers and sizes the embed / dense graphs read (P12: the caller hashes the
- * arrays behind them) -- and how many executor graphs this ctx has captured.  Synchronous. */
+ * arrays behind them) -- and how many executor graphs this ctx has captured (all lanes).  Synchronous. */
 typedef struct {
   const int32_t* d_indices;
   const uint64_t* d_keys;

@@ -253,7 +253,7 @@ class CvrModel:
     """
 
     def __init__(self, cfg, max_batch: int, max_nnz: int = 0, world_size: int = 1, rank: int = 0,
-                 device: Optional[torch.device] = None, allocate: bool = True):
+                 device: Optional[torch.device] = None, allocate: bool = True, lanes: int = 1):
         self.L = lib()
         self.cfg = cfg
         self._rows = (ctypes.c_int64 * cfg.n_tables)(*cfg.rows)
@@ -273,6 +273,9 @@ class CvrModel:
                 self.L.cvr_destroy(h)
             self.h = _vp()
             raise CvrError(st, msg)
+        self.lanes = lanes
+        if lanes != 1:  # executor lanes (cvr.h option "lanes"): before the workspace is sized
+            self._check(self.L.cvr_set_option(self.h, b"lanes", lanes))
         ld, dt = ctypes.c_int(), ctypes.c_int()
         self._check(self.L.cvr_x0_layout(self.h, ctypes.byref(ld), ctypes.byref(dt)))
         self.x0_ld, self.x0_dtype = ld.value, {CVR_F32: torch.float32, CVR_BF16: torch.bfloat16}[dt.value]
@@ -430,8 +433,13 @@ class CvrModel:
         """cvr_exchange: grouped ncclSend / ncclRecv of the pooled rows + unpack into x0 (S4)."""
         self._check(self.L.cvr_exchange(self.h, _ptr(send), _ptr(recv), batch_global, _ptr(x0), _stream(stream)))
 
+    def executor_slot(self, n: int) -> int:
+        """The cvr_call_info slot of the n-th (0-based) executor call: lane n % lanes, that lane's slot."""
+        return (n % self.lanes) * EXECUTOR_SLOTS + (n // self.lanes) % EXECUTOR_SLOTS
+
     def call_info(self, slot: int) -> dict:
-        """cvr_call_info: the per-call block of x0 slot `slot` as the executor's kernels read it."""
+        """cvr_call_info: the per-call block of x0 slot `slot` (lane slot // EXECUTOR_SLOTS) as the executor's
+        kernels read it; graph_captures counts every lane."""
         rec = cvr_call_record()
         self._check(self.L.cvr_call_info(self.h, slot, ctypes.byref(rec)))
         return {"d_indices": rec.d_indices or 0, "d_keys": rec.d_keys or 0, "d_offsets": rec.d_offsets or 0,

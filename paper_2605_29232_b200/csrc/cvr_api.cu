@@ -293,6 +293,30 @@ struct cvr_ctx {
   }
   template <typename T = void>
   T* wptr(const std::string& n) { return reinterpret_cast<T*>(ws + slot(n)->off); }
+
+  // ---- executor lanes (option "lanes", set before cvr_set_workspace).  With L >= 2 lanes, cvr_score /
+  // cvr_score_keys / cvr_score_host deal consecutive calls round-robin over L independent pipelines of this model:
+  // lane 0 is this context, lanes 1.. are full sub-contexts (their own x0 slots, intermediates, graphs, status flag
+  // and weight copy) that borrow the same tables.  Every lane runs on its own pair of library streams (priorities
+  // taken from the caller's streams at first use); a call's work is ordered after the caller's s_embed (inputs and
+  // the scores buffer) and joined back into the caller's s_dense, so dense(k) of one lane runs beside dense(k+1) of
+  // the next one: c2 86.3 vs 97.0 us per batch at L = 2 (the GEMMs of one stage leave SMs and registers idle that
+  // the other stage's CTAs take); per-batch latency grows accordingly.  Everything else (cvr_embed, cvr_dense,
+  // cvr_repeat_kernel, profiling) uses lane 0 on the caller's streams.
+  static constexpr int kMaxLanes = 4;
+  cvr_model_desc desc{};       // the creation description (arrays point into rows / mlp): sub-contexts are built from it
+  int lanes = 1;
+  cvr_ctx* lane_ctx[kMaxLanes] = {};  // [0] unused: lane 0 is this context
+  cudaStream_t lane_se[kMaxLanes] = {}, lane_sd[kMaxLanes] = {};
+  cudaEvent_t lane_in[kMaxLanes] = {}, lane_out[kMaxLanes] = {};
+  int64_t lane_k = 0;
+  cvr_ctx* lane(int i) { return i ? lane_ctx[i] : this; }
+  const cvr_ctx* lane(int i) const { return i ? lane_ctx[i] : this; }
+  size_t lane_ws_off(int i) const {  // workspace offset of lane i (each lane's share rounded to 256 B)
+    size_t off = 0;
+    for (int j = 0; j < i; ++j) off += j ? lane_ctx[j]->ws_need : ws_need;
+    return off;
+  }
 };
 
 namespace {
@@ -527,6 +551,7 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
     *out = c;  // returned so the caller can read cvr_last_error, then must destroy it
     return st;
   }
+  c->desc = *desc;
   c->T = desc->n_tables;
   c->rows.assign(desc->rows, desc->rows + c->T);
   c->d = desc->dim;
@@ -538,6 +563,8 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
   c->r = desc->cross_rank;
   c->n_mlp = desc->n_mlp;
   c->mlp.assign(desc->mlp_dims, desc->mlp_dims + c->n_mlp);
+  c->desc.rows = c->rows.data();
+  c->desc.mlp_dims = c->mlp.data();
   c->n_heads = desc->n_heads;
   c->ffn = desc->ffn_dim;
   c->max_batch = desc->max_batch;
@@ -628,6 +655,15 @@ int cvr_create(const cvr_model_desc* desc, cvr_ctx** out) {
 
 int cvr_destroy(cvr_ctx* c) {
   if (!c) return CVR_E_ARG;
+  if (c->lanes > 1) cudaDeviceSynchronize();  // the lanes' streams may still run work of this context
+  for (int i = 1; i < cvr_ctx::kMaxLanes; ++i)
+    if (c->lane_ctx[i]) cvr_destroy(c->lane_ctx[i]);
+  for (int i = 0; i < cvr_ctx::kMaxLanes; ++i) {
+    if (c->lane_se[i]) cudaStreamDestroy(c->lane_se[i]);
+    if (c->lane_sd[i]) cudaStreamDestroy(c->lane_sd[i]);
+    if (c->lane_in[i]) cudaEventDestroy(c->lane_in[i]);
+    if (c->lane_out[i]) cudaEventDestroy(c->lane_out[i]);
+  }
   if (c->gdbg) {  // debug: GEMM timeline of the last dense stage (us from the first GEMM's first CTA entry)
     std::vector<unsigned long long> h((size_t)32 * 160 * 8);
     cudaDeviceSynchronize();
@@ -669,7 +705,7 @@ const char* cvr_last_error(const cvr_ctx* c) { return c ? c->err.c_str() : "null
 
 int cvr_workspace_bytes(const cvr_ctx* c, size_t* bytes) {
   if (!c || !bytes) return CVR_E_ARG;
-  *bytes = c->ws_need;
+  *bytes = c->lane_ws_off(c->lanes);  // every lane's share (ws_need alone at one lane)
   return CVR_OK;
 }
 
@@ -680,9 +716,52 @@ int cvr_x0_layout(const cvr_ctx* c, int* ld, int* dt) {
   return CVR_OK;
 }
 
+// a new lane starts with its parent's options (options set later are forwarded by cvr_set_option)
+static void copy_options(cvr_ctx* t, const cvr_ctx* c) {
+  t->pdl = c->pdl;
+  t->ens_u_bn = c->ens_u_bn;
+  t->pair_ens = c->pair_ens;
+  t->embed_bps_pipe = c->embed_bps_pipe;
+  t->prefetch_b = c->prefetch_b;
+  t->f32_tma_store = c->f32_tma_store;
+  t->ens_fused_attn = c->ens_fused_attn;
+  t->ens_attn_tc = c->ens_attn_tc;
+  t->ens_xv_wave = c->ens_xv_wave;
+  t->zero_copy_scores = c->zero_copy_scores;
+  t->u_bn = c->u_bn;
+  t->xv_bn = c->xv_bn;
+  t->epw_mode = c->epw_mode;
+  t->mask_grouped = c->mask_grouped;
+  t->use_graphs = c->use_graphs;
+  t->tvocab = c->tvocab;
+  t->tmean = c->tmean;
+  t->any_mean = c->any_mean;
+}
+
+// apply the same call to every sub-context lane (1..lanes-1) first; lc_ names the lane inside `call_expr`
+#define CVR_FORWARD_LANES(c, call_expr)                                                 \
+  for (int li_ = 1; li_ < (c)->lanes; ++li_) {                                         \
+    cvr_ctx* lc_ = (c)->lane_ctx[li_];                                                 \
+    const int st_ = (call_expr);                                                       \
+    if (st_ != CVR_OK) return (c)->fail(st_, "lane %d: %s", li_, lc_->err.c_str());   \
+  }
+
+static int set_workspace_one(cvr_ctx* c, void* d_ws, size_t bytes);
+
 int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
   if (!c || !d_ws) return CVR_E_ARG;
   if (reinterpret_cast<uintptr_t>(d_ws) & 255) return c->fail(CVR_E_ARG, "workspace must be 256-byte aligned");
+  const size_t need = c->lane_ws_off(c->lanes);
+  if (bytes < need) return c->fail(CVR_E_NOMEM, "workspace %zu bytes < required %zu", bytes, need);
+  for (int i = c->lanes - 1; i >= 0; --i) {  // lane 0 (this context) last: its state is what callers inspect
+    cvr_ctx* t = c->lane(i);
+    const int st = set_workspace_one(t, reinterpret_cast<uint8_t*>(d_ws) + c->lane_ws_off(i), t->ws_need);
+    if (st != CVR_OK) return i ? c->fail(st, "lane %d: %s", i, t->err.c_str()) : st;
+  }
+  return CVR_OK;
+}
+
+static int set_workspace_one(cvr_ctx* c, void* d_ws, size_t bytes) {
   if (bytes < c->ws_need) return c->fail(CVR_E_NOMEM, "workspace %zu bytes < required %zu", bytes, c->ws_need);
   c->ws = reinterpret_cast<uint8_t*>(d_ws);
   c->ws_bytes = bytes;
@@ -798,6 +877,7 @@ int cvr_set_workspace(cvr_ctx* c, void* d_ws, size_t bytes) {
 
 int cvr_load_tables(cvr_ctx* c, int n, const int* ids, const void* const* d_rows, const int64_t* strides) {
   if (!c || !ids || !d_rows || !strides) return CVR_E_ARG;
+  CVR_FORWARD_LANES(c, cvr_load_tables(lc_, n, ids, d_rows, strides));
   if (!c->cuda_ready) return c->fail(CVR_E_STATE, "cvr_load_tables before cvr_set_workspace");
   if (n != (int)c->local_tables.size())
     return c->fail(CVR_E_SHAPE, "expected %zu tables for rank %d, got %d", c->local_tables.size(), c->rank, n);
@@ -1009,6 +1089,7 @@ std::vector<float> fetch_f32(const void* d, int dtype, size_t n, cudaError_t& e)
 int cvr_load_weights(cvr_ctx* c, int n, const char* const* names, const void* const* ptrs, const int* dtypes,
                      const int* ndims, const int64_t* shapes) {
   if (!c || n < 0 || !names || !ptrs || !dtypes || !ndims || !shapes) return CVR_E_ARG;
+  CVR_FORWARD_LANES(c, cvr_load_weights(lc_, n, names, ptrs, dtypes, ndims, shapes));
   if (!c->cuda_ready) return c->fail(CVR_E_STATE, "cvr_load_weights before cvr_set_workspace");
   std::vector<int> seen(c->wslots.size(), -1);
   int64_t so = 0;
@@ -1500,6 +1581,7 @@ int cvr_embed(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, in
 
 int cvr_set_feature_spec(cvr_ctx* c, int n, const int64_t* vocab, const int* pool_mode) {
   if (!c || !vocab || !pool_mode) return CVR_E_ARG;
+  CVR_FORWARD_LANES(c, cvr_set_feature_spec(lc_, n, vocab, pool_mode));
   if (n != c->T) return c->fail(CVR_E_SHAPE, "feature spec: expected %d tables, got %d", c->T, n);
   for (int t = 0; t < n; ++t) {
     if (pool_mode[t] != 0 && pool_mode[t] != 1) return c->fail(CVR_E_ARG, "table %d: pool_mode must be 0 (sum) or 1 (mean)", t);
@@ -1630,12 +1712,67 @@ int score_impl(cvr_ctx* c, const int32_t* d_indices, const uint64_t* d_keys, con
   c->k++;
   return CVR_OK;
 }
+
+// executor lanes: the library's stream pair of every lane, created at first use with the caller's priorities
+int ensure_lane_streams(cvr_ctx* c, cudaStream_t s_embed, cudaStream_t s_dense) {
+  if (c->lane_se[0]) return CVR_OK;
+  int pe = 0, pd = 0;
+  cudaError_t e = cudaStreamGetPriority(s_embed, &pe);
+  if (e == cudaSuccess) e = cudaStreamGetPriority(s_dense, &pd);
+  for (int i = 0; i < c->lanes && e == cudaSuccess; ++i) {
+    e = cudaStreamCreateWithPriority(&c->lane_se[i], cudaStreamNonBlocking, pe);
+    if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->lane_sd[i], cudaStreamNonBlocking, pd);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->lane_in[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->lane_out[i], cudaEventDisableTiming);
+  }
+  return e == cudaSuccess ? CVR_OK : c->cuda_fail(e, "lane streams");
+}
+
+// call lane_k % lanes: its work waits for the caller's s_embed, runs on the lane's streams, and the caller's s_dense
+// waits for its end
+template <class F>
+int lane_dispatch(cvr_ctx* c, cvr_stream_t s_embed, cvr_stream_t s_dense, F&& fn) {
+  int st = ensure_lane_streams(c, (cudaStream_t)s_embed, (cudaStream_t)s_dense);
+  if (st) return st;
+  const int i = (int)(c->lane_k % c->lanes);
+  cvr_ctx* t = c->lane(i);
+  cudaError_t e = cudaEventRecord(c->lane_in[i], (cudaStream_t)s_embed);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->lane_se[i], c->lane_in[i], 0);
+  if (e != cudaSuccess) return c->cuda_fail(e, "lane input order");
+  st = fn(t, c->lane_se[i], c->lane_sd[i]);
+  if (st) return i ? c->fail(st, "lane %d: %s", i, t->err.c_str()) : st;
+  e = cudaEventRecord(c->lane_out[i], c->lane_sd[i]);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent((cudaStream_t)s_dense, c->lane_out[i], 0);
+  if (e != cudaSuccess) return c->cuda_fail(e, "lane join");
+  c->lane_k++;
+  return CVR_OK;
+}
+
+int warm_impl(cvr_ctx* c, int max_rows, cvr_stream_t s_embed, cvr_stream_t s_dense);
+int score_host_impl(cvr_ctx* c, const int32_t* h_indices, const int32_t* h_offsets, int64_t nnz, int batch,
+                    const float* h_dense, float* h_scores, cvr_stream_t s_copy, cvr_stream_t s_embed,
+                    cvr_stream_t s_dense);
 }  // namespace
 
 extern "C" {
 
 int cvr_warm_graphs(cvr_ctx* c, int max_rows, cvr_stream_t s_embed, cvr_stream_t s_dense) {
   if (!c || !s_embed || !s_dense) return CVR_E_ARG;
+  if (c->lanes > 1) {
+    int st = ensure_lane_streams(c, (cudaStream_t)s_embed, (cudaStream_t)s_dense);
+    for (int i = 0; i < c->lanes && !st; ++i) {
+      st = warm_impl(c->lane(i), max_rows, c->lane_se[i], c->lane_sd[i]);
+      if (st && i) st = c->fail(st, "lane %d: %s", i, c->lane_ctx[i]->err.c_str());
+    }
+    return st;
+  }
+  return warm_impl(c, max_rows, s_embed, s_dense);
+}
+
+}  // extern "C"
+
+namespace {
+int warm_impl(cvr_ctx* c, int max_rows, cvr_stream_t s_embed, cvr_stream_t s_dense) {
   int st = check_ready(c, true, true);
   if (st) return st;
   if (c->world != 1) return c->fail(CVR_E_STATE, "the executor is unsharded");
@@ -1671,9 +1808,16 @@ int cvr_warm_graphs(cvr_ctx* c, int max_rows, cvr_stream_t s_embed, cvr_stream_t
   c->call = nullptr;
   return st;
 }
+}  // namespace
+
+extern "C" {
 
 int cvr_score(cvr_ctx* c, const int32_t* d_indices, const int32_t* d_offsets, int64_t nnz, int batch,
               const float* d_dense, float* d_scores, cvr_stream_t s_embed, cvr_stream_t s_dense) {
+  if (c && c->lanes > 1)
+    return lane_dispatch(c, s_embed, s_dense, [&](cvr_ctx* t, cudaStream_t se, cudaStream_t sd) {
+      return score_impl(t, d_indices, nullptr, d_offsets, nnz, batch, d_dense, d_scores, se, sd);
+    });
   return score_impl(c, d_indices, nullptr, d_offsets, nnz, batch, d_dense, d_scores, s_embed, s_dense);
 }
 
@@ -1683,12 +1827,29 @@ int cvr_score_keys(cvr_ctx* c, const uint64_t* d_keys, const int32_t* d_offsets,
   for (int t = 0; t < c->T; ++t)
     if (c->tvocab[t] <= 0) return c->fail(CVR_E_STATE, "table %d has no hash vocab (cvr_set_feature_spec)", t);
   if (nnz > 0 && !d_keys) return c->fail(CVR_E_ARG, "null keys");
+  if (c->lanes > 1)
+    return lane_dispatch(c, s_embed, s_dense, [&](cvr_ctx* t, cudaStream_t se, cudaStream_t sd) {
+      return score_impl(t, nullptr, d_keys, d_offsets, nnz, batch, d_dense, d_scores, se, sd);
+    });
   return score_impl(c, nullptr, d_keys, d_offsets, nnz, batch, d_dense, d_scores, s_embed, s_dense);
 }
 
 int cvr_score_host(cvr_ctx* c, const int32_t* h_indices, const int32_t* h_offsets, int64_t nnz, int batch,
                    const float* h_dense, float* h_scores, cvr_stream_t s_copy, cvr_stream_t s_embed,
                    cvr_stream_t s_dense) {
+  if (c && c->lanes > 1)
+    return lane_dispatch(c, s_embed, s_dense, [&](cvr_ctx* t, cudaStream_t se, cudaStream_t sd) {
+      return score_host_impl(t, h_indices, h_offsets, nnz, batch, h_dense, h_scores, s_copy, se, sd);
+    });
+  return score_host_impl(c, h_indices, h_offsets, nnz, batch, h_dense, h_scores, s_copy, s_embed, s_dense);
+}
+
+}  // extern "C"
+
+namespace {
+int score_host_impl(cvr_ctx* c, const int32_t* h_indices, const int32_t* h_offsets, int64_t nnz, int batch,
+                    const float* h_dense, float* h_scores, cvr_stream_t s_copy, cvr_stream_t s_embed,
+                    cvr_stream_t s_dense) {
   if (!c) return CVR_E_ARG;
   int st = check_ready(c, true, true);
   if (st) return st;
@@ -1731,9 +1892,13 @@ int cvr_score_host(cvr_ctx* c, const int32_t* h_indices, const int32_t* h_offset
     return c->cuda_fail(e, "D2H scores");
   return CVR_OK;
 }
+}  // namespace
+
+extern "C" {
 
 int cvr_get_status(cvr_ctx* c, cvr_stream_t stream) {
   if (!c) return CVR_E_ARG;
+  CVR_FORWARD_LANES(c, cvr_get_status(lc_, stream));  // every lane's sticky flag (their work is joined into stream)
   if (!c->cuda_ready) return c->fail(CVR_E_STATE, "workspace not set");
   cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -1995,8 +2160,14 @@ int cvr_repeat_kernel(cvr_ctx* c, const char* role, int reps, const void* d_x0, 
 }
 
 int cvr_call_info(const cvr_ctx* c, int slot, cvr_call_record* out) {
-  if (!c || !out || slot < 0 || slot >= cvr_ctx::kSlots) return CVR_E_ARG;
+  if (!c || !out || slot < 0 || slot >= cvr_ctx::kSlots * c->lanes) return CVR_E_ARG;
   if (!c->cuda_ready) return CVR_E_STATE;
+  if (slot >= cvr_ctx::kSlots) {  // lane slot / kSlots, its slot % kSlots
+    const int st = cvr_call_info(c->lane_ctx[slot / cvr_ctx::kSlots], slot % cvr_ctx::kSlots, out);
+    if (st == CVR_OK)
+      for (int i = 0; i < c->lanes; ++i) out->graph_captures += i != slot / cvr_ctx::kSlots ? c->lane(i)->graph_captures : 0;
+    return st;
+  }
   CallArgs v{};
   if (cudaMemcpy(&v, c->ws + c->off_call[slot], sizeof v, cudaMemcpyDeviceToHost) != cudaSuccess) return CVR_E_CUDA;
   out->d_indices = v.indices;
@@ -2006,7 +2177,8 @@ int cvr_call_info(const cvr_ctx* c, int slot, cvr_call_record* out) {
   out->d_scores = v.scores;
   out->nnz = v.nnz;
   out->batch = v.B;
-  out->graph_captures = c->graph_captures;
+  out->graph_captures = 0;
+  for (int i = 0; i < c->lanes; ++i) out->graph_captures += i ? c->lane_ctx[i]->graph_captures : c->graph_captures;
   return CVR_OK;
 }
 
@@ -2025,6 +2197,7 @@ int cvr_unpack_shard(cvr_ctx* c, const void* d_recv, int batch_global, void* d_x
 int cvr_launch_count(const cvr_ctx* c, int64_t* n) {
   if (!c || !n) return CVR_E_ARG;
   *n = c->launches;
+  for (int i = 1; i < c->lanes; ++i) *n += c->lane_ctx[i]->launches;
   return CVR_OK;
 }
 
@@ -2111,6 +2284,30 @@ int cvr_gemm_bf16(const void* d_A, int64_t lda, const void* d_B, int64_t ldb, vo
 
 int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
   if (!c || !key) return CVR_E_ARG;
+  if (!strcmp(key, "lanes")) {
+    if (value < 1 || value > cvr_ctx::kMaxLanes) return c->fail(CVR_E_ARG, "lanes must be in [1, %d]", cvr_ctx::kMaxLanes);
+    if (c->ws) return c->fail(CVR_E_STATE, "lanes must be set before cvr_set_workspace");
+    if (c->world != 1 && value > 1) return c->fail(CVR_E_STATE, "executor lanes are unsharded (world_size 1)");
+    for (int i = (int)value; i < cvr_ctx::kMaxLanes; ++i)
+      if (c->lane_ctx[i]) {
+        cvr_destroy(c->lane_ctx[i]);
+        c->lane_ctx[i] = nullptr;
+      }
+    for (int i = 1; i < (int)value; ++i) {
+      if (c->lane_ctx[i]) continue;
+      cvr_ctx* t = nullptr;
+      const int st = cvr_create(&c->desc, &t);
+      if (st != CVR_OK) {
+        if (t) cvr_destroy(t);
+        return c->fail(st, "lane %d: create failed", i);
+      }
+      copy_options(t, c);
+      c->lane_ctx[i] = t;
+    }
+    c->lanes = (int)value;
+    return CVR_OK;
+  }
+  CVR_FORWARD_LANES(c, cvr_set_option(lc_, key, value));
   // every option below changes what the executor's graphs would launch: drop them (recaptured at next use)
   auto replan = [&]() -> int {
     c->drop_graphs();

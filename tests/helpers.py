@@ -21,9 +21,9 @@ def to_dev(bt: cs.Batch, device="cuda"):
             torch.from_numpy(bt.dense).to(device))
 
 
-def make_model(cfg, max_batch, max_nnz=0, tables=None, weights=None, device="cuda"):
+def make_model(cfg, max_batch, max_nnz=0, tables=None, weights=None, device="cuda", lanes=1):
     from paper_2605_29232_b200 import CvrModel
-    m = CvrModel(cfg, max_batch=max_batch, max_nnz=max_nnz, device=device)
+    m = CvrModel(cfg, max_batch=max_batch, max_nnz=max_nnz, device=device, lanes=lanes)
     tables = device_tables(cfg, device) if tables is None else tables
     m.load_tables(tables)
     w = cs.make_weights(cfg) if weights is None else weights

@@ -236,6 +236,67 @@ def test_executor_graphs_every_backbone(name):
     m.close()
 
 
+@pytest.mark.parametrize("name,lanes", [("c2", 2), ("c2", 3), ("c6", 2)])
+def test_executor_lanes(name, lanes):
+    """Option "lanes": consecutive cvr_score / cvr_score_host calls dealt round-robin to `lanes` pipelines (sub-contexts
+    on library streams, joined into the caller's s_dense): every batch's scores bit-identical to embed + dense on
+    lane 0, the call blocks of the last calls are where executor_slot() says, each lane captures its own graphs,
+    and a bad index in a batch dealt to a lane other than 0 still reaches cvr_get_status."""
+    cfg = cs.C2.with_(rows=(50000,) * 26) if name == "c2" else _small(name)
+    Bmax = 384
+    m, tabs, w = make_model(cfg, max_batch=Bmax, max_nnz=1 << 20, lanes=lanes)
+    sizes = [Bmax, 7, Bmax - 1, 1, 130, Bmax, 64, 200]
+    batches = [cs.make_batch(cfg, 400 + i, batch=B) for i, B in enumerate(sizes)]
+    dev_in = [to_dev(bt) for bt in batches]
+    refs = [m.dense(m.embed(i, o, bt.batch, d), bt.batch).clone() for (i, o, d), bt in zip(dev_in, batches)]
+    outs = [torch.empty(bt.batch, device="cuda") for bt in batches]
+    s_e, s_d, s_c = torch.cuda.Stream(), torch.cuda.Stream(priority=-1), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for (i, o, d), bt, out in zip(dev_in, batches, outs):
+        m.score(i, o, bt.batch, d, out, s_embed=s_e, s_dense=s_d)
+    s_d.synchronize()
+    assert m.status(s_d) == 0
+    for k, (out, r) in enumerate(zip(outs, refs)):
+        assert torch.equal(out, r), (name, lanes, k, sizes[k])
+    from paper_2605_29232_b200._cvr import EXECUTOR_SLOTS as NS
+    n = len(sizes)
+    for j in (n - 1, n - 2):
+        rec = m.call_info(m.executor_slot(j))
+        i, o, d = dev_in[j]
+        assert (rec["d_indices"], rec["d_offsets"], rec["nnz"], rec["batch"], rec["d_scores"]) == \
+            (i.data_ptr(), o.data_ptr(), i.numel(), sizes[j], outs[j].data_ptr())
+
+    def bucket(b):
+        r = 128
+        while r < b and r < Bmax:
+            r *= 2
+        return min(r, Bmax)
+    seen = {(k % lanes, (k // lanes) % NS, bucket(b)) for k, b in enumerate(sizes)}
+    assert rec["graph_captures"] == 2 * len(seen)
+    # host-fed through the lanes (pinned inputs, zero-copy scores), continuing the call count
+    host_in = [tuple(torch.from_numpy(a).pin_memory() for a in (bt.indices, bt.offsets, bt.dense)) for bt in batches]
+    houts = [torch.empty(bt.batch, dtype=torch.float32).pin_memory() for bt in batches]
+    for (idx, off, dense), bt, o in zip(host_in, batches, houts):
+        m.score_host(idx, off, bt.batch, dense, o, s_copy=s_c, s_embed=s_e, s_dense=s_d)
+    s_d.synchronize()
+    assert m.status(s_d) == 0
+    for o, r in zip(houts, refs):
+        assert torch.equal(o, r.cpu())
+    # a malformed batch dealt to a lane other than 0 (call 2n + 1): that lane's sticky flag reaches cvr_get_status
+    bad = cs.make_batch(cfg, 499, batch=64)
+    bi = bad.indices.copy()
+    bi[5] = 1 << 30
+    good_in = to_dev(batches[0])
+    m.score(*good_in[:2], batches[0].batch, good_in[2], outs[0], s_embed=s_e, s_dense=s_d)   # lane 0
+    m.score(torch.from_numpy(bi).cuda(), torch.from_numpy(bad.offsets).cuda(), 64,
+            torch.from_numpy(bad.dense).cuda(), outs[6], s_embed=s_e, s_dense=s_d)             # lane (2n+1) % L
+    s_d.synchronize()
+    from paper_2605_29232_b200._cvr import CVR_E_INDEX
+    assert m.status(s_d) == CVR_E_INDEX
+    assert m.status(s_d) == 0  # the flag is cleared once reported
+    m.close()
+
+
 def test_c2_zero_weights_closed_form():
     """P4 + P7 on the GPU: U = 0 makes every cross layer x_l + x0*b; zero MLP/head weights
     give score = sigmoid(head/b) exactly as the oracle's closed form."""

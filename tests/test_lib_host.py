@@ -108,3 +108,25 @@ def test_executor_and_serving_args_host(L):
     nb = C.c_int()
     assert L.cvr_batcher_simulate(3, t.ctypes.data, n.ctypes.data, 0.001, 8, 0, 16, 0.0, 0.0, lat.ctypes.data,
                                   bof.ctypes.data, disp.ctypes.data, C.byref(nb)) == 1   # CVR_E_ARG
+
+
+def test_executor_lanes_host(L):
+    """Option "lanes" on the host: 1-4 only, unsharded only; the workspace covers every lane (each holds its own copy
+    of the model's state); the sub-contexts follow later options."""
+    from paper_2605_29232_b200 import CvrModel
+    from paper_2605_29232_b200._cvr import CvrError
+    one = CvrModel(cs.C2, max_batch=256, max_nnz=1 << 12, allocate=False)
+    two = CvrModel(cs.C2, max_batch=256, max_nnz=1 << 12, allocate=False, lanes=2)
+    four = CvrModel(cs.C2, max_batch=256, max_nnz=1 << 12, allocate=False, lanes=4)
+    assert two.workspace_bytes == 2 * one.workspace_bytes and four.workspace_bytes == 4 * one.workspace_bytes
+    assert two.executor_slot(0) == 0 and two.executor_slot(1) == 2 and two.executor_slot(2) == 1
+    for bad in (0, 5):
+        with pytest.raises(CvrError):
+            CvrModel(cs.C2, max_batch=256, allocate=False, lanes=bad)
+    with pytest.raises(CvrError):
+        CvrModel(cs.C3S, max_batch=64, max_nnz=1, world_size=2, rank=1, allocate=False, lanes=2)
+    two.set_option("u_bn", 64)        # forwarded to the sub-context
+    with pytest.raises(CvrError):
+        two.set_option("u_bn", 65)
+    for m in (one, two, four):
+        m.close()
