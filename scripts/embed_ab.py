@@ -26,8 +26,11 @@ cbyts = sum(distinct_rows(b) * row + b.nnz * 4 + (cfg.n_tables * B + 1) * 4 + B 
 s = torch.cuda.Stream()
 x0 = m.new_x0(B)
 K = 200
+settings = json.loads(sys.argv[1]) if len(sys.argv) > 1 else [{}]
 for rep in range(3):
-    for v2 in [0]:
+    for v2 in settings:
+        for k, v in v2.items():
+            m.set_option(k, v)
         for i in range(8):
             m.embed(*dev[i % 4][:2], B, dev[i % 4][2], x0=x0, stream=s)
         torch.cuda.synchronize()
@@ -37,4 +40,6 @@ for rep in range(3):
                           "us": round(us, 2), "GBps_alg": round(byts / us / 1e3, 1),
                           "frac_hbm": round(byts / us / 1e3 / 6556.5, 3),
                           "frac_hbm_compulsory": round(cbyts / us / 1e3 / 6556.5, 3)}))
+        for k in v2:  # (every option this script varies defaults to 0)
+            m.set_option(k, 0)
 assert m.status(s) == 0

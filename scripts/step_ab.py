@@ -6,7 +6,7 @@ from paper_2605_29232_b200 import CvrModel
 cfg = cs.CONFIGS[os.environ.get("CFG", "c2")]; B = cfg.batch
 NR = int(os.environ.get("RING", "8"))
 ring = [cs.make_batch(cfg, 900 + i) for i in range(NR)]
-m = CvrModel(cfg, max_batch=B, max_nnz=max(b.nnz for b in ring))
+m = CvrModel(cfg, max_batch=B, max_nnz=max(b.nnz for b in ring), lanes=int(os.environ.get("LANES", "1")))
 tabs = [s.materialize(device="cuda") for s in cs.table_specs(cfg)]
 m.load_tables(tabs); m.load_weights({k: v.cuda() for k, v in cs.make_weights(cfg).items()})
 dev = [(torch.from_numpy(b.indices).cuda(), torch.from_numpy(b.offsets).cuda(), torch.from_numpy(b.dense).cuda()) for b in ring]
