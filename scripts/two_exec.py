@@ -19,7 +19,8 @@ for E in [int(x) for x in os.environ.get("E", "1,2").split(",")]:
     for e in range(E):
         m = CvrModel(cfg, max_batch=B, max_nnz=max(b.nnz for b in ring))
         m.load_tables(tabs); m.load_weights(w)
-        ms.append((m, torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1)))
+        pr = [int(x) for x in os.environ.get("PRIOS", "0,-1," * E).strip(",").split(",")]
+        ms.append((m, torch.cuda.Stream(priority=pr[2 * e]), torch.cuda.Stream(priority=pr[2 * e + 1])))
     def step(i):
         m, se, sd = ms[i % E]
         ip, op, nnz, dp, sp = raw[i % NR]
