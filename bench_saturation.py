@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--rel-eps", type=float, default=0.07)
     ap.add_argument("--max-items", type=int, default=8192)
     ap.add_argument("--pool", type=int, default=1 << 16)
+    ap.add_argument("--lanes", type=int, default=1, help="executor lanes of the served model (cvr.h option)")
     args = ap.parse_args()
     cfg = cs.C2
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
@@ -46,7 +47,7 @@ def main():
     view = ItemPoolView(pool.offsets, pool.indices, pool.dense, cfg.n_tables)
     item_nnz = np.diff(pool.offsets).reshape(cfg.n_tables, args.pool).sum(axis=0)
     max_nnz = int(np.sort(item_nnz)[-args.max_items:].sum())
-    m = CvrModel(cfg, max_batch=args.max_items, max_nnz=max_nnz, device=dev)
+    m = CvrModel(cfg, max_batch=args.max_items, max_nnz=max_nnz, device=dev, lanes=args.lanes)
     m.load_tables([s.materialize(device=dev) for s in cs.table_specs(cfg)])
     m.load_weights({k: v.to(dev) for k, v in cs.make_weights(cfg).items()})
     log = []
