@@ -30,12 +30,13 @@ using namespace cvr;
 enum KernelId {
   K_EMBED = 0, K_GEMM_V, K_GEMM_U, K_GEMM_MLP, K_GEMM_HEAD, K_DENSE_F32, K_UNPACK, K_ENS_QKV, K_MHA,
   K_ENS_FFN1, K_ENS_FFN2_LN, K_HEAD_FIN, K_MASK_PROJ, K_MASK_HIDDEN, K_MASK_MUL, K_ENS_QKV_ATTN, K_SET_CALL,
-  K_PEER, K_COUNT
+  K_PEER, K_ENS_FFN_FUSED, K_COUNT
 };
 static const char* kKernelNames[K_COUNT] = {
     "embed_bag_pool", "gemm_xV",  "gemm_tU_cross",  "gemm_mlp_relu", "gemm_mlp_head", "dense_f32_dcn",
     "shard_unpack",   "gemm_ens_qkv", "mha64", "gemm_ens_ffn1", "gemm_ens_ffn2_ln", "head_finalize",
-    "gemm_mask_proj", "gemm_mask_hidden", "gemm_mask_mul", "gemm_ens_qkv_attn", "set_call", "peer_flags"};
+    "gemm_mask_proj", "gemm_mask_hidden", "gemm_mask_mul", "gemm_ens_qkv_attn", "set_call", "peer_flags",
+    "gemm_ens_ffn_fused"};
 
 namespace {
 
@@ -174,6 +175,7 @@ struct cvr_ctx {
     bool st_S_ok = false;
     std::vector<CUtensorMap> V, U, Wqkv, W1, Wcat;
     std::vector<CUtensorMap> V256;                     // V with 256-row boxes: t = X V^T as one-wave 128 x 256 tiles
+    std::vector<CUtensorMap> W1f, W2f, Wof;            // the fused FFN's weight boxes (W1 128 rows; W2 256; Wo 128)
     CUtensorMap tok_user;
   } ens;
   // MaskNet: x0' = ReLU(W_in x0 + b_in) [B, Wp]; H = ReLU(x0' V_all^T + c_all)
@@ -215,6 +217,9 @@ struct cvr_ctx {
   // version with P staged in shared memory and one epilogue group ran 597 us
   bool ens_attn_tc = true;
   bool ens_xv_wave = true;      // option "ens_xv_wave": config 4's t = X V^T as one wave of 128 x 256 tiles
+  // option "ens_ffn_fused": config 4's FFN1 + out-projection + FFN2 + LN as one kernel (ffn_fused.cu; the hidden
+  // activations never reach HBM), bit-identical to FFN1 GEMM + [O | h] GEMM with the LN epilogue
+  bool ens_ffn_fused = false;
   bool zero_copy_scores = true;  // option "zero_copy_scores": cvr_score_host writes scores into pinned h_scores
   int u_bn = 192;              // option "u_bn": N tile of the low-rank U GEMM (192 when W % 192 == 0, else 64)
   int xv_bn = 0;               // option "xv_bn": N tile of t = x_l V^T (0 = by wave count, see pick_bn_xv)
@@ -727,6 +732,7 @@ static void copy_options(cvr_ctx* t, const cvr_ctx* c) {
   t->ens_fused_attn = c->ens_fused_attn;
   t->ens_attn_tc = c->ens_attn_tc;
   t->ens_xv_wave = c->ens_xv_wave;
+  t->ens_ffn_fused = c->ens_ffn_fused;
   t->zero_copy_scores = c->zero_copy_scores;
   t->u_bn = c->u_bn;
   t->xv_bn = c->xv_bn;
@@ -946,6 +952,9 @@ int encode_plan_ensemble(cvr_ctx* c) {
   E.V256.assign(c->n_cross, {});
   E.W1.assign(c->n_cross, {});
   E.Wcat.assign(c->n_cross, {});
+  E.W1f.assign(c->n_cross, {});
+  E.W2f.assign(c->n_cross, {});
+  E.Wof.assign(c->n_cross, {});
   bool ok = true;
   for (int l = 0; l < c->n_cross; ++l) {
     const std::string p = "ens/" + std::to_string(l) + "/";
@@ -967,6 +976,9 @@ int encode_plan_ensemble(cvr_ctx* c) {
     cudaError_t e5 = cudaMemcpy(c->ws + E.off_catb[l], bo.data(), D * 4, cudaMemcpyHostToDevice);
     if (e1 || e2 || e3 || e4 || e5) return c->fail(CVR_E_CUDA, "assembling [Wo | W2]");
     ok &= encode_tmap_bf16(&E.Wcat[l], c->ws + E.off_catW[l], D, D + F, D + F, 256 / dv, &er) == 0;
+    ok &= encode_tmap_bf16(&E.W1f[l], c->wptr(p + "ffn/W1"), F, D, D, 128, &er) == 0;
+    ok &= encode_tmap_bf16(&E.W2f[l], c->ws + E.off_catW[l], D, D + F, D + F, 256, &er) == 0;
+    ok &= encode_tmap_bf16(&E.Wof[l], c->ws + E.off_catW[l], D, D + F, D + F, 128, &er) == 0;
     // head-major [q_h | k_h | v_h] copies of Wqkv / bqkv for the fused QKV + attention GEMM (EPI_ATTN)
     if (D == 64 * c->n_heads) {
       std::vector<float> bq(3 * D), bh(3 * D);
@@ -1377,6 +1389,40 @@ int do_dense_ensemble(cvr_ctx* c, const CUtensorMap* flat_x0, const CUtensorMap*
         c->pend(K_MHA, s);
         if (e != cudaSuccess) return c->cuda_fail(e, "mha64");
       }
+    }
+    if (c->ens_ffn_fused && D == 256 && c->ffn % 128 == 0) {
+      // FFN1 + out-projection + FFN2 + branch-sum LN in one kernel: h stays in TMEM / shared memory
+      FfnArgs f{};
+      f.tmX = tok_xl;
+      f.tmO = &E.tm_cat;
+      f.tmW1 = &E.W1f[l];
+      f.tmW2 = &E.W2f[l];
+      f.tmWo = &E.Wof[l];
+      f.tmS = &E.ld_Stok;
+      f.tmOut = even ? &E.sttok_xa : &E.sttok_xb;
+      f.b1 = c->wptr<float>(p + "ffn/b1");
+      f.bcat = c->at<float>(E.off_catb[l]);
+      f.gamma = c->wptr<float>(p + "ln/gamma");
+      f.beta = c->wptr<float>(p + "ln/beta");
+      f.M = BT;
+      f.F = c->ffn;
+      f.D = D;
+      f.m_mult = T;
+      f.num_sms = c->num_sms;
+      f.pdl = c->pdl;
+      f.call = c->call;
+      if (c->only_kid < 0 || c->only_kid == K_ENS_FFN_FUSED) {
+        const int reps = c->only_kid == K_ENS_FFN_FUSED ? c->only_reps : 1;
+        for (int i = 0; i < reps; ++i) {
+          c->pbeg(s);
+          e = launch_ffn_fused(f, s);
+          c->pend(K_ENS_FFN_FUSED, s);
+          if (e != cudaSuccess) return c->cuda_fail(e, "ens fused ffn");
+        }
+      }
+      flat_xl = even ? &E.flat_xa : &E.flat_xb;
+      tok_xl = even ? &E.tok_xa : &E.tok_xb;
+      continue;
     }
     // FFN hidden -> cat[:, D:]
     GemmArgs a5 = ga(tok_xl, &E.W1[l], BT, c->ffn, D, 256, EPI_BIAS_RELU);
@@ -2323,6 +2369,7 @@ int cvr_set_option(cvr_ctx* c, const char* key, int64_t value) {
   if (!strcmp(key, "pair")) return flag(c->pair_ens);
   if (!strcmp(key, "f32_tma_store")) return flag(c->f32_tma_store);
   if (!strcmp(key, "ens_xv_wave")) return flag(c->ens_xv_wave);
+  if (!strcmp(key, "ens_ffn_fused")) return flag(c->ens_ffn_fused);
   if (!strcmp(key, "ens_fused_attn")) return flag(c->ens_fused_attn);
   if (!strcmp(key, "ens_attn_tc")) return flag(c->ens_attn_tc);
   if (!strcmp(key, "mask_grouped")) return flag(c->mask_grouped);

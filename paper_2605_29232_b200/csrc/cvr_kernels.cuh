@@ -98,6 +98,20 @@ struct DenseF32Args {
 };
 cudaError_t launch_dense_f32(const DenseF32Args& a, cudaStream_t s);
 
+// ---- config 4: FFN1 + out-projection + FFN2 + branch-sum LN in one tcgen05 kernel (ffn_fused.cu) ----------
+struct FfnArgs {
+  const CUtensorMap *tmX, *tmO;          // X tokens [M, D] and cat [M, D + F] (O = its first D columns), box 64 x 128
+  const CUtensorMap *tmW1;               // W1 [F, D], box 64 x 128
+  const CUtensorMap *tmW2, *tmWo;        // [Wo | W2] [D, D + F]: box 64 x 256 (W2 part), 64 x 128 (Wo halves)
+  const CUtensorMap *tmS;                // S fp32 [M, D] (the DCN branch), box 32 x 32
+  const CUtensorMap *tmOut;              // X' bf16 [M, D], store box 64 x 32
+  const float *b1, *bcat, *gamma, *beta; // b1 [F]; bo + b2 [D]; LN affine [D]
+  int M, F, D, m_mult, num_sms;
+  bool pdl;
+  const CallArgs* call;                  // executor graphs: tokens = call->B * m_mult
+};
+cudaError_t launch_ffn_fused(const FfnArgs& g, cudaStream_t s);
+
 // ---- K4: tcgen05 bf16 GEMM with fused epilogues --------------------------------------------------
 enum Epi {
   EPI_STORE = 0,         // bf16 C

@@ -163,3 +163,23 @@ def test_c4_attention_on_tcgen05(c4small, B):
     # the two cores differ only by fp32 summation order (then bf16 rounding flips amplified through 4 layers):
     # their distance to the oracle must be of the same size
     assert np.percentile(err, 99) <= 1.5 * np.percentile(err_ref, 99) + 1e-4
+
+
+@pytest.mark.parametrize("B", [131, 512])
+def test_c4_fused_ffn_bitexact(c4small, B):
+    """Option ens_ffn_fused: FFN1 + out-projection + FFN2 + branch-sum LN as one kernel (the hidden activations stay in
+    TMEM / shared memory): the output accumulator sees the unfused GEMM's K order and every rounding point is the
+    same, so scores are bit-identical to FFN1 GEMM + [O | h] GEMM with the LN epilogue.  B = 131: 8384 tokens, the
+    last 128-token tile holds 64."""
+    cfg, m, tabs, w = c4small
+    bt = cs.make_batch(cfg, 12, batch=B)
+    idx, off, dense = to_dev(bt)
+    x0 = m.embed(idx, off, B, dense)
+    s0 = m.dense(x0, B).clone()
+    m.set_option("ens_ffn_fused", 1)
+    try:
+        s1 = m.dense(x0, B).clone()
+    finally:
+        m.set_option("ens_ffn_fused", 0)
+    assert m.status() == 0
+    assert torch.equal(s0, s1), (s0 - s1).abs().max().item()
