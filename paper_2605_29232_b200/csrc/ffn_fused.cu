@@ -60,8 +60,9 @@ __global__ void __launch_bounds__(FFN_THREADS, 1)
   uint64_t* afull = xempty + 1;      // [2] FFN1 accumulator ready
   uint64_t* aempty = afull + 2;      // [2] FFN1 accumulator drained (4 warps)
   uint64_t* hfull = aempty + 2;      // h chunk staged (4 warps)
-  uint64_t* hempty = hfull + 1;      // h chunk read by FFN2
-  uint64_t* ofull = hempty + 1;      // output accumulator complete
+  uint64_t* hempty = hfull + 1;      // [2] h k-block kb read by FFN2 (the epilogue refills k-block 0 while FFN2
+                                     // still reads k-block 1)
+  uint64_t* ofull = hempty + 2;      // output accumulator complete
   uint64_t* oempty = ofull + 1;      // output accumulator drained (4 warps)
   uint64_t* sfull = oempty + 1;      // [4 warps][2] S chunk landed
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(sfull + 8);
@@ -83,7 +84,8 @@ __global__ void __launch_bounds__(FFN_THREADS, 1)
       ptx::mbar_init(&aempty[b], 4);
     }
     ptx::mbar_init(hfull, 4);
-    ptx::mbar_init(hempty, 1);
+    ptx::mbar_init(&hempty[0], 1);
+    ptx::mbar_init(&hempty[1], 1);
     ptx::mbar_init(ofull, 1);
     ptx::mbar_init(oempty, 4);
     for (int i = 0; i < 8; ++i) ptx::mbar_init(&sfull[i], 1);
@@ -204,8 +206,8 @@ __global__ void __launch_bounds__(FFN_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < 4; ++k) ptx::umma_bf16_ss(tmem, ad + 2 * k, bd + 2 * k, id256, 1);
           release();
+          ptx::umma_commit(&hempty[kb]);
         }
-        ptx::umma_commit(hempty);
         ++hc;
         (void)c;
       };
@@ -258,7 +260,6 @@ __global__ void __launch_bounds__(FFN_THREADS, 1)
         const int b = ca & 1;
         ptx::mbar_wait(&afull[b], (ca >> 1) & 1);
         ptx::tc_fence_after();
-        if (hc >= 1) ptx::mbar_wait(hempty, (hc - 1) & 1);  // FFN2 of the previous chunk has read sH
         const uint32_t trow = tmem + 256 + 128 * b + lanebase;
         const uint32_t hbase = ptx::smem_u32(sH);
 #pragma unroll 1
@@ -274,6 +275,9 @@ __global__ void __launch_bounds__(FFN_THREADS, 1)
             v[4 * u + 2] = fmaxf(v[4 * u + 2] + bb.z, 0.f);
             v[4 * u + 3] = fmaxf(v[4 * u + 3] + bb.w, 0.f);
           }
+          // FFN2 of the previous chunk has read this h k-block (the first wait per k-block; the accumulator read and
+          // the bias work above already overlap it)
+          if ((cc & 63) == 0 && hc >= 1) ptx::mbar_wait(&hempty[cc >> 6], (hc - 1) & 1);
           sts32_bf16(hbase + (cc >> 6) * SUBT, r, (cc & 63) >> 3, v);
         }
         ptx::tc_fence_before();
@@ -312,11 +316,17 @@ __global__ void __launch_bounds__(FFN_THREADS, 1)
           ptx::mbar_arrive_expect_tx(&sfull[wq * 2 + b], 4096);
           ptx::tma_load_2d(myS + b * 4096, &tmS, &sfull[wq * 2 + b], c + 64, m0 + q * 32);
         }
+        const float4* bc4 = reinterpret_cast<const float4*>(g.bcat + c);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          v[j] = v[j] + __ldg(g.bcat + c + j) + x[j];
-          sum += v[j];
+        for (int u = 0; u < 8; ++u) {
+          const float4 bb = __ldg(bc4 + u);
+          v[4 * u] = v[4 * u] + bb.x + x[4 * u];
+          v[4 * u + 1] = v[4 * u + 1] + bb.y + x[4 * u + 1];
+          v[4 * u + 2] = v[4 * u + 2] + bb.z + x[4 * u + 2];
+          v[4 * u + 3] = v[4 * u + 3] + bb.w + x[4 * u + 3];
         }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) sum += v[j];
         st32_tmem(orow + c, v);
       }
       sk += FD / 32;
@@ -345,8 +355,16 @@ __global__ void __launch_bounds__(FFN_THREADS, 1)
           const int c = 64 * blk + 32 * half;
           float v[32];
           ld32_tmem(orow + c, v);
+          const float4* ga4 = reinterpret_cast<const float4*>(g.gamma + c);
+          const float4* be4 = reinterpret_cast<const float4*>(g.beta + c);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = (v[j] - mean) * rstd * __ldg(g.gamma + c + j) + __ldg(g.beta + c + j);
+          for (int u = 0; u < 8; ++u) {
+            const float4 ga = __ldg(ga4 + u), be = __ldg(be4 + u);
+            v[4 * u] = (v[4 * u] - mean) * rstd * ga.x + be.x;
+            v[4 * u + 1] = (v[4 * u + 1] - mean) * rstd * ga.y + be.y;
+            v[4 * u + 2] = (v[4 * u + 2] - mean) * rstd * ga.z + be.z;
+            v[4 * u + 3] = (v[4 * u + 3] - mean) * rstd * ga.w + be.w;
+          }
           sts32_bf16(sb, lane, half * 4, v);
         }
         ptx::fence_async_smem();

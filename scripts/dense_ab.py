@@ -32,7 +32,7 @@ for rep in range(3):
         res[i].append(a.elapsed_time(b) / K * 1e3)
         for k in st:  # restore defaults
             m.set_option(k, {"pdl": 1, "graphs": 1, "ens_u_bn": 128, "pair": 1, "u_bn": 192, "xv_bn": 0, "epw": 2,
-                             "ens_attn_tc": 1}.get(k, 1))
+                             "ens_attn_tc": 1, "ens_ffn_fused": 0}.get(k, 1))
 roles = [r for r in os.environ.get("ROLES", "").split(",") if r]
 for i, st in enumerate(settings):
     out = {"setting": st, "us_per_dense": [round(x, 2) for x in res[i]], "min": round(min(res[i]), 2)}
@@ -42,6 +42,8 @@ for i, st in enumerate(settings):
     for role in roles:  # per-launch time of one GEMM role in a PDL chain of its own launches (cvr_repeat_kernel)
         n = m.repeat_kernel(role, 4, x0, B, stream=s)
         torch.cuda.synchronize()
+        if n == 0:  # this role does not run under this setting
+            continue
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(s)
         for _ in range(3):
@@ -49,5 +51,5 @@ for i, st in enumerate(settings):
         b.record(s); torch.cuda.synchronize()
         out[role + "_us"] = round(a.elapsed_time(b) * 1e3 / (3 * n), 2)
     for k in st:
-        m.set_option(k, {"ens_attn_tc": 1}.get(k, 1))
+        m.set_option(k, {"ens_attn_tc": 1, "ens_ffn_fused": 0}.get(k, 1))
     print(json.dumps(out))
