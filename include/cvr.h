@@ -278,7 +278,8 @@ int cvr_unpack_shard(cvr_ctx* ctx, const void* d_recv, int batch_global, void* d
  * config 4: "pair" [1] 2-CTA (cta_group::2) tiles, "ens_u_bn" [128] N tile of the DCN U GEMM, "ens_fused_attn" [1]
  * the QKV projection + attention as one GEMM (else QKV GEMM + mha64), "ens_attn_tc" [1] that GEMM's attention on
  * tcgen05 (S = Q K^T, O = P V as UMMAs in TMEM; else mma.sync in the epilogue), "f32_tma_store" [1] the fp32 DCN-branch
- * output through staged TMA stores, "ens_xv_wave" [1] t = X V^T as one wave of 128 x 256 tiles; MaskNet:
+ * output through staged TMA stores, "ens_xv_wave" [1] t = X V^T as one wave of 128 x 256 tiles, "ens_ffn_fused" [0]
+ * FFN1 + out-projection + FFN2 + LN as one kernel (hidden activations never stored; measured slower); MaskNet:
  * "mask_grouped" [1] parallel blocks as one grouped GEMM.  Every variant is bit-identical to the default.
  * "lanes" [1] executor lanes (1-4, see cvr_score): only before cvr_set_workspace (else CVR_E_STATE), unsharded
  * only; sub-contexts are created here and every later option, table, weight and feature-spec call is applied to
