@@ -428,3 +428,27 @@ def test_c3_rank_slice_dense_stage_vs_oracle():
     err = np.abs(s[torch.from_numpy(sel).cuda()].double().cpu().numpy() - ref)
     m.close()
     assert err.max() <= TOL_BF16, err.max()
+
+
+@pytest.mark.slow
+def test_c2_full_size_two_lanes_vs_oracle():
+    """BASELINE.json configs[1] at full size (26 tables of 1e5-1e6 rows x 64 bf16, B = 4096) in the launch configuration
+    bench.py times: the executor with two lanes, four pipelined batches (two per lane, both x0 slots of lane 0 and one
+    of lane 1), every one of each batch's 4096 scores against the fp64 oracle (gate 2e-3)."""
+    cfg = cs.C2
+    ring = [cs.make_batch(cfg, 910 + i) for i in range(4)]
+    m, tabs, w = make_model(cfg, max_batch=cfg.batch, max_nnz=max(b.nnz for b in ring), lanes=2)
+    dev_in = [to_dev(b) for b in ring]
+    outs = [torch.empty(cfg.batch, device="cuda") for _ in ring]
+    s_e, s_d = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
+    torch.cuda.synchronize()
+    for (i, o, d), bt, out in zip(dev_in, ring, outs):
+        m.score(i, o, bt.batch, d, out, s_embed=s_e, s_dense=s_d)
+    s_d.synchronize()
+    assert m.status(s_d) == 0
+    specs = cs.table_specs(cfg)
+    for k, (bt, out) in enumerate(zip(ring, outs)):
+        ref = O.score_forward(cfg, specs, w, bt)["scores"]
+        err = np.abs(out.double().cpu().numpy() - ref)
+        assert err.max() <= TOL_BF16, (k, err.max(), np.percentile(err, 99))
+    m.close()
