@@ -14,7 +14,7 @@ src = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "gpurun_out")
 
 # kernel template -> role (gemm_bf16_kernel<BN, EPI, AR, CG, CN>; Epi enum in cvr_kernels.cuh)
 EPI = {0: "STORE", 1: "BIAS_RELU", 2: "CROSS", 3: "HEAD", 4: "BIAS", 5: "CROSS_F32", 6: "BIAS_ADD_F32", 7: "SUM_LN",
-       8: "HEAD_PARTIAL", 9: "MASK", 10: "ATTN"}
+       8: "HEAD_PARTIAL", 9: "MASK", 10: "ATTN", 11: "ATTN_TC"}
 
 
 def role(name):
@@ -24,8 +24,10 @@ def role(name):
         # role names of config 2 (for c6: BIAS_RELU = projection / mask hidden / MLP, MASK = mask blocks)
         r = {(0,): "gemm_xV", (2,): "gemm_tU_cross", (1,): "gemm_mlp_relu", (3,): "gemm_mlp_head",
              (9,): "gemm_mask_mul", (10,): "gemm_ens_qkv_attn", (5,): "gemm_tU_cross", (7,): "gemm_ens_ffn2_ln",
-             (8,): "gemm_mlp_head"}.get((epi,), f"gemm_{EPI.get(epi, epi)}")
+             (8,): "gemm_mlp_head", (11,): "gemm_ens_qkv_attn"}.get((epi,), f"gemm_{EPI.get(epi, epi)}")
         return f"{r} [BN={bn}{' pair' if cg == 2 else ''}]"
+    if "ffn_fused" in name:
+        return "gemm_ens_ffn_fused"
     for k in ("embed_bag", "dense_f32", "unpack", "mha64", "head_finalize", "set_call"):
         if k in name:
             return k
