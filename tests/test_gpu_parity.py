@@ -452,3 +452,39 @@ def test_c2_full_size_two_lanes_vs_oracle():
         err = np.abs(out.double().cpu().numpy() - ref)
         assert err.max() <= TOL_BF16, (k, err.max(), np.percentile(err, 99))
     m.close()
+
+
+@pytest.mark.parametrize("lanes", [1, 2])
+def test_executor_empty_batches_and_bags(lanes):
+    """Edge cases through the executor: a batch of 0 rows between real batches (no work, no error, the neighbours'
+    scores unchanged) and a batch whose every bag is empty (x0's embedding columns all 0: every score equals the
+    oracle's on the all-empty batch), one and two lanes."""
+    cfg = cs.C2.with_(rows=(5000,) * 26)
+    Bmax = 256
+    m, tabs, w = make_model(cfg, max_batch=Bmax, max_nnz=1 << 18, lanes=lanes)
+    a = cs.make_batch(cfg, 500, batch=200)
+    empty = cs.make_batch(cfg, 501, batch=130)
+    empty_off = np.zeros_like(empty.offsets)                    # every bag [0, 0): nnz = 0
+    dev_a = to_dev(a)
+    ref_a = m.dense(m.embed(*dev_a[:2], a.batch, dev_a[2]), a.batch).clone()
+    s_e, s_d = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
+    out1, out2 = torch.empty(a.batch, device="cuda"), torch.empty(a.batch, device="cuda")
+    oute = torch.empty(empty.batch, device="cuda")
+    zero_idx = torch.zeros(1, dtype=torch.int32, device="cuda")
+    zero_off = torch.zeros(cfg.n_tables * 1 + 1, dtype=torch.int32, device="cuda")
+    dummy_scores = torch.empty(1, device="cuda")
+    dense0 = torch.zeros(1, cfg.n_dense, device="cuda")
+    torch.cuda.synchronize()
+    m.score(*dev_a[:2], a.batch, dev_a[2], out1, s_embed=s_e, s_dense=s_d)
+    m.L.cvr_score(m.h, zero_idx.data_ptr(), zero_off.data_ptr(), 0, 0, dense0.data_ptr(), dummy_scores.data_ptr(),
+                  s_e.cuda_stream, s_d.cuda_stream)                              # batch of 0 rows
+    m.score(zero_idx[:0], torch.from_numpy(empty_off).cuda(), empty.batch, torch.from_numpy(empty.dense).cuda(), oute,
+            s_embed=s_e, s_dense=s_d)                                             # every bag empty
+    m.score(*dev_a[:2], a.batch, dev_a[2], out2, s_embed=s_e, s_dense=s_d)
+    s_d.synchronize()
+    assert m.status(s_d) == 0
+    assert torch.equal(out1, ref_a) and torch.equal(out2, ref_a)
+    eb = cs.Batch(empty.batch, cfg.n_tables, np.zeros(0, np.int32), empty_off, empty.dense)
+    ref_e = O.score_forward(cfg, cs.table_specs(cfg), w, eb)["scores"]
+    assert np.abs(oute.double().cpu().numpy() - ref_e).max() <= TOL_BF16
+    m.close()
