@@ -17,7 +17,7 @@ raw = [(i.data_ptr(), o.data_ptr(), i.numel(), d.data_ptr(), out.data_ptr()) for
 settings = json.loads(sys.argv[1])
 K = int(os.environ.get("K", "500"))
 DEF = {"u_bn": 192, "epw": 0, "pdl": 1, "graphs": 1, "embed_bps": 0, "xv_bn": 0, "prefetch_b": 1,
-       "ens_fused_attn": 1, "zero_copy_scores": 1}
+       "ens_fused_attn": 1, "zero_copy_scores": 1, "ens_ffn_fused": 0}  # (restored after each setting; others -> 1)
 for rep in range(3):
     for st in settings:
         for k, v in st.items(): m.set_option(k, v)
