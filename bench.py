@@ -236,9 +236,12 @@ WORKLOADS = {
     "c6": "c6: SURVEY.md §8(f) #1 MaskNet on config 2's features (ReLU projection 1728->2048, 2 parallel mask "
           "blocks r=512, MLP 4096-1024-512-256-1; PAPER.md Table 1 MaskNet defaults), not a BASELINE.json config",
 }
+DATA_SRC = {"c1": "BASELINE.json configs[0]", "c2": "BASELINE.json configs[1]", "c3": "BASELINE.json configs[2]",
+            "c3s": "BASELINE.json configs[2] (strong-scaling variant)", "c4": "BASELINE.json configs[3]",
+            "c6": "config 2's features (MaskNet, SURVEY.md §8(f) #1)"}
 # executor lanes per config (cvr.h option "lanes"): c2 86.3 vs 97.0 us per batch with two pipelines dealt batches
-# round-robin (scripts/two_exec.py); c6 no gain (137-143 vs 140-141); the others one
-LANES = {"c2": 2}
+# round-robin (scripts/two_exec.py), c1 15.6 vs 20.5 (three or four: 16.0); c4 and c6 no gain; the others one
+LANES = {"c2": 2, "c1": 2}
 TOL = {"c1": 1e-5, "c2": 2e-3, "c3": 2e-3, "c3s": 2e-3, "c4": 2e-3, "c6": 2e-3}
 
 
@@ -785,7 +788,7 @@ def run_cvr(args, cfg, emit=True):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": el_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32" if cfg.act_dtype == "f32" else "bf16", "data": "synthetic (cvr_synth: seeded, BASELINE.json configs[1] shapes/distributions)",
+        "dtype": "f32" if cfg.act_dtype == "f32" else "bf16", "data": "synthetic (cvr_synth: seeded, %s shapes/distributions)" % DATA_SRC.get(cfg.name, cfg.name),
         "config": {"workload": WORKLOADS[cfg.name], "global_batch": B * world, "batch_per_gpu": B,
                    "parallelism": f"replicas x{world} (two-stream decoupled executor per GPU"
                                   + (f", {lanes} executor lanes: batches dealt round-robin to {lanes} pipelines)"
