@@ -488,3 +488,37 @@ def test_executor_empty_batches_and_bags(lanes):
     ref_e = O.score_forward(cfg, cs.table_specs(cfg), w, eb)["scores"]
     assert np.abs(oute.double().cpu().numpy() - ref_e).max() <= TOL_BF16
     m.close()
+
+
+@pytest.mark.parametrize("lanes", [2, 3])
+def test_executor_lanes_stress(lanes):
+    """Race check for the lanes: 60 batches of random size (1 .. max_batch), device-fed and host-fed calls
+    interleaved at random, inputs and outputs in distinct buffers, one synchronisation at the end; every batch's
+    scores bit-identical to embed + dense of the same batch."""
+    cfg = cs.C2.with_(rows=(20000,) * 26)
+    Bmax = 512
+    m, tabs, w = make_model(cfg, max_batch=Bmax, max_nnz=1 << 20, lanes=lanes)
+    rng = np.random.default_rng(7)
+    sizes = rng.integers(1, Bmax + 1, 60)
+    batches = [cs.make_batch(cfg, 600 + i, batch=int(b)) for i, b in enumerate(sizes)]
+    dev_in = [to_dev(bt) for bt in batches]
+    refs = [m.dense(m.embed(i, o, bt.batch, d), bt.batch).clone() for (i, o, d), bt in zip(dev_in, batches)]
+    host = rng.random(len(batches)) < 0.4
+    host_in = [tuple(torch.from_numpy(a).pin_memory() for a in (bt.indices, bt.offsets, bt.dense)) if h else None
+               for bt, h in zip(batches, host)]
+    outs = [torch.empty(bt.batch).pin_memory() if h else torch.empty(bt.batch, device="cuda")
+            for bt, h in zip(batches, host)]
+    s_e, s_d, s_c = torch.cuda.Stream(), torch.cuda.Stream(priority=-1), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for k, bt in enumerate(batches):
+        if host[k]:
+            idx, off, dense = host_in[k]
+            m.score_host(idx, off, bt.batch, dense, outs[k], s_copy=s_c, s_embed=s_e, s_dense=s_d)
+        else:
+            i, o, d = dev_in[k]
+            m.score(i, o, bt.batch, d, outs[k], s_embed=s_e, s_dense=s_d)
+    s_d.synchronize()
+    assert m.status(s_d) == 0
+    for k, (out, r) in enumerate(zip(outs, refs)):
+        assert torch.equal(out.cuda() if host[k] else out, r), (k, int(sizes[k]), bool(host[k]))
+    m.close()
