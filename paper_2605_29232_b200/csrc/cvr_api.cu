@@ -1771,7 +1771,16 @@ int ensure_lane_streams(cvr_ctx* c, cudaStream_t s_embed, cudaStream_t s_dense) 
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->lane_in[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->lane_out[i], cudaEventDisableTiming);
   }
-  return e == cudaSuccess ? CVR_OK : c->cuda_fail(e, "lane streams");
+  if (e == cudaSuccess) return CVR_OK;
+  for (int i = 0; i < cvr_ctx::kMaxLanes; ++i) {  // all or nothing: the next call retries from scratch
+    if (c->lane_se[i]) cudaStreamDestroy(c->lane_se[i]);
+    if (c->lane_sd[i]) cudaStreamDestroy(c->lane_sd[i]);
+    if (c->lane_in[i]) cudaEventDestroy(c->lane_in[i]);
+    if (c->lane_out[i]) cudaEventDestroy(c->lane_out[i]);
+    c->lane_se[i] = c->lane_sd[i] = nullptr;
+    c->lane_in[i] = c->lane_out[i] = nullptr;
+  }
+  return c->cuda_fail(e, "lane streams");
 }
 
 // call lane_k % lanes: its work waits for the caller's s_embed, runs on the lane's streams, and the caller's s_dense
