@@ -663,6 +663,7 @@ def run_cvr(args, cfg, emit=True):
         "bound": "hbm", "per_step": 1, "us_per_launch": emb_us, "achieved": ebytes / emb_us / 1e3, "unit": "GB/s",
         "peak": pk["hbm"], "frac": ebytes / emb_us / 1e3 / pk["hbm"], "algorithmic_bytes": ebytes,
         "frac_compulsory": cbytes / emb_us / 1e3 / pk["hbm"], "compulsory_bytes": cbytes,
+        "traffic": None,  # (filled from profiles/ncu_traffic.json below: DRAM bytes per launch, cold-cache ncu)
         "uniform_index_control": {"us": embed_uniform_us, "algorithmic_bytes": ubytes,
                                   "achieved": ubytes / embed_uniform_us / 1e3,
                                   "frac": ubytes / embed_uniform_us / 1e3 / pk["hbm"]},
@@ -672,6 +673,7 @@ def run_cvr(args, cfg, emit=True):
     if os.path.exists(tp):
         with open(tp) as f:
             traffic_db = json.load(f).get(cfg.name, {})
+    kernels["embed_bag_pool"]["traffic"] = traffic_db.get("embed_bag_pool")
     for role, d in kt.items():
         wk = role_work(cfg, B, role)
         t_s = d["us_per_launch"] / 1e6
