@@ -236,14 +236,14 @@ def test_executor_graphs_every_backbone(name):
     m.close()
 
 
-@pytest.mark.parametrize("name,lanes", [("c2", 2), ("c2", 3), ("c6", 2)])
+@pytest.mark.parametrize("name,lanes", [("c1", 2), ("c2", 2), ("c2", 3), ("c6", 2)])
 def test_executor_lanes(name, lanes):
     """Option "lanes": consecutive cvr_score / cvr_score_host calls dealt round-robin to `lanes` pipelines (sub-contexts
     on library streams, joined into the caller's s_dense): every batch's scores bit-identical to embed + dense on
     lane 0, the call blocks of the last calls are where executor_slot() says, each lane captures its own graphs,
     and a bad index in a batch dealt to a lane other than 0 still reaches cvr_get_status."""
     cfg = cs.C2.with_(rows=(50000,) * 26) if name == "c2" else _small(name)
-    Bmax = 384
+    Bmax = 256 if name == "c1" else 384
     m, tabs, w = make_model(cfg, max_batch=Bmax, max_nnz=1 << 20, lanes=lanes)
     sizes = [Bmax, 7, Bmax - 1, 1, 130, Bmax, 64, 200]
     batches = [cs.make_batch(cfg, 400 + i, batch=B) for i, B in enumerate(sizes)]
