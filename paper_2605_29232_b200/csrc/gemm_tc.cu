@@ -98,7 +98,8 @@ struct Cfg {
   // epilogue warp per quadrant it had 2 stages: 348-354 us; one buffer alone, 5 stages: no change; + the split
   // epilogue: 320 us) -- its B producer then issues a tile's x0 / x_l loads after the tile's weight k-blocks, once the
   // previous tile's epilogue has released the buffer
-  static constexpr int EIN_NBUF = EPI == EPI_CROSS_F32 ? 1 : 2;
+  // (MaskNet's EPI_MASK likewise: 2 -> 3 ring stages at BN = 128; c6 mask GEMM 30.3 -> 25.9 us, step 142 -> 137 us)
+  static constexpr int EIN_NBUF = (EPI == EPI_CROSS_F32 || EPI == EPI_MASK) ? 1 : 2;
   // EPI_ATTN staging: Q | K | V of a tile's 128 tokens, bf16, row stride ATT_LD (padded: conflict-free ldmatrix).
   // (An unpadded XOR-swizzled layout freed a third ring stage but measured slower: 469 vs 381 us per layer.)
   static constexpr int ATT_LD = 72;
