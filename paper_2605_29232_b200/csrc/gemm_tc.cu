@@ -108,7 +108,13 @@ struct Cfg {
   // EPI_CROSS_F32 with a tmOut map: fp32 32 x 32 chunks staged per epilogue warp (double-buffered) and TMA-stored
   // (coalesced) instead of per-thread row stores
   static constexpr int F32_NBUF = CG == 2 ? 2 : 1;  // (single-CTA tiles: the ring needs the room)
-  static constexpr int SLN_BUFS = 3;                 // EPI_SUM_LN: fp32 input chunks in flight per epilogue warp
+  static constexpr int SLN_BUFS = 2;                 // EPI_SUM_LN: fp32 input chunks in flight per epilogue warp
+  // shared-memory budget: 225 KB leaves room (2 x 1 KB reserved) for two co-resident gather CTAs of the next batch;
+  // config 4's DCN U (fp32 output) and FFN2 + LN GEMMs take the whole 227 KB instead: one more operand ring stage
+  // each (3 -> 4; SUM_LN with 2 input chunks per warp instead of 3): U 301 -> 284 us, FFN2 + LN 416 -> 377 us per
+  // launch, c4 step -1.5-2% (its gather has the other GEMMs to hide under).  (MaskNet's mask GEMM at 227 KB: 26.2 ->
+  // 23.8 us per launch but no faster c6 step -- its gather then loses those SMs.)
+  static constexpr int BUDGET = (EPI == EPI_CROSS_F32 || EPI == EPI_SUM_LN) ? 227 * 1024 : kSmemBudget;
   static constexpr int F32_BYTES = EPI == EPI_CROSS_F32 ? 4 * EPW * F32_NBUF * 32 * 32 * 4
                                   : (EPI == EPI_SUM_LN ? 4 * EPW * SLN_BUFS * 32 * 32 * 4 : 0);  // SUM_LN input ring
   static constexpr int EPI_BYTES =
@@ -116,7 +122,7 @@ struct Cfg {
   static constexpr int BAR_BYTES = 512;
   // EPI_HEAD with a split epilogue: the EPW warps' partial dot products per row ([EPW][BM] fp32)
   static constexpr int Z_BYTES = EPI == EPI_HEAD ? EPW * BM * 4 : 0;
-  static constexpr int STAGES_FIT = (kSmemBudget - 1024 - BAR_BYTES - EPI_BYTES - Z_BYTES) / STAGE;
+  static constexpr int STAGES_FIT = (BUDGET - 1024 - BAR_BYTES - EPI_BYTES - Z_BYTES) / STAGE;
 #ifndef CVR_MAX_STAGES
 #define CVR_MAX_STAGES 8
 #endif
