@@ -114,7 +114,9 @@ struct Cfg {
   // each (3 -> 4; SUM_LN with 2 input chunks per warp instead of 3): U 301 -> 284 us, FFN2 + LN 416 -> 377 us per
   // launch, c4 step -1.5-2% (its gather has the other GEMMs to hide under).  (MaskNet's mask GEMM at 227 KB: 26.2 ->
   // 23.8 us per launch but no faster c6 step -- its gather then loses those SMs.)
-  static constexpr int BUDGET = (EPI == EPI_CROSS_F32 || EPI == EPI_SUM_LN) ? 227 * 1024 : kSmemBudget;
+  // The 2-CTA (CG = 2) tiles -- config 4 only (pair_ens) -- likewise: FFN1 325 -> 315 us, the head's 16384 -> 2048
+  // layer 440 -> 397 us (4 -> 5 stages).
+  static constexpr int BUDGET = (EPI == EPI_CROSS_F32 || EPI == EPI_SUM_LN || CG == 2) ? 227 * 1024 : kSmemBudget;
   static constexpr int F32_BYTES = EPI == EPI_CROSS_F32 ? 4 * EPW * F32_NBUF * 32 * 32 * 4
                                   : (EPI == EPI_SUM_LN ? 4 * EPW * SLN_BUFS * 32 * 32 * 4 : 0);  // SUM_LN input ring
   static constexpr int EPI_BYTES =
