@@ -109,7 +109,8 @@ struct Cfg {
   // (coalesced) instead of per-thread row stores
   static constexpr int F32_NBUF = CG == 2 ? 2 : 1;  // (single-CTA tiles: the ring needs the room)
   static constexpr int SLN_BUFS = 2;                 // EPI_SUM_LN: fp32 input chunks in flight per epilogue warp
-  // shared-memory budget: 225 KB leaves room (2 x 1 KB reserved) for two co-resident gather CTAs of the next batch;
+  // shared-memory budget: 225 KB leaves room (2 x 1 KB reserved) for two co-resident gather CTAs of the next batch
+  // (every kernel at 227 KB: c2 step 86.1 -> 95.2 us at two lanes, 97.2 -> 101.1 at one; c6 unchanged);
   // config 4's DCN U (fp32 output) and FFN2 + LN GEMMs take the whole 227 KB instead: one more operand ring stage
   // each (3 -> 4; SUM_LN with 2 input chunks per warp instead of 3): U 301 -> 284 us, FFN2 + LN 416 -> 377 us per
   // launch, c4 step -1.5-2% (its gather has the other GEMMs to hide under).  (MaskNet's mask GEMM at 227 KB: 26.2 ->
